@@ -1,0 +1,217 @@
+/*
+ * halo.h — C ABI of libhalo.so: the per-step eighth-shell (neutral-territory)
+ * domain-decomposition halo exchange of arXiv 2509.21527, B200-native.
+ *
+ * Citations: P:<n> = line n of the paper text; R<n> = a reading of
+ * the paper recorded in DESIGN.md ("Readings").
+ *
+ * Model (Alg. 1):
+ *   - A periodic rectangular box L[3] is split into grid[0] x grid[1] x grid[2]
+ *     cells ("DD ranks"), rank = (cx*np_y + cy)*np_z + cz (R5).
+ *   - Each DD rank owns a coordinate array x and a force array f of `capacity`
+ *     rows.  Rows [0, n_home) are its home atoms; halo rows received in the
+ *     coordinate halo are appended contiguously after them, pulses in global
+ *     order z -> y -> x (R12).
+ *   - A row is `layout` floats: 3 (12-byte float3, GROMACS rvec) or 4 (16-byte
+ *     float4; x: w copied, never shifted; f: w accumulated like x,y,z) (R25).
+ *   - One PROCESS drives one GPU and hosts a contiguous block of DD ranks
+ *     ("local ranks"): ranks [proc*R/nprocs, (proc+1)*R/nprocs), R = nranks.
+ *     With nprocs == nranks this is the paper's one-rank-per-GPU setup; with
+ *     nprocs < nranks several DD ranks share one GPU and are executed by the
+ *     same kernel launch (never as separate spinning launches).
+ *
+ * Conventions for every call:
+ *   - Returns halo_status; HALO_OK == 0.  No C++ exception crosses the ABI.
+ *   - On error the ctx keeps a message readable with halo_last_error().
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Device pointers are plain CUDA device pointers (e.g. torch data_ptr()).
+ *   - A ctx is not thread-safe; use one ctx per process.
+ *   - COLLECTIVE calls must be made by every process, the same number of
+ *     times, in the same order (they synchronise through device-side flags).
+ */
+#ifndef HALO_H_
+#define HALO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HALO_API __attribute__((visibility("default")))
+#else
+#define HALO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HALO_ABI_VERSION 1
+#define HALO_MAX_PULSES 6     /* up to two pulses per dimension */
+#define HALO_MAX_RANKS 64     /* DD ranks per job supported by this build */
+#define HALO_MAX_LOCAL 64     /* DD ranks per process */
+
+typedef struct halo_ctx halo_ctx; /* opaque */
+
+typedef enum {
+  HALO_OK = 0,
+  HALO_ERR_ARG = 1,         /* bad argument (NULL, out of range, misaligned) */
+  HALO_ERR_GEOMETRY = 2,    /* invalid grid/box/cutoff/pulses, or a home atom outside its cell */
+  HALO_ERR_CAPACITY = 3,    /* n_home + sum(recv) > capacity on some rank (agreed by all ranks) */
+  HALO_ERR_STATE = 4,       /* call out of order (e.g. exchange before set_maps) */
+  HALO_ERR_CUDA = 5,        /* a CUDA runtime error; text in halo_last_error() */
+  HALO_ERR_PEER = 6,        /* IPC import failed or a peer blob is inconsistent */
+  HALO_ERR_TIMEOUT = 7,     /* a device-side wait exceeded the timeout (protocol bug or dead peer) */
+  HALO_ERR_UNSUPPORTED = 8  /* valid request this build does not support */
+} halo_status;
+
+/* Flags (halo_config.flags). */
+#define HALO_F_ATOMIC_UNPACK  (1u << 0) /* unordered f unpack (paper's atomicAdd); default is the
+                                           deterministic pulse-descending order (bit-exact vs oracle, R15) */
+#define HALO_F_NO_HOME_CHECK  (1u << 1) /* skip the "home atoms lie in their cell" check in halo_set_maps */
+#define HALO_F_GPU_FENCE      (1u << 2) /* per-CTA gpu-scope release + sys-scope release by the last CTA
+                                           only (the paper's P:425-427 scheme); default: per-CTA sys fence */
+#define HALO_F_TIMERS         (1u << 3) /* record %globaltimer spans of each exchange kernel */
+
+typedef struct {
+  int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */
+  float box[3];       /* box lengths L_x, L_y, L_z in nm (rectangular) */
+  float cutoff;       /* communication cutoff rc in nm: 0 < rc < min(L)/2 */
+  int pulses[3];      /* pulses per dim: >= 1 iff grid[d] > 1, <= grid[d]-1, pulses*L/grid >= rc */
+  int layout;         /* 3 or 4 floats per row of x and f */
+  int capacity;       /* rows of every registered x and f array (home + halo) */
+  int device;         /* CUDA device ordinal this process uses */
+  unsigned flags;     /* HALO_F_* */
+  int nprocs;         /* processes (GPUs) in the job; nranks % nprocs == 0 */
+  int proc;           /* this process, 0 <= proc < nprocs */
+  double timeout_s;   /* bound of every device-side wait; <= 0 selects 10 s */
+} halo_config;
+
+/* Validate `cfg` and create a context (PulseData/CommContext).
+ * Geometry is validated before any CUDA call: an invalid config returns
+ * HALO_ERR_GEOMETRY/HALO_ERR_ARG without touching the GPU.  Then selects
+ * cfg->device and allocates the library-owned control block.
+ * *out receives the ctx (NULL on error; use halo_strerror). */
+HALO_API halo_status halo_init(const halo_config* cfg, halo_ctx** out);
+
+/* DD ranks hosted by this process: [*first_rank, *first_rank + *n_local). */
+HALO_API halo_status halo_local_ranks(const halo_ctx* ctx, int* first_rank, int* n_local);
+
+/* Total pulses (sum of cfg.pulses) and the global pulse order: dims[p] = 0/1/2
+ * (x/y/z), in z -> y -> x order.  dims may be NULL. */
+HALO_API halo_status halo_pulse_order(const halo_ctx* ctx, int* npulse, int* dims);
+
+/* Bytes of the caller-owned `scratch` device buffer each local rank needs
+ * (flags, handshake slots, index maps, force receive buffers; 256-B aligned). */
+HALO_API halo_status halo_scratch_bytes(const halo_ctx* ctx, size_t* bytes);
+
+/* Register the device buffers of local rank `local` (0 <= local < n_local):
+ * x, f: capacity*layout floats, 16-B aligned; scratch: halo_scratch_bytes().
+ * Caller-owned; they must stay allocated at fixed addresses until halo_destroy
+ * because peer processes map them (P:436-439 symmetric/registered buffers).
+ * Zero-fills scratch (stream-ordered on the legacy stream, synchronised). */
+HALO_API halo_status halo_register_buffers(halo_ctx* ctx, int local, void* x, void* f, void* scratch);
+
+/* CUDA-IPC export of this process's registered x and scratch buffers (replaces
+ * nvshmem_ptr / symmetric allocation).  blob == NULL: *len = size needed.
+ * The caller all-gathers the blobs (e.g. torch.distributed all_gather_object). */
+HALO_API halo_status halo_ipc_export(halo_ctx* ctx, void* blob, size_t* len);
+
+/* Import the nprocs blobs (rank order, each len_each bytes, own blob included
+ * and skipped) and open the peer mappings.  Not needed when nprocs == 1. */
+HALO_API halo_status halo_ipc_import(halo_ctx* ctx, const void* blobs, size_t len_each);
+
+/* COLLECTIVE.  Neighbour-search step (every nstlist steps): build every
+ * pulse's send index map from x[0:n_home) of each local rank (n_home[local]),
+ * agree sizes/offsets with the neighbours through device flags, and exchange
+ * the coordinates pulse by pulse (forwarding needs the earlier pulses' rows).
+ * Selection (R2, R3): float64(x_d) - b_d[c_d] < float64(rc), strict, over the
+ * candidate rows (k = 0: all rows present before the dim's first pulse; k > 0:
+ * rows received in pulse (d, k-1)), ascending row order (R11).  Host-synchronises.
+ * Errors are agreed by all ranks (every rank returns the same status). */
+HALO_API halo_status halo_set_maps(halo_ctx* ctx, const int* n_home, void* stream);
+
+/* COLLECTIVE test entry: like halo_set_maps but with caller-given maps.
+ * send_sizes[local*npulse + p]; maps[local*npulse + p] = host int32 array of
+ * send_sizes[...] ascending local row indices.  Coordinates are exchanged as
+ * in halo_set_maps. */
+HALO_API halo_status halo_set_maps_explicit(halo_ctx* ctx, const int* n_home, const int* send_sizes,
+                                   const int* const* maps, void* stream);
+
+/* Layout of local rank `local` after set_maps (host arrays sized npulse; any may be NULL):
+ * recv_off[p] = atomOffset, recv_size[p], send_size[p], remote_off[p] = where
+ * this rank's pulse-p rows land on its receiver, dep_mask[p] = bit q set iff
+ * map_p reads rows received in pulse q (the wait set of Alg. 4, R9). */
+HALO_API halo_status halo_get_layout(const halo_ctx* ctx, int local, int* n_home, int* n_total, int* npulse,
+                            int* recv_off, int* recv_size, int* send_size, int* remote_off,
+                            unsigned* dep_mask);
+
+/* Copy map of (local, pulse) to host (cap ints available); for parity tests. */
+HALO_API halo_status halo_get_map(const halo_ctx* ctx, int local, int pulse, int* host_out, int cap);
+
+/* COLLECTIVE, asynchronous, HOT PATH (Alg. 3 FusedPackCommX, Alg. 4, Alg. 5):
+ * one kernel launch on `stream` that, for every local rank and pulse, gathers
+ * x rows through the map, adds the periodic shift (float32 add of the full
+ * 3-vector on the wrapping rank, R25), writes them straight into the receiver's
+ * x at its atomOffset over NVLink peer stores, forwards dependent rows after an
+ * acquire-wait on the flags of exactly the pulses they came from (R9), and
+ * notifies each receiver with one system-scope release store per pulse.
+ * When `stream` has executed it, rows [n_home, n_total) hold this step's halo.
+ * CUDA-graph capturable (the sequence number lives in device memory).
+ * Precondition (R17): steps alternate exchange_x / exchange_f on all ranks. */
+HALO_API halo_status halo_exchange_x(halo_ctx* ctx, void* stream);
+
+/* COLLECTIVE, asynchronous, HOT PATH (Alg. 6 FusedCommUnpackF, Alg. 5 DEP_MGMT):
+ * one kernel launch: each halo slice is pushed back to the rank that sent it
+ * once every later pulse that forwarded rows of it has been unpacked locally
+ * (P:412), and received slices are scatter-added into f through the map
+ * (pulses descending, one float32 add per entry: bit-exact vs the oracle, R15;
+ * HALO_F_ATOMIC_UNPACK: unordered).  fshift (device, [n_local][3][3] float64,
+ * may be NULL) is ADDED the received force sums of the pulses this rank
+ * shifted (R13).  accumulate = 0 overwrites and is only supported with a single
+ * pulse in total (R14), else HALO_ERR_UNSUPPORTED.  Halo rows of f keep their
+ * values.  CUDA-graph capturable. */
+HALO_API halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void* stream);
+
+/* COLLECTIVE end-to-end step through host buffers (the e2e measurement path):
+ * per local rank copies x_home[l] (n_home*layout floats, pinned host) and
+ * f_all[l] (n_total*layout floats) to the device, runs exchange_x and
+ * exchange_f, copies the halo x rows to x_halo_out[l] ((n_total-n_home)*layout
+ * floats), the home f rows to f_home_out[l] and fshift (n_local*9 doubles) to
+ * fshift_host; any output may be NULL.  Enqueued on `stream`; synchronises it. */
+HALO_API halo_status halo_step_host(halo_ctx* ctx, const float* const* x_home, const float* const* f_all,
+                           float* const* x_halo_out, float* const* f_home_out, double* fshift_host,
+                           void* stream);
+
+/* Baseline building blocks (the NCCL send/recv schedule of P:178-181 / Fig. 1
+ * drives these from the host; not on the fused path):
+ * pack pulse p of local rank into sendbuf (send_size*layout floats, shift applied);
+ * unpack a received force slice (send_size*layout floats) into f (+ fshift). */
+HALO_API halo_status halo_pack_x_pulse(halo_ctx* ctx, int local, int pulse, float* sendbuf, void* stream);
+HALO_API halo_status halo_unpack_f_pulse(halo_ctx* ctx, int local, int pulse, const float* recvbuf,
+                                double* fshift, int accumulate, void* stream);
+
+/* Device-side kernel spans (HALO_F_TIMERS): last exchange_x and exchange_f
+ * durations in ns (max end - min start over the CTAs), read after halo_sync. */
+HALO_API halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns);
+
+/* Floors (measurement): ping-pong `iters` round trips of a
+ * system-scope release/acquire flag between this process's local rank 0 and
+ * DD rank `peer_rank` (COLLECTIVE between the two processes only; other
+ * processes must not call).  *one_way_us = median round trip / 2. */
+HALO_API halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, double* one_way_us);
+
+/* Host-block until all work this ctx enqueued is done; surfaces device error
+ * words (HALO_ERR_TIMEOUT) and CUDA errors. */
+HALO_API halo_status halo_sync(halo_ctx* ctx);
+
+HALO_API const char* halo_strerror(halo_status s);
+HALO_API const char* halo_last_error(const halo_ctx* ctx);
+
+/* Close peer mappings and free library-owned memory.  Callers barrier across
+ * processes before freeing the registered buffers. */
+HALO_API halo_status halo_destroy(halo_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALO_H_ */

@@ -1,0 +1,81 @@
+"""ctypes loader of libhalo.so (argument marshalling only; fails loudly if missing)."""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_size_t, c_uint, c_uint64, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhalo.so")
+
+HALO_OK = 0
+STATUS_NAMES = {0: "HALO_OK", 1: "HALO_ERR_ARG", 2: "HALO_ERR_GEOMETRY", 3: "HALO_ERR_CAPACITY",
+                4: "HALO_ERR_STATE", 5: "HALO_ERR_CUDA", 6: "HALO_ERR_PEER", 7: "HALO_ERR_TIMEOUT",
+                8: "HALO_ERR_UNSUPPORTED"}
+
+HALO_F_ATOMIC_UNPACK = 1 << 0
+HALO_F_NO_HOME_CHECK = 1 << 1
+HALO_F_GPU_FENCE = 1 << 2
+HALO_F_TIMERS = 1 << 3
+HALO_MAX_PULSES = 6
+
+# every symbol include/halo.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "halo_init", "halo_local_ranks", "halo_pulse_order", "halo_scratch_bytes", "halo_register_buffers",
+    "halo_ipc_export", "halo_ipc_import", "halo_set_maps", "halo_set_maps_explicit", "halo_get_layout",
+    "halo_get_map", "halo_exchange_x", "halo_exchange_f", "halo_step_host", "halo_pack_x_pulse",
+    "halo_unpack_f_pulse", "halo_get_timers", "halo_floor_pingpong", "halo_sync", "halo_strerror",
+    "halo_last_error", "halo_destroy",
+]
+
+
+class halo_config(ctypes.Structure):
+    _fields_ = [("grid", c_int * 3), ("box", c_float * 3), ("cutoff", c_float), ("pulses", c_int * 3),
+                ("layout", c_int), ("capacity", c_int), ("device", c_int), ("flags", c_uint),
+                ("nprocs", c_int), ("proc", c_int), ("timeout_s", c_double)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libhalo.so; raises if it has not been built (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libhalo.so not found at {path}: run `python -m paper_2509_21527_b200.build` "
+                           "(there is no CPU or PyTorch fallback)")
+    lib = ctypes.CDLL(path)
+    P = c_void_p
+    IP = POINTER(c_int)
+    sig = {
+        "halo_init": ([POINTER(halo_config), POINTER(c_void_p)], c_int),
+        "halo_local_ranks": ([P, IP, IP], c_int),
+        "halo_pulse_order": ([P, IP, IP], c_int),
+        "halo_scratch_bytes": ([P, POINTER(c_size_t)], c_int),
+        "halo_register_buffers": ([P, c_int, P, P, P], c_int),
+        "halo_ipc_export": ([P, P, POINTER(c_size_t)], c_int),
+        "halo_ipc_import": ([P, P, c_size_t], c_int),
+        "halo_set_maps": ([P, IP, P], c_int),
+        "halo_set_maps_explicit": ([P, IP, IP, POINTER(IP), P], c_int),
+        "halo_get_layout": ([P, c_int, IP, IP, IP, IP, IP, IP, IP, POINTER(c_uint)], c_int),
+        "halo_get_map": ([P, c_int, c_int, IP, c_int], c_int),
+        "halo_exchange_x": ([P, P], c_int),
+        "halo_exchange_f": ([P, P, c_int, P], c_int),
+        "halo_step_host": ([P, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), P, P], c_int),
+        "halo_pack_x_pulse": ([P, c_int, c_int, P, P], c_int),
+        "halo_unpack_f_pulse": ([P, c_int, c_int, P, P, c_int, P], c_int),
+        "halo_get_timers": ([P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
+        "halo_floor_pingpong": ([P, c_int, c_int, POINTER(c_double)], c_int),
+        "halo_sync": ([P], c_int),
+        "halo_strerror": ([c_int], c_char_p),
+        "halo_last_error": ([P], c_char_p),
+        "halo_destroy": ([P], c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib

@@ -1,0 +1,167 @@
+// halo_internal.h — device-visible plan structures and PTX memory-ordering
+// helpers of libhalo.  Private to libhalo (not part of the C ABI).
+//
+// Data layout in HBM:
+//   x, f      caller-owned, capacity rows x layout floats per DD rank
+//   scratch   caller-owned per DD rank, peer-mapped (CUDA IPC):
+//               [0, 4096)                ScratchHdr: flags written by peers
+//               [4096, ...)              P index maps (int32, capacity each)
+//               [..., ...)               P force receive buffers (capacity rows each)
+//   ctrl      library-owned per process: sequence numbers, completion
+//             counters, local "unpacked" flags, set_maps results
+//   plan      library-owned per process: RankDev[], PulseDev[], work items
+#pragma once
+#include <stdint.h>
+#include "../../include/halo.h"
+
+namespace halo {
+
+constexpr int kMaxP = HALO_MAX_PULSES;
+constexpr int kMaxLocal = HALO_MAX_LOCAL;
+constexpr int kMaxRanks = HALO_MAX_RANKS;
+constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
+constexpr int kHdrBytes = 4096;
+
+// Written by PEERS (system scope).  Each array on its own 128-B lines.
+struct __align__(128) ScratchHdr {
+  uint64_t flag_x[8];      // flag_x[p] = seq: the x-sender (upper neighbour) finished pulse p
+  uint64_t pad0[8];
+  uint64_t flag_f[8];      // flag_f[p] = seq: the x-receiver (lower neighbour) pushed slice p
+  uint64_t pad1[8];
+  uint64_t meta_size[8];   // set_maps: (epoch << 32) | send_size of the upper neighbour
+  uint64_t pad2[8];
+  uint64_t meta_off[8];    // set_maps: (epoch << 32) | atomOffset granted by the lower neighbour
+  uint64_t pad3[8];
+  uint64_t ping;           // floor ping-pong flag
+  uint64_t pad4[15];
+  uint64_t status[kMaxRanks];  // set_maps error agreement: (epoch << 32) | err, per source rank
+};
+static_assert(sizeof(ScratchHdr) <= kHdrBytes, "ScratchHdr too large");
+
+// Library-owned control block (device memory, one per process).
+struct Ctrl {
+  uint64_t seq_x;                       // last completed exchange_x sequence number
+  uint64_t seq_f;                       // last completed exchange_f sequence number
+  uint32_t done_x, done_f;              // CTAs finished in the current launch
+  uint64_t t_start_x, t_end_x, t_start_f, t_end_f;  // globaltimer spans (HALO_F_TIMERS)
+  uint64_t span_x, span_f;
+  uint32_t cnt_x[kMaxLocal][kMaxP];       // per-pulse CTA completion counters (Alg. 5 blockCompletionCounter)
+  uint32_t cnt_push[kMaxLocal][kMaxP];
+  uint32_t cnt_unpack[kMaxLocal][kMaxP];
+  uint64_t unpacked[kMaxLocal][kMaxP];    // local flag: pulse p scatter-added (gpu scope)
+  // set_maps results (read back by the host)
+  int32_t send_size[kMaxLocal][kMaxP];
+  int32_t n_indep[kMaxLocal][kMaxP];
+  int32_t recv_size[kMaxLocal][kMaxP];
+  int32_t atom_offset[kMaxLocal][kMaxP];
+  int32_t remote_off[kMaxLocal][kMaxP];
+  uint32_t dep[kMaxLocal][kMaxP];
+  int32_t n_total[kMaxLocal];
+  int32_t err[kMaxLocal];                 // set_maps error bits (kErr*)
+  int32_t agreed_err[kMaxLocal];          // OR over all ranks after the status exchange
+};
+
+enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };
+
+struct RankDev {
+  float* x;                 // own x (capacity rows)
+  float* f;                 // own f
+  ScratchHdr* hdr;          // own scratch header
+  int32_t* maps;            // own maps region (P slots of map_stride ints)
+  float* fbuf;              // own force receive buffers (P slots of fbuf_stride floats)
+  int n_home;
+  int n_total;
+  int rank;                 // global DD rank
+  int pad;
+};
+
+struct PulseDev {
+  const int32_t* map;       // own map of this pulse (send_size entries, ascending)
+  float* x_dst;             // receiver's x + remote_off rows (peer pointer)
+  uint64_t* flag_x_dst;     // &receiver.hdr->flag_x[p]
+  float* fbuf_dst;          // x-sender's force receive buffer of pulse p (peer pointer)
+  uint64_t* flag_f_dst;     // &x-sender.hdr->flag_f[p]
+  const float* fbuf_own;    // own force receive buffer of pulse p
+  float shift[3];           // +L_d on the dim axis when has_shift (R25)
+  int has_shift;
+  int dim;
+  int send_size;
+  int n_indep;              // entries < n_home (Alg. 4 depOffset = n_home, R8)
+  int atom_offset;          // own receive range of pulse p
+  int recv_size;
+  uint32_t dep_x;           // pulses q < p whose receive range map_p reads (R9)
+  uint32_t fdep;            // pulses q > p whose maps read slice p: push(p) waits unpacked[q]
+  uint32_t chain;           // pulses q > p with send_size > 0 (deterministic unpack order)
+  int n_items_x;
+  int n_items_push;
+  int n_items_unpack;
+  int pad;
+};
+
+enum : uint8_t { kItemXIndep = 0, kItemXDep = 1, kItemPush = 2, kItemUnpack = 3 };
+
+struct Item {
+  uint16_t lrank;
+  uint8_t pulse;
+  uint8_t kind;
+  uint32_t begin;
+  uint32_t end;
+};
+
+struct ExParams {
+  const RankDev* ranks;
+  const PulseDev* pulses;   // [n_local * P]
+  const Item* items;
+  int n_items;
+  int n_local;
+  int P;
+  int p_lo, p_hi;           // pulse range of this launch (set_maps runs one pulse at a time)
+  Ctrl* ctrl;
+  int* err_host;            // host-mapped error word (timeout)
+  uint64_t timeout_ns;
+  unsigned flags;
+  double* fshift;           // [n_local][3][3] or nullptr
+  int accumulate;
+};
+
+struct SelParams {
+  const RankDev* ranks;
+  Ctrl* ctrl;
+  int p;                    // pulse index
+  int dim;
+  double rc;
+  const int32_t* cand;      // [n_local][2] candidate row range
+  const double* b_lo;       // [n_local] lower plane b_d[c_d] of the pulse's dim
+  const double* home_lo;    // [n_local][3] (home check; nullptr = skip)
+  const double* home_hi;    // [n_local][3]
+  int decomposed_mask;      // bit d set iff grid[d] > 1
+  int map_stride;
+  int layout;
+};
+
+struct HsParams {
+  Ctrl* ctrl;
+  int p;
+  uint32_t epoch;
+  int capacity;
+  int n_local;
+  ScratchHdr* own[kMaxLocal];
+  uint64_t* size_dst[kMaxLocal];   // &lower.hdr->meta_size[p]
+  uint64_t* off_dst[kMaxLocal];    // &upper.hdr->meta_off[p]
+  int* err_host;
+  uint64_t timeout_ns;
+};
+
+struct StatusParams {
+  Ctrl* ctrl;
+  uint32_t epoch;
+  int nranks;
+  int n_local;
+  int first_rank;
+  ScratchHdr* own[kMaxLocal];
+  ScratchHdr* all[kMaxRanks];       // every rank's scratch header (local or peer-mapped)
+  int* err_host;
+  uint64_t timeout_ns;
+};
+
+}  // namespace halo

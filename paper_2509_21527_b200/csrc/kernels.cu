@@ -1,0 +1,645 @@
+// kernels.cu — sm_100a kernels of libhalo.
+//
+//   k_exchange_x   fused gather + periodic shift + NVLink peer store + per-pulse
+//                  completion + system-scope release flag (Alg. 3 FusedPackCommX,
+//                  Alg. 4 packWithDeps, Alg. 5 syncAndCommWithDeps DATA)
+//   k_exchange_f   dependency-gated push of halo force slices + flag-gated
+//                  ordered scatter-add + fp64 shift forces (Alg. 6
+//                  FusedCommUnpackF, Alg. 5 DEP_MGMT), push variant (R18/R23)
+//   k_select       set_maps: fp64 slab predicate + order-preserving compaction (R2, R3, R11)
+//   k_handshake    set_maps: send size -> receiver, atomOffset -> sender (device flags)
+//   k_depmask      set_maps: wait set of each pulse (R9) and depOffset split (R8)
+//   k_status       set_maps: all-to-all error agreement
+//   k_pack_x / k_unpack_f   per-pulse kernels of the NCCL baseline schedule
+//   k_pingpong     one-way peer flag latency floor
+//
+// All cross-rank synchronisation is release/acquire on 64-bit monotonic
+// sequence numbers (R17).  Every spin is bounded by %globaltimer (timeout ->
+// host-mapped error word, HALO_ERR_TIMEOUT on the next call).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "halo_internal.h"
+
+namespace halo {
+
+// ----------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acqrel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Report a timeout once: host-mapped word (system scope) + give up.
+__device__ __noinline__ void report_timeout(int* err_host, int code) {
+  volatile int* e = err_host;
+  if (*e == 0) *e = code;
+  fence_sys();
+}
+
+// Bounded spin: returns false on timeout.  `sys` selects the scope of the acquire.
+template <bool kSys>
+__device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t v, uint64_t timeout_ns, int* err_host,
+                                         int code) {
+  if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
+  const uint64_t t0 = gtimer();
+  for (;;) {
+    if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
+    if (*(volatile int*)err_host != 0) return false;  // another wait already failed: drain
+    if (gtimer() - t0 > timeout_ns) {
+      report_timeout(err_host, code);
+      return false;
+    }
+  }
+}
+
+// Wait until (*p >> 32) == epoch; returns the low 32 bits (or 0xffffffff on timeout).
+__device__ __forceinline__ uint32_t wait_epoch(const uint64_t* p, uint32_t epoch, uint64_t timeout_ns,
+                                               int* err_host, int code) {
+  const uint64_t t0 = gtimer();
+  for (;;) {
+    uint64_t v = ld_acquire_sys(p);
+    if ((uint32_t)(v >> 32) == epoch) return (uint32_t)v;
+    if (*(volatile int*)err_host != 0) return 0xffffffffu;
+    if (gtimer() - t0 > timeout_ns) {
+      report_timeout(err_host, code);
+      return 0xffffffffu;
+    }
+  }
+}
+
+// timeout codes: kind << 16 | lrank << 8 | pulse
+__device__ __forceinline__ int tcode(int kind, int lr, int p) { return (kind << 16) | (lr << 8) | p; }
+
+// ------------------------------------------------------------- per-CTA timing
+__device__ __forceinline__ void timer_start(unsigned flags, uint64_t* t_start) {
+  if ((flags & HALO_F_TIMERS) && threadIdx.x == 0) atomicMin((unsigned long long*)t_start, gtimer());
+}
+
+// Kernel epilogue: the last CTA publishes the sequence number (graph-safe) and timer span.
+__device__ __forceinline__ void finish_launch(unsigned flags, uint32_t* done, uint64_t* seq_slot, uint64_t seq,
+                                              uint64_t* t_start, uint64_t* t_end, uint64_t* span) {
+  if (threadIdx.x == 0) {
+    if (flags & HALO_F_TIMERS) atomicMax((unsigned long long*)t_end, gtimer());
+    uint32_t old = atom_add_acqrel_gpu(done, 1u);
+    if (old == gridDim.x - 1) {
+      *done = 0;
+      if (flags & HALO_F_TIMERS) {
+        *span = *t_end - *t_start;
+        *t_start = ~0ull;
+        *t_end = 0;
+      }
+      st_release_gpu(seq_slot, seq);
+    }
+  }
+}
+
+// ------------------------------------------------------------ exchange x (hot)
+template <int W>
+__device__ __forceinline__ void x_rows(const PulseDev& pd, const float* __restrict__ x, uint32_t b, uint32_t e,
+                                       bool dep) {
+  const int32_t* __restrict__ map = pd.map;
+  float* __restrict__ dst = pd.x_dst;
+  const bool sh = pd.has_shift != 0;
+  const float s0 = pd.shift[0], s1 = pd.shift[1], s2 = pd.shift[2];
+  for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    const int idx = __ldg(map + i);
+    if constexpr (W == 4) {
+      const float4* src = reinterpret_cast<const float4*>(x) + idx;
+      // dependent rows were written by a peer during this kernel: bypass L1 (.cg)
+      float4 v = dep ? __ldcg(src) : __ldg(src);
+      if (sh) {  // float32 add of the full 3-vector; w is never shifted (R25)
+        v.x = __fadd_rn(v.x, s0);
+        v.y = __fadd_rn(v.y, s1);
+        v.z = __fadd_rn(v.z, s2);
+      }
+      reinterpret_cast<float4*>(dst)[i] = v;
+    } else {
+      const float* src = x + 3 * (size_t)idx;
+      float a, bb, c;
+      if (dep) {
+        a = __ldcg(src); bb = __ldcg(src + 1); c = __ldcg(src + 2);
+      } else {
+        a = __ldg(src); bb = __ldg(src + 1); c = __ldg(src + 2);
+      }
+      if (sh) {
+        a = __fadd_rn(a, s0);
+        bb = __fadd_rn(bb, s1);
+        c = __fadd_rn(c, s2);
+      }
+      float* o = dst + 3 * (size_t)i;
+      o[0] = a; o[1] = bb; o[2] = c;
+    }
+  }
+}
+
+// Notify the receiver once per pulse: every CTA fences its peer stores and
+// increments the pulse's completion counter; the last CTA stores the flag
+// (Alg. 5: "only threadIdx.x = 0 proceeds to notify").
+__device__ __forceinline__ void pulse_complete_sys(unsigned flags, uint32_t* cnt, int n_items, uint64_t* flag_dst,
+                                                   uint64_t seq) {
+  if (flags & HALO_F_GPU_FENCE) fence_gpu(); else fence_sys();
+  uint32_t old = atom_add_acqrel_gpu(cnt, 1u);
+  if (old == (uint32_t)n_items - 1) {
+    *cnt = 0;  // no other CTA of this launch touches it again
+    st_release_sys(flag_dst, seq);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__ ExParams P) {
+  __shared__ uint64_t s_seq;
+  Ctrl* ctrl = P.ctrl;
+  if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
+  timer_start(P.flags, &ctrl->t_start_x);
+  __syncthreads();
+  const uint64_t seq = s_seq;
+  const uint32_t lo_mask = (P.p_lo > 0) ? ((1u << P.p_lo) - 1u) : 0u;
+
+  for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
+    const Item w = P.items[it];
+    const PulseDev& pd = P.pulses[w.lrank * P.P + w.pulse];
+    const RankDev& rd = P.ranks[w.lrank];
+    const bool dep = (w.kind == kItemXDep);
+    if (dep) {
+      // Alg. 4: leader acquire-waits exactly the pulses the dependent entries came
+      // from (R9; pulses below p_lo completed in earlier launches), then a barrier.
+      if (threadIdx.x == 0) {
+        uint32_t m = pd.dep_x & ~lo_mask;
+        while (m) {
+          const int q = __ffs(m) - 1;
+          m &= m - 1;
+          wait_geq<true>(&rd.hdr->flag_x[q], seq, P.timeout_ns, P.err_host, tcode(1, w.lrank, q));
+        }
+      }
+      __syncthreads();
+    }
+    x_rows<W>(pd, rd.x, w.begin, w.end, dep);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      pulse_complete_sys(P.flags, &ctrl->cnt_x[w.lrank][w.pulse], pd.n_items_x, pd.flag_x_dst, seq);
+  }
+  // The launch completes only when this process's halos are complete, so that
+  // stream-ordered consumers (non-local NB) see them.
+  if (blockIdx.x < P.n_local && threadIdx.x == 0) {
+    const int lr = blockIdx.x;
+    const RankDev& rd = P.ranks[lr];
+    for (int p = P.p_lo; p < P.p_hi; ++p) {
+      if (P.pulses[lr * P.P + p].recv_size > 0)
+        wait_geq<true>(&rd.hdr->flag_x[p], seq, P.timeout_ns, P.err_host, tcode(2, lr, p));
+    }
+  }
+  __syncthreads();
+  finish_launch(P.flags, &ctrl->done_x, &ctrl->seq_x, seq, &ctrl->t_start_x, &ctrl->t_end_x, &ctrl->span_x);
+}
+
+// ------------------------------------------------------------ exchange f (hot)
+template <int W>
+__device__ __forceinline__ void push_rows(const PulseDev& pd, const float* __restrict__ f, uint32_t b, uint32_t e) {
+  // slice rows [atom_offset + b, atom_offset + e) -> peer fbuf rows [b, e): contiguous
+  const float* src = f + (size_t)(pd.atom_offset + b) * W;
+  float* dst = pd.fbuf_dst + (size_t)b * W;
+  const uint32_t n = (e - b) * W;
+  if constexpr (W == 4) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (uint32_t i = threadIdx.x; i < (e - b); i += blockDim.x) d4[i] = __ldcg(s4 + i);
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcg(src + i);
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int W>
+__device__ __forceinline__ void unpack_rows(const PulseDev& pd, float* __restrict__ f, uint32_t b, uint32_t e,
+                                            bool atomic, bool accumulate, double* fshift_rank) {
+  const int32_t* __restrict__ map = pd.map;
+  const float* __restrict__ buf = pd.fbuf_own;
+  const bool do_shift = (fshift_rank != nullptr) && pd.has_shift;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    const int t = __ldg(map + i);
+    float v[4];
+    if constexpr (W == 4) {
+      float4 q = __ldcg(reinterpret_cast<const float4*>(buf) + i);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      v[0] = __ldcg(buf + 3 * (size_t)i); v[1] = __ldcg(buf + 3 * (size_t)i + 1); v[2] = __ldcg(buf + 3 * (size_t)i + 2);
+    }
+    float* dst = f + (size_t)t * W;
+    if (!accumulate) {
+#pragma unroll
+      for (int c = 0; c < W; ++c) dst[c] = v[c];
+    } else if (atomic) {
+#pragma unroll
+      for (int c = 0; c < W; ++c) atomicAdd(dst + c, v[c]);
+    } else {
+      if constexpr (W == 4) {
+        float4 o = __ldcg(reinterpret_cast<const float4*>(dst));
+        o.x = __fadd_rn(o.x, v[0]); o.y = __fadd_rn(o.y, v[1]); o.z = __fadd_rn(o.z, v[2]); o.w = __fadd_rn(o.w, v[3]);
+        *reinterpret_cast<float4*>(dst) = o;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dst[c] = __fadd_rn(__ldcg(dst + c), v[c]);
+      }
+    }
+    if (do_shift) { a0 += (double)v[0]; a1 += (double)v[1]; a2 += (double)v[2]; }
+  }
+  if (do_shift) {
+    a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2);
+    if ((threadIdx.x & 31) == 0) {
+      double* fs = fshift_rank + 3 * pd.dim;
+      atomicAdd(fs + 0, a0); atomicAdd(fs + 1, a1); atomicAdd(fs + 2, a2);
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__ ExParams P) {
+  __shared__ uint64_t s_seq;
+  Ctrl* ctrl = P.ctrl;
+  if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
+  timer_start(P.flags, &ctrl->t_start_f);
+  __syncthreads();
+  const uint64_t seq = s_seq;
+  const bool atomic = (P.flags & HALO_F_ATOMIC_UNPACK) != 0;
+
+  for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
+    const Item w = P.items[it];
+    const PulseDev& pd = P.pulses[w.lrank * P.P + w.pulse];
+    const RankDev& rd = P.ranks[w.lrank];
+    if (w.kind == kItemPush) {
+      // DEP_MGMT (Alg. 5): slice p is final once every later pulse that
+      // forwarded rows of it has been unpacked here.
+      if (threadIdx.x == 0) {
+        uint32_t m = pd.fdep;
+        while (m) {
+          const int q = __ffs(m) - 1;
+          m &= m - 1;
+          wait_geq<false>(&ctrl->unpacked[w.lrank][q], seq, P.timeout_ns, P.err_host, tcode(3, w.lrank, q));
+        }
+      }
+      __syncthreads();
+      push_rows<W>(pd, rd.f, w.begin, w.end);
+      __syncthreads();
+      if (threadIdx.x == 0)
+        pulse_complete_sys(P.flags, &ctrl->cnt_push[w.lrank][w.pulse], pd.n_items_push, pd.flag_f_dst, seq);
+    } else {  // kItemUnpack
+      if (threadIdx.x == 0) {
+        wait_geq<true>(&rd.hdr->flag_f[w.pulse], seq, P.timeout_ns, P.err_host, tcode(4, w.lrank, w.pulse));
+        if (!atomic) {  // deterministic: pulses descending (R15)
+          uint32_t m = pd.chain;
+          while (m) {
+            const int q = __ffs(m) - 1;
+            m &= m - 1;
+            wait_geq<false>(&ctrl->unpacked[w.lrank][q], seq, P.timeout_ns, P.err_host, tcode(5, w.lrank, q));
+          }
+        }
+      }
+      __syncthreads();
+      double* fs = P.fshift ? P.fshift + 9 * w.lrank : nullptr;
+      unpack_rows<W>(pd, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_gpu();
+        uint32_t old = atom_add_acqrel_gpu(&ctrl->cnt_unpack[w.lrank][w.pulse], 1u);
+        if (old == (uint32_t)pd.n_items_unpack - 1) {
+          ctrl->cnt_unpack[w.lrank][w.pulse] = 0;
+          st_release_gpu(&ctrl->unpacked[w.lrank][w.pulse], seq);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  finish_launch(P.flags, &ctrl->done_f, &ctrl->seq_f, seq, &ctrl->t_start_f, &ctrl->t_end_f, &ctrl->span_f);
+}
+
+// ------------------------------------------------------------- set_maps kernels
+// One CTA (1024 threads) per local rank: ordered compaction of the candidate
+// rows [cand0, cand1) with the fp64 slab predicate (R2, R3).  Also checks, on
+// the first pulse, that home atoms lie in the rank's cell.
+__global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelParams S) {
+  const int lr = blockIdx.x;
+  const RankDev& rd = S.ranks[lr];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_cnt[32];
+  __shared__ int s_total;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  if (S.home_lo != nullptr) {
+    for (int i = threadIdx.x; i < rd.n_home; i += blockDim.x) {
+      bool bad = false;
+      for (int d = 0; d < 3; ++d) {
+        if (!(S.decomposed_mask & (1 << d))) continue;
+        const double v = (double)rd.x[(size_t)i * S.layout + d];
+        bad |= !(v >= S.home_lo[3 * lr + d] && v < S.home_hi[3 * lr + d]);
+      }
+      if (bad) s_bad = 1;
+    }
+  }
+  const int c0 = S.cand[2 * lr], c1 = S.cand[2 * lr + 1];
+  int32_t* out = rd.maps + (size_t)S.p * S.map_stride;
+  const double blo = S.b_lo[lr];
+  int base = 0;
+  for (int t0 = c0; t0 < c1; t0 += blockDim.x) {
+    const int i = t0 + threadIdx.x;
+    bool sel = false;
+    if (i < c1) {
+      const double v = (double)rd.x[(size_t)i * S.layout + S.dim];
+      sel = __dsub_rn(v, blo) < S.rc;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0) s_cnt[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      const int c = (lane < (int)(blockDim.x >> 5)) ? s_cnt[lane] : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      s_cnt[lane] = incl - c;
+      if (lane == 31) s_total = incl;
+    }
+    __syncthreads();
+    if (sel) out[base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u))] = i;
+    base += s_total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    S.ctrl->send_size[lr][S.p] = base;
+    if (s_bad) S.ctrl->err[lr] |= kErrGeometry;
+  }
+}
+
+// One warp per local rank (lane 0): size -> receiver, wait own size, grant
+// atomOffset -> sender, wait own grant.  All local ranks are co-resident.
+__global__ void k_handshake(const __grid_constant__ HsParams H) {
+  if (threadIdx.x != 0) return;
+  const int lr = blockIdx.x;
+  Ctrl* c = H.ctrl;
+  const int p = H.p;
+  const uint64_t ep = (uint64_t)H.epoch << 32;
+  const uint32_t sz = (uint32_t)c->send_size[lr][p];
+  st_release_sys(H.size_dst[lr], ep | sz);
+  uint32_t recv = wait_epoch(&H.own[lr]->meta_size[p], H.epoch, H.timeout_ns, H.err_host, tcode(6, lr, p));
+  if (recv == 0xffffffffu) recv = 0;
+  const int off = c->n_total[lr];
+  uint32_t grant = (uint32_t)off;
+  if ((long long)off + (long long)recv > (long long)H.capacity) {
+    c->err[lr] |= kErrCapacity;
+    grant = 0xffffffffu;
+    recv = 0;
+  }
+  st_release_sys(H.off_dst[lr], ep | grant);
+  const uint32_t roff = wait_epoch(&H.own[lr]->meta_off[p], H.epoch, H.timeout_ns, H.err_host, tcode(7, lr, p));
+  if (roff == 0xffffffffu) {  // receiver out of capacity (or timeout): send nothing
+    c->send_size[lr][p] = 0;
+    c->remote_off[lr][p] = 0;
+  } else {
+    c->remote_off[lr][p] = (int)roff;
+  }
+  c->recv_size[lr][p] = (int)recv;
+  c->atom_offset[lr][p] = off;
+  c->n_total[lr] = off + (int)recv;
+}
+
+// One CTA per local rank: dep mask of pulse p (which earlier receive ranges the
+// map reads, R9) and the number of entries < n_home (depOffset split, R8).
+__global__ void __launch_bounds__(256) k_depmask(const RankDev* ranks, Ctrl* ctrl, int p, int map_stride) {
+  const int lr = blockIdx.x;
+  const RankDev& rd = ranks[lr];
+  __shared__ unsigned s_mask;
+  __shared__ int s_indep;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) { s_mask = 0; s_indep = 0; s_bad = 0; }
+  __syncthreads();
+  const int n = ctrl->send_size[lr][p];
+  const int32_t* map = rd.maps + (size_t)p * map_stride;
+  unsigned m = 0;
+  int indep = 0;
+  bool bad = false;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int idx = map[i];
+    if (idx < rd.n_home) { ++indep; continue; }
+    bool found = false;
+    for (int q = 0; q < p; ++q) {
+      const int a = ctrl->atom_offset[lr][q], r = ctrl->recv_size[lr][q];
+      if (idx >= a && idx < a + r) { m |= 1u << q; found = true; break; }
+    }
+    bad |= !found;
+  }
+  if (m) atomicOr(&s_mask, m);
+  if (indep) atomicAdd(&s_indep, indep);
+  if (bad) s_bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctrl->dep[lr][p] = s_mask;
+    ctrl->n_indep[lr][p] = s_indep;
+    if (s_bad) ctrl->err[lr] |= kErrMap;
+  }
+}
+
+// One CTA per local rank, one thread per destination rank: error agreement.
+__global__ void k_status(const __grid_constant__ StatusParams S) {
+  const int lr = blockIdx.x;
+  const int me = S.first_rank + lr;
+  const uint64_t ep = (uint64_t)S.epoch << 32;
+  __shared__ int s_or;
+  if (threadIdx.x == 0) s_or = 0;
+  __syncthreads();
+  const uint32_t mine = (uint32_t)S.ctrl->err[lr];
+  for (int t = threadIdx.x; t < S.nranks; t += blockDim.x) st_release_sys(&S.all[t]->status[me], ep | mine);
+  for (int t = threadIdx.x; t < S.nranks; t += blockDim.x) {
+    const uint32_t v = wait_epoch(&S.own[lr]->status[t], S.epoch, S.timeout_ns, S.err_host, tcode(8, lr, 0));
+    if (v != 0xffffffffu && v != 0) atomicOr(&s_or, (int)v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) S.ctrl->agreed_err[lr] = s_or;
+}
+
+// ---------------------------------------------------- NCCL-baseline pulse kernels
+template <int W>
+__global__ void k_pack_x(const int32_t* __restrict__ map, int n, const float* __restrict__ x, float* __restrict__ out,
+                         int has_shift, float s0, float s1, float s2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int idx = map[i];
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < W; ++c) v[c] = x[(size_t)idx * W + c];
+    if (has_shift) { v[0] = __fadd_rn(v[0], s0); v[1] = __fadd_rn(v[1], s1); v[2] = __fadd_rn(v[2], s2); }
+#pragma unroll
+    for (int c = 0; c < W; ++c) out[(size_t)i * W + c] = v[c];
+  }
+}
+
+template <int W>
+__global__ void k_unpack_f(const int32_t* __restrict__ map, int n, const float* __restrict__ buf, float* __restrict__ f,
+                           int accumulate, double* fs_dim) {
+  double a0 = 0, a1 = 0, a2 = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int t = map[i];
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < W; ++c) v[c] = buf[(size_t)i * W + c];
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      float* d = f + (size_t)t * W + c;
+      *d = accumulate ? __fadd_rn(*d, v[c]) : v[c];
+    }
+    a0 += v[0]; a1 += v[1]; a2 += v[2];
+  }
+  if (fs_dim) {
+    a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2);
+    if ((threadIdx.x & 31) == 0) { atomicAdd(fs_dim, a0); atomicAdd(fs_dim + 1, a1); atomicAdd(fs_dim + 2, a2); }
+  }
+}
+
+// --------------------------------------------------------------- latency floor
+__global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator,
+                           uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 1; i <= iters; ++i) {
+    const uint64_t v = base + (uint64_t)i;
+    if (initiator) {
+      const uint64_t t0 = gtimer();
+      st_release_sys(peer, v);
+      if (!wait_geq<true>(own, v, timeout_ns, err_host, tcode(9, 0, 0))) return;
+      rtt_ns[i - 1] = gtimer() - t0;
+    } else {
+      if (!wait_geq<true>(own, v, timeout_ns, err_host, tcode(9, 1, 0))) return;
+      st_release_sys(peer, v);
+    }
+  }
+}
+
+// ------------------------------------------------------------- host launchers
+static cudaError_t launch_coop(const void* fn, int grid, int block, void** args, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStream_t st) {
+  void* args[] = {(void*)&p};
+  const void* fn = layout == 4 ? (const void*)k_exchange_x<4> : (const void*)k_exchange_x<3>;
+  return launch_coop(fn, grid, kThreads, args, st);
+}
+
+cudaError_t launch_exchange_f(const ExParams& p, int layout, int grid, cudaStream_t st) {
+  void* args[] = {(void*)&p};
+  const void* fn = layout == 4 ? (const void*)k_exchange_f<4> : (const void*)k_exchange_f<3>;
+  return launch_coop(fn, grid, kThreads, args, st);
+}
+
+cudaError_t max_coresident(int layout, int* x_blocks, int* f_blocks) {
+  int dev = 0, sms = 0, bx = 0, bf = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &bx, layout == 4 ? (const void*)k_exchange_x<4> : (const void*)k_exchange_x<3>, kThreads, 0);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &bf, layout == 4 ? (const void*)k_exchange_f<4> : (const void*)k_exchange_f<3>, kThreads, 0);
+  if (e != cudaSuccess) return e;
+  *x_blocks = bx * sms;
+  *f_blocks = bf * sms;
+  return cudaSuccess;
+}
+
+cudaError_t launch_select(const SelParams& s, int n_local, cudaStream_t st) {
+  void* args[] = {(void*)&s};
+  return cudaLaunchKernel((const void*)k_select, dim3(n_local), dim3(1024), args, 0, st);
+}
+
+cudaError_t launch_handshake(const HsParams& h, cudaStream_t st) {
+  void* args[] = {(void*)&h};
+  return launch_coop((const void*)k_handshake, h.n_local, 32, args, st);
+}
+
+cudaError_t launch_depmask(const RankDev* ranks, Ctrl* ctrl, int p, int map_stride, int n_local, cudaStream_t st) {
+  k_depmask<<<n_local, 256, 0, st>>>(ranks, ctrl, p, map_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_status(const StatusParams& s, cudaStream_t st) {
+  void* args[] = {(void*)&s};
+  return launch_coop((const void*)k_status, s.n_local, 64, args, st);
+}
+
+cudaError_t launch_pack_x(int layout, const int32_t* map, int n, const float* x, float* out, int has_shift,
+                          const float* shift, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (n + 255) / 256;
+  if (layout == 4)
+    k_pack_x<4><<<grid, 256, 0, st>>>(map, n, x, out, has_shift, shift[0], shift[1], shift[2]);
+  else
+    k_pack_x<3><<<grid, 256, 0, st>>>(map, n, x, out, has_shift, shift[0], shift[1], shift[2]);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* buf, float* f, int accumulate,
+                            double* fs_dim, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (n + 255) / 256;
+  if (layout == 4)
+    k_unpack_f<4><<<grid, 256, 0, st>>>(map, n, buf, f, accumulate, fs_dim);
+  else
+    k_unpack_f<3><<<grid, 256, 0, st>>>(map, n, buf, f, accumulate, fs_dim);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator,
+                            uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st) {
+  k_pingpong<<<1, 32, 0, st>>>(own, peer, iters, base, initiator, rtt_ns, timeout_ns, err_host);
+  return cudaGetLastError();
+}
+
+}  // namespace halo

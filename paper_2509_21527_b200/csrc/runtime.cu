@@ -1,0 +1,963 @@
+// runtime.cu — host side of libhalo: config validation, pulse plan, IPC peer
+// table, set_maps driver, work-item tables, C ABI entry points.
+//
+// Citations: P:<n> = PAPER.md line, R<n> = DESIGN.md reading.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "halo_internal.h"
+
+namespace halo {
+cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStream_t st);
+cudaError_t launch_exchange_f(const ExParams& p, int layout, int grid, cudaStream_t st);
+cudaError_t max_coresident(int layout, int* x_blocks, int* f_blocks);
+cudaError_t launch_select(const SelParams& s, int n_local, cudaStream_t st);
+cudaError_t launch_handshake(const HsParams& h, cudaStream_t st);
+cudaError_t launch_depmask(const RankDev* ranks, Ctrl* ctrl, int p, int map_stride, int n_local, cudaStream_t st);
+cudaError_t launch_status(const StatusParams& s, cudaStream_t st);
+cudaError_t launch_pack_x(int layout, const int32_t* map, int n, const float* x, float* out, int has_shift,
+                          const float* shift, cudaStream_t st);
+cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* buf, float* f, int accumulate,
+                            double* fs_dim, cudaStream_t st);
+cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator,
+                            uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
+}  // namespace halo
+
+using namespace halo;
+
+namespace {
+
+constexpr uint32_t kBlobMagic = 0x48414c4fu;  // "HALO"
+
+struct BlobHdr {
+  uint32_t magic;
+  uint32_t version;
+  int32_t proc;
+  int32_t n_local;
+  int32_t first_rank;
+  int32_t device;
+  int32_t layout;
+  int32_t capacity;
+  uint64_t pid;
+};
+struct BlobEntry {
+  cudaIpcMemHandle_t hx;
+  uint64_t offx;
+  cudaIpcMemHandle_t hs;
+  uint64_t offs;
+};
+
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda link,
+// so the library loads on hosts without a driver).
+typedef int (*PFN_memGetAddressRange)(unsigned long long* base, size_t* size, unsigned long long dptr);
+
+PFN_memGetAddressRange get_addr_range_fn() {
+  static PFN_memGetAddressRange fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_memGetAddressRange)p;
+  }
+  return fn;
+}
+
+}  // namespace
+
+struct halo_ctx {
+  halo_config cfg{};
+  int nranks = 0, n_local = 0, first_rank = 0, P = 0, W = 3;
+  int pdim[kMaxP] = {0}, pk[kMaxP] = {0};
+  size_t map_stride = 0, fbuf_stride = 0, scratch_bytes = 0;
+  std::string last_error;
+
+  // registered local buffers
+  std::vector<float*> x, f;
+  std::vector<char*> scratch;
+  // every rank's peer view (local pointers for this process's ranks)
+  std::vector<float*> peer_x;
+  std::vector<char*> peer_scratch;
+  std::vector<void*> opened;  // IPC bases to close
+  bool peers_ready = false;
+
+  // library-owned device memory
+  Ctrl* ctrl = nullptr;
+  char* plan = nullptr;
+  size_t plan_bytes = 0;
+  RankDev* d_ranks = nullptr;
+  PulseDev* d_pulses = nullptr;
+  Item* d_items_x = nullptr;
+  Item* d_items_f = nullptr;
+  int n_items_x = 0, n_items_f = 0;
+  double* d_fshift_tmp = nullptr;  // halo_step_host
+  char* d_small = nullptr;          // set_maps argument staging
+  uint64_t* d_rtt = nullptr;
+  int* err_host = nullptr;          // host-mapped error word
+  int* err_dev = nullptr;
+
+  // host plan
+  std::vector<RankDev> h_ranks;
+  std::vector<PulseDev> h_pulses;
+  std::vector<Item> h_items_x, h_items_f;
+  std::vector<int> n_home, n_total;
+  std::vector<int> send_size, recv_size, atom_offset, remote_off, n_indep;  // [n_local*P]
+  std::vector<unsigned> dep;
+  bool maps_ready = false;
+  bool x_done = false;
+  uint32_t epoch = 0;
+  uint64_t ping_base = 0;
+  int max_x = 0, max_f = 0;
+  int item_rows = 512;
+
+  int cell(int r, int d) const {
+    const int* g = cfg.grid;
+    if (d == 2) return r % g[2];
+    if (d == 1) return (r / g[2]) % g[1];
+    return r / (g[1] * g[2]);
+  }
+  int rank_of(int cx, int cy, int cz) const { return (cx * cfg.grid[1] + cy) * cfg.grid[2] + cz; }
+  int neighbour(int r, int d, int delta) const {
+    int c[3] = {cell(r, 0), cell(r, 1), cell(r, 2)};
+    c[d] = ((c[d] + delta) % cfg.grid[d] + cfg.grid[d]) % cfg.grid[d];
+    return rank_of(c[0], c[1], c[2]);
+  }
+  // b_d[k] = float64(L_d) * k / grid[d]  (R3: multiply then divide, IEEE double)
+  double plane(int d, int k) const { return (double)cfg.box[d] * (double)k / (double)cfg.grid[d]; }
+  ScratchHdr* hdr_of(int r) const { return reinterpret_cast<ScratchHdr*>(peer_scratch[r]); }
+  int32_t* maps_of_local(int l) const { return reinterpret_cast<int32_t*>(scratch[l] + kHdrBytes); }
+  float* fbuf_of(int r) const {
+    return reinterpret_cast<float*>(peer_scratch[r] + kHdrBytes + (size_t)P * map_stride * sizeof(int32_t));
+  }
+};
+
+// --------------------------------------------------------------------- helpers
+static halo_status fail(halo_ctx* c, halo_status s, const std::string& msg) {
+  if (c) c->last_error = msg;
+  return s;
+}
+static halo_status cuda_fail(halo_ctx* c, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  (void)cudaGetLastError();
+  return fail(c, HALO_ERR_CUDA, m);
+}
+#define CK(call)                                                   \
+  do {                                                             \
+    cudaError_t e__ = (call);                                      \
+    if (e__ != cudaSuccess) return cuda_fail(ctx, e__, #call);     \
+  } while (0)
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static halo_status check_err_word(halo_ctx* ctx) {
+  if (ctx->err_host && *(volatile int*)ctx->err_host != 0) {
+    char buf[128];
+    int code = *(volatile int*)ctx->err_host;
+    snprintf(buf, sizeof buf, "device wait timed out (kind %d, local rank %d, pulse %d)", code >> 16,
+             (code >> 8) & 0xff, code & 0xff);
+    return fail(ctx, HALO_ERR_TIMEOUT, buf);
+  }
+  return HALO_OK;
+}
+
+static halo_status validate(const halo_config* c, std::string& why) {
+  if (!c) { why = "cfg is NULL"; return HALO_ERR_ARG; }
+  if (c->layout != 3 && c->layout != 4) { why = "layout must be 3 or 4"; return HALO_ERR_ARG; }
+  if (c->capacity <= 0) { why = "capacity must be > 0"; return HALO_ERR_ARG; }
+  if (c->nprocs < 1 || c->proc < 0 || c->proc >= c->nprocs) { why = "bad nprocs/proc"; return HALO_ERR_ARG; }
+  long long nr = 1;
+  int P = 0;
+  for (int d = 0; d < 3; ++d) {
+    if (c->grid[d] < 1) { why = "grid[d] must be >= 1"; return HALO_ERR_GEOMETRY; }
+    nr *= c->grid[d];
+    if ((c->grid[d] > 1) != (c->pulses[d] >= 1)) { why = "pulses[d] >= 1 iff grid[d] > 1"; return HALO_ERR_GEOMETRY; }
+    if (c->pulses[d] > std::max(c->grid[d] - 1, 0)) { why = "pulses[d] must be <= grid[d]-1"; return HALO_ERR_GEOMETRY; }
+    if (c->pulses[d] > 2) { why = "at most two pulses per dimension (P:143)"; return HALO_ERR_UNSUPPORTED; }
+    if (!(c->box[d] > 0.0f) || !std::isfinite(c->box[d])) { why = "box lengths must be > 0"; return HALO_ERR_GEOMETRY; }
+    if (c->grid[d] > 1 && (double)c->pulses[d] * ((double)c->box[d] / c->grid[d]) < (double)c->cutoff) {
+      why = "not enough pulses: pulses[d]*L_d/grid[d] < rc";
+      return HALO_ERR_GEOMETRY;
+    }
+    P += c->grid[d] > 1 ? c->pulses[d] : 0;
+  }
+  double minL = std::min(std::min((double)c->box[0], (double)c->box[1]), (double)c->box[2]);
+  if (!((double)c->cutoff > 0.0 && (double)c->cutoff < minL / 2.0)) { why = "need 0 < rc < min(L)/2"; return HALO_ERR_GEOMETRY; }
+  if (nr > kMaxRanks) { why = "too many ranks for this build (HALO_MAX_RANKS)"; return HALO_ERR_UNSUPPORTED; }
+  if (nr % c->nprocs != 0) { why = "nranks must be a multiple of nprocs"; return HALO_ERR_ARG; }
+  if (nr / c->nprocs > kMaxLocal) { why = "too many ranks per process (HALO_MAX_LOCAL)"; return HALO_ERR_UNSUPPORTED; }
+  if (P > kMaxP) { why = "too many pulses"; return HALO_ERR_UNSUPPORTED; }
+  return HALO_OK;
+}
+
+// ------------------------------------------------------------------- C ABI
+extern "C" {
+
+const char* halo_strerror(halo_status s) {
+  switch (s) {
+    case HALO_OK: return "ok";
+    case HALO_ERR_ARG: return "invalid argument";
+    case HALO_ERR_GEOMETRY: return "invalid geometry";
+    case HALO_ERR_CAPACITY: return "capacity exceeded";
+    case HALO_ERR_STATE: return "call out of order";
+    case HALO_ERR_CUDA: return "CUDA error";
+    case HALO_ERR_PEER: return "peer/IPC error";
+    case HALO_ERR_TIMEOUT: return "device wait timed out";
+    case HALO_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* halo_last_error(const halo_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
+  if (!out) return HALO_ERR_ARG;
+  *out = nullptr;
+  std::string why;
+  halo_status s = validate(cfg, why);
+  if (s != HALO_OK) return s;
+  halo_ctx* ctx = new halo_ctx();
+  ctx->cfg = *cfg;
+  if (ctx->cfg.timeout_s <= 0) ctx->cfg.timeout_s = 10.0;
+  ctx->W = cfg->layout;
+  ctx->nranks = cfg->grid[0] * cfg->grid[1] * cfg->grid[2];
+  ctx->n_local = ctx->nranks / cfg->nprocs;
+  ctx->first_rank = cfg->proc * ctx->n_local;
+  const int order[3] = {2, 1, 0};  // z -> y -> x
+  for (int i = 0; i < 3; ++i) {
+    const int d = order[i];
+    if (cfg->grid[d] > 1)
+      for (int k = 0; k < cfg->pulses[d]; ++k) {
+        ctx->pdim[ctx->P] = d;
+        ctx->pk[ctx->P] = k;
+        ctx->P++;
+      }
+  }
+  ctx->map_stride = align_up((size_t)cfg->capacity, 64);
+  ctx->fbuf_stride = align_up((size_t)cfg->capacity * cfg->layout, 64);
+  ctx->scratch_bytes = kHdrBytes + (size_t)ctx->P * ctx->map_stride * sizeof(int32_t) +
+                       (size_t)ctx->P * ctx->fbuf_stride * sizeof(float);
+  ctx->x.assign(ctx->n_local, nullptr);
+  ctx->f.assign(ctx->n_local, nullptr);
+  ctx->scratch.assign(ctx->n_local, nullptr);
+  ctx->peer_x.assign(ctx->nranks, nullptr);
+  ctx->peer_scratch.assign(ctx->nranks, nullptr);
+  if (const char* e = getenv("HALO_ITEM_ROWS")) ctx->item_rows = std::max(32, atoi(e));
+
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->ctrl, sizeof(Ctrl));
+  if (e == cudaSuccess) e = cudaMemset(ctx->ctrl, 0, sizeof(Ctrl));
+  if (e == cudaSuccess) {
+    uint64_t init[4] = {~0ull, 0, ~0ull, 0};
+    e = cudaMemcpy(&ctx->ctrl->t_start_x, init, sizeof init, cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) e = cudaHostAlloc(&ctx->err_host, 64, cudaHostAllocMapped);
+  if (e == cudaSuccess) { memset(ctx->err_host, 0, 64); e = cudaHostGetDevicePointer(&ctx->err_dev, ctx->err_host, 0); }
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_small, 64 * 1024);
+  if (e == cudaSuccess) e = max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
+  if (e != cudaSuccess) {
+    // keep ctx to carry the message? The ABI returns NULL on error; print once.
+    fprintf(stderr, "halo_init: %s\n", cudaGetErrorString(e));
+    (void)cudaGetLastError();
+    halo_destroy(ctx);
+    return HALO_ERR_CUDA;
+  }
+  *out = ctx;
+  return HALO_OK;
+}
+
+halo_status halo_local_ranks(const halo_ctx* ctx, int* first_rank, int* n_local) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (first_rank) *first_rank = ctx->first_rank;
+  if (n_local) *n_local = ctx->n_local;
+  return HALO_OK;
+}
+
+halo_status halo_pulse_order(const halo_ctx* ctx, int* npulse, int* dims) {
+  if (!ctx || !npulse) return HALO_ERR_ARG;
+  *npulse = ctx->P;
+  if (dims)
+    for (int p = 0; p < ctx->P; ++p) dims[p] = ctx->pdim[p];
+  return HALO_OK;
+}
+
+halo_status halo_scratch_bytes(const halo_ctx* ctx, size_t* bytes) {
+  if (!ctx || !bytes) return HALO_ERR_ARG;
+  *bytes = ctx->scratch_bytes;
+  return HALO_OK;
+}
+
+halo_status halo_register_buffers(halo_ctx* ctx, int local, void* x, void* f, void* scratch) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (local < 0 || local >= ctx->n_local) return fail(ctx, HALO_ERR_ARG, "local rank out of range");
+  if (!x || !f || !scratch) return fail(ctx, HALO_ERR_ARG, "NULL buffer");
+  if (((uintptr_t)x | (uintptr_t)f) & 15) return fail(ctx, HALO_ERR_ARG, "x and f must be 16-B aligned");
+  if ((uintptr_t)scratch & 255) return fail(ctx, HALO_ERR_ARG, "scratch must be 256-B aligned");
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaMemset(scratch, 0, ctx->scratch_bytes));
+  CK(cudaDeviceSynchronize());
+  ctx->x[local] = (float*)x;
+  ctx->f[local] = (float*)f;
+  ctx->scratch[local] = (char*)scratch;
+  const int r = ctx->first_rank + local;
+  ctx->peer_x[r] = (float*)x;
+  ctx->peer_scratch[r] = (char*)scratch;
+  ctx->maps_ready = false;
+  bool all = true;
+  for (int l = 0; l < ctx->n_local; ++l) all &= ctx->scratch[l] != nullptr;
+  if (all && ctx->cfg.nprocs == 1) ctx->peers_ready = true;
+  return HALO_OK;
+}
+
+halo_status halo_ipc_export(halo_ctx* ctx, void* blob, size_t* len) {
+  if (!ctx || !len) return HALO_ERR_ARG;
+  const size_t need = sizeof(BlobHdr) + (size_t)ctx->n_local * sizeof(BlobEntry);
+  if (!blob) { *len = need; return HALO_OK; }
+  if (*len < need) return fail(ctx, HALO_ERR_ARG, "blob too small");
+  for (int l = 0; l < ctx->n_local; ++l)
+    if (!ctx->x[l]) return fail(ctx, HALO_ERR_STATE, "register all local buffers before export");
+  PFN_memGetAddressRange range = get_addr_range_fn();
+  if (!range) return fail(ctx, HALO_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+  CK(cudaSetDevice(ctx->cfg.device));
+  BlobHdr h{};
+  h.magic = kBlobMagic;
+  h.version = HALO_ABI_VERSION;
+  h.proc = ctx->cfg.proc;
+  h.n_local = ctx->n_local;
+  h.first_rank = ctx->first_rank;
+  h.device = ctx->cfg.device;
+  h.layout = ctx->cfg.layout;
+  h.capacity = ctx->cfg.capacity;
+  h.pid = 0;
+  memcpy(blob, &h, sizeof h);
+  BlobEntry* ents = reinterpret_cast<BlobEntry*>((char*)blob + sizeof h);
+  for (int l = 0; l < ctx->n_local; ++l) {
+    BlobEntry be{};
+    unsigned long long base = 0;
+    size_t sz = 0;
+    if (range(&base, &sz, (unsigned long long)(uintptr_t)ctx->x[l]) != 0)
+      return fail(ctx, HALO_ERR_PEER, "cuMemGetAddressRange(x) failed");
+    CK(cudaIpcGetMemHandle(&be.hx, (void*)(uintptr_t)base));
+    be.offx = (uintptr_t)ctx->x[l] - base;
+    if (range(&base, &sz, (unsigned long long)(uintptr_t)ctx->scratch[l]) != 0)
+      return fail(ctx, HALO_ERR_PEER, "cuMemGetAddressRange(scratch) failed");
+    CK(cudaIpcGetMemHandle(&be.hs, (void*)(uintptr_t)base));
+    be.offs = (uintptr_t)ctx->scratch[l] - base;
+    memcpy(&ents[l], &be, sizeof be);
+  }
+  *len = need;
+  return HALO_OK;
+}
+
+halo_status halo_ipc_import(halo_ctx* ctx, const void* blobs, size_t len_each) {
+  if (!ctx || !blobs) return HALO_ERR_ARG;
+  const size_t need = sizeof(BlobHdr) + (size_t)ctx->n_local * sizeof(BlobEntry);
+  if (len_each < need) return fail(ctx, HALO_ERR_ARG, "blob length too small");
+  CK(cudaSetDevice(ctx->cfg.device));
+  std::map<std::string, char*> opened;
+  for (int pr = 0; pr < ctx->cfg.nprocs; ++pr) {
+    const char* b = (const char*)blobs + (size_t)pr * len_each;
+    BlobHdr h;
+    memcpy(&h, b, sizeof h);
+    if (h.magic != kBlobMagic || h.version != HALO_ABI_VERSION || h.proc != pr || h.n_local != ctx->n_local ||
+        h.layout != ctx->cfg.layout || h.capacity != ctx->cfg.capacity)
+      return fail(ctx, HALO_ERR_PEER, "inconsistent peer blob (proc " + std::to_string(pr) + ")");
+    if (pr == ctx->cfg.proc) continue;
+    const BlobEntry* ents = reinterpret_cast<const BlobEntry*>(b + sizeof h);
+    for (int l = 0; l < h.n_local; ++l) {
+      BlobEntry be;
+      memcpy(&be, &ents[l], sizeof be);
+      char* bases[2] = {nullptr, nullptr};
+      const cudaIpcMemHandle_t* hs[2] = {&be.hx, &be.hs};
+      for (int k = 0; k < 2; ++k) {
+        std::string key((const char*)hs[k], sizeof(cudaIpcMemHandle_t));
+        auto it = opened.find(key);
+        if (it != opened.end()) { bases[k] = it->second; continue; }
+        void* ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, *hs[k], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          (void)cudaGetLastError();
+          return fail(ctx, HALO_ERR_PEER, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        }
+        opened[key] = (char*)ptr;
+        ctx->opened.push_back(ptr);
+        bases[k] = (char*)ptr;
+      }
+      const int r = h.first_rank + l;
+      ctx->peer_x[r] = reinterpret_cast<float*>(bases[0] + be.offx);
+      ctx->peer_scratch[r] = bases[1] + be.offs;
+    }
+  }
+  for (int r = 0; r < ctx->nranks; ++r)
+    if (!ctx->peer_x[r] || !ctx->peer_scratch[r]) return fail(ctx, HALO_ERR_PEER, "missing peer buffers");
+  ctx->peers_ready = true;
+  ctx->maps_ready = false;
+  return HALO_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------- plan construction
+static void fill_rank_dev(halo_ctx* ctx) {
+  ctx->h_ranks.resize(ctx->n_local);
+  for (int l = 0; l < ctx->n_local; ++l) {
+    RankDev& rd = ctx->h_ranks[l];
+    rd.x = ctx->x[l];
+    rd.f = ctx->f[l];
+    rd.hdr = reinterpret_cast<ScratchHdr*>(ctx->scratch[l]);
+    rd.maps = ctx->maps_of_local(l);
+    rd.fbuf = ctx->fbuf_of(ctx->first_rank + l);
+    rd.n_home = ctx->n_home[l];
+    rd.n_total = ctx->n_total[l];
+    rd.rank = ctx->first_rank + l;
+  }
+}
+
+static void fill_pulse_dev(halo_ctx* ctx, int l, int p) {
+  PulseDev& pd = ctx->h_pulses[l * ctx->P + p];
+  memset(&pd, 0, sizeof pd);
+  const int r = ctx->first_rank + l;
+  const int d = ctx->pdim[p];
+  const int lower = ctx->neighbour(r, d, -1);  // coordinates go to the lower neighbour (R1)
+  const int upper = ctx->neighbour(r, d, +1);
+  const int W = ctx->W;
+  const int i = l * ctx->P + p;
+  pd.map = ctx->maps_of_local(l) + (size_t)p * ctx->map_stride;
+  pd.x_dst = ctx->peer_x[lower] + (size_t)ctx->remote_off[i] * W;
+  pd.flag_x_dst = &ctx->hdr_of(lower)->flag_x[p];
+  pd.fbuf_dst = ctx->fbuf_of(upper) + (size_t)p * ctx->fbuf_stride;
+  pd.flag_f_dst = &ctx->hdr_of(upper)->flag_f[p];
+  pd.fbuf_own = ctx->fbuf_of(r) + (size_t)p * ctx->fbuf_stride;
+  pd.has_shift = ctx->cell(r, d) == 0;  // the wrapping sender adds +L_d (R1, R25)
+  pd.shift[0] = pd.shift[1] = pd.shift[2] = 0.0f;
+  if (pd.has_shift) pd.shift[d] = ctx->cfg.box[d];
+  pd.dim = d;
+  pd.send_size = ctx->send_size[i];
+  pd.n_indep = ctx->n_indep[i];
+  pd.atom_offset = ctx->atom_offset[i];
+  pd.recv_size = ctx->recv_size[i];
+  pd.dep_x = ctx->dep[i];
+  uint32_t fdep = 0, chain = 0;
+  for (int q = p + 1; q < ctx->P; ++q) {
+    if (ctx->dep[l * ctx->P + q] & (1u << p)) fdep |= 1u << q;
+    if (ctx->send_size[l * ctx->P + q] > 0) chain |= 1u << q;
+  }
+  pd.fdep = fdep;
+  pd.chain = chain;
+}
+
+static void add_items(std::vector<Item>& v, int l, int p, uint8_t kind, int b, int e, int rows) {
+  for (int s = b; s < e; s += rows) {
+    Item it;
+    it.lrank = (uint16_t)l;
+    it.pulse = (uint8_t)p;
+    it.kind = kind;
+    it.begin = (uint32_t)s;
+    it.end = (uint32_t)std::min(e, s + rows);
+    v.push_back(it);
+  }
+}
+
+// x items: independent chunks of every pulse first, then dependent chunks in
+// pulse order (deadlock-free static schedule).
+static void build_x_items(halo_ctx* ctx, int p_lo, int p_hi) {
+  auto& v = ctx->h_items_x;
+  v.clear();
+  const int R = ctx->item_rows;
+  for (int p = p_lo; p < p_hi; ++p)
+    for (int l = 0; l < ctx->n_local; ++l) {
+      const int i = l * ctx->P + p;
+      add_items(v, l, p, kItemXIndep, 0, ctx->n_indep[i], R);
+    }
+  for (int p = p_lo; p < p_hi; ++p)
+    for (int l = 0; l < ctx->n_local; ++l) {
+      const int i = l * ctx->P + p;
+      add_items(v, l, p, kItemXDep, ctx->n_indep[i], ctx->send_size[i], R);
+    }
+  for (int l = 0; l < ctx->n_local; ++l)
+    for (int p = 0; p < ctx->P; ++p) ctx->h_pulses[l * ctx->P + p].n_items_x = 0;
+  for (const Item& it : v) ctx->h_pulses[it.lrank * ctx->P + it.pulse].n_items_x++;
+}
+
+// f items: level by level from the last pulse down: push(p) then unpack(p).
+static void build_f_items(halo_ctx* ctx) {
+  auto& v = ctx->h_items_f;
+  v.clear();
+  const int R = ctx->item_rows;
+  for (int p = ctx->P - 1; p >= 0; --p) {
+    for (int l = 0; l < ctx->n_local; ++l) add_items(v, l, p, kItemPush, 0, ctx->recv_size[l * ctx->P + p], R);
+    for (int l = 0; l < ctx->n_local; ++l) add_items(v, l, p, kItemUnpack, 0, ctx->send_size[l * ctx->P + p], R);
+  }
+  for (int l = 0; l < ctx->n_local; ++l)
+    for (int p = 0; p < ctx->P; ++p) {
+      PulseDev& pd = ctx->h_pulses[l * ctx->P + p];
+      pd.n_items_push = pd.n_items_unpack = 0;
+    }
+  for (const Item& it : v) {
+    PulseDev& pd = ctx->h_pulses[it.lrank * ctx->P + it.pulse];
+    if (it.kind == kItemPush) pd.n_items_push++; else pd.n_items_unpack++;
+  }
+}
+
+static halo_status upload_plan(halo_ctx* ctx) {
+  const size_t a = 256;
+  const size_t nr = align_up(sizeof(RankDev) * ctx->n_local, a);
+  const size_t np = align_up(sizeof(PulseDev) * std::max(1, ctx->n_local * ctx->P), a);
+  const size_t nx = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_x.size()), a);
+  const size_t nf = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_f.size()), a);
+  const size_t need = nr + np + nx + nf;
+  if (need > ctx->plan_bytes) {
+    if (ctx->plan) CK(cudaFree(ctx->plan));
+    ctx->plan = nullptr;
+    CK(cudaMalloc(&ctx->plan, need));
+    ctx->plan_bytes = need;
+  }
+  ctx->d_ranks = reinterpret_cast<RankDev*>(ctx->plan);
+  ctx->d_pulses = reinterpret_cast<PulseDev*>(ctx->plan + nr);
+  ctx->d_items_x = reinterpret_cast<Item*>(ctx->plan + nr + np);
+  ctx->d_items_f = reinterpret_cast<Item*>(ctx->plan + nr + np + nx);
+  CK(cudaMemcpy(ctx->d_ranks, ctx->h_ranks.data(), sizeof(RankDev) * ctx->n_local, cudaMemcpyHostToDevice));
+  if (ctx->P)
+    CK(cudaMemcpy(ctx->d_pulses, ctx->h_pulses.data(), sizeof(PulseDev) * ctx->n_local * ctx->P,
+                  cudaMemcpyHostToDevice));
+  if (!ctx->h_items_x.empty())
+    CK(cudaMemcpy(ctx->d_items_x, ctx->h_items_x.data(), sizeof(Item) * ctx->h_items_x.size(), cudaMemcpyHostToDevice));
+  if (!ctx->h_items_f.empty())
+    CK(cudaMemcpy(ctx->d_items_f, ctx->h_items_f.data(), sizeof(Item) * ctx->h_items_f.size(), cudaMemcpyHostToDevice));
+  ctx->n_items_x = (int)ctx->h_items_x.size();
+  ctx->n_items_f = (int)ctx->h_items_f.size();
+  return HALO_OK;
+}
+
+static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p_lo, int p_hi) {
+  ExParams P{};
+  P.ranks = ctx->d_ranks;
+  P.pulses = ctx->d_pulses;
+  P.items = items;
+  P.n_items = n_items;
+  P.n_local = ctx->n_local;
+  P.P = ctx->P;
+  P.p_lo = p_lo;
+  P.p_hi = p_hi;
+  P.ctrl = ctx->ctrl;
+  P.err_host = ctx->err_dev;
+  P.timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);
+  P.flags = ctx->cfg.flags;
+  P.fshift = nullptr;
+  P.accumulate = 1;
+  return P;
+}
+
+static int grid_for(int n_items, int n_local, int max_blocks) {
+  int g = std::min(n_items, max_blocks);
+  return std::max(std::max(g, n_local), 1);
+}
+
+// Pull the set_maps results of every local rank back to the host.
+static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st) {
+  const int L = ctx->n_local, P = ctx->P;
+  std::vector<int32_t> buf(kMaxLocal * kMaxP);
+  auto pull = [&](void* dev, std::vector<int>& dst) -> halo_status {
+    cudaError_t e = cudaMemcpyAsync(buf.data(), dev, sizeof(int32_t) * kMaxLocal * kMaxP, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "pull_ctrl");
+    for (int l = 0; l < L; ++l)
+      for (int p = 0; p < P; ++p) dst[l * P + p] = buf[l * kMaxP + p];
+    return HALO_OK;
+  };
+  halo_status s;
+  if ((s = pull(ctx->ctrl->send_size, ctx->send_size)) != HALO_OK) return s;
+  if ((s = pull(ctx->ctrl->recv_size, ctx->recv_size)) != HALO_OK) return s;
+  if ((s = pull(ctx->ctrl->atom_offset, ctx->atom_offset)) != HALO_OK) return s;
+  if ((s = pull(ctx->ctrl->remote_off, ctx->remote_off)) != HALO_OK) return s;
+  if ((s = pull(ctx->ctrl->n_indep, ctx->n_indep)) != HALO_OK) return s;
+  std::vector<int> depi(L * P);
+  if ((s = pull(ctx->ctrl->dep, depi)) != HALO_OK) return s;
+  for (int i = 0; i < L * P; ++i) ctx->dep[i] = (unsigned)depi[i];
+  int32_t nt[kMaxLocal];
+  CK(cudaMemcpyAsync(nt, ctx->ctrl->n_total, sizeof nt, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int l = 0; l < L; ++l) ctx->n_total[l] = nt[l];
+  return HALO_OK;
+}
+
+// Shared driver of halo_set_maps / halo_set_maps_explicit.
+static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* send_sizes, const int* const* maps,
+                                 cudaStream_t st) {
+  if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "register buffers and import peers first");
+  CK(cudaSetDevice(ctx->cfg.device));
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  const int L = ctx->n_local, P = ctx->P, W = ctx->W;
+  ctx->maps_ready = false;
+  ctx->x_done = false;
+  ctx->epoch++;
+  ctx->n_home.assign(n_home, n_home + L);
+  ctx->n_total = ctx->n_home;
+  ctx->send_size.assign(L * P, 0);
+  ctx->recv_size.assign(L * P, 0);
+  ctx->atom_offset.assign(L * P, 0);
+  ctx->remote_off.assign(L * P, 0);
+  ctx->n_indep.assign(L * P, 0);
+  ctx->dep.assign(L * P, 0u);
+  ctx->h_pulses.assign(std::max(1, L * P), PulseDev{});
+  int local_err = 0;
+  for (int l = 0; l < L; ++l)
+    if (n_home[l] < 0 || n_home[l] > ctx->cfg.capacity) local_err |= kErrCapacity;
+
+  // reset device-side set_maps state
+  {
+    int32_t zero[kMaxLocal * kMaxP] = {0};
+    int32_t nt[kMaxLocal] = {0}, errs[kMaxLocal] = {0};
+    for (int l = 0; l < L; ++l) {
+      nt[l] = std::min(std::max(n_home[l], 0), ctx->cfg.capacity);
+      errs[l] = local_err;
+    }
+    CK(cudaMemcpyAsync(ctx->ctrl->send_size, zero, sizeof zero, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->ctrl->dep, zero, sizeof zero, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->ctrl->n_indep, zero, sizeof zero, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->ctrl->n_total, nt, sizeof nt, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->ctrl->err, errs, sizeof errs, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    for (int l = 0; l < L; ++l) ctx->n_total[l] = nt[l];
+  }
+  ctx->n_home.assign(ctx->n_total.begin(), ctx->n_total.end());
+  fill_rank_dev(ctx);
+  // ranks/pulse tables are needed by the select/depmask kernels already
+  ctx->h_items_x.clear();
+  ctx->h_items_f.clear();
+  if ((s = upload_plan(ctx)) != HALO_OK) return s;
+
+  const uint64_t timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);
+  std::vector<int> dim_start(L, 0);
+  for (int p = 0; p < P; ++p) {
+    const int d = ctx->pdim[p], k = ctx->pk[p];
+    if (k == 0)
+      for (int l = 0; l < L; ++l) dim_start[l] = ctx->n_total[l];
+    if (maps) {
+      // explicit maps (test entry): validate on the host and upload
+      int errs_now = 0;
+      for (int l = 0; l < L; ++l) {
+        const int i = l * P + p;
+        const int n = send_sizes[i];
+        const int* m = maps[i];
+        bool ok = n >= 0 && n <= ctx->cfg.capacity && (n == 0 || m != nullptr);
+        for (int j = 0; ok && j < n; ++j) ok = m[j] >= 0 && m[j] < ctx->n_total[l] && (j == 0 || m[j] > m[j - 1]);
+        if (!ok) { errs_now |= kErrMap; continue; }
+        if (n) CK(cudaMemcpyAsync(ctx->maps_of_local(l) + (size_t)p * ctx->map_stride, m, sizeof(int) * n,
+                                  cudaMemcpyHostToDevice, st));
+        int32_t nn = n;
+        CK(cudaMemcpyAsync(&ctx->ctrl->send_size[l][p], &nn, sizeof nn, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      if (errs_now) {
+        for (int l = 0; l < L; ++l) {
+          int32_t e = errs_now;
+          CK(cudaMemcpyAsync(&ctx->ctrl->err[l], &e, sizeof e, cudaMemcpyHostToDevice, st));
+          CK(cudaStreamSynchronize(st));
+        }
+      }
+    } else {
+      // GPU map builder: candidate ranges and planes (R2, R3)
+      char* sm = ctx->d_small;
+      std::vector<int32_t> cand(2 * L);
+      std::vector<double> blo(L), hlo(3 * L), hhi(3 * L);
+      for (int l = 0; l < L; ++l) {
+        const int r = ctx->first_rank + l;
+        if (k == 0) {
+          cand[2 * l] = 0;
+          cand[2 * l + 1] = dim_start[l];
+        } else {
+          const int q = l * P + (p - 1);
+          cand[2 * l] = ctx->atom_offset[q];
+          cand[2 * l + 1] = ctx->atom_offset[q] + ctx->recv_size[q];
+        }
+        blo[l] = ctx->plane(d, ctx->cell(r, d));
+        for (int dd = 0; dd < 3; ++dd) {
+          hlo[3 * l + dd] = ctx->plane(dd, ctx->cell(r, dd));
+          hhi[3 * l + dd] = ctx->plane(dd, ctx->cell(r, dd) + 1);
+        }
+      }
+      CK(cudaMemcpyAsync(sm, cand.data(), sizeof(int32_t) * 2 * L, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(sm + 2048, blo.data(), sizeof(double) * L, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(sm + 4096, hlo.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(sm + 8192, hhi.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
+      SelParams S{};
+      S.ranks = ctx->d_ranks;
+      S.ctrl = ctx->ctrl;
+      S.p = p;
+      S.dim = d;
+      S.rc = (double)ctx->cfg.cutoff;
+      S.cand = reinterpret_cast<const int32_t*>(sm);
+      S.b_lo = reinterpret_cast<const double*>(sm + 2048);
+      const bool check = (p == 0) && !(ctx->cfg.flags & HALO_F_NO_HOME_CHECK);
+      S.home_lo = check ? reinterpret_cast<const double*>(sm + 4096) : nullptr;
+      S.home_hi = check ? reinterpret_cast<const double*>(sm + 8192) : nullptr;
+      S.decomposed_mask = (ctx->cfg.grid[0] > 1) | ((ctx->cfg.grid[1] > 1) << 1) | ((ctx->cfg.grid[2] > 1) << 2);
+      S.map_stride = (int)ctx->map_stride;
+      S.layout = W;
+      CK(launch_select(S, L, st));
+    }
+    // handshake with the neighbours (device flags)
+    HsParams H{};
+    H.ctrl = ctx->ctrl;
+    H.p = p;
+    H.epoch = ctx->epoch;
+    H.capacity = ctx->cfg.capacity;
+    H.n_local = L;
+    H.err_host = ctx->err_dev;
+    H.timeout_ns = timeout_ns;
+    for (int l = 0; l < L; ++l) {
+      const int r = ctx->first_rank + l;
+      H.own[l] = ctx->hdr_of(r);
+      H.size_dst[l] = &ctx->hdr_of(ctx->neighbour(r, d, -1))->meta_size[p];
+      H.off_dst[l] = &ctx->hdr_of(ctx->neighbour(r, d, +1))->meta_off[p];
+    }
+    CK(launch_handshake(H, st));
+    CK(launch_depmask(ctx->d_ranks, ctx->ctrl, p, (int)ctx->map_stride, L, st));
+    if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
+    if ((s = check_err_word(ctx)) != HALO_OK) return s;
+    // exchange the coordinates of this pulse now: pulse p+1 forwards them
+    for (int l = 0; l < L; ++l)
+      for (int q = 0; q <= p; ++q) fill_pulse_dev(ctx, l, q);
+    fill_rank_dev(ctx);
+    build_x_items(ctx, p, p + 1);
+    if ((s = upload_plan(ctx)) != HALO_OK) return s;
+    ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
+    CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
+    CK(cudaStreamSynchronize(st));
+    if ((s = check_err_word(ctx)) != HALO_OK) return s;
+  }
+  // error agreement over all ranks
+  StatusParams SP{};
+  SP.ctrl = ctx->ctrl;
+  SP.epoch = ctx->epoch;
+  SP.nranks = ctx->nranks;
+  SP.n_local = L;
+  SP.first_rank = ctx->first_rank;
+  for (int l = 0; l < L; ++l) SP.own[l] = ctx->hdr_of(ctx->first_rank + l);
+  for (int r = 0; r < ctx->nranks; ++r) SP.all[r] = ctx->hdr_of(r);
+  SP.err_host = ctx->err_dev;
+  SP.timeout_ns = timeout_ns;
+  CK(launch_status(SP, st));
+  int32_t agreed[kMaxLocal];
+  CK(cudaMemcpyAsync(agreed, ctx->ctrl->agreed_err, sizeof agreed, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((s = check_err_word(ctx)) != HALO_OK) return s;
+  int any = 0;
+  for (int l = 0; l < L; ++l) any |= agreed[l];
+  if (any & kErrCapacity) return fail(ctx, HALO_ERR_CAPACITY, "n_home + received rows exceed capacity on some rank");
+  if (any & kErrGeometry) return fail(ctx, HALO_ERR_GEOMETRY, "a home atom lies outside its rank's cell");
+  if (any & kErrMap) return fail(ctx, HALO_ERR_ARG, "invalid explicit map on some rank");
+  // final plan: all pulses
+  for (int l = 0; l < L; ++l)
+    for (int p = 0; p < P; ++p) fill_pulse_dev(ctx, l, p);
+  fill_rank_dev(ctx);
+  build_x_items(ctx, 0, P);
+  build_f_items(ctx);
+  if ((s = upload_plan(ctx)) != HALO_OK) return s;
+  ctx->maps_ready = true;
+  ctx->x_done = true;  // set_maps exchanged every pulse's coordinates
+  return HALO_OK;
+}
+
+extern "C" {
+
+halo_status halo_set_maps(halo_ctx* ctx, const int* n_home, void* stream) {
+  if (!ctx || !n_home) return HALO_ERR_ARG;
+  return set_maps_impl(ctx, n_home, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+halo_status halo_set_maps_explicit(halo_ctx* ctx, const int* n_home, const int* send_sizes, const int* const* maps,
+                                   void* stream) {
+  if (!ctx || !n_home || (ctx->P > 0 && (!send_sizes || !maps))) return HALO_ERR_ARG;
+  return set_maps_impl(ctx, n_home, send_sizes, maps, (cudaStream_t)stream);
+}
+
+halo_status halo_get_layout(const halo_ctx* ctx, int local, int* n_home, int* n_total, int* npulse, int* recv_off,
+                            int* recv_size, int* send_size, int* remote_off, unsigned* dep_mask) {
+  if (!ctx || local < 0 || local >= ctx->n_local) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return HALO_ERR_STATE;
+  if (n_home) *n_home = ctx->n_home[local];
+  if (n_total) *n_total = ctx->n_total[local];
+  if (npulse) *npulse = ctx->P;
+  for (int p = 0; p < ctx->P; ++p) {
+    const int i = local * ctx->P + p;
+    if (recv_off) recv_off[p] = ctx->atom_offset[i];
+    if (recv_size) recv_size[p] = ctx->recv_size[i];
+    if (send_size) send_size[p] = ctx->send_size[i];
+    if (remote_off) remote_off[p] = ctx->remote_off[i];
+    if (dep_mask) dep_mask[p] = ctx->dep[i];
+  }
+  return HALO_OK;
+}
+
+halo_status halo_get_map(const halo_ctx* ctx, int local, int pulse, int* host_out, int cap) {
+  if (!ctx || local < 0 || local >= ctx->n_local || pulse < 0 || pulse >= ctx->P || (!host_out && cap > 0))
+    return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return HALO_ERR_STATE;
+  const int n = ctx->send_size[local * ctx->P + pulse];
+  if (cap < n) return HALO_ERR_ARG;
+  if (n == 0) return HALO_OK;
+  cudaError_t e = cudaMemcpy(host_out, ctx->maps_of_local(local) + (size_t)pulse * ctx->map_stride, sizeof(int) * n,
+                             cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return HALO_ERR_CUDA;
+  }
+  return HALO_OK;
+}
+
+halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "exchange_x before set_maps");
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  ctx->x_done = true;
+  if (ctx->P == 0) return HALO_OK;
+  ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, 0, ctx->P);
+  CK(launch_exchange_x(X, ctx->W, grid_for(ctx->n_items_x, ctx->n_local, ctx->max_x), (cudaStream_t)stream));
+  return HALO_OK;
+}
+
+halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->maps_ready || !ctx->x_done) return fail(ctx, HALO_ERR_STATE, "exchange_f before set_maps/exchange_x");
+  if (!accumulate && ctx->P != 1) return fail(ctx, HALO_ERR_UNSUPPORTED, "accumulate=0 needs exactly one pulse (R14)");
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  if (ctx->P == 0) return HALO_OK;
+  ExParams F = make_params(ctx, ctx->d_items_f, ctx->n_items_f, 0, ctx->P);
+  F.fshift = fshift;
+  F.accumulate = accumulate ? 1 : 0;
+  CK(launch_exchange_f(F, ctx->W, grid_for(ctx->n_items_f, ctx->n_local, ctx->max_f), (cudaStream_t)stream));
+  return HALO_OK;
+}
+
+halo_status halo_step_host(halo_ctx* ctx, const float* const* x_home, const float* const* f_all,
+                           float* const* x_halo_out, float* const* f_home_out, double* fshift_host, void* stream) {
+  if (!ctx || !x_home || !f_all) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "step before set_maps");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int W = ctx->W;
+  for (int l = 0; l < ctx->n_local; ++l) {
+    CK(cudaMemcpyAsync(ctx->x[l], x_home[l], sizeof(float) * W * ctx->n_home[l], cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->f[l], f_all[l], sizeof(float) * W * ctx->n_total[l], cudaMemcpyHostToDevice, st));
+  }
+  halo_status s = halo_exchange_x(ctx, stream);
+  if (s != HALO_OK) return s;
+  // halo x leaves before exchange_f: a neighbour's next exchange_x may only
+  // overwrite these rows after our exchange_f has pushed (R17)
+  if (x_halo_out)
+    for (int l = 0; l < ctx->n_local; ++l)
+      if (x_halo_out[l] && ctx->n_total[l] > ctx->n_home[l])
+        CK(cudaMemcpyAsync(x_halo_out[l], ctx->x[l] + (size_t)W * ctx->n_home[l],
+                           sizeof(float) * W * (ctx->n_total[l] - ctx->n_home[l]), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemsetAsync(ctx->d_fshift_tmp, 0, sizeof(double) * 9 * ctx->n_local, st));
+  s = halo_exchange_f(ctx, ctx->d_fshift_tmp, 1, stream);
+  if (s != HALO_OK) return s;
+  if (f_home_out)
+    for (int l = 0; l < ctx->n_local; ++l)
+      if (f_home_out[l])
+        CK(cudaMemcpyAsync(f_home_out[l], ctx->f[l], sizeof(float) * W * ctx->n_home[l], cudaMemcpyDeviceToHost, st));
+  if (fshift_host)
+    CK(cudaMemcpyAsync(fshift_host, ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return check_err_word(ctx);
+}
+
+halo_status halo_pack_x_pulse(halo_ctx* ctx, int local, int pulse, float* sendbuf, void* stream) {
+  if (!ctx || local < 0 || local >= ctx->n_local || pulse < 0 || pulse >= ctx->P || !sendbuf) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "pack before set_maps");
+  const PulseDev& pd = ctx->h_pulses[local * ctx->P + pulse];
+  CK(launch_pack_x(ctx->W, pd.map, pd.send_size, ctx->x[local], sendbuf, pd.has_shift, pd.shift, (cudaStream_t)stream));
+  return HALO_OK;
+}
+
+halo_status halo_unpack_f_pulse(halo_ctx* ctx, int local, int pulse, const float* recvbuf, double* fshift,
+                                int accumulate, void* stream) {
+  if (!ctx || local < 0 || local >= ctx->n_local || pulse < 0 || pulse >= ctx->P || !recvbuf) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "unpack before set_maps");
+  const PulseDev& pd = ctx->h_pulses[local * ctx->P + pulse];
+  double* fs = (fshift && pd.has_shift) ? fshift + 9 * local + 3 * pd.dim : nullptr;
+  CK(launch_unpack_f(ctx->W, pd.map, pd.send_size, recvbuf, ctx->f[local], accumulate, fs, (cudaStream_t)stream));
+  return HALO_OK;
+}
+
+halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
+  if (!ctx) return HALO_ERR_ARG;
+  uint64_t v[2];
+  CK(cudaMemcpy(v, &ctx->ctrl->span_x, sizeof v, cudaMemcpyDeviceToHost));
+  if (x_ns) *x_ns = v[0];
+  if (f_ns) *f_ns = v[1];
+  return HALO_OK;
+}
+
+halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, double* one_way_us) {
+  if (!ctx || peer_rank < 0 || peer_rank >= ctx->nranks || iters <= 0) return HALO_ERR_ARG;
+  if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
+  const int me = ctx->first_rank;
+  if (peer_rank >= ctx->first_rank && peer_rank < ctx->first_rank + ctx->n_local && peer_rank != me)
+    return fail(ctx, HALO_ERR_UNSUPPORTED, "ping-pong peer must live in another process");
+  CK(cudaSetDevice(ctx->cfg.device));
+  // the initiator is the process that hosts the lower of the two ranks
+  const bool initiator = me < peer_rank;
+  if (ctx->d_rtt == nullptr || iters > 1 << 16) {
+    if (ctx->d_rtt) CK(cudaFree(ctx->d_rtt));
+    CK(cudaMalloc(&ctx->d_rtt, sizeof(uint64_t) * std::max(iters, 1 << 16)));
+  }
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  uint64_t* own = &ctx->hdr_of(me)->ping;
+  uint64_t* peer = &ctx->hdr_of(peer_rank)->ping;
+  CK(launch_pingpong(own, peer, iters, ctx->ping_base, initiator ? 1 : 0, ctx->d_rtt,
+                     (uint64_t)(ctx->cfg.timeout_s * 1e9), ctx->err_dev, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaStreamDestroy(st));
+  ctx->ping_base += (uint64_t)iters;
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  if (one_way_us) {
+    *one_way_us = 0.0;
+    if (initiator) {
+      std::vector<uint64_t> v(iters);
+      CK(cudaMemcpy(v.data(), ctx->d_rtt, sizeof(uint64_t) * iters, cudaMemcpyDeviceToHost));
+      std::sort(v.begin(), v.end());
+      *one_way_us = (double)v[iters / 2] / 2.0 / 1000.0;
+    }
+  }
+  return HALO_OK;
+}
+
+halo_status halo_sync(halo_ctx* ctx) {
+  if (!ctx) return HALO_ERR_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  return check_err_word(ctx);
+}
+
+halo_status halo_destroy(halo_ctx* ctx) {
+  if (!ctx) return HALO_OK;
+  (void)cudaSetDevice(ctx->cfg.device);
+  (void)cudaDeviceSynchronize();
+  for (void* p : ctx->opened) (void)cudaIpcCloseMemHandle(p);
+  if (ctx->plan) (void)cudaFree(ctx->plan);
+  if (ctx->ctrl) (void)cudaFree(ctx->ctrl);
+  if (ctx->d_fshift_tmp) (void)cudaFree(ctx->d_fshift_tmp);
+  if (ctx->d_small) (void)cudaFree(ctx->d_small);
+  if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
+  if (ctx->err_host) (void)cudaFreeHost(ctx->err_host);
+  (void)cudaGetLastError();
+  delete ctx;
+  return HALO_OK;
+}
+
+}  // extern "C"

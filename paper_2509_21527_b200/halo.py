@@ -1,0 +1,176 @@
+"""Thin Python binding of the libhalo C ABI (include/halo.h).
+
+Same names as the C calls; argument marshalling only — every step of the halo
+exchange runs in libhalo's CUDA kernels.  Pointers are plain integers (e.g.
+``tensor.data_ptr()``); streams are ``torch.cuda.Stream.cuda_stream`` ints.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import c_double, c_int, c_size_t, c_uint, c_uint64, c_void_p
+
+import numpy as np
+
+from . import _lib
+from ._lib import halo_config, STATUS_NAMES
+
+
+class HaloError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Halo:
+    """One context per process (hosts nranks/nprocs DD ranks)."""
+
+    def __init__(self, grid, box, cutoff, pulses, layout=3, capacity=1 << 16, device=0, flags=0,
+                 nprocs=1, proc=0, timeout_s=10.0):
+        self.lib = _lib.load()
+        cfg = halo_config()
+        cfg.grid[:] = [int(v) for v in grid]
+        cfg.box[:] = [float(v) for v in box]
+        cfg.cutoff = float(cutoff)
+        cfg.pulses[:] = [int(v) for v in pulses]
+        cfg.layout = int(layout)
+        cfg.capacity = int(capacity)
+        cfg.device = int(device)
+        cfg.flags = int(flags)
+        cfg.nprocs = int(nprocs)
+        cfg.proc = int(proc)
+        cfg.timeout_s = float(timeout_s)
+        self.cfg = cfg
+        self.layout = int(layout)
+        h = c_void_p()
+        st = self.lib.halo_init(ctypes.byref(cfg), ctypes.byref(h))
+        if st != 0:
+            raise HaloError(st, self.lib.halo_strerror(st).decode())
+        self.h = h
+
+    # ---------------------------------------------------------------- helpers
+    def _ck(self, st):
+        if st != 0:
+            msg = self.lib.halo_last_error(self.h).decode() if self.h else ""
+            raise HaloError(st, msg or self.lib.halo_strerror(st).decode())
+
+    def local_ranks(self):
+        a, b = c_int(), c_int()
+        self._ck(self.lib.halo_local_ranks(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def pulse_order(self):
+        n = c_int()
+        dims = (c_int * _lib.HALO_MAX_PULSES)()
+        self._ck(self.lib.halo_pulse_order(self.h, ctypes.byref(n), dims))
+        return [dims[i] for i in range(n.value)]
+
+    def scratch_bytes(self) -> int:
+        b = c_size_t()
+        self._ck(self.lib.halo_scratch_bytes(self.h, ctypes.byref(b)))
+        return b.value
+
+    def register_buffers(self, local, x_ptr, f_ptr, scratch_ptr):
+        self._ck(self.lib.halo_register_buffers(self.h, int(local), c_void_p(x_ptr), c_void_p(f_ptr),
+                                                c_void_p(scratch_ptr)))
+
+    def ipc_export(self) -> bytes:
+        n = c_size_t()
+        self._ck(self.lib.halo_ipc_export(self.h, None, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        self._ck(self.lib.halo_ipc_export(self.h, buf, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def ipc_import(self, blobs):
+        ln = len(blobs[0])
+        assert all(len(b) == ln for b in blobs)
+        buf = ctypes.create_string_buffer(b"".join(blobs), ln * len(blobs))
+        self._ck(self.lib.halo_ipc_import(self.h, buf, c_size_t(ln)))
+
+    def set_maps(self, n_home, stream=0):
+        arr = (c_int * len(n_home))(*[int(v) for v in n_home])
+        self._ck(self.lib.halo_set_maps(self.h, arr, c_void_p(stream)))
+
+    def set_maps_explicit(self, n_home, maps, stream=0):
+        """maps[local][pulse] = int array of ascending local row indices."""
+        nl = len(n_home)
+        P = len(self.pulse_order())
+        arr = (c_int * nl)(*[int(v) for v in n_home])
+        sizes = (c_int * max(1, nl * P))()
+        ptrs = (ctypes.POINTER(c_int) * max(1, nl * P))()
+        keep = []
+        for l in range(nl):
+            for p in range(P):
+                m = np.ascontiguousarray(maps[l][p], dtype=np.int32)
+                keep.append(m)
+                sizes[l * P + p] = m.size
+                ptrs[l * P + p] = m.ctypes.data_as(ctypes.POINTER(c_int))
+        self._ck(self.lib.halo_set_maps_explicit(self.h, arr, sizes, ptrs, c_void_p(stream)))
+
+    def get_layout(self, local):
+        P = _lib.HALO_MAX_PULSES
+        nh, nt, npl = c_int(), c_int(), c_int()
+        ro, rs, ss, rm = (c_int * P)(), (c_int * P)(), (c_int * P)(), (c_int * P)()
+        dm = (c_uint * P)()
+        self._ck(self.lib.halo_get_layout(self.h, int(local), ctypes.byref(nh), ctypes.byref(nt), ctypes.byref(npl),
+                                          ro, rs, ss, rm, dm))
+        n = npl.value
+        return dict(n_home=nh.value, n_total=nt.value, npulse=n, recv_off=list(ro[:n]), recv_size=list(rs[:n]),
+                    send_size=list(ss[:n]), remote_off=list(rm[:n]), dep_mask=list(dm[:n]))
+
+    def get_map(self, local, pulse) -> np.ndarray:
+        lay = self.get_layout(local)
+        n = lay["send_size"][pulse]
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        self._ck(self.lib.halo_get_map(self.h, int(local), int(pulse),
+                                       out.ctypes.data_as(ctypes.POINTER(c_int)), c_int(n)))
+        return out[:n]
+
+    def exchange_x(self, stream=0):
+        self._ck(self.lib.halo_exchange_x(self.h, c_void_p(stream)))
+
+    def exchange_f(self, fshift_ptr=0, accumulate=True, stream=0):
+        self._ck(self.lib.halo_exchange_f(self.h, c_void_p(fshift_ptr or None), int(bool(accumulate)),
+                                          c_void_p(stream)))
+
+    def step_host(self, x_home_ptrs, f_all_ptrs, x_halo_out_ptrs=None, f_home_out_ptrs=None, fshift_ptr=0,
+                  stream=0):
+        n = len(x_home_ptrs)
+
+        def arr(ptrs):
+            if ptrs is None:
+                return None
+            return (c_void_p * n)(*[c_void_p(p) for p in ptrs])
+
+        self._ck(self.lib.halo_step_host(self.h, arr(x_home_ptrs), arr(f_all_ptrs), arr(x_halo_out_ptrs),
+                                         arr(f_home_out_ptrs), c_void_p(fshift_ptr or None), c_void_p(stream)))
+
+    def pack_x_pulse(self, local, pulse, sendbuf_ptr, stream=0):
+        self._ck(self.lib.halo_pack_x_pulse(self.h, int(local), int(pulse), c_void_p(sendbuf_ptr), c_void_p(stream)))
+
+    def unpack_f_pulse(self, local, pulse, recvbuf_ptr, fshift_ptr=0, accumulate=True, stream=0):
+        self._ck(self.lib.halo_unpack_f_pulse(self.h, int(local), int(pulse), c_void_p(recvbuf_ptr),
+                                              c_void_p(fshift_ptr or None), int(bool(accumulate)), c_void_p(stream)))
+
+    def get_timers(self):
+        a, b = c_uint64(), c_uint64()
+        self._ck(self.lib.halo_get_timers(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def floor_pingpong(self, peer_rank, iters=10000) -> float:
+        v = c_double()
+        self._ck(self.lib.halo_floor_pingpong(self.h, int(peer_rank), int(iters), ctypes.byref(v)))
+        return v.value
+
+    def sync(self):
+        self._ck(self.lib.halo_sync(self.h))
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            self.lib.halo_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass

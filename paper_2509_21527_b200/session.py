@@ -1,0 +1,99 @@
+"""PyTorch plumbing around the C ABI: device memory, streams and the process
+group that swaps CUDA-IPC blobs (north_star: "PyTorch is used only for device
+memory, streams and the process group").  No halo arithmetic here.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .halo import Halo
+
+
+def assign_home(X: np.ndarray, L, grid):
+    """Home DD rank of every atom (input preparation at a neighbour-search step,
+    not a hot-path step): c_d = number of interior planes float64(L_d)*k/grid[d]
+    (k = 1..grid[d]-1) that are <= float64(x_d); rank = (cx*np_y + cy)*np_z + cz.
+    Returns a list, per rank, of atom ids in ascending order."""
+    X = np.asarray(X, dtype=np.float32)
+    c = np.zeros((X.shape[0], 3), dtype=np.int64)
+    for d in range(3):
+        Ld = float(np.float32(L[d]))
+        inner = np.array([Ld * k / grid[d] for k in range(1, grid[d])], dtype=np.float64)
+        c[:, d] = np.searchsorted(inner, X[:, d].astype(np.float64), side="right")
+    r = (c[:, 0] * grid[1] + c[:, 1]) * grid[2] + c[:, 2]
+    order = np.argsort(r, kind="stable")
+    counts = np.bincount(r, minlength=grid[0] * grid[1] * grid[2])
+    out, s = [], 0
+    for n in counts:
+        out.append(order[s:s + n])
+        s += n
+    return out
+
+
+class HaloSession:
+    """One per process: allocates (torch) x, f, scratch for every local DD rank,
+    registers them, and imports the peers' IPC blobs over ``torch.distributed``."""
+
+    def __init__(self, grid, box, cutoff, pulses, layout=3, capacity=1 << 16, device=0, flags=0,
+                 nprocs=1, proc=0, timeout_s=10.0, group=None):
+        self.device = torch.device("cuda", device)
+        torch.cuda.set_device(self.device)
+        self.halo = Halo(grid, box, cutoff, pulses, layout=layout, capacity=capacity, device=device, flags=flags,
+                         nprocs=nprocs, proc=proc, timeout_s=timeout_s)
+        self.grid, self.box, self.cutoff, self.pulses = tuple(grid), tuple(box), cutoff, tuple(pulses)
+        self.layout, self.capacity, self.nprocs, self.proc = layout, capacity, nprocs, proc
+        self.first_rank, self.n_local = self.halo.local_ranks()
+        self.npulse = len(self.halo.pulse_order())
+        sb = self.halo.scratch_bytes()
+        self.x = [torch.zeros(capacity, layout, dtype=torch.float32, device=self.device) for _ in range(self.n_local)]
+        self.f = [torch.zeros(capacity, layout, dtype=torch.float32, device=self.device) for _ in range(self.n_local)]
+        self.scratch = [torch.zeros(sb, dtype=torch.uint8, device=self.device) for _ in range(self.n_local)]
+        for l in range(self.n_local):
+            self.halo.register_buffers(l, self.x[l].data_ptr(), self.f[l].data_ptr(), self.scratch[l].data_ptr())
+        if nprocs > 1:
+            import torch.distributed as dist
+            blob = self.halo.ipc_export()
+            blobs = [None] * nprocs
+            dist.all_gather_object(blobs, blob, group=group)
+            self.halo.ipc_import(blobs)
+        self.n_home = [0] * self.n_local
+
+    # ------------------------------------------------------------- inputs
+    def load_home(self, rows_per_local):
+        """rows_per_local[l]: float32 [n_home, layout] (or [n_home, 3] + zero w) host array."""
+        for l, rows in enumerate(rows_per_local):
+            rows = np.asarray(rows, dtype=np.float32)
+            n = rows.shape[0]
+            if n > self.capacity:
+                raise ValueError("n_home exceeds capacity")
+            t = torch.zeros(n, self.layout, dtype=torch.float32)
+            t[:, :rows.shape[1]] = torch.from_numpy(rows)
+            self.x[l][:n].copy_(t.to(self.device))
+            self.n_home[l] = n
+        torch.cuda.synchronize(self.device)
+
+    def set_maps(self, stream=None):
+        self.halo.set_maps(self.n_home, stream=self._s(stream))
+
+    def set_maps_explicit(self, maps, stream=None):
+        self.halo.set_maps_explicit(self.n_home, maps, stream=self._s(stream))
+
+    def layout_of(self, l):
+        return self.halo.get_layout(l)
+
+    def exchange_x(self, stream=None):
+        self.halo.exchange_x(stream=self._s(stream))
+
+    def exchange_f(self, fshift=None, accumulate=True, stream=None):
+        self.halo.exchange_f(fshift.data_ptr() if fshift is not None else 0, accumulate, stream=self._s(stream))
+
+    @staticmethod
+    def _s(stream):
+        if stream is None:
+            return torch.cuda.current_stream().cuda_stream
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    def destroy(self):
+        self.halo.sync()
+        self.halo.destroy()

@@ -1,0 +1,130 @@
+"""GPU-vs-oracle parity harness (test-only).  Runs the CUDA path through the C ABI
+(via the Python binding) and compares with oracle/ element by element.
+
+Tolerances:
+  maps, layout, dep masks, halo x, f (deterministic mode): bit-exact
+  f (HALO_F_ATOMIC_UNPACK): per component |g - o| <= P * 2^-24 * sum|terms|  (R16)
+  fshift (fp64, unordered reduction): |g - o| <= 1e-10 * sum over all rows |F|
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import torch
+
+from oracle import decompose, force_halo
+from synth import forces_int, forces_normal, get_config, water_box
+from synth.water import charges
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load_system(name, seed, layout=3):
+    """(L, rc, grid, pulses, X, W) for a config name or a golden W* example."""
+    if name.startswith("W"):
+        with open(os.path.join(GOLD, name + ".json")) as f:
+            g = json.load(f)
+        X = np.array(g["X"], np.float32)
+        L, rc, grid, pulses = tuple(g["L"]), g["rc"], tuple(g["grid"]), tuple(g["pulses"])
+    else:
+        c = get_config(name)
+        X = water_box(c.n_atoms, c.L, seed)
+        L, rc, grid, pulses = c.L, c.rc, c.grid, c.pulses
+    W = charges(X.shape[0]) if layout == 4 else None
+    return L, rc, grid, pulses, X, W
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.int32)
+
+
+class Case:
+    """Oracle side of one parity case."""
+
+    def __init__(self, name, seed=1, layout=3, force_kind="int"):
+        self.name, self.seed, self.layout = name, seed, layout
+        self.L, self.rc, self.grid, self.pulses, self.X, self.W = load_system(name, seed, layout)
+        self.states = decompose(self.X, self.L, self.rc, self.grid, self.pulses, W=self.W)
+        self.nranks = len(self.states)
+        self.capacity = max(max(s.x.shape[0] for s in self.states), 1) + 64
+        mk = forces_int if force_kind == "int" else forces_normal
+        self.F = [mk(s.x.shape[0], 1000 * seed + 7 * s.rank + 3, width=layout) for s in self.states]
+        self.Fo, self.fshift = force_halo(self.states, [f.copy() for f in self.F])
+        self.fabs_total = float(sum(np.abs(f[:, :3].astype(np.float64)).sum() for f in self.F))
+
+    def absum_gid(self):
+        if not hasattr(self, "_absum"):
+            acc = np.zeros((self.X.shape[0], 3))
+            for s, f in zip(self.states, self.F):
+                np.add.at(acc, s.gid, np.abs(f[:, :3].astype(np.float64)))
+            self._absum = acc
+        return self._absum
+
+    def home_rows(self, r):
+        s = self.states[r]
+        return s.x[: s.n_home]
+
+
+def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit=False, steps=1):
+    """Drive the CUDA path for the local ranks of `sess` and compare with the oracle.
+    Returns a dict of per-check booleans (asserts on the way)."""
+    first, nl = sess.first_rank, sess.n_local
+    sess.load_home([case.home_rows(first + l) for l in range(nl)])
+    if use_explicit:
+        maps = [[case.states[first + l].pulses[p].map for p in range(sess.npulse)] for l in range(nl)]
+        sess.set_maps_explicit(maps)
+    else:
+        sess.set_maps()
+    torch.cuda.synchronize()
+    for l in range(nl):
+        r = first + l
+        st = case.states[r]
+        lay = sess.layout_of(l)
+        assert lay["n_home"] == st.n_home, (r, lay, st.n_home)
+        assert lay["n_total"] == st.x.shape[0], (r, lay["n_total"], st.x.shape[0])
+        for p, pi in enumerate(st.pulses):
+            got = (lay["send_size"][p], lay["recv_size"][p], lay["recv_off"][p], lay["remote_off"][p])
+            exp = (pi.send_size, pi.recv_size, pi.atom_offset, pi.remote_offset)
+            assert got == exp, (r, p, got, exp)
+            assert lay["dep_mask"][p] == sum(1 << q for q in pi.dep), (r, p, lay["dep_mask"][p], pi.dep)
+            np.testing.assert_array_equal(sess.halo.get_map(l, p), pi.map)
+    for step in range(steps):
+        # poison halo rows (sentinel NaN payload): exchange_x must overwrite every one (G3)
+        for l in range(nl):
+            st = case.states[first + l]
+            sess.x[l][st.n_home: st.x.shape[0]] = float("nan")
+        sess.exchange_x()
+        torch.cuda.synchronize()
+        for l in range(nl):
+            st = case.states[first + l]
+            got = sess.x[l][: st.x.shape[0]].cpu().numpy()
+            np.testing.assert_array_equal(bits(got), bits(st.x), err_msg=f"halo x rank {first + l} step {step}")
+        if not check_forces:
+            continue
+        for l in range(nl):
+            r = first + l
+            n = case.F[r].shape[0]
+            sess.f[l][:n] = torch.from_numpy(case.F[r]).to(sess.device)
+        fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=sess.device)
+        sess.exchange_f(fshift=fshift)
+        torch.cuda.synchronize()
+        fs = fshift.cpu().numpy()
+        for l in range(nl):
+            r = first + l
+            n = case.F[r].shape[0]
+            got = sess.f[l][:n].cpu().numpy()
+            exp = case.Fo[r]
+            if not atomic:
+                np.testing.assert_array_equal(bits(got), bits(exp), err_msg=f"f rank {r} step {step}")
+            else:
+                # unordered adds (R16): home rows within P * 2^-24 * sum|terms| of the ordered result
+                st = case.states[r]
+                P = max(1, sess.npulse)
+                bound = 2 * P * 2.0 ** -24 * case.absum_gid()[st.gid[: st.n_home]] * 1.0000001
+                err = np.abs(got[: st.n_home, :3].astype(np.float64) - exp[: st.n_home, :3].astype(np.float64))
+                assert np.all(err <= bound), (r, float(err.max()))
+            tol = 1e-10 * case.fabs_total
+            assert np.all(np.abs(fs[l] - case.fshift[r]) <= tol), (r, fs[l], case.fshift[r])
+    return True

@@ -1,0 +1,255 @@
+"""GPU parity (-m gpu): CUDA path through the C ABI vs the oracle, one process,
+all DD ranks of a config hosted by one GPU (one kernel launch covers them all).
+
+Bar: maps, layout, dependency masks, halo x and forces
+bit-exact (deterministic unpack); fshift within the fp64 reduction bound.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.parity_common import Case, run_gpu_case, bits
+
+pytestmark = pytest.mark.gpu
+
+
+def session_for(case, flags=0, layout=None, capacity=None):
+    from paper_2509_21527_b200.session import HaloSession
+    return HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout or case.layout,
+                       capacity=capacity or case.capacity, device=0, flags=flags, timeout_s=5.0)
+
+
+@pytest.mark.parametrize("name", ["W1", "W2", "W3", "C1", "T3D", "T2P", "T2D", "T4x2", "C2", "C5", "C3"])
+def test_parity_int_forces(name):
+    case = Case(name, seed=1, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess, steps=2)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("name", ["C1", "T3D", "T2P", "C2", "C5", "C3"])
+@pytest.mark.parametrize("seed", [2, 3])
+def test_parity_real_forces(name, seed):
+    case = Case(name, seed=seed, force_kind="normal")
+    sess = session_for(case)
+    run_gpu_case(case, sess)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("name", ["W2", "T3D", "T2P", "C2"])
+def test_parity_float4(name):
+    case = Case(name, seed=1, layout=4, force_kind="normal")
+    sess = session_for(case)
+    run_gpu_case(case, sess)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("name", ["T3D", "T2P", "C3"])
+def test_parity_explicit_maps(name):
+    case = Case(name, seed=2, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess, use_explicit=True)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("name,kind", [("T3D", "int"), ("C2", "int"), ("C3", "normal"), ("C5", "normal")])
+def test_parity_atomic_unpack(name, kind):
+    from paper_2509_21527_b200 import HALO_F_ATOMIC_UNPACK
+    case = Case(name, seed=1, force_kind=kind)
+    sess = session_for(case, flags=HALO_F_ATOMIC_UNPACK)
+    run_gpu_case(case, sess, atomic=(kind != "int"))
+    sess.destroy()
+
+
+@pytest.mark.parametrize("name", ["T3D", "C3"])
+def test_parity_paper_fence_variant(name):
+    from paper_2509_21527_b200 import HALO_F_GPU_FENCE
+    case = Case(name, seed=3, force_kind="int")
+    sess = session_for(case, flags=HALO_F_GPU_FENCE)
+    run_gpu_case(case, sess, steps=3)
+    sess.destroy()
+
+
+def test_moved_coordinates_between_ns_steps():
+    """Hot-path exchange_x with maps fixed and home coordinates moved: every halo
+    row equals fl32(X'[gid] + s*L) (closed form X1 on the moved positions)."""
+    case = Case("C3", seed=1)
+    sess = session_for(case)
+    run_gpu_case(case, sess, check_forces=False)
+    rng = np.random.default_rng(5)
+    Xm = (case.X + rng.uniform(-0.01, 0.01, size=case.X.shape).astype(np.float32)).astype(np.float32)
+    L32 = np.array(case.L, np.float32)
+    for l in range(sess.n_local):
+        st = case.states[l]
+        sess.x[l][: st.n_home] = torch.from_numpy(Xm[st.gid[: st.n_home]]).to(sess.device)
+    sess.exchange_x()
+    torch.cuda.synchronize()
+    for l in range(sess.n_local):
+        st = case.states[l]
+        exp = Xm[st.gid].copy()
+        for d in range(3):
+            m = st.s[:, d] == 1
+            exp[m, d] = (exp[m, d] + L32[d]).astype(np.float32)
+        got = sess.x[l][: st.x.shape[0]].cpu().numpy()
+        np.testing.assert_array_equal(bits(got), bits(exp))
+    sess.destroy()
+
+
+def test_cuda_graph_replay():
+    """x+f captured once into a CUDA graph and replayed: the device-resident
+    sequence numbers keep every replay correct."""
+    case = Case("C3", seed=2, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess)
+    s = torch.cuda.Stream()
+    fshift = torch.zeros(sess.n_local, 3, 3, dtype=torch.float64, device=sess.device)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        sess.exchange_x(stream=s)
+        sess.exchange_f(fshift=fshift, stream=s)
+    for rep in range(5):
+        for l in range(sess.n_local):
+            st = case.states[l]
+            sess.x[l][st.n_home: st.x.shape[0]] = float("nan")
+            sess.f[l][: case.F[l].shape[0]] = torch.from_numpy(case.F[l]).to(sess.device)
+        fshift.zero_()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        for l in range(sess.n_local):
+            st = case.states[l]
+            np.testing.assert_array_equal(bits(sess.x[l][: st.x.shape[0]].cpu().numpy()), bits(st.x))
+            np.testing.assert_array_equal(bits(sess.f[l][: case.F[l].shape[0]].cpu().numpy()), bits(case.Fo[l]))
+            np.testing.assert_array_equal(fshift[l].cpu().numpy(), case.fshift[l])
+    sess.destroy()
+
+
+def test_step_host_e2e():
+    case = Case("C2", seed=1, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess, check_forces=False)
+    nl = sess.n_local
+    xh = [torch.from_numpy(np.ascontiguousarray(case.home_rows(l))).pin_memory() for l in range(nl)]
+    fa = [torch.from_numpy(case.F[l]).pin_memory() for l in range(nl)]
+    xo = [torch.empty(case.states[l].x.shape[0] - case.states[l].n_home, 3).pin_memory() for l in range(nl)]
+    fo = [torch.empty(case.states[l].n_home, 3).pin_memory() for l in range(nl)]
+    fs = torch.zeros(nl, 3, 3, dtype=torch.float64).pin_memory()
+    sess.halo.step_host([t.data_ptr() for t in xh], [t.data_ptr() for t in fa], [t.data_ptr() for t in xo],
+                        [t.data_ptr() for t in fo], fs.data_ptr(), stream=torch.cuda.current_stream().cuda_stream)
+    for l in range(nl):
+        st = case.states[l]
+        np.testing.assert_array_equal(bits(xo[l].numpy()), bits(st.x[st.n_home:]))
+        np.testing.assert_array_equal(bits(fo[l].numpy()), bits(case.Fo[l][: st.n_home]))
+        np.testing.assert_array_equal(fs[l].numpy(), case.fshift[l])
+    sess.destroy()
+
+
+def test_baseline_pack_unpack_kernels():
+    """Per-pulse pack/unpack kernels of the NCCL schedule reproduce the oracle when
+    driven serially on one GPU (transfers done with torch copies)."""
+    case = Case("T3D", seed=1, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess, check_forces=False)
+    nl, P = sess.n_local, sess.npulse
+    lays = [sess.layout_of(l) for l in range(nl)]
+    for l in range(nl):
+        st = case.states[l]
+        sess.x[l][st.n_home: st.x.shape[0]] = 0.0
+    for p in range(P):  # serialized pulses
+        for l in range(nl):
+            pi = case.states[l].pulses[p]
+            buf = torch.empty(max(pi.send_size, 1), 3, device=sess.device)
+            sess.halo.pack_x_pulse(l, p, buf.data_ptr())
+            dst = pi.send_rank
+            off = case.states[dst].pulses[p].atom_offset
+            if pi.send_size:
+                sess.x[dst][off: off + pi.send_size] = buf[: pi.send_size]
+        torch.cuda.synchronize()
+    for l in range(nl):
+        st = case.states[l]
+        np.testing.assert_array_equal(bits(sess.x[l][: st.x.shape[0]].cpu().numpy()), bits(st.x))
+    for l in range(nl):
+        sess.f[l][: case.F[l].shape[0]] = torch.from_numpy(case.F[l]).to(sess.device)
+    fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=sess.device)
+    for p in range(P - 1, -1, -1):
+        bufs = []
+        for l in range(nl):
+            pi = case.states[l].pulses[p]
+            u = pi.send_rank
+            ui = case.states[u].pulses[p]
+            bufs.append(sess.f[u][ui.atom_offset: ui.atom_offset + ui.recv_size].clone())
+        for l in range(nl):
+            sess.halo.unpack_f_pulse(l, p, bufs[l].data_ptr(), fshift.data_ptr() + 0)
+        torch.cuda.synchronize()
+    for l in range(nl):
+        np.testing.assert_array_equal(bits(sess.f[l][: case.F[l].shape[0]].cpu().numpy()), bits(case.Fo[l]))
+        np.testing.assert_array_equal(fshift[l].cpu().numpy(), case.fshift[l])
+    sess.destroy()
+
+
+def test_errors():
+    from paper_2509_21527_b200 import HaloError
+    case = Case("C1", seed=1)
+    # exchange before set_maps -> STATE
+    sess = session_for(case)
+    with pytest.raises(HaloError) as e:
+        sess.exchange_x()
+    assert e.value.status == 4
+    sess.destroy()
+    # capacity overflow agreed on all ranks
+    small = max(s.n_home for s in case.states) + 10
+    sess = session_for(case, capacity=small)
+    sess.load_home([case.home_rows(l) for l in range(sess.n_local)])
+    with pytest.raises(HaloError) as e:
+        sess.set_maps()
+    assert e.value.status == 3
+    with pytest.raises(HaloError):
+        sess.exchange_x()
+    sess.destroy()
+    # home atom outside its cell -> GEOMETRY
+    sess = session_for(case)
+    rows = [case.home_rows(l).copy() for l in range(sess.n_local)]
+    rows[0][0, 2] = 3.0  # rank 0 owns z in [0, L/2)
+    sess.load_home(rows)
+    with pytest.raises(HaloError) as e:
+        sess.set_maps()
+    assert e.value.status == 2
+    sess.destroy()
+    # accumulate=0 with more than one pulse -> UNSUPPORTED
+    case3 = Case("T3D", seed=1)
+    sess = session_for(case3)
+    run_gpu_case(case3, sess, check_forces=False)
+    with pytest.raises(HaloError) as e:
+        sess.exchange_f(accumulate=False)
+    assert e.value.status == 8
+    sess.destroy()
+
+
+def test_accumulate_false_single_pulse():
+    case = Case("C1", seed=1, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess, check_forces=False)
+    from oracle import force_halo
+    Fo, _ = force_halo(case.states, [f.copy() for f in case.F], accumulate=False)
+    for l in range(sess.n_local):
+        sess.f[l][: case.F[l].shape[0]] = torch.from_numpy(case.F[l]).to(sess.device)
+    sess.exchange_f(accumulate=False)
+    torch.cuda.synchronize()
+    for l in range(sess.n_local):
+        np.testing.assert_array_equal(bits(sess.f[l][: case.F[l].shape[0]].cpu().numpy()), bits(Fo[l]))
+    sess.destroy()
+
+
+def test_timers_and_many_steps():
+    from paper_2509_21527_b200 import HALO_F_TIMERS
+    case = Case("C2", seed=1, force_kind="int")
+    sess = session_for(case, flags=HALO_F_TIMERS)
+    run_gpu_case(case, sess, check_forces=True)
+    for _ in range(200):
+        sess.exchange_x()
+        sess.exchange_f()
+    sess.halo.sync()
+    tx, tf = sess.halo.get_timers()
+    assert 0 < tx < 10_000_000 and 0 < tf < 10_000_000
+    sess.destroy()
