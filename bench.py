@@ -1,0 +1,523 @@
+#!/usr/bin/env python
+"""bench.py — x+f halo exchange µs/step on 1/2/4/8 B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl fused|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
+
+A step = one exchange_x + one exchange_f of the whole DD grid (every §8(a)
+row).  The workload's DD ranks are spread over the N GPUs (nranks/N per GPU,
+all of a GPU's ranks in one kernel launch); the system is fixed as N grows
+(strong scaling).  Timing: W warm-up steps, then K steps, each preceded by
+an L2 flush (256 MiB write) and the reset of f to this step's non-bonded
+forces (both outside the timed spans); CUDA events on the launching stream;
+max over ranks.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "x+f halo exchange us/step (max over ranks); achieved NVLink GB/s vs 900"
+UNIT = "us/step"
+SEED = 2509
+
+
+# ------------------------------------------------------------------ dist utils
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def max_over_ranks(v: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(v)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ workload
+def build_workload(cfg_name):
+    from synth import get_config, water_box
+    c = get_config(cfg_name)
+    X = water_box(c.n_atoms, c.L, SEED, slab=c.slab)
+    return c, X
+
+
+def workload_desc(c, n_gpus, layout):
+    return {"workload": f"{c.name}: {c.desc}", "n_atoms": int(c.n_atoms), "grid": list(c.grid),
+            "pulses": list(c.pulses), "rc_nm": c.rc, "box_nm": list(c.L), "dd_ranks": c.nranks,
+            "dd_ranks_per_gpu": c.nranks // n_gpus, "layout": f"float{layout}", "seed": SEED,
+            "l2": "flushed: 256 MiB write before every timed step",
+            "forces": "normal(0,300) float32, reset before every step"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clocks and throttle reasons of the GPUs in use during the timed region (NVML)."""
+
+    def __init__(self, devices, period_s=0.005):
+        self.devices, self.period = devices, period_s
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.handles = [pynvml.nvmlDeviceGetHandleByIndex(d) for d in devices]
+            self.max_mhz = max(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM) for h in self.handles)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake_slowdown",
+        }
+        while not self._stop.is_set():
+            for h in self.handles:
+                try:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    for bit, name in names.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable"}
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ cpu legs
+def oracle_step_timing(c, X, budget_s=15.0, max_steps=None, warmup=1):
+    """The oracle (as it stands) per step: fixed-map x halo + force halo, all DD
+    ranks serially, on this host; maps built once outside the timed region."""
+    from oracle import coord_halo_step, decompose, force_halo  # cpu_baseline leg only
+    from synth import forces_normal
+    states = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    F = [forces_normal(s.x.shape[0], 77 + s.rank) for s in states]
+    xh = [s.x[: s.n_home].copy() for s in states]
+    for _ in range(warmup):
+        coord_halo_step(states, xh)
+        force_halo(states, F)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        coord_halo_step(states, xh)
+        force_halo(states, F)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_steps is not None and n >= max_steps):
+            break
+    return el / n * 1e6, n
+
+
+# ------------------------------------------------------------------ main arm
+def run_fused(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_21527_b200 import HALO_F_TIMERS
+    from paper_2509_21527_b200.session import HaloSession, assign_home
+    from synth import forces_normal
+
+    c, X = build_workload(args.config)
+    if c.nranks % world != 0:
+        raise SystemExit(f"config {c.name} has {c.nranks} DD ranks, not divisible by {world} GPUs")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    homes = assign_home(X, c.L, c.grid)
+    cap = int(max(len(h) for h in homes) * 2.2) + 4096
+    flags = HALO_F_TIMERS if args.timers else 0
+    sess = HaloSession(c.grid, c.L, c.rc, c.pulses, layout=args.layout, capacity=cap, device=local, flags=flags,
+                       nprocs=world, proc=rank, timeout_s=20.0)
+    first, nl = sess.first_rank, sess.n_local
+    sess.load_home([X[homes[first + l]] for l in range(nl)])
+    sess.set_maps()
+    lay = [sess.layout_of(l) for l in range(nl)]
+    P = sess.npulse
+    W = args.layout
+    F0 = []
+    for l in range(nl):
+        n = lay[l]["n_total"]
+        F0.append(torch.from_numpy(forces_normal(n, 5000 + first + l, width=W)).to(dev))
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=dev)
+
+    def reset_f():
+        for l in range(nl):
+            sess.f[l][: F0[l].shape[0]].copy_(F0[l])
+
+    def step():
+        sess.exchange_x()
+        sess.exchange_f(fshift=fshift)
+
+    for _ in range(args.warmup):
+        reset_f()
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    sampler = ClockSampler([local])
+    sampler.start()
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    torch.cuda.synchronize()
+    barrier()
+    for k in range(K):
+        reset_f()
+        flush.fill_(float(k))
+        ev[k][0].record(stream)
+        sess.exchange_x()
+        ev[k][1].record(stream)
+        sess.exchange_f(fshift=fshift)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    sampler.stop()
+    xs = [ev[k][0].elapsed_time(ev[k][1]) * 1e3 for k in range(K)]
+    fs = [ev[k][1].elapsed_time(ev[k][2]) * 1e3 for k in range(K)]
+    tot = [a + b for a, b in zip(xs, fs)]
+    my = {"step": float(np.mean(tot)), "x": float(np.mean(xs)), "f": float(np.mean(fs)),
+          "step_median": float(np.median(tot))}
+    res = {k: max_over_ranks(v) for k, v in my.items()}
+    dev_spans = None
+    if args.timers:
+        tx, tf = sess.halo.get_timers()
+        dev_spans = {"x_us": max_over_ranks(tx / 1e3), "f_us": max_over_ranks(tf / 1e3)}
+
+    # CUDA-graph mode: one captured x+f step, replayed (flush between replays)
+    graph_us = None
+    if not args.no_graph:
+        gs = torch.cuda.Stream(device=dev)
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        barrier()
+        with torch.cuda.graph(g, stream=gs):
+            sess.exchange_x(stream=gs)
+            sess.exchange_f(fshift=fshift, stream=gs)
+        torch.cuda.synchronize()
+        barrier()
+        gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+        for k in range(min(K, 2000) + args.warmup):
+            reset_f()
+            flush.fill_(1.0)
+            kk = k - args.warmup
+            if kk >= 0:
+                gev[kk][0].record(stream)
+            g.replay()
+            if kk >= 0:
+                gev[kk][1].record(stream)
+        torch.cuda.synchronize()
+        nk = min(K, 2000)
+        graph_us = max_over_ranks(float(np.mean([gev[k][0].elapsed_time(gev[k][1]) * 1e3 for k in range(nk)])))
+        barrier()
+        del g
+
+    # e2e through the C-ABI host-buffer call (pinned host memory; H2D + D2H inside)
+    xh = [torch.from_numpy(np.ascontiguousarray(
+        np.pad(X[homes[first + l]], ((0, 0), (0, W - 3))).astype(np.float32))).pin_memory() for l in range(nl)]
+    fa = [F0[l].cpu().pin_memory() for l in range(nl)]
+    xo = [torch.empty(max(lay[l]["n_total"] - lay[l]["n_home"], 1), W).pin_memory() for l in range(nl)]
+    fo = [torch.empty(max(lay[l]["n_home"], 1), W).pin_memory() for l in range(nl)]
+    fsh = torch.zeros(nl, 3, 3, dtype=torch.float64).pin_memory()
+    h2d = sum(4 * W * (lay[l]["n_home"] + lay[l]["n_total"]) for l in range(nl))
+    d2h = sum(4 * W * lay[l]["n_total"] for l in range(nl)) + 72 * nl
+
+    def host_step():
+        sess.halo.step_host([t.data_ptr() for t in xh], [t.data_ptr() for t in fa], [t.data_ptr() for t in xo],
+                            [t.data_ptr() for t in fo], fsh.data_ptr(), stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        host_step()
+    barrier()
+    Ke = K
+    eev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(Ke)]
+    for k in range(Ke):
+        flush.fill_(1.0)
+        eev[k][0].record(stream)
+        host_step()
+        eev[k][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_us = max_over_ranks(float(np.mean([eev[k][0].elapsed_time(eev[k][1]) * 1e3 for k in range(Ke)])))
+    barrier()
+
+    # NCCL send/recv baseline on the same maps (one DD rank per GPU only)
+    nccl = None
+    if world > 1 and nl == 1 and not args.no_nccl:
+        nccl = run_nccl_baseline(sess, lay[0], F0[0], flush, K, args.warmup, W)
+
+    # latency floor: peer flag ping-pong between process 0 and process 1
+    floor = None
+    if world > 1:
+        t0 = None
+        if rank in (0, 1):
+            peer = sess.first_rank + sess.n_local if rank == 0 else 0
+            t0 = sess.halo.floor_pingpong(peer, iters=10000)
+        barrier()
+        t0 = max_over_ranks(t0 or 0.0)
+        floor = {"t0_one_way_us": t0}
+
+    # algorithmic bytes per launch (this GPU), DESIGN.md "Roofline"
+    rows_x = sum(sum(lay[l]["send_size"]) for l in range(nl))
+    rows_f = sum(sum(lay[l]["recv_size"]) for l in range(nl))
+    bx = (4 + 8 * W) * rows_x            # map + gather read + peer write
+    bf = (4 + 20 * W) * rows_f           # slice read + peer write + buf read + map + RMW f
+    # rows that cross NVLink (receiver on another GPU), both directions
+    per_gpu = c.nranks // world
+    remote_rows = 0
+    for l in range(nl):
+        r = first + l
+        for p in range(P):
+            dst = _neighbour(c.grid, r, sess.halo.pulse_order()[p], -1)
+            if dst // per_gpu != r // per_gpu:
+                remote_rows += lay[l]["send_size"][p]
+    nvl_bytes = remote_rows * 4 * W * 2  # x out + f back (per direction)
+
+    peaks = load_peaks()
+    dom = "x" if res["x"] >= res["f"] else "f"
+    dom_bytes = bx if dom == "x" else bf
+    dom_us = res[dom]
+    achieved = dom_bytes / (dom_us * 1e-6) / 1e9
+    traffic = load_traffic(c.name, world, dom)
+    roof = {"bound": "hbm", "kernel": f"k_exchange_{dom}", "achieved": round(achieved, 3),
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 6),
+            "traffic": traffic, "algorithmic_bytes_per_launch": int(dom_bytes),
+            "note": "latency-bound path: the HBM bytes of every config take < 1 us; see latency_floor / DESIGN.md"}
+    out = {
+        "metric": METRIC, "value": round(res["step"], 3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(res["step"] / 1e3, 6), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict(workload_desc(c, world, W), parallelism=f"spatial DD {c.grid[0]}x{c.grid[1]}x{c.grid[2]}",
+                       mode="eager, one exchange_x + one exchange_f launch per GPU per step"),
+        "x_us": round(res["x"], 3), "f_us": round(res["f"], 3), "step_median_us": round(res["step_median"], 3),
+        "graph_us_per_step": None if graph_us is None else round(graph_us, 3),
+        "clocks": sampler.summary(),
+        "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
+                "d2h_bytes_per_step": int(d2h) * world, "path": "halo_step_host (C ABI, pinned host buffers)"},
+        "gpu_launches": 2 * K * world,
+        "roofline": roof,
+        "nvlink": {"bytes_per_step_per_gpu_per_direction": int(nvl_bytes),
+                   "achieved_gbs": round(nvl_bytes / (res["step"] * 1e-6) / 1e9, 3) if nvl_bytes else 0.0,
+                   "peak_gbs": 900.0, "measured_peer_copy_gbs": 770.0},
+        "latency_floor": floor,
+        "nccl_baseline": nccl,
+        "device_spans": dev_spans,
+    }
+    if floor and floor["t0_one_way_us"]:
+        t0 = floor["t0_one_way_us"]
+        fl = 2 * P * t0 + 2 * nvl_bytes / 770e9 * 1e6
+        floor["floor_step_us"] = round(fl, 3)
+        floor["value_over_floor"] = round(res["step"] / fl, 3)
+    if world == 1 and rank == 0 and not args.no_cpu:
+        us, n = oracle_step_timing(c, X, budget_s=args.cpu_budget)
+        out["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"{c.name} full workload ({c.nranks} DD ranks, {P} pulses), {n} oracle "
+                                         f"steps (fixed-map x halo + force halo), numpy single thread"}
+    sess.destroy()
+    return out
+
+
+def _neighbour(grid, r, d, delta):
+    c = [r // (grid[1] * grid[2]), (r // grid[2]) % grid[1], r % grid[2]]
+    c[d] = (c[d] + delta) % grid[d]
+    return (c[0] * grid[1] + c[1]) * grid[2] + c[2]
+
+
+def run_nccl_baseline(sess, lay, F0, flush, K, warmup, W):
+    """Serialized per-pulse schedule (Fig. 1) with NCCL send/recv: pack kernel ->
+    grouped ncclSend/ncclRecv -> (forces, reverse) ncclSend/ncclRecv -> unpack kernel."""
+    import torch
+    import torch.distributed as dist
+    dev = sess.device
+    P = sess.npulse
+    dims = sess.halo.pulse_order()
+    me = sess.first_rank
+    grid = sess.grid
+    sendbuf = [torch.empty(max(lay["send_size"][p], 1), W, device=dev) for p in range(P)]
+    fbuf = [torch.empty(max(lay["send_size"][p], 1), W, device=dev) for p in range(P)]
+    fshift = torch.zeros(1, 3, 3, dtype=torch.float64, device=dev)
+    x, f = sess.x[0], sess.f[0]
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for p in range(P):
+            lo, up = _neighbour(grid, me, dims[p], -1), _neighbour(grid, me, dims[p], +1)
+            n_s, n_r, off = lay["send_size"][p], lay["recv_size"][p], lay["recv_off"][p]
+            sess.halo.pack_x_pulse(0, p, sendbuf[p].data_ptr(), stream=stream.cuda_stream)
+            ops = []
+            if n_s:
+                ops.append(dist.P2POp(dist.isend, sendbuf[p][:n_s], lo))
+            if n_r:
+                ops.append(dist.P2POp(dist.irecv, x[off: off + n_r], up))
+            for w in dist.batch_isend_irecv(ops) if ops else []:
+                w.wait()
+        for p in range(P - 1, -1, -1):
+            lo, up = _neighbour(grid, me, dims[p], -1), _neighbour(grid, me, dims[p], +1)
+            n_s, n_r, off = lay["send_size"][p], lay["recv_size"][p], lay["recv_off"][p]
+            ops = []
+            if n_r:
+                ops.append(dist.P2POp(dist.isend, f[off: off + n_r], up))
+            if n_s:
+                ops.append(dist.P2POp(dist.irecv, fbuf[p][:n_s], lo))
+            for w in dist.batch_isend_irecv(ops) if ops else []:
+                w.wait()
+            sess.halo.unpack_f_pulse(0, p, fbuf[p].data_ptr(), fshift.data_ptr(), stream=stream.cuda_stream)
+
+    for _ in range(warmup):
+        f[: F0.shape[0]].copy_(F0)
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    for k in range(K):
+        f[: F0.shape[0]].copy_(F0)
+        flush.fill_(1.0)
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    us = max_over_ranks(float(np.mean([ev[k][0].elapsed_time(ev[k][1]) * 1e3 for k in range(K)])))
+    barrier()
+    return {"us_per_step": round(us, 3), "schedule": "per-pulse pack -> NCCL send/recv -> unpack (torch "
+            "batch_isend_irecv), same maps", "launches_per_step": 2 * P}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def load_traffic(cfg, world, dom):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"{cfg}/n{world}/{dom}")
+    except Exception:
+        return None
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return None
+    c, X = build_workload(args.config)
+    # warm-up steps W, then K timed steps, each step one full oracle x+f over all DD ranks
+    from oracle import coord_halo_step, decompose, force_halo
+    from synth import forces_normal
+    states = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    F = [forces_normal(s.x.shape[0], 77 + s.rank) for s in states]
+    xh = [s.x[: s.n_home].copy() for s in states]
+    for _ in range(args.warmup):
+        coord_halo_step(states, xh)
+        force_halo(states, F)
+    ts = []
+    t_end = time.perf_counter() + args.cpu_budget * 8
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        coord_halo_step(states, xh)
+        force_halo(states, F)
+        ts.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    us = float(np.mean(ts)) * 1e6
+    P = len(states[0].pulses)
+    samp = f"{c.name} full workload ({c.nranks} DD ranks, {P} pulses), {len(ts)} of {args.steps} steps"
+    return {"impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
+            "steps": len(ts), "warmup": args.warmup, "ms_per_step": round(us / 1e3, 4), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_desc(c, world, 3),
+            "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": samp},
+            "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--layout", type=int, default=3, choices=(3, 4))
+    ap.add_argument("--impl", default="fused", choices=("fused", "reference"))
+    ap.add_argument("--timers", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+    if args.gpus is not None and args.gpus != world and world != 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    out = run_fused(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -93,6 +93,14 @@ typedef struct {
  * *out receives the ctx (NULL on error; use halo_strerror). */
 HALO_API halo_status halo_init(const halo_config* cfg, halo_ctx** out);
 
+/* Host-only query (no CUDA call, usable before choosing a device): validates
+ * `cfg` like halo_init and returns the DD ranks this process would host
+ * ([*first_rank, *first_rank + *n_local)), the pulse count and order (dims[p]
+ * in 0/1/2 = x/y/z, z -> y -> x; dims sized HALO_MAX_PULSES or NULL)
+ * and halo_scratch_bytes().  Any output pointer may be NULL. */
+HALO_API halo_status halo_query_config(const halo_config* cfg, int* first_rank, int* n_local, int* npulse,
+                                       int* dims, size_t* scratch_bytes);
+
 /* DD ranks hosted by this process: [*first_rank, *first_rank + *n_local). */
 HALO_API halo_status halo_local_ranks(const halo_ctx* ctx, int* first_rank, int* n_local);
 

@@ -118,6 +118,7 @@ class PulseInfo:
     shift: bool = False       # this rank applied +L_dim when sending
     map: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
     dep: frozenset = frozenset()  # earlier pulses whose receive ranges map touches (R9)
+    shift_vec: np.ndarray = field(default_factory=lambda: np.zeros(3, np.float32))  # +L_dim e_dim if shift
 
 
 @dataclass
@@ -200,6 +201,8 @@ def decompose(X, L, rc, grid, pulses, W=None):
                     dep.add(q)
             info = PulseInfo(dim=d, k=k, send_rank=rank_of(lower, grid), recv_rank=rank_of(upper, grid),
                              send_size=int(mp.size), shift=bool(shift), map=mp, dep=frozenset(dep))
+            if shift:
+                info.shift_vec = sv.copy()
             st.pulses.append(info)
             sends.append((info.send_rank, payload, st.gid[mp].copy(), st.s[mp].copy(), shift, st.rank))
         # receivers append (receiver = sender's lower neighbour)
@@ -218,9 +221,33 @@ def decompose(X, L, rc, grid, pulses, W=None):
     return states
 
 
-def coord_halo_values(states, plist_len=None):
-    """Per-rank halo rows x[n_home:] (convenience accessor)."""
-    return [st.x[st.n_home:] for st in states]
+def coord_halo_step(states, x_home):
+    """Per-step coordinate halo with the maps of the last neighbour-search step
+    fixed (Alg. 3 P:252-262 with Alg. 4's forwarding, run serially pulse by
+    pulse): returns new per-rank x arrays whose rows [0, n_home) are x_home[r]
+    and whose halo rows are re-gathered through the stored maps, shifted by
+    +L_d (float32 add of the full 3-vector, R25) on wrapping sends.
+
+    x_home: list of [n_home_r, width] float32 arrays.  The box lengths are taken
+    from the shift the rank recorded: states carry them in ``pulse.shift_vec``.
+    """
+    xs = []
+    for st, xh in zip(states, x_home):
+        x = np.zeros_like(st.x)
+        x[: st.n_home] = xh
+        xs.append(x)
+    P = len(states[0].pulses) if states else 0
+    for p in range(P):
+        sends = []
+        for st in states:
+            pi = st.pulses[p]
+            payload = xs[st.rank][pi.map].copy()
+            if pi.shift:
+                payload[:, :3] = payload[:, :3] + pi.shift_vec
+            sends.append((pi.send_rank, st.pulses[p].remote_offset, payload))
+        for dst, off, payload in sends:
+            xs[dst][off: off + payload.shape[0]] = payload
+    return xs
 
 
 def force_halo(states, F, fshift_in=None, accumulate=True):

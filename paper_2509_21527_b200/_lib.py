@@ -21,7 +21,7 @@ HALO_MAX_PULSES = 6
 
 # every symbol include/halo.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "halo_init", "halo_local_ranks", "halo_pulse_order", "halo_scratch_bytes", "halo_register_buffers",
+    "halo_init", "halo_query_config", "halo_local_ranks", "halo_pulse_order", "halo_scratch_bytes", "halo_register_buffers",
     "halo_ipc_export", "halo_ipc_import", "halo_set_maps", "halo_set_maps_explicit", "halo_get_layout",
     "halo_get_map", "halo_exchange_x", "halo_exchange_f", "halo_step_host", "halo_pack_x_pulse",
     "halo_unpack_f_pulse", "halo_get_timers", "halo_floor_pingpong", "halo_sync", "halo_strerror",
@@ -51,6 +51,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     IP = POINTER(c_int)
     sig = {
         "halo_init": ([POINTER(halo_config), POINTER(c_void_p)], c_int),
+        "halo_query_config": ([POINTER(halo_config), IP, IP, IP, IP, POINTER(c_size_t)], c_int),
         "halo_local_ranks": ([P, IP, IP], c_int),
         "halo_pulse_order": ([P, IP, IP], c_int),
         "halo_scratch_bytes": ([P, POINTER(c_size_t)], c_int),

@@ -274,6 +274,30 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   return HALO_OK;
 }
 
+halo_status halo_query_config(const halo_config* cfg, int* first_rank, int* n_local, int* npulse, int* dims,
+                              size_t* scratch_bytes) {
+  std::string why;
+  halo_status s = validate(cfg, why);
+  if (s != HALO_OK) return s;
+  const int nr = cfg->grid[0] * cfg->grid[1] * cfg->grid[2];
+  const int nl = nr / cfg->nprocs;
+  int P = 0;
+  const int order[3] = {2, 1, 0};
+  for (int i = 0; i < 3; ++i)
+    if (cfg->grid[order[i]] > 1)
+      for (int k = 0; k < cfg->pulses[order[i]]; ++k) {
+        if (dims) dims[P] = order[i];
+        ++P;
+      }
+  if (first_rank) *first_rank = cfg->proc * nl;
+  if (n_local) *n_local = nl;
+  if (npulse) *npulse = P;
+  if (scratch_bytes)
+    *scratch_bytes = kHdrBytes + (size_t)P * align_up((size_t)cfg->capacity, 64) * sizeof(int32_t) +
+                     (size_t)P * align_up((size_t)cfg->capacity * cfg->layout, 64) * sizeof(float);
+  return HALO_OK;
+}
+
 halo_status halo_local_ranks(const halo_ctx* ctx, int* first_rank, int* n_local) {
   if (!ctx) return HALO_ERR_ARG;
   if (first_rank) *first_rank = ctx->first_rank;

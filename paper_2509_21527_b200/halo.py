@@ -21,24 +21,45 @@ class HaloError(RuntimeError):
         self.status = status
 
 
+def make_config(grid, box, cutoff, pulses, layout=3, capacity=1 << 16, device=0, flags=0, nprocs=1, proc=0,
+                timeout_s=10.0) -> halo_config:
+    cfg = halo_config()
+    cfg.grid[:] = [int(v) for v in grid]
+    cfg.box[:] = [float(v) for v in box]
+    cfg.cutoff = float(cutoff)
+    cfg.pulses[:] = [int(v) for v in pulses]
+    cfg.layout = int(layout)
+    cfg.capacity = int(capacity)
+    cfg.device = int(device)
+    cfg.flags = int(flags)
+    cfg.nprocs = int(nprocs)
+    cfg.proc = int(proc)
+    cfg.timeout_s = float(timeout_s)
+    return cfg
+
+
+def query_config(grid, box, cutoff, pulses, layout=3, capacity=1 << 16, nprocs=1, proc=0):
+    """halo_query_config: host-only plan (no CUDA).  Returns dict(first_rank, n_local, dims, scratch_bytes)."""
+    lib = _lib.load()
+    cfg = make_config(grid, box, cutoff, pulses, layout, capacity, 0, 0, nprocs, proc)
+    a, b, n = c_int(), c_int(), c_int()
+    dims = (c_int * _lib.HALO_MAX_PULSES)()
+    sb = c_size_t()
+    st = lib.halo_query_config(ctypes.byref(cfg), ctypes.byref(a), ctypes.byref(b), ctypes.byref(n), dims,
+                               ctypes.byref(sb))
+    if st != 0:
+        raise HaloError(st, lib.halo_strerror(st).decode())
+    return dict(first_rank=a.value, n_local=b.value, dims=[dims[i] for i in range(n.value)],
+                scratch_bytes=sb.value)
+
+
 class Halo:
     """One context per process (hosts nranks/nprocs DD ranks)."""
 
     def __init__(self, grid, box, cutoff, pulses, layout=3, capacity=1 << 16, device=0, flags=0,
                  nprocs=1, proc=0, timeout_s=10.0):
         self.lib = _lib.load()
-        cfg = halo_config()
-        cfg.grid[:] = [int(v) for v in grid]
-        cfg.box[:] = [float(v) for v in box]
-        cfg.cutoff = float(cutoff)
-        cfg.pulses[:] = [int(v) for v in pulses]
-        cfg.layout = int(layout)
-        cfg.capacity = int(capacity)
-        cfg.device = int(device)
-        cfg.flags = int(flags)
-        cfg.nprocs = int(nprocs)
-        cfg.proc = int(proc)
-        cfg.timeout_s = float(timeout_s)
+        cfg = make_config(grid, box, cutoff, pulses, layout, capacity, device, flags, nprocs, proc, timeout_s)
         self.cfg = cfg
         self.layout = int(layout)
         h = c_void_p()

@@ -331,3 +331,25 @@ def test_float4_w_copied_unshifted():
     st = decompose(X, c.L, c.rc, c.grid, c.pulses, W=W)
     for s in st:
         np.testing.assert_array_equal(s.x[:, 3], W[s.gid])
+
+
+@pytest.mark.parametrize("name", ["T3D", "T2P", "C2", "T4x2"])
+def test_coord_halo_step_fixed_maps(name):
+    """Per-step x halo with fixed maps: reproduces the NS-step halo, and for moved
+    home coordinates every halo row equals fl32(X'[gid] + s*L) (closed form X1)."""
+    from oracle import coord_halo_step
+    c, X = system(name, 3)
+    st = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    xs = coord_halo_step(st, [s.x[: s.n_home] for s in st])
+    for s, x in zip(st, xs):
+        np.testing.assert_array_equal(x, s.x)
+    rng = np.random.default_rng(9)
+    Xm = (X + rng.uniform(-0.02, 0.02, size=X.shape).astype(np.float32)).astype(np.float32)
+    xs = coord_halo_step(st, [Xm[s.gid[: s.n_home]] for s in st])
+    L32 = np.array(c.L, np.float32)
+    for s, x in zip(st, xs):
+        exp = Xm[s.gid].copy()
+        for d in range(3):
+            m = s.s[:, d] == 1
+            exp[m, d] = (exp[m, d] + L32[d]).astype(np.float32)
+        np.testing.assert_array_equal(x, exp)
