@@ -122,6 +122,7 @@ struct ExParams {
   unsigned flags;
   double* fshift;           // [n_local][3][3] or nullptr
   int accumulate;
+  uint32_t poll_ns;         // __nanosleep between flag polls (0 = tight spin)
 };
 
 struct SelParams {

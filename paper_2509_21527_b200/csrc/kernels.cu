@@ -68,17 +68,26 @@ __device__ __noinline__ void report_timeout(int* err_host, int code) {
 }
 
 // Bounded spin: returns false on timeout.  `sys` selects the scope of the acquire.
+// The flag is polled back to back; the timer and the (host-mapped, PCIe)
+// error word are only looked at every 1024 polls so they never sit on the
+// latency path.
 template <bool kSys>
 __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t v, uint64_t timeout_ns, int* err_host,
-                                         int code) {
+                                         int code, uint32_t poll_ns = 0) {
   if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
-  const uint64_t t0 = gtimer();
-  for (;;) {
+  uint64_t t0 = 0;
+  for (uint32_t it = 1;; ++it) {
+    if (poll_ns) __nanosleep(poll_ns);
     if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
-    if (*(volatile int*)err_host != 0) return false;  // another wait already failed: drain
-    if (gtimer() - t0 > timeout_ns) {
-      report_timeout(err_host, code);
-      return false;
+    if ((it & 1023u) == 0) {
+      const uint64_t now = gtimer();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > timeout_ns) {
+        report_timeout(err_host, code);
+        return false;
+      }
+      if (*(volatile int*)err_host != 0) return false;  // another wait already failed: drain
     }
   }
 }
@@ -86,14 +95,19 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t v, uint64_t
 // Wait until (*p >> 32) == epoch; returns the low 32 bits (or 0xffffffff on timeout).
 __device__ __forceinline__ uint32_t wait_epoch(const uint64_t* p, uint32_t epoch, uint64_t timeout_ns,
                                                int* err_host, int code) {
-  const uint64_t t0 = gtimer();
-  for (;;) {
-    uint64_t v = ld_acquire_sys(p);
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    const uint64_t v = ld_acquire_sys(p);
     if ((uint32_t)(v >> 32) == epoch) return (uint32_t)v;
-    if (*(volatile int*)err_host != 0) return 0xffffffffu;
-    if (gtimer() - t0 > timeout_ns) {
-      report_timeout(err_host, code);
-      return 0xffffffffu;
+    if ((it & 1023u) == 1023u) {
+      const uint64_t now = gtimer();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > timeout_ns) {
+        report_timeout(err_host, code);
+        return 0xffffffffu;
+      }
+      if (*(volatile int*)err_host != 0) return 0xffffffffu;
     }
   }
 }
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
         while (m) {
           const int q = __ffs(m) - 1;
           m &= m - 1;
-          wait_geq<true>(&rd.hdr->flag_x[q], seq, P.timeout_ns, P.err_host, tcode(1, w.lrank, q));
+          wait_geq<true>(&rd.hdr->flag_x[q], seq, P.timeout_ns, P.err_host, tcode(1, w.lrank, q), P.poll_ns);
         }
       }
       __syncthreads();
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
     const RankDev& rd = P.ranks[lr];
     for (int p = P.p_lo; p < P.p_hi; ++p) {
       if (P.pulses[lr * P.P + p].recv_size > 0)
-        wait_geq<true>(&rd.hdr->flag_x[p], seq, P.timeout_ns, P.err_host, tcode(2, lr, p));
+        wait_geq<true>(&rd.hdr->flag_x[p], seq, P.timeout_ns, P.err_host, tcode(2, lr, p), P.poll_ns);
     }
   }
   __syncthreads();
@@ -311,7 +325,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
         while (m) {
           const int q = __ffs(m) - 1;
           m &= m - 1;
-          wait_geq<false>(&ctrl->unpacked[w.lrank][q], seq, P.timeout_ns, P.err_host, tcode(3, w.lrank, q));
+          wait_geq<false>(&ctrl->unpacked[w.lrank][q], seq, P.timeout_ns, P.err_host, tcode(3, w.lrank, q), P.poll_ns);
         }
       }
       __syncthreads();
@@ -321,13 +335,13 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
         pulse_complete_sys(P.flags, &ctrl->cnt_push[w.lrank][w.pulse], pd.n_items_push, pd.flag_f_dst, seq);
     } else {  // kItemUnpack
       if (threadIdx.x == 0) {
-        wait_geq<true>(&rd.hdr->flag_f[w.pulse], seq, P.timeout_ns, P.err_host, tcode(4, w.lrank, w.pulse));
+        wait_geq<true>(&rd.hdr->flag_f[w.pulse], seq, P.timeout_ns, P.err_host, tcode(4, w.lrank, w.pulse), P.poll_ns);
         if (!atomic) {  // deterministic: pulses descending (R15)
           uint32_t m = pd.chain;
           while (m) {
             const int q = __ffs(m) - 1;
             m &= m - 1;
-            wait_geq<false>(&ctrl->unpacked[w.lrank][q], seq, P.timeout_ns, P.err_host, tcode(5, w.lrank, q));
+            wait_geq<false>(&ctrl->unpacked[w.lrank][q], seq, P.timeout_ns, P.err_host, tcode(5, w.lrank, q), P.poll_ns);
           }
         }
       }

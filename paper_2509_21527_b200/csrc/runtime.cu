@@ -117,6 +117,7 @@ struct halo_ctx {
   uint64_t ping_base = 0;
   int max_x = 0, max_f = 0;
   int item_rows = 512;
+  uint32_t poll_ns = 0;
 
   int cell(int r, int d) const {
     const int* g = cfg.grid;
@@ -250,6 +251,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   ctx->peer_x.assign(ctx->nranks, nullptr);
   ctx->peer_scratch.assign(ctx->nranks, nullptr);
   if (const char* e = getenv("HALO_ITEM_ROWS")) ctx->item_rows = std::max(32, atoi(e));
+  if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = (uint32_t)std::max(0, atoi(e));
 
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ctrl, sizeof(Ctrl));
@@ -577,6 +579,7 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.flags = ctx->cfg.flags;
   P.fshift = nullptr;
   P.accumulate = 1;
+  P.poll_ns = ctx->poll_ns;
   return P;
 }
 

@@ -67,7 +67,7 @@ class Case:
         return s.x[: s.n_home]
 
 
-def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit=False, steps=1):
+def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit=False, steps=1, barrier=None):
     """Drive the CUDA path for the local ranks of `sess` and compare with the oracle.
     Returns a dict of per-check booleans (asserts on the way)."""
     first, nl = sess.first_rank, sess.n_local
@@ -95,6 +95,11 @@ def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit
         for l in range(nl):
             st = case.states[first + l]
             sess.x[l][st.n_home: st.x.shape[0]] = float("nan")
+        if barrier is not None:
+            # the poison is written outside the protocol: every process must have
+            # poisoned before any peer stores this step's halo (R17)
+            torch.cuda.synchronize()
+            barrier()
         sess.exchange_x()
         torch.cuda.synchronize()
         for l in range(nl):

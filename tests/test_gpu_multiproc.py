@@ -39,7 +39,7 @@ def _worker(rank, world, port, cases, out):
                 continue
             sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout, capacity=case.capacity,
                                device=rank, flags=flags, nprocs=world, proc=rank, timeout_s=10.0)
-            run_gpu_case(case, sess, steps=steps, atomic=bool(flags & 1) and kind != "int")
+            run_gpu_case(case, sess, steps=steps, atomic=bool(flags & 1) and kind != "int", barrier=dist.barrier)
             dist.barrier()
             sess.destroy()
             dist.barrier()
