@@ -71,6 +71,11 @@ typedef enum {
 #define HALO_F_GPU_FENCE      (1u << 2) /* per-CTA gpu-scope release + sys-scope release by the last CTA
                                            only (the paper's P:425-427 scheme); default: per-CTA sys fence */
 #define HALO_F_TIMERS         (1u << 3) /* record %globaltimer spans of each exchange kernel */
+#define HALO_F_PAPER_FLAGS    (1u << 4) /* the paper's per-pulse signalling (Alg. 5: per-CTA completion counter,
+                                           one release flag per pulse, receiver acquire-wait; force slices
+                                           pushed then scatter-added).  Default: the LL protocol (every 8-B
+                                           store carries a 32-bit sequence tag; row-level forwarding; the
+                                           force halo is a deterministic gather) */
 
 typedef struct {
   int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */

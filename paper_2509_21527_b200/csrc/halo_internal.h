@@ -6,7 +6,12 @@
 //   scratch   caller-owned per DD rank, peer-mapped (CUDA IPC):
 //               [0, 4096)                ScratchHdr: flags written by peers
 //               [4096, ...)              P index maps (int32, capacity each)
-//               [..., ...)               P force receive buffers (capacity rows each)
+//               [..., ...)               P force receive buffers, flag protocol (capacity rows each)
+//               [..., ...)               P coordinate LL receive buffers (capacity*layout u64 units)
+//               [..., ...)               P force LL receive buffers (capacity*layout u64 units)
+//             An LL unit is {fp32 value (low word), 32-bit sequence tag (high word)}
+//             written with one 8-byte store: single-copy atomic, so a reader that
+//             sees the current tag sees the value (no fence, no flag).
 //   ctrl      library-owned per process: sequence numbers, completion
 //             counters, local "unpacked" flags, set_maps results
 //   plan      library-owned per process: RankDev[], PulseDev[], work items
@@ -69,9 +74,19 @@ struct RankDev {
   ScratchHdr* hdr;          // own scratch header
   int32_t* maps;            // own maps region (P slots of map_stride ints)
   float* fbuf;              // own force receive buffers (P slots of fbuf_stride floats)
+  uint64_t* xll;            // own coordinate LL receive buffers (P slots of ll_stride units)
+  uint64_t* fll;            // own force LL receive buffers (P slots of ll_stride units)
+  // force gather (LL protocol): task rows in level order, CSR of contributions
+  const int32_t* task_row;  // [n_tasks] row index
+  const int32_t* task_off;  // [n_tasks + 1] contribution offsets
+  const uint32_t* contrib;  // (q << 24) | i, pulses descending per row (R15)
   int n_home;
   int n_total;
   int rank;                 // global DD rank
+  int wrap_mask;            // bit p set iff this rank shifts in pulse p
+  int recv_off[kMaxP];      // own receive range of each pulse
+  int recv_size[kMaxP];
+  int pulse_dim[kMaxP];
   int pad;
 };
 
@@ -92,13 +107,16 @@ struct PulseDev {
   uint32_t dep_x;           // pulses q < p whose receive range map_p reads (R9)
   uint32_t fdep;            // pulses q > p whose maps read slice p: push(p) waits unpacked[q]
   uint32_t chain;           // pulses q > p with send_size > 0 (deterministic unpack order)
+  uint64_t* xll_dst;        // receiver's coordinate LL buffer of pulse p (peer pointer), LL protocol
+  uint64_t* fll_dst;        // x-sender's force LL buffer of pulse p (peer pointer), LL protocol
   int n_items_x;
   int n_items_push;
   int n_items_unpack;
   int pad;
 };
 
-enum : uint8_t { kItemXIndep = 0, kItemXDep = 1, kItemPush = 2, kItemUnpack = 3 };
+enum : uint8_t { kItemXIndep = 0, kItemXDep = 1, kItemPush = 2, kItemUnpack = 3, kItemXRecv = 4, kItemGather = 5 };
+constexpr uint8_t kHomeLevel = 0xff;   // Item.pulse of gather items over home rows
 
 struct Item {
   uint16_t lrank;
@@ -123,6 +141,7 @@ struct ExParams {
   double* fshift;           // [n_local][3][3] or nullptr
   int accumulate;
   uint32_t poll_ns;         // __nanosleep between flag polls (0 = tight spin)
+  uint64_t ll_stride;       // u64 units per pulse slot of the LL receive buffers
 };
 
 struct SelParams {

@@ -18,125 +18,11 @@
 // host-mapped error word, HALO_ERR_TIMEOUT on the next call).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include "halo_internal.h"
+#include "ptx.cuh"
 
 namespace halo {
-
-// ----------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t atom_add_acqrel_gpu(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Report a timeout once: host-mapped word (system scope) + give up.
-__device__ __noinline__ void report_timeout(int* err_host, int code) {
-  volatile int* e = err_host;
-  if (*e == 0) *e = code;
-  fence_sys();
-}
-
-// Bounded spin: returns false on timeout.  `sys` selects the scope of the acquire.
-// The flag is polled back to back; the timer and the (host-mapped, PCIe)
-// error word are only looked at every 1024 polls so they never sit on the
-// latency path.
-template <bool kSys>
-__device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t v, uint64_t timeout_ns, int* err_host,
-                                         int code, uint32_t poll_ns = 0) {
-  if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
-  uint64_t t0 = 0;
-  for (uint32_t it = 1;; ++it) {
-    if (poll_ns) __nanosleep(poll_ns);
-    if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
-    if ((it & 1023u) == 0) {
-      const uint64_t now = gtimer();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        report_timeout(err_host, code);
-        return false;
-      }
-      if (*(volatile int*)err_host != 0) return false;  // another wait already failed: drain
-    }
-  }
-}
-
-// Wait until (*p >> 32) == epoch; returns the low 32 bits (or 0xffffffff on timeout).
-__device__ __forceinline__ uint32_t wait_epoch(const uint64_t* p, uint32_t epoch, uint64_t timeout_ns,
-                                               int* err_host, int code) {
-  uint64_t t0 = 0;
-  for (uint32_t it = 0;; ++it) {
-    const uint64_t v = ld_acquire_sys(p);
-    if ((uint32_t)(v >> 32) == epoch) return (uint32_t)v;
-    if ((it & 1023u) == 1023u) {
-      const uint64_t now = gtimer();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        report_timeout(err_host, code);
-        return 0xffffffffu;
-      }
-      if (*(volatile int*)err_host != 0) return 0xffffffffu;
-    }
-  }
-}
-
-// timeout codes: kind << 16 | lrank << 8 | pulse
-__device__ __forceinline__ int tcode(int kind, int lr, int p) { return (kind << 16) | (lr << 8) | p; }
-
-// ------------------------------------------------------------- per-CTA timing
-__device__ __forceinline__ void timer_start(unsigned flags, uint64_t* t_start) {
-  if ((flags & HALO_F_TIMERS) && threadIdx.x == 0) atomicMin((unsigned long long*)t_start, gtimer());
-}
-
-// Kernel epilogue: the last CTA publishes the sequence number (graph-safe) and timer span.
-__device__ __forceinline__ void finish_launch(unsigned flags, uint32_t* done, uint64_t* seq_slot, uint64_t seq,
-                                              uint64_t* t_start, uint64_t* t_end, uint64_t* span) {
-  if (threadIdx.x == 0) {
-    if (flags & HALO_F_TIMERS) atomicMax((unsigned long long*)t_end, gtimer());
-    uint32_t old = atom_add_acqrel_gpu(done, 1u);
-    if (old == gridDim.x - 1) {
-      *done = 0;
-      if (flags & HALO_F_TIMERS) {
-        *span = *t_end - *t_start;
-        *t_start = ~0ull;
-        *t_end = 0;
-      }
-      st_release_gpu(seq_slot, seq);
-    }
-  }
-}
 
 // ------------------------------------------------------------ exchange x (hot)
 template <int W>
@@ -565,7 +451,16 @@ __global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t ba
 }
 
 // ------------------------------------------------------------- host launchers
-static cudaError_t launch_coop(const void* fn, int grid, int block, void** args, cudaStream_t st) {
+static int coop_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HALO_COOP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
+cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -575,20 +470,20 @@ static cudaError_t launch_coop(const void* fn, int grid, int block, void** args,
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = coop_enabled() ? 1 : 0;
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStream_t st) {
   void* args[] = {(void*)&p};
   const void* fn = layout == 4 ? (const void*)k_exchange_x<4> : (const void*)k_exchange_x<3>;
-  return launch_coop(fn, grid, kThreads, args, st);
+  return launch_coop_kernel(fn, grid, kThreads, args, st);
 }
 
 cudaError_t launch_exchange_f(const ExParams& p, int layout, int grid, cudaStream_t st) {
   void* args[] = {(void*)&p};
   const void* fn = layout == 4 ? (const void*)k_exchange_f<4> : (const void*)k_exchange_f<3>;
-  return launch_coop(fn, grid, kThreads, args, st);
+  return launch_coop_kernel(fn, grid, kThreads, args, st);
 }
 
 cudaError_t max_coresident(int layout, int* x_blocks, int* f_blocks) {
@@ -615,7 +510,7 @@ cudaError_t launch_select(const SelParams& s, int n_local, cudaStream_t st) {
 
 cudaError_t launch_handshake(const HsParams& h, cudaStream_t st) {
   void* args[] = {(void*)&h};
-  return launch_coop((const void*)k_handshake, h.n_local, 32, args, st);
+  return launch_coop_kernel((const void*)k_handshake, h.n_local, 32, args, st);
 }
 
 cudaError_t launch_depmask(const RankDev* ranks, Ctrl* ctrl, int p, int map_stride, int n_local, cudaStream_t st) {
@@ -625,7 +520,7 @@ cudaError_t launch_depmask(const RankDev* ranks, Ctrl* ctrl, int p, int map_stri
 
 cudaError_t launch_status(const StatusParams& s, cudaStream_t st) {
   void* args[] = {(void*)&s};
-  return launch_coop((const void*)k_status, s.n_local, 64, args, st);
+  return launch_coop_kernel((const void*)k_status, s.n_local, 64, args, st);
 }
 
 cudaError_t launch_pack_x(int layout, const int32_t* map, int n, const float* x, float* out, int has_shift,

@@ -29,6 +29,9 @@ cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* 
                             double* fs_dim, cudaStream_t st);
 cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
+cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
+cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
+cudaError_t max_coresident_ll(int layout, int* x_blocks, int* f_blocks);
 }  // namespace halo
 
 using namespace halo;
@@ -77,7 +80,8 @@ struct halo_ctx {
   halo_config cfg{};
   int nranks = 0, n_local = 0, first_rank = 0, P = 0, W = 3;
   int pdim[kMaxP] = {0}, pk[kMaxP] = {0};
-  size_t map_stride = 0, fbuf_stride = 0, scratch_bytes = 0;
+  size_t map_stride = 0, fbuf_stride = 0, ll_stride = 0, scratch_bytes = 0;
+  bool ll = true;                   // LL protocol (default) vs the paper's flag protocol
   std::string last_error;
 
   // registered local buffers
@@ -103,6 +107,11 @@ struct halo_ctx {
   uint64_t* d_rtt = nullptr;
   int* err_host = nullptr;          // host-mapped error word
   int* err_dev = nullptr;
+  char* d_csr = nullptr;            // force-gather tasks + CSR of all local ranks (LL protocol)
+  size_t csr_bytes = 0;
+  std::vector<int32_t*> csr_task_row, csr_task_off;
+  std::vector<uint32_t*> csr_contrib;
+  std::vector<std::vector<int>> level_begin;  // [local][P+2]: task index where level P-1..0, home start
 
   // host plan
   std::vector<RankDev> h_ranks;
@@ -138,6 +147,11 @@ struct halo_ctx {
   float* fbuf_of(int r) const {
     return reinterpret_cast<float*>(peer_scratch[r] + kHdrBytes + (size_t)P * map_stride * sizeof(int32_t));
   }
+  uint64_t* xll_of(int r) const {
+    return reinterpret_cast<uint64_t*>(peer_scratch[r] + kHdrBytes + (size_t)P * map_stride * sizeof(int32_t) +
+                                       (size_t)P * fbuf_stride * sizeof(float));
+  }
+  uint64_t* fll_of(int r) const { return xll_of(r) + (size_t)P * ll_stride; }
 };
 
 // --------------------------------------------------------------------- helpers
@@ -158,6 +172,21 @@ static halo_status cuda_fail(halo_ctx* c, cudaError_t e, const char* where) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Scratch layout of one DD rank (halo_internal.h): header | maps | force
+// buffers (paper protocol) | coordinate LL buffers | force LL buffers.
+struct ScratchLayout {
+  size_t map_stride, fbuf_stride, ll_stride, total;
+};
+static ScratchLayout scratch_layout(int P, int capacity, int layout) {
+  ScratchLayout L;
+  L.map_stride = align_up((size_t)capacity, 64);                // int32 per pulse slot
+  L.fbuf_stride = align_up((size_t)capacity * layout, 64);      // fp32 per pulse slot
+  L.ll_stride = align_up((size_t)capacity * layout, 32);        // u64 units per pulse slot
+  L.total = kHdrBytes + (size_t)P * L.map_stride * sizeof(int32_t) + (size_t)P * L.fbuf_stride * sizeof(float) +
+            2 * (size_t)P * L.ll_stride * sizeof(uint64_t);
+  return L;
+}
+
 static halo_status check_err_word(halo_ctx* ctx) {
   if (ctx->err_host && *(volatile int*)ctx->err_host != 0) {
     char buf[128];
@@ -172,7 +201,7 @@ static halo_status check_err_word(halo_ctx* ctx) {
 static halo_status validate(const halo_config* c, std::string& why) {
   if (!c) { why = "cfg is NULL"; return HALO_ERR_ARG; }
   if (c->layout != 3 && c->layout != 4) { why = "layout must be 3 or 4"; return HALO_ERR_ARG; }
-  if (c->capacity <= 0) { why = "capacity must be > 0"; return HALO_ERR_ARG; }
+  if (c->capacity <= 0 || c->capacity >= (1 << 24)) { why = "capacity must be in (0, 2^24)"; return HALO_ERR_ARG; }
   if (c->nprocs < 1 || c->proc < 0 || c->proc >= c->nprocs) { why = "bad nprocs/proc"; return HALO_ERR_ARG; }
   long long nr = 1;
   int P = 0;
@@ -241,10 +270,14 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
         ctx->P++;
       }
   }
-  ctx->map_stride = align_up((size_t)cfg->capacity, 64);
-  ctx->fbuf_stride = align_up((size_t)cfg->capacity * cfg->layout, 64);
-  ctx->scratch_bytes = kHdrBytes + (size_t)ctx->P * ctx->map_stride * sizeof(int32_t) +
-                       (size_t)ctx->P * ctx->fbuf_stride * sizeof(float);
+  {
+    const ScratchLayout SL = scratch_layout(ctx->P, cfg->capacity, cfg->layout);
+    ctx->map_stride = SL.map_stride;
+    ctx->fbuf_stride = SL.fbuf_stride;
+    ctx->ll_stride = SL.ll_stride;
+    ctx->scratch_bytes = SL.total;
+  }
+  ctx->ll = !(cfg->flags & HALO_F_PAPER_FLAGS);
   ctx->x.assign(ctx->n_local, nullptr);
   ctx->f.assign(ctx->n_local, nullptr);
   ctx->scratch.assign(ctx->n_local, nullptr);
@@ -264,7 +297,9 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) { memset(ctx->err_host, 0, 64); e = cudaHostGetDevicePointer(&ctx->err_dev, ctx->err_host, 0); }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_small, 64 * 1024);
-  if (e == cudaSuccess) e = max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
+  if (e == cudaSuccess)
+    e = ctx->ll ? max_coresident_ll(cfg->layout, &ctx->max_x, &ctx->max_f)
+                : max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
   if (e != cudaSuccess) {
     // keep ctx to carry the message? The ABI returns NULL on error; print once.
     fprintf(stderr, "halo_init: %s\n", cudaGetErrorString(e));
@@ -294,9 +329,7 @@ halo_status halo_query_config(const halo_config* cfg, int* first_rank, int* n_lo
   if (first_rank) *first_rank = cfg->proc * nl;
   if (n_local) *n_local = nl;
   if (npulse) *npulse = P;
-  if (scratch_bytes)
-    *scratch_bytes = kHdrBytes + (size_t)P * align_up((size_t)cfg->capacity, 64) * sizeof(int32_t) +
-                     (size_t)P * align_up((size_t)cfg->capacity * cfg->layout, 64) * sizeof(float);
+  if (scratch_bytes) *scratch_bytes = scratch_layout(P, cfg->capacity, cfg->layout).total;
   return HALO_OK;
 }
 
@@ -444,6 +477,26 @@ static void fill_rank_dev(halo_ctx* ctx) {
     rd.n_home = ctx->n_home[l];
     rd.n_total = ctx->n_total[l];
     rd.rank = ctx->first_rank + l;
+    rd.xll = ctx->xll_of(rd.rank);
+    rd.fll = ctx->fll_of(rd.rank);
+    rd.task_row = l < (int)ctx->csr_task_row.size() ? ctx->csr_task_row[l] : nullptr;
+    rd.task_off = l < (int)ctx->csr_task_off.size() ? ctx->csr_task_off[l] : nullptr;
+    rd.contrib = l < (int)ctx->csr_contrib.size() ? ctx->csr_contrib[l] : nullptr;
+    rd.wrap_mask = 0;
+    for (int p = 0; p < kMaxP; ++p) {
+      rd.recv_off[p] = 0;
+      rd.recv_size[p] = 0;
+      rd.pulse_dim[p] = 0;
+    }
+    for (int p = 0; p < ctx->P; ++p) {
+      const int i = l * ctx->P + p;
+      if (i < (int)ctx->atom_offset.size()) {
+        rd.recv_off[p] = ctx->atom_offset[i];
+        rd.recv_size[p] = ctx->recv_size[i];
+      }
+      rd.pulse_dim[p] = ctx->pdim[p];
+      if (ctx->cell(rd.rank, ctx->pdim[p]) == 0) rd.wrap_mask |= 1 << p;
+    }
   }
 }
 
@@ -478,6 +531,8 @@ static void fill_pulse_dev(halo_ctx* ctx, int l, int p) {
   }
   pd.fdep = fdep;
   pd.chain = chain;
+  pd.xll_dst = ctx->xll_of(lower) + (size_t)p * ctx->ll_stride;
+  pd.fll_dst = ctx->fll_of(upper) + (size_t)p * ctx->ll_stride;
 }
 
 static void add_items(std::vector<Item>& v, int l, int p, uint8_t kind, int b, int e, int rows) {
@@ -533,6 +588,127 @@ static void build_f_items(halo_ctx* ctx) {
   }
 }
 
+// LL protocol x items: sends of independent entries (all pulses), sends of
+// dependent entries by pulse, then the receives (LL units -> x rows).
+static void build_x_items_ll(halo_ctx* ctx, int p_lo, int p_hi) {
+  auto& v = ctx->h_items_x;
+  v.clear();
+  const int R = ctx->item_rows;
+  for (int p = p_lo; p < p_hi; ++p)
+    for (int l = 0; l < ctx->n_local; ++l) add_items(v, l, p, kItemXIndep, 0, ctx->n_indep[l * ctx->P + p], R);
+  for (int p = p_lo; p < p_hi; ++p)
+    for (int l = 0; l < ctx->n_local; ++l) {
+      const int i = l * ctx->P + p;
+      add_items(v, l, p, kItemXDep, ctx->n_indep[i], ctx->send_size[i], R);
+    }
+  for (int p = p_lo; p < p_hi; ++p)
+    for (int l = 0; l < ctx->n_local; ++l) add_items(v, l, p, kItemXRecv, 0, ctx->recv_size[l * ctx->P + p], R);
+}
+
+// Force gather plan of every local rank (LL protocol), built on the host at the
+// NS step from the final maps: task rows in level order (slice rows of pulse
+// P-1, ..., of pulse 0, then home rows that receive forces) and, per task row,
+// its contributions (q, i) with map_q[i] == row, pulses descending (R15).
+static halo_status build_csr(halo_ctx* ctx, cudaStream_t st) {
+  const int L = ctx->n_local, P = ctx->P;
+  std::vector<std::vector<int32_t>> trow(L), toff(L);
+  std::vector<std::vector<uint32_t>> contrib(L);
+  ctx->level_begin.assign(L, std::vector<int>(P + 2, 0));
+  for (int l = 0; l < L; ++l) {
+    const int nt = ctx->n_total[l], nh = ctx->n_home[l];
+    std::vector<int> cnt(nt, 0);
+    std::vector<uint8_t> mask(nt, 0);
+    std::vector<std::vector<int32_t>> maps(P);
+    for (int q = 0; q < P; ++q) {
+      const int n = ctx->send_size[l * P + q];
+      maps[q].resize(n);
+      if (n)
+        CK(cudaMemcpyAsync(maps[q].data(), ctx->maps_of_local(l) + (size_t)q * ctx->map_stride, sizeof(int32_t) * n,
+                           cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (int q = 0; q < P; ++q)
+      for (int32_t t : maps[q]) {
+        cnt[t]++;
+        mask[t] |= (uint8_t)(1u << q);
+      }
+    std::vector<int32_t> task_of(nt, -1);
+    auto& tr = trow[l];
+    auto& lb = ctx->level_begin[l];
+    for (int k = 0; k < P; ++k) {  // level k = pulse P-1-k
+      const int p = P - 1 - k;
+      lb[k] = (int)tr.size();
+      const int a = ctx->atom_offset[l * P + p], n = ctx->recv_size[l * P + p];
+      for (int t = a; t < a + n; ++t) {
+        task_of[t] = (int)tr.size();
+        tr.push_back(t);
+      }
+    }
+    lb[P] = (int)tr.size();
+    for (int t = 0; t < nh; ++t)
+      if (cnt[t]) {
+        task_of[t] = (int)tr.size();
+        tr.push_back(t);
+      }
+    lb[P + 1] = (int)tr.size();
+    auto& to = toff[l];
+    to.assign(tr.size() + 1, 0);
+    for (size_t k = 0; k < tr.size(); ++k) to[k + 1] = to[k] + cnt[tr[k]];
+    auto& cb = contrib[l];
+    cb.assign(to.back(), 0u);
+    for (int q = 0; q < P; ++q)
+      for (size_t i = 0; i < maps[q].size(); ++i) {
+        const int t = maps[q][i];
+        if (task_of[t] < 0) return fail(ctx, HALO_ERR_ARG, "map entry targets a row with no gather task");
+        const int pos = __builtin_popcount((unsigned)mask[t] >> (q + 1));
+        cb[to[task_of[t]] + pos] = ((uint32_t)q << 24) | (uint32_t)i;
+      }
+  }
+  size_t need = 0;
+  for (int l = 0; l < L; ++l)
+    need += align_up(trow[l].size() * 4 + 4, 256) + align_up(toff[l].size() * 4, 256) +
+            align_up(contrib[l].size() * 4 + 4, 256);
+  if (need > ctx->csr_bytes) {
+    if (ctx->d_csr) CK(cudaFree(ctx->d_csr));
+    ctx->d_csr = nullptr;
+    CK(cudaMalloc(&ctx->d_csr, need));
+    ctx->csr_bytes = need;
+  }
+  ctx->csr_task_row.assign(L, nullptr);
+  ctx->csr_task_off.assign(L, nullptr);
+  ctx->csr_contrib.assign(L, nullptr);
+  char* cur = ctx->d_csr;
+  for (int l = 0; l < L; ++l) {
+    ctx->csr_task_row[l] = reinterpret_cast<int32_t*>(cur);
+    if (!trow[l].empty())
+      CK(cudaMemcpyAsync(cur, trow[l].data(), trow[l].size() * 4, cudaMemcpyHostToDevice, st));
+    cur += align_up(trow[l].size() * 4 + 4, 256);
+    ctx->csr_task_off[l] = reinterpret_cast<int32_t*>(cur);
+    CK(cudaMemcpyAsync(cur, toff[l].data(), toff[l].size() * 4, cudaMemcpyHostToDevice, st));
+    cur += align_up(toff[l].size() * 4, 256);
+    ctx->csr_contrib[l] = reinterpret_cast<uint32_t*>(cur);
+    if (!contrib[l].empty())
+      CK(cudaMemcpyAsync(cur, contrib[l].data(), contrib[l].size() * 4, cudaMemcpyHostToDevice, st));
+    cur += align_up(contrib[l].size() * 4 + 4, 256);
+  }
+  CK(cudaStreamSynchronize(st));
+  return HALO_OK;
+}
+
+// LL protocol f items: gather tasks level by level (slice of pulse P-1 first),
+// home rows last: every wait targets a strictly earlier level.
+static void build_f_items_ll(halo_ctx* ctx) {
+  auto& v = ctx->h_items_f;
+  v.clear();
+  const int R = ctx->item_rows, P = ctx->P;
+  for (int k = 0; k <= P; ++k)
+    for (int l = 0; l < ctx->n_local; ++l) {
+      const auto& lb = ctx->level_begin[l];
+      const uint8_t level = k < P ? (uint8_t)(P - 1 - k) : kHomeLevel;
+      add_items(v, l, level, kItemGather, lb[k], lb[k + 1], R);
+    }
+}
+
 static halo_status upload_plan(halo_ctx* ctx) {
   const size_t a = 256;
   const size_t nr = align_up(sizeof(RankDev) * ctx->n_local, a);
@@ -580,6 +756,7 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.fshift = nullptr;
   P.accumulate = 1;
   P.poll_ns = ctx->poll_ns;
+  P.ll_stride = ctx->ll_stride;
   return P;
 }
 
@@ -756,10 +933,16 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     for (int l = 0; l < L; ++l)
       for (int q = 0; q <= p; ++q) fill_pulse_dev(ctx, l, q);
     fill_rank_dev(ctx);
-    build_x_items(ctx, p, p + 1);
+    if (ctx->ll)
+      build_x_items_ll(ctx, p, p + 1);
+    else
+      build_x_items(ctx, p, p + 1);
     if ((s = upload_plan(ctx)) != HALO_OK) return s;
     ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
-    CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
+    if (ctx->ll)
+      CK(launch_exchange_x_ll(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
+    else
+      CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
     CK(cudaStreamSynchronize(st));
     if ((s = check_err_word(ctx)) != HALO_OK) return s;
   }
@@ -787,9 +970,15 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   // final plan: all pulses
   for (int l = 0; l < L; ++l)
     for (int p = 0; p < P; ++p) fill_pulse_dev(ctx, l, p);
+  if (ctx->ll) {
+    if ((s = build_csr(ctx, st)) != HALO_OK) return s;
+    build_x_items_ll(ctx, 0, P);
+    build_f_items_ll(ctx);
+  } else {
+    build_x_items(ctx, 0, P);
+    build_f_items(ctx);
+  }
   fill_rank_dev(ctx);
-  build_x_items(ctx, 0, P);
-  build_f_items(ctx);
   if ((s = upload_plan(ctx)) != HALO_OK) return s;
   ctx->maps_ready = true;
   ctx->x_done = true;  // set_maps exchanged every pulse's coordinates
@@ -851,7 +1040,11 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   ctx->x_done = true;
   if (ctx->P == 0) return HALO_OK;
   ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, 0, ctx->P);
-  CK(launch_exchange_x(X, ctx->W, grid_for(ctx->n_items_x, ctx->n_local, ctx->max_x), (cudaStream_t)stream));
+  const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->max_x);
+  if (ctx->ll)
+    CK(launch_exchange_x_ll(X, ctx->W, grid, (cudaStream_t)stream));
+  else
+    CK(launch_exchange_x(X, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
 }
 
@@ -865,7 +1058,11 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   ExParams F = make_params(ctx, ctx->d_items_f, ctx->n_items_f, 0, ctx->P);
   F.fshift = fshift;
   F.accumulate = accumulate ? 1 : 0;
-  CK(launch_exchange_f(F, ctx->W, grid_for(ctx->n_items_f, ctx->n_local, ctx->max_f), (cudaStream_t)stream));
+  const int grid = grid_for(ctx->n_items_f, ctx->n_local, ctx->max_f);
+  if (ctx->ll)
+    CK(launch_exchange_f_ll(F, ctx->W, grid, (cudaStream_t)stream));
+  else
+    CK(launch_exchange_f(F, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
 }
 
@@ -981,6 +1178,7 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_fshift_tmp) (void)cudaFree(ctx->d_fshift_tmp);
   if (ctx->d_small) (void)cudaFree(ctx->d_small);
   if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
+  if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
   if (ctx->err_host) (void)cudaFreeHost(ctx->err_host);
   (void)cudaGetLastError();
   delete ctx;

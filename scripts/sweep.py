@@ -26,6 +26,8 @@ VARIANTS = {
     "rows2048": ({"HALO_ITEM_ROWS": "2048"}, 0),
     "gpufence": ({}, 4),
     "atomic": ({}, 1),
+    "nocoop": ({"HALO_COOP": "0"}, 0),
+    "nocoop_gpufence": ({"HALO_COOP": "0"}, 4),
 }
 
 
@@ -53,6 +55,25 @@ def main():
     cap = int(max(len(h) for h in homes) * 2.2) + 4096
     dev = torch.device("cuda", local)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    # reference: back-to-back tiny torch kernels (launch floor of a plain launch)
+    tiny = torch.zeros(1, device=dev)
+    st0 = torch.cuda.current_stream()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(200)]
+    for k in range(220):
+        kk = k - 20
+        if kk >= 0:
+            evs[kk][0].record(st0)
+        tiny.add_(1.0)
+        if kk >= 0:
+            evs[kk][1].record(st0)
+        tiny.add_(1.0)
+        if kk >= 0:
+            evs[kk][2].record(st0)
+    torch.cuda.synchronize()
+    if rank == 0:
+        print(json.dumps({"variant": "torch_tiny_kernel", "us": round(float(np.mean(
+            [e[0].elapsed_time(e[1]) * 1e3 for e in evs])), 2), "us2": round(float(np.mean(
+            [e[1].elapsed_time(e[2]) * 1e3 for e in evs])), 2)}), flush=True)
     for name in args.variants.split(","):
         env, flags = VARIANTS[name]
         saved = {k: os.environ.get(k) for k in env}

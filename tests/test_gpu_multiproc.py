@@ -49,16 +49,20 @@ def _worker(rank, world, port, cases, out):
         out[rank] = traceback.format_exc()
 
 
-CASES = [
+PAPER = 1 << 4
+CASES = [  # (config, seed, forces, flags, layout, steps); flags 0 = LL protocol
     ("C1", 1, "int", 0, 3, 2),
     ("W3", 1, "int", 0, 3, 1),
     ("T3D", 2, "normal", 0, 3, 2),
     ("C2", 1, "normal", 0, 3, 2),
     ("C3", 1, "int", 0, 3, 3),
-    ("C3", 2, "normal", 4, 3, 2),    # HALO_F_GPU_FENCE (paper's signalling scheme)
     ("C5", 1, "normal", 0, 3, 2),
     ("T2P", 1, "int", 0, 4, 2),
-    ("C3", 3, "int", 1, 3, 2),       # HALO_F_ATOMIC_UNPACK, integer forces: exact
+    ("C1", 2, "int", PAPER, 3, 2),
+    ("C3", 2, "normal", PAPER, 3, 2),
+    ("C3", 2, "normal", PAPER | 4, 3, 2),   # + HALO_F_GPU_FENCE (paper's exact fence scheme)
+    ("C5", 1, "normal", PAPER, 3, 2),
+    ("C3", 3, "int", PAPER | 1, 3, 2),      # + HALO_F_ATOMIC_UNPACK, integer forces: exact
 ]
 
 

@@ -12,6 +12,9 @@ from tests.parity_common import Case, run_gpu_case, bits
 
 pytestmark = pytest.mark.gpu
 
+PAPER = 1 << 4  # HALO_F_PAPER_FLAGS: the paper's per-pulse flag protocol; 0 = LL protocol (default)
+PROTOS = [pytest.param(0, id="ll"), pytest.param(PAPER, id="paper")]
+
 
 def session_for(case, flags=0, layout=None, capacity=None):
     from paper_2509_21527_b200.session import HaloSession
@@ -19,35 +22,39 @@ def session_for(case, flags=0, layout=None, capacity=None):
                        capacity=capacity or case.capacity, device=0, flags=flags, timeout_s=5.0)
 
 
+@pytest.mark.parametrize("proto", PROTOS)
 @pytest.mark.parametrize("name", ["W1", "W2", "W3", "C1", "T3D", "T2P", "T2D", "T4x2", "C2", "C5", "C3"])
-def test_parity_int_forces(name):
+def test_parity_int_forces(name, proto):
     case = Case(name, seed=1, force_kind="int")
-    sess = session_for(case)
+    sess = session_for(case, flags=proto)
     run_gpu_case(case, sess, steps=2)
     sess.destroy()
 
 
+@pytest.mark.parametrize("proto", PROTOS)
 @pytest.mark.parametrize("name", ["C1", "T3D", "T2P", "C2", "C5", "C3"])
 @pytest.mark.parametrize("seed", [2, 3])
-def test_parity_real_forces(name, seed):
+def test_parity_real_forces(name, seed, proto):
     case = Case(name, seed=seed, force_kind="normal")
-    sess = session_for(case)
+    sess = session_for(case, flags=proto)
     run_gpu_case(case, sess)
     sess.destroy()
 
 
+@pytest.mark.parametrize("proto", PROTOS)
 @pytest.mark.parametrize("name", ["W2", "T3D", "T2P", "C2"])
-def test_parity_float4(name):
+def test_parity_float4(name, proto):
     case = Case(name, seed=1, layout=4, force_kind="normal")
-    sess = session_for(case)
+    sess = session_for(case, flags=proto)
     run_gpu_case(case, sess)
     sess.destroy()
 
 
+@pytest.mark.parametrize("proto", PROTOS)
 @pytest.mark.parametrize("name", ["T3D", "T2P", "C3"])
-def test_parity_explicit_maps(name):
+def test_parity_explicit_maps(name, proto):
     case = Case(name, seed=2, force_kind="int")
-    sess = session_for(case)
+    sess = session_for(case, flags=proto)
     run_gpu_case(case, sess, use_explicit=True)
     sess.destroy()
 
@@ -56,7 +63,7 @@ def test_parity_explicit_maps(name):
 def test_parity_atomic_unpack(name, kind):
     from paper_2509_21527_b200 import HALO_F_ATOMIC_UNPACK
     case = Case(name, seed=1, force_kind=kind)
-    sess = session_for(case, flags=HALO_F_ATOMIC_UNPACK)
+    sess = session_for(case, flags=HALO_F_ATOMIC_UNPACK | PAPER)
     run_gpu_case(case, sess, atomic=(kind != "int"))
     sess.destroy()
 
@@ -65,7 +72,7 @@ def test_parity_atomic_unpack(name, kind):
 def test_parity_paper_fence_variant(name):
     from paper_2509_21527_b200 import HALO_F_GPU_FENCE
     case = Case(name, seed=3, force_kind="int")
-    sess = session_for(case, flags=HALO_F_GPU_FENCE)
+    sess = session_for(case, flags=HALO_F_GPU_FENCE | PAPER)
     run_gpu_case(case, sess, steps=3)
     sess.destroy()
 
@@ -95,11 +102,12 @@ def test_moved_coordinates_between_ns_steps():
     sess.destroy()
 
 
-def test_cuda_graph_replay():
+@pytest.mark.parametrize("proto", PROTOS)
+def test_cuda_graph_replay(proto):
     """x+f captured once into a CUDA graph and replayed: the device-resident
     sequence numbers keep every replay correct."""
     case = Case("C3", seed=2, force_kind="int")
-    sess = session_for(case)
+    sess = session_for(case, flags=proto)
     run_gpu_case(case, sess)
     s = torch.cuda.Stream()
     fshift = torch.zeros(sess.n_local, 3, 3, dtype=torch.float64, device=sess.device)
@@ -226,9 +234,10 @@ def test_errors():
     sess.destroy()
 
 
-def test_accumulate_false_single_pulse():
+@pytest.mark.parametrize("proto", PROTOS)
+def test_accumulate_false_single_pulse(proto):
     case = Case("C1", seed=1, force_kind="int")
-    sess = session_for(case)
+    sess = session_for(case, flags=proto)
     run_gpu_case(case, sess, check_forces=False)
     from oracle import force_halo
     Fo, _ = force_halo(case.states, [f.copy() for f in case.F], accumulate=False)
@@ -241,10 +250,11 @@ def test_accumulate_false_single_pulse():
     sess.destroy()
 
 
-def test_timers_and_many_steps():
+@pytest.mark.parametrize("proto", PROTOS)
+def test_timers_and_many_steps(proto):
     from paper_2509_21527_b200 import HALO_F_TIMERS
     case = Case("C2", seed=1, force_kind="int")
-    sess = session_for(case, flags=HALO_F_TIMERS)
+    sess = session_for(case, flags=HALO_F_TIMERS | proto)
     run_gpu_case(case, sess, check_forces=True)
     for _ in range(200):
         sess.exchange_x()
