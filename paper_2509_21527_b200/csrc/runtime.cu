@@ -125,7 +125,7 @@ struct halo_ctx {
   uint32_t epoch = 0;
   uint64_t ping_base = 0;
   int max_x = 0, max_f = 0;
-  int item_rows = 512;
+  int item_rows = 128;
   uint32_t poll_ns = 0;
 
   int cell(int r, int d) const {

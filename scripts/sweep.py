@@ -21,7 +21,12 @@ VARIANTS = {
     "base": ({}, 0),
     "poll64": ({"HALO_POLL_NS": "64"}, 0),
     "poll256": ({"HALO_POLL_NS": "256"}, 0),
+    "rows32": ({"HALO_ITEM_ROWS": "32"}, 0),
+    "rows64": ({"HALO_ITEM_ROWS": "64"}, 0),
     "rows128": ({"HALO_ITEM_ROWS": "128"}, 0),
+    "rows256": ({"HALO_ITEM_ROWS": "256"}, 0),
+    "paper": ({}, 16),
+    "paper_gpufence": ({}, 16 | 4),
     "rows1024": ({"HALO_ITEM_ROWS": "1024"}, 0),
     "rows2048": ({"HALO_ITEM_ROWS": "2048"}, 0),
     "gpufence": ({}, 4),
