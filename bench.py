@@ -296,13 +296,17 @@ def run_fused(args, rank, world, local):
     # latency floor: peer flag ping-pong between process 0 and process 1
     floor = None
     if world > 1:
-        t0 = None
+        t0 = t0r = None
         if rank in (0, 1):
             peer = sess.first_rank + sess.n_local if rank == 0 else 0
-            t0 = sess.halo.floor_pingpong(peer, iters=10000)
+            t0 = sess.halo.floor_pingpong(peer, iters=10000, relaxed=False)
+            t0r = sess.halo.floor_pingpong(peer, iters=10000, relaxed=True)
         barrier()
         t0 = max_over_ranks(t0 or 0.0)
-        floor = {"t0_one_way_us": t0}
+        t0r = max_over_ranks(t0r or 0.0)
+        floor = {"t0_one_way_us": t0r, "t0_release_acquire_us": t0,
+                 "note": "t0 = relaxed 8-B peer store seen by a relaxed poll (the LL unit); median of 1e4 "
+                         "round trips / 2"}
 
     # algorithmic bytes per launch (this GPU), DESIGN.md "Roofline"
     rows_x = sum(sum(lay[l]["send_size"]) for l in range(nl))

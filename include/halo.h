@@ -208,10 +208,12 @@ HALO_API halo_status halo_unpack_f_pulse(halo_ctx* ctx, int local, int pulse, co
 HALO_API halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns);
 
 /* Floors (measurement): ping-pong `iters` round trips of a
- * system-scope release/acquire flag between this process's local rank 0 and
- * DD rank `peer_rank` (COLLECTIVE between the two processes only; other
- * processes must not call).  *one_way_us = median round trip / 2. */
-HALO_API halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, double* one_way_us);
+ * 64-bit flag between this process's local rank 0 and DD rank `peer_rank`
+ * (COLLECTIVE between the two processes only; other processes must not call).
+ * relaxed = 0: st.release.sys / ld.acquire.sys (the paper's signal);
+ * relaxed = 1: st.relaxed.sys / ld.relaxed.sys (the LL protocol's unit).
+ * *one_way_us = median round trip / 2 (initiator; 0 on the responder). */
+HALO_API halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, int relaxed, double* one_way_us);
 
 /* Host-block until all work this ctx enqueued is done; surfaces device error
  * words (HALO_ERR_TIMEOUT) and CUDA errors. */

@@ -69,7 +69,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_pack_x_pulse": ([P, c_int, c_int, P, P], c_int),
         "halo_unpack_f_pulse": ([P, c_int, c_int, P, P, c_int, P], c_int),
         "halo_get_timers": ([P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
-        "halo_floor_pingpong": ([P, c_int, c_int, POINTER(c_double)], c_int),
+        "halo_floor_pingpong": ([P, c_int, c_int, c_int, POINTER(c_double)], c_int),
         "halo_sync": ([P], c_int),
         "halo_strerror": ([c_int], c_char_p),
         "halo_last_error": ([P], c_char_p),

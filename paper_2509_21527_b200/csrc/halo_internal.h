@@ -74,19 +74,9 @@ struct RankDev {
   ScratchHdr* hdr;          // own scratch header
   int32_t* maps;            // own maps region (P slots of map_stride ints)
   float* fbuf;              // own force receive buffers (P slots of fbuf_stride floats)
-  uint64_t* xll;            // own coordinate LL receive buffers (P slots of ll_stride units)
-  uint64_t* fll;            // own force LL receive buffers (P slots of ll_stride units)
-  // force gather (LL protocol): task rows in level order, CSR of contributions
-  const int32_t* task_row;  // [n_tasks] row index
-  const int32_t* task_off;  // [n_tasks + 1] contribution offsets
-  const uint32_t* contrib;  // (q << 24) | i, pulses descending per row (R15)
   int n_home;
   int n_total;
   int rank;                 // global DD rank
-  int wrap_mask;            // bit p set iff this rank shifts in pulse p
-  int recv_off[kMaxP];      // own receive range of each pulse
-  int recv_size[kMaxP];
-  int pulse_dim[kMaxP];
   int pad;
 };
 
@@ -126,6 +116,42 @@ struct Item {
   uint32_t end;
 };
 
+// LL protocol work records: each CTA loads one 128-B record (one coalesced
+// line) that carries every pointer it needs, so a cold-L2 launch pays one
+// round trip for its plan instead of a chain of dependent loads.
+struct __align__(128) XRec {
+  uint8_t kind;             // kItemXIndep / kItemXDep / kItemXRecv
+  uint8_t pulse;
+  uint16_t lrank;
+  uint32_t n_units;         // rows * layout
+  float shift[3];           // +L_d on the dim axis, 0 elsewhere (R25)
+  uint32_t has_shift;
+  const int32_t* map;       // send: map_p + begin
+  const float* x;           // send: own x base
+  uint64_t* ll;             // send: receiver's LL slot p + begin*W; recv: own LL slot p + begin*W
+  float* xdst;              // recv: own x + (recv_off_p + begin)*W
+  const uint64_t* xll_own;  // dep send: own coordinate LL base (slot q at + q*ll_stride)
+  int32_t recv_off[kMaxP];  // dep send: own receive ranges
+  int32_t recv_size[kMaxP];
+};
+static_assert(sizeof(XRec) == 128, "XRec must be one 128-B line");
+
+struct __align__(128) GRec {
+  uint8_t kind;             // kItemGather
+  uint8_t level;            // slice of this pulse, or kHomeLevel
+  uint16_t lrank;
+  uint32_t n_units;         // tasks * layout
+  uint32_t wrap_mask;       // pulses this rank shifted in (fshift, R13)
+  uint8_t pulse_dim[8];
+  uint32_t pad;
+  const int4* tasks;        // 32-B task records (row, n, contrib[6]) + begin
+  float* f;                 // own f base
+  const uint64_t* fll_own;  // own force LL base (slot q at + q*ll_stride)
+  uint64_t* push;           // slice rows: x-sender's LL slot p minus recv_off_p*W (index by row*W + c)
+  uint8_t pad2[128 - 56];
+};
+static_assert(sizeof(GRec) == 128, "GRec must be one 128-B line");
+
 struct ExParams {
   const RankDev* ranks;
   const PulseDev* pulses;   // [n_local * P]
@@ -142,6 +168,8 @@ struct ExParams {
   int accumulate;
   uint32_t poll_ns;         // __nanosleep between flag polls (0 = tight spin)
   uint64_t ll_stride;       // u64 units per pulse slot of the LL receive buffers
+  const XRec* xrec;         // LL protocol work records (x)
+  const GRec* grec;         // LL protocol work records (f)
 };
 
 struct SelParams {

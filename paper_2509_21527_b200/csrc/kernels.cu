@@ -433,19 +433,31 @@ __global__ void k_unpack_f(const int32_t* __restrict__ map, int n, const float* 
 }
 
 // --------------------------------------------------------------- latency floor
-__global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator,
+__global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                            uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   for (int i = 1; i <= iters; ++i) {
     const uint64_t v = base + (uint64_t)i;
+    const uint64_t t0 = gtimer();
     if (initiator) {
-      const uint64_t t0 = gtimer();
-      st_release_sys(peer, v);
-      if (!wait_geq<true>(own, v, timeout_ns, err_host, tcode(9, 0, 0))) return;
+      if (relaxed) st_relaxed_sys(peer, v); else st_release_sys(peer, v);
+    }
+    if (relaxed) {
+      uint64_t t1 = 0;
+      for (uint32_t it = 1; ld_relaxed_sys(own) < v; ++it) {
+        if ((it & 1023u) == 0) {
+          const uint64_t now = gtimer();
+          if (t1 == 0) t1 = now;
+          else if (now - t1 > timeout_ns) { report_timeout(err_host, tcode(9, initiator, 1)); return; }
+        }
+      }
+    } else if (!wait_geq<true>(own, v, timeout_ns, err_host, tcode(9, initiator, 0))) {
+      return;
+    }
+    if (initiator) {
       rtt_ns[i - 1] = gtimer() - t0;
     } else {
-      if (!wait_geq<true>(own, v, timeout_ns, err_host, tcode(9, 1, 0))) return;
-      st_release_sys(peer, v);
+      if (relaxed) st_relaxed_sys(peer, v); else st_release_sys(peer, v);
     }
   }
 }
@@ -545,9 +557,9 @@ cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator,
+cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st) {
-  k_pingpong<<<1, 32, 0, st>>>(own, peer, iters, base, initiator, rtt_ns, timeout_ns, err_host);
+  k_pingpong<<<1, 32, 0, st>>>(own, peer, iters, base, initiator, relaxed, rtt_ns, timeout_ns, err_host);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,8 @@
 //     and a halo slice row is pushed back as soon as it is final (Alg. 5
 //     DEP_MGMT at row granularity).  Bit-exact with the oracle, no atomics.
 //
+// Each CTA loads one 128-B work record (XRec / GRec) per item: after an L2
+// flush the plan costs one memory round trip, not a chain of dependent loads.
 // Items are processed in a static order in which every wait targets an
 // earlier item, and the grid is launched cooperatively.
 #include <cuda_runtime.h>
@@ -27,81 +29,90 @@ __device__ __forceinline__ uint64_t ll_pack(float v, uint32_t tag) {
   return ((uint64_t)tag << 32) | (uint64_t)__float_as_uint(v);
 }
 
-// Poll one LL unit until it carries `tag`; bounded like every other wait.
-__device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
+// Slow path: poll one LL unit until it carries `tag`; bounded like every wait.
+__device__ __noinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
                                          int code) {
-  uint64_t v = ld_relaxed_sys(u);
-  if ((uint32_t)(v >> 32) == tag) return __uint_as_float((uint32_t)v);
   uint64_t t0 = 0;
   for (uint32_t it = 1;; ++it) {
-    v = ld_relaxed_sys(u);
-    if ((uint32_t)(v >> 32) == tag) return __uint_as_float((uint32_t)v);
+    const uint64_t v = ld_relaxed_sys(u);
+    if ((uint32_t)(v >> 32) == tag) return v;
     if ((it & 1023u) == 0) {
       const uint64_t now = gtimer();
       if (t0 == 0) {
         t0 = now;
       } else if (now - t0 > timeout_ns) {
         report_timeout(err_host, code);
-        return __uint_as_float((uint32_t)v);
+        return v;
       }
-      if (*(volatile int*)err_host != 0) return __uint_as_float((uint32_t)v);
+      if (*(volatile int*)err_host != 0) return v;
     }
   }
+}
+
+__device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
+                                         int code) {
+  uint64_t v = ld_relaxed_sys(u);
+  if ((uint32_t)(v >> 32) != tag) v = ll_spin(u, tag, timeout_ns, err_host, code);
+  return __uint_as_float((uint32_t)v);
+}
+
+// Cooperative load of one 128-B record into shared memory (one coalesced line).
+template <class Rec>
+__device__ __forceinline__ void load_rec(Rec* dst, const Rec* src) {
+  if (threadIdx.x < 32)
+    reinterpret_cast<uint32_t*>(dst)[threadIdx.x] = __ldg(reinterpret_cast<const uint32_t*>(src) + threadIdx.x);
 }
 
 // ---------------------------------------------------------------- x (LL)
 template <int W>
 __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constant__ ExParams P) {
+  __shared__ XRec r;
   __shared__ uint64_t s_seq;
   Ctrl* ctrl = P.ctrl;
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
-  __syncthreads();
-  const uint64_t seq = s_seq;
-  const uint32_t tag = (uint32_t)seq;
-
+  uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    const Item w = P.items[it];
-    const RankDev& rd = P.ranks[w.lrank];
-    const uint32_t u0 = w.begin * W, u1 = w.end * W;
-    if (w.kind == kItemXRecv) {
-      // this rank's halo rows of pulse p: LL units -> x rows [recv_off, +recv_size)
-      const uint64_t* src = rd.xll + (size_t)w.pulse * P.ll_stride;
-      float* dst = rd.x + (size_t)rd.recv_off[w.pulse] * W;
-      for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x)
-        dst[u] = ll_wait(src + u, tag, P.timeout_ns, P.err_host, tcode(10, w.lrank, w.pulse));
-      continue;
-    }
-    // SEND: gather through the map, shift (R25), tag, store into the receiver's LL buffer
-    const PulseDev& pd = P.pulses[w.lrank * P.P + w.pulse];
-    const int32_t* __restrict__ map = pd.map;
-    const float* __restrict__ x = rd.x;
-    uint64_t* dst = pd.xll_dst;
-    const bool dep = (w.kind == kItemXDep);
-    const bool sh = pd.has_shift != 0;
-    for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-      const uint32_t i = u / W;
-      const int c = (int)(u - i * W);
-      const int idx = __ldg(map + i);
-      float v;
-      if (!dep) {
-        v = __ldg(x + (size_t)idx * W + c);  // home row: never written during the kernel
-      } else {
-        // forwarded row: find the pulse it arrived in (Alg. 4 dependent part, R8/R9)
-        int q = 0;
-        while (q < P.P - 1 && (unsigned)(idx - rd.recv_off[q]) >= (unsigned)rd.recv_size[q]) ++q;
-        if (q < P.p_lo) {
-          v = __ldcg(x + (size_t)idx * W + c);  // arrived in an earlier launch (set_maps)
+    load_rec(&r, P.xrec + it);
+    __syncthreads();
+    seq = s_seq;
+    const uint32_t tag = (uint32_t)seq;
+    const uint32_t n = r.n_units;
+    if (r.kind == kItemXRecv) {
+      // this rank's halo rows of one pulse: LL units -> x rows
+      for (uint32_t u = threadIdx.x; u < n; u += blockDim.x)
+        r.xdst[u] = ll_wait(r.ll + u, tag, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse));
+    } else {
+      // SEND: gather through the map, shift (R25), tag, store into the receiver's LL slot
+      const bool dep = r.kind == kItemXDep;
+      for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) {
+        const uint32_t i = u / W;
+        const int c = (int)(u - i * W);
+        const int idx = __ldg(r.map + i);
+        float v;
+        if (!dep) {
+          v = __ldg(r.x + (size_t)idx * W + c);  // home row: never written during the kernel
         } else {
-          const uint64_t* src = rd.xll + (size_t)q * P.ll_stride + (size_t)(idx - rd.recv_off[q]) * W + c;
-          v = ll_wait(src, tag, P.timeout_ns, P.err_host, tcode(11, w.lrank, q));
+          // forwarded row: the pulse it arrived in (Alg. 4 dependent part, R8/R9)
+          int q = 0;
+          while (q < P.P - 1 && (unsigned)(idx - r.recv_off[q]) >= (unsigned)r.recv_size[q]) ++q;
+          if (q < P.p_lo) {
+            v = __ldcg(r.x + (size_t)idx * W + c);  // arrived in an earlier launch (set_maps)
+          } else {
+            const uint64_t* src = r.xll_own + (size_t)q * P.ll_stride + (size_t)(idx - r.recv_off[q]) * W + c;
+            v = ll_wait(src, tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, q));
+          }
         }
+        if (r.has_shift && c < 3) v = __fadd_rn(v, r.shift[c]);
+        st_relaxed_sys(r.ll + u, ll_pack(v, tag));
       }
-      if (sh && c < 3) v = __fadd_rn(v, pd.shift[c]);
-      st_relaxed_sys(dst + u, ll_pack(v, tag));
     }
+    __syncthreads();
   }
-  __syncthreads();
+  if (seq == 0) {  // CTA without items
+    __syncthreads();
+    seq = s_seq;
+  }
   finish_launch(P.flags, &ctrl->done_x, &ctrl->seq_x, seq, &ctrl->t_start_x, &ctrl->t_end_x, &ctrl->span_x);
 }
 
@@ -113,71 +124,81 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 template <int W>
-__global__ void __launch_bounds__(kThreads) k_exchange_f_ll(const __grid_constant__ ExParams P) {
+__global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
+  __shared__ GRec g;
   __shared__ uint64_t s_seq;
   Ctrl* ctrl = P.ctrl;
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
   timer_start(P.flags, &ctrl->t_start_f);
-  __syncthreads();
-  const uint64_t seq = s_seq;
-  const uint32_t tag = (uint32_t)seq;
-
+  uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    const Item w = P.items[it];
-    const RankDev& rd = P.ranks[w.lrank];
-    const int level = w.pulse;  // pulse whose slice these rows are, or kHomeLevel
-    const bool push = level != kHomeLevel;
-    uint64_t* pdst = nullptr;
-    int poff = 0;
-    if (push) {
-      const PulseDev& pd = P.pulses[w.lrank * P.P + level];
-      pdst = pd.fll_dst;
-      poff = rd.recv_off[level];
-    }
-    const int wrap = (P.fshift != nullptr) ? rd.wrap_mask : 0;
-    double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-    float* __restrict__ f = rd.f;
-    const uint32_t u0 = w.begin * W, u1 = w.end * W;
-    for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-      const uint32_t k = u / W;
-      const int c = (int)(u - k * W);
-      const int t = __ldg(rd.task_row + k);
-      const int j0 = __ldg(rd.task_off + k), j1 = __ldg(rd.task_off + k + 1);
-      float v = f[(size_t)t * W + c];
-      for (int j = j0; j < j1; ++j) {  // contributions, pulses descending (R15)
-        const uint32_t cc = __ldg(rd.contrib + j);
-        const int q = (int)(cc >> 24);
-        const uint32_t i = cc & 0xffffffu;
-        const float val = ll_wait(rd.fll + (size_t)q * P.ll_stride + (size_t)i * W + c, tag, P.timeout_ns,
-                                  P.err_host, tcode(12, w.lrank, q));
-        v = P.accumulate ? __fadd_rn(v, val) : val;
-        if (((wrap >> q) & 1) && c < 3) {
-          const int d = rd.pulse_dim[q];
+    load_rec(&g, P.grec + it);
+    __syncthreads();
+    seq = s_seq;
+    const uint32_t tag = (uint32_t)seq;
+    const uint32_t n = g.n_units;
+    const bool push = g.level != kHomeLevel;
+    const uint32_t wrap = (P.fshift != nullptr) ? g.wrap_mask : 0u;
+    // stride = a multiple of W, so every thread keeps one component c
+    const uint32_t S = (blockDim.x / W) * W;
+    const int c = (int)(threadIdx.x % W);
+    double acc[3] = {0.0, 0.0, 0.0};  // fshift partial sums of component c, per dim
+    if (threadIdx.x < S) {
+      for (uint32_t u = threadIdx.x; u < n; u += S) {
+        const uint32_t k = u / W;
+        const int4 a = __ldg(g.tasks + 2 * k);
+        const int4 b = __ldg(g.tasks + 2 * k + 1);
+        const int t = a.x, m = a.y;
+        const uint32_t cc[kMaxP] = {(uint32_t)a.z, (uint32_t)a.w, (uint32_t)b.x,
+                                    (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
+        float v = g.f[(size_t)t * W + c];
+        // issue every contribution's load at once, then resolve stragglers
+        uint64_t w[kMaxP];
 #pragma unroll
-          for (int dd = 0; dd < 3; ++dd)
+        for (int j = 0; j < kMaxP; ++j)
+          if (j < m)
+            w[j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride +
+                                  (size_t)(cc[j] & 0xffffffu) * W + c);
 #pragma unroll
-            for (int cc2 = 0; cc2 < 3; ++cc2)
-              if (dd == d && cc2 == c) acc[dd][cc2] += (double)val;
+        for (int j = 0; j < kMaxP; ++j) {
+          if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
+            const int q = (int)(cc[j] >> 24);
+            if ((uint32_t)(w[j] >> 32) != tag)
+              w[j] = ll_spin(g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
+                             P.timeout_ns, P.err_host, tcode(12, g.lrank, q));
+            const float val = __uint_as_float((uint32_t)w[j]);
+            v = P.accumulate ? __fadd_rn(v, val) : val;
+            if ((wrap >> q) & 1u) {
+              const int d = g.pulse_dim[q];
+              if (d == 0) acc[0] += (double)val;
+              else if (d == 1) acc[1] += (double)val;
+              else acc[2] += (double)val;
+            }
+          }
         }
+        g.f[(size_t)t * W + c] = v;
+        if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
       }
-      f[(size_t)t * W + c] = v;
-      if (push) st_relaxed_sys(pdst + (size_t)(t - poff) * W + c, ll_pack(v, tag));
     }
     if (wrap) {  // shift forces (R13): warp-reduce, one fp64 atomic per (dim, comp) per warp
-      double* fs = P.fshift + 9 * w.lrank;
+      double* fs = P.fshift + 9 * g.lrank;
       for (int d = 0; d < 3; ++d) {
         bool has = false;
-        for (int q = 0; q < P.P; ++q) has |= ((wrap >> q) & 1) && rd.pulse_dim[q] == d;
+        for (int q = 0; q < P.P; ++q) has |= ((wrap >> q) & 1u) && g.pulse_dim[q] == d;
         if (!has) continue;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double s = warp_sum_d(acc[d][c]);
-          if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(fs + 3 * d + c, s);
+        for (int c2 = 0; c2 < 3; ++c2) {
+          const double s = warp_sum_d((c == c2 && threadIdx.x < S) ? acc[d] : 0.0);
+          if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(fs + 3 * d + c2, s);
         }
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
+  if (seq == 0) {
+    __syncthreads();
+    seq = s_seq;
+  }
   finish_launch(P.flags, &ctrl->done_f, &ctrl->seq_f, seq, &ctrl->t_start_f, &ctrl->t_end_f, &ctrl->span_f);
 }
 

@@ -27,7 +27,7 @@ cudaError_t launch_pack_x(int layout, const int32_t* map, int n, const float* x,
                           const float* shift, cudaStream_t st);
 cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* buf, float* f, int accumulate,
                             double* fs_dim, cudaStream_t st);
-cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator,
+cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
 cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
 cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
@@ -109,8 +109,11 @@ struct halo_ctx {
   int* err_dev = nullptr;
   char* d_csr = nullptr;            // force-gather tasks + CSR of all local ranks (LL protocol)
   size_t csr_bytes = 0;
-  std::vector<int32_t*> csr_task_row, csr_task_off;
-  std::vector<uint32_t*> csr_contrib;
+  std::vector<int4*> csr_tasks;     // per local rank: 32-B task records (row, n, contrib[6])
+  std::vector<XRec> h_xrec;
+  std::vector<GRec> h_grec;
+  XRec* d_xrec = nullptr;
+  GRec* d_grec = nullptr;
   std::vector<std::vector<int>> level_begin;  // [local][P+2]: task index where level P-1..0, home start
 
   // host plan
@@ -477,26 +480,6 @@ static void fill_rank_dev(halo_ctx* ctx) {
     rd.n_home = ctx->n_home[l];
     rd.n_total = ctx->n_total[l];
     rd.rank = ctx->first_rank + l;
-    rd.xll = ctx->xll_of(rd.rank);
-    rd.fll = ctx->fll_of(rd.rank);
-    rd.task_row = l < (int)ctx->csr_task_row.size() ? ctx->csr_task_row[l] : nullptr;
-    rd.task_off = l < (int)ctx->csr_task_off.size() ? ctx->csr_task_off[l] : nullptr;
-    rd.contrib = l < (int)ctx->csr_contrib.size() ? ctx->csr_contrib[l] : nullptr;
-    rd.wrap_mask = 0;
-    for (int p = 0; p < kMaxP; ++p) {
-      rd.recv_off[p] = 0;
-      rd.recv_size[p] = 0;
-      rd.pulse_dim[p] = 0;
-    }
-    for (int p = 0; p < ctx->P; ++p) {
-      const int i = l * ctx->P + p;
-      if (i < (int)ctx->atom_offset.size()) {
-        rd.recv_off[p] = ctx->atom_offset[i];
-        rd.recv_size[p] = ctx->recv_size[i];
-      }
-      rd.pulse_dim[p] = ctx->pdim[p];
-      if (ctx->cell(rd.rank, ctx->pdim[p]) == 0) rd.wrap_mask |= 1 << p;
-    }
   }
 }
 
@@ -664,32 +647,32 @@ static halo_status build_csr(halo_ctx* ctx, cudaStream_t st) {
         cb[to[task_of[t]] + pos] = ((uint32_t)q << 24) | (uint32_t)i;
       }
   }
+  // pack 32-B task records: row, n, contrib[0..5] (pulses descending)
+  std::vector<std::vector<int32_t>> rec(L);
+  for (int l = 0; l < L; ++l) {
+    auto& r = rec[l];
+    r.assign(trow[l].size() * 8 + 8, 0);
+    for (size_t k = 0; k < trow[l].size(); ++k) {
+      const int n = toff[l][k + 1] - toff[l][k];
+      r[8 * k] = trow[l][k];
+      r[8 * k + 1] = n;
+      for (int j = 0; j < n; ++j) r[8 * k + 2 + j] = (int32_t)contrib[l][toff[l][k] + j];
+    }
+  }
   size_t need = 0;
-  for (int l = 0; l < L; ++l)
-    need += align_up(trow[l].size() * 4 + 4, 256) + align_up(toff[l].size() * 4, 256) +
-            align_up(contrib[l].size() * 4 + 4, 256);
+  for (int l = 0; l < L; ++l) need += align_up(rec[l].size() * 4, 256);
   if (need > ctx->csr_bytes) {
     if (ctx->d_csr) CK(cudaFree(ctx->d_csr));
     ctx->d_csr = nullptr;
     CK(cudaMalloc(&ctx->d_csr, need));
     ctx->csr_bytes = need;
   }
-  ctx->csr_task_row.assign(L, nullptr);
-  ctx->csr_task_off.assign(L, nullptr);
-  ctx->csr_contrib.assign(L, nullptr);
+  ctx->csr_tasks.assign(L, nullptr);
   char* cur = ctx->d_csr;
   for (int l = 0; l < L; ++l) {
-    ctx->csr_task_row[l] = reinterpret_cast<int32_t*>(cur);
-    if (!trow[l].empty())
-      CK(cudaMemcpyAsync(cur, trow[l].data(), trow[l].size() * 4, cudaMemcpyHostToDevice, st));
-    cur += align_up(trow[l].size() * 4 + 4, 256);
-    ctx->csr_task_off[l] = reinterpret_cast<int32_t*>(cur);
-    CK(cudaMemcpyAsync(cur, toff[l].data(), toff[l].size() * 4, cudaMemcpyHostToDevice, st));
-    cur += align_up(toff[l].size() * 4, 256);
-    ctx->csr_contrib[l] = reinterpret_cast<uint32_t*>(cur);
-    if (!contrib[l].empty())
-      CK(cudaMemcpyAsync(cur, contrib[l].data(), contrib[l].size() * 4, cudaMemcpyHostToDevice, st));
-    cur += align_up(contrib[l].size() * 4 + 4, 256);
+    ctx->csr_tasks[l] = reinterpret_cast<int4*>(cur);
+    CK(cudaMemcpyAsync(cur, rec[l].data(), rec[l].size() * 4, cudaMemcpyHostToDevice, st));
+    cur += align_up(rec[l].size() * 4, 256);
   }
   CK(cudaStreamSynchronize(st));
   return HALO_OK;
@@ -709,13 +692,74 @@ static void build_f_items_ll(halo_ctx* ctx) {
     }
 }
 
+// 128-B work records of the LL kernels, one per item (halo_internal.h XRec/GRec).
+static void build_xrec(halo_ctx* ctx) {
+  const int W = ctx->W, P = ctx->P;
+  ctx->h_xrec.assign(ctx->h_items_x.size(), XRec{});
+  for (size_t k = 0; k < ctx->h_items_x.size(); ++k) {
+    const Item& w = ctx->h_items_x[k];
+    XRec& r = ctx->h_xrec[k];
+    memset(&r, 0, sizeof r);
+    const int l = w.lrank, p = w.pulse, rk = ctx->first_rank + l;
+    const PulseDev& pd = ctx->h_pulses[l * P + p];
+    r.kind = w.kind;
+    r.pulse = (uint8_t)p;
+    r.lrank = (uint16_t)l;
+    r.n_units = (w.end - w.begin) * W;
+    for (int c = 0; c < 3; ++c) r.shift[c] = pd.shift[c];
+    r.has_shift = pd.has_shift;
+    r.x = ctx->x[l];
+    r.xll_own = ctx->xll_of(rk);
+    for (int q = 0; q < kMaxP; ++q) {
+      r.recv_off[q] = q < P ? ctx->atom_offset[l * P + q] : 0;
+      r.recv_size[q] = q < P ? ctx->recv_size[l * P + q] : 0;
+    }
+    if (w.kind == kItemXRecv) {
+      r.ll = ctx->xll_of(rk) + (size_t)p * ctx->ll_stride + (size_t)w.begin * W;
+      r.xdst = ctx->x[l] + (size_t)(ctx->atom_offset[l * P + p] + w.begin) * W;
+    } else {
+      r.map = pd.map + w.begin;
+      r.ll = pd.xll_dst + (size_t)w.begin * W;
+    }
+  }
+}
+
+static void build_grec(halo_ctx* ctx) {
+  const int W = ctx->W, P = ctx->P;
+  ctx->h_grec.assign(ctx->h_items_f.size(), GRec{});
+  for (size_t k = 0; k < ctx->h_items_f.size(); ++k) {
+    const Item& w = ctx->h_items_f[k];
+    GRec& g = ctx->h_grec[k];
+    memset(&g, 0, sizeof g);
+    const int l = w.lrank, rk = ctx->first_rank + l;
+    g.kind = kItemGather;
+    g.level = w.pulse;
+    g.lrank = (uint16_t)l;
+    g.n_units = (w.end - w.begin) * W;
+    g.wrap_mask = 0;
+    for (int q = 0; q < P; ++q) {
+      g.pulse_dim[q] = (uint8_t)ctx->pdim[q];
+      if (ctx->cell(rk, ctx->pdim[q]) == 0) g.wrap_mask |= 1u << q;
+    }
+    g.tasks = ctx->csr_tasks[l] + 2 * (size_t)w.begin;
+    g.f = ctx->f[l];
+    g.fll_own = ctx->fll_of(rk);
+    if (w.pulse != kHomeLevel) {
+      const PulseDev& pd = ctx->h_pulses[l * P + w.pulse];
+      g.push = pd.fll_dst - (ptrdiff_t)ctx->atom_offset[l * P + w.pulse] * W;
+    }
+  }
+}
+
 static halo_status upload_plan(halo_ctx* ctx) {
   const size_t a = 256;
   const size_t nr = align_up(sizeof(RankDev) * ctx->n_local, a);
   const size_t np = align_up(sizeof(PulseDev) * std::max(1, ctx->n_local * ctx->P), a);
   const size_t nx = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_x.size()), a);
   const size_t nf = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_f.size()), a);
-  const size_t need = nr + np + nx + nf;
+  const size_t nxr = align_up(sizeof(XRec) * std::max<size_t>(1, ctx->h_xrec.size()), a);
+  const size_t ngr = align_up(sizeof(GRec) * std::max<size_t>(1, ctx->h_grec.size()), a);
+  const size_t need = nr + np + nx + nf + nxr + ngr;
   if (need > ctx->plan_bytes) {
     if (ctx->plan) CK(cudaFree(ctx->plan));
     ctx->plan = nullptr;
@@ -726,6 +770,12 @@ static halo_status upload_plan(halo_ctx* ctx) {
   ctx->d_pulses = reinterpret_cast<PulseDev*>(ctx->plan + nr);
   ctx->d_items_x = reinterpret_cast<Item*>(ctx->plan + nr + np);
   ctx->d_items_f = reinterpret_cast<Item*>(ctx->plan + nr + np + nx);
+  ctx->d_xrec = reinterpret_cast<XRec*>(ctx->plan + nr + np + nx + nf);
+  ctx->d_grec = reinterpret_cast<GRec*>(ctx->plan + nr + np + nx + nf + nxr);
+  if (!ctx->h_xrec.empty())
+    CK(cudaMemcpy(ctx->d_xrec, ctx->h_xrec.data(), sizeof(XRec) * ctx->h_xrec.size(), cudaMemcpyHostToDevice));
+  if (!ctx->h_grec.empty())
+    CK(cudaMemcpy(ctx->d_grec, ctx->h_grec.data(), sizeof(GRec) * ctx->h_grec.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_ranks, ctx->h_ranks.data(), sizeof(RankDev) * ctx->n_local, cudaMemcpyHostToDevice));
   if (ctx->P)
     CK(cudaMemcpy(ctx->d_pulses, ctx->h_pulses.data(), sizeof(PulseDev) * ctx->n_local * ctx->P,
@@ -757,6 +807,8 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.accumulate = 1;
   P.poll_ns = ctx->poll_ns;
   P.ll_stride = ctx->ll_stride;
+  P.xrec = ctx->d_xrec;
+  P.grec = ctx->d_grec;
   return P;
 }
 
@@ -933,10 +985,12 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     for (int l = 0; l < L; ++l)
       for (int q = 0; q <= p; ++q) fill_pulse_dev(ctx, l, q);
     fill_rank_dev(ctx);
-    if (ctx->ll)
+    if (ctx->ll) {
       build_x_items_ll(ctx, p, p + 1);
-    else
+      build_xrec(ctx);
+    } else {
       build_x_items(ctx, p, p + 1);
+    }
     if ((s = upload_plan(ctx)) != HALO_OK) return s;
     ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
     if (ctx->ll)
@@ -974,7 +1028,11 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     if ((s = build_csr(ctx, st)) != HALO_OK) return s;
     build_x_items_ll(ctx, 0, P);
     build_f_items_ll(ctx);
+    build_xrec(ctx);
+    build_grec(ctx);
   } else {
+    ctx->h_xrec.clear();
+    ctx->h_grec.clear();
     build_x_items(ctx, 0, P);
     build_f_items(ctx);
   }
@@ -1125,7 +1183,7 @@ halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
   return HALO_OK;
 }
 
-halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, double* one_way_us) {
+halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, int relaxed, double* one_way_us) {
   if (!ctx || peer_rank < 0 || peer_rank >= ctx->nranks || iters <= 0) return HALO_ERR_ARG;
   if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
   const int me = ctx->first_rank;
@@ -1142,7 +1200,7 @@ halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, double*
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   uint64_t* own = &ctx->hdr_of(me)->ping;
   uint64_t* peer = &ctx->hdr_of(peer_rank)->ping;
-  CK(launch_pingpong(own, peer, iters, ctx->ping_base, initiator ? 1 : 0, ctx->d_rtt,
+  CK(launch_pingpong(own, peer, iters, ctx->ping_base, initiator ? 1 : 0, relaxed ? 1 : 0, ctx->d_rtt,
                      (uint64_t)(ctx->cfg.timeout_s * 1e9), ctx->err_dev, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaStreamDestroy(st));

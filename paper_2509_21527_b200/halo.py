@@ -177,9 +177,9 @@ class Halo:
         self._ck(self.lib.halo_get_timers(self.h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
-    def floor_pingpong(self, peer_rank, iters=10000) -> float:
+    def floor_pingpong(self, peer_rank, iters=10000, relaxed=False) -> float:
         v = c_double()
-        self._ck(self.lib.halo_floor_pingpong(self.h, int(peer_rank), int(iters), ctypes.byref(v)))
+        self._ck(self.lib.halo_floor_pingpong(self.h, int(peer_rank), int(iters), int(bool(relaxed)), ctypes.byref(v)))
         return v.value
 
     def sync(self):
