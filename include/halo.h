@@ -207,6 +207,12 @@ HALO_API halo_status halo_unpack_f_pulse(halo_ctx* ctx, int local, int pulse, co
  * durations in ns (max end - min start over the CTAs), read after halo_sync. */
 HALO_API halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns);
 
+/* Per-CTA device timestamps of the last exchange_x (which = 0) or exchange_f
+ * (which = 1) launch, HALO_F_TIMERS only (the paper's %globaltimer
+ * instrumentation): out[4*i .. 4*i+3] = CTA i's [start, plan record
+ * loaded, items done, exit] in ns; *n = CTAs recorded (<= cap/4).  Synchronises. */
+HALO_API halo_status halo_get_trace(halo_ctx* ctx, int which, uint64_t* out, int cap, int* n);
+
 /* Floors (measurement): ping-pong `iters` round trips of a
  * 64-bit flag between this process's local rank 0 and DD rank `peer_rank`
  * (COLLECTIVE between the two processes only; other processes must not call).

@@ -26,6 +26,7 @@ constexpr int kMaxLocal = HALO_MAX_LOCAL;
 constexpr int kMaxRanks = HALO_MAX_RANKS;
 constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
 constexpr int kHdrBytes = 4096;
+constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
 struct __align__(128) ScratchHdr {
@@ -64,6 +65,9 @@ struct Ctrl {
   int32_t n_total[kMaxLocal];
   int32_t err[kMaxLocal];                 // set_maps error bits (kErr*)
   int32_t agreed_err[kMaxLocal];          // OR over all ranks after the status exchange
+  // HALO_F_TIMERS: per-CTA %globaltimer stamps of the last x (0) / f (1) launch:
+  // [start, plan record loaded, items done, exit]
+  uint64_t trace[2][kTraceCTAs][4];
 };
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };

@@ -69,12 +69,15 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
   __shared__ XRec r;
   __shared__ uint64_t s_seq;
   Ctrl* ctrl = P.ctrl;
+  const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
+  if (trace) ctrl->trace[0][blockIdx.x][0] = gtimer();
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
     load_rec(&r, P.xrec + it);
     __syncthreads();
+    if (trace && seq == 0) ctrl->trace[0][blockIdx.x][1] = gtimer();
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     const uint32_t n = r.n_units;
@@ -113,7 +116,9 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
     __syncthreads();
     seq = s_seq;
   }
+  if (trace) ctrl->trace[0][blockIdx.x][2] = gtimer();
   finish_launch(P.flags, &ctrl->done_x, &ctrl->seq_x, seq, &ctrl->t_start_x, &ctrl->t_end_x, &ctrl->span_x);
+  if (trace) ctrl->trace[0][blockIdx.x][3] = gtimer();
 }
 
 // ---------------------------------------------------------------- f (LL)
@@ -127,13 +132,17 @@ template <int W>
 __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
   __shared__ GRec g;
   __shared__ uint64_t s_seq;
+  __shared__ double s_fs[kThreads / 32][9];
   Ctrl* ctrl = P.ctrl;
+  const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
+  if (trace) ctrl->trace[1][blockIdx.x][0] = gtimer();
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
   timer_start(P.flags, &ctrl->t_start_f);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
     load_rec(&g, P.grec + it);
     __syncthreads();
+    if (trace && seq == 0) ctrl->trace[1][blockIdx.x][1] = gtimer();
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     const uint32_t n = g.n_units;
@@ -180,17 +189,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
         if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
       }
     }
-    if (wrap) {  // shift forces (R13): warp-reduce, one fp64 atomic per (dim, comp) per warp
-      double* fs = P.fshift + 9 * g.lrank;
-      for (int d = 0; d < 3; ++d) {
-        bool has = false;
-        for (int q = 0; q < P.P; ++q) has |= ((wrap >> q) & 1u) && g.pulse_dim[q] == d;
-        if (!has) continue;
+    if (wrap) {  // shift forces (R13): warp-reduce, CTA-reduce, one fp64 atomic per (dim, comp) per item
+      for (int d = 0; d < 3; ++d)
 #pragma unroll
         for (int c2 = 0; c2 < 3; ++c2) {
           const double s = warp_sum_d((c == c2 && threadIdx.x < S) ? acc[d] : 0.0);
-          if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(fs + 3 * d + c2, s);
+          if ((threadIdx.x & 31) == 0) s_fs[threadIdx.x >> 5][3 * d + c2] = s;
         }
+      __syncthreads();
+      if (threadIdx.x < 9) {
+        double s = 0.0;
+        for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) s += s_fs[wv][threadIdx.x];
+        if (s != 0.0) atomicAdd(P.fshift + 9 * g.lrank + threadIdx.x, s);
       }
     }
     __syncthreads();
@@ -199,7 +209,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
     __syncthreads();
     seq = s_seq;
   }
+  if (trace) ctrl->trace[1][blockIdx.x][2] = gtimer();
   finish_launch(P.flags, &ctrl->done_f, &ctrl->seq_f, seq, &ctrl->t_start_f, &ctrl->t_end_f, &ctrl->span_f);
+  if (trace) ctrl->trace[1][blockIdx.x][3] = gtimer();
 }
 
 // ------------------------------------------------------------- launchers

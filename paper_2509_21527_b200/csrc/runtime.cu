@@ -128,6 +128,7 @@ struct halo_ctx {
   uint32_t epoch = 0;
   uint64_t ping_base = 0;
   int max_x = 0, max_f = 0;
+  int last_grid[2] = {0, 0};
   int item_rows = 128;
   uint32_t poll_ns = 0;
 
@@ -1099,6 +1100,7 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   if (ctx->P == 0) return HALO_OK;
   ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, 0, ctx->P);
   const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->max_x);
+  ctx->last_grid[0] = grid;
   if (ctx->ll)
     CK(launch_exchange_x_ll(X, ctx->W, grid, (cudaStream_t)stream));
   else
@@ -1117,6 +1119,7 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   F.fshift = fshift;
   F.accumulate = accumulate ? 1 : 0;
   const int grid = grid_for(ctx->n_items_f, ctx->n_local, ctx->max_f);
+  ctx->last_grid[1] = grid;
   if (ctx->ll)
     CK(launch_exchange_f_ll(F, ctx->W, grid, (cudaStream_t)stream));
   else
@@ -1180,6 +1183,17 @@ halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
   CK(cudaMemcpy(v, &ctx->ctrl->span_x, sizeof v, cudaMemcpyDeviceToHost));
   if (x_ns) *x_ns = v[0];
   if (f_ns) *f_ns = v[1];
+  return HALO_OK;
+}
+
+halo_status halo_get_trace(halo_ctx* ctx, int which, uint64_t* out, int cap, int* n) {
+  if (!ctx || which < 0 || which > 1 || !out || !n) return HALO_ERR_ARG;
+  const int m = std::min(std::min(ctx->last_grid[which], kTraceCTAs), cap / 4);
+  *n = m;
+  if (m <= 0) return HALO_OK;
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 4 * m, cudaMemcpyDeviceToHost));
   return HALO_OK;
 }
 

@@ -177,6 +177,14 @@ class Halo:
         self._ck(self.lib.halo_get_timers(self.h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    def get_trace(self, which):
+        """Per-CTA [start, record loaded, items done, exit] ns of the last x (0) / f (1) launch."""
+        cap = 4 * 2048
+        buf = (c_uint64 * cap)()
+        n = c_int()
+        self._ck(self.lib.halo_get_trace(self.h, int(which), buf, cap, ctypes.byref(n)))
+        return np.array(buf[: 4 * n.value], dtype=np.uint64).reshape(-1, 4)
+
     def floor_pingpong(self, peer_rank, iters=10000, relaxed=False) -> float:
         v = c_double()
         self._ck(self.lib.halo_floor_pingpong(self.h, int(peer_rank), int(iters), int(bool(relaxed)), ctypes.byref(v)))

@@ -1,0 +1,97 @@
+"""Per-CTA device timeline of one x+f step (HALO_F_TIMERS trace), after W warm-up steps.
+
+    python scripts/trace.py --config C3 [--flush]
+    torchrun --nproc-per-node 2 scripts/trace.py --config C1 --flush
+
+Prints, per kernel, quantiles (µs, relative to the x kernel's first CTA start)
+of CTA start / plan-record loaded / items done / exit, and the gap between the
+x kernel's last exit and the f kernel's first start.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def q(a):
+    return [round(float(v), 2) for v in np.quantile(a, [0.0, 0.5, 0.9, 1.0])]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--flush", action="store_true")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--flags", type=int, default=0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    import bench
+    from paper_2509_21527_b200 import HALO_F_TIMERS
+    from paper_2509_21527_b200.session import HaloSession, assign_home
+    from synth import forces_normal
+    c, X = bench.build_workload(args.config)
+    homes = assign_home(X, c.L, c.grid)
+    cap = int(max(len(h) for h in homes) * 2.2) + 4096
+    dev = torch.device("cuda", local)
+    sess = HaloSession(c.grid, c.L, c.rc, c.pulses, capacity=cap, device=local, flags=HALO_F_TIMERS | args.flags,
+                       nprocs=world, proc=rank, timeout_s=20.0)
+    first, nl = sess.first_rank, sess.n_local
+    sess.load_home([X[homes[first + l]] for l in range(nl)])
+    sess.set_maps()
+    F0 = [torch.from_numpy(forces_normal(sess.layout_of(l)["n_total"], 1 + l)).to(dev) for l in range(nl)]
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream()
+    out = []
+    for k in range(args.steps):
+        for l in range(nl):
+            sess.f[l][: F0[l].shape[0]].copy_(F0[l])
+        if args.flush:
+            flush.fill_(1.0)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(st)
+        sess.exchange_x()
+        e1.record(st)
+        sess.exchange_f(fshift=fshift)
+        e2.record(st)
+        torch.cuda.synchronize()
+        tx = sess.halo.get_trace(0).astype(np.int64)
+        tf = sess.halo.get_trace(1).astype(np.int64)
+        t0 = tx[:, 0].min()
+        res = {
+            "step": k, "rank": rank, "x_event_us": round(e0.elapsed_time(e1) * 1e3, 2),
+            "f_event_us": round(e1.elapsed_time(e2) * 1e3, 2), "x_ctas": int(tx.shape[0]), "f_ctas": int(tf.shape[0]),
+            "x_start": q((tx[:, 0] - t0) / 1e3), "x_rec": q((tx[:, 1] - t0) / 1e3),
+            "x_done": q((tx[:, 2] - t0) / 1e3), "x_exit": q((tx[:, 3] - t0) / 1e3),
+            "gap_x_exit_to_f_start": round(float((tf[:, 0].min() - tx[:, 3].max()) / 1e3), 2),
+            "f_start": q((tf[:, 0] - t0) / 1e3), "f_rec": q((tf[:, 1] - t0) / 1e3),
+            "f_done": q((tf[:, 2] - t0) / 1e3), "f_exit": q((tf[:, 3] - t0) / 1e3),
+        }
+        out.append(res)
+    if world > 1:
+        allres = [None] * world
+        dist.all_gather_object(allres, out[-1])
+    else:
+        allres = [out[-1]]
+    if rank == 0:
+        for r in allres:
+            print(json.dumps(r), flush=True)
+    sess.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
