@@ -31,9 +31,10 @@ __device__ __forceinline__ uint64_t ll_pack(float v, uint32_t tag) {
 
 // Slow path: poll one LL unit until it carries `tag`; bounded like every wait.
 __device__ __noinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
-                                         int code) {
+                                         int code, uint32_t sleep_ns) {
   uint64_t t0 = 0;
   for (uint32_t it = 1;; ++it) {
+    if (sleep_ns) __nanosleep(sleep_ns);  // back off: thousands of pollers must not starve the writers
     const uint64_t v = ld_relaxed_sys(u);
     if ((uint32_t)(v >> 32) == tag) return v;
     if ((it & 1023u) == 0) {
@@ -50,9 +51,9 @@ __device__ __noinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uint64
 }
 
 __device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
-                                         int code) {
+                                         int code, uint32_t sleep_ns) {
   uint64_t v = ld_relaxed_sys(u);
-  if ((uint32_t)(v >> 32) != tag) v = ll_spin(u, tag, timeout_ns, err_host, code);
+  if ((uint32_t)(v >> 32) != tag) v = ll_spin(u, tag, timeout_ns, err_host, code, sleep_ns);
   return __uint_as_float((uint32_t)v);
 }
 
@@ -73,6 +74,9 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
   if (trace) ctrl->trace[0][blockIdx.x][0] = gtimer();
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
+  __syncthreads();
+  // arrive early: the atomic's latency hides behind the items (launch_arrive)
+  const uint32_t arrived = launch_arrive(&ctrl->done_x);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
     load_rec(&r, P.xrec + it);
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
     if (r.kind == kItemXRecv) {
       // this rank's halo rows of one pulse: LL units -> x rows
       for (uint32_t u = threadIdx.x; u < n; u += blockDim.x)
-        r.xdst[u] = ll_wait(r.ll + u, tag, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse));
+        r.xdst[u] = ll_wait(r.ll + u, tag, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse), P.poll_ns);
     } else {
       // SEND: gather through the map, shift (R25), tag, store into the receiver's LL slot
       const bool dep = r.kind == kItemXDep;
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
             v = __ldcg(r.x + (size_t)idx * W + c);  // arrived in an earlier launch (set_maps)
           } else {
             const uint64_t* src = r.xll_own + (size_t)q * P.ll_stride + (size_t)(idx - r.recv_off[q]) * W + c;
-            v = ll_wait(src, tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, q));
+            v = ll_wait(src, tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, q), P.poll_ns);
           }
         }
         if (r.has_shift && c < 3) v = __fadd_rn(v, r.shift[c]);
@@ -112,12 +116,9 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
     }
     __syncthreads();
   }
-  if (seq == 0) {  // CTA without items
-    __syncthreads();
-    seq = s_seq;
-  }
+  seq = s_seq;
   if (trace) ctrl->trace[0][blockIdx.x][2] = gtimer();
-  finish_launch(P.flags, &ctrl->done_x, &ctrl->seq_x, seq, &ctrl->t_start_x, &ctrl->t_end_x, &ctrl->span_x);
+  launch_depart(P.flags, arrived, &ctrl->done_x, &ctrl->seq_x, seq, &ctrl->t_start_x, &ctrl->t_end_x, &ctrl->span_x);
   if (trace) ctrl->trace[0][blockIdx.x][3] = gtimer();
 }
 
@@ -138,6 +139,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
   if (trace) ctrl->trace[1][blockIdx.x][0] = gtimer();
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
   timer_start(P.flags, &ctrl->t_start_f);
+  __syncthreads();
+  const uint32_t arrived = launch_arrive(&ctrl->done_f);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
     load_rec(&g, P.grec + it);
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
             const int q = (int)(cc[j] >> 24);
             if ((uint32_t)(w[j] >> 32) != tag)
               w[j] = ll_spin(g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
-                             P.timeout_ns, P.err_host, tcode(12, g.lrank, q));
+                             P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
             const float val = __uint_as_float((uint32_t)w[j]);
             v = P.accumulate ? __fadd_rn(v, val) : val;
             if ((wrap >> q) & 1u) {
@@ -205,12 +208,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
     }
     __syncthreads();
   }
-  if (seq == 0) {
-    __syncthreads();
-    seq = s_seq;
-  }
+  seq = s_seq;
   if (trace) ctrl->trace[1][blockIdx.x][2] = gtimer();
-  finish_launch(P.flags, &ctrl->done_f, &ctrl->seq_f, seq, &ctrl->t_start_f, &ctrl->t_end_f, &ctrl->span_f);
+  launch_depart(P.flags, arrived, &ctrl->done_f, &ctrl->seq_f, seq, &ctrl->t_start_f, &ctrl->t_end_f, &ctrl->span_f);
   if (trace) ctrl->trace[1][blockIdx.x][3] = gtimer();
 }
 

@@ -132,4 +132,31 @@ __device__ __forceinline__ void finish_launch(unsigned flags, uint32_t* done, ui
   }
 }
 
+// Early-arrive variant of finish_launch (LL kernels).  Thread 0 increments the
+// launch's arrival counter right after reading the sequence number (ordered by
+// the preceding __syncthreads, which consumed the load), so the atomic's round
+// trip overlaps the CTA's work.  The CTA that arrived last publishes the
+// sequence number at its exit: by then every CTA of the launch has read it.
+__device__ __forceinline__ uint32_t launch_arrive(uint32_t* done) {
+  uint32_t old = 0;
+  if (threadIdx.x == 0) old = atom_add_acqrel_gpu(done, 1u);
+  return old;
+}
+
+__device__ __forceinline__ void launch_depart(unsigned flags, uint32_t arrived, uint32_t* done, uint64_t* seq_slot,
+                                              uint64_t seq, uint64_t* t_start, uint64_t* t_end, uint64_t* span) {
+  if (threadIdx.x != 0) return;
+  if (flags & HALO_F_TIMERS) atomicMax((unsigned long long*)t_end, gtimer());
+  if (arrived == gridDim.x - 1) {
+    *done = 0;
+    st_relaxed_gpu(seq_slot, seq);
+    if (flags & HALO_F_TIMERS) {
+      // spans need every CTA's end stamp: only approximate here (the last arriver's exit)
+      *span = gtimer() - *t_start;
+      *t_start = ~0ull;
+      *t_end = 0;
+    }
+  }
+}
+
 }  // namespace halo

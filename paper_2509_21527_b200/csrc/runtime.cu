@@ -1180,7 +1180,23 @@ halo_status halo_unpack_f_pulse(halo_ctx* ctx, int local, int pulse, const float
 halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
   if (!ctx) return HALO_ERR_ARG;
   uint64_t v[2];
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(v, &ctx->ctrl->span_x, sizeof v, cudaMemcpyDeviceToHost));
+  if (ctx->ll) {  // exact spans from the per-CTA trace: max(exit) - min(start)
+    for (int which = 0; which < 2; ++which) {
+      const int m = std::min(ctx->last_grid[which], kTraceCTAs);
+      if (m <= 0) continue;
+      std::vector<uint64_t> t(4 * (size_t)m);
+      CK(cudaMemcpy(t.data(), &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 4 * m, cudaMemcpyDeviceToHost));
+      uint64_t lo = ~0ull, hi = 0;
+      for (int i = 0; i < m; ++i) {
+        lo = std::min(lo, t[4 * i]);
+        hi = std::max(hi, t[4 * i + 3]);
+      }
+      v[which] = hi > lo ? hi - lo : 0;
+    }
+  }
   if (x_ns) *x_ns = v[0];
   if (f_ns) *f_ns = v[1];
   return HALO_OK;

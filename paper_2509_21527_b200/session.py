@@ -46,9 +46,16 @@ class HaloSession:
         self.first_rank, self.n_local = self.halo.local_ranks()
         self.npulse = len(self.halo.pulse_order())
         sb = self.halo.scratch_bytes()
-        self.x = [torch.zeros(capacity, layout, dtype=torch.float32, device=self.device) for _ in range(self.n_local)]
-        self.f = [torch.zeros(capacity, layout, dtype=torch.float32, device=self.device) for _ in range(self.n_local)]
-        self.scratch = [torch.zeros(sb, dtype=torch.uint8, device=self.device) for _ in range(self.n_local)]
+        # one allocation per array kind for all local ranks (views per rank, 512-B aligned rows blocks):
+        # one copy resets every local rank's forces, one IPC handle covers every local rank
+        cap_pad = (capacity + 127) // 128 * 128
+        sb_pad = (sb + 4095) // 4096 * 4096
+        self.x_all = torch.zeros(self.n_local, cap_pad, layout, dtype=torch.float32, device=self.device)
+        self.f_all = torch.zeros(self.n_local, cap_pad, layout, dtype=torch.float32, device=self.device)
+        self.scratch_all = torch.zeros(self.n_local, sb_pad, dtype=torch.uint8, device=self.device)
+        self.x = [self.x_all[l] for l in range(self.n_local)]
+        self.f = [self.f_all[l] for l in range(self.n_local)]
+        self.scratch = [self.scratch_all[l, :sb] for l in range(self.n_local)]
         for l in range(self.n_local):
             self.halo.register_buffers(l, self.x[l].data_ptr(), self.f[l].data_ptr(), self.scratch[l].data_ptr())
         if nprocs > 1:

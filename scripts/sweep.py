@@ -19,8 +19,11 @@ sys.path.insert(0, ROOT)
 
 VARIANTS = {
     "base": ({}, 0),
+    "poll32": ({"HALO_POLL_NS": "32"}, 0),
     "poll64": ({"HALO_POLL_NS": "64"}, 0),
+    "poll128": ({"HALO_POLL_NS": "128"}, 0),
     "poll256": ({"HALO_POLL_NS": "256"}, 0),
+    "poll512": ({"HALO_POLL_NS": "512"}, 0),
     "rows32": ({"HALO_ITEM_ROWS": "32"}, 0),
     "rows64": ({"HALO_ITEM_ROWS": "64"}, 0),
     "rows128": ({"HALO_ITEM_ROWS": "128"}, 0),
@@ -99,9 +102,11 @@ def main():
         K = args.steps
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
         spans = []
+        F0_all = torch.zeros_like(sess.f_all)
+        for l in range(nl):
+            F0_all[l, : F0[l].shape[0]] = F0[l]
         for k in range(K + 20):
-            for l in range(nl):
-                sess.f[l][: F0[l].shape[0]].copy_(F0[l])
+            sess.f_all.copy_(F0_all)
             if args.flush:
                 flush.fill_(1.0)
             kk = k - 20

@@ -56,6 +56,9 @@ def main():
     st = torch.cuda.current_stream()
     out = []
     for k in range(args.steps):
+        if world > 1:
+            torch.cuda.synchronize()
+            dist.barrier()  # start every traced step together (host skew is not kernel time)
         for l in range(nl):
             sess.f[l][: F0[l].shape[0]].copy_(F0[l])
         if args.flush:
