@@ -109,7 +109,8 @@ struct PulseDev {
   int pad;
 };
 
-enum : uint8_t { kItemXIndep = 0, kItemXDep = 1, kItemPush = 2, kItemUnpack = 3, kItemXRecv = 4, kItemGather = 5 };
+enum : uint8_t { kItemXIndep = 0, kItemXDep = 1, kItemPush = 2, kItemUnpack = 3, kItemXRecv = 4, kItemGather = 5,
+                 kItemFshift = 6 };
 constexpr uint8_t kHomeLevel = 0xff;   // Item.pulse of gather items over home rows
 
 struct Item {
@@ -141,18 +142,19 @@ struct __align__(128) XRec {
 static_assert(sizeof(XRec) == 128, "XRec must be one 128-B line");
 
 struct __align__(128) GRec {
-  uint8_t kind;             // kItemGather
+  uint8_t kind;             // kItemGather or kItemFshift
   uint8_t level;            // slice of this pulse, or kHomeLevel
   uint16_t lrank;
-  uint32_t n_units;         // tasks * layout
-  uint32_t wrap_mask;       // pulses this rank shifted in (fshift, R13)
+  uint32_t n_units;         // gather: tasks * layout
+  uint32_t wrap_mask;       // fshift: pulses this rank shifted in (R13)
   uint8_t pulse_dim[8];
   uint32_t pad;
-  const int4* tasks;        // 32-B task records (row, n, contrib[6]) + begin
-  float* f;                 // own f base
+  const int4* tasks;        // gather: 32-B task records (row, n, contrib[6]) + begin
+  float* f;                 // gather: own f base
   const uint64_t* fll_own;  // own force LL base (slot q at + q*ll_stride)
-  uint64_t* push;           // slice rows: x-sender's LL slot p minus recv_off_p*W (index by row*W + c)
-  uint8_t pad2[128 - 56];
+  uint64_t* push;           // gather of slice rows: x-sender's LL slot p minus recv_off_p*W (index row*W + c)
+  int32_t send_size[kMaxP]; // fshift: entries of each pulse's force LL slot
+  uint8_t pad2[128 - 80];
 };
 static_assert(sizeof(GRec) == 128, "GRec must be one 128-B line");
 

@@ -129,8 +129,46 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// One CTA sums, per dimension d and component c, every force unit the rank
+// received back in its wrapping pulses: fshift[d][c] += sum (R13).  Each thread
+// keeps one component (stride = a multiple of W); warp shuffles then warps in
+// index order: a fixed reduction tree, so the result is reproducible bit for bit.
 template <int W>
-__global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
+__device__ __noinline__ void fshift_item(const GRec& g, const ExParams& P, uint32_t tag, double (*s_fs)[9]) {
+  const uint32_t S = (blockDim.x / W) * W;
+  const int c = (int)(threadIdx.x % W);
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (threadIdx.x < S && c < 3) {
+    for (int q = 0; q < P.P; ++q) {
+      if (!((g.wrap_mask >> q) & 1u)) continue;
+      const int d = g.pulse_dim[q];
+      const uint64_t* src = g.fll_own + (size_t)q * P.ll_stride;
+      const uint32_t n = (uint32_t)g.send_size[q] * W;
+      double sacc = 0.0;
+      for (uint32_t u = threadIdx.x; u < n; u += S)
+        sacc += (double)ll_wait(src + u, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, q), P.poll_ns);
+      if (d == 0) acc[0] += sacc;
+      else if (d == 1) acc[1] += sacc;
+      else acc[2] += sacc;
+    }
+  }
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int c2 = 0; c2 < 3; ++c2) {
+      const double s = warp_sum_d((c == c2 && threadIdx.x < S) ? acc[d] : 0.0);
+      if ((threadIdx.x & 31) == 0) s_fs[threadIdx.x >> 5][3 * d + c2] = s;
+    }
+  __syncthreads();
+  if (threadIdx.x < 9) {
+    double s = 0.0;
+    for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) s += s_fs[wv][threadIdx.x];
+    double* fs = P.fshift + 9 * g.lrank + threadIdx.x;
+    *fs = *fs + s;  // only this CTA writes this rank's shift forces
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_constant__ ExParams P) {
   __shared__ GRec g;
   __shared__ uint64_t s_seq;
   __shared__ double s_fs[kThreads / 32][9];
@@ -148,63 +186,42 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
     if (trace && seq == 0) ctrl->trace[1][blockIdx.x][1] = gtimer();
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
+    if (g.kind == kItemFshift) {
+      // shift forces of this rank (R13): sum of every received force unit of its
+      // wrapping pulses; fixed-order warp + CTA reduction (deterministic, no atomics)
+      if (P.fshift != nullptr) fshift_item<W>(g, P, tag, s_fs);
+      __syncthreads();
+      continue;
+    }
     const uint32_t n = g.n_units;
     const bool push = g.level != kHomeLevel;
-    const uint32_t wrap = (P.fshift != nullptr) ? g.wrap_mask : 0u;
-    // stride = a multiple of W, so every thread keeps one component c
-    const uint32_t S = (blockDim.x / W) * W;
-    const int c = (int)(threadIdx.x % W);
-    double acc[3] = {0.0, 0.0, 0.0};  // fshift partial sums of component c, per dim
-    if (threadIdx.x < S) {
-      for (uint32_t u = threadIdx.x; u < n; u += S) {
-        const uint32_t k = u / W;
-        const int4 a = __ldg(g.tasks + 2 * k);
-        const int4 b = __ldg(g.tasks + 2 * k + 1);
-        const int t = a.x, m = a.y;
-        const uint32_t cc[kMaxP] = {(uint32_t)a.z, (uint32_t)a.w, (uint32_t)b.x,
-                                    (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
-        float v = g.f[(size_t)t * W + c];
-        // issue every contribution's load at once, then resolve stragglers
-        uint64_t w[kMaxP];
+    for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) {
+      const uint32_t k = u / W;
+      const int c = (int)(u - k * W);
+      const int4 a = __ldg(g.tasks + 2 * k);
+      const int4 b = __ldg(g.tasks + 2 * k + 1);
+      const int t = a.x, m = a.y;
+      const uint32_t cc[kMaxP] = {(uint32_t)a.z, (uint32_t)a.w, (uint32_t)b.x,
+                                  (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
+      float v = g.f[(size_t)t * W + c];
+      // issue every contribution's load at once, then resolve stragglers
+      uint64_t w[kMaxP];
 #pragma unroll
-        for (int j = 0; j < kMaxP; ++j)
-          if (j < m)
-            w[j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride +
-                                  (size_t)(cc[j] & 0xffffffu) * W + c);
+      for (int j = 0; j < kMaxP; ++j)
+        if (j < m)
+          w[j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c);
 #pragma unroll
-        for (int j = 0; j < kMaxP; ++j) {
-          if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
-            const int q = (int)(cc[j] >> 24);
-            if ((uint32_t)(w[j] >> 32) != tag)
-              w[j] = ll_spin(g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
-                             P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
-            const float val = __uint_as_float((uint32_t)w[j]);
-            v = P.accumulate ? __fadd_rn(v, val) : val;
-            if ((wrap >> q) & 1u) {
-              const int d = g.pulse_dim[q];
-              if (d == 0) acc[0] += (double)val;
-              else if (d == 1) acc[1] += (double)val;
-              else acc[2] += (double)val;
-            }
-          }
+      for (int j = 0; j < kMaxP; ++j) {
+        if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
+          if ((uint32_t)(w[j] >> 32) != tag)
+            w[j] = ll_spin(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
+                           P.timeout_ns, P.err_host, tcode(12, g.lrank, (int)(cc[j] >> 24)), P.poll_ns);
+          const float val = __uint_as_float((uint32_t)w[j]);
+          v = P.accumulate ? __fadd_rn(v, val) : val;
         }
-        g.f[(size_t)t * W + c] = v;
-        if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
       }
-    }
-    if (wrap) {  // shift forces (R13): warp-reduce, CTA-reduce, one fp64 atomic per (dim, comp) per item
-      for (int d = 0; d < 3; ++d)
-#pragma unroll
-        for (int c2 = 0; c2 < 3; ++c2) {
-          const double s = warp_sum_d((c == c2 && threadIdx.x < S) ? acc[d] : 0.0);
-          if ((threadIdx.x & 31) == 0) s_fs[threadIdx.x >> 5][3 * d + c2] = s;
-        }
-      __syncthreads();
-      if (threadIdx.x < 9) {
-        double s = 0.0;
-        for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) s += s_fs[wv][threadIdx.x];
-        if (s != 0.0) atomicAdd(P.fshift + 9 * g.lrank + threadIdx.x, s);
-      }
+      g.f[(size_t)t * W + c] = v;
+      if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
     }
     __syncthreads();
   }

@@ -691,6 +691,19 @@ static void build_f_items_ll(halo_ctx* ctx) {
       const uint8_t level = k < P ? (uint8_t)(P - 1 - k) : kHomeLevel;
       add_items(v, l, level, kItemGather, lb[k], lb[k + 1], R);
     }
+  // shift-force reductions last: they wait on every wrapping pulse's force units
+  for (int l = 0; l < ctx->n_local; ++l) {
+    const int rk = ctx->first_rank + l;
+    bool wraps = false;
+    for (int q = 0; q < P; ++q) wraps |= ctx->cell(rk, ctx->pdim[q]) == 0 && ctx->send_size[l * P + q] > 0;
+    if (!wraps) continue;
+    Item it;
+    it.lrank = (uint16_t)l;
+    it.pulse = kHomeLevel;
+    it.kind = kItemFshift;
+    it.begin = it.end = 0;
+    v.push_back(it);
+  }
 }
 
 // 128-B work records of the LL kernels, one per item (halo_internal.h XRec/GRec).
@@ -733,8 +746,9 @@ static void build_grec(halo_ctx* ctx) {
     GRec& g = ctx->h_grec[k];
     memset(&g, 0, sizeof g);
     const int l = w.lrank, rk = ctx->first_rank + l;
-    g.kind = kItemGather;
+    g.kind = w.kind;
     g.level = w.pulse;
+    for (int q = 0; q < kMaxP; ++q) g.send_size[q] = q < P ? ctx->send_size[l * P + q] : 0;
     g.lrank = (uint16_t)l;
     g.n_units = (w.end - w.begin) * W;
     g.wrap_mask = 0;
@@ -742,10 +756,10 @@ static void build_grec(halo_ctx* ctx) {
       g.pulse_dim[q] = (uint8_t)ctx->pdim[q];
       if (ctx->cell(rk, ctx->pdim[q]) == 0) g.wrap_mask |= 1u << q;
     }
-    g.tasks = ctx->csr_tasks[l] + 2 * (size_t)w.begin;
+    g.tasks = w.kind == kItemGather ? ctx->csr_tasks[l] + 2 * (size_t)w.begin : nullptr;
     g.f = ctx->f[l];
     g.fll_own = ctx->fll_of(rk);
-    if (w.pulse != kHomeLevel) {
+    if (w.kind == kItemGather && w.pulse != kHomeLevel) {
       const PulseDev& pd = ctx->h_pulses[l * P + w.pulse];
       g.push = pd.fll_dst - (ptrdiff_t)ctx->atom_offset[l * P + w.pulse] * W;
     }

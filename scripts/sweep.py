@@ -99,6 +99,7 @@ def main():
         F0 = [torch.from_numpy(forces_normal(sess.layout_of(l)["n_total"], 1 + l, width=args.layout)).to(dev)
               for l in range(nl)]
         st = torch.cuda.current_stream()
+        fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=dev)
         K = args.steps
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
         spans = []
@@ -115,7 +116,7 @@ def main():
             sess.exchange_x()
             if kk >= 0:
                 ev[kk][1].record(st)
-            sess.exchange_f()
+            sess.exchange_f(fshift=fshift)
             if kk >= 0:
                 ev[kk][2].record(st)
             if kk >= 0 and kk % 50 == 0:
