@@ -153,8 +153,11 @@ struct __align__(128) GRec {
   float* f;                 // gather: own f base
   const uint64_t* fll_own;  // own force LL base (slot q at + q*ll_stride)
   uint64_t* push;           // gather of slice rows: x-sender's LL slot p minus recv_off_p*W (index row*W + c)
-  int32_t send_size[kMaxP]; // fshift: entries of each pulse's force LL slot
-  uint8_t pad2[128 - 80];
+  double* part;             // gather: this item's fshift partial slot (9 doubles); combine: slot 0
+  uint64_t* pflag;          // gather: this item's partial-ready flag; combine: flag of slot 0
+  uint32_t n_slots;         // combine: gather items of this rank
+  uint32_t pad3;
+  uint8_t pad2[128 - 80];   // keep one 128-B line
 };
 static_assert(sizeof(GRec) == 128, "GRec must be one 128-B line");
 

@@ -129,41 +129,36 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// One CTA sums, per dimension d and component c, every force unit the rank
-// received back in its wrapping pulses: fshift[d][c] += sum (R13).  Each thread
-// keeps one component (stride = a multiple of W); warp shuffles then warps in
-// index order: a fixed reduction tree, so the result is reproducible bit for bit.
-template <int W>
-__device__ __noinline__ void fshift_item(const GRec& g, const ExParams& P, uint32_t tag, double (*s_fs)[9]) {
-  const uint32_t S = (blockDim.x / W) * W;
-  const int c = (int)(threadIdx.x % W);
-  double acc[3] = {0.0, 0.0, 0.0};
-  if (threadIdx.x < S && c < 3) {
-    for (int q = 0; q < P.P; ++q) {
-      if (!((g.wrap_mask >> q) & 1u)) continue;
-      const int d = g.pulse_dim[q];
-      const uint64_t* src = g.fll_own + (size_t)q * P.ll_stride;
-      const uint32_t n = (uint32_t)g.send_size[q] * W;
-      double sacc = 0.0;
-      for (uint32_t u = threadIdx.x; u < n; u += S)
-        sacc += (double)ll_wait(src + u, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, q), P.poll_ns);
-      if (d == 0) acc[0] += sacc;
-      else if (d == 1) acc[1] += sacc;
-      else acc[2] += sacc;
-    }
-  }
-  for (int d = 0; d < 3; ++d)
+// Deterministic CTA reduction of 9 doubles per thread (fixed shuffle tree, warps in
+// index order); thread j < 9 returns the total of output j.
+__device__ __forceinline__ double cta_sum9(const double* v, double (*s_fs)[9], int j_out) {
 #pragma unroll
-    for (int c2 = 0; c2 < 3; ++c2) {
-      const double s = warp_sum_d((c == c2 && threadIdx.x < S) ? acc[d] : 0.0);
-      if ((threadIdx.x & 31) == 0) s_fs[threadIdx.x >> 5][3 * d + c2] = s;
-    }
+  for (int j = 0; j < 9; ++j) {
+    const double s = warp_sum_d(v[j]);
+    if ((threadIdx.x & 31) == 0) s_fs[threadIdx.x >> 5][j] = s;
+  }
   __syncthreads();
+  double tot = 0.0;
+  if (j_out < 9)
+    for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) tot += s_fs[wv][j_out];
+  __syncthreads();
+  return tot;
+}
+
+// Combine item of one rank (R13): waits for every gather item's partial shift
+// forces (flag per slot, no contention) and adds their fixed-order sum to
+// fshift.  Only this CTA writes the rank's fshift: deterministic, no atomics.
+__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint64_t seq, double (*s_fs)[9]) {
+  double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint32_t sl = threadIdx.x; sl < g.n_slots; sl += blockDim.x) {
+    wait_geq<false>(g.pflag + sl, seq, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0));
+#pragma unroll
+    for (int j = 0; j < 9; ++j) v[j] += __ldcg(g.part + 9 * (size_t)sl + j);
+  }
+  const double tot = cta_sum9(v, s_fs, threadIdx.x);
   if (threadIdx.x < 9) {
-    double s = 0.0;
-    for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) s += s_fs[wv][threadIdx.x];
     double* fs = P.fshift + 9 * g.lrank + threadIdx.x;
-    *fs = *fs + s;  // only this CTA writes this rank's shift forces
+    *fs = *fs + tot;
   }
 }
 
@@ -187,41 +182,62 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     if (g.kind == kItemFshift) {
-      // shift forces of this rank (R13): sum of every received force unit of its
-      // wrapping pulses; fixed-order warp + CTA reduction (deterministic, no atomics)
-      if (P.fshift != nullptr) fshift_item<W>(g, P, tag, s_fs);
+      if (P.fshift != nullptr) fshift_combine(g, P, seq, s_fs);
       __syncthreads();
       continue;
     }
     const uint32_t n = g.n_units;
     const bool push = g.level != kHomeLevel;
-    for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) {
-      const uint32_t k = u / W;
-      const int c = (int)(u - k * W);
-      const int4 a = __ldg(g.tasks + 2 * k);
-      const int4 b = __ldg(g.tasks + 2 * k + 1);
-      const int t = a.x, m = a.y;
-      const uint32_t cc[kMaxP] = {(uint32_t)a.z, (uint32_t)a.w, (uint32_t)b.x,
-                                  (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
-      float v = g.f[(size_t)t * W + c];
-      // issue every contribution's load at once, then resolve stragglers
-      uint64_t w[kMaxP];
+    const bool part = (P.fshift != nullptr) && (g.part != nullptr);
+    const uint32_t wrap = part ? g.wrap_mask : 0u;
+    // stride = a multiple of W: every thread keeps one component c
+    const uint32_t S = (blockDim.x / W) * W;
+    const int c = (int)(threadIdx.x % W);
+    double acc[3] = {0.0, 0.0, 0.0};  // shift-force partials of component c, per dim (R13)
+    if (threadIdx.x < S) {
+      for (uint32_t u = threadIdx.x; u < n; u += S) {
+        const uint32_t k = u / W;
+        const int4 a = __ldg(g.tasks + 2 * k);
+        const int4 b = __ldg(g.tasks + 2 * k + 1);
+        const int t = a.x, m = a.y;
+        const uint32_t cc[kMaxP] = {(uint32_t)a.z, (uint32_t)a.w, (uint32_t)b.x,
+                                    (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
+        float v = g.f[(size_t)t * W + c];
+        // issue every contribution's load at once, then resolve stragglers
+        uint64_t w[kMaxP];
 #pragma unroll
-      for (int j = 0; j < kMaxP; ++j)
-        if (j < m)
-          w[j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c);
+        for (int j = 0; j < kMaxP; ++j)
+          if (j < m)
+            w[j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c);
 #pragma unroll
-      for (int j = 0; j < kMaxP; ++j) {
-        if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
-          if ((uint32_t)(w[j] >> 32) != tag)
-            w[j] = ll_spin(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
-                           P.timeout_ns, P.err_host, tcode(12, g.lrank, (int)(cc[j] >> 24)), P.poll_ns);
-          const float val = __uint_as_float((uint32_t)w[j]);
-          v = P.accumulate ? __fadd_rn(v, val) : val;
+        for (int j = 0; j < kMaxP; ++j) {
+          if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
+            const int q = (int)(cc[j] >> 24);
+            if ((uint32_t)(w[j] >> 32) != tag)
+              w[j] = ll_spin(g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
+                             P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
+            const float val = __uint_as_float((uint32_t)w[j]);
+            v = P.accumulate ? __fadd_rn(v, val) : val;
+            if (((wrap >> q) & 1u) && c < 3) {
+              const int d = g.pulse_dim[q];
+              if (d == 0) acc[0] += (double)val;
+              else if (d == 1) acc[1] += (double)val;
+              else acc[2] += (double)val;
+            }
+          }
         }
+        g.f[(size_t)t * W + c] = v;
+        if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
       }
-      g.f[(size_t)t * W + c] = v;
-      if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
+    }
+    if (part) {  // this item's shift-force partial -> its own slot, then its flag
+      double pv[9];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) pv[j] = (threadIdx.x < S && c == j % 3) ? acc[j / 3] : 0.0;
+      const double tot = cta_sum9(pv, s_fs, threadIdx.x);
+      if (threadIdx.x < 9) g.part[threadIdx.x] = tot;
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_gpu(g.pflag, seq);
     }
     __syncthreads();
   }

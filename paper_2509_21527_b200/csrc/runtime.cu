@@ -114,6 +114,8 @@ struct halo_ctx {
   std::vector<GRec> h_grec;
   XRec* d_xrec = nullptr;
   GRec* d_grec = nullptr;
+  char* d_fsp = nullptr;            // fshift partial slots + flags (LL protocol)
+  size_t fsp_bytes = 0;
   std::vector<std::vector<int>> level_begin;  // [local][P+2]: task index where level P-1..0, home start
 
   // host plan
@@ -691,11 +693,11 @@ static void build_f_items_ll(halo_ctx* ctx) {
       const uint8_t level = k < P ? (uint8_t)(P - 1 - k) : kHomeLevel;
       add_items(v, l, level, kItemGather, lb[k], lb[k + 1], R);
     }
-  // shift-force reductions last: they wait on every wrapping pulse's force units
+  // shift-force combines last: each waits for its rank's gather partials
   for (int l = 0; l < ctx->n_local; ++l) {
     const int rk = ctx->first_rank + l;
     bool wraps = false;
-    for (int q = 0; q < P; ++q) wraps |= ctx->cell(rk, ctx->pdim[q]) == 0 && ctx->send_size[l * P + q] > 0;
+    for (int q = 0; q < P; ++q) wraps |= ctx->cell(rk, ctx->pdim[q]) == 0;
     if (!wraps) continue;
     Item it;
     it.lrank = (uint16_t)l;
@@ -738,17 +740,41 @@ static void build_xrec(halo_ctx* ctx) {
   }
 }
 
-static void build_grec(halo_ctx* ctx) {
-  const int W = ctx->W, P = ctx->P;
+static halo_status build_grec(halo_ctx* ctx) {
+  const int W = ctx->W, P = ctx->P, L = ctx->n_local;
+  // fshift partial slots: one per gather item of a rank that shifts in some pulse
+  std::vector<int> nslot(L, 0), wraps(L, 0);
+  for (int l = 0; l < L; ++l)
+    for (int q = 0; q < P; ++q)
+      if (ctx->cell(ctx->first_rank + l, ctx->pdim[q]) == 0) wraps[l] = 1;
+  for (const Item& w : ctx->h_items_f)
+    if (w.kind == kItemGather && wraps[w.lrank]) nslot[w.lrank]++;
+  std::vector<size_t> part_off(L), flag_off(L);
+  size_t need = 0;
+  for (int l = 0; l < L; ++l) {
+    part_off[l] = need;
+    need += align_up(sizeof(double) * 9 * std::max(nslot[l], 1), 256);
+    flag_off[l] = need;
+    need += align_up(sizeof(uint64_t) * std::max(nslot[l], 1), 256);
+  }
+  if (need > ctx->fsp_bytes) {
+    if (ctx->d_fsp) CK(cudaFree(ctx->d_fsp));
+    ctx->d_fsp = nullptr;
+    CK(cudaMalloc(&ctx->d_fsp, need));
+    CK(cudaMemset(ctx->d_fsp, 0, need));  // flags start below every sequence number
+    ctx->fsp_bytes = need;
+  }
+  std::vector<int> next(L, 0);
   ctx->h_grec.assign(ctx->h_items_f.size(), GRec{});
   for (size_t k = 0; k < ctx->h_items_f.size(); ++k) {
     const Item& w = ctx->h_items_f[k];
     GRec& g = ctx->h_grec[k];
     memset(&g, 0, sizeof g);
     const int l = w.lrank, rk = ctx->first_rank + l;
+    double* part = reinterpret_cast<double*>(ctx->d_fsp + part_off[l]);
+    uint64_t* pflag = reinterpret_cast<uint64_t*>(ctx->d_fsp + flag_off[l]);
     g.kind = w.kind;
     g.level = w.pulse;
-    for (int q = 0; q < kMaxP; ++q) g.send_size[q] = q < P ? ctx->send_size[l * P + q] : 0;
     g.lrank = (uint16_t)l;
     g.n_units = (w.end - w.begin) * W;
     g.wrap_mask = 0;
@@ -756,14 +782,26 @@ static void build_grec(halo_ctx* ctx) {
       g.pulse_dim[q] = (uint8_t)ctx->pdim[q];
       if (ctx->cell(rk, ctx->pdim[q]) == 0) g.wrap_mask |= 1u << q;
     }
-    g.tasks = w.kind == kItemGather ? ctx->csr_tasks[l] + 2 * (size_t)w.begin : nullptr;
     g.f = ctx->f[l];
     g.fll_own = ctx->fll_of(rk);
-    if (w.kind == kItemGather && w.pulse != kHomeLevel) {
-      const PulseDev& pd = ctx->h_pulses[l * P + w.pulse];
-      g.push = pd.fll_dst - (ptrdiff_t)ctx->atom_offset[l * P + w.pulse] * W;
+    if (w.kind == kItemGather) {
+      g.tasks = ctx->csr_tasks[l] + 2 * (size_t)w.begin;
+      if (wraps[l]) {
+        g.part = part + 9 * (size_t)next[l];
+        g.pflag = pflag + next[l];
+        next[l]++;
+      }
+      if (w.pulse != kHomeLevel) {
+        const PulseDev& pd = ctx->h_pulses[l * P + w.pulse];
+        g.push = pd.fll_dst - (ptrdiff_t)ctx->atom_offset[l * P + w.pulse] * W;
+      }
+    } else {  // kItemFshift: combine of the rank's slots
+      g.part = part;
+      g.pflag = pflag;
+      g.n_slots = (uint32_t)nslot[l];
     }
   }
+  return HALO_OK;
 }
 
 static halo_status upload_plan(halo_ctx* ctx) {
@@ -1044,7 +1082,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     build_x_items_ll(ctx, 0, P);
     build_f_items_ll(ctx);
     build_xrec(ctx);
-    build_grec(ctx);
+    if ((s = build_grec(ctx)) != HALO_OK) return s;
   } else {
     ctx->h_xrec.clear();
     ctx->h_grec.clear();
@@ -1281,6 +1319,7 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_small) (void)cudaFree(ctx->d_small);
   if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
   if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
+  if (ctx->d_fsp) (void)cudaFree(ctx->d_fsp);
   if (ctx->err_host) (void)cudaFreeHost(ctx->err_host);
   (void)cudaGetLastError();
   delete ctx;
