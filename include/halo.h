@@ -209,8 +209,10 @@ HALO_API halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_
 
 /* Per-CTA device timestamps of the last exchange_x (which = 0) or exchange_f
  * (which = 1) launch, HALO_F_TIMERS only (the paper's %globaltimer
- * instrumentation): out[4*i .. 4*i+3] = CTA i's [start, plan record
- * loaded, items done, exit] in ns; *n = CTAs recorded (<= cap/4).  Synchronises. */
+ * instrumentation): out[8*i .. 8*i+7] = CTA i's [start, plan record
+ * loaded, items done, exit, item0 tag, item0 end, item1 tag, item1 end] in ns,
+ * tag = kind << 16 | local rank << 8 | pulse; *n = CTAs recorded (<= cap/8).
+ * LL protocol kernels only.  Synchronises. */
 HALO_API halo_status halo_get_trace(halo_ctx* ctx, int which, uint64_t* out, int cap, int* n);
 
 /* Floors (measurement): ping-pong `iters` round trips of a

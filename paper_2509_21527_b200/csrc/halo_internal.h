@@ -66,8 +66,9 @@ struct Ctrl {
   int32_t err[kMaxLocal];                 // set_maps error bits (kErr*)
   int32_t agreed_err[kMaxLocal];          // OR over all ranks after the status exchange
   // HALO_F_TIMERS: per-CTA %globaltimer stamps of the last x (0) / f (1) launch:
-  // [start, plan record loaded, items done, exit]
-  uint64_t trace[2][kTraceCTAs][4];
+  // [start, plan record loaded, items done, exit, item0 tag, item0 end, item1 tag, item1 end]
+  // tag = kind << 16 | lrank << 8 | pulse (level)
+  uint64_t trace[2][kTraceCTAs][8];
 };
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };

@@ -115,6 +115,13 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
       }
     }
     __syncthreads();
+    if (trace) {
+      const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
+      if (slot < 2) {
+        ctrl->trace[0][blockIdx.x][4 + 2 * slot] = ((uint64_t)r.kind << 16) | ((uint64_t)r.lrank << 8) | r.pulse;
+        ctrl->trace[0][blockIdx.x][5 + 2 * slot] = gtimer();
+      }
+    }
   }
   seq = s_seq;
   if (trace) ctrl->trace[0][blockIdx.x][2] = gtimer();
@@ -184,6 +191,13 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
     if (g.kind == kItemFshift) {
       if (P.fshift != nullptr) fshift_combine(g, P, seq, s_fs);
       __syncthreads();
+      if (trace) {
+        const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
+        if (slot < 2) {
+          ctrl->trace[1][blockIdx.x][4 + 2 * slot] = ((uint64_t)g.kind << 16) | ((uint64_t)g.lrank << 8) | g.level;
+          ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();
+        }
+      }
       continue;
     }
     const uint32_t n = g.n_units;
@@ -238,6 +252,14 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
       if (threadIdx.x < 9) g.part[threadIdx.x] = tot;
       __syncthreads();
       if (threadIdx.x == 0) st_release_gpu(g.pflag, seq);
+    }
+    __syncthreads();
+    if (trace) {
+      const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
+      if (slot < 2) {
+        ctrl->trace[1][blockIdx.x][4 + 2 * slot] = ((uint64_t)g.kind << 16) | ((uint64_t)g.lrank << 8) | g.level;
+        ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();
+      }
     }
     __syncthreads();
   }

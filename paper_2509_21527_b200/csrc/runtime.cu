@@ -1239,12 +1239,12 @@ halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
     for (int which = 0; which < 2; ++which) {
       const int m = std::min(ctx->last_grid[which], kTraceCTAs);
       if (m <= 0) continue;
-      std::vector<uint64_t> t(4 * (size_t)m);
-      CK(cudaMemcpy(t.data(), &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 4 * m, cudaMemcpyDeviceToHost));
+      std::vector<uint64_t> t(8 * (size_t)m);
+      CK(cudaMemcpy(t.data(), &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 8 * m, cudaMemcpyDeviceToHost));
       uint64_t lo = ~0ull, hi = 0;
       for (int i = 0; i < m; ++i) {
-        lo = std::min(lo, t[4 * i]);
-        hi = std::max(hi, t[4 * i + 3]);
+        lo = std::min(lo, t[8 * i]);
+        hi = std::max(hi, t[8 * i + 3]);
       }
       v[which] = hi > lo ? hi - lo : 0;
     }
@@ -1256,12 +1256,12 @@ halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
 
 halo_status halo_get_trace(halo_ctx* ctx, int which, uint64_t* out, int cap, int* n) {
   if (!ctx || which < 0 || which > 1 || !out || !n) return HALO_ERR_ARG;
-  const int m = std::min(std::min(ctx->last_grid[which], kTraceCTAs), cap / 4);
+  const int m = std::min(std::min(ctx->last_grid[which], kTraceCTAs), cap / 8);
   *n = m;
   if (m <= 0) return HALO_OK;
   CK(cudaSetDevice(ctx->cfg.device));
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(out, &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 4 * m, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 8 * m, cudaMemcpyDeviceToHost));
   return HALO_OK;
 }
 

@@ -178,12 +178,13 @@ class Halo:
         return a.value, b.value
 
     def get_trace(self, which):
-        """Per-CTA [start, record loaded, items done, exit] ns of the last x (0) / f (1) launch."""
-        cap = 4 * 2048
+        """Per-CTA [start, record loaded, items done, exit, item0 tag, item0 end, item1 tag, item1 end]
+        (ns; tag = kind << 16 | lrank << 8 | pulse) of the last x (0) / f (1) launch."""
+        cap = 8 * 2048
         buf = (c_uint64 * cap)()
         n = c_int()
         self._ck(self.lib.halo_get_trace(self.h, int(which), buf, cap, ctypes.byref(n)))
-        return np.array(buf[: 4 * n.value], dtype=np.uint64).reshape(-1, 4)
+        return np.array(buf[: 8 * n.value], dtype=np.uint64).reshape(-1, 8)
 
     def floor_pingpong(self, peer_rank, iters=10000, relaxed=False) -> float:
         v = c_double()

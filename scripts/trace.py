@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--flush", action="store_true")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--no-fshift", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -67,7 +68,7 @@ def main():
         e0.record(st)
         sess.exchange_x()
         e1.record(st)
-        sess.exchange_f(fshift=fshift)
+        sess.exchange_f(fshift=None if args.no_fshift else fshift)
         e2.record(st)
         torch.cuda.synchronize()
         tx = sess.halo.get_trace(0).astype(np.int64)
@@ -82,6 +83,18 @@ def main():
             "f_start": q((tf[:, 0] - t0) / 1e3), "f_rec": q((tf[:, 1] - t0) / 1e3),
             "f_done": q((tf[:, 2] - t0) / 1e3), "f_exit": q((tf[:, 3] - t0) / 1e3),
         }
+        # per (kind, level) item end quantiles, relative to the kernel's first CTA start
+        for nm, tr in (("x", tx), ("f", tf)):
+            tk0 = tr[:, 0].min()
+            groups = {}
+            for row in tr:
+                for sl in range(2):
+                    tag, end = int(row[4 + 2 * sl]), int(row[5 + 2 * sl])
+                    if end == 0 or end < tk0:
+                        continue
+                    key = f"k{tag >> 16}_p{tag & 0xff}"
+                    groups.setdefault(key, []).append((end - tk0) / 1e3)
+            res[nm + "_items"] = {k: q(np.array(v)) + [len(v)] for k, v in sorted(groups.items())}
         out.append(res)
     if world > 1:
         allres = [None] * world
