@@ -45,6 +45,15 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Report a timeout once: host-mapped word (system scope) + give up.
 static __device__ __noinline__ void report_timeout(int* err_host, int code) {
   volatile int* e = err_host;
@@ -52,29 +61,34 @@ static __device__ __noinline__ void report_timeout(int* err_host, int code) {
   fence_sys();
 }
 
-// Bounded spin: returns false on timeout.  `sys` selects the scope of the acquire.
-// The flag is polled back to back; the timer and the (host-mapped, PCIe)
-// error word are only looked at every 1024 polls so they never sit on the
-// latency path.
+// Bounded spin: returns false on timeout.  `kSys` selects the scope of the acquire.
+// Polls with RELAXED loads (an ld.acquire compiles to LDG.STRONG + CCTL.IVALL, i.e.
+// it invalidates the SM's whole L1 on every poll, which slows every co-resident
+// CTA); once the value is seen, one acquire load of the same (monotonic) word
+// establishes the synchronisation.  The timer and the host-mapped (PCIe) error
+// word are only looked at every 1024 polls, never on the latency path.
 template <bool kSys>
 __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t v, uint64_t timeout_ns, int* err_host,
                                          int code, uint32_t poll_ns = 0) {
-  if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
-  uint64_t t0 = 0;
-  for (uint32_t it = 1;; ++it) {
-    if (poll_ns) __nanosleep(poll_ns);
-    if ((kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= v) return true;
-    if ((it & 1023u) == 0) {
-      const uint64_t now = gtimer();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        report_timeout(err_host, code);
-        return false;
+  if ((kSys ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) < v) {
+    uint64_t t0 = 0;
+    for (uint32_t it = 1;; ++it) {
+      if (poll_ns) __nanosleep(poll_ns);
+      if ((kSys ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) >= v) break;
+      if ((it & 1023u) == 0) {
+        const uint64_t now = gtimer();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > timeout_ns) {
+          report_timeout(err_host, code);
+          return false;
+        }
+        if (*(volatile int*)err_host != 0) return false;  // another wait already failed: drain
       }
-      if (*(volatile int*)err_host != 0) return false;  // another wait already failed: drain
     }
   }
+  (void)(kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p));
+  return true;
 }
 
 // Wait until (*p >> 32) == epoch; returns the low 32 bits (or 0xffffffff on timeout).
@@ -82,8 +96,11 @@ __device__ __forceinline__ uint32_t wait_epoch(const uint64_t* p, uint32_t epoch
                                                int* err_host, int code) {
   uint64_t t0 = 0;
   for (uint32_t it = 0;; ++it) {
-    const uint64_t v = ld_acquire_sys(p);
-    if ((uint32_t)(v >> 32) == epoch) return (uint32_t)v;
+    uint64_t v = ld_relaxed_sys(p);
+    if ((uint32_t)(v >> 32) == epoch) {
+      v = ld_acquire_sys(p);  // same word (only its writer changes it during this epoch)
+      return (uint32_t)v;
+    }
     if ((it & 1023u) == 1023u) {
       const uint64_t now = gtimer();
       if (t0 == 0) {
@@ -99,15 +116,6 @@ __device__ __forceinline__ uint32_t wait_epoch(const uint64_t* p, uint32_t epoch
 
 // timeout codes: kind << 16 | lrank << 8 | pulse
 __device__ __forceinline__ int tcode(int kind, int lr, int p) { return (kind << 16) | (lr << 8) | p; }
-
-__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // ------------------------------------------------------------- per-CTA timing
 __device__ __forceinline__ void timer_start(unsigned flags, uint64_t* t_start) {
