@@ -154,8 +154,9 @@ struct __align__(128) GRec {
   float* f;                 // gather: own f base
   const uint64_t* fll_own;  // own force LL base (slot q at + q*ll_stride)
   uint64_t* push;           // gather of slice rows: x-sender's LL slot p minus recv_off_p*W (index row*W + c)
-  double* part;             // gather: this item's fshift partial slot (9 doubles); combine: slot 0
-  uint64_t* pflag;          // gather: this item's partial-ready flag; combine: flag of slot 0
+  uint64_t* part;           // gather: this item's fshift partial slot (9 doubles as 18 LL units: hi, lo
+                            // words); combine: slot 0
+  uint64_t* pflag;          // unused (kept for layout)
   uint32_t n_slots;         // combine: gather items of this rank
   uint32_t pad3;
   uint8_t pad2[128 - 80];   // keep one 128-B line

@@ -152,15 +152,20 @@ __device__ __forceinline__ double cta_sum9(const double* v, double (*s_fs)[9], i
   return tot;
 }
 
-// Combine item of one rank (R13): waits for every gather item's partial shift
-// forces (flag per slot, no contention) and adds their fixed-order sum to
-// fshift.  Only this CTA writes the rank's fshift: deterministic, no atomics.
-__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint64_t seq, double (*s_fs)[9]) {
+// Combine item of one rank (R13): polls every gather item's shift-force partial
+// (9 doubles stored as tagged LL units, so no flag and no fence) and adds their
+// fixed-order sum to fshift.  Only this CTA writes the rank's fshift:
+// deterministic, no atomics.
+__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_fs)[9]) {
   double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (uint32_t sl = threadIdx.x; sl < g.n_slots; sl += blockDim.x) {
-    wait_geq<false>(g.pflag + sl, seq, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0));
+    const uint64_t* u = g.part + 18 * (size_t)sl;
 #pragma unroll
-    for (int j = 0; j < 9; ++j) v[j] += __ldcg(g.part + 9 * (size_t)sl + j);
+    for (int j = 0; j < 9; ++j) {
+      const uint32_t hi = __float_as_uint(ll_wait(u + 2 * j, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0));
+      const uint32_t lo = __float_as_uint(ll_wait(u + 2 * j + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0));
+      v[j] += __hiloint2double((int)hi, (int)lo);
+    }
   }
   const double tot = cta_sum9(v, s_fs, threadIdx.x);
   if (threadIdx.x < 9) {
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     if (g.kind == kItemFshift) {
-      if (P.fshift != nullptr) fshift_combine(g, P, seq, s_fs);
+      if (P.fshift != nullptr) fshift_combine(g, P, tag, s_fs);
       __syncthreads();
       if (trace) {
         const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
@@ -249,9 +254,12 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
 #pragma unroll
       for (int j = 0; j < 9; ++j) pv[j] = (threadIdx.x < S && c == j % 3) ? acc[j / 3] : 0.0;
       const double tot = cta_sum9(pv, s_fs, threadIdx.x);
-      if (threadIdx.x < 9) g.part[threadIdx.x] = tot;
-      __syncthreads();
-      if (threadIdx.x == 0) st_release_gpu(g.pflag, seq);
+      if (threadIdx.x < 9) {  // tagged halves: the combine needs no flag and no fence
+        st_relaxed_gpu(g.part + 2 * threadIdx.x,
+                       ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));
+        st_relaxed_gpu(g.part + 2 * threadIdx.x + 1,
+                       ll_pack(__uint_as_float((uint32_t)__double2loint(tot)), tag));
+      }
     }
     __syncthreads();
     if (trace) {

@@ -147,7 +147,10 @@ __device__ __forceinline__ void finish_launch(unsigned flags, uint32_t* done, ui
 // sequence number at its exit: by then every CTA of the launch has read it.
 __device__ __forceinline__ uint32_t launch_arrive(uint32_t* done) {
   uint32_t old = 0;
-  if (threadIdx.x == 0) old = atom_add_acqrel_gpu(done, 1u);
+  // relaxed: the sequence-number load it must follow was consumed before the
+  // barrier that precedes this call; no fence (a MEMBAR drains behind pollers)
+  if (threadIdx.x == 0)
+    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(done) : "memory");
   return old;
 }
 

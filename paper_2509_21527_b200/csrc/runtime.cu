@@ -751,11 +751,11 @@ static halo_status build_grec(halo_ctx* ctx) {
     if (w.kind == kItemGather && wraps[w.lrank]) nslot[w.lrank]++;
   std::vector<size_t> part_off(L), flag_off(L);
   size_t need = 0;
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < L; ++l) {  // 18 tagged LL units (hi/lo words of 9 doubles) per slot
     part_off[l] = need;
-    need += align_up(sizeof(double) * 9 * std::max(nslot[l], 1), 256);
+    need += align_up(sizeof(uint64_t) * 18 * std::max(nslot[l], 1), 256);
     flag_off[l] = need;
-    need += align_up(sizeof(uint64_t) * std::max(nslot[l], 1), 256);
+    need += 256;
   }
   if (need > ctx->fsp_bytes) {
     if (ctx->d_fsp) CK(cudaFree(ctx->d_fsp));
@@ -771,7 +771,7 @@ static halo_status build_grec(halo_ctx* ctx) {
     GRec& g = ctx->h_grec[k];
     memset(&g, 0, sizeof g);
     const int l = w.lrank, rk = ctx->first_rank + l;
-    double* part = reinterpret_cast<double*>(ctx->d_fsp + part_off[l]);
+    uint64_t* part = reinterpret_cast<uint64_t*>(ctx->d_fsp + part_off[l]);
     uint64_t* pflag = reinterpret_cast<uint64_t*>(ctx->d_fsp + flag_off[l]);
     g.kind = w.kind;
     g.level = w.pulse;
@@ -787,7 +787,7 @@ static halo_status build_grec(halo_ctx* ctx) {
     if (w.kind == kItemGather) {
       g.tasks = ctx->csr_tasks[l] + 2 * (size_t)w.begin;
       if (wraps[l]) {
-        g.part = part + 9 * (size_t)next[l];
+        g.part = part + 18 * (size_t)next[l];
         g.pflag = pflag + next[l];
         next[l]++;
       }
