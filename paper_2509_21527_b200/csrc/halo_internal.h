@@ -179,6 +179,7 @@ struct ExParams {
   int accumulate;
   uint32_t poll_ns;         // __nanosleep between flag polls (0 = tight spin)
   uint64_t ll_stride;       // u64 units per pulse slot of the LL receive buffers
+  uint32_t debug;           // HALO_DEBUG experiment bits (0 in production)
   const XRec* xrec;         // LL protocol work records (x)
   const GRec* grec;         // LL protocol work records (f)
 };

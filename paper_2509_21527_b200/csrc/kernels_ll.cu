@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     if (g.kind == kItemFshift) {
-      if (P.fshift != nullptr) fshift_combine(g, P, tag, s_fs);
+      if (P.fshift != nullptr && !(P.debug & 2)) fshift_combine(g, P, tag, s_fs);
       __syncthreads();
       if (trace) {
         const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
       double pv[9];
 #pragma unroll
       for (int j = 0; j < 9; ++j) pv[j] = (threadIdx.x < S && c == j % 3) ? acc[j / 3] : 0.0;
-      const double tot = cta_sum9(pv, s_fs, threadIdx.x);
+      const double tot = (P.debug & 1) ? 0.0 : cta_sum9(pv, s_fs, threadIdx.x);
       if (threadIdx.x < 9) {  // tagged halves: the combine needs no flag and no fence
         st_relaxed_gpu(g.part + 2 * threadIdx.x,
                        ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));

@@ -133,6 +133,7 @@ struct halo_ctx {
   int last_grid[2] = {0, 0};
   int item_rows = 128;
   uint32_t poll_ns = 0;
+  uint32_t debug = 0;
 
   int cell(int r, int d) const {
     const int* g = cfg.grid;
@@ -291,6 +292,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   ctx->peer_scratch.assign(ctx->nranks, nullptr);
   if (const char* e = getenv("HALO_ITEM_ROWS")) ctx->item_rows = std::max(32, atoi(e));
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = (uint32_t)std::max(0, atoi(e));
+  if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ctrl, sizeof(Ctrl));
@@ -859,6 +861,7 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.fshift = nullptr;
   P.accumulate = 1;
   P.poll_ns = ctx->poll_ns;
+  P.debug = ctx->debug;
   P.ll_stride = ctx->ll_stride;
   P.xrec = ctx->d_xrec;
   P.grec = ctx->d_grec;
