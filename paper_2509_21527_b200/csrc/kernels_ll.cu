@@ -136,38 +136,45 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Deterministic CTA reduction of 9 doubles per thread (fixed shuffle tree, warps in
-// index order); thread j < 9 returns the total of output j.
-__device__ __forceinline__ double cta_sum9(const double* v, double (*s_fs)[9], int j_out) {
+// Deterministic CTA reduction of 9 doubles per thread: a fixed pairwise tree in
+// shared memory (no warp shuffles: a full-mask SHFL after the divergent polling
+// loop made lanes wait for their warp's slowest poll before pushing, which cost
+// ~10 us per level at C3).  Thread j < 9 returns the total of output j.
+__device__ __forceinline__ double cta_tree9(double (*s_red)[kThreads], int j_out) {
+  for (int h = kThreads / 2; h > 0; h >>= 1) {
+    __syncthreads();
+    if ((int)threadIdx.x < h)
 #pragma unroll
-  for (int j = 0; j < 9; ++j) {
-    const double s = warp_sum_d(v[j]);
-    if ((threadIdx.x & 31) == 0) s_fs[threadIdx.x >> 5][j] = s;
+      for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] += s_red[j][threadIdx.x + h];
   }
   __syncthreads();
-  double tot = 0.0;
-  if (j_out < 9)
-    for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) tot += s_fs[wv][j_out];
+  const double tot = (j_out < 9) ? s_red[j_out][0] : 0.0;
   __syncthreads();
   return tot;
+}
+
+__device__ __forceinline__ double cta_sum9(const double* v, double (*s_red)[kThreads], int j_out) {
+#pragma unroll
+  for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] = v[j];
+  return cta_tree9(s_red, j_out);
 }
 
 // Combine item of one rank (R13): polls every gather item's shift-force partial
 // (9 doubles stored as tagged LL units, so no flag and no fence) and adds their
 // fixed-order sum to fshift.  Only this CTA writes the rank's fshift:
 // deterministic, no atomics.
-__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_fs)[9]) {
-  double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_fs)[kThreads]) {
+#pragma unroll
+  for (int j = 0; j < 9; ++j) s_fs[j][threadIdx.x] = 0.0;
   for (uint32_t sl = threadIdx.x; sl < g.n_slots; sl += blockDim.x) {
     const uint64_t* u = g.part + 18 * (size_t)sl;
-#pragma unroll
     for (int j = 0; j < 9; ++j) {
       const uint32_t hi = __float_as_uint(ll_wait(u + 2 * j, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0));
       const uint32_t lo = __float_as_uint(ll_wait(u + 2 * j + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0));
-      v[j] += __hiloint2double((int)hi, (int)lo);
+      s_fs[j][threadIdx.x] += __hiloint2double((int)hi, (int)lo);
     }
   }
-  const double tot = cta_sum9(v, s_fs, threadIdx.x);
+  const double tot = cta_tree9(s_fs, threadIdx.x);
   if (threadIdx.x < 9) {
     double* fs = P.fshift + 9 * g.lrank + threadIdx.x;
     *fs = *fs + tot;
@@ -178,7 +185,7 @@ template <int W>
 __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_constant__ ExParams P) {
   __shared__ GRec g;
   __shared__ uint64_t s_seq;
-  __shared__ double s_fs[kThreads / 32][9];
+  __shared__ double s_fs[9][kThreads];
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[1][blockIdx.x][0] = gtimer();
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     if (g.kind == kItemFshift) {
-      if (P.fshift != nullptr && !(P.debug & 2)) fshift_combine(g, P, tag, s_fs);
+      if (P.fshift != nullptr) fshift_combine(g, P, tag, s_fs);
       __syncthreads();
       if (trace) {
         const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
@@ -250,10 +257,9 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
       }
     }
     if (part) {  // this item's shift-force partial -> its own slot, then its flag
-      double pv[9];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) pv[j] = (threadIdx.x < S && c == j % 3) ? acc[j / 3] : 0.0;
-      const double tot = (P.debug & 1) ? 0.0 : cta_sum9(pv, s_fs, threadIdx.x);
+      for (int j = 0; j < 9; ++j) s_fs[j][threadIdx.x] = (threadIdx.x < S && c == j % 3) ? acc[j / 3] : 0.0;
+      const double tot = cta_tree9(s_fs, threadIdx.x);
       if (threadIdx.x < 9) {  // tagged halves: the combine needs no flag and no fence
         st_relaxed_gpu(g.part + 2 * threadIdx.x,
                        ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));
