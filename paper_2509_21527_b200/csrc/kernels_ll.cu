@@ -166,12 +166,30 @@ __device__ __forceinline__ double cta_sum9(const double* v, double (*s_red)[kThr
 __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_fs)[kThreads]) {
 #pragma unroll
   for (int j = 0; j < 9; ++j) s_fs[j][threadIdx.x] = 0.0;
-  for (uint32_t sl = threadIdx.x; sl < g.n_slots; sl += blockDim.x) {
-    const uint64_t* u = g.part + 18 * (size_t)sl;
-    for (int j = 0; j < 9; ++j) {
-      const uint32_t hi = __float_as_uint(ll_wait(u + 2 * j, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0));
-      const uint32_t lo = __float_as_uint(ll_wait(u + 2 * j + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0));
-      s_fs[j][threadIdx.x] += __hiloint2double((int)hi, (int)lo);
+  // pair p = slot * 9 + j owns LL units 2p (hi word) and 2p + 1 (lo word); each
+  // thread takes a fixed set of pairs and issues up to 8 pairs' loads at once
+  const uint32_t n_pairs = g.n_slots * 9;
+  constexpr int kB = 8;
+  for (uint32_t base = threadIdx.x; base < n_pairs; base += kB * blockDim.x) {
+    uint64_t hv[kB], lv[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const uint32_t pp = base + k * blockDim.x;
+      if (pp < n_pairs) {
+        hv[k] = ld_relaxed_sys(g.part + 2 * (size_t)pp);
+        lv[k] = ld_relaxed_sys(g.part + 2 * (size_t)pp + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const uint32_t pp = base + k * blockDim.x;
+      if (pp < n_pairs) {
+        if ((uint32_t)(hv[k] >> 32) != tag)
+          hv[k] = ll_spin(g.part + 2 * (size_t)pp, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0);
+        if ((uint32_t)(lv[k] >> 32) != tag)
+          lv[k] = ll_spin(g.part + 2 * (size_t)pp + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0);
+        s_fs[pp % 9][threadIdx.x] += __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
+      }
     }
   }
   const double tot = cta_tree9(s_fs, threadIdx.x);
