@@ -472,18 +472,43 @@ static int coop_enabled() {
   return v;
 }
 
-cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args, cudaStream_t st) {
+static int pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HALO_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
+// Exchange-kernel launch: cooperative (every CTA co-resident)
+// unless HALO_COOP=0; `pdl` adds programmatic stream serialisation (the kernel
+// is scheduled while its predecessor drains and blocks in griddepcontrol.wait).
+cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (coop_enabled()) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  }
+  if (pdl && pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = coop_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args, cudaStream_t st) {
+  return launch_coop_kernel_ex(fn, grid, block, args, st, false);
 }
 
 cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStream_t st) {

@@ -72,6 +72,10 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[0][blockIdx.x][0] = gtimer();
+  pdl_launch_dependents();
+  // the plan record is static: load it while the previous kernel drains (PDL)
+  if ((int)blockIdx.x < P.n_items) load_rec(&r, P.xrec + blockIdx.x);
+  pdl_wait();  // everything below may depend on earlier work of the stream
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
   __syncthreads();
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
   const uint32_t arrived = launch_arrive(&ctrl->done_x);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    load_rec(&r, P.xrec + it);
+    if (it != (int)blockIdx.x) load_rec(&r, P.xrec + it);
     __syncthreads();
     if (trace && seq == 0) ctrl->trace[0][blockIdx.x][1] = gtimer();
     seq = s_seq;
@@ -207,13 +211,16 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[1][blockIdx.x][0] = gtimer();
+  pdl_launch_dependents();
+  if ((int)blockIdx.x < P.n_items) load_rec(&g, P.grec + blockIdx.x);  // static: before the PDL wait
+  pdl_wait();
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
   timer_start(P.flags, &ctrl->t_start_f);
   __syncthreads();
   const uint32_t arrived = launch_arrive(&ctrl->done_f);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    load_rec(&g, P.grec + it);
+    if (it != (int)blockIdx.x) load_rec(&g, P.grec + it);
     __syncthreads();
     if (trace && seq == 0) ctrl->trace[1][blockIdx.x][1] = gtimer();
     seq = s_seq;
@@ -302,18 +309,18 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
 }
 
 // ------------------------------------------------------------- launchers
-cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args, cudaStream_t st);
+cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl);
 
 cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, cudaStream_t st) {
   void* args[] = {(void*)&p};
   const void* fn = layout == 4 ? (const void*)k_exchange_x_ll<4> : (const void*)k_exchange_x_ll<3>;
-  return launch_coop_kernel(fn, grid, kThreads, args, st);
+  return launch_coop_kernel_ex(fn, grid, kThreads, args, st, true);
 }
 
 cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, cudaStream_t st) {
   void* args[] = {(void*)&p};
   const void* fn = layout == 4 ? (const void*)k_exchange_f_ll<4> : (const void*)k_exchange_f_ll<3>;
-  return launch_coop_kernel(fn, grid, kThreads, args, st);
+  return launch_coop_kernel_ex(fn, grid, kThreads, args, st, true);
 }
 
 cudaError_t max_coresident_ll(int layout, int* x_blocks, int* f_blocks) {

@@ -54,6 +54,11 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
   return v;
 }
 
+// Programmatic dependent launch (sm_90+): let the next kernel of the stream be
+// scheduled now, and block until the previous kernel's memory is complete.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Report a timeout once: host-mapped word (system scope) + give up.
 static __device__ __noinline__ void report_timeout(int* err_host, int code) {
   volatile int* e = err_host;

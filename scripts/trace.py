@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-fshift", action="store_true")
+    ap.add_argument("--queue", type=int, default=0, help="queue this many un-synchronised steps before the traced one")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -56,12 +57,20 @@ def main():
     fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream()
     out = []
+    F0_all = torch.zeros_like(sess.f_all)
+    for l in range(nl):
+        F0_all[l, : F0[l].shape[0]] = F0[l]
     for k in range(args.steps):
         if world > 1:
             torch.cuda.synchronize()
             dist.barrier()  # start every traced step together (host skew is not kernel time)
-        for l in range(nl):
-            sess.f[l][: F0[l].shape[0]].copy_(F0[l])
+        for _ in range(args.queue):  # steady state: the host runs ahead of the GPU
+            sess.f_all.copy_(F0_all)
+            if args.flush:
+                flush.fill_(1.0)
+            sess.exchange_x()
+            sess.exchange_f(fshift=None if args.no_fshift else fshift)
+        sess.f_all.copy_(F0_all)
         if args.flush:
             flush.fill_(1.0)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
