@@ -463,11 +463,16 @@ __global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t ba
 }
 
 // ------------------------------------------------------------- host launchers
+// Cooperative launch (hardware-checked co-residency) is opt-in (HALO_COOP=1):
+// it disables programmatic dependent launch, which hides ~4 us of launch gap per
+// kernel.  Without it, co-residency holds because the grid never exceeds the
+// occupancy-computed capacity and PDL dependents are only scheduled once every
+// CTA of the primary grid is resident.
 static int coop_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HALO_COOP");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v;
 }

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-fshift", action="store_true")
+    ap.add_argument("--no-mid-event", action="store_true", help="no event between x and f (keeps PDL)")
     ap.add_argument("--queue", type=int, default=0, help="queue this many un-synchronised steps before the traced one")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
@@ -76,7 +77,8 @@ def main():
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(st)
         sess.exchange_x()
-        e1.record(st)
+        if not args.no_mid_event:
+            e1.record(st)
         sess.exchange_f(fshift=None if args.no_fshift else fshift)
         e2.record(st)
         torch.cuda.synchronize()
@@ -84,8 +86,9 @@ def main():
         tf = sess.halo.get_trace(1).astype(np.int64)
         t0 = tx[:, 0].min()
         res = {
-            "step": k, "rank": rank, "x_event_us": round(e0.elapsed_time(e1) * 1e3, 2),
-            "f_event_us": round(e1.elapsed_time(e2) * 1e3, 2), "x_ctas": int(tx.shape[0]), "f_ctas": int(tf.shape[0]),
+            "step": k, "rank": rank, "x_event_us": (round(e0.elapsed_time(e1) * 1e3, 2) if not args.no_mid_event else None),
+            "f_event_us": (round(e1.elapsed_time(e2) * 1e3, 2) if not args.no_mid_event else None),
+            "step_event_us": round(e0.elapsed_time(e2) * 1e3, 2), "x_ctas": int(tx.shape[0]), "f_ctas": int(tf.shape[0]),
             "x_start": q((tx[:, 0] - t0) / 1e3), "x_rec": q((tx[:, 1] - t0) / 1e3),
             "x_done": q((tx[:, 2] - t0) / 1e3), "x_exit": q((tx[:, 3] - t0) / 1e3),
             "gap_x_exit_to_f_start": round(float((tf[:, 0].min() - tx[:, 3].max()) / 1e3), 2),
