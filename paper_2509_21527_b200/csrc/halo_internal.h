@@ -9,6 +9,7 @@
 //               [..., ...)               P force receive buffers, flag protocol (capacity rows each)
 //               [..., ...)               P coordinate LL receive buffers (capacity*layout u64 units)
 //               [..., ...)               P force LL receive buffers (capacity*layout u64 units)
+//               [..., ...)               P shift-force slot areas (ceil(capacity/32) slots of 6 u64 units)
 //             An LL unit is {fp32 value (low word), 32-bit sequence tag (high word)}
 //             written with one 8-byte store: single-copy atomic, so a reader that
 //             sees the current tag sees the value (no fence, no flag).
@@ -27,6 +28,7 @@ constexpr int kMaxRanks = HALO_MAX_RANKS;
 constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
 constexpr int kHdrBytes = 4096;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
+constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-force slot area)
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
 struct __align__(128) ScratchHdr {
@@ -147,19 +149,18 @@ struct __align__(128) GRec {
   uint8_t level;            // slice of this pulse, or kHomeLevel
   uint16_t lrank;
   uint32_t n_units;         // gather: tasks * layout
-  uint32_t wrap_mask;       // fshift: pulses this rank shifted in (R13)
+  uint32_t wrap_mask;       // combine: pulses this rank shifted in (R13)
   uint8_t pulse_dim[8];
   uint32_t pad;
   const int4* tasks;        // gather: 32-B task records (row, n, contrib[6]) + begin
   float* f;                 // gather: own f base
   const uint64_t* fll_own;  // own force LL base (slot q at + q*ll_stride)
   uint64_t* push;           // gather of slice rows: x-sender's LL slot p minus recv_off_p*W (index row*W + c)
-  uint64_t* part;           // gather: this item's fshift partial slot (9 doubles as 18 LL units: hi, lo
-                            // words); combine: slot 0
-  uint64_t* pflag;          // unused (kept for layout)
-  uint32_t n_slots;         // combine: gather items of this rank
-  uint32_t pad3;
-  uint8_t pad2[128 - 80];   // keep one 128-B line
+  uint64_t* part;           // gather of a slice whose x-sender shifted in that pulse: the x-sender's
+                            // shift-force slot of this item (3 doubles = 6 LL units, peer pointer);
+                            // combine: own shift-force slot area
+  uint32_t nslot[kMaxP];    // combine: slots of each pulse (0 unless this rank shifted in it)
+  uint8_t pad2[128 - 88];   // keep one 128-B line
 };
 static_assert(sizeof(GRec) == 128, "GRec must be one 128-B line");
 
@@ -180,6 +181,7 @@ struct ExParams {
   uint32_t poll_ns;         // __nanosleep between flag polls (0 = tight spin)
   uint64_t ll_stride;       // u64 units per pulse slot of the LL receive buffers
   uint32_t debug;           // HALO_DEBUG experiment bits (0 in production)
+  uint32_t fsp_slots;       // shift-force slots per pulse in each rank's scratch
   const XRec* xrec;         // LL protocol work records (x)
   const GRec* grec;         // LL protocol work records (f)
 };

@@ -30,7 +30,7 @@ __device__ __forceinline__ uint64_t ll_pack(float v, uint32_t tag) {
 }
 
 // Slow path: poll one LL unit until it carries `tag`; bounded like every wait.
-__device__ __noinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
+__device__ __forceinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
                                          int code, uint32_t sleep_ns) {
   uint64_t t0 = 0;
   for (uint32_t it = 1;; ++it) {
@@ -157,46 +157,52 @@ __device__ __forceinline__ double cta_tree9(double (*s_red)[kThreads], int j_out
   return tot;
 }
 
+__device__ __forceinline__ double cta_tree3(double (*s_red)[kThreads], int j_out) {
+  for (int h = kThreads / 2; h > 0; h >>= 1) {
+    __syncthreads();
+    if ((int)threadIdx.x < h)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) s_red[j][threadIdx.x] += s_red[j][threadIdx.x + h];
+  }
+  __syncthreads();
+  const double tot = (j_out < 3) ? s_red[j_out][0] : 0.0;
+  __syncthreads();
+  return tot;
+}
+
 __device__ __forceinline__ double cta_sum9(const double* v, double (*s_red)[kThreads], int j_out) {
 #pragma unroll
   for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] = v[j];
   return cta_tree9(s_red, j_out);
 }
 
-// Combine item of one rank (R13): polls every gather item's shift-force partial
-// (9 doubles stored as tagged LL units, so no flag and no fence) and adds their
-// fixed-order sum to fshift.  Only this CTA writes the rank's fshift:
-// deterministic, no atomics.
-__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_fs)[kThreads]) {
+// Combine item of one rank (R13): the pushers of its wrapping pulses summed,
+// per work item, the forces they pushed back to it (3 doubles per slot as tagged
+// LL units: no flag, no fence).  One thread per (pulse, slot, component) triple
+// in a fixed assignment, then a fixed tree: deterministic, no atomics; only this
+// CTA writes the rank's fshift.
+__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_red)[kThreads],
+                                            uint32_t fsp_slots) {
 #pragma unroll
-  for (int j = 0; j < 9; ++j) s_fs[j][threadIdx.x] = 0.0;
-  // pair p = slot * 9 + j owns LL units 2p (hi word) and 2p + 1 (lo word); each
-  // thread takes a fixed set of pairs and issues up to 8 pairs' loads at once
-  const uint32_t n_pairs = g.n_slots * 9;
-  constexpr int kB = 8;
-  for (uint32_t base = threadIdx.x; base < n_pairs; base += kB * blockDim.x) {
-    uint64_t hv[kB], lv[kB];
-#pragma unroll
-    for (int k = 0; k < kB; ++k) {
-      const uint32_t pp = base + k * blockDim.x;
-      if (pp < n_pairs) {
-        hv[k] = ld_relaxed_sys(g.part + 2 * (size_t)pp);
-        lv[k] = ld_relaxed_sys(g.part + 2 * (size_t)pp + 1);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kB; ++k) {
-      const uint32_t pp = base + k * blockDim.x;
-      if (pp < n_pairs) {
-        if ((uint32_t)(hv[k] >> 32) != tag)
-          hv[k] = ll_spin(g.part + 2 * (size_t)pp, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0);
-        if ((uint32_t)(lv[k] >> 32) != tag)
-          lv[k] = ll_spin(g.part + 2 * (size_t)pp + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0);
-        s_fs[pp % 9][threadIdx.x] += __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
-      }
+  for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] = 0.0;
+  for (int q = 0; q < P.P; ++q) {
+    const uint32_t n = g.nslot[q] * 3;  // (slot, component) pairs of pulse q
+    if (n == 0) continue;
+    const int d = g.pulse_dim[q];
+    const uint64_t* base = g.part + (size_t)q * fsp_slots * 6;
+    for (uint32_t pp = threadIdx.x; pp < n; pp += blockDim.x) {
+      const uint64_t hv = ld_relaxed_sys(base + 2 * (size_t)pp);
+      const uint64_t lv = ld_relaxed_sys(base + 2 * (size_t)pp + 1);
+      const uint32_t hi = (uint32_t)((uint32_t)(hv >> 32) == tag ? hv
+                                      : ll_spin(base + 2 * (size_t)pp, tag, P.timeout_ns, P.err_host,
+                                                tcode(13, g.lrank, q), 0));
+      const uint32_t lo = (uint32_t)((uint32_t)(lv >> 32) == tag ? lv
+                                      : ll_spin(base + 2 * (size_t)pp + 1, tag, P.timeout_ns, P.err_host,
+                                                tcode(13, g.lrank, q), 0));
+      s_red[3 * d + (int)(pp % 3)][threadIdx.x] += __hiloint2double((int)hi, (int)lo);
     }
   }
-  const double tot = cta_tree9(s_fs, threadIdx.x);
+  const double tot = cta_tree9(s_red, threadIdx.x);
   if (threadIdx.x < 9) {
     double* fs = P.fshift + 9 * g.lrank + threadIdx.x;
     *fs = *fs + tot;
@@ -204,7 +210,7 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
 }
 
 template <int W>
-__global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_constant__ ExParams P) {
+__global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
   __shared__ GRec g;
   __shared__ uint64_t s_seq;
   __shared__ double s_fs[9][kThreads];
@@ -212,7 +218,18 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[1][blockIdx.x][0] = gtimer();
   pdl_launch_dependents();
-  if ((int)blockIdx.x < P.n_items) load_rec(&g, P.grec + blockIdx.x);  // static: before the PDL wait
+  // static plan data (work record, first gather task record) is loaded while the
+  // previous kernel of the stream drains (PDL); f itself is read after the wait
+  int4 pre_a = make_int4(0, 0, 0, 0), pre_b = make_int4(0, 0, 0, 0);
+  if ((int)blockIdx.x < P.n_items) {
+    load_rec(&g, P.grec + blockIdx.x);
+    __syncthreads();
+    if (g.kind == kItemGather && threadIdx.x < (blockDim.x / W) * W && threadIdx.x < g.n_units) {
+      const uint32_t k = threadIdx.x / W;
+      pre_a = __ldg(g.tasks + 2 * k);
+      pre_b = __ldg(g.tasks + 2 * k + 1);
+    }
+  }
   pdl_wait();
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
   timer_start(P.flags, &ctrl->t_start_f);
@@ -220,13 +237,16 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
   const uint32_t arrived = launch_arrive(&ctrl->done_f);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    if (it != (int)blockIdx.x) load_rec(&g, P.grec + it);
+    if (it != (int)blockIdx.x) {
+      __syncthreads();  // everyone is done with the previous record
+      load_rec(&g, P.grec + it);
+    }
     __syncthreads();
     if (trace && seq == 0) ctrl->trace[1][blockIdx.x][1] = gtimer();
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     if (g.kind == kItemFshift) {
-      if (P.fshift != nullptr) fshift_combine(g, P, tag, s_fs);
+      if (P.fshift != nullptr) fshift_combine(g, P, tag, s_fs, P.fsp_slots);
       __syncthreads();
       if (trace) {
         const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
@@ -239,17 +259,23 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
     }
     const uint32_t n = g.n_units;
     const bool push = g.level != kHomeLevel;
+    // this item also sums what it pushes when the receiving x-sender shifted (R13)
     const bool part = (P.fshift != nullptr) && (g.part != nullptr);
-    const uint32_t wrap = part ? g.wrap_mask : 0u;
     // stride = a multiple of W: every thread keeps one component c
     const uint32_t S = (blockDim.x / W) * W;
     const int c = (int)(threadIdx.x % W);
-    double acc[3] = {0.0, 0.0, 0.0};  // shift-force partials of component c, per dim (R13)
+    double acc = 0.0;
     if (threadIdx.x < S) {
       for (uint32_t u = threadIdx.x; u < n; u += S) {
         const uint32_t k = u / W;
-        const int4 a = __ldg(g.tasks + 2 * k);
-        const int4 b = __ldg(g.tasks + 2 * k + 1);
+        int4 a, b;
+        if (u == threadIdx.x && it == (int)blockIdx.x) {
+          a = pre_a;  // prefetched before the PDL wait
+          b = pre_b;
+        } else {
+          a = __ldg(g.tasks + 2 * k);
+          b = __ldg(g.tasks + 2 * k + 1);
+        }
         const int t = a.x, m = a.y;
         const uint32_t cc[kMaxP] = {(uint32_t)a.z, (uint32_t)a.w, (uint32_t)b.x,
                                     (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
@@ -269,27 +295,20 @@ __global__ void __launch_bounds__(kThreads, 5) k_exchange_f_ll(const __grid_cons
                              P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
             const float val = __uint_as_float((uint32_t)w[j]);
             v = P.accumulate ? __fadd_rn(v, val) : val;
-            if (((wrap >> q) & 1u) && c < 3) {
-              const int d = g.pulse_dim[q];
-              if (d == 0) acc[0] += (double)val;
-              else if (d == 1) acc[1] += (double)val;
-              else acc[2] += (double)val;
-            }
           }
         }
         g.f[(size_t)t * W + c] = v;
         if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
+        if (part) acc += (double)v;
       }
     }
-    if (part) {  // this item's shift-force partial -> its own slot, then its flag
+    if (part) {  // fixed-tree CTA sum of the pushed forces per component -> the x-sender's slot
 #pragma unroll
-      for (int j = 0; j < 9; ++j) s_fs[j][threadIdx.x] = (threadIdx.x < S && c == j % 3) ? acc[j / 3] : 0.0;
-      const double tot = cta_tree9(s_fs, threadIdx.x);
-      if (threadIdx.x < 9) {  // tagged halves: the combine needs no flag and no fence
-        st_relaxed_gpu(g.part + 2 * threadIdx.x,
-                       ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));
-        st_relaxed_gpu(g.part + 2 * threadIdx.x + 1,
-                       ll_pack(__uint_as_float((uint32_t)__double2loint(tot)), tag));
+      for (int j = 0; j < 3; ++j) s_fs[j][threadIdx.x] = (threadIdx.x < S && c == j) ? acc : 0.0;
+      const double tot = cta_tree3(s_fs, threadIdx.x);
+      if (threadIdx.x < 3) {
+        st_relaxed_sys(g.part + 2 * threadIdx.x, ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));
+        st_relaxed_sys(g.part + 2 * threadIdx.x + 1, ll_pack(__uint_as_float((uint32_t)__double2loint(tot)), tag));
       }
     }
     __syncthreads();

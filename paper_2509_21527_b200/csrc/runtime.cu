@@ -80,7 +80,7 @@ struct halo_ctx {
   halo_config cfg{};
   int nranks = 0, n_local = 0, first_rank = 0, P = 0, W = 3;
   int pdim[kMaxP] = {0}, pk[kMaxP] = {0};
-  size_t map_stride = 0, fbuf_stride = 0, ll_stride = 0, scratch_bytes = 0;
+  size_t map_stride = 0, fbuf_stride = 0, ll_stride = 0, fsp_slots = 0, scratch_bytes = 0;
   bool ll = true;                   // LL protocol (default) vs the paper's flag protocol
   std::string last_error;
 
@@ -114,8 +114,7 @@ struct halo_ctx {
   std::vector<GRec> h_grec;
   XRec* d_xrec = nullptr;
   GRec* d_grec = nullptr;
-  char* d_fsp = nullptr;            // fshift partial slots + flags (LL protocol)
-  size_t fsp_bytes = 0;
+
   std::vector<std::vector<int>> level_begin;  // [local][P+2]: task index where level P-1..0, home start
 
   // host plan
@@ -159,6 +158,7 @@ struct halo_ctx {
                                        (size_t)P * fbuf_stride * sizeof(float));
   }
   uint64_t* fll_of(int r) const { return xll_of(r) + (size_t)P * ll_stride; }
+  uint64_t* fsp_of(int r) const { return fll_of(r) + (size_t)P * ll_stride; }  // 6 units per slot
 };
 
 // --------------------------------------------------------------------- helpers
@@ -182,15 +182,16 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // Scratch layout of one DD rank (halo_internal.h): header | maps | force
 // buffers (paper protocol) | coordinate LL buffers | force LL buffers.
 struct ScratchLayout {
-  size_t map_stride, fbuf_stride, ll_stride, total;
+  size_t map_stride, fbuf_stride, ll_stride, fsp_slots, total;
 };
 static ScratchLayout scratch_layout(int P, int capacity, int layout) {
   ScratchLayout L;
   L.map_stride = align_up((size_t)capacity, 64);                // int32 per pulse slot
   L.fbuf_stride = align_up((size_t)capacity * layout, 64);      // fp32 per pulse slot
   L.ll_stride = align_up((size_t)capacity * layout, 32);        // u64 units per pulse slot
+  L.fsp_slots = align_up(((size_t)capacity + kMinItemRows - 1) / kMinItemRows, 8);  // shift-force slots per pulse
   L.total = kHdrBytes + (size_t)P * L.map_stride * sizeof(int32_t) + (size_t)P * L.fbuf_stride * sizeof(float) +
-            2 * (size_t)P * L.ll_stride * sizeof(uint64_t);
+            2 * (size_t)P * L.ll_stride * sizeof(uint64_t) + (size_t)P * L.fsp_slots * 6 * sizeof(uint64_t);
   return L;
 }
 
@@ -282,6 +283,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     ctx->map_stride = SL.map_stride;
     ctx->fbuf_stride = SL.fbuf_stride;
     ctx->ll_stride = SL.ll_stride;
+    ctx->fsp_slots = SL.fsp_slots;
     ctx->scratch_bytes = SL.total;
   }
   ctx->ll = !(cfg->flags & HALO_F_PAPER_FLAGS);
@@ -695,11 +697,11 @@ static void build_f_items_ll(halo_ctx* ctx) {
       const uint8_t level = k < P ? (uint8_t)(P - 1 - k) : kHomeLevel;
       add_items(v, l, level, kItemGather, lb[k], lb[k + 1], R);
     }
-  // shift-force combines last: each waits for its rank's gather partials
+  // shift-force combines last: each waits for the partials its pushers wrote
   for (int l = 0; l < ctx->n_local; ++l) {
     const int rk = ctx->first_rank + l;
     bool wraps = false;
-    for (int q = 0; q < P; ++q) wraps |= ctx->cell(rk, ctx->pdim[q]) == 0;
+    for (int q = 0; q < P; ++q) wraps |= ctx->cell(rk, ctx->pdim[q]) == 0 && ctx->send_size[l * P + q] > 0;
     if (!wraps) continue;
     Item it;
     it.lrank = (uint16_t)l;
@@ -743,38 +745,14 @@ static void build_xrec(halo_ctx* ctx) {
 }
 
 static halo_status build_grec(halo_ctx* ctx) {
-  const int W = ctx->W, P = ctx->P, L = ctx->n_local;
-  // fshift partial slots: one per gather item of a rank that shifts in some pulse
-  std::vector<int> nslot(L, 0), wraps(L, 0);
-  for (int l = 0; l < L; ++l)
-    for (int q = 0; q < P; ++q)
-      if (ctx->cell(ctx->first_rank + l, ctx->pdim[q]) == 0) wraps[l] = 1;
-  for (const Item& w : ctx->h_items_f)
-    if (w.kind == kItemGather && wraps[w.lrank]) nslot[w.lrank]++;
-  std::vector<size_t> part_off(L), flag_off(L);
-  size_t need = 0;
-  for (int l = 0; l < L; ++l) {  // 18 tagged LL units (hi/lo words of 9 doubles) per slot
-    part_off[l] = need;
-    need += align_up(sizeof(uint64_t) * 18 * std::max(nslot[l], 1), 256);
-    flag_off[l] = need;
-    need += 256;
-  }
-  if (need > ctx->fsp_bytes) {
-    if (ctx->d_fsp) CK(cudaFree(ctx->d_fsp));
-    ctx->d_fsp = nullptr;
-    CK(cudaMalloc(&ctx->d_fsp, need));
-    CK(cudaMemset(ctx->d_fsp, 0, need));  // flags start below every sequence number
-    ctx->fsp_bytes = need;
-  }
-  std::vector<int> next(L, 0);
+  const int W = ctx->W, P = ctx->P;
+  const int R = ctx->item_rows;
   ctx->h_grec.assign(ctx->h_items_f.size(), GRec{});
   for (size_t k = 0; k < ctx->h_items_f.size(); ++k) {
     const Item& w = ctx->h_items_f[k];
     GRec& g = ctx->h_grec[k];
     memset(&g, 0, sizeof g);
     const int l = w.lrank, rk = ctx->first_rank + l;
-    uint64_t* part = reinterpret_cast<uint64_t*>(ctx->d_fsp + part_off[l]);
-    uint64_t* pflag = reinterpret_cast<uint64_t*>(ctx->d_fsp + flag_off[l]);
     g.kind = w.kind;
     g.level = w.pulse;
     g.lrank = (uint16_t)l;
@@ -788,19 +766,22 @@ static halo_status build_grec(halo_ctx* ctx) {
     g.fll_own = ctx->fll_of(rk);
     if (w.kind == kItemGather) {
       g.tasks = ctx->csr_tasks[l] + 2 * (size_t)w.begin;
-      if (wraps[l]) {
-        g.part = part + 18 * (size_t)next[l];
-        g.pflag = pflag + next[l];
-        next[l]++;
-      }
       if (w.pulse != kHomeLevel) {
-        const PulseDev& pd = ctx->h_pulses[l * P + w.pulse];
-        g.push = pd.fll_dst - (ptrdiff_t)ctx->atom_offset[l * P + w.pulse] * W;
+        const int p = w.pulse;
+        const PulseDev& pd = ctx->h_pulses[l * P + p];
+        g.push = pd.fll_dst - (ptrdiff_t)ctx->atom_offset[l * P + p] * W;
+        // the x-sender of pulse p (upper neighbour) shifted these rows iff its cell is 0:
+        // this item also sums what it pushes into that rank's shift-force slot
+        const int upper = ctx->neighbour(rk, ctx->pdim[p], +1);
+        if (ctx->cell(upper, ctx->pdim[p]) == 0) {
+          const int slot = (int)(w.begin - ctx->level_begin[l][P - 1 - p]) / R;
+          g.part = ctx->fsp_of(upper) + ((size_t)p * ctx->fsp_slots + slot) * 6;
+        }
       }
-    } else {  // kItemFshift: combine of the rank's slots
-      g.part = part;
-      g.pflag = pflag;
-      g.n_slots = (uint32_t)nslot[l];
+    } else {  // kItemFshift: combine of the slots the pushers wrote into this rank
+      g.part = ctx->fsp_of(rk);
+      for (int q = 0; q < P; ++q)
+        g.nslot[q] = (g.wrap_mask >> q & 1u) ? (uint32_t)((ctx->send_size[l * P + q] + R - 1) / R) : 0u;
     }
   }
   return HALO_OK;
@@ -862,6 +843,7 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.accumulate = 1;
   P.poll_ns = ctx->poll_ns;
   P.debug = ctx->debug;
+  P.fsp_slots = (uint32_t)ctx->fsp_slots;
   P.ll_stride = ctx->ll_stride;
   P.xrec = ctx->d_xrec;
   P.grec = ctx->d_grec;
@@ -1322,7 +1304,6 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_small) (void)cudaFree(ctx->d_small);
   if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
   if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
-  if (ctx->d_fsp) (void)cudaFree(ctx->d_fsp);
   if (ctx->err_host) (void)cudaFreeHost(ctx->err_host);
   (void)cudaGetLastError();
   delete ctx;

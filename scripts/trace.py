@@ -96,13 +96,16 @@ def main():
             "f_done": q((tf[:, 2] - t0) / 1e3), "f_exit": q((tf[:, 3] - t0) / 1e3),
         }
         # per (kind, level) item end quantiles, relative to the kernel's first CTA start
+        x_end = tx[:, 3].max()
         for nm, tr in (("x", tx), ("f", tf)):
-            tk0 = tr[:, 0].min()
+            # x items: relative to the x kernel's first CTA; f items: relative to the
+            # x kernel's last exit (with PDL the f CTAs start before it)
+            tk0 = tr[:, 0].min() if nm == "x" else x_end
             groups = {}
             for row in tr:
                 for sl in range(2):
                     tag, end = int(row[4 + 2 * sl]), int(row[5 + 2 * sl])
-                    if end == 0 or end < tk0:
+                    if end == 0 or end < tr[:, 0].min():
                         continue
                     key = f"k{tag >> 16}_p{tag & 0xff}"
                     groups.setdefault(key, []).append((end - tk0) / 1e3)
