@@ -29,6 +29,7 @@ constexpr int kThreads = 256;          // threads per CTA of the exchange kernel
 constexpr int kHdrBytes = 4096;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
 constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-force slot area)
+constexpr int kMaxItemRows = 512;      // largest work item (x items carry their map slice in shared memory)
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
 struct __align__(128) ScratchHdr {
@@ -183,6 +184,8 @@ struct ExParams {
   uint32_t debug;           // HALO_DEBUG experiment bits (0 in production)
   uint32_t fsp_slots;       // shift-force slots per pulse in each rank's scratch
   const XRec* xrec;         // LL protocol work records (x)
+  const int32_t* xmap;      // per x item: its map slice (item_rows entries), loaded with the record
+  int item_rows;
   const GRec* grec;         // LL protocol work records (f)
 };
 

@@ -69,12 +69,17 @@ template <int W>
 __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constant__ ExParams P) {
   __shared__ XRec r;
   __shared__ uint64_t s_seq;
+  __shared__ int32_t s_map[kMaxItemRows];
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[0][blockIdx.x][0] = gtimer();
   pdl_launch_dependents();
-  // the plan record is static: load it while the previous kernel drains (PDL)
-  if ((int)blockIdx.x < P.n_items) load_rec(&r, P.xrec + blockIdx.x);
+  // the plan record and its map slice are static: one round trip, issued while
+  // the previous kernel drains (PDL)
+  if ((int)blockIdx.x < P.n_items) {
+    load_rec(&r, P.xrec + blockIdx.x);
+    for (int t = threadIdx.x; t < P.item_rows; t += blockDim.x) s_map[t] = __ldg(P.xmap + (size_t)blockIdx.x * P.item_rows + t);
+  }
   pdl_wait();  // everything below may depend on earlier work of the stream
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
@@ -83,7 +88,11 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
   const uint32_t arrived = launch_arrive(&ctrl->done_x);
   uint64_t seq = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    if (it != (int)blockIdx.x) load_rec(&r, P.xrec + it);
+    if (it != (int)blockIdx.x) {
+      __syncthreads();  // everyone is done with the previous record
+      load_rec(&r, P.xrec + it);
+      for (int t = threadIdx.x; t < P.item_rows; t += blockDim.x) s_map[t] = __ldg(P.xmap + (size_t)it * P.item_rows + t);
+    }
     __syncthreads();
     if (trace && seq == 0) ctrl->trace[0][blockIdx.x][1] = gtimer();
     seq = s_seq;
@@ -99,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
       for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) {
         const uint32_t i = u / W;
         const int c = (int)(u - i * W);
-        const int idx = __ldg(r.map + i);
+        const int idx = s_map[i];
         float v;
         if (!dep) {
           v = __ldg(r.x + (size_t)idx * W + c);  // home row: never written during the kernel

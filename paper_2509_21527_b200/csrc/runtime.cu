@@ -111,6 +111,9 @@ struct halo_ctx {
   size_t csr_bytes = 0;
   std::vector<int4*> csr_tasks;     // per local rank: 32-B task records (row, n, contrib[6])
   std::vector<XRec> h_xrec;
+  std::vector<int32_t> h_xmap;          // per x item: its map slice (item_rows entries), loaded with the record
+  std::vector<std::vector<std::vector<int32_t>>> h_maps;  // host copy of every local rank's maps [l][p]
+  int32_t* d_xmap = nullptr;
   std::vector<GRec> h_grec;
   XRec* d_xrec = nullptr;
   GRec* d_grec = nullptr;
@@ -292,7 +295,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   ctx->scratch.assign(ctx->n_local, nullptr);
   ctx->peer_x.assign(ctx->nranks, nullptr);
   ctx->peer_scratch.assign(ctx->nranks, nullptr);
-  if (const char* e = getenv("HALO_ITEM_ROWS")) ctx->item_rows = std::max(32, atoi(e));
+  if (const char* e = getenv("HALO_ITEM_ROWS")) ctx->item_rows = std::min(kMaxItemRows, std::max(kMinItemRows, atoi(e)));
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = (uint32_t)std::max(0, atoi(e));
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
@@ -608,15 +611,7 @@ static halo_status build_csr(halo_ctx* ctx, cudaStream_t st) {
     const int nt = ctx->n_total[l], nh = ctx->n_home[l];
     std::vector<int> cnt(nt, 0);
     std::vector<uint8_t> mask(nt, 0);
-    std::vector<std::vector<int32_t>> maps(P);
-    for (int q = 0; q < P; ++q) {
-      const int n = ctx->send_size[l * P + q];
-      maps[q].resize(n);
-      if (n)
-        CK(cudaMemcpyAsync(maps[q].data(), ctx->maps_of_local(l) + (size_t)q * ctx->map_stride, sizeof(int32_t) * n,
-                           cudaMemcpyDeviceToHost, st));
-    }
-    CK(cudaStreamSynchronize(st));
+    const std::vector<std::vector<int32_t>>& maps = ctx->h_maps[l];
     for (int q = 0; q < P; ++q)
       for (int32_t t : maps[q]) {
         cnt[t]++;
@@ -714,8 +709,9 @@ static void build_f_items_ll(halo_ctx* ctx) {
 
 // 128-B work records of the LL kernels, one per item (halo_internal.h XRec/GRec).
 static void build_xrec(halo_ctx* ctx) {
-  const int W = ctx->W, P = ctx->P;
+  const int W = ctx->W, P = ctx->P, R = ctx->item_rows;
   ctx->h_xrec.assign(ctx->h_items_x.size(), XRec{});
+  ctx->h_xmap.assign(ctx->h_items_x.size() * (size_t)R, 0);
   for (size_t k = 0; k < ctx->h_items_x.size(); ++k) {
     const Item& w = ctx->h_items_x[k];
     XRec& r = ctx->h_xrec[k];
@@ -740,6 +736,8 @@ static void build_xrec(halo_ctx* ctx) {
     } else {
       r.map = pd.map + w.begin;
       r.ll = pd.xll_dst + (size_t)w.begin * W;
+      const auto& m = ctx->h_maps[l][p];
+      std::copy(m.begin() + w.begin, m.begin() + w.end, ctx->h_xmap.begin() + k * (size_t)R);
     }
   }
 }
@@ -795,7 +793,8 @@ static halo_status upload_plan(halo_ctx* ctx) {
   const size_t nf = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_f.size()), a);
   const size_t nxr = align_up(sizeof(XRec) * std::max<size_t>(1, ctx->h_xrec.size()), a);
   const size_t ngr = align_up(sizeof(GRec) * std::max<size_t>(1, ctx->h_grec.size()), a);
-  const size_t need = nr + np + nx + nf + nxr + ngr;
+  const size_t nxm = align_up(sizeof(int32_t) * std::max<size_t>(1, ctx->h_xmap.size()), a);
+  const size_t need = nr + np + nx + nf + nxr + ngr + nxm;
   if (need > ctx->plan_bytes) {
     if (ctx->plan) CK(cudaFree(ctx->plan));
     ctx->plan = nullptr;
@@ -808,6 +807,9 @@ static halo_status upload_plan(halo_ctx* ctx) {
   ctx->d_items_f = reinterpret_cast<Item*>(ctx->plan + nr + np + nx);
   ctx->d_xrec = reinterpret_cast<XRec*>(ctx->plan + nr + np + nx + nf);
   ctx->d_grec = reinterpret_cast<GRec*>(ctx->plan + nr + np + nx + nf + nxr);
+  ctx->d_xmap = reinterpret_cast<int32_t*>(ctx->plan + nr + np + nx + nf + nxr + ngr);
+  if (!ctx->h_xmap.empty())
+    CK(cudaMemcpy(ctx->d_xmap, ctx->h_xmap.data(), sizeof(int32_t) * ctx->h_xmap.size(), cudaMemcpyHostToDevice));
   if (!ctx->h_xrec.empty())
     CK(cudaMemcpy(ctx->d_xrec, ctx->h_xrec.data(), sizeof(XRec) * ctx->h_xrec.size(), cudaMemcpyHostToDevice));
   if (!ctx->h_grec.empty())
@@ -846,6 +848,8 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.fsp_slots = (uint32_t)ctx->fsp_slots;
   P.ll_stride = ctx->ll_stride;
   P.xrec = ctx->d_xrec;
+  P.xmap = ctx->d_xmap;
+  P.item_rows = ctx->item_rows;
   P.grec = ctx->d_grec;
   return P;
 }
@@ -883,6 +887,20 @@ static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st) {
   return HALO_OK;
 }
 
+// Host copy of pulse p's maps of every local rank (sizes final after the handshake).
+static halo_status pull_maps(halo_ctx* ctx, int p, cudaStream_t st) {
+  for (int l = 0; l < ctx->n_local; ++l) {
+    const int n = ctx->send_size[l * ctx->P + p];
+    auto& m = ctx->h_maps[l][p];
+    m.resize(n);
+    if (n)
+      CK(cudaMemcpyAsync(m.data(), ctx->maps_of_local(l) + (size_t)p * ctx->map_stride, sizeof(int32_t) * n,
+                         cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return HALO_OK;
+}
+
 // Shared driver of halo_set_maps / halo_set_maps_explicit.
 static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* send_sizes, const int* const* maps,
                                  cudaStream_t st) {
@@ -903,6 +921,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   ctx->n_indep.assign(L * P, 0);
   ctx->dep.assign(L * P, 0u);
   ctx->h_pulses.assign(std::max(1, L * P), PulseDev{});
+  ctx->h_maps.assign(L, std::vector<std::vector<int32_t>>(P));
   int local_err = 0;
   for (int l = 0; l < L; ++l)
     if (n_home[l] < 0 || n_home[l] > ctx->cfg.capacity) local_err |= kErrCapacity;
@@ -1019,6 +1038,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     CK(launch_depmask(ctx->d_ranks, ctx->ctrl, p, (int)ctx->map_stride, L, st));
     if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
     if ((s = check_err_word(ctx)) != HALO_OK) return s;
+    if ((s = pull_maps(ctx, p, st)) != HALO_OK) return s;
     // exchange the coordinates of this pulse now: pulse p+1 forwards them
     for (int l = 0; l < L; ++l)
       for (int q = 0; q <= p; ++q) fill_pulse_dev(ctx, l, q);
