@@ -28,6 +28,8 @@ VARIANTS = {
     "rows64": ({"HALO_ITEM_ROWS": "64"}, 0),
     "rows128": ({"HALO_ITEM_ROWS": "128"}, 0),
     "rows256": ({"HALO_ITEM_ROWS": "256"}, 0),
+    "rows96": ({"HALO_ITEM_ROWS": "96"}, 0),
+    "rows192": ({"HALO_ITEM_ROWS": "192"}, 0),
     "paper": ({}, 16),
     "paper_gpufence": ({}, 16 | 4),
     "rows1024": ({"HALO_ITEM_ROWS": "1024"}, 0),

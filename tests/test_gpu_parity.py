@@ -263,3 +263,22 @@ def test_timers_and_many_steps(proto):
     tx, tf = sess.halo.get_timers()
     assert 0 < tx < 10_000_000 and 0 < tf < 10_000_000
     sess.destroy()
+
+
+@pytest.mark.parametrize("name", ["C4-1D", "C4-2D", "C4-3D"])
+def test_parity_full_size_c4(name):
+    """BASELINE configs[3] at full size (1.07M atoms), every element compared."""
+    case = Case(name, seed=1, force_kind="normal")
+    sess = session_for(case)
+    run_gpu_case(case, sess)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("rows", ["32", "512"])
+def test_parity_item_size_bounds(rows, monkeypatch):
+    """Smallest and largest work items (HALO_ITEM_ROWS is read at halo_init)."""
+    monkeypatch.setenv("HALO_ITEM_ROWS", rows)
+    case = Case("C3", seed=2, force_kind="normal")
+    sess = session_for(case)
+    run_gpu_case(case, sess, steps=2)
+    sess.destroy()
