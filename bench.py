@@ -240,7 +240,9 @@ def run_fused(args, rank, world, local):
     xs = [ev3[k][0].elapsed_time(ev3[k][1]) * 1e3 for k in range(Kx)]
     fs = [ev3[k][1].elapsed_time(ev3[k][2]) * 1e3 for k in range(Kx)]
     my = {"step": float(np.mean(tot)), "x": float(np.mean(xs)), "f": float(np.mean(fs)),
-          "step_median": float(np.median(tot))}
+          "step_median": float(np.median(tot)), "step_p90": float(np.percentile(tot, 90)),
+          "step_p99": float(np.percentile(tot, 99)), "step_max": float(np.max(tot)),
+          "x_median": float(np.median(xs)), "f_median": float(np.median(fs))}
     res = {k: max_over_ranks(v) for k, v in my.items()}
     dev_spans = None
     if args.timers:
@@ -356,6 +358,9 @@ def run_fused(args, rank, world, local):
         "config": dict(workload_desc(c, world, W), parallelism=f"spatial DD {c.grid[0]}x{c.grid[1]}x{c.grid[2]}",
                        mode="eager, one exchange_x + one exchange_f launch per GPU per step"),
         "x_us": round(res["x"], 3), "f_us": round(res["f"], 3), "step_median_us": round(res["step_median"], 3),
+        "step_percentiles_us": {"p90": round(res["step_p90"], 3), "p99": round(res["step_p99"], 3),
+                                "max": round(res["step_max"], 3)},
+        "x_median_us": round(res["x_median"], 3), "f_median_us": round(res["f_median"], 3),
         "x_f_split_note": "x_us / f_us: a separate loop with an event between the two launches (the event "
                           "disables programmatic dependent launch, so x_us + f_us > value)",
         "graph_us_per_step": None if graph_us is None else round(graph_us, 3),
