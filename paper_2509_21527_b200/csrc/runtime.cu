@@ -133,7 +133,7 @@ struct halo_ctx {
   uint64_t ping_base = 0;
   int max_x = 0, max_f = 0;
   int last_grid[2] = {0, 0};
-  int item_rows = 128;
+  int item_rows = 64;
   uint32_t poll_ns = 0;
   uint32_t debug = 0;
 
