@@ -376,15 +376,24 @@ def run_fused(args, rank, world, local):
         "nvlink": {"bytes_per_step_per_gpu_per_direction": int(nvl_bytes),
                    "achieved_gbs": round(nvl_bytes / (res["step"] * 1e-6) / 1e9, 3) if nvl_bytes else 0.0,
                    "peak_gbs": 900.0, "measured_peer_copy_gbs": 770.0},
-        "latency_floor": floor,
+        "latency_floor": floor or None,
         "nccl_baseline": nccl,
         "device_spans": dev_spans,
     }
-    if floor and floor["t0_one_way_us"]:
+    launch_eager = max_over_ranks(sess.halo.floor_launch(1000, graph=False))
+    launch_graph = max_over_ranks(sess.halo.floor_launch(1000, graph=True))
+    if floor is None:
+        floor = {}
+    floor["launch_us_eager"] = round(launch_eager, 3)
+    floor["launch_us_graph"] = round(launch_graph, 3)
+    if floor.get("t0_one_way_us"):
         t0 = floor["t0_one_way_us"]
         fl = 2 * P * t0 + 2 * nvl_bytes / 770e9 * 1e6
         floor["floor_step_us"] = round(fl, 3)
         floor["value_over_floor"] = round(res["step"] / fl, 3)
+        fl2 = fl + 2 * launch_eager
+        floor["floor_step_with_launch_us"] = round(fl2, 3)
+        floor["value_over_floor_with_launch"] = round(res["step"] / fl2, 3)
     if world == 1 and rank == 0 and not args.no_cpu:
         us, n = oracle_step_timing(c, X, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle",

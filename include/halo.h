@@ -223,6 +223,13 @@ HALO_API halo_status halo_get_trace(halo_ctx* ctx, int which, uint64_t* out, int
  * *one_way_us = median round trip / 2 (initiator; 0 on the responder). */
 HALO_API halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, int relaxed, double* one_way_us);
 
+/* Launch floor (SURVEY 8(d) floor iii): mean device time per launch of an
+ * empty kernel launched back to back the way the exchange kernels are
+ * (regular launch + programmatic dependent launch), `iters` launches between
+ * two events on an internal stream; graph = 1 captures them in a CUDA graph and
+ * times its replay.  Synchronises. */
+HALO_API halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_per_launch);
+
 /* Host-block until all work this ctx enqueued is done; surfaces device error
  * words (HALO_ERR_TIMEOUT) and CUDA errors. */
 HALO_API halo_status halo_sync(halo_ctx* ctx);

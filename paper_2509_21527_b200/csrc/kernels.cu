@@ -462,6 +462,12 @@ __global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t ba
   }
 }
 
+// Empty kernel with the exchange kernels' PDL prologue (launch floor).
+__global__ void k_empty() {
+  pdl_launch_dependents();
+  pdl_wait();
+}
+
 // ------------------------------------------------------------- host launchers
 // Cooperative launch (hardware-checked co-residency) is opt-in (HALO_COOP=1):
 // it disables programmatic dependent launch, which hides ~4 us of launch gap per
@@ -510,6 +516,11 @@ cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** ar
   cfg.attrs = attr;
   cfg.numAttrs = n;
   return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t launch_empty(int grid, cudaStream_t st) {
+  void* args[] = {nullptr};
+  return launch_coop_kernel_ex((const void*)k_empty, grid, kThreads, args, st, true);
 }
 
 cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args, cudaStream_t st) {

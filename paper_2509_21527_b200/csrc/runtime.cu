@@ -32,6 +32,7 @@ cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t b
 cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
 cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
 cudaError_t max_coresident_ll(int layout, int* x_blocks, int* f_blocks);
+cudaError_t launch_empty(int grid, cudaStream_t st);
 }  // namespace halo
 
 using namespace halo;
@@ -1303,6 +1304,47 @@ halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, int rel
       *one_way_us = (double)v[iters / 2] / 2.0 / 1000.0;
     }
   }
+  return HALO_OK;
+}
+
+halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_per_launch) {
+  if (!ctx || iters <= 0 || !us_per_launch) return HALO_ERR_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int grid = std::max(1, std::min(ctx->max_x, 512));
+  float ms = 0.f;
+  if (!graph) {
+    for (int i = 0; i < 10; ++i) CK(launch_empty(grid, st));
+    CK(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) CK(launch_empty(grid, st));
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+  } else {
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) CK(launch_empty(grid, st));
+    CK(cudaStreamEndCapture(st, &g));
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    CK(cudaGraphLaunch(ge, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventRecord(e0, st));
+    CK(cudaGraphLaunch(ge, st));
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    CK(cudaGraphExecDestroy(ge));
+    CK(cudaGraphDestroy(g));
+  }
+  *us_per_launch = 1e3 * (double)ms / iters;
+  CK(cudaEventDestroy(e0));
+  CK(cudaEventDestroy(e1));
+  CK(cudaStreamDestroy(st));
   return HALO_OK;
 }
 

@@ -191,6 +191,11 @@ class Halo:
         self._ck(self.lib.halo_floor_pingpong(self.h, int(peer_rank), int(iters), int(bool(relaxed)), ctypes.byref(v)))
         return v.value
 
+    def floor_launch(self, iters=1000, graph=False) -> float:
+        v = c_double()
+        self._ck(self.lib.halo_floor_launch(self.h, int(iters), int(bool(graph)), ctypes.byref(v)))
+        return v.value
+
     def sync(self):
         self._ck(self.lib.halo_sync(self.h))
 
