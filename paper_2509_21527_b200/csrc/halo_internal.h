@@ -76,6 +76,10 @@ struct Ctrl {
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };
 
+// HALO_DEBUG bits: protocol mutations for the dependency-safety tests (G3);
+// never set in production.
+enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u };
+
 struct RankDev {
   float* x;                 // own x (capacity rows)
   float* f;                 // own f

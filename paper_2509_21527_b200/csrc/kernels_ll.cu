@@ -116,8 +116,10 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
           // forwarded row: the pulse it arrived in (Alg. 4 dependent part, R8/R9)
           int q = 0;
           while (q < P.P - 1 && (unsigned)(idx - r.recv_off[q]) >= (unsigned)r.recv_size[q]) ++q;
-          if (q < P.p_lo) {
-            v = __ldcg(r.x + (size_t)idx * W + c);  // arrived in an earlier launch (set_maps)
+          if (q < P.p_lo || (P.debug & kMutateXNoWait)) {
+            // arrived in an earlier launch (set_maps); kMutateXNoWait: the protocol
+            // mutation the sentinel tests must catch (forward without waiting)
+            v = __ldcg(r.x + (size_t)idx * W + c);
           } else {
             const uint64_t* src = r.xll_own + (size_t)q * P.ll_stride + (size_t)(idx - r.recv_off[q]) * W + c;
             v = ll_wait(src, tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, q), P.poll_ns);
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
         for (int j = 0; j < kMaxP; ++j) {
           if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
             const int q = (int)(cc[j] >> 24);
-            if ((uint32_t)(w[j] >> 32) != tag)
+            if ((uint32_t)(w[j] >> 32) != tag && !(P.debug & kMutateFNoWait))
               w[j] = ll_spin(g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
                              P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
             const float val = __uint_as_float((uint32_t)w[j]);

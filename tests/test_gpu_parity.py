@@ -282,3 +282,35 @@ def test_parity_item_size_bounds(rows, monkeypatch):
     sess = session_for(case)
     run_gpu_case(case, sess, steps=2)
     sess.destroy()
+
+
+@pytest.mark.parametrize("mut", [16, 32])
+def test_mutation_is_caught(mut, monkeypatch):
+    """Dependency safety (G3): with a protocol mutation (16: forward x rows without
+    waiting for their arrival; 32: add force contributions without checking their
+    sequence tag) the poisoned/bit-exact parity check must fail on a 3D grid with
+    forwarding.  Proves the parity tests can see a protocol race."""
+    monkeypatch.setenv("HALO_DEBUG", str(mut))
+    case = Case("C3", seed=1, force_kind="int")
+    sess = session_for(case, capacity=case.capacity)
+    failed = False
+    try:
+        for _ in range(3):
+            run_gpu_case(case, sess, steps=2)
+    except AssertionError:
+        failed = True
+    sess.destroy()
+    assert failed, "mutation not detected"
+
+
+def test_two_neighbour_search_epochs():
+    """set_maps twice on one context with different systems (atoms migrate, home
+    counts change): the second epoch's maps, halo and forces are bit-exact."""
+    case1 = Case("C2", seed=1, force_kind="int")
+    case2 = Case("C2", seed=5, force_kind="normal")
+    cap = max(case1.capacity, case2.capacity)
+    sess = session_for(case1, capacity=cap)
+    run_gpu_case(case1, sess, steps=2)
+    run_gpu_case(case2, sess, steps=2)
+    run_gpu_case(case1, sess, steps=1)
+    sess.destroy()
