@@ -174,6 +174,7 @@ struct ExParams {
   const PulseDev* pulses;   // [n_local * P]
   const Item* items;
   int n_items;
+  int n_tail;               // LL f: trailing items that get one dedicated CTA each (shift-force combines)
   int n_local;
   int P;
   int p_lo, p_hi;           // pulse range of this launch (set_maps runs one pulse at a time)

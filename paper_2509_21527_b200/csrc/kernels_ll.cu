@@ -232,8 +232,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
   // static plan data (work record, first gather task record) is loaded while the
   // previous kernel of the stream drains (PDL); f itself is read after the wait
   int4 pre_a = make_int4(0, 0, 0, 0), pre_b = make_int4(0, 0, 0, 0);
-  if ((int)blockIdx.x < P.n_items) {
-    load_rec(&g, P.grec + blockIdx.x);
+  // items [0, n_main) round-robin over CTAs [0, G - n_tail); the n_tail shift-force
+  // combines (last in the item order) get one dedicated CTA each, so they start
+  // polling at once instead of behind their CTA's earlier items
+  const int n_main = P.n_items - P.n_tail;
+  const int Gm = (int)gridDim.x - P.n_tail;
+  const int first = ((int)blockIdx.x < Gm) ? (int)blockIdx.x : n_main + ((int)blockIdx.x - Gm);
+  const int stride = ((int)blockIdx.x < Gm) ? Gm : P.n_items;
+  const int end = ((int)blockIdx.x < Gm) ? n_main : P.n_items;
+  if (first < end) {
+    load_rec(&g, P.grec + first);
     __syncthreads();
     if (g.kind == kItemGather && threadIdx.x < (blockDim.x / W) * W && threadIdx.x < g.n_units) {
       const uint32_t k = threadIdx.x / W;
@@ -247,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
   __syncthreads();
   const uint32_t arrived = launch_arrive(&ctrl->done_f);
   uint64_t seq = 0;
-  for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    if (it != (int)blockIdx.x) {
+  for (int it = first; it < end; it += stride) {
+    if (it != first) {
       __syncthreads();  // everyone is done with the previous record
       load_rec(&g, P.grec + it);
     }
@@ -260,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
       if (P.fshift != nullptr) fshift_combine(g, P, tag, s_fs, P.fsp_slots);
       __syncthreads();
       if (trace) {
-        const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
+        const int slot = (it - first) / stride;
         if (slot < 2) {
           ctrl->trace[1][blockIdx.x][4 + 2 * slot] = ((uint64_t)g.kind << 16) | ((uint64_t)g.lrank << 8) | g.level;
           ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
       for (uint32_t u = threadIdx.x; u < n; u += S) {
         const uint32_t k = u / W;
         int4 a, b;
-        if (u == threadIdx.x && it == (int)blockIdx.x) {
+        if (u == threadIdx.x && it == first) {
           a = pre_a;  // prefetched before the PDL wait
           b = pre_b;
         } else {
@@ -324,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
     }
     __syncthreads();
     if (trace) {
-      const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
+      const int slot = (it - first) / stride;
       if (slot < 2) {
         ctrl->trace[1][blockIdx.x][4 + 2 * slot] = ((uint64_t)g.kind << 16) | ((uint64_t)g.lrank << 8) | g.level;
         ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();

@@ -103,6 +103,7 @@ struct halo_ctx {
   Item* d_items_x = nullptr;
   Item* d_items_f = nullptr;
   int n_items_x = 0, n_items_f = 0;
+  int n_tail_f = 0;                 // LL: shift-force combine items at the end of the f list
   double* d_fshift_tmp = nullptr;  // halo_step_host
   char* d_small = nullptr;          // set_maps argument staging
   uint64_t* d_rtt = nullptr;
@@ -706,6 +707,8 @@ static void build_f_items_ll(halo_ctx* ctx) {
     it.begin = it.end = 0;
     v.push_back(it);
   }
+  ctx->n_tail_f = 0;
+  for (const Item& it : v) ctx->n_tail_f += it.kind == kItemFshift;
 }
 
 // 128-B work records of the LL kernels, one per item (halo_internal.h XRec/GRec).
@@ -1176,7 +1179,12 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   ExParams F = make_params(ctx, ctx->d_items_f, ctx->n_items_f, 0, ctx->P);
   F.fshift = fshift;
   F.accumulate = accumulate ? 1 : 0;
-  const int grid = grid_for(ctx->n_items_f, ctx->n_local, ctx->max_f);
+  int grid = grid_for(ctx->n_items_f, ctx->n_local, ctx->max_f);
+  if (ctx->ll) {  // dedicated CTAs for the combines
+    F.n_tail = ctx->n_tail_f;
+    grid = std::min(ctx->n_items_f - ctx->n_tail_f, ctx->max_f - ctx->n_tail_f) + ctx->n_tail_f;
+    grid = std::max(grid, 1);
+  }
   ctx->last_grid[1] = grid;
   if (ctx->ll)
     CK(launch_exchange_f_ll(F, ctx->W, grid, (cudaStream_t)stream));
