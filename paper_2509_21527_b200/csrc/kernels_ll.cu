@@ -196,21 +196,38 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
                                             uint32_t fsp_slots) {
 #pragma unroll
   for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] = 0.0;
-  for (int q = 0; q < P.P; ++q) {
-    const uint32_t n = g.nslot[q] * 3;  // (slot, component) pairs of pulse q
-    if (n == 0) continue;
-    const int d = g.pulse_dim[q];
-    const uint64_t* base = g.part + (size_t)q * fsp_slots * 6;
-    for (uint32_t pp = threadIdx.x; pp < n; pp += blockDim.x) {
-      const uint64_t hv = ld_relaxed_sys(base + 2 * (size_t)pp);
-      const uint64_t lv = ld_relaxed_sys(base + 2 * (size_t)pp + 1);
-      const uint32_t hi = (uint32_t)((uint32_t)(hv >> 32) == tag ? hv
-                                      : ll_spin(base + 2 * (size_t)pp, tag, P.timeout_ns, P.err_host,
-                                                tcode(13, g.lrank, q), 0));
-      const uint32_t lo = (uint32_t)((uint32_t)(lv >> 32) == tag ? lv
-                                      : ll_spin(base + 2 * (size_t)pp + 1, tag, P.timeout_ns, P.err_host,
-                                                tcode(13, g.lrank, q), 0));
-      s_red[3 * d + (int)(pp % 3)][threadIdx.x] += __hiloint2double((int)hi, (int)lo);
+  // one flat index space over (pulse, slot, component) triples; every load of a
+  // thread is issued before any wait is resolved
+  uint32_t off[kMaxP + 1];
+  off[0] = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxP; ++q) off[q + 1] = off[q] + (q < P.P ? g.nslot[q] * 3 : 0u);
+  const uint32_t n = off[kMaxP];
+  constexpr int kB = 4;
+  for (uint32_t base = threadIdx.x; base < n; base += kB * blockDim.x) {
+    const uint64_t* ptr[kB];
+    uint64_t hv[kB], lv[kB];
+    int dc[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const uint32_t e = base + k * blockDim.x;
+      ptr[k] = nullptr;
+      if (e < n) {
+        int q = 0;
+        while (e >= off[q + 1]) ++q;
+        const uint32_t pp = e - off[q];  // slot * 3 + component
+        ptr[k] = g.part + (size_t)q * fsp_slots * 6 + 2 * (size_t)pp;
+        dc[k] = 3 * g.pulse_dim[q] + (int)(pp % 3);
+        hv[k] = ld_relaxed_sys(ptr[k]);
+        lv[k] = ld_relaxed_sys(ptr[k] + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      if (ptr[k] == nullptr) continue;
+      if ((uint32_t)(hv[k] >> 32) != tag) hv[k] = ll_spin(ptr[k], tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0);
+      if ((uint32_t)(lv[k] >> 32) != tag) lv[k] = ll_spin(ptr[k] + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0);
+      s_red[dc[k]][threadIdx.x] += __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
     }
   }
   const double tot = cta_tree9(s_red, threadIdx.x);
