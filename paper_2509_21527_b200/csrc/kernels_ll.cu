@@ -194,6 +194,8 @@ __device__ __forceinline__ double cta_sum9(const double* v, double (*s_red)[kThr
 // CTA writes the rank's fshift.
 __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_red)[kThreads],
                                             uint32_t fsp_slots) {
+  // only this CTA writes the rank's fshift: read it now, off the tail
+  const double fs_old = (threadIdx.x < 9) ? P.fshift[9 * g.lrank + threadIdx.x] : 0.0;
 #pragma unroll
   for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] = 0.0;
   // one flat index space over (pulse, slot, component) triples; every load of a
@@ -231,10 +233,7 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
     }
   }
   const double tot = cta_tree9(s_red, threadIdx.x);
-  if (threadIdx.x < 9) {
-    double* fs = P.fshift + 9 * g.lrank + threadIdx.x;
-    *fs = *fs + tot;
-  }
+  if (threadIdx.x < 9) P.fshift[9 * g.lrank + threadIdx.x] = fs_old + tot;
 }
 
 template <int W>
