@@ -394,6 +394,9 @@ def run_fused(args, rank, world, local):
         fl2 = fl + 2 * launch_eager
         floor["floor_step_with_launch_us"] = round(fl2, 3)
         floor["value_over_floor_with_launch"] = round(res["step"] / fl2, 3)
+        # the bound that actually limits this path: the measured latency floor
+        roof["latency"] = {"floor_us": round(fl2, 3), "frac": round(fl2 / res["step"], 4),
+                           "definition": "2*P*t0 + 2*NVLink bytes/770 GB/s + 2 launches (eager)"}
     if world == 1 and rank == 0 and not args.no_cpu:
         us, n = oracle_step_timing(c, X, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle",

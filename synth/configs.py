@@ -45,6 +45,13 @@ CONFIGS = {
     # configs[4]: 45k box on 8 ranks, 2 pulses (1D along z, w = 0.957 nm < rc)
     "C5": Config("C5", 45000, (7.656, 7.656, 7.656), (1, 1, 8), (0, 0, 2), 1.0,
                  "45k-atom box on 8 ranks (1D z), 2 pulses per dim (latency-bound limit)"),
+    # C4-bw: bandwidth probe, C4 1D with the cutoff swept up to 8 nm
+    "C4-bw2": Config("C4-bw2", 1066629, (21.68, 21.68, 21.68), (1, 1, 2), (0, 0, 1), 2.0,
+                     "C4 1D 2-rank, rc 2 nm (bandwidth probe)"),
+    "C4-bw5": Config("C4-bw5", 1066629, (21.68, 21.68, 21.68), (1, 1, 2), (0, 0, 1), 5.0,
+                     "C4 1D 2-rank, rc 5 nm (bandwidth probe)"),
+    "C4-bw8": Config("C4-bw8", 1066629, (21.68, 21.68, 21.68), (1, 1, 2), (0, 0, 1), 8.0,
+                     "C4 1D 2-rank, rc 8 nm (bandwidth probe)"),
     # small oracle-self cases (SURVEY.md §8(c) parity matrix)
     "T3D": Config("T3D", 1500, (2.46, 2.46, 2.46), (2, 2, 2), (1, 1, 1), 1.0,
                   "tiny 3D 2x2x2 water box"),
