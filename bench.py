@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+PROTO_FLAGS = {"ll": 0, "paper": 1 << 4, "ce": 1 << 5}  # HALO_F_PAPER_FLAGS, HALO_F_CE_PATH
 METRIC = "x+f halo exchange us/step (max over ranks); achieved NVLink GB/s vs 900"
 UNIT = "us/step"
 SEED = 2509
@@ -172,7 +173,7 @@ def run_fused(args, rank, world, local):
     torch.cuda.set_device(dev)
     homes = assign_home(X, c.L, c.grid)
     cap = int(max(len(h) for h in homes) * 2.2) + 4096
-    flags = HALO_F_TIMERS if args.timers else 0
+    flags = (HALO_F_TIMERS if args.timers else 0) | PROTO_FLAGS[args.proto]
     sess = HaloSession(c.grid, c.L, c.rc, c.pulses, layout=args.layout, capacity=cap, device=local, flags=flags,
                        nprocs=world, proc=rank, timeout_s=20.0)
     first, nl = sess.first_rank, sess.n_local
@@ -359,7 +360,9 @@ def run_fused(args, rank, world, local):
         "warmup": args.warmup, "ms_per_step": round(res["step"] / 1e3, 6), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(workload_desc(c, world, W), parallelism=f"spatial DD {c.grid[0]}x{c.grid[1]}x{c.grid[2]}",
-                       mode="eager, one exchange_x + one exchange_f launch per GPU per step"),
+                       protocol=args.proto,
+                       mode=("eager, one exchange_x + one exchange_f launch per GPU per step" if args.proto != "ce"
+                             else "eager, copy-engine path: per pulse pack + cudaMemcpyAsync + flag kernels")),
         "x_us": round(res["x"], 3), "f_us": round(res["f"], 3), "step_median_us": round(res["step_median"], 3),
         "step_percentiles_us": {"p90": round(res["step_p90"], 3), "p99": round(res["step_p99"], 3),
                                 "max": round(res["step_max"], 3)},
@@ -371,7 +374,7 @@ def run_fused(args, rank, world, local):
         "clocks": sampler.summary(),
         "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
                 "d2h_bytes_per_step": int(d2h) * world, "path": "halo_step_host (C ABI, pinned host buffers)"},
-        "gpu_launches": 2 * K * world,
+        "gpu_launches": (2 if args.proto != "ce" else 4 * P) * K * world,
         "roofline": roof,
         "nvlink": {"bytes_per_step_per_gpu_per_direction": int(nvl_bytes),
                    "achieved_gbs": round(nvl_bytes / (res["step"] * 1e-6) / 1e9, 3) if nvl_bytes else 0.0,
@@ -413,48 +416,19 @@ def _neighbour(grid, r, d, delta):
 
 
 def run_nccl_baseline(sess, lay, F0, flush, K, warmup, W):
-    """Serialized per-pulse schedule (Fig. 1) with NCCL send/recv: pack kernel ->
-    grouped ncclSend/ncclRecv -> (forces, reverse) ncclSend/ncclRecv -> unpack kernel."""
+    """Serialized per-pulse schedule (Fig. 1) with NCCL send/recv on the same maps
+    (paper_2509_21527_b200.nccl_baseline): pack kernel -> grouped send/recv -> (forces, reverse)
+    send/recv -> unpack kernel."""
     import torch
-    import torch.distributed as dist
+    from paper_2509_21527_b200.nccl_baseline import NcclSchedule
     dev = sess.device
-    P = sess.npulse
-    dims = sess.halo.pulse_order()
-    me = sess.first_rank
-    grid = sess.grid
-    sendbuf = [torch.empty(max(lay["send_size"][p], 1), W, device=dev) for p in range(P)]
-    fbuf = [torch.empty(max(lay["send_size"][p], 1), W, device=dev) for p in range(P)]
+    sched = NcclSchedule(sess)
     fshift = torch.zeros(1, 3, 3, dtype=torch.float64, device=dev)
-    x, f = sess.x[0], sess.f[0]
+    f = sess.f[0]
     stream = torch.cuda.current_stream()
-
-    def step():
-        for p in range(P):
-            lo, up = _neighbour(grid, me, dims[p], -1), _neighbour(grid, me, dims[p], +1)
-            n_s, n_r, off = lay["send_size"][p], lay["recv_size"][p], lay["recv_off"][p]
-            sess.halo.pack_x_pulse(0, p, sendbuf[p].data_ptr(), stream=stream.cuda_stream)
-            ops = []
-            if n_s:
-                ops.append(dist.P2POp(dist.isend, sendbuf[p][:n_s], lo))
-            if n_r:
-                ops.append(dist.P2POp(dist.irecv, x[off: off + n_r], up))
-            for w in dist.batch_isend_irecv(ops) if ops else []:
-                w.wait()
-        for p in range(P - 1, -1, -1):
-            lo, up = _neighbour(grid, me, dims[p], -1), _neighbour(grid, me, dims[p], +1)
-            n_s, n_r, off = lay["send_size"][p], lay["recv_size"][p], lay["recv_off"][p]
-            ops = []
-            if n_r:
-                ops.append(dist.P2POp(dist.isend, f[off: off + n_r], up))
-            if n_s:
-                ops.append(dist.P2POp(dist.irecv, fbuf[p][:n_s], lo))
-            for w in dist.batch_isend_irecv(ops) if ops else []:
-                w.wait()
-            sess.halo.unpack_f_pulse(0, p, fbuf[p].data_ptr(), fshift.data_ptr(), stream=stream.cuda_stream)
-
     for _ in range(warmup):
         f[: F0.shape[0]].copy_(F0)
-        step()
+        sched.step(fshift)
     torch.cuda.synchronize()
     barrier()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
@@ -462,13 +436,13 @@ def run_nccl_baseline(sess, lay, F0, flush, K, warmup, W):
         f[: F0.shape[0]].copy_(F0)
         flush.fill_(1.0)
         ev[k][0].record(stream)
-        step()
+        sched.step(fshift)
         ev[k][1].record(stream)
     torch.cuda.synchronize()
     us = max_over_ranks(float(np.mean([ev[k][0].elapsed_time(ev[k][1]) * 1e3 for k in range(K)])))
     barrier()
     return {"us_per_step": round(us, 3), "schedule": "per-pulse pack -> NCCL send/recv -> unpack (torch "
-            "batch_isend_irecv), same maps", "launches_per_step": 2 * P}
+            "batch_isend_irecv), same maps", "launches_per_step": 2 * sess.npulse}
 
 
 def load_peaks():
@@ -533,6 +507,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--layout", type=int, default=3, choices=(3, 4))
     ap.add_argument("--impl", default="fused", choices=("fused", "reference"))
+    ap.add_argument("--proto", default="ll", choices=sorted(PROTO_FLAGS),
+                    help="ll: default LL protocol; paper: per-pulse flags (Alg. 5); ce: copy-engine path")
     ap.add_argument("--timers", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")

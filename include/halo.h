@@ -76,6 +76,14 @@ typedef enum {
                                            pushed then scatter-added).  Default: the LL protocol (every 8-B
                                            store carries a 32-bit sequence tag; row-level forwarding; the
                                            force halo is a deterministic gather) */
+#define HALO_F_CE_PATH        (1u << 5) /* copy-engine path (north_star: "a copy-engine path covers large
+                                           contiguous pulses"): per pulse, a local gather kernel packs the send
+                                           rows (skipped when the map is one contiguous unshifted run), ONE
+                                           cudaMemcpyAsync moves them over NVLink, a one-thread-per-rank kernel
+                                           releases the pulse flag on the peer and acquire-waits its own; forces:
+                                           CE copy of the contiguous halo slice, flag, ordered scatter-add.
+                                           ~3 launches + L copies per pulse; bit-exact like the default.
+                                           Takes precedence over HALO_F_PAPER_FLAGS (set_maps uses its kernels). */
 
 typedef struct {
   int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */

@@ -194,6 +194,31 @@ struct ExParams {
   const GRec* grec;         // LL protocol work records (f)
 };
 
+// Copy-engine path (HALO_F_CE_PATH, kernels_ce.cu): one entry per (pulse, local rank).
+struct CeEnt {
+  const int32_t* map;       // map_p (send_size entries)
+  const float* src;         // pack: own x; unpack: own force receive buffer of pulse p
+  float* dst;               // pack: staging rows; unpack: own f
+  int n;                    // send_size_p
+  int pack;                 // pack: 1 iff a gather is needed (map not one contiguous run, or shifted)
+  int has_shift;
+  int dim;
+  float shift[3];
+  int pad;
+};
+
+struct CeSyncParams {
+  uint64_t* seq_slot;       // &ctrl->seq_x or &ctrl->seq_f
+  uint64_t* dst[kMaxLocal]; // flag on the peer this local rank's copy went to
+  const uint64_t* own[kMaxLocal];  // own flag of the pulse
+  int n_local;
+  int publish;              // last sync of the exchange: store seq into seq_slot
+  int kind;                 // 0 = x, 1 = f (timeout code)
+  int pulse;
+  int* err_host;
+  uint64_t timeout_ns;
+};
+
 struct SelParams {
   const RankDev* ranks;
   Ctrl* ctrl;

@@ -33,6 +33,10 @@ cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, cudaSt
 cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
 cudaError_t max_coresident_ll(int layout, int* x_blocks, int* f_blocks);
 cudaError_t launch_empty(int grid, cudaStream_t st);
+cudaError_t launch_ce_pack(int layout, const CeEnt* ents, int n_local, int max_rows, cudaStream_t st);
+cudaError_t launch_ce_unpack(int layout, const CeEnt* ents, int n_local, int max_rows, double* fshift, int accumulate,
+                             cudaStream_t st);
+cudaError_t launch_ce_sync(const CeSyncParams& s, cudaStream_t st);
 }  // namespace halo
 
 using namespace halo;
@@ -83,6 +87,7 @@ struct halo_ctx {
   int pdim[kMaxP] = {0}, pk[kMaxP] = {0};
   size_t map_stride = 0, fbuf_stride = 0, ll_stride = 0, fsp_slots = 0, scratch_bytes = 0;
   bool ll = true;                   // LL protocol (default) vs the paper's flag protocol
+  bool ce = false;                  // copy-engine path (HALO_F_CE_PATH; set_maps uses the paper kernels)
   std::string last_error;
 
   // registered local buffers
@@ -119,6 +124,19 @@ struct halo_ctx {
   std::vector<GRec> h_grec;
   XRec* d_xrec = nullptr;
   GRec* d_grec = nullptr;
+
+  // copy-engine path (HALO_F_CE_PATH): per pulse, per local rank
+  struct CeCopy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  std::vector<CeEnt> h_ce_pack, h_ce_unpack;   // [P][n_local]
+  std::vector<CeCopy> ce_copy_x, ce_copy_f;    // [P][n_local]
+  std::vector<int> ce_pack_rows, ce_unpack_rows;  // [P]: largest entry needing the kernel (0 = no launch)
+  CeEnt* d_ce = nullptr;                       // pack table then unpack table
+  float* d_stage = nullptr;                    // contiguous send rows of every (pulse, local rank) that packs
+  size_t ce_bytes = 0, stage_bytes = 0;
 
   std::vector<std::vector<int>> level_begin;  // [local][P+2]: task index where level P-1..0, home start
 
@@ -291,7 +309,8 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     ctx->fsp_slots = SL.fsp_slots;
     ctx->scratch_bytes = SL.total;
   }
-  ctx->ll = !(cfg->flags & HALO_F_PAPER_FLAGS);
+  ctx->ce = (cfg->flags & HALO_F_CE_PATH) != 0;
+  ctx->ll = !(cfg->flags & HALO_F_PAPER_FLAGS) && !ctx->ce;
   ctx->x.assign(ctx->n_local, nullptr);
   ctx->f.assign(ctx->n_local, nullptr);
   ctx->scratch.assign(ctx->n_local, nullptr);
@@ -905,6 +924,121 @@ static halo_status pull_maps(halo_ctx* ctx, int p, cudaStream_t st) {
   return HALO_OK;
 }
 
+// Copy-engine plan (HALO_F_CE_PATH, kernels_ce.cu): per (pulse, local rank) the
+// x gather entry (skipped for a contiguous unshifted map: the CE reads x
+// directly), the x copy to the receiver, the force-slice copy to the x-sender
+// (contiguous by construction, R12) and the scatter-add entry.
+static halo_status build_ce(halo_ctx* ctx) {
+  const int L = ctx->n_local, P = ctx->P, W = ctx->W;
+  ctx->h_ce_pack.assign((size_t)P * L, CeEnt{});
+  ctx->h_ce_unpack.assign((size_t)P * L, CeEnt{});
+  ctx->ce_copy_x.assign((size_t)P * L, halo_ctx::CeCopy{nullptr, nullptr, 0});
+  ctx->ce_copy_f.assign((size_t)P * L, halo_ctx::CeCopy{nullptr, nullptr, 0});
+  ctx->ce_pack_rows.assign(P, 0);
+  ctx->ce_unpack_rows.assign(P, 0);
+  size_t stage_rows = 0;
+  for (int p = 0; p < P; ++p)
+    for (int l = 0; l < L; ++l) stage_rows += ctx->send_size[l * P + p];
+  const size_t need_stage = std::max<size_t>(stage_rows * W * sizeof(float), 256);
+  if (need_stage > ctx->stage_bytes) {
+    if (ctx->d_stage) CK(cudaFree(ctx->d_stage));
+    ctx->d_stage = nullptr;
+    CK(cudaMalloc(&ctx->d_stage, need_stage));
+    ctx->stage_bytes = need_stage;
+  }
+  float* stage = ctx->d_stage;
+  for (int p = 0; p < P; ++p)
+    for (int l = 0; l < L; ++l) {
+      const int i = l * P + p, k = p * L + l;
+      const PulseDev& pd = ctx->h_pulses[i];
+      const auto& m = ctx->h_maps[l][p];
+      const int n = (int)m.size();
+      bool contiguous = n > 0;
+      for (int j = 1; contiguous && j < n; ++j) contiguous = m[j] == m[0] + j;
+      CeEnt& e = ctx->h_ce_pack[k];
+      e.map = pd.map;
+      e.src = ctx->x[l];
+      e.dst = stage;
+      e.n = n;
+      e.pack = (n > 0 && (pd.has_shift || !contiguous)) ? 1 : 0;
+      e.has_shift = pd.has_shift;
+      e.dim = pd.dim;
+      for (int c = 0; c < 3; ++c) e.shift[c] = pd.shift[c];
+      if (e.pack) ctx->ce_pack_rows[p] = std::max(ctx->ce_pack_rows[p], n);
+      ctx->ce_copy_x[k] = {pd.x_dst, e.pack ? (const void*)stage : (const void*)(ctx->x[l] + (size_t)(n ? m[0] : 0) * W),
+                           (size_t)n * W * sizeof(float)};
+      stage += (size_t)n * W;
+      CeEnt& u = ctx->h_ce_unpack[k];
+      u = e;
+      u.src = pd.fbuf_own;
+      u.dst = ctx->f[l];
+      u.pack = 0;
+      ctx->ce_unpack_rows[p] = std::max(ctx->ce_unpack_rows[p], n);
+      // force slice of pulse p (this rank's receive range) -> the x-sender's force buffer
+      ctx->ce_copy_f[k] = {pd.fbuf_dst, ctx->f[l] + (size_t)pd.atom_offset * W, (size_t)pd.recv_size * W * sizeof(float)};
+    }
+  const size_t need = 2 * sizeof(CeEnt) * std::max<size_t>(1, (size_t)P * L);
+  if (need > ctx->ce_bytes) {
+    if (ctx->d_ce) CK(cudaFree(ctx->d_ce));
+    ctx->d_ce = nullptr;
+    CK(cudaMalloc(&ctx->d_ce, need));
+    ctx->ce_bytes = need;
+  }
+  if (P) {
+    CK(cudaMemcpy(ctx->d_ce, ctx->h_ce_pack.data(), sizeof(CeEnt) * P * L, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_ce + (size_t)P * L, ctx->h_ce_unpack.data(), sizeof(CeEnt) * P * L, cudaMemcpyHostToDevice));
+  }
+  return HALO_OK;
+}
+
+static CeSyncParams ce_sync_params(halo_ctx* ctx, int kind, int p, bool publish) {
+  CeSyncParams S{};
+  S.seq_slot = kind == 0 ? &ctx->ctrl->seq_x : &ctx->ctrl->seq_f;
+  for (int l = 0; l < ctx->n_local; ++l) {
+    const PulseDev& pd = ctx->h_pulses[l * ctx->P + p];
+    ScratchHdr* own = ctx->hdr_of(ctx->first_rank + l);
+    S.dst[l] = kind == 0 ? pd.flag_x_dst : pd.flag_f_dst;
+    S.own[l] = kind == 0 ? &own->flag_x[p] : &own->flag_f[p];
+  }
+  S.n_local = ctx->n_local;
+  S.publish = publish ? 1 : 0;
+  S.kind = kind;
+  S.pulse = p;
+  S.err_host = ctx->err_dev;
+  S.timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);
+  return S;
+}
+
+// x over the copy engine: per pulse ascending, gather -> CE copy -> flag + wait.
+static halo_status ce_exchange_x(halo_ctx* ctx, cudaStream_t st) {
+  const int L = ctx->n_local, P = ctx->P;
+  for (int p = 0; p < P; ++p) {
+    CK(launch_ce_pack(ctx->W, ctx->d_ce + (size_t)p * L, L, ctx->ce_pack_rows[p], st));
+    for (int l = 0; l < L; ++l) {
+      const halo_ctx::CeCopy& c = ctx->ce_copy_x[(size_t)p * L + l];
+      if (c.bytes) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, st));
+    }
+    CK(launch_ce_sync(ce_sync_params(ctx, 0, p, p == P - 1), st));
+  }
+  return HALO_OK;
+}
+
+// f over the copy engine: per pulse descending, CE copy of the halo slice ->
+// flag + wait -> ordered scatter-add (+ shift forces).
+static halo_status ce_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, cudaStream_t st) {
+  const int L = ctx->n_local, P = ctx->P;
+  for (int p = P - 1; p >= 0; --p) {
+    for (int l = 0; l < L; ++l) {
+      const halo_ctx::CeCopy& c = ctx->ce_copy_f[(size_t)p * L + l];
+      if (c.bytes) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, st));
+    }
+    CK(launch_ce_sync(ce_sync_params(ctx, 1, p, p == 0), st));
+    CK(launch_ce_unpack(ctx->W, ctx->d_ce + (size_t)P * L + (size_t)p * L, L, ctx->ce_unpack_rows[p], fshift,
+                        accumulate, st));
+  }
+  return HALO_OK;
+}
+
 // Shared driver of halo_set_maps / halo_set_maps_explicit.
 static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* send_sizes, const int* const* maps,
                                  cudaStream_t st) {
@@ -1100,6 +1234,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   }
   fill_rank_dev(ctx);
   if ((s = upload_plan(ctx)) != HALO_OK) return s;
+  if (ctx->ce && (s = build_ce(ctx)) != HALO_OK) return s;
   ctx->maps_ready = true;
   ctx->x_done = true;  // set_maps exchanged every pulse's coordinates
   return HALO_OK;
@@ -1159,6 +1294,7 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   if (s != HALO_OK) return s;
   ctx->x_done = true;
   if (ctx->P == 0) return HALO_OK;
+  if (ctx->ce) return ce_exchange_x(ctx, (cudaStream_t)stream);
   ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, 0, ctx->P);
   const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->max_x);
   ctx->last_grid[0] = grid;
@@ -1176,6 +1312,7 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   halo_status s = check_err_word(ctx);
   if (s != HALO_OK) return s;
   if (ctx->P == 0) return HALO_OK;
+  if (ctx->ce) return ce_exchange_f(ctx, fshift, accumulate ? 1 : 0, (cudaStream_t)stream);
   ExParams F = make_params(ctx, ctx->d_items_f, ctx->n_items_f, 0, ctx->P);
   F.fshift = fshift;
   F.accumulate = accumulate ? 1 : 0;
@@ -1374,6 +1511,8 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_small) (void)cudaFree(ctx->d_small);
   if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
   if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
+  if (ctx->d_ce) (void)cudaFree(ctx->d_ce);
+  if (ctx->d_stage) (void)cudaFree(ctx->d_stage);
   if (ctx->err_host) (void)cudaFreeHost(ctx->err_host);
   (void)cudaGetLastError();
   delete ctx;
