@@ -314,20 +314,32 @@ def run_fused(args, rank, world, local):
     if world > 1 and nl == 1 and not args.no_nccl:
         nccl = run_nccl_baseline(sess, lay[0], F0[0], flush, K, args.warmup, W)
 
-    # latency floor: peer flag ping-pong between process 0 and process 1
+    # latency floor: peer flag ping-pong between process 0 and process 1; bandwidth
+    # floor: one-directional SM peer stores and copy-engine copies 0 -> 1
     floor = None
-    if world > 1:
+    if world > 1 and not args.no_floors:
         t0 = t0r = None
+        bw = {}
         if rank in (0, 1):
             peer = sess.first_rank + sess.n_local if rank == 0 else 0
             t0 = sess.halo.floor_pingpong(peer, iters=10000, relaxed=False)
             t0r = sess.halo.floor_pingpong(peer, iters=10000, relaxed=True)
         barrier()
+        if rank == 0:
+            peer = sess.first_rank + sess.n_local
+            area = (2 * P * cap * W * 8) // 16 * 16  # LL receive areas of the peer's scratch
+            for name, nb in (("8MiB", 8 << 20), ("1MiB", 1 << 20), ("64KiB", 64 << 10)):
+                nb = min(nb, area)
+                bw[name] = {"bytes": nb,
+                            "sm_gbs": round(sess.halo.floor_bandwidth(peer, nb, mode=0, iters=50), 1),
+                            "ce_gbs": round(sess.halo.floor_bandwidth(peer, nb, mode=1, iters=50), 1)}
+        barrier()
         t0 = max_over_ranks(t0 or 0.0)
         t0r = max_over_ranks(t0r or 0.0)
-        floor = {"t0_one_way_us": t0r, "t0_release_acquire_us": t0,
+        floor = {"t0_one_way_us": t0r, "t0_release_acquire_us": t0, "bandwidth": bw or None,
                  "note": "t0 = relaxed 8-B peer store seen by a relaxed poll (the LL unit); median of 1e4 "
-                         "round trips / 2"}
+                         "round trips / 2.  bandwidth: back-to-back transfers GPU0 -> GPU1, SM 16-B stores "
+                         "(8 CTAs/SM) and cudaMemcpyAsync (copy engine), measured on rank 0"}
 
     # algorithmic bytes per launch (this GPU), DESIGN.md "Roofline"
     rows_x = sum(sum(lay[l]["send_size"]) for l in range(nl))
@@ -378,20 +390,25 @@ def run_fused(args, rank, world, local):
         "roofline": roof,
         "nvlink": {"bytes_per_step_per_gpu_per_direction": int(nvl_bytes),
                    "achieved_gbs": round(nvl_bytes / (res["step"] * 1e-6) / 1e9, 3) if nvl_bytes else 0.0,
-                   "peak_gbs": 900.0, "measured_peer_copy_gbs": 770.0},
+                   "peak_gbs": 900.0},
         "latency_floor": floor or None,
         "nccl_baseline": nccl,
         "device_spans": dev_spans,
     }
-    launch_eager = max_over_ranks(sess.halo.floor_launch(1000, graph=False))
-    launch_graph = max_over_ranks(sess.halo.floor_launch(1000, graph=True))
+    launch_eager = max_over_ranks(sess.halo.floor_launch(1000, graph=False)) if not args.no_floors else 0.0
+    launch_graph = max_over_ranks(sess.halo.floor_launch(1000, graph=True)) if not args.no_floors else 0.0
     if floor is None:
         floor = {}
     floor["launch_us_eager"] = round(launch_eager, 3)
     floor["launch_us_graph"] = round(launch_graph, 3)
     if floor.get("t0_one_way_us"):
         t0 = floor["t0_one_way_us"]
-        fl = 2 * P * t0 + 2 * nvl_bytes / 770e9 * 1e6
+        bw_peer = ((floor.get("bandwidth") or {}).get("8MiB") or {}).get("sm_gbs") or 770.0
+        # nvl_bytes already holds x out + f back (one direction): x and f are serial, so their
+        # bandwidth terms add once each
+        fl = 2 * P * t0 + nvl_bytes / (bw_peer * 1e9) * 1e6
+        out["nvlink"]["measured_peer_store_gbs"] = bw_peer
+        out["nvlink"]["frac_of_measured"] = round(out["nvlink"]["achieved_gbs"] / bw_peer, 4)
         floor["floor_step_us"] = round(fl, 3)
         floor["value_over_floor"] = round(res["step"] / fl, 3)
         fl2 = fl + 2 * launch_eager
@@ -399,7 +416,8 @@ def run_fused(args, rank, world, local):
         floor["value_over_floor_with_launch"] = round(res["step"] / fl2, 3)
         # the bound that actually limits this path: the measured latency floor
         roof["latency"] = {"floor_us": round(fl2, 3), "frac": round(fl2 / res["step"], 4),
-                           "definition": "2*P*t0 + 2*NVLink bytes/770 GB/s + 2 launches (eager)"}
+                           "definition": "2*P*t0 + (x+f NVLink bytes per direction)/BW_peer (measured SM peer-store GB/s, 8 MiB) "
+                                         "+ 2 launches (eager)"}
     if world == 1 and rank == 0 and not args.no_cpu:
         us, n = oracle_step_timing(c, X, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -513,6 +531,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-floors", action="store_true", help="skip the latency/bandwidth/launch floor probes")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

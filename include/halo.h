@@ -223,6 +223,14 @@ HALO_API halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_
  * LL protocol kernels only.  Synchronises. */
 HALO_API halo_status halo_get_trace(halo_ctx* ctx, int which, uint64_t* out, int cap, int* n);
 
+/* Debug (pin G4, "emitting system-scope operations only from the
+ * last block"): with HALO_DEBUG=64 in the environment at halo_init, the paper
+ * protocol (HALO_F_PAPER_FLAGS) counts its system-scope flag stores; out[l*P + p]
+ * = cumulative count for local rank l, pulse p of the x (which = 0) or force
+ * (which = 1) exchange since init (set_maps' per-pulse x launches included).
+ * cap >= n_local * npulse.  Synchronises. */
+HALO_API halo_status halo_get_notify_counts(halo_ctx* ctx, int which, uint32_t* out, int cap);
+
 /* Floors (measurement): ping-pong `iters` round trips of a
  * 64-bit flag between this process's local rank 0 and DD rank `peer_rank`
  * (COLLECTIVE between the two processes only; other processes must not call).
@@ -237,6 +245,18 @@ HALO_API halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters
  * two events on an internal stream; graph = 1 captures them in a CUDA graph and
  * times its replay.  Synchronises. */
 HALO_API halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_per_launch);
+
+/* Bandwidth floor (SURVEY 8(d) floor ii): one-directional GB/s of `iters`
+ * back-to-back transfers of `bytes` (multiple of 16, at most the LL receive
+ * area of a rank's scratch) from this process's local rank 0 into DD rank
+ * `peer_rank`'s scratch LL receive area.  mode 0 = SM stores (16-B vectors from
+ * 8 CTAs per SM, the hot path's transport), mode 1 = copy engine
+ * (cudaMemcpyAsync, the HALO_F_CE_PATH transport).  One-sided: the peer's
+ * process must be idle (no exchange in flight; the caller barriers before and
+ * after), its LL areas are overwritten with data whose tags never match a
+ * live sequence number.  Synchronises. */
+HALO_API halo_status halo_floor_bandwidth(halo_ctx* ctx, int peer_rank, size_t bytes, int mode, int iters,
+                                          double* gbs);
 
 /* Host-block until all work this ctx enqueued is done; surfaces device error
  * words (HALO_ERR_TIMEOUT) and CUDA errors. */

@@ -6,7 +6,8 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_size_t, c_uint, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhalo.so")
+# HALO_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants in scripts/)
+LIB_PATH = os.environ.get("HALO_LIB_PATH") or os.path.join(HERE, "libhalo.so")
 
 HALO_OK = 0
 STATUS_NAMES = {0: "HALO_OK", 1: "HALO_ERR_ARG", 2: "HALO_ERR_GEOMETRY", 3: "HALO_ERR_CAPACITY",
@@ -26,7 +27,7 @@ EXPORTS = [
     "halo_init", "halo_query_config", "halo_local_ranks", "halo_pulse_order", "halo_scratch_bytes", "halo_register_buffers",
     "halo_ipc_export", "halo_ipc_import", "halo_set_maps", "halo_set_maps_explicit", "halo_get_layout",
     "halo_get_map", "halo_exchange_x", "halo_exchange_f", "halo_step_host", "halo_pack_x_pulse",
-    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_floor_pingpong", "halo_floor_launch", "halo_sync", "halo_strerror",
+    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_bandwidth", "halo_sync", "halo_strerror",
     "halo_last_error", "halo_destroy",
 ]
 
@@ -71,14 +72,18 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_unpack_f_pulse": ([P, c_int, c_int, P, P, c_int, P], c_int),
         "halo_get_timers": ([P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
         "halo_get_trace": ([P, c_int, POINTER(c_uint64), c_int, POINTER(c_int)], c_int),
+        "halo_get_notify_counts": ([P, c_int, POINTER(c_uint), c_int], c_int),
         "halo_floor_pingpong": ([P, c_int, c_int, c_int, POINTER(c_double)], c_int),
         "halo_floor_launch": ([P, c_int, c_int, POINTER(c_double)], c_int),
+        "halo_floor_bandwidth": ([P, c_int, c_size_t, c_int, c_int, POINTER(c_double)], c_int),
         "halo_sync": ([P], c_int),
         "halo_strerror": ([c_int], c_char_p),
         "halo_last_error": ([P], c_char_p),
         "halo_destroy": ([P], c_int),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("HALO_LIB_PATH") and not hasattr(lib, name):
+            continue  # an older build under A/B timing may lack newer entry points
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

@@ -72,13 +72,15 @@ struct Ctrl {
   // [start, plan record loaded, items done, exit, item0 tag, item0 end, item1 tag, item1 end]
   // tag = kind << 16 | lrank << 8 | pulse (level)
   uint64_t trace[2][kTraceCTAs][8];
+  // HALO_DEBUG & kCountNotify (pin G4): system-scope flag stores per (x/f, local rank, pulse), cumulative
+  uint32_t notify[2][kMaxLocal][kMaxP];
 };
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };
 
 // HALO_DEBUG bits: protocol mutations for the dependency-safety tests (G3);
 // never set in production.
-enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u };
+enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u, kCountNotify = 64u };
 
 struct RankDev {
   float* x;                 // own x (capacity rows)

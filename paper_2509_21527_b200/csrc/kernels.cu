@@ -67,12 +67,13 @@ __device__ __forceinline__ void x_rows(const PulseDev& pd, const float* __restri
 // increments the pulse's completion counter; the last CTA stores the flag
 // (Alg. 5: "only threadIdx.x = 0 proceeds to notify").
 __device__ __forceinline__ void pulse_complete_sys(unsigned flags, uint32_t* cnt, int n_items, uint64_t* flag_dst,
-                                                   uint64_t seq) {
+                                                   uint64_t seq, uint32_t* notify_count) {
   if (flags & HALO_F_GPU_FENCE) fence_gpu(); else fence_sys();
   uint32_t old = atom_add_acqrel_gpu(cnt, 1u);
   if (old == (uint32_t)n_items - 1) {
     *cnt = 0;  // no other CTA of this launch touches it again
     st_release_sys(flag_dst, seq);
+    if (notify_count) atomicAdd(notify_count, 1u);  // debug (pin G4): one notification per pulse per step
   }
 }
 
@@ -107,7 +108,8 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
     x_rows<W>(pd, rd.x, w.begin, w.end, dep);
     __syncthreads();
     if (threadIdx.x == 0)
-      pulse_complete_sys(P.flags, &ctrl->cnt_x[w.lrank][w.pulse], pd.n_items_x, pd.flag_x_dst, seq);
+      pulse_complete_sys(P.flags, &ctrl->cnt_x[w.lrank][w.pulse], pd.n_items_x, pd.flag_x_dst, seq,
+                         (P.debug & kCountNotify) ? &ctrl->notify[0][w.lrank][w.pulse] : nullptr);
   }
   // The launch completes only when this process's halos are complete, so that
   // stream-ordered consumers (non-local NB) see them.
@@ -218,7 +220,8 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
       push_rows<W>(pd, rd.f, w.begin, w.end);
       __syncthreads();
       if (threadIdx.x == 0)
-        pulse_complete_sys(P.flags, &ctrl->cnt_push[w.lrank][w.pulse], pd.n_items_push, pd.flag_f_dst, seq);
+        pulse_complete_sys(P.flags, &ctrl->cnt_push[w.lrank][w.pulse], pd.n_items_push, pd.flag_f_dst, seq,
+                           (P.debug & kCountNotify) ? &ctrl->notify[1][w.lrank][w.pulse] : nullptr);
     } else {  // kItemUnpack
       if (threadIdx.x == 0) {
         wait_geq<true>(&rd.hdr->flag_f[w.pulse], seq, P.timeout_ns, P.err_host, tcode(4, w.lrank, w.pulse), P.poll_ns);
@@ -460,6 +463,26 @@ __global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t ba
       if (relaxed) st_relaxed_sys(peer, v); else st_release_sys(peer, v);
     }
   }
+}
+
+// Bandwidth floor: 16-B vector copy src -> dst (dst may be a peer pointer:
+// NVLink SM stores), 4 independent loads in flight per thread.
+__global__ void __launch_bounds__(256) k_bw_copy(const int4* __restrict__ src, int4* __restrict__ dst, size_t n16) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += 4 * stride) {
+    int4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k * stride < n16) v[k] = __ldcg(src + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k * stride < n16) dst[i + k * stride] = v[k];
+  }
+}
+
+cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st) {
+  k_bw_copy<<<grid, 256, 0, st>>>((const int4*)src, (int4*)dst, bytes / 16);
+  return cudaGetLastError();
 }
 
 // Empty kernel with the exchange kernels' PDL prologue (launch floor).

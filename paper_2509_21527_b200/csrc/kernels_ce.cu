@@ -34,18 +34,31 @@
 
 namespace halo {
 
+// 4 units per thread per batch: all gathers of a batch in flight before the stores.
 template <int W>
 __global__ void __launch_bounds__(256) k_ce_pack(const CeEnt* __restrict__ ents) {
   const CeEnt& e = ents[blockIdx.y];
   if (!e.pack) return;
   const uint32_t n = (uint32_t)e.n * W;
   const float s[3] = {e.shift[0], e.shift[1], e.shift[2]};
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    const uint32_t i = u / W;
-    const int c = (int)(u - i * W);
-    float v = __ldg(e.src + (size_t)__ldg(e.map + i) * W + c);
-    if (e.has_shift && c < 3) v = __fadd_rn(v, s[c]);
-    e.dst[u] = v;  // coalesced
+  const uint32_t G = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < n; base += 4 * G) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t u = base + k * G;
+      if (u < n) {
+        const uint32_t i = u / W;
+        v[k] = __ldg(e.src + (size_t)__ldg(e.map + i) * W + (u - i * W));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t u = base + k * G;
+      if (u >= n) continue;
+      const int c = (int)(u % W);
+      e.dst[u] = (e.has_shift && c < 3) ? __fadd_rn(v[k], s[c]) : v[k];  // coalesced
+    }
   }
 }
 
@@ -61,19 +74,34 @@ __global__ void __launch_bounds__(256) k_ce_unpack(const CeEnt* __restrict__ ent
   const uint32_t n = (uint32_t)e.n;
   const bool fs = fshift != nullptr && e.has_shift;
   double a[3] = {0.0, 0.0, 0.0};
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int t = __ldg(e.map + i);
-    float v[W];
+  const uint32_t G = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < n; base += 2 * G) {
+    int t[2];
+    float v[2][W], o[2][W];
 #pragma unroll
-    for (int c = 0; c < W; ++c) v[c] = __ldcg(e.src + (size_t)i * W + c);  // written by a peer's copy engine
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t i = base + k * G;
+      if (i >= n) continue;
+      t[k] = __ldg(e.map + i);
 #pragma unroll
-    for (int c = 0; c < W; ++c) {
-      float* d = e.dst + (size_t)t * W + c;
-      *d = accumulate ? __fadd_rn(*d, v[c]) : v[c];  // targets unique within a pulse
+      for (int c = 0; c < W; ++c) v[k][c] = __ldcg(e.src + (size_t)i * W + c);  // written by a peer's copy engine
     }
-    if (fs) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) a[c] += (double)v[c];
+    for (int k = 0; k < 2; ++k) {
+      if (base + k * G >= n) continue;
+#pragma unroll
+      for (int c = 0; c < W; ++c) o[k][c] = e.dst[(size_t)t[k] * W + c];
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (base + k * G >= n) continue;
+#pragma unroll
+      for (int c = 0; c < W; ++c)  // targets unique within a pulse
+        e.dst[(size_t)t[k] * W + c] = accumulate ? __fadd_rn(o[k][c], v[k][c]) : v[k][c];
+      if (fs) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) a[c] += (double)v[k][c];
+      }
     }
   }
   if (!fs) return;  // uniform over the CTA

@@ -65,7 +65,12 @@ __device__ __forceinline__ void load_rec(Rec* dst, const Rec* src) {
 }
 
 // ---------------------------------------------------------------- x (LL)
-template <int W>
+// kU = units per thread per batch: 1 for the latency regime (64-row items, at
+// most one unit per thread; fewest registers = most co-resident CTAs), 4 for
+// large items (bandwidth regime: every load of a batch is issued before any
+// store — the stores are asm volatile with a memory clobber, so one unit at a
+// time would serialise a full memory latency per unit).
+template <int W, int kU>
 __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constant__ ExParams P) {
   __shared__ XRec r;
   __shared__ uint64_t s_seq;
@@ -98,35 +103,81 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     const uint32_t n = r.n_units;
+    const uint32_t B = blockDim.x;
     if (r.kind == kItemXRecv) {
       // this rank's halo rows of one pulse: LL units -> x rows
-      for (uint32_t u = threadIdx.x; u < n; u += blockDim.x)
-        r.xdst[u] = ll_wait(r.ll + u, tag, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse), P.poll_ns);
-    } else {
-      // SEND: gather through the map, shift (R25), tag, store into the receiver's LL slot
-      const bool dep = r.kind == kItemXDep;
-      for (uint32_t u = threadIdx.x; u < n; u += blockDim.x) {
-        const uint32_t i = u / W;
-        const int c = (int)(u - i * W);
-        const int idx = s_map[i];
-        float v;
-        if (!dep) {
-          v = __ldg(r.x + (size_t)idx * W + c);  // home row: never written during the kernel
-        } else {
-          // forwarded row: the pulse it arrived in (Alg. 4 dependent part, R8/R9)
-          int q = 0;
-          while (q < P.P - 1 && (unsigned)(idx - r.recv_off[q]) >= (unsigned)r.recv_size[q]) ++q;
-          if (q < P.p_lo || (P.debug & kMutateXNoWait)) {
-            // arrived in an earlier launch (set_maps); kMutateXNoWait: the protocol
-            // mutation the sentinel tests must catch (forward without waiting)
-            v = __ldcg(r.x + (size_t)idx * W + c);
-          } else {
-            const uint64_t* src = r.xll_own + (size_t)q * P.ll_stride + (size_t)(idx - r.recv_off[q]) * W + c;
-            v = ll_wait(src, tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, q), P.poll_ns);
+      for (uint32_t base = threadIdx.x; base < n; base += kU * B) {
+        uint64_t w[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k)
+          if (base + k * B < n) w[k] = ld_relaxed_sys(r.ll + base + k * B);
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          const uint32_t u = base + k * B;
+          if (u >= n) continue;
+          if ((uint32_t)(w[k] >> 32) != tag)
+            w[k] = ll_spin(r.ll + u, tag, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse), P.poll_ns);
+          r.xdst[u] = __uint_as_float((uint32_t)w[k]);
+        }
+      }
+    } else if (r.kind == kItemXIndep) {
+      // SEND of home rows: gather through the map, shift (R25), tag, store into the receiver's LL slot
+      for (uint32_t base = threadIdx.x; base < n; base += kU * B) {
+        float v[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          const uint32_t u = base + k * B;
+          if (u < n) {
+            const uint32_t i = u / W;
+            v[k] = __ldg(r.x + (size_t)s_map[i] * W + (u - i * W));  // home row: never written during the kernel
           }
         }
-        if (r.has_shift && c < 3) v = __fadd_rn(v, r.shift[c]);
-        st_relaxed_sys(r.ll + u, ll_pack(v, tag));
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          const uint32_t u = base + k * B;
+          if (u >= n) continue;
+          const int c = (int)(u % W);
+          const float o = (r.has_shift && c < 3) ? __fadd_rn(v[k], r.shift[c]) : v[k];
+          st_relaxed_sys(r.ll + u, ll_pack(o, tag));
+        }
+      }
+    } else {
+      // SEND of forwarded rows: the pulse each arrived in (Alg. 4 dependent part, R8/R9);
+      // the row-level wait is the LL tag of the source unit
+      for (uint32_t base = threadIdx.x; base < n; base += kU * B) {
+        uint64_t w[kU];
+        const uint64_t* src[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          const uint32_t u = base + k * B;
+          src[k] = nullptr;
+          if (u < n) {
+            const uint32_t i = u / W;
+            const int c = (int)(u - i * W);
+            const int idx = s_map[i];
+            int q = 0;
+            while (q < P.P - 1 && (unsigned)(idx - r.recv_off[q]) >= (unsigned)r.recv_size[q]) ++q;
+            if (q < P.p_lo || (P.debug & kMutateXNoWait)) {
+              // arrived in an earlier launch (set_maps); kMutateXNoWait: the protocol
+              // mutation the sentinel tests must catch (forward without waiting)
+              w[k] = ((uint64_t)tag << 32) | __float_as_uint(__ldcg(r.x + (size_t)idx * W + c));
+            } else {
+              src[k] = r.xll_own + (size_t)q * P.ll_stride + (size_t)(idx - r.recv_off[q]) * W + c;
+              w[k] = ld_relaxed_sys(src[k]);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          const uint32_t u = base + k * B;
+          if (u >= n) continue;
+          if (src[k] != nullptr && (uint32_t)(w[k] >> 32) != tag)
+            w[k] = ll_spin(src[k], tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, r.pulse), P.poll_ns);
+          const int c = (int)(u % W);
+          float v = __uint_as_float((uint32_t)w[k]);
+          if (r.has_shift && c < 3) v = __fadd_rn(v, r.shift[c]);
+          st_relaxed_sys(r.ll + u, ll_pack(v, tag));
+        }
       }
     }
     __syncthreads();
@@ -236,7 +287,8 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
   if (threadIdx.x < 9) P.fshift[9 * g.lrank + threadIdx.x] = fs_old + tot;
 }
 
-template <int W>
+// kF = units per thread per batch (1: latency regime, 2: large items), as kU above.
+template <int W, int kF>
 __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
   __shared__ GRec g;
   __shared__ uint64_t s_seq;
@@ -301,40 +353,63 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
     const int c = (int)(threadIdx.x % W);
     double acc = 0.0;
     if (threadIdx.x < S) {
-      for (uint32_t u = threadIdx.x; u < n; u += S) {
-        const uint32_t k = u / W;
-        int4 a, b;
-        if (u == threadIdx.x && it == first) {
-          a = pre_a;  // prefetched before the PDL wait
-          b = pre_b;
-        } else {
-          a = __ldg(g.tasks + 2 * k);
-          b = __ldg(g.tasks + 2 * k + 1);
-        }
-        const int t = a.x, m = a.y;
-        const uint32_t cc[kMaxP] = {(uint32_t)a.z, (uint32_t)a.w, (uint32_t)b.x,
-                                    (uint32_t)b.y, (uint32_t)b.z, (uint32_t)b.w};
-        float v = g.f[(size_t)t * W + c];
-        // issue every contribution's load at once, then resolve stragglers
-        uint64_t w[kMaxP];
+      // task records, f and the contributions of a batch are loaded before any
+      // wait or store
+      for (uint32_t base = threadIdx.x; base < n; base += kF * S) {
+        int4 a[kF], b[kF];
 #pragma unroll
-        for (int j = 0; j < kMaxP; ++j)
-          if (j < m)
-            w[j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c);
-#pragma unroll
-        for (int j = 0; j < kMaxP; ++j) {
-          if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
-            const int q = (int)(cc[j] >> 24);
-            if ((uint32_t)(w[j] >> 32) != tag && !(P.debug & kMutateFNoWait))
-              w[j] = ll_spin(g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c, tag,
-                             P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
-            const float val = __uint_as_float((uint32_t)w[j]);
-            v = P.accumulate ? __fadd_rn(v, val) : val;
+        for (int k = 0; k < kF; ++k) {
+          const uint32_t u = base + k * S;
+          if (u >= n) continue;
+          if (u == threadIdx.x && it == first) {
+            a[k] = pre_a;  // prefetched before the PDL wait
+            b[k] = pre_b;
+          } else {
+            a[k] = __ldg(g.tasks + 2 * (u / W));
+            b[k] = __ldg(g.tasks + 2 * (u / W) + 1);
           }
         }
-        g.f[(size_t)t * W + c] = v;
-        if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(v, tag));
-        if (part) acc += (double)v;
+        // contributions j < kPre are loaded with the batch, any further ones (more
+        // than kPre pulses touching one row) when resolved
+        constexpr int kPre = 3;
+        float v[kF];
+        uint64_t w[kF][kPre];
+#pragma unroll
+        for (int k = 0; k < kF; ++k) {
+          const uint32_t u = base + k * S;
+          if (u >= n) continue;
+          const uint32_t cc[kMaxP] = {(uint32_t)a[k].z, (uint32_t)a[k].w, (uint32_t)b[k].x,
+                                      (uint32_t)b[k].y, (uint32_t)b[k].z, (uint32_t)b[k].w};
+          v[k] = g.f[(size_t)a[k].x * W + c];
+#pragma unroll
+          for (int j = 0; j < kPre; ++j)
+            if (j < a[k].y)
+              w[k][j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c);
+        }
+#pragma unroll
+        for (int k = 0; k < kF; ++k) {
+          const uint32_t u = base + k * S;
+          if (u >= n) continue;
+          const int t = a[k].x, m = a[k].y;
+          const uint32_t cc[kMaxP] = {(uint32_t)a[k].z, (uint32_t)a[k].w, (uint32_t)b[k].x,
+                                      (uint32_t)b[k].y, (uint32_t)b[k].z, (uint32_t)b[k].w};
+          float vv = v[k];
+#pragma unroll
+          for (int j = 0; j < kMaxP; ++j) {
+            if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
+              const int q = (int)(cc[j] >> 24);
+              const uint64_t* src = g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c;
+              uint64_t wj = j < kPre ? w[k][j < kPre ? j : 0] : ld_relaxed_sys(src);
+              if ((uint32_t)(wj >> 32) != tag && !(P.debug & kMutateFNoWait))
+                wj = ll_spin(src, tag, P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
+              const float val = __uint_as_float((uint32_t)wj);
+              vv = P.accumulate ? __fadd_rn(vv, val) : val;
+            }
+          }
+          g.f[(size_t)t * W + c] = vv;
+          if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(vv, tag));
+          if (part) acc += (double)vv;
+        }
       }
     }
     if (part) {  // fixed-tree CTA sum of the pushed forces per component -> the x-sender's slot
@@ -365,29 +440,35 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
 // ------------------------------------------------------------- launchers
 cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl);
 
-cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, cudaStream_t st) {
-  void* args[] = {(void*)&p};
-  const void* fn = layout == 4 ? (const void*)k_exchange_x_ll<4> : (const void*)k_exchange_x_ll<3>;
-  return launch_coop_kernel_ex(fn, grid, kThreads, args, st, true);
+template <int W>
+static const void* x_fn(bool wide) {
+  return wide ? (const void*)k_exchange_x_ll<W, 4> : (const void*)k_exchange_x_ll<W, 1>;
+}
+template <int W>
+static const void* f_fn(bool wide) {
+  return wide ? (const void*)k_exchange_f_ll<W, 2> : (const void*)k_exchange_f_ll<W, 1>;
 }
 
-cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, cudaStream_t st) {
+// wide = the plan's work items are large (bandwidth regime): batched variants
+cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st) {
   void* args[] = {(void*)&p};
-  const void* fn = layout == 4 ? (const void*)k_exchange_f_ll<4> : (const void*)k_exchange_f_ll<3>;
-  return launch_coop_kernel_ex(fn, grid, kThreads, args, st, true);
+  return launch_coop_kernel_ex(layout == 4 ? x_fn<4>(wide) : x_fn<3>(wide), grid, kThreads, args, st, true);
 }
 
-cudaError_t max_coresident_ll(int layout, int* x_blocks, int* f_blocks) {
+cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st) {
+  void* args[] = {(void*)&p};
+  return launch_coop_kernel_ex(layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide), grid, kThreads, args, st, true);
+}
+
+cudaError_t max_coresident_ll(int layout, bool wide, int* x_blocks, int* f_blocks) {
   int dev = 0, sms = 0, bx = 0, bf = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &bx, layout == 4 ? (const void*)k_exchange_x_ll<4> : (const void*)k_exchange_x_ll<3>, kThreads, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bx, layout == 4 ? x_fn<4>(wide) : x_fn<3>(wide), kThreads, 0);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &bf, layout == 4 ? (const void*)k_exchange_f_ll<4> : (const void*)k_exchange_f_ll<3>, kThreads, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide), kThreads, 0);
   if (e != cudaSuccess) return e;
   *x_blocks = bx * sms;
   *f_blocks = bf * sms;

@@ -29,14 +29,15 @@ cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* 
                             double* fs_dim, cudaStream_t st);
 cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
-cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
-cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, cudaStream_t st);
-cudaError_t max_coresident_ll(int layout, int* x_blocks, int* f_blocks);
+cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st);
+cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st);
+cudaError_t max_coresident_ll(int layout, bool wide, int* x_blocks, int* f_blocks);
 cudaError_t launch_empty(int grid, cudaStream_t st);
 cudaError_t launch_ce_pack(int layout, const CeEnt* ents, int n_local, int max_rows, cudaStream_t st);
 cudaError_t launch_ce_unpack(int layout, const CeEnt* ents, int n_local, int max_rows, double* fshift, int accumulate,
                              cudaStream_t st);
 cudaError_t launch_ce_sync(const CeSyncParams& s, cudaStream_t st);
+cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
 }  // namespace halo
 
 using namespace halo;
@@ -151,9 +152,14 @@ struct halo_ctx {
   bool x_done = false;
   uint32_t epoch = 0;
   uint64_t ping_base = 0;
-  int max_x = 0, max_f = 0;
+  int max_x = 0, max_f = 0;         // co-resident CTAs of the exchange kernels (LL: narrow variants)
+  int max_x_w = 0, max_f_w = 0;     // LL: batched variants for large work items
+  bool wide() const { return ll && item_rows >= 256; }
+  int cap_x() const { return wide() ? max_x_w : max_x; }
+  int cap_f() const { return wide() ? max_f_w : max_f; }
   int last_grid[2] = {0, 0};
   int item_rows = 64;
+  bool item_rows_fixed = false;     // HALO_ITEM_ROWS given: no adaptive choice
   uint32_t poll_ns = 0;
   uint32_t debug = 0;
 
@@ -316,7 +322,10 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   ctx->scratch.assign(ctx->n_local, nullptr);
   ctx->peer_x.assign(ctx->nranks, nullptr);
   ctx->peer_scratch.assign(ctx->nranks, nullptr);
-  if (const char* e = getenv("HALO_ITEM_ROWS")) ctx->item_rows = std::min(kMaxItemRows, std::max(kMinItemRows, atoi(e)));
+  if (const char* e = getenv("HALO_ITEM_ROWS")) {
+    ctx->item_rows = std::min(kMaxItemRows, std::max(kMinItemRows, atoi(e)));
+    ctx->item_rows_fixed = true;
+  }
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = (uint32_t)std::max(0, atoi(e));
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
@@ -332,8 +341,9 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_small, 64 * 1024);
   if (e == cudaSuccess)
-    e = ctx->ll ? max_coresident_ll(cfg->layout, &ctx->max_x, &ctx->max_f)
+    e = ctx->ll ? max_coresident_ll(cfg->layout, false, &ctx->max_x, &ctx->max_f)
                 : max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
+  if (e == cudaSuccess && ctx->ll) e = max_coresident_ll(cfg->layout, true, &ctx->max_x_w, &ctx->max_f_w);
   if (e != cudaSuccess) {
     // keep ctx to carry the message? The ABI returns NULL on error; print once.
     fprintf(stderr, "halo_init: %s\n", cudaGetErrorString(e));
@@ -1190,7 +1200,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     if ((s = upload_plan(ctx)) != HALO_OK) return s;
     ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
     if (ctx->ll)
-      CK(launch_exchange_x_ll(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
+      CK(launch_exchange_x_ll(X, W, grid_for(ctx->n_items_x, L, ctx->cap_x()), ctx->wide(), st));
     else
       CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
     CK(cudaStreamSynchronize(st));
@@ -1217,6 +1227,17 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   if (any & kErrCapacity) return fail(ctx, HALO_ERR_CAPACITY, "n_home + received rows exceed capacity on some rank");
   if (any & kErrGeometry) return fail(ctx, HALO_ERR_GEOMETRY, "a home atom lies outside its rank's cell");
   if (any & kErrMap) return fail(ctx, HALO_ERR_ARG, "invalid explicit map on some rank");
+  // work-item size: 64 rows (latency regime; swept 32-512 at C3) unless the
+  // pulses are so large that a CTA would run more than ~2 items in sequence —
+  // then larger items (fewer dependent record/map round trips per row)
+  if (!ctx->item_rows_fixed) {
+    long rows = 0;
+    for (int i = 0; i < L * P; ++i) rows += std::max(ctx->send_size[i], ctx->recv_size[i]);
+    const long ctas = std::max(1, std::min(ctx->max_x, ctx->max_f));
+    int R = 64;
+    while (R < kMaxItemRows && rows / R > 2 * ctas) R *= 2;
+    ctx->item_rows = R;
+  }
   // final plan: all pulses
   for (int l = 0; l < L; ++l)
     for (int p = 0; p < P; ++p) fill_pulse_dev(ctx, l, p);
@@ -1296,10 +1317,10 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   if (ctx->P == 0) return HALO_OK;
   if (ctx->ce) return ce_exchange_x(ctx, (cudaStream_t)stream);
   ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, 0, ctx->P);
-  const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->max_x);
+  const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
   ctx->last_grid[0] = grid;
   if (ctx->ll)
-    CK(launch_exchange_x_ll(X, ctx->W, grid, (cudaStream_t)stream));
+    CK(launch_exchange_x_ll(X, ctx->W, grid, ctx->wide(), (cudaStream_t)stream));
   else
     CK(launch_exchange_x(X, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
@@ -1316,15 +1337,15 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   ExParams F = make_params(ctx, ctx->d_items_f, ctx->n_items_f, 0, ctx->P);
   F.fshift = fshift;
   F.accumulate = accumulate ? 1 : 0;
-  int grid = grid_for(ctx->n_items_f, ctx->n_local, ctx->max_f);
+  int grid = grid_for(ctx->n_items_f, ctx->n_local, ctx->cap_f());
   if (ctx->ll) {  // dedicated CTAs for the combines
     F.n_tail = ctx->n_tail_f;
-    grid = std::min(ctx->n_items_f - ctx->n_tail_f, ctx->max_f - ctx->n_tail_f) + ctx->n_tail_f;
+    grid = std::min(ctx->n_items_f - ctx->n_tail_f, ctx->cap_f() - ctx->n_tail_f) + ctx->n_tail_f;
     grid = std::max(grid, 1);
   }
   ctx->last_grid[1] = grid;
   if (ctx->ll)
-    CK(launch_exchange_f_ll(F, ctx->W, grid, (cudaStream_t)stream));
+    CK(launch_exchange_f_ll(F, ctx->W, grid, ctx->wide(), (cudaStream_t)stream));
   else
     CK(launch_exchange_f(F, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
@@ -1402,6 +1423,17 @@ halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
   }
   if (x_ns) *x_ns = v[0];
   if (f_ns) *f_ns = v[1];
+  return HALO_OK;
+}
+
+halo_status halo_get_notify_counts(halo_ctx* ctx, int which, uint32_t* out, int cap) {
+  if (!ctx || which < 0 || which > 1 || !out || cap < ctx->n_local * ctx->P) return HALO_ERR_ARG;
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  uint32_t v[kMaxLocal][kMaxP];
+  CK(cudaMemcpy(v, &ctx->ctrl->notify[which][0][0], sizeof v, cudaMemcpyDeviceToHost));
+  for (int l = 0; l < ctx->n_local; ++l)
+    for (int p = 0; p < ctx->P; ++p) out[l * ctx->P + p] = v[l][p];
   return HALO_OK;
 }
 
@@ -1487,6 +1519,42 @@ halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_pe
     CK(cudaGraphDestroy(g));
   }
   *us_per_launch = 1e3 * (double)ms / iters;
+  CK(cudaEventDestroy(e0));
+  CK(cudaEventDestroy(e1));
+  CK(cudaStreamDestroy(st));
+  return HALO_OK;
+}
+
+halo_status halo_floor_bandwidth(halo_ctx* ctx, int peer_rank, size_t bytes, int mode, int iters, double* gbs) {
+  if (!ctx || peer_rank < 0 || peer_rank >= ctx->nranks || iters <= 0 || !gbs || (mode != 0 && mode != 1))
+    return HALO_ERR_ARG;
+  if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
+  // the coordinate + force LL receive areas of the peer's scratch (2 * P slots)
+  const size_t area = 2 * (size_t)ctx->P * ctx->ll_stride * sizeof(uint64_t);
+  bytes = bytes / 16 * 16;
+  if (bytes == 0 || bytes > area) return fail(ctx, HALO_ERR_ARG, "bytes must be in [16, LL receive area]");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int me = ctx->first_rank;
+  char* src = reinterpret_cast<char*>(ctx->xll_of(me));
+  char* dst = reinterpret_cast<char*>(ctx->xll_of(peer_rank));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  int sms = 148, dev = ctx->cfg.device;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  auto one = [&]() -> cudaError_t {
+    return mode == 0 ? launch_bw_copy(src, dst, bytes, 8 * sms, st) : cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+  };
+  for (int i = 0; i < 3; ++i) CK(one());
+  CK(cudaEventRecord(e0, st));
+  for (int i = 0; i < iters; ++i) CK(one());
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  *gbs = (double)bytes * iters / (1e-3 * (double)ms) / 1e9;
   CK(cudaEventDestroy(e0));
   CK(cudaEventDestroy(e1));
   CK(cudaStreamDestroy(st));

@@ -177,6 +177,13 @@ class Halo:
         self._ck(self.lib.halo_get_timers(self.h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
+    def get_notify_counts(self, which):
+        """Cumulative system-scope flag stores per (local rank, pulse) (HALO_DEBUG=64, paper protocol)."""
+        nl, P = self.local_ranks()[1], len(self.pulse_order())
+        buf = (c_uint * max(1, nl * P))()
+        self._ck(self.lib.halo_get_notify_counts(self.h, int(which), buf, len(buf)))
+        return np.array(buf[: nl * P], dtype=np.int64).reshape(nl, P)
+
     def get_trace(self, which):
         """Per-CTA [start, record loaded, items done, exit, item0 tag, item0 end, item1 tag, item1 end]
         (ns; tag = kind << 16 | lrank << 8 | pulse) of the last x (0) / f (1) launch."""
@@ -194,6 +201,13 @@ class Halo:
     def floor_launch(self, iters=1000, graph=False) -> float:
         v = c_double()
         self._ck(self.lib.halo_floor_launch(self.h, int(iters), int(bool(graph)), ctypes.byref(v)))
+        return v.value
+
+    def floor_bandwidth(self, peer_rank, nbytes, mode=0, iters=20) -> float:
+        """GB/s of SM peer stores (mode 0) or copy-engine copies (mode 1) into peer_rank's scratch."""
+        v = c_double()
+        self._ck(self.lib.halo_floor_bandwidth(self.h, int(peer_rank), c_size_t(int(nbytes)), int(mode), int(iters),
+                                               ctypes.byref(v)))
         return v.value
 
     def sync(self):

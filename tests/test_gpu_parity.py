@@ -317,3 +317,26 @@ def test_two_neighbour_search_epochs():
     run_gpu_case(case2, sess, steps=2)
     run_gpu_case(case1, sess, steps=1)
     sess.destroy()
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_notification_minimality_paper_protocol(name, monkeypatch):
+    """Pin G4: the paper protocol emits exactly ONE system-scope flag
+    store per (rank, pulse) per exchange, from the last CTA of the pulse."""
+    monkeypatch.setenv("HALO_DEBUG", "64")
+    case = Case(name, seed=1, force_kind="int")
+    sess = session_for(case, flags=PAPER)
+    run_gpu_case(case, sess)  # set_maps + one checked step
+    x0, f0 = sess.halo.get_notify_counts(0), sess.halo.get_notify_counts(1)
+    K = 7
+    for _ in range(K):
+        sess.exchange_x()
+        sess.exchange_f()
+    sess.halo.sync()
+    dx, df = sess.halo.get_notify_counts(0) - x0, sess.halo.get_notify_counts(1) - f0
+    for l in range(sess.n_local):
+        lay = sess.layout_of(l)
+        for p in range(sess.npulse):
+            assert dx[l, p] == K * (lay["send_size"][p] > 0), (l, p, dx[l, p])
+            assert df[l, p] == K * (lay["recv_size"][p] > 0), (l, p, df[l, p])
+    sess.destroy()
