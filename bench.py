@@ -173,7 +173,7 @@ def run_fused(args, rank, world, local):
     torch.cuda.set_device(dev)
     homes = assign_home(X, c.L, c.grid)
     cap = int(max(len(h) for h in homes) * 2.2) + 4096
-    flags = (HALO_F_TIMERS if args.timers else 0) | PROTO_FLAGS[args.proto]
+    flags = (HALO_F_TIMERS if args.timers else 0) | PROTO_FLAGS[args.proto] | ((1 << 6) if args.l2_persist else 0)
     sess = HaloSession(c.grid, c.L, c.rc, c.pulses, layout=args.layout, capacity=cap, device=local, flags=flags,
                        nprocs=world, proc=rank, timeout_s=20.0)
     first, nl = sess.first_rank, sess.n_local
@@ -372,7 +372,8 @@ def run_fused(args, rank, world, local):
         "warmup": args.warmup, "ms_per_step": round(res["step"] / 1e3, 6), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(workload_desc(c, world, W), parallelism=f"spatial DD {c.grid[0]}x{c.grid[1]}x{c.grid[2]}",
-                       protocol=args.proto,
+                       protocol=args.proto, plan_in_l2=("persisting (HALO_F_L2_PERSIST)" if args.l2_persist
+                                                        else "flushed with everything else"),
                        mode=("eager, one exchange_x + one exchange_f launch per GPU per step" if args.proto != "ce"
                              else "eager, copy-engine path: per pulse pack + cudaMemcpyAsync + flag kernels")),
         "x_us": round(res["x"], 3), "f_us": round(res["f"], 3), "step_median_us": round(res["step_median"], 3),
@@ -395,10 +396,19 @@ def run_fused(args, rank, world, local):
         "nccl_baseline": nccl,
         "device_spans": dev_spans,
     }
+    if world == 1 and nl > 1 and not args.no_floors:
+        # all DD ranks on one GPU: the same-GPU flag round trip (two CTAs of one launch)
+        t0 = sess.halo.floor_pingpong(first + 1, iters=10000, relaxed=False)
+        t0r = sess.halo.floor_pingpong(first + 1, iters=10000, relaxed=True)
+        floor = {"t0_one_way_us": t0r, "t0_release_acquire_us": t0, "bandwidth": None,
+                 "note": "same-GPU floor: relaxed 8-B store seen by a relaxed poll from another CTA (L2 "
+                         "round trip); median of 1e4 round trips / 2"}
+        out["latency_floor"] = floor
     launch_eager = max_over_ranks(sess.halo.floor_launch(1000, graph=False)) if not args.no_floors else 0.0
     launch_graph = max_over_ranks(sess.halo.floor_launch(1000, graph=True)) if not args.no_floors else 0.0
     if floor is None:
         floor = {}
+        out["latency_floor"] = floor
     floor["launch_us_eager"] = round(launch_eager, 3)
     floor["launch_us_graph"] = round(launch_graph, 3)
     if floor.get("t0_one_way_us"):
@@ -528,6 +538,7 @@ def main():
     ap.add_argument("--proto", default="ll", choices=sorted(PROTO_FLAGS),
                     help="ll: default LL protocol; paper: per-pulse flags (Alg. 5); ce: copy-engine path")
     ap.add_argument("--timers", action="store_true")
+    ap.add_argument("--l2-persist", action="store_true", help="HALO_F_L2_PERSIST: static plan in persisting L2")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -84,6 +84,11 @@ typedef enum {
                                            CE copy of the contiguous halo slice, flag, ordered scatter-add.
                                            ~3 launches + L copies per pulse; bit-exact like the default.
                                            Takes precedence over HALO_F_PAPER_FLAGS (set_maps uses its kernels). */
+#define HALO_F_L2_PERSIST     (1u << 6) /* LL protocol: keep the static plan (work-item blocks: records, map
+                                           slices, gather task records; rebuilt only by set_maps) in the
+                                           persisting L2 carve-out (access-policy window on the exchange
+                                           launches; raises cudaLimitPersistingL2CacheSize device-wide to the
+                                           plan size if lower).  Coordinates and forces are never persisted. */
 
 typedef struct {
   int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */
@@ -233,7 +238,9 @@ HALO_API halo_status halo_get_notify_counts(halo_ctx* ctx, int which, uint32_t* 
 
 /* Floors (measurement): ping-pong `iters` round trips of a
  * 64-bit flag between this process's local rank 0 and DD rank `peer_rank`
- * (COLLECTIVE between the two processes only; other processes must not call).
+ * (COLLECTIVE between the two processes only; other processes must not call;
+ * a peer hosted by this process is served by a second CTA of the same launch:
+ * the same-GPU floor).
  * relaxed = 0: st.release.sys / ld.acquire.sys (the paper's signal);
  * relaxed = 1: st.relaxed.sys / ld.relaxed.sys (the LL protocol's unit).
  * *one_way_us = median round trip / 2 (initiator; 0 on the responder). */

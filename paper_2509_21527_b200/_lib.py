@@ -20,6 +20,7 @@ HALO_F_GPU_FENCE = 1 << 2
 HALO_F_TIMERS = 1 << 3
 HALO_F_PAPER_FLAGS = 1 << 4
 HALO_F_CE_PATH = 1 << 5
+HALO_F_L2_PERSIST = 1 << 6
 HALO_MAX_PULSES = 6
 
 # every symbol include/halo.h declares (checked by tests/test_abi.py)

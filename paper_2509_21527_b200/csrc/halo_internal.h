@@ -131,9 +131,10 @@ struct Item {
   uint32_t end;
 };
 
-// LL protocol work records: each CTA loads one 128-B record (one coalesced
-// line) that carries every pointer it needs, so a cold-L2 launch pays one
-// round trip for its plan instead of a chain of dependent loads.
+// LL protocol work records: each item's block starts with one 128-B record that
+// carries every pointer it needs, followed by the item's map slice (x) or task
+// records (f), so a cold-L2 launch pays one round trip for its plan instead of a
+// chain of dependent loads; the next item's block is prefetched (cp.async).
 struct __align__(128) XRec {
   uint8_t kind;             // kItemXIndep / kItemXDep / kItemXRecv
   uint8_t pulse;
@@ -159,7 +160,7 @@ struct __align__(128) GRec {
   uint32_t wrap_mask;       // combine: pulses this rank shifted in (R13)
   uint8_t pulse_dim[8];
   uint32_t pad;
-  const int4* tasks;        // gather: 32-B task records (row, n, contrib[6]) + begin
+  const int4* tasks;        // unused (the task records follow the GRec in its item block)
   float* f;                 // gather: own f base
   const uint64_t* fll_own;  // own force LL base (slot q at + q*ll_stride)
   uint64_t* push;           // gather of slice rows: x-sender's LL slot p minus recv_off_p*W (index row*W + c)
@@ -190,10 +191,9 @@ struct ExParams {
   uint64_t ll_stride;       // u64 units per pulse slot of the LL receive buffers
   uint32_t debug;           // HALO_DEBUG experiment bits (0 in production)
   uint32_t fsp_slots;       // shift-force slots per pulse in each rank's scratch
-  const XRec* xrec;         // LL protocol work records (x)
-  const int32_t* xmap;      // per x item: its map slice (item_rows entries), loaded with the record
+  const char* xblk;         // LL x item blocks: [XRec | map slice, item_rows int32], 128 + 4*item_rows B each
+  const char* fblk;         // LL f item blocks: [GRec | task records, item_rows x 32 B], 128 + 32*item_rows B each
   int item_rows;
-  const GRec* grec;         // LL protocol work records (f)
 };
 
 // Copy-engine path (HALO_F_CE_PATH, kernels_ce.cu): one entry per (pulse, local rank).

@@ -436,9 +436,17 @@ __global__ void k_unpack_f(const int32_t* __restrict__ map, int n, const float* 
 }
 
 // --------------------------------------------------------------- latency floor
+// One CTA per side; launched with 2 CTAs when both ranks live on this GPU
+// (CTA 1 plays the responder: own/peer swapped).
 __global__ void k_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                            uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (threadIdx.x != 0) return;
+  if (blockIdx.x == 1) {
+    uint64_t* t = own;
+    own = peer;
+    peer = t;
+    initiator = 0;
+  }
   for (int i = 1; i <= iters; ++i) {
     const uint64_t v = base + (uint64_t)i;
     const uint64_t t0 = gtimer();
@@ -518,14 +526,20 @@ static int pdl_enabled() {
 // Exchange-kernel launch: cooperative (every CTA co-resident)
 // unless HALO_COOP=0; `pdl` adds programmatic stream serialisation (the kernel
 // is scheduled while its predecessor drains and blocks in griddepcontrol.wait).
-cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl) {
+cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl,
+                                  size_t smem, const cudaAccessPolicyWindow* win) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int n = 0;
+  if (win != nullptr && win->num_bytes > 0) {  // HALO_F_L2_PERSIST: the static plan stays in L2
+    attr[n].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[n].val.accessPolicyWindow = *win;
+    ++n;
+  }
   if (coop_enabled()) {
     attr[n].id = cudaLaunchAttributeCooperative;
     attr[n].val.cooperative = 1;
@@ -543,11 +557,11 @@ cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** ar
 
 cudaError_t launch_empty(int grid, cudaStream_t st) {
   void* args[] = {nullptr};
-  return launch_coop_kernel_ex((const void*)k_empty, grid, kThreads, args, st, true);
+  return launch_coop_kernel_ex((const void*)k_empty, grid, kThreads, args, st, true, 0, nullptr);
 }
 
 cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args, cudaStream_t st) {
-  return launch_coop_kernel_ex(fn, grid, block, args, st, false);
+  return launch_coop_kernel_ex(fn, grid, block, args, st, false, 0, nullptr);
 }
 
 cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStream_t st) {
@@ -623,7 +637,8 @@ cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* 
 
 cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st) {
-  k_pingpong<<<1, 32, 0, st>>>(own, peer, iters, base, initiator, relaxed, rtt_ns, timeout_ns, err_host);
+  k_pingpong<<<initiator == 2 ? 2 : 1, 32, 0, st>>>(own, peer, iters, base, initiator == 2 ? 1 : initiator, relaxed,
+                                                    rtt_ns, timeout_ns, err_host);
   return cudaGetLastError();
 }
 

@@ -57,13 +57,6 @@ __device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64
   return __uint_as_float((uint32_t)v);
 }
 
-// Cooperative load of one 128-B record into shared memory (one coalesced line).
-template <class Rec>
-__device__ __forceinline__ void load_rec(Rec* dst, const Rec* src) {
-  if (threadIdx.x < 32)
-    reinterpret_cast<uint32_t*>(dst)[threadIdx.x] = __ldg(reinterpret_cast<const uint32_t*>(src) + threadIdx.x);
-}
-
 // ---------------------------------------------------------------- x (LL)
 // kU = units per thread per batch: 1 for the latency regime (64-row items, at
 // most one unit per thread; fewest registers = most co-resident CTAs), 4 for
@@ -72,33 +65,31 @@ __device__ __forceinline__ void load_rec(Rec* dst, const Rec* src) {
 // time would serialise a full memory latency per unit).
 template <int W, int kU>
 __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constant__ ExParams P) {
-  __shared__ XRec r;
+  // two item blocks [XRec | map slice of item_rows ints], double-buffered: the
+  // next item's block is fetched (cp.async) while the current one is processed
+  extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq;
-  __shared__ int32_t s_map[kMaxItemRows];
+  const uint32_t XB = 128u + 4u * (uint32_t)P.item_rows;
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[0][blockIdx.x][0] = gtimer();
   pdl_launch_dependents();
-  // the plan record and its map slice are static: one round trip, issued while
-  // the previous kernel drains (PDL)
-  if ((int)blockIdx.x < P.n_items) {
-    load_rec(&r, P.xrec + blockIdx.x);
-    for (int t = threadIdx.x; t < P.item_rows; t += blockDim.x) s_map[t] = __ldg(P.xmap + (size_t)blockIdx.x * P.item_rows + t);
-  }
+  // the first block is static plan data: fetched while the previous kernel drains (PDL)
+  if ((int)blockIdx.x < P.n_items) cp_async_block(s_blk, P.xblk + (size_t)blockIdx.x * XB, XB);
   pdl_wait();  // everything below may depend on earlier work of the stream
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
+  cp_async_wait_all();
   __syncthreads();
   // arrive early: the atomic's latency hides behind the items (launch_arrive)
   const uint32_t arrived = launch_arrive(&ctrl->done_x);
   uint64_t seq = 0;
+  int cur = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    if (it != (int)blockIdx.x) {
-      __syncthreads();  // everyone is done with the previous record
-      load_rec(&r, P.xrec + it);
-      for (int t = threadIdx.x; t < P.item_rows; t += blockDim.x) s_map[t] = __ldg(P.xmap + (size_t)it * P.item_rows + t);
-    }
-    __syncthreads();
+    if (it + (int)gridDim.x < P.n_items)
+      cp_async_block(s_blk + (cur ^ 1) * XB, P.xblk + (size_t)(it + gridDim.x) * XB, XB);
+    const XRec& r = *reinterpret_cast<const XRec*>(s_blk + cur * XB);
+    const int32_t* s_map = reinterpret_cast<const int32_t*>(s_blk + cur * XB + 128);
     if (trace && seq == 0) ctrl->trace[0][blockIdx.x][1] = gtimer();
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
@@ -180,7 +171,6 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
         }
       }
     }
-    __syncthreads();
     if (trace) {
       const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
       if (slot < 2) {
@@ -188,6 +178,9 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
         ctrl->trace[0][blockIdx.x][5 + 2 * slot] = gtimer();
       }
     }
+    cp_async_wait_all();  // the next block has landed ...
+    __syncthreads();      // ... for every thread, and everyone is done with this one
+    cur ^= 1;
   }
   seq = s_seq;
   if (trace) ctrl->trace[0][blockIdx.x][2] = gtimer();
@@ -289,17 +282,17 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
 
 // kF = units per thread per batch (1: latency regime, 2: large items), as kU above.
 template <int W, int kF>
-__global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
-  __shared__ GRec g;
+__global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
+  // two item blocks [GRec | task records of item_rows rows (32 B each)], double-
+  // buffered like the x kernel's
+  extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq;
   __shared__ double s_fs[9][kThreads];
+  const uint32_t FB = 128u + 32u * (uint32_t)P.item_rows;
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[1][blockIdx.x][0] = gtimer();
   pdl_launch_dependents();
-  // static plan data (work record, first gather task record) is loaded while the
-  // previous kernel of the stream drains (PDL); f itself is read after the wait
-  int4 pre_a = make_int4(0, 0, 0, 0), pre_b = make_int4(0, 0, 0, 0);
   // items [0, n_main) round-robin over CTAs [0, G - n_tail); the n_tail shift-force
   // combines (last in the item order) get one dedicated CTA each, so they start
   // polling at once instead of behind their CTA's earlier items
@@ -308,33 +301,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
   const int first = ((int)blockIdx.x < Gm) ? (int)blockIdx.x : n_main + ((int)blockIdx.x - Gm);
   const int stride = ((int)blockIdx.x < Gm) ? Gm : P.n_items;
   const int end = ((int)blockIdx.x < Gm) ? n_main : P.n_items;
-  if (first < end) {
-    load_rec(&g, P.grec + first);
-    __syncthreads();
-    if (g.kind == kItemGather && threadIdx.x < (blockDim.x / W) * W && threadIdx.x < g.n_units) {
-      const uint32_t k = threadIdx.x / W;
-      pre_a = __ldg(g.tasks + 2 * k);
-      pre_b = __ldg(g.tasks + 2 * k + 1);
-    }
-  }
+  // the first block is static plan data: fetched while the previous kernel of the
+  // stream drains (PDL); f itself is read after the wait
+  if (first < end) cp_async_block(s_blk, P.fblk + (size_t)first * FB, FB);
   pdl_wait();
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
   timer_start(P.flags, &ctrl->t_start_f);
+  cp_async_wait_all();
   __syncthreads();
   const uint32_t arrived = launch_arrive(&ctrl->done_f);
   uint64_t seq = 0;
+  int cur = 0;
   for (int it = first; it < end; it += stride) {
-    if (it != first) {
-      __syncthreads();  // everyone is done with the previous record
-      load_rec(&g, P.grec + it);
-    }
-    __syncthreads();
+    if (it + stride < end) cp_async_block(s_blk + (cur ^ 1) * FB, P.fblk + (size_t)(it + stride) * FB, FB);
+    const GRec& g = *reinterpret_cast<const GRec*>(s_blk + cur * FB);
+    const int4* tasks = reinterpret_cast<const int4*>(s_blk + cur * FB + 128);
     if (trace && seq == 0) ctrl->trace[1][blockIdx.x][1] = gtimer();
     seq = s_seq;
     const uint32_t tag = (uint32_t)seq;
     if (g.kind == kItemFshift) {
       if (P.fshift != nullptr) fshift_combine(g, P, tag, s_fs, P.fsp_slots);
-      __syncthreads();
       if (trace) {
         const int slot = (it - first) / stride;
         if (slot < 2) {
@@ -342,6 +328,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
           ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();
         }
       }
+      cp_async_wait_all();
+      __syncthreads();
+      cur ^= 1;
       continue;
     }
     const uint32_t n = g.n_units;
@@ -361,13 +350,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
         for (int k = 0; k < kF; ++k) {
           const uint32_t u = base + k * S;
           if (u >= n) continue;
-          if (u == threadIdx.x && it == first) {
-            a[k] = pre_a;  // prefetched before the PDL wait
-            b[k] = pre_b;
-          } else {
-            a[k] = __ldg(g.tasks + 2 * (u / W));
-            b[k] = __ldg(g.tasks + 2 * (u / W) + 1);
-          }
+          a[k] = tasks[2 * (u / W)];
+          b[k] = tasks[2 * (u / W) + 1];
         }
         // contributions j < kPre are loaded with the batch, any further ones (more
         // than kPre pulses touching one row) when resolved
@@ -421,7 +405,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
         st_relaxed_sys(g.part + 2 * threadIdx.x + 1, ll_pack(__uint_as_float((uint32_t)__double2loint(tot)), tag));
       }
     }
-    __syncthreads();
     if (trace) {
       const int slot = (it - first) / stride;
       if (slot < 2) {
@@ -429,7 +412,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
         ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();
       }
     }
+    cp_async_wait_all();
     __syncthreads();
+    cur ^= 1;
   }
   seq = s_seq;
   if (trace) ctrl->trace[1][blockIdx.x][2] = gtimer();
@@ -438,7 +423,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_exchange_f_ll(const __grid_cons
 }
 
 // ------------------------------------------------------------- launchers
-cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl);
+cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl,
+                                  size_t smem, const cudaAccessPolicyWindow* win);
 
 template <int W>
 static const void* x_fn(bool wide) {
@@ -449,26 +435,44 @@ static const void* f_fn(bool wide) {
   return wide ? (const void*)k_exchange_f_ll<W, 2> : (const void*)k_exchange_f_ll<W, 1>;
 }
 
+// Dynamic shared memory of the LL kernels: two item blocks.
+size_t x_smem_bytes(int rows) { return 2 * (128 + 4 * (size_t)rows); }
+size_t f_smem_bytes(int rows) { return 2 * (128 + 32 * (size_t)rows); }
+
 // wide = the plan's work items are large (bandwidth regime): batched variants
-cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st) {
+cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
+                                 cudaStream_t st) {
   void* args[] = {(void*)&p};
-  return launch_coop_kernel_ex(layout == 4 ? x_fn<4>(wide) : x_fn<3>(wide), grid, kThreads, args, st, true);
+  return launch_coop_kernel_ex(layout == 4 ? x_fn<4>(wide) : x_fn<3>(wide), grid, kThreads, args, st, true,
+                               x_smem_bytes(p.item_rows), win);
 }
 
-cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st) {
+cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
+                                 cudaStream_t st) {
   void* args[] = {(void*)&p};
-  return launch_coop_kernel_ex(layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide), grid, kThreads, args, st, true);
+  return launch_coop_kernel_ex(layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide), grid, kThreads, args, st, true,
+                               f_smem_bytes(p.item_rows), win);
 }
 
+// Co-resident CTAs per GPU for the narrow (items <= 128 rows) or wide (<= 512)
+// variants, at the largest item size each runs with (a smaller launch only fits
+// more).  Also opts the kernels into their dynamic shared memory.
 cudaError_t max_coresident_ll(int layout, bool wide, int* x_blocks, int* f_blocks) {
   int dev = 0, sms = 0, bx = 0, bf = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bx, layout == 4 ? x_fn<4>(wide) : x_fn<3>(wide), kThreads, 0);
+  const int rows = wide ? kMaxItemRows : 128;
+  const void* fx = layout == 4 ? x_fn<4>(wide) : x_fn<3>(wide);
+  const void* ff = layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide);
+  e = cudaFuncSetAttribute(fx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)x_smem_bytes(kMaxItemRows));
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide), kThreads, 0);
+  e = cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f_smem_bytes(kMaxItemRows));
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bx, fx, kThreads, x_smem_bytes(rows));
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, ff, kThreads, f_smem_bytes(rows));
   if (e != cudaSuccess) return e;
   *x_blocks = bx * sms;
   *f_blocks = bf * sms;

@@ -54,6 +54,22 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
   return v;
 }
 
+// Asynchronous global -> shared copies (LDGSTS): the next work item's block is
+// fetched while the current one is processed.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Block copy of `bytes` (multiple of 16) by the whole CTA, asynchronous.
+__device__ __forceinline__ void cp_async_block(void* smem, const void* gmem, uint32_t bytes) {
+  for (uint32_t o = threadIdx.x * 16u; o < bytes; o += blockDim.x * 16u)
+    cp_async16(static_cast<char*>(smem) + o, static_cast<const char*>(gmem) + o);
+  cp_async_commit();
+}
+
 // Programmatic dependent launch (sm_90+): let the next kernel of the stream be
 // scheduled now, and block until the previous kernel's memory is complete.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

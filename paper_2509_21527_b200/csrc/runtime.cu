@@ -29,8 +29,10 @@ cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* 
                             double* fs_dim, cudaStream_t st);
 cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
-cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st);
-cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, cudaStream_t st);
+cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
+                                 cudaStream_t st);
+cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
+                                 cudaStream_t st);
 cudaError_t max_coresident_ll(int layout, bool wide, int* x_blocks, int* f_blocks);
 cudaError_t launch_empty(int grid, cudaStream_t st);
 cudaError_t launch_ce_pack(int layout, const CeEnt* ents, int n_local, int max_rows, cudaStream_t st);
@@ -117,14 +119,14 @@ struct halo_ctx {
   int* err_dev = nullptr;
   char* d_csr = nullptr;            // force-gather tasks + CSR of all local ranks (LL protocol)
   size_t csr_bytes = 0;
-  std::vector<int4*> csr_tasks;     // per local rank: 32-B task records (row, n, contrib[6])
+  std::vector<std::vector<int32_t>> h_tasks;  // per local rank: 32-B task records (row, n, contrib[6]), 8 ints each
   std::vector<XRec> h_xrec;
-  std::vector<int32_t> h_xmap;          // per x item: its map slice (item_rows entries), loaded with the record
+  std::vector<int32_t> h_xmap;          // per x item: its map slice (item_rows entries)
+  std::vector<char> h_xblk, h_fblk;     // item blocks [record | map slice] / [record | task records]
+  char* d_xblk = nullptr;
+  char* d_fblk = nullptr;
   std::vector<std::vector<std::vector<int32_t>>> h_maps;  // host copy of every local rank's maps [l][p]
-  int32_t* d_xmap = nullptr;
   std::vector<GRec> h_grec;
-  XRec* d_xrec = nullptr;
-  GRec* d_grec = nullptr;
 
   // copy-engine path (HALO_F_CE_PATH): per pulse, per local rank
   struct CeCopy {
@@ -152,6 +154,7 @@ struct halo_ctx {
   bool x_done = false;
   uint32_t epoch = 0;
   uint64_t ping_base = 0;
+  cudaAccessPolicyWindow l2win{};    // HALO_F_L2_PERSIST: the static plan (item blocks) persists in L2
   int max_x = 0, max_f = 0;         // co-resident CTAs of the exchange kernels (LL: narrow variants)
   int max_x_w = 0, max_f_w = 0;     // LL: batched variants for large work items
   bool wide() const { return ll && item_rows >= 256; }
@@ -692,22 +695,9 @@ static halo_status build_csr(halo_ctx* ctx, cudaStream_t st) {
       for (int j = 0; j < n; ++j) r[8 * k + 2 + j] = (int32_t)contrib[l][toff[l][k] + j];
     }
   }
-  size_t need = 0;
-  for (int l = 0; l < L; ++l) need += align_up(rec[l].size() * 4, 256);
-  if (need > ctx->csr_bytes) {
-    if (ctx->d_csr) CK(cudaFree(ctx->d_csr));
-    ctx->d_csr = nullptr;
-    CK(cudaMalloc(&ctx->d_csr, need));
-    ctx->csr_bytes = need;
-  }
-  ctx->csr_tasks.assign(L, nullptr);
-  char* cur = ctx->d_csr;
-  for (int l = 0; l < L; ++l) {
-    ctx->csr_tasks[l] = reinterpret_cast<int4*>(cur);
-    CK(cudaMemcpyAsync(cur, rec[l].data(), rec[l].size() * 4, cudaMemcpyHostToDevice, st));
-    cur += align_up(rec[l].size() * 4, 256);
-  }
-  CK(cudaStreamSynchronize(st));
+  // kept on the host: each f item block carries its rows' records (build_grec)
+  ctx->h_tasks = std::move(rec);
+  (void)st;
   return HALO_OK;
 }
 
@@ -773,6 +763,12 @@ static void build_xrec(halo_ctx* ctx) {
       std::copy(m.begin() + w.begin, m.begin() + w.end, ctx->h_xmap.begin() + k * (size_t)R);
     }
   }
+  const size_t XB = 128 + 4 * (size_t)R;
+  ctx->h_xblk.assign(ctx->h_items_x.size() * XB, 0);
+  for (size_t k = 0; k < ctx->h_items_x.size(); ++k) {
+    memcpy(&ctx->h_xblk[k * XB], &ctx->h_xrec[k], sizeof(XRec));
+    memcpy(&ctx->h_xblk[k * XB + 128], &ctx->h_xmap[k * (size_t)R], 4 * (size_t)R);
+  }
 }
 
 static halo_status build_grec(halo_ctx* ctx) {
@@ -796,7 +792,7 @@ static halo_status build_grec(halo_ctx* ctx) {
     g.f = ctx->f[l];
     g.fll_own = ctx->fll_of(rk);
     if (w.kind == kItemGather) {
-      g.tasks = ctx->csr_tasks[l] + 2 * (size_t)w.begin;
+      g.tasks = nullptr;
       if (w.pulse != kHomeLevel) {
         const int p = w.pulse;
         const PulseDev& pd = ctx->h_pulses[l * P + p];
@@ -815,6 +811,14 @@ static halo_status build_grec(halo_ctx* ctx) {
         g.nslot[q] = (g.wrap_mask >> q & 1u) ? (uint32_t)((ctx->send_size[l * P + q] + R - 1) / R) : 0u;
     }
   }
+  const size_t FB = 128 + 32 * (size_t)R;
+  ctx->h_fblk.assign(ctx->h_items_f.size() * FB, 0);
+  for (size_t k = 0; k < ctx->h_items_f.size(); ++k) {
+    const Item& w = ctx->h_items_f[k];
+    memcpy(&ctx->h_fblk[k * FB], &ctx->h_grec[k], sizeof(GRec));
+    if (w.kind == kItemGather)
+      memcpy(&ctx->h_fblk[k * FB + 128], &ctx->h_tasks[w.lrank][8 * (size_t)w.begin], 32 * (size_t)(w.end - w.begin));
+  }
   return HALO_OK;
 }
 
@@ -824,9 +828,9 @@ static halo_status upload_plan(halo_ctx* ctx) {
   const size_t np = align_up(sizeof(PulseDev) * std::max(1, ctx->n_local * ctx->P), a);
   const size_t nx = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_x.size()), a);
   const size_t nf = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_f.size()), a);
-  const size_t nxr = align_up(sizeof(XRec) * std::max<size_t>(1, ctx->h_xrec.size()), a);
-  const size_t ngr = align_up(sizeof(GRec) * std::max<size_t>(1, ctx->h_grec.size()), a);
-  const size_t nxm = align_up(sizeof(int32_t) * std::max<size_t>(1, ctx->h_xmap.size()), a);
+  const size_t nxr = align_up(std::max<size_t>(1, ctx->h_xblk.size()), a);
+  const size_t ngr = align_up(std::max<size_t>(1, ctx->h_fblk.size()), a);
+  const size_t nxm = 0;
   const size_t need = nr + np + nx + nf + nxr + ngr + nxm;
   if (need > ctx->plan_bytes) {
     if (ctx->plan) CK(cudaFree(ctx->plan));
@@ -838,15 +842,12 @@ static halo_status upload_plan(halo_ctx* ctx) {
   ctx->d_pulses = reinterpret_cast<PulseDev*>(ctx->plan + nr);
   ctx->d_items_x = reinterpret_cast<Item*>(ctx->plan + nr + np);
   ctx->d_items_f = reinterpret_cast<Item*>(ctx->plan + nr + np + nx);
-  ctx->d_xrec = reinterpret_cast<XRec*>(ctx->plan + nr + np + nx + nf);
-  ctx->d_grec = reinterpret_cast<GRec*>(ctx->plan + nr + np + nx + nf + nxr);
-  ctx->d_xmap = reinterpret_cast<int32_t*>(ctx->plan + nr + np + nx + nf + nxr + ngr);
-  if (!ctx->h_xmap.empty())
-    CK(cudaMemcpy(ctx->d_xmap, ctx->h_xmap.data(), sizeof(int32_t) * ctx->h_xmap.size(), cudaMemcpyHostToDevice));
-  if (!ctx->h_xrec.empty())
-    CK(cudaMemcpy(ctx->d_xrec, ctx->h_xrec.data(), sizeof(XRec) * ctx->h_xrec.size(), cudaMemcpyHostToDevice));
-  if (!ctx->h_grec.empty())
-    CK(cudaMemcpy(ctx->d_grec, ctx->h_grec.data(), sizeof(GRec) * ctx->h_grec.size(), cudaMemcpyHostToDevice));
+  ctx->d_xblk = ctx->plan + nr + np + nx + nf;
+  ctx->d_fblk = ctx->plan + nr + np + nx + nf + nxr;
+  if (!ctx->h_xblk.empty())
+    CK(cudaMemcpy(ctx->d_xblk, ctx->h_xblk.data(), ctx->h_xblk.size(), cudaMemcpyHostToDevice));
+  if (!ctx->h_fblk.empty())
+    CK(cudaMemcpy(ctx->d_fblk, ctx->h_fblk.data(), ctx->h_fblk.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_ranks, ctx->h_ranks.data(), sizeof(RankDev) * ctx->n_local, cudaMemcpyHostToDevice));
   if (ctx->P)
     CK(cudaMemcpy(ctx->d_pulses, ctx->h_pulses.data(), sizeof(PulseDev) * ctx->n_local * ctx->P,
@@ -880,10 +881,9 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.debug = ctx->debug;
   P.fsp_slots = (uint32_t)ctx->fsp_slots;
   P.ll_stride = ctx->ll_stride;
-  P.xrec = ctx->d_xrec;
-  P.xmap = ctx->d_xmap;
+  P.xblk = ctx->d_xblk;
+  P.fblk = ctx->d_fblk;
   P.item_rows = ctx->item_rows;
-  P.grec = ctx->d_grec;
   return P;
 }
 
@@ -1200,7 +1200,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     if ((s = upload_plan(ctx)) != HALO_OK) return s;
     ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
     if (ctx->ll)
-      CK(launch_exchange_x_ll(X, W, grid_for(ctx->n_items_x, L, ctx->cap_x()), ctx->wide(), st));
+      CK(launch_exchange_x_ll(X, W, grid_for(ctx->n_items_x, L, ctx->cap_x()), ctx->wide(), nullptr, st));
     else
       CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
     CK(cudaStreamSynchronize(st));
@@ -1250,12 +1250,31 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   } else {
     ctx->h_xrec.clear();
     ctx->h_grec.clear();
+    ctx->h_xblk.clear();
+    ctx->h_fblk.clear();
     build_x_items(ctx, 0, P);
     build_f_items(ctx);
   }
   fill_rank_dev(ctx);
   if ((s = upload_plan(ctx)) != HALO_OK) return s;
   if (ctx->ce && (s = build_ce(ctx)) != HALO_OK) return s;
+  ctx->l2win = cudaAccessPolicyWindow{};
+  if ((ctx->cfg.flags & HALO_F_L2_PERSIST) && ctx->ll) {
+    // the item blocks (records, map slices, task records) are re-read every step
+    // and change only here: keep them in the persisting L2 carve-out
+    int dev = ctx->cfg.device, max_win = 0, max_persist = 0;
+    CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    const size_t bytes = std::min(ctx->plan_bytes, (size_t)std::min(max_win, max_persist));
+    size_t cur = 0;
+    CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    if (cur < bytes) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+    ctx->l2win.base_ptr = ctx->plan;
+    ctx->l2win.num_bytes = bytes;
+    ctx->l2win.hitRatio = 1.0f;
+    ctx->l2win.hitProp = cudaAccessPropertyPersisting;
+    ctx->l2win.missProp = cudaAccessPropertyStreaming;
+  }
   ctx->maps_ready = true;
   ctx->x_done = true;  // set_maps exchanged every pulse's coordinates
   return HALO_OK;
@@ -1320,7 +1339,7 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
   ctx->last_grid[0] = grid;
   if (ctx->ll)
-    CK(launch_exchange_x_ll(X, ctx->W, grid, ctx->wide(), (cudaStream_t)stream));
+    CK(launch_exchange_x_ll(X, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
   else
     CK(launch_exchange_x(X, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
@@ -1345,7 +1364,7 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   }
   ctx->last_grid[1] = grid;
   if (ctx->ll)
-    CK(launch_exchange_f_ll(F, ctx->W, grid, ctx->wide(), (cudaStream_t)stream));
+    CK(launch_exchange_f_ll(F, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
   else
     CK(launch_exchange_f(F, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
@@ -1452,11 +1471,12 @@ halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, int rel
   if (!ctx || peer_rank < 0 || peer_rank >= ctx->nranks || iters <= 0) return HALO_ERR_ARG;
   if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
   const int me = ctx->first_rank;
-  if (peer_rank >= ctx->first_rank && peer_rank < ctx->first_rank + ctx->n_local && peer_rank != me)
-    return fail(ctx, HALO_ERR_UNSUPPORTED, "ping-pong peer must live in another process");
+  if (peer_rank == me) return fail(ctx, HALO_ERR_ARG, "ping-pong peer must differ from local rank 0");
+  // both ranks on this GPU: one launch plays both sides (2 CTAs); else the
+  // initiator is the process that hosts the lower of the two ranks
+  const bool local = peer_rank >= ctx->first_rank && peer_rank < ctx->first_rank + ctx->n_local;
   CK(cudaSetDevice(ctx->cfg.device));
-  // the initiator is the process that hosts the lower of the two ranks
-  const bool initiator = me < peer_rank;
+  const bool initiator = local || me < peer_rank;
   if (ctx->d_rtt == nullptr || iters > 1 << 16) {
     if (ctx->d_rtt) CK(cudaFree(ctx->d_rtt));
     CK(cudaMalloc(&ctx->d_rtt, sizeof(uint64_t) * std::max(iters, 1 << 16)));
@@ -1465,7 +1485,7 @@ halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, int rel
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   uint64_t* own = &ctx->hdr_of(me)->ping;
   uint64_t* peer = &ctx->hdr_of(peer_rank)->ping;
-  CK(launch_pingpong(own, peer, iters, ctx->ping_base, initiator ? 1 : 0, relaxed ? 1 : 0, ctx->d_rtt,
+  CK(launch_pingpong(own, peer, iters, ctx->ping_base, local ? 2 : (initiator ? 1 : 0), relaxed ? 1 : 0, ctx->d_rtt,
                      (uint64_t)(ctx->cfg.timeout_s * 1e9), ctx->err_dev, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaStreamDestroy(st));

@@ -17,13 +17,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def run(lib, args, port):
+    lib, _, extra = lib.partition("+")
     env = dict(os.environ, HALO_LIB_PATH=os.path.join(ROOT, lib))
     if args.env:
         for kv in args.env.split(","):
             k, v = kv.split("=", 1)
             env[k] = v
     bench = [os.path.join(ROOT, "bench.py"), "--steps", str(args.steps), "--warmup", "20", "--config", args.config,
-             "--no-graph", "--no-cpu", "--no-nccl", "--no-floors", "--proto", args.proto]
+             "--no-graph", "--no-cpu", "--no-nccl", "--no-floors", "--proto", args.proto, *args.bench_args.split(), *[a for a in extra.split("+") if a]]
     if args.gpus > 1:
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr", "127.0.0.1", "--master-port", str(port), *bench, "--gpus", str(args.gpus)]
@@ -45,8 +46,10 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--proto", default="ll")
     ap.add_argument("--env", default="")
+    ap.add_argument("--bench-args", default="", help="extra bench.py arguments, e.g. '--l2-persist'")
     args = ap.parse_args()
     libs = [kv.split("=", 1) for kv in args.libs.split(",")]
+    # name=path or name=path+ARGS: '+' appends bench arguments for that variant only (e.g. new=lib.so+--l2-persist)
     res = {n: [] for n, _ in libs}
     port = 29600
     for _ in range(args.reps):
