@@ -253,6 +253,15 @@ HALO_API halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters
  * times its replay.  Synchronises. */
 HALO_API halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_per_launch);
 
+/* Launch floor of a kernel that wrote to (NVLink) peer memory: as
+ * halo_floor_launch, but `words` threads of each launch also store one 8-B word
+ * each into DD rank `peer_rank`'s LL receive area (words <= that area and <=
+ * grid threads).  The difference to halo_floor_launch is the completion cost of
+ * a kernel with remote writes.  One-sided: the peer's process must be idle (no
+ * exchange in flight); synchronises. */
+HALO_API halo_status halo_floor_launch_remote(halo_ctx* ctx, int peer_rank, int words, int iters, int graph,
+                                              double* us_per_launch);
+
 /* Bandwidth floor (SURVEY 8(d) floor ii): one-directional GB/s of `iters`
  * back-to-back transfers of `bytes` (multiple of 16, at most the LL receive
  * area of a rank's scratch) from this process's local rank 0 into DD rank

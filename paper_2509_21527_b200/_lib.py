@@ -28,7 +28,7 @@ EXPORTS = [
     "halo_init", "halo_query_config", "halo_local_ranks", "halo_pulse_order", "halo_scratch_bytes", "halo_register_buffers",
     "halo_ipc_export", "halo_ipc_import", "halo_set_maps", "halo_set_maps_explicit", "halo_get_layout",
     "halo_get_map", "halo_exchange_x", "halo_exchange_f", "halo_step_host", "halo_pack_x_pulse",
-    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_bandwidth", "halo_sync", "halo_strerror",
+    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_launch_remote", "halo_floor_bandwidth", "halo_sync", "halo_strerror",
     "halo_last_error", "halo_destroy",
 ]
 
@@ -76,6 +76,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_get_notify_counts": ([P, c_int, POINTER(c_uint), c_int], c_int),
         "halo_floor_pingpong": ([P, c_int, c_int, c_int, POINTER(c_double)], c_int),
         "halo_floor_launch": ([P, c_int, c_int, POINTER(c_double)], c_int),
+        "halo_floor_launch_remote": ([P, c_int, c_int, c_int, c_int, POINTER(c_double)], c_int),
         "halo_floor_bandwidth": ([P, c_int, c_size_t, c_int, c_int, POINTER(c_double)], c_int),
         "halo_sync": ([P], c_int),
         "halo_strerror": ([c_int], c_char_p),

@@ -80,7 +80,8 @@ enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };
 
 // HALO_DEBUG bits: protocol mutations for the dependency-safety tests (G3);
 // never set in production.
-enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u, kCountNotify = 64u };
+enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u, kCountNotify = 64u, kFenceAfterPeerStores = 128u,
+                   kLocalSink = 256u };  // timing experiment: peer stores go to own memory, receivers do not wait
 
 struct RankDev {
   float* x;                 // own x (capacity rows)

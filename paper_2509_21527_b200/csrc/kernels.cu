@@ -494,9 +494,14 @@ cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, c
 }
 
 // Empty kernel with the exchange kernels' PDL prologue (launch floor).
-__global__ void k_empty() {
+// remote != nullptr: threads [0, nwords) of the grid also store one 8-B word
+// each there (a peer's scratch): the launch floor of a kernel that wrote to
+// NVLink peer memory.
+__global__ void k_empty(uint64_t* remote, uint32_t nwords) {
   pdl_launch_dependents();
   pdl_wait();
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (remote != nullptr && g < nwords) st_relaxed_sys(remote + g, 0ull);
 }
 
 // ------------------------------------------------------------- host launchers
@@ -555,8 +560,8 @@ cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** ar
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-cudaError_t launch_empty(int grid, cudaStream_t st) {
-  void* args[] = {nullptr};
+cudaError_t launch_empty(int grid, cudaStream_t st, uint64_t* remote, uint32_t nwords) {
+  void* args[] = {(void*)&remote, (void*)&nwords};
   return launch_coop_kernel_ex((const void*)k_empty, grid, kThreads, args, st, true, 0, nullptr);
 }
 

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
         for (int k = 0; k < kU; ++k) {
           const uint32_t u = base + k * B;
           if (u >= n) continue;
-          if ((uint32_t)(w[k] >> 32) != tag)
+          if ((uint32_t)(w[k] >> 32) != tag && !(P.debug & kLocalSink))
             w[k] = ll_spin(r.ll + u, tag, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse), P.poll_ns);
           r.xdst[u] = __uint_as_float((uint32_t)w[k]);
         }
@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
           if (u >= n) continue;
           const int c = (int)(u % W);
           const float o = (r.has_shift && c < 3) ? __fadd_rn(v[k], r.shift[c]) : v[k];
-          st_relaxed_sys(r.ll + u, ll_pack(o, tag));
+          uint64_t* dst = (P.debug & kLocalSink) ? const_cast<uint64_t*>(r.xll_own) + (size_t)r.pulse * P.ll_stride + u
+                                                 : r.ll + u;
+          st_relaxed_sys(dst, ll_pack(o, tag));
         }
       }
     } else {
@@ -162,15 +164,19 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
         for (int k = 0; k < kU; ++k) {
           const uint32_t u = base + k * B;
           if (u >= n) continue;
-          if (src[k] != nullptr && (uint32_t)(w[k] >> 32) != tag)
+          if (src[k] != nullptr && (uint32_t)(w[k] >> 32) != tag && !(P.debug & kLocalSink))
             w[k] = ll_spin(src[k], tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, r.pulse), P.poll_ns);
           const int c = (int)(u % W);
           float v = __uint_as_float((uint32_t)w[k]);
           if (r.has_shift && c < 3) v = __fadd_rn(v, r.shift[c]);
-          st_relaxed_sys(r.ll + u, ll_pack(v, tag));
+          uint64_t* dst = (P.debug & kLocalSink) ? const_cast<uint64_t*>(r.xll_own) + (size_t)r.pulse * P.ll_stride + u
+                                                 : r.ll + u;
+          st_relaxed_sys(dst, ll_pack(v, tag));
         }
       }
     }
+    // experiment (HALO_DEBUG=128): drain this thread's peer stores inside the item
+    if ((P.debug & kFenceAfterPeerStores) && r.kind != kItemXRecv) fence_sys();
     if (trace) {
       const int slot = (it - (int)blockIdx.x) / (int)gridDim.x;
       if (slot < 2) {
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
     const uint32_t n = g.n_units;
     const bool push = g.level != kHomeLevel;
     // this item also sums what it pushes when the receiving x-sender shifted (R13)
-    const bool part = (P.fshift != nullptr) && (g.part != nullptr);
+    const bool part = (P.fshift != nullptr) && (g.part != nullptr) && !(P.debug & kLocalSink);
     // stride = a multiple of W: every thread keeps one component c
     const uint32_t S = (blockDim.x / W) * W;
     const int c = (int)(threadIdx.x % W);
@@ -384,18 +390,22 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
               const int q = (int)(cc[j] >> 24);
               const uint64_t* src = g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c;
               uint64_t wj = j < kPre ? w[k][j < kPre ? j : 0] : ld_relaxed_sys(src);
-              if ((uint32_t)(wj >> 32) != tag && !(P.debug & kMutateFNoWait))
+              if ((uint32_t)(wj >> 32) != tag && !(P.debug & (kMutateFNoWait | kLocalSink)))
                 wj = ll_spin(src, tag, P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
               const float val = __uint_as_float((uint32_t)wj);
               vv = P.accumulate ? __fadd_rn(vv, val) : val;
             }
           }
           g.f[(size_t)t * W + c] = vv;
-          if (push) st_relaxed_sys(g.push + (size_t)t * W + c, ll_pack(vv, tag));
+          if (push)
+            st_relaxed_sys((P.debug & kLocalSink) ? const_cast<uint64_t*>(g.fll_own) + (size_t)t * W + c
+                                                  : g.push + (size_t)t * W + c,
+                           ll_pack(vv, tag));
           if (part) acc += (double)vv;
         }
       }
     }
+    if ((P.debug & kFenceAfterPeerStores) && push) fence_sys();  // experiment (HALO_DEBUG=128)
     if (part) {  // fixed-tree CTA sum of the pushed forces per component -> the x-sender's slot
 #pragma unroll
       for (int j = 0; j < 3; ++j) s_fs[j][threadIdx.x] = (threadIdx.x < S && c == j) ? acc : 0.0;

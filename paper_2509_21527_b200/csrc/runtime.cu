@@ -34,7 +34,7 @@ cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool w
 cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
                                  cudaStream_t st);
 cudaError_t max_coresident_ll(int layout, bool wide, int* x_blocks, int* f_blocks);
-cudaError_t launch_empty(int grid, cudaStream_t st);
+cudaError_t launch_empty(int grid, cudaStream_t st, uint64_t* remote, uint32_t nwords);
 cudaError_t launch_ce_pack(int layout, const CeEnt* ents, int n_local, int max_rows, cudaStream_t st);
 cudaError_t launch_ce_unpack(int layout, const CeEnt* ents, int n_local, int max_rows, double* fshift, int accumulate,
                              cudaStream_t st);
@@ -1504,7 +1504,8 @@ halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters, int rel
   return HALO_OK;
 }
 
-halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_per_launch) {
+static halo_status floor_launch_impl(halo_ctx* ctx, int iters, int graph, uint64_t* remote, uint32_t nwords,
+                                     double* us_per_launch) {
   if (!ctx || iters <= 0 || !us_per_launch) return HALO_ERR_ARG;
   CK(cudaSetDevice(ctx->cfg.device));
   cudaStream_t st;
@@ -1515,9 +1516,9 @@ halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_pe
   const int grid = std::max(1, std::min(ctx->max_x, 512));
   float ms = 0.f;
   if (!graph) {
-    for (int i = 0; i < 10; ++i) CK(launch_empty(grid, st));
+    for (int i = 0; i < 10; ++i) CK(launch_empty(grid, st, remote, nwords));
     CK(cudaEventRecord(e0, st));
-    for (int i = 0; i < iters; ++i) CK(launch_empty(grid, st));
+    for (int i = 0; i < iters; ++i) CK(launch_empty(grid, st, remote, nwords));
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -1525,7 +1526,7 @@ halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_pe
     cudaGraph_t g;
     cudaGraphExec_t ge;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < iters; ++i) CK(launch_empty(grid, st));
+    for (int i = 0; i < iters; ++i) CK(launch_empty(grid, st, remote, nwords));
     CK(cudaStreamEndCapture(st, &g));
     CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphLaunch(ge, st));
@@ -1543,6 +1544,21 @@ halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_pe
   CK(cudaEventDestroy(e1));
   CK(cudaStreamDestroy(st));
   return HALO_OK;
+}
+
+halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_per_launch) {
+  return floor_launch_impl(ctx, iters, graph, nullptr, 0, us_per_launch);
+}
+
+halo_status halo_floor_launch_remote(halo_ctx* ctx, int peer_rank, int words, int iters, int graph,
+                                     double* us_per_launch) {
+  if (!ctx || peer_rank < 0 || peer_rank >= ctx->nranks || words < 0) return HALO_ERR_ARG;
+  if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
+  const int grid = std::max(1, std::min(ctx->max_x, 512));
+  const size_t area = 2 * (size_t)ctx->P * ctx->ll_stride;  // u64 words of the peer's LL receive areas
+  if ((size_t)words > std::min(area, (size_t)grid * kThreads)) return fail(ctx, HALO_ERR_ARG, "too many words");
+  // the peer's LL receive areas: the caller keeps the peer idle (no exchange in flight)
+  return floor_launch_impl(ctx, iters, graph, ctx->xll_of(peer_rank), (uint32_t)words, us_per_launch);
 }
 
 halo_status halo_floor_bandwidth(halo_ctx* ctx, int peer_rank, size_t bytes, int mode, int iters, double* gbs) {

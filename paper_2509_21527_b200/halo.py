@@ -203,6 +203,12 @@ class Halo:
         self._ck(self.lib.halo_floor_launch(self.h, int(iters), int(bool(graph)), ctypes.byref(v)))
         return v.value
 
+    def floor_launch_remote(self, peer_rank, words=1, iters=1000, graph=False) -> float:
+        v = c_double()
+        self._ck(self.lib.halo_floor_launch_remote(self.h, int(peer_rank), int(words), int(iters), int(bool(graph)),
+                                                   ctypes.byref(v)))
+        return v.value
+
     def floor_bandwidth(self, peer_rank, nbytes, mode=0, iters=20) -> float:
         """GB/s of SM peer stores (mode 0) or copy-engine copies (mode 1) into peer_rank's scratch."""
         v = c_double()

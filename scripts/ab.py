@@ -18,7 +18,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def run(lib, args, port):
     lib, _, extra = lib.partition("+")
+    lib, *kvs = lib.split("@")  # path@KEY=VAL@KEY2=VAL2: environment of this variant only
     env = dict(os.environ, HALO_LIB_PATH=os.path.join(ROOT, lib))
+    for kv in kvs:
+        k, v = kv.split("=", 1)
+        env[k] = v
     if args.env:
         for kv in args.env.split(","):
             k, v = kv.split("=", 1)
@@ -49,7 +53,8 @@ def main():
     ap.add_argument("--bench-args", default="", help="extra bench.py arguments, e.g. '--l2-persist'")
     args = ap.parse_args()
     libs = [kv.split("=", 1) for kv in args.libs.split(",")]
-    # name=path or name=path+ARGS: '+' appends bench arguments for that variant only (e.g. new=lib.so+--l2-persist)
+    # name=path[@K=V...][+ARG...]: per-variant environment and bench arguments
+    # (e.g. fence=lib.so@HALO_DEBUG=128, l2=lib.so+--l2-persist)
     res = {n: [] for n, _ in libs}
     port = 29600
     for _ in range(args.reps):
