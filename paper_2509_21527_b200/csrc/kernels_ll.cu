@@ -201,40 +201,28 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Deterministic CTA reduction of 9 doubles per thread: a fixed pairwise tree in
-// shared memory (no warp shuffles: a full-mask SHFL after the divergent polling
-// loop made lanes wait for their warp's slowest poll before pushing, which cost
-// ~10 us per level at C3).  Thread j < 9 returns the total of output j.
-__device__ __forceinline__ double cta_tree9(double (*s_red)[kThreads], int j_out) {
-  for (int h = kThreads / 2; h > 0; h >>= 1) {
-    __syncthreads();
-    if ((int)threadIdx.x < h)
-#pragma unroll
-      for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] += s_red[j][threadIdx.x + h];
+// Deterministic CTA reduction of N outputs held per thread in s_red[j][tid]:
+// output j is summed by warp (j mod warps), each lane over a fixed strided slice
+// of the threads, then a fixed xor-shuffle tree; threads j < N return output j.
+// Every thread has passed the __syncthreads before any shuffle, so no lane
+// waits for another's polling loop (a full-mask SHFL right after the divergent
+// polling loop had cost ~10 us per level at C3); 2 barriers instead of the 9 of
+// a pairwise shared-memory tree.
+template <int N>
+__device__ __noinline__ double cta_reduce(double (*s_red)[kThreads], int j_out) {
+  __shared__ double s_out[9];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+  for (int j = warp; j < N; j += nw) {
+    double v = 0.0;
+    for (int t = lane; t < kThreads; t += 32) v += s_red[j][t];
+    v = warp_sum_d(v);
+    if (lane == 0) s_out[j] = v;
   }
   __syncthreads();
-  const double tot = (j_out < 9) ? s_red[j_out][0] : 0.0;
+  const double tot = (j_out < N) ? s_out[j_out] : 0.0;
   __syncthreads();
   return tot;
-}
-
-__device__ __forceinline__ double cta_tree3(double (*s_red)[kThreads], int j_out) {
-  for (int h = kThreads / 2; h > 0; h >>= 1) {
-    __syncthreads();
-    if ((int)threadIdx.x < h)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) s_red[j][threadIdx.x] += s_red[j][threadIdx.x + h];
-  }
-  __syncthreads();
-  const double tot = (j_out < 3) ? s_red[j_out][0] : 0.0;
-  __syncthreads();
-  return tot;
-}
-
-__device__ __forceinline__ double cta_sum9(const double* v, double (*s_red)[kThreads], int j_out) {
-#pragma unroll
-  for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] = v[j];
-  return cta_tree9(s_red, j_out);
 }
 
 // Combine item of one rank (R13): the pushers of its wrapping pulses summed,
@@ -282,7 +270,7 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
       s_red[dc[k]][threadIdx.x] += __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
     }
   }
-  const double tot = cta_tree9(s_red, threadIdx.x);
+  const double tot = cta_reduce<9>(s_red, threadIdx.x);
   if (threadIdx.x < 9) P.fshift[9 * g.lrank + threadIdx.x] = fs_old + tot;
 }
 
@@ -409,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
     if (part) {  // fixed-tree CTA sum of the pushed forces per component -> the x-sender's slot
 #pragma unroll
       for (int j = 0; j < 3; ++j) s_fs[j][threadIdx.x] = (threadIdx.x < S && c == j) ? acc : 0.0;
-      const double tot = cta_tree3(s_fs, threadIdx.x);
+      const double tot = cta_reduce<3>(s_fs, threadIdx.x);
       if (threadIdx.x < 3) {
         st_relaxed_sys(g.part + 2 * threadIdx.x, ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));
         st_relaxed_sys(g.part + 2 * threadIdx.x + 1, ll_pack(__uint_as_float((uint32_t)__double2loint(tot)), tag));

@@ -340,3 +340,45 @@ def test_notification_minimality_paper_protocol(name, monkeypatch):
             assert dx[l, p] == K * (lay["send_size"][p] > 0), (l, p, dx[l, p])
             assert df[l, p] == K * (lay["recv_size"][p] > 0), (l, p, df[l, p])
     sess.destroy()
+
+
+@pytest.mark.parametrize("proto", PROTOS)
+def test_parity_under_concurrent_compute(proto):
+    """Alg. 2 schedule: the exchanges run on a high-priority stream while
+    a GEMM that fills every SM runs on another stream; results stay bit-exact and the
+    co-resident grids make progress."""
+    case = Case("C3", seed=2, force_kind="int")
+    sess = session_for(case, flags=proto)
+    run_gpu_case(case, sess)  # set_maps + one checked step
+    s_nl = torch.cuda.Stream(priority=-1)
+    s_loc = torch.cuda.Stream()
+    A = torch.randn(4096, 4096, device=sess.device, dtype=torch.bfloat16)
+    for _ in range(3):
+        for l in range(sess.n_local):
+            st = case.states[l]
+            sess.x[l][st.n_home: st.x.shape[0]] = float("nan")
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s_loc):
+            for _ in range(4):
+                torch.mm(A, A)
+        sess.exchange_x(stream=s_nl)
+        with torch.cuda.stream(s_loc):
+            torch.mm(A, A)
+        torch.cuda.synchronize()
+        for l in range(sess.n_local):
+            st = case.states[l]
+            np.testing.assert_array_equal(bits(sess.x[l][: st.x.shape[0]].cpu().numpy()), bits(st.x))
+            sess.f[l][: case.F[l].shape[0]] = torch.from_numpy(case.F[l]).to(sess.device)
+        fshift = torch.zeros(sess.n_local, 3, 3, dtype=torch.float64, device=sess.device)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s_loc):
+            for _ in range(4):
+                torch.mm(A, A)
+        sess.exchange_f(fshift=fshift, stream=s_nl)
+        torch.cuda.synchronize()
+        fs = fshift.cpu().numpy()
+        for l in range(sess.n_local):
+            n = case.F[l].shape[0]
+            np.testing.assert_array_equal(bits(sess.f[l][:n].cpu().numpy()), bits(case.Fo[l]))
+            assert np.all(np.abs(fs[l] - case.fshift[l]) <= 1e-10 * case.fabs_total)
+    sess.destroy()
