@@ -30,11 +30,22 @@ __device__ __forceinline__ uint64_t ll_pack(float v, uint32_t tag) {
 }
 
 // Slow path: poll one LL unit until it carries `tag`; bounded like every wait.
+// Tight polling for the first kTight polls (the latency regime: data arrives
+// within a few us), then exponential __nanosleep backoff up to ~2 us per poll:
+// a wait that lasts because the peer's grid is not yet resident (it shares the
+// SMs with a concurrent compute kernel, Alg. 2) must not steal that kernel's
+// issue slots and L2 bandwidth.  sleep_ns > 0 (HALO_POLL_NS) forces a fixed sleep.
 __device__ __forceinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
                                          int code, uint32_t sleep_ns) {
+  constexpr uint32_t kTight = 16;
   uint64_t t0 = 0;
   for (uint32_t it = 1;; ++it) {
-    if (sleep_ns) __nanosleep(sleep_ns);  // back off: thousands of pollers must not starve the writers
+    if (sleep_ns) {
+      __nanosleep(sleep_ns);
+    } else if (it > kTight) {
+      const uint32_t sh = min((it - kTight) >> 3, 4u);
+      __nanosleep(128u << sh);
+    }
     const uint64_t v = ld_relaxed_sys(u);
     if ((uint32_t)(v >> 32) == tag) return v;
     if ((it & 1023u) == 0) {

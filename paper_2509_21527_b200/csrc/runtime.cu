@@ -157,9 +157,10 @@ struct halo_ctx {
   cudaAccessPolicyWindow l2win{};    // HALO_F_L2_PERSIST: the static plan (item blocks) persists in L2
   int max_x = 0, max_f = 0;         // co-resident CTAs of the exchange kernels (LL: narrow variants)
   int max_x_w = 0, max_f_w = 0;     // LL: batched variants for large work items
+  int grid_cap = 0;                 // HALO_CTAS_PER_SM x SMs (0 = occupancy limit only)
   bool wide() const { return ll && item_rows >= 256; }
-  int cap_x() const { return wide() ? max_x_w : max_x; }
-  int cap_f() const { return wide() ? max_f_w : max_f; }
+  int cap_x() const { const int c = wide() ? max_x_w : max_x; return grid_cap ? std::min(c, grid_cap) : c; }
+  int cap_f() const { const int c = wide() ? max_f_w : max_f; return grid_cap ? std::min(c, grid_cap) : c; }
   int last_grid[2] = {0, 0};
   int item_rows = 64;
   bool item_rows_fixed = false;     // HALO_ITEM_ROWS given: no adaptive choice
@@ -347,6 +348,14 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     e = ctx->ll ? max_coresident_ll(cfg->layout, false, &ctx->max_x, &ctx->max_f)
                 : max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
   if (e == cudaSuccess && ctx->ll) e = max_coresident_ll(cfg->layout, true, &ctx->max_x_w, &ctx->max_f_w);
+  if (e == cudaSuccess) {
+    // HALO_CTAS_PER_SM: cap the exchange grids (fewer, longer-lived CTAs; leaves SM
+    // slots to a concurrently running compute kernel, Alg. 2)
+    int sms = 0;
+    if (const char* v = getenv("HALO_CTAS_PER_SM"))
+      if (atoi(v) > 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess)
+        ctx->grid_cap = atoi(v) * sms;
+  }
   if (e != cudaSuccess) {
     // keep ctx to carry the message? The ABI returns NULL on error; print once.
     fprintf(stderr, "halo_init: %s\n", cudaGetErrorString(e));

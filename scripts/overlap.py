@@ -7,10 +7,11 @@ The GPU-resident time-step skeleton of Alg. 2 with synthetic non-bonded work:
     local stream  : Local NB (synthetic GEMM, ns_per_atom x home atoms)
     non-local (high priority): exchange_x -> Non-local NB (ns_per_atom x halo atoms) -> exchange_f
 
-The synthetic NB kernels are bf16 cuBLAS GEMMs sized (calibrated once) to take
+The synthetic NB kernels are batched bf16 GEMMs of 128^3 tiles (one short CTA
+per tile, like the NB kernel's pair-list chunks), calibrated to take
 ``ns_per_atom`` (default 1.85 ns, the paper's 1.7-2.0 ns/atom) times the
-atoms: a load that occupies every SM, so the halo kernels run under SM
-contention.  No L2 flush (steady state: the GEMMs evict L2 anyway).
+atoms: they fill every SM, so the halo kernels run under SM contention and
+get slots as tiles retire (high-priority stream).  No L2 flush (steady state: the GEMMs evict L2 anyway).
 
 Reports the paper's device-side metrics, max over ranks:
   local      Local work: start -> end of the local NB kernel
@@ -39,34 +40,39 @@ sys.path.insert(0, ROOT)
 PROTOS = {"ll": 0, "paper": 1 << 4, "ce": 1 << 5}
 
 
-def calibrate_gemm(dev, target_us):
-    """Square bf16 GEMM size whose duration is ~target_us (>= 64)."""
-    if target_us <= 0:
-        return 0
-    sizes = [256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144, 8192]
-    best, times = 0, {}
-    for n in sizes:
-        a = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
-        b = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
-        for _ in range(3):
-            torch.mm(a, b)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(10):
-            torch.mm(a, b)
-        e1.record()
-        torch.cuda.synchronize()
-        times[n] = e0.elapsed_time(e1) * 1e3 / 10
-        if times[n] >= target_us:
-            break
-    # interpolate on n^3
-    ns = sorted(times)
-    for lo, hi in zip(ns, ns[1:]):
-        if times[lo] <= target_us <= times[hi]:
-            f = (target_us - times[lo]) / max(times[hi] - times[lo], 1e-9)
-            n3 = lo ** 3 + f * (hi ** 3 - lo ** 3)
-            return max(64, int(round(n3 ** (1 / 3) / 64)) * 64)
-    return ns[-1] if target_us > times[ns[-1]] else ns[0]
+class SyntheticNB:
+    """Synthetic non-bonded kernel: a batched bf16 GEMM of 128x128x128 tiles — one
+    short-lived CTA per tile, like the NB kernel's one CTA per pair-list chunk, so
+    a high-priority halo kernel gets SM slots as tiles retire.  The batch count is
+    calibrated once so the launch takes ~target_us."""
+
+    def __init__(self, dev, target_us):
+        self.t = torch.randn(1, 128, 128, device=dev, dtype=torch.bfloat16)
+        self.n = 0
+        if target_us <= 0:
+            return
+        nb, per = 256, None
+        for _ in range(12):
+            a = self.t.expand(nb, 128, 128)
+            for _ in range(3):
+                torch.bmm(a, a)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                torch.bmm(a, a)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / 5
+            per = us / nb
+            if us >= 0.5 * target_us:
+                break
+            nb *= 4
+        self.n = max(1, int(round(target_us / per)))
+        self.a = self.t.expand(self.n, 128, 128).contiguous()
+
+    def __call__(self):
+        if self.n:
+            torch.bmm(self.a, self.a)
 
 
 def main():
@@ -112,11 +118,8 @@ def main():
         lay = [sess.layout_of(l) for l in range(nl_ranks)]
         n_halo = sum(l_["n_total"] - l_["n_home"] for l_ in lay)
         if sizes is None:  # calibrate once (same for every protocol)
-            sizes = (calibrate_gemm(dev, args.ns_per_atom * n_home / 1e3),
-                     calibrate_gemm(dev, args.ns_per_atom * n_halo / 1e3))
-        nloc, nnl = sizes
-        A = torch.randn(max(nloc, 64), max(nloc, 64), device=dev, dtype=torch.bfloat16)
-        B = torch.randn(max(nnl, 64), max(nnl, 64), device=dev, dtype=torch.bfloat16)
+            sizes = (SyntheticNB(dev, args.ns_per_atom * n_home / 1e3), SyntheticNB(dev, args.ns_per_atom * n_halo / 1e3))
+        nb_loc, nb_nl = sizes
         F0 = torch.zeros_like(sess.f_all)
         for l in range(nl_ranks):
             n = lay[l]["n_total"]
@@ -133,8 +136,7 @@ def main():
             s_nl.wait_event(ev["start"][k])
             with torch.cuda.stream(s_loc):
                 ev["l0"][k].record(s_loc)
-                if nloc:
-                    torch.mm(A, A)
+                nb_loc()
                 ev["l1"][k].record(s_loc)
             with torch.cuda.stream(s_nl):
                 ev["n0"][k].record(s_nl)
@@ -143,8 +145,7 @@ def main():
                         sched.exchange_x(stream=s_nl)
                     else:
                         sess.exchange_x(stream=s_nl)
-                if nnl:
-                    torch.mm(B, B)
+                nb_nl()
                 if exchange:
                     if sched is not None:
                         sched.exchange_f(fshift, stream=s_nl)
@@ -176,8 +177,62 @@ def main():
             out.update({key + "local_us": round(mx(loc), 2), key + "nonlocal_us": round(mx(non), 2),
                         key + "nonoverlap_us": round(mx(nov), 2), key + "step_us": round(mx(stp), 2)})
         out["exchange_cost_us"] = round(out["step_us"] - out["compute_only_step_us"], 2)
+        # CUDA-graph mode (the step is graph-capturable): G steps captured once
+        # (fork/join with plain events), replayed; time per step from events around the replay
+        if sched is None:
+            G = 20
+            fork = [torch.cuda.Event() for _ in range(G)]
+            jl = [torch.cuda.Event() for _ in range(G)]
+            jn = [torch.cuda.Event() for _ in range(G)]
+
+            s_cap = torch.cuda.Stream(device=dev)  # the legacy default stream cannot be captured
+
+            def step_g(k, exchange):
+                fork[k].record(s_cap)
+                s_loc.wait_event(fork[k])
+                s_nl.wait_event(fork[k])
+                with torch.cuda.stream(s_loc):
+                    nb_loc()
+                    jl[k].record(s_loc)
+                with torch.cuda.stream(s_nl):
+                    if exchange:
+                        sess.exchange_x(stream=s_nl)
+                    nb_nl()
+                    if exchange:
+                        sess.exchange_f(fshift=fshift, stream=s_nl)
+                    jn[k].record(s_nl)
+                s_cap.wait_event(jl[k])
+                s_cap.wait_event(jn[k])
+                with torch.cuda.stream(s_cap):
+                    sess.f_all.copy_(F0)
+
+            for exchange in (True, False):
+                torch.cuda.synchronize()
+                bench.barrier()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s_cap):
+                    for k in range(G):
+                        step_g(k, exchange)
+                torch.cuda.synchronize()
+                bench.barrier()
+                for _ in range(3):
+                    g.replay()
+                torch.cuda.synchronize()
+                bench.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                R = max(1, args.steps // G)
+                e0.record()
+                for _ in range(R):
+                    g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                bench.barrier()
+                key = "graph_step_us" if exchange else "graph_compute_only_step_us"
+                out[key] = round(mx(e0.elapsed_time(e1) * 1e3 / (R * G)), 2)
+                del g
+            out["graph_exchange_cost_us"] = round(out["graph_step_us"] - out["graph_compute_only_step_us"], 2)
         res = {"config": c.name, "gpus": world, "proto": proto, "ns_per_atom": args.ns_per_atom,
-               "home_atoms_per_gpu": n_home, "halo_atoms_per_gpu": n_halo, "gemm_local": nloc, "gemm_nonlocal": nnl,
+               "home_atoms_per_gpu": n_home, "halo_atoms_per_gpu": n_halo, "nb_tiles_local": nb_loc.n, "nb_tiles_nonlocal": nb_nl.n,
                **out}
         results.append(res)
         sess.destroy()
