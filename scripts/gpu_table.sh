@@ -28,3 +28,11 @@ run C4-2D 4 ll
 run C5 4 ll
 run C3 4 ce
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/t_reference_C3.json 2> gpurun_out/t_reference_C3.err
+# overlap (f1): Alg. 2 skeleton with synthetic NB
+timeout 900 python scripts/overlap.py --config C3 > gpurun_out/t_overlap_C3_n1.txt 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29530 scripts/overlap.py --config C1 > gpurun_out/t_overlap_C1_n2.txt 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 scripts/overlap.py --config C3 > gpurun_out/t_overlap_C3_n2.txt 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 scripts/overlap.py --config C4-1D > gpurun_out/t_overlap_C41D_n2.txt 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 scripts/overlap.py --config C2 > gpurun_out/t_overlap_C2_n4.txt 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29534 scripts/overlap.py --config C4-2D > gpurun_out/t_overlap_C42D_n4.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_multiproc.py -x -q > gpurun_out/t_pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/t_pytest_mp.log

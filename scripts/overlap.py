@@ -49,6 +49,7 @@ class SyntheticNB:
     def __init__(self, dev, target_us):
         self.t = torch.randn(1, 128, 128, device=dev, dtype=torch.bfloat16)
         self.n = 0
+        self.us = 0.0
         if target_us <= 0:
             return
         nb, per = 256, None
@@ -68,7 +69,23 @@ class SyntheticNB:
                 break
             nb *= 4
         self.n = max(1, int(round(target_us / per)))
+        for _ in range(2):  # refine at the final size (per-tile time depends on occupancy)
+            self.a = self.t.expand(self.n, 128, 128).contiguous()
+            us = self.time()
+            self.n = max(1, int(round(self.n * target_us / max(us, 1e-3))))
         self.a = self.t.expand(self.n, 128, 128).contiguous()
+        self.us = self.time()
+
+    def time(self):
+        for _ in range(3):
+            torch.bmm(self.a, self.a)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            torch.bmm(self.a, self.a)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / 5
 
     def __call__(self):
         if self.n:
@@ -233,6 +250,7 @@ def main():
             out["graph_exchange_cost_us"] = round(out["graph_step_us"] - out["graph_compute_only_step_us"], 2)
         res = {"config": c.name, "gpus": world, "proto": proto, "ns_per_atom": args.ns_per_atom,
                "home_atoms_per_gpu": n_home, "halo_atoms_per_gpu": n_halo, "nb_tiles_local": nb_loc.n, "nb_tiles_nonlocal": nb_nl.n,
+               "nb_local_alone_us": round(nb_loc.us, 2), "nb_nonlocal_alone_us": round(nb_nl.us, 2),
                **out}
         results.append(res)
         sess.destroy()
