@@ -107,14 +107,17 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
     const uint32_t n = r.n_units;
     const uint32_t B = blockDim.x;
     if (r.kind == kItemXRecv) {
-      // this rank's halo rows of one pulse: LL units -> x rows
-      for (uint32_t base = threadIdx.x; base < n; base += kU * B) {
-        uint64_t w[kU];
+      // this rank's halo rows of one pulse: LL units -> x rows.  Receive items are
+      // larger than send items (HALO_RECV_MULT x rows, runtime.cu) and always take
+      // 4 units per thread per batch: the polls of a batch are in flight together.
+      constexpr int kR = 4;
+      for (uint32_t base = threadIdx.x; base < n; base += kR * B) {
+        uint64_t w[kR];
 #pragma unroll
-        for (int k = 0; k < kU; ++k)
+        for (int k = 0; k < kR; ++k)
           if (base + k * B < n) w[k] = ld_relaxed_sys(r.ll + base + k * B);
 #pragma unroll
-        for (int k = 0; k < kU; ++k) {
+        for (int k = 0; k < kR; ++k) {
           const uint32_t u = base + k * B;
           if (u >= n) continue;
           if ((uint32_t)(w[k] >> 32) != tag && !(P.debug & kLocalSink))

@@ -166,6 +166,7 @@ struct halo_ctx {
   bool item_rows_fixed = false;     // HALO_ITEM_ROWS given: no adaptive choice
   uint32_t poll_ns = 0;
   uint32_t debug = 0;
+  int recv_mult = 4;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT)
 
   int cell(int r, int d) const {
     const int* g = cfg.grid;
@@ -331,6 +332,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     ctx->item_rows_fixed = true;
   }
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = (uint32_t)std::max(0, atoi(e));
+  if (const char* e = getenv("HALO_RECV_MULT")) ctx->recv_mult = std::min(16, std::max(1, atoi(e)));
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
   cudaError_t e = cudaSetDevice(cfg->device);
@@ -638,7 +640,8 @@ static void build_x_items_ll(halo_ctx* ctx, int p_lo, int p_hi) {
       add_items(v, l, p, kItemXDep, ctx->n_indep[i], ctx->send_size[i], R);
     }
   for (int p = p_lo; p < p_hi; ++p)
-    for (int l = 0; l < ctx->n_local; ++l) add_items(v, l, p, kItemXRecv, 0, ctx->recv_size[l * ctx->P + p], R);
+    for (int l = 0; l < ctx->n_local; ++l)
+      add_items(v, l, p, kItemXRecv, 0, ctx->recv_size[l * ctx->P + p], std::min(kMaxItemRows, ctx->recv_mult * R));
 }
 
 // Force gather plan of every local rank (LL protocol), built on the host at the

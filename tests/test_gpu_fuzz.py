@@ -1,0 +1,43 @@
+"""Fuzz parity (-m gpu): random grids, boxes, cutoffs, 1-2 pulses per dim, float3 /
+float4, uniform or clustered atoms (ranks with no home atoms, empty maps), all
+three transports; every case bit-exact vs the oracle (maps, layout, halo x, f),
+fshift within the fp64 bound."""
+import numpy as np
+import pytest
+
+from oracle import decompose, force_halo
+from synth import forces_int, forces_normal
+from synth.water import charges
+from tests.fuzz_cases import random_case
+from tests.parity_common import run_gpu_case
+
+pytestmark = pytest.mark.gpu
+
+
+class FuzzCase:
+    def __init__(self, seed):
+        self.name = f"fuzz{seed}"
+        self.L, self.rc, self.grid, self.pulses, self.X, self.layout = random_case(seed)
+        W = charges(self.X.shape[0]) if self.layout == 4 else None
+        self.states = decompose(self.X, self.L, self.rc, self.grid, self.pulses, W=W)
+        self.nranks = len(self.states)
+        self.capacity = max(max(s.x.shape[0] for s in self.states), 1) + 64
+        mk = forces_int if seed % 2 == 0 else forces_normal
+        self.F = [mk(s.x.shape[0], 31 * seed + s.rank, width=self.layout) for s in self.states]
+        self.Fo, self.fshift = force_halo(self.states, [f.copy() for f in self.F])
+        self.fabs_total = float(sum(np.abs(f[:, :3].astype(np.float64)).sum() for f in self.F))
+
+    def home_rows(self, r):
+        s = self.states[r]
+        return s.x[: s.n_home]
+
+
+@pytest.mark.parametrize("proto", [0, 1 << 4, 1 << 5], ids=["ll", "paper", "ce"])
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_parity(seed, proto):
+    from paper_2509_21527_b200.session import HaloSession
+    case = FuzzCase(seed)
+    sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=case.layout, capacity=case.capacity,
+                       device=0, flags=proto, timeout_s=5.0)
+    run_gpu_case(case, sess, steps=2)
+    sess.destroy()

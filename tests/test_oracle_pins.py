@@ -353,3 +353,35 @@ def test_coord_halo_step_fixed_maps(name):
             m = s.s[:, d] == 1
             exp[m, d] = (exp[m, d] + L32[d]).astype(np.float32)
         np.testing.assert_array_equal(x, exp)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_geometries_pinned(seed):
+    """The oracle on random geometries (tests/fuzz_cases.py: 1-4 cells per dim, 1-2
+    pulses, uniform or clustered atoms, empty ranks): X1 closed form, X2 import
+    zone by brute force, F1 per-atom totals, F2 conservation, F3 shift forces."""
+    from tests.fuzz_cases import random_case
+    L, rc, grid, pulses, X, _ = random_case(seed)
+    st = decompose(X, L, rc, grid, pulses)
+    L32 = np.array(L, np.float32)
+    for s in st:
+        exp = X[s.gid].copy()
+        for d in range(3):
+            m = s.s[:, d] == 1
+            exp[m, d] = (exp[m, d] + L32[d]).astype(np.float32)
+        np.testing.assert_array_equal(s.x[:, :3], exp)
+        inner, outer = pins.direct_gather(X, L, rc, grid, s.rank, eps=1e-5)
+        have = [(int(g), tuple(int(v) for v in sv)) for g, sv in zip(s.gid, s.s)]
+        assert len(have) == len(set(have))
+        assert inner <= set(have) <= outer
+    F = [forces_int(s.x.shape[0], 7 * seed + s.rank) for s in st]
+    Fo, fs = force_halo(st, F)
+    tot = pins.scatter_totals([s.gid for s in st], F, X.shape[0])
+    got = np.zeros((X.shape[0], 3))
+    for s, f in zip(st, Fo):
+        got[s.gid[:s.n_home]] = f[:s.n_home]
+    np.testing.assert_array_equal(got, tot)
+    fs_tot = sum(fs) if fs else np.zeros((3, 3))
+    for d in range(3):
+        exp = sum(f[s.s[:, d] == 1].astype(np.float64).sum(axis=0) for s, f in zip(st, F))
+        np.testing.assert_array_equal(fs_tot[d], exp)
