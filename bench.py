@@ -28,7 +28,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-PROTO_FLAGS = {"ll": 0, "paper": 1 << 4, "ce": 1 << 5}  # HALO_F_PAPER_FLAGS, HALO_F_CE_PATH
+# HALO_F_PAPER_FLAGS (+ HALO_F_TMA_STORE | HALO_F_TMA_GET: the paper's TMA put / get), HALO_F_CE_PATH
+PROTO_FLAGS = {"ll": 0, "paper": 1 << 4, "paper_tma": (1 << 4) | (1 << 7) | (1 << 8), "ce": 1 << 5}
 METRIC = "x+f halo exchange us/step (max over ranks); achieved NVLink GB/s vs 900"
 UNIT = "us/step"
 SEED = 2509
@@ -431,6 +432,8 @@ def run_fused(args, rank, world, local):
         roof["latency"] = {"floor_us": round(fl2, 3), "frac": round(fl2 / res["step"], 4),
                            "definition": "2*P*t0 + (x+f NVLink bytes per direction)/BW_peer (measured SM peer-store GB/s, 8 MiB) "
                                          "+ 2 launches (eager)"}
+    if not args.no_ns:
+        out["ns_step"] = ns_step_timing(sess, c, X, homes, dev)
     if world == 1 and rank == 0 and not args.no_cpu:
         us, n = oracle_step_timing(c, X, budget_s=args.cpu_budget)
         out["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -438,6 +441,53 @@ def run_fused(args, rank, world, local):
                                          f"steps (fixed-map x halo + force halo), numpy single thread"}
     sess.destroy()
     return out
+
+
+def ns_step_timing(sess, c, X, homes, dev, reps=3):
+    """The NS step that precedes the hot path every nstlist steps:
+    halo_migrate (home-atom redistribution) + halo_set_maps (GPU map build + the
+    coordinate exchange of every pulse), host wall time around each call (both
+    host-synchronise), max over ranks, median of `reps` NS steps.  Atoms move by
+    normal(0, 0.05 nm) per component between NS steps (synth.displacements, then
+    torch normal draws on the device for later steps).  Not part of `value`."""
+    import torch
+    from synth import displacements
+    first, nl, cap = sess.first_rank, sess.n_local, sess.capacity
+    Xm = displacements(X, c.L, 4242, n_far=0)
+    gid = []
+    for l in range(nl):
+        h = homes[first + l]
+        sess.x[l][: h.size, :3] = torch.from_numpy(Xm[h]).to(dev)
+        g = torch.zeros(cap, dtype=torch.int32, device=dev)
+        g[: h.size] = torch.from_numpy(h.astype(np.int32)).to(dev)
+        gid.append(g)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4243 + first)
+    t_mig, t_maps, moved = [], [], []
+    for rep in range(reps + 1):
+        if rep:
+            for l in range(nl):
+                n = sess.n_home[l]
+                sess.x[l][:n, :3] += 0.05 * torch.randn(n, 3, generator=gen, device=dev)
+        before = [set(gid[l][: sess.n_home[l]].tolist()) for l in range(nl)] if rep == 1 else None
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        sess.migrate(gid)
+        t1 = time.perf_counter()
+        barrier()
+        t2 = time.perf_counter()
+        sess.set_maps()
+        t3 = time.perf_counter()
+        if rep:
+            t_mig.append(max_over_ranks((t1 - t0) * 1e6))
+            t_maps.append(max_over_ranks((t3 - t2) * 1e6))
+        if before is not None:
+            moved.append(sum(len(set(gid[l][: sess.n_home[l]].tolist()) - before[l]) for l in range(nl)))
+    return {"migrate_us": round(float(np.median(t_mig)), 1), "set_maps_us": round(float(np.median(t_maps)), 1),
+            "rows_moved_between_ranks_local": int(moved[0]) if moved else 0, "reps": reps,
+            "note": "NS step every nstlist steps (P:976: 200): halo_migrate + halo_set_maps, host wall "
+                    "(both host-synchronise), max over ranks; not in value"}
 
 
 def _neighbour(grid, r, d, delta):
@@ -539,7 +589,9 @@ def main():
     ap.add_argument("--layout", type=int, default=3, choices=(3, 4))
     ap.add_argument("--impl", default="fused", choices=("fused", "reference"))
     ap.add_argument("--proto", default="ll", choices=sorted(PROTO_FLAGS),
-                    help="ll: default LL protocol; paper: per-pulse flags (Alg. 5); ce: copy-engine path")
+                    help="ll: default LL protocol; paper: per-pulse flags (Alg. 5); paper_tma: the same with the "
+                         "x put as warp-leader TMA bulk stores (Alg. 3) and the force halo as a receiver-driven "
+                         "TMA get (Alg. 6); ce: copy-engine path")
     ap.add_argument("--timers", action="store_true")
     ap.add_argument("--l2-persist", action="store_true", help="HALO_F_L2_PERSIST: static plan in persisting L2")
     ap.add_argument("--no-graph", action="store_true")
@@ -547,6 +599,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-floors", action="store_true", help="skip the latency/bandwidth/launch floor probes")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-ns", action="store_true", help="skip the NS-step (halo_migrate + halo_set_maps) timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()

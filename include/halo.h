@@ -89,6 +89,18 @@ typedef enum {
                                            persisting L2 carve-out (access-policy window on the exchange
                                            launches; raises cudaLimitPersistingL2CacheSize device-wide to the
                                            plan size if lower).  Coordinates and forces are never persisted. */
+#define HALO_F_TMA_STORE      (1u << 7) /* with HALO_F_PAPER_FLAGS only: the x put as the paper's warp-leader TMA
+                                           store (Alg. 3): each warp packs a 32-row chunk into
+                                           shared memory, one cp.async.bulk store writes it into the receiver's
+                                           x over NVLink.  HALO_ERR_UNSUPPORTED with the LL or copy-engine path. */
+#define HALO_F_TMA_GET        (1u << 8) /* with HALO_F_PAPER_FLAGS only: the force halo as the paper's receiver-
+                                           driven get (Alg. 6): the x-receiver only signals
+                                           that its halo slice p is final; the x-sender acquire-waits, bulk-loads
+                                           (TMA) each chunk of the slice from the peer's f into shared memory and
+                                           scatter-adds it (same order, same bits as the push).  The reader then
+                                           acks each slice (one flag per pulse), and an exchange_f launch
+                                           completes only after its slices were read, so f may be overwritten
+                                           once the stream passes exchange_f (DESIGN R26).  f is peer-mapped. */
 
 typedef struct {
   int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */
@@ -162,6 +174,29 @@ HALO_API halo_status halo_set_maps(halo_ctx* ctx, const int* n_home, void* strea
  * in halo_set_maps. */
 HALO_API halo_status halo_set_maps_explicit(halo_ctx* ctx, const int* n_home, const int* send_sizes,
                                    const int* const* maps, void* stream);
+
+/* COLLECTIVE, NS step: home-atom redistribution before
+ * halo_set_maps.  Between NS steps atoms move (the decomposition is
+ * rebuilt every nstlist steps); the domains own the atoms inside their region
+ * (P:139-141), so every home atom is re-homed first.
+ *   n_home_in[l]   home rows of local rank l in x (and gid, v) before the call
+ *   gid[l]         DEVICE int32[capacity]: global atom ids of those rows, strictly
+ *                  ascending (the order halo_set_maps' maps refer to, R11)
+ *   v[l]           DEVICE float[capacity*layout] rows carried along unchanged
+ *                  (velocities, ...); v == NULL or v[l] == NULL: no payload
+ *   n_home_out[l]  (host, out) home rows after the call.
+ * Each row is wrapped into the box in float32 (R29: x >= L_d -> x - L_d,
+ * x < 0 -> x + L_d, a result of L_d or -0.0 -> +0.0; the w of float4 rows is
+ * copied), assigned to the rank whose cell holds it (R3/R4) and moved there
+ * (peer stores + loads over NVLink through the scratch staging area); afterwards
+ * rank r holds exactly the atoms of its cell in x/gid/v[0:n_home_out), ascending
+ * gid, bit-exact copies.  An atom may move at most one cell per dimension between
+ * NS steps (R30); otherwise HALO_ERR_GEOMETRY.  HALO_ERR_CAPACITY when a rank
+ * would hold more than `capacity` rows.  Errors are agreed by all ranks.  Halo
+ * rows of x and the maps are invalid afterwards: call halo_set_maps next.
+ * Host-synchronises on `stream`. */
+HALO_API halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gid, float* const* v,
+                                  int* n_home_out, void* stream);
 
 /* Layout of local rank `local` after set_maps (host arrays sized npulse; any may be NULL):
  * recv_off[p] = atomOffset, recv_size[p], send_size[p], remote_off[p] = where

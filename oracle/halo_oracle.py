@@ -221,6 +221,64 @@ def decompose(X, L, rc, grid, pulses, W=None):
     return states
 
 
+def wrap_coord(x, L):
+    """R29 (paper silent; GROMACS puts atoms back in the box at NS steps): ONE
+    periodic wrap in float32 — x >= L -> fl32(x - L); x < 0 -> fl32(x + L) — then
+    a result equal to L (a tiny negative x) or to zero (incl. -0.0) becomes +0.0.
+    Returns (wrapped float32, ok) with ok = 0 <= wrapped < L (else the atom moved
+    more than a box length)."""
+    L = np.float32(L)
+    x = np.float32(x)
+    if x >= L:
+        x = np.float32(x - L)
+    elif x < np.float32(0.0):
+        x = np.float32(x + L)
+    if x == L or x == np.float32(0.0):
+        x = np.float32(0.0)
+    return x, bool(np.float32(0.0) <= x < L)
+
+
+def migrate(homes, L, grid):
+    """NS-step home-atom redistribution: the domains own the
+    atoms inside their region, re-established at every
+    neighbour-search step.  Plain definition, atom by atom:
+
+    homes[r] = (gid [n] int, x [n, W] float32, v [n, W] float32 or None): rank r's
+    home rows before the step (positions possibly moved out of the cell/box).
+    Every row is wrapped (``wrap_coord`` per component; a float4 w is copied),
+    assigned to the rank of its cell (``home_cell``, R3/R4) and collected there;
+    each rank's new rows are sorted by gid.  R30: an atom may move at most one
+    cell per dimension (periodically) from its old rank's cell; else ValueError.
+    Returns the new homes in the same form."""
+    b = planes(L, grid)
+    nr = grid[0] * grid[1] * grid[2]
+    got = [[] for _ in range(nr)]
+    for r, (gid, x, v) in enumerate(homes):
+        c_old = cell_of(r, grid)
+        for i in range(len(gid)):
+            row = np.array(x[i], dtype=np.float32).copy()
+            for d in range(3):
+                row[d], ok = wrap_coord(row[d], L[d])
+                if not ok:
+                    raise ValueError(f"atom {gid[i]} moved more than a box length")
+            c_new = home_cell(row[:3], b, grid)
+            for d in range(3):
+                if (c_new[d] - c_old[d]) % grid[d] not in (0, 1 % grid[d], (grid[d] - 1) % grid[d]):
+                    raise ValueError(f"atom {gid[i]} moved more than one cell in dim {d} (R30)")
+            got[rank_of(c_new, grid)].append((int(gid[i]), row, None if v is None else np.asarray(v[i], np.float32)))
+    out = []
+    for r in range(nr):
+        rows = sorted(got[r], key=lambda t: t[0])
+        W = homes[0][1].shape[1]
+        g = np.array([t[0] for t in rows], dtype=np.int64)
+        x = np.array([t[1] for t in rows], dtype=np.float32).reshape(-1, W)
+        v = None
+        if homes[0][2] is not None:
+            v = np.array([t[2] for t in rows], dtype=np.float32).reshape(-1, W)
+        out.append((g, x, v))
+    return out
+
+
 def coord_halo_step(states, x_home):
     """Per-step coordinate halo with the maps of the last neighbour-search step
     fixed (Alg. 3 P:252-262 with Alg. 4's forwarding, run serially pulse by

@@ -30,6 +30,7 @@ constexpr int kHdrBytes = 4096;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
 constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-force slot area)
 constexpr int kMaxItemRows = 512;      // largest work item (x items carry their map slice in shared memory)
+constexpr uint32_t kPollTight = 0xffffffffu;  // ExParams.poll_ns: tight polling only, no backoff (HALO_POLL_NS=-1)
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
 struct __align__(128) ScratchHdr {
@@ -44,6 +45,11 @@ struct __align__(128) ScratchHdr {
   uint64_t ping;           // floor ping-pong flag
   uint64_t pad4[15];
   uint64_t status[kMaxRanks];  // set_maps error agreement: (epoch << 32) | err, per source rank
+  uint64_t consumed[8];    // HALO_F_TMA_GET: consumed[p] = seq: the x-sender has read (got) slice p
+  // halo_migrate, indexed by the SOURCE / DESTINATION global rank, (epoch << 32) | value:
+  uint64_t mig_cnt[kMaxRanks];  // rows source s sends here (release: its staging rows are written)
+  uint64_t mig_off[kMaxRanks];  // where they start in source s's staging-out area
+  uint64_t mig_ack[kMaxRanks];  // destination t has copied what this rank sent it
 };
 static_assert(sizeof(ScratchHdr) <= kHdrBytes, "ScratchHdr too large");
 
@@ -77,6 +83,52 @@ struct Ctrl {
 };
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };
+
+// ---------------------------------------------------------------- halo_migrate
+// (csrc/kernels_ns.cu).  The stencil of a rank = the distinct
+// ranks of the cells c + delta, delta in {-1,0,1}^3 (periodic): the only ranks a
+// home atom may move to between NS steps (R30), and, symmetrically, the only
+// ranks it can receive atoms from.  Staging area rows are SoA: x (layout
+// floats), v (layout floats), gid (int32), capacity rows each.
+constexpr int kStencil = 27;
+struct MigRank {
+  float* x;                   // own x (rows re-written in place by the merge)
+  int32_t* gid;               // own gid array (caller's)
+  float* v;                   // payload rows or nullptr
+  char* stage_out;            // own staging-out (grouped by destination, ascending gid per group)
+  char* stage_in;             // own staging-in (the lists received, concatenated)
+  ScratchHdr* hdr;            // own header
+  ScratchHdr* nb_hdr[kStencil];      // headers of the stencil ranks
+  const char* nb_stage[kStencil];    // their staging-out areas (peer pointers)
+  int nb_rank[kStencil];
+  int n_nb;                   // distinct stencil ranks (self included)
+  int rank;
+  int n_home;
+  int pad;
+};
+struct MigParams {
+  const MigRank* r;           // n_local entries (device)
+  Ctrl* ctrl;
+  const double* planes;       // planes[d*(kMaxRanks+1) + k] = float64(L_d)*k/grid[d], k = 0..grid[d] (R3)
+  int grid[3];
+  float box[3];
+  int n_local;
+  int layout;
+  int has_v;
+  int capacity;
+  uint32_t epoch;
+  int* err_host;
+  uint64_t timeout_ns;
+};
+// per local rank results of the migration kernels
+struct MigCtrl {
+  int32_t out_cnt[kMaxLocal][kStencil];   // rows this rank sends to stencil rank k (self included)
+  int32_t out_off[kMaxLocal][kStencil];
+  int32_t in_cnt[kMaxLocal][kStencil];    // rows received from stencil rank k
+  int32_t in_src_off[kMaxLocal][kStencil];  // ... starting there in its staging-out
+  int32_t in_off[kMaxLocal][kStencil + 1];  // prefix of in_cnt: list k is rows [in_off[k], in_off[k+1]) of staging-in
+  int32_t err[kMaxLocal];
+};
 
 // HALO_DEBUG bits: protocol mutations for the dependency-safety tests (G3);
 // never set in production.
@@ -114,6 +166,8 @@ struct PulseDev {
   uint32_t chain;           // pulses q > p with send_size > 0 (deterministic unpack order)
   uint64_t* xll_dst;        // receiver's coordinate LL buffer of pulse p (peer pointer), LL protocol
   uint64_t* fll_dst;        // x-sender's force LL buffer of pulse p (peer pointer), LL protocol
+  const float* f_src;       // HALO_F_TMA_GET: the x-receiver's f at its remote_off rows (peer pointer)
+  uint64_t* consumed_dst;   // HALO_F_TMA_GET: &x-receiver.hdr->consumed[p]
   int n_items_x;
   int n_items_push;
   int n_items_unpack;
@@ -188,10 +242,12 @@ struct ExParams {
   unsigned flags;
   double* fshift;           // [n_local][3][3] or nullptr
   int accumulate;
-  uint32_t poll_ns;         // __nanosleep between flag polls (0 = tight spin)
+  uint32_t poll_ns;         // __nanosleep between flag polls (0 = tight, then backoff; kPollTight = tight only)
   uint64_t ll_stride;       // u64 units per pulse slot of the LL receive buffers
   uint32_t debug;           // HALO_DEBUG experiment bits (0 in production)
   uint32_t fsp_slots;       // shift-force slots per pulse in each rank's scratch
+  uint64_t seq;             // LL: this launch's sequence number by value (eager launches; 0 = read
+                            // ctrl->seq_x/f + 1 in the kernel: graph-captured launches, R17)
   const char* xblk;         // LL x item blocks: [XRec | map slice, item_rows int32], 128 + 4*item_rows B each
   const char* fblk;         // LL f item blocks: [GRec | task records, item_rows x 32 B], 128 + 32*item_rows B each
   int item_rows;

@@ -63,6 +63,70 @@ __device__ __forceinline__ void x_rows(const PulseDev& pd, const float* __restri
   }
 }
 
+// HALO_F_TMA_STORE: the paper's NVLink put (Alg. 3): each warp
+// packs a 32-row chunk (gather + shift) into its own shared-memory buffer and the
+// warp leader issues one asynchronous bulk (TMA) store of the chunk into the
+// receiver's x; the other warps keep packing.  Bulk stores need 16-B aligned
+// addresses and sizes: the chunk is staged at the destination's offset mod 16, the
+// aligned body goes by TMA, the unaligned head/tail floats (float3 rows only) by
+// lane stores.  Double-buffered per warp; before the CTA's completion
+// notification every leader waits for its stores to be performed.
+constexpr int kStageFloats = 32 * 4 + 4;  // one chunk of 32 rows (<= 16 B each) + 16 B of alignment slack
+template <int W>
+__device__ __forceinline__ void x_rows_tma(const PulseDev& pd, const float* __restrict__ x, uint32_t b, uint32_t e,
+                                           bool dep, float (*stage)[2][kStageFloats]) {
+  const int32_t* __restrict__ map = pd.map;
+  const bool sh = pd.has_shift != 0;
+  const float s0 = pd.shift[0], s1 = pd.shift[1], s2 = pd.shift[2];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  uint32_t k = 0;
+  for (uint32_t r0 = b + 32 * warp; r0 < e; r0 += 32 * nw, ++k) {
+    float* buf = stage[warp][k & 1];
+    if (k >= 2) {  // the store issued from this buffer two chunks ago has read it
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+    }
+    const uint32_t n = min(32u, e - r0);
+    float* gdst = pd.x_dst + (size_t)r0 * W;
+    const uint32_t mis = (uint32_t)(((uintptr_t)gdst & 15u) >> 2);  // floats before the next 16-B boundary's origin
+    if (lane < n) {
+      const int idx = __ldg(map + r0 + lane);
+      float v[4];
+      if constexpr (W == 4) {
+        const float4* src = reinterpret_cast<const float4*>(x) + idx;
+        const float4 t = dep ? __ldcg(src) : __ldg(src);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+      } else {
+        const float* src = x + 3 * (size_t)idx;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = dep ? __ldcg(src + c) : __ldg(src + c);
+      }
+      if (sh) {  // float32 add of the full 3-vector; w is never shifted (R25)
+        v[0] = __fadd_rn(v[0], s0);
+        v[1] = __fadd_rn(v[1], s1);
+        v[2] = __fadd_rn(v[2], s2);
+      }
+#pragma unroll
+      for (int c = 0; c < W; ++c) buf[mis + lane * W + c] = v[c];
+    }
+    fence_proxy_async_smem();  // this lane's generic smem writes -> visible to the bulk copy
+    __syncwarp();
+    const uint32_t total = n * W;
+    const uint32_t head = mis ? min(4u - mis, total) : 0u;
+    const uint32_t body = ((total - head) >> 2) << 2;
+    if (lane == 0 && body) {
+      bulk_store(gdst + head, buf + mis + head, body * 4u);
+      bulk_commit();
+    }
+    if (lane < head) gdst[lane] = buf[mis + lane];
+    if (lane < total - head - body) gdst[head + body + lane] = buf[mis + head + body + lane];
+  }
+  if (lane == 0 && k) {
+    bulk_wait_all();            // this warp's bulk stores are performed ...
+    fence_proxy_async_global();  // ... and ordered before the generic release that notifies the peer
+  }
+}
+
 // Notify the receiver once per pulse: every CTA fences its peer stores and
 // increments the pulse's completion counter; the last CTA stores the flag
 // (Alg. 5: "only threadIdx.x = 0 proceeds to notify").
@@ -77,9 +141,10 @@ __device__ __forceinline__ void pulse_complete_sys(unsigned flags, uint32_t* cnt
   }
 }
 
-template <int W>
+template <int W, bool kTma>
 __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__ ExParams P) {
   __shared__ uint64_t s_seq;
+  __shared__ __align__(16) float s_stage[kTma ? kThreads / 32 : 1][2][kStageFloats];  // HALO_F_TMA_STORE chunks
   Ctrl* ctrl = P.ctrl;
   if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
@@ -105,7 +170,10 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
       }
       __syncthreads();
     }
-    x_rows<W>(pd, rd.x, w.begin, w.end, dep);
+    if constexpr (kTma)
+      x_rows_tma<W>(pd, rd.x, w.begin, w.end, dep, s_stage);
+    else
+      x_rows<W>(pd, rd.x, w.begin, w.end, dep);
     __syncthreads();
     if (threadIdx.x == 0)
       pulse_complete_sys(P.flags, &ctrl->cnt_x[w.lrank][w.pulse], pd.n_items_x, pd.flag_x_dst, seq,
@@ -147,17 +215,22 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <int W>
-__device__ __forceinline__ void unpack_rows(const PulseDev& pd, float* __restrict__ f, uint32_t b, uint32_t e,
-                                            bool atomic, bool accumulate, double* fshift_rank) {
+// buf: row i of the pulse at buf + i*W — the own receive buffer (push; written by
+// a peer during this kernel: .cg loads) or, kSmem, the chunk just bulk-loaded
+// into shared memory (HALO_F_TMA_GET).
+template <int W, bool kSmem>
+__device__ __forceinline__ void unpack_rows(const PulseDev& pd, const float* buf, float* __restrict__ f, uint32_t b,
+                                            uint32_t e, bool atomic, bool accumulate, double* fshift_rank) {
   const int32_t* __restrict__ map = pd.map;
-  const float* __restrict__ buf = pd.fbuf_own;
   const bool do_shift = (fshift_rank != nullptr) && pd.has_shift;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (uint32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
     const int t = __ldg(map + i);
     float v[4];
-    if constexpr (W == 4) {
+    if constexpr (kSmem) {
+#pragma unroll
+      for (int c = 0; c < W; ++c) v[c] = buf[(size_t)i * W + c];
+    } else if constexpr (W == 4) {
       float4 q = __ldcg(reinterpret_cast<const float4*>(buf) + i);
       v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
     } else {
@@ -191,11 +264,27 @@ __device__ __forceinline__ void unpack_rows(const PulseDev& pd, float* __restric
   }
 }
 
-template <int W>
+// kGet (HALO_F_TMA_GET): the paper's receiver-driven force transport (Alg. 6
+// P:394-398): push items only signal that slice p is final (no data), unpack
+// items bulk-load (TMA) their chunk of the slice from the peer's f into shared
+// memory after the acquire-wait and scatter-add it from there; the last unpack
+// CTA of a pulse acks the read (consumed flag), and the launch completes only
+// when this process's slices were read by their consumers (R26).
+constexpr int kGetFloats = kMaxItemRows * 4 + 8;  // largest item (16-B rows) + 16 B of alignment slack each side
+template <int W, bool kGet>
 __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__ ExParams P) {
   __shared__ uint64_t s_seq;
+  __shared__ __align__(16) float s_get[kGet ? kGetFloats : 4];
+  __shared__ __align__(8) uint64_t s_bar;
+  uint32_t phase = 0;
   Ctrl* ctrl = P.ctrl;
-  if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
+  if (threadIdx.x == 0) {
+    s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
+    if constexpr (kGet) {
+      mbar_init(&s_bar, 1);
+      fence_mbar_init();
+    }
+  }
   timer_start(P.flags, &ctrl->t_start_f);
   __syncthreads();
   const uint64_t seq = s_seq;
@@ -217,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
         }
       }
       __syncthreads();
-      push_rows<W>(pd, rd.f, w.begin, w.end);
+      if constexpr (!kGet) push_rows<W>(pd, rd.f, w.begin, w.end);  // get: the flag alone says "slice p is final"
       __syncthreads();
       if (threadIdx.x == 0)
         pulse_complete_sys(P.flags, &ctrl->cnt_push[w.lrank][w.pulse], pd.n_items_push, pd.flag_f_dst, seq,
@@ -234,9 +323,28 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
           }
         }
       }
+      // get: one bulk load of the chunk's 16-B aligned cover (at most 12 B on each
+      // side that are not used) from the peer's f, issued after the acquire
+      const float* buf = pd.fbuf_own;
+      if constexpr (kGet) {
+        const uintptr_t src = (uintptr_t)(pd.f_src + (size_t)w.begin * W);
+        const uintptr_t a0 = src & ~(uintptr_t)15;
+        const uintptr_t a1 = (src + (size_t)(w.end - w.begin) * W * 4 + 15) & ~(uintptr_t)15;
+        if (threadIdx.x == 0) {
+          fence_proxy_async_global();  // the acquire above orders the async-proxy read
+          bulk_load(s_get, (const void*)a0, (uint32_t)(a1 - a0), &s_bar);
+        }
+        buf = reinterpret_cast<const float*>(reinterpret_cast<const char*>(s_get) + (src - a0)) - (size_t)w.begin * W;
+      }
       __syncthreads();
       double* fs = P.fshift ? P.fshift + 9 * w.lrank : nullptr;
-      unpack_rows<W>(pd, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs);
+      if constexpr (kGet) {
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        unpack_rows<W, true>(pd, buf, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs);
+      } else {
+        unpack_rows<W, false>(pd, buf, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs);
+      }
       __syncthreads();
       if (threadIdx.x == 0) {
         fence_gpu();
@@ -244,8 +352,18 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
         if (old == (uint32_t)pd.n_items_unpack - 1) {
           ctrl->cnt_unpack[w.lrank][w.pulse] = 0;
           st_release_gpu(&ctrl->unpacked[w.lrank][w.pulse], seq);
+          if constexpr (kGet) st_release_sys(pd.consumed_dst, seq);  // every chunk of slice p was read
         }
       }
+    }
+  }
+  if constexpr (kGet) {
+    // the peers have read this process's halo slices: f may be overwritten after the launch
+    if (blockIdx.x < P.n_local && threadIdx.x == 0) {
+      const int lr = blockIdx.x;
+      for (int p = 0; p < P.P; ++p)
+        if (P.pulses[lr * P.P + p].recv_size > 0)
+          wait_geq<true>(&P.ranks[lr].hdr->consumed[p], seq, P.timeout_ns, P.err_host, tcode(14, lr, p), P.poll_ns);
     }
   }
   __syncthreads();
@@ -569,15 +687,25 @@ cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args,
   return launch_coop_kernel_ex(fn, grid, block, args, st, false, 0, nullptr);
 }
 
+static const void* x_paper_fn(int layout, bool tma) {
+  if (tma) return layout == 4 ? (const void*)k_exchange_x<4, true> : (const void*)k_exchange_x<3, true>;
+  return layout == 4 ? (const void*)k_exchange_x<4, false> : (const void*)k_exchange_x<3, false>;
+}
+
 cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStream_t st) {
   void* args[] = {(void*)&p};
-  const void* fn = layout == 4 ? (const void*)k_exchange_x<4> : (const void*)k_exchange_x<3>;
+  const void* fn = x_paper_fn(layout, (p.flags & HALO_F_TMA_STORE) != 0);
   return launch_coop_kernel(fn, grid, kThreads, args, st);
+}
+
+static const void* f_paper_fn(int layout, bool get) {
+  if (get) return layout == 4 ? (const void*)k_exchange_f<4, true> : (const void*)k_exchange_f<3, true>;
+  return layout == 4 ? (const void*)k_exchange_f<4, false> : (const void*)k_exchange_f<3, false>;
 }
 
 cudaError_t launch_exchange_f(const ExParams& p, int layout, int grid, cudaStream_t st) {
   void* args[] = {(void*)&p};
-  const void* fn = layout == 4 ? (const void*)k_exchange_f<4> : (const void*)k_exchange_f<3>;
+  const void* fn = f_paper_fn(layout, (p.flags & HALO_F_TMA_GET) != 0);
   return launch_coop_kernel(fn, grid, kThreads, args, st);
 }
 
@@ -587,12 +715,18 @@ cudaError_t max_coresident(int layout, int* x_blocks, int* f_blocks) {
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &bx, layout == 4 ? (const void*)k_exchange_x<4> : (const void*)k_exchange_x<3>, kThreads, 0);
+  // the smaller of the two x variants (SM stores / TMA stores with their staging buffers)
+  int bt = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bx, x_paper_fn(layout, false), kThreads, 0);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &bf, layout == 4 ? (const void*)k_exchange_f<4> : (const void*)k_exchange_f<3>, kThreads, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bt, x_paper_fn(layout, true), kThreads, 0);
   if (e != cudaSuccess) return e;
+  bx = bx < bt ? bx : bt;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, f_paper_fn(layout, false), kThreads, 0);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bt, f_paper_fn(layout, true), kThreads, 0);
+  if (e != cudaSuccess) return e;
+  bf = bf < bt ? bf : bt;
   *x_blocks = bx * sms;
   *f_blocks = bf * sms;
   return cudaSuccess;

@@ -30,33 +30,37 @@ __device__ __forceinline__ uint64_t ll_pack(float v, uint32_t tag) {
 }
 
 // Slow path: poll one LL unit until it carries `tag`; bounded like every wait.
-// Tight polling for the first kTight polls (the latency regime: data arrives
-// within a few us), then exponential __nanosleep backoff up to ~2 us per poll:
-// a wait that lasts because the peer's grid is not yet resident (it shares the
-// SMs with a concurrent compute kernel, Alg. 2) must not steal that kernel's
-// issue slots and L2 bandwidth.  sleep_ns > 0 (HALO_POLL_NS) forces a fixed sleep.
+// Tight polling for the first ~kTightNs of the wait (the latency regime: data
+// arrives within a few us, and every poll counts), then exponential __nanosleep
+// backoff up to ~2 us per poll: a wait that lasts because the peer's grid is not
+// yet resident (it shares the SMs with a concurrent compute kernel, Alg. 2) must
+// not steal that kernel's issue slots and L2 bandwidth.  The clock is read every
+// 16 polls.  sleep_ns > 0 (HALO_POLL_NS) forces a fixed sleep; kPollTight
+// (HALO_POLL_NS=-1) never sleeps.
 __device__ __forceinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
                                          int code, uint32_t sleep_ns) {
-  constexpr uint32_t kTight = 16;
-  uint64_t t0 = 0;
+  constexpr uint64_t kTightNs = 20000;
+  const uint64_t t0 = gtimer();
+  uint32_t backoff = 0;  // 0 = tight; else the current sleep in ns
   for (uint32_t it = 1;; ++it) {
     if (sleep_ns) {
-      __nanosleep(sleep_ns);
-    } else if (it > kTight) {
-      const uint32_t sh = min((it - kTight) >> 3, 4u);
-      __nanosleep(128u << sh);
+      if (sleep_ns != kPollTight) __nanosleep(sleep_ns);
+    } else if (backoff) {
+      __nanosleep(backoff);
+      if (backoff < 2048u && (it & 7u) == 0) backoff <<= 1;
     }
     const uint64_t v = ld_relaxed_sys(u);
     if ((uint32_t)(v >> 32) == tag) return v;
-    if ((it & 1023u) == 0) {
-      const uint64_t now = gtimer();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        report_timeout(err_host, code);
-        return v;
+    if ((it & 15u) == 0) {
+      const uint64_t el = gtimer() - t0;
+      if (!backoff && el > kTightNs) backoff = 128u;
+      if ((it & 1023u) == 0) {
+        if (el > timeout_ns) {
+          report_timeout(err_host, code);
+          return v;
+        }
+        if (*(volatile int*)err_host != 0) return v;
       }
-      if (*(volatile int*)err_host != 0) return v;
     }
   }
 }
@@ -80,25 +84,40 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
   // next item's block is fetched (cp.async) while the current one is processed
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq;
+  __shared__ __align__(8) uint64_t s_bar[2];  // one mbarrier per item-block buffer
   const uint32_t XB = 128u + 4u * (uint32_t)P.item_rows;
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
   if (trace) ctrl->trace[0][blockIdx.x][0] = gtimer();
   pdl_launch_dependents();
-  // the first block is static plan data: fetched while the previous kernel drains (PDL)
-  if ((int)blockIdx.x < P.n_items) cp_async_block(s_blk, P.xblk + (size_t)blockIdx.x * XB, XB);
+  // the first block is static plan data: one bulk (TMA) copy, issued while the
+  // previous kernel drains (PDL)
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+    if ((int)blockIdx.x < P.n_items) bulk_load(s_blk, P.xblk + (size_t)blockIdx.x * XB, XB, &s_bar[0]);
+  }
+  uint32_t phase = 0u;  // bit b = the parity to wait for on s_bar[b] (a register, not an indexed array)
   pdl_wait();  // everything below may depend on earlier work of the stream
-  if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_x) + 1;
+  // by value when the host knows it (no cold dependent load on the critical path)
+  if (threadIdx.x == 0) s_seq = P.seq ? P.seq : ld_relaxed_gpu(&ctrl->seq_x) + 1;
   timer_start(P.flags, &ctrl->t_start_x);
-  cp_async_wait_all();
-  __syncthreads();
+  __syncthreads();  // barrier init visible to every thread
+  if ((int)blockIdx.x < P.n_items) {
+    mbar_wait(&s_bar[0], phase & 1u);
+    phase ^= 1u;
+  }
   // arrive early: the atomic's latency hides behind the items (launch_arrive)
   const uint32_t arrived = launch_arrive(&ctrl->done_x);
   uint64_t seq = 0;
   int cur = 0;
   for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
-    if (it + (int)gridDim.x < P.n_items)
-      cp_async_block(s_blk + (cur ^ 1) * XB, P.xblk + (size_t)(it + gridDim.x) * XB, XB);
+    const bool more = it + (int)gridDim.x < P.n_items;
+    if (more && threadIdx.x == 0) {
+      fence_proxy_async_smem();  // generic reads of that buffer (previous item) before the async write
+      bulk_load(s_blk + (cur ^ 1) * XB, P.xblk + (size_t)(it + gridDim.x) * XB, XB, &s_bar[cur ^ 1]);
+    }
     const XRec& r = *reinterpret_cast<const XRec*>(s_blk + cur * XB);
     const int32_t* s_map = reinterpret_cast<const int32_t*>(s_blk + cur * XB + 128);
     if (trace && seq == 0) ctrl->trace[0][blockIdx.x][1] = gtimer();
@@ -198,8 +217,11 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
         ctrl->trace[0][blockIdx.x][5 + 2 * slot] = gtimer();
       }
     }
-    cp_async_wait_all();  // the next block has landed ...
-    __syncthreads();      // ... for every thread, and everyone is done with this one
+    if (more) {  // the next block has landed
+      mbar_wait(&s_bar[cur ^ 1], (phase >> (cur ^ 1)) & 1u);
+      phase ^= 1u << (cur ^ 1);
+    }
+    __syncthreads();  // everyone is done with this block before it is refilled
     cur ^= 1;
   }
   seq = s_seq;
@@ -295,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
   // buffered like the x kernel's
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq;
+  __shared__ __align__(8) uint64_t s_bar[2];  // one mbarrier per item-block buffer
   __shared__ double s_fs[9][kThreads];
   const uint32_t FB = 128u + 32u * (uint32_t)P.item_rows;
   Ctrl* ctrl = P.ctrl;
@@ -311,17 +334,30 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
   const int end = ((int)blockIdx.x < Gm) ? n_main : P.n_items;
   // the first block is static plan data: fetched while the previous kernel of the
   // stream drains (PDL); f itself is read after the wait
-  if (first < end) cp_async_block(s_blk, P.fblk + (size_t)first * FB, FB);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+    if (first < end) bulk_load(s_blk, P.fblk + (size_t)first * FB, FB, &s_bar[0]);
+  }
+  uint32_t phase = 0u;  // bit b = the parity to wait for on s_bar[b] (a register, not an indexed array)
   pdl_wait();
-  if (threadIdx.x == 0) s_seq = ld_relaxed_gpu(&ctrl->seq_f) + 1;
+  if (threadIdx.x == 0) s_seq = P.seq ? P.seq : ld_relaxed_gpu(&ctrl->seq_f) + 1;
   timer_start(P.flags, &ctrl->t_start_f);
-  cp_async_wait_all();
   __syncthreads();
+  if (first < end) {
+    mbar_wait(&s_bar[0], phase & 1u);
+    phase ^= 1u;
+  }
   const uint32_t arrived = launch_arrive(&ctrl->done_f);
   uint64_t seq = 0;
   int cur = 0;
   for (int it = first; it < end; it += stride) {
-    if (it + stride < end) cp_async_block(s_blk + (cur ^ 1) * FB, P.fblk + (size_t)(it + stride) * FB, FB);
+    const bool more = it + stride < end;
+    if (more && threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      bulk_load(s_blk + (cur ^ 1) * FB, P.fblk + (size_t)(it + stride) * FB, FB, &s_bar[cur ^ 1]);
+    }
     const GRec& g = *reinterpret_cast<const GRec*>(s_blk + cur * FB);
     const int4* tasks = reinterpret_cast<const int4*>(s_blk + cur * FB + 128);
     if (trace && seq == 0) ctrl->trace[1][blockIdx.x][1] = gtimer();
@@ -336,7 +372,10 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
           ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();
         }
       }
-      cp_async_wait_all();
+      if (more) {
+        mbar_wait(&s_bar[cur ^ 1], (phase >> (cur ^ 1)) & 1u);
+        phase ^= 1u << (cur ^ 1);
+      }
       __syncthreads();
       cur ^= 1;
       continue;
@@ -424,7 +463,10 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
         ctrl->trace[1][blockIdx.x][5 + 2 * slot] = gtimer();
       }
     }
-    cp_async_wait_all();
+    if (more) {
+      mbar_wait(&s_bar[cur ^ 1], (phase >> (cur ^ 1)) & 1u);
+      phase ^= 1u << (cur ^ 1);
+    }
     __syncthreads();
     cur ^= 1;
   }

@@ -70,6 +70,52 @@ __device__ __forceinline__ void cp_async_block(void* smem, const void* gmem, uin
   cp_async_commit();
 }
 
+// Bulk (TMA engine) global -> shared copy completing on an mbarrier: one
+// elected thread moves a whole work-item block (cp.async.bulk; 16-B aligned,
+// size a multiple of 16), every thread waits on the barrier's phase.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Issue the copy (caller: one thread).  The barrier's current phase completes
+// when `bytes` have landed.
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+// Bulk (TMA engine) shared -> global store, bulk-group completion (the paper's
+// warp-leader TMA put, Alg. 3).  The destination may be a peer GPU's
+// memory (CUDA-IPC mapping over NVLink).  16-B aligned, size a multiple of 16.
+__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gmem), "r"(smem_u32(smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// all but the newest N groups have finished READING shared memory (buffer reuse)
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+// every group of this thread is complete: its writes are performed
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// order async-proxy global writes with the generic proxy (the release that follows)
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 // Programmatic dependent launch (sm_90+): let the next kernel of the stream be
 // scheduled now, and block until the previous kernel's memory is complete.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -94,7 +140,7 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t v, uint64_t
   if ((kSys ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) < v) {
     uint64_t t0 = 0;
     for (uint32_t it = 1;; ++it) {
-      if (poll_ns) __nanosleep(poll_ns);
+      if (poll_ns && poll_ns != 0xffffffffu) __nanosleep(poll_ns);  // 0xffffffff: kPollTight
       if ((kSys ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) >= v) break;
       if ((it & 1023u) == 0) {
         const uint64_t now = gtimer();

@@ -19,6 +19,7 @@ namespace halo {
 cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStream_t st);
 cudaError_t launch_exchange_f(const ExParams& p, int layout, int grid, cudaStream_t st);
 cudaError_t max_coresident(int layout, int* x_blocks, int* f_blocks);
+cudaError_t launch_migrate(const MigParams& M, MigCtrl* C, int max_rows, int phase, cudaStream_t st);
 cudaError_t launch_select(const SelParams& s, int n_local, cudaStream_t st);
 cudaError_t launch_handshake(const HsParams& h, cudaStream_t st);
 cudaError_t launch_depmask(const RankDev* ranks, Ctrl* ctrl, int p, int map_stride, int n_local, cudaStream_t st);
@@ -64,6 +65,8 @@ struct BlobEntry {
   uint64_t offx;
   cudaIpcMemHandle_t hs;
   uint64_t offs;
+  cudaIpcMemHandle_t hf;  // f: read by peers only with HALO_F_TMA_GET (receiver-driven get)
+  uint64_t offf;
 };
 
 // cuMemGetAddressRange through the runtime's driver entry point (no -lcuda link,
@@ -89,6 +92,8 @@ struct halo_ctx {
   int nranks = 0, n_local = 0, first_rank = 0, P = 0, W = 3;
   int pdim[kMaxP] = {0}, pk[kMaxP] = {0};
   size_t map_stride = 0, fbuf_stride = 0, ll_stride = 0, fsp_slots = 0, scratch_bytes = 0;
+  size_t mig_off = 0;                // halo_migrate staging: [out | in] at this scratch offset
+  size_t mig_stage = 0;              // bytes of one staging area (x | v | gid rows, capacity each)
   bool ll = true;                   // LL protocol (default) vs the paper's flag protocol
   bool ce = false;                  // copy-engine path (HALO_F_CE_PATH; set_maps uses the paper kernels)
   std::string last_error;
@@ -98,6 +103,7 @@ struct halo_ctx {
   std::vector<char*> scratch;
   // every rank's peer view (local pointers for this process's ranks)
   std::vector<float*> peer_x;
+  std::vector<float*> peer_f;
   std::vector<char*> peer_scratch;
   std::vector<void*> opened;  // IPC bases to close
   bool peers_ready = false;
@@ -114,6 +120,9 @@ struct halo_ctx {
   int n_tail_f = 0;                 // LL: shift-force combine items at the end of the f list
   double* d_fshift_tmp = nullptr;  // halo_step_host
   char* d_small = nullptr;          // set_maps argument staging
+  MigRank* d_mig = nullptr;         // halo_migrate: per local rank tables
+  MigCtrl* d_migctrl = nullptr;
+  double* d_planes = nullptr;
   uint64_t* d_rtt = nullptr;
   int* err_host = nullptr;          // host-mapped error word
   int* err_dev = nullptr;
@@ -166,7 +175,12 @@ struct halo_ctx {
   bool item_rows_fixed = false;     // HALO_ITEM_ROWS given: no adaptive choice
   uint32_t poll_ns = 0;
   uint32_t debug = 0;
-  int recv_mult = 4;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT)
+  // LL sequence numbers mirrored on the host: launches take them by value until the
+  // ctx is first used under stream capture (a replayed graph must read the device
+  // counter, R17); every LL launch advances the device counter in any case
+  uint64_t seq_host_x = 0, seq_host_f = 0;
+  bool captured = false;
+  int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
 
   int cell(int r, int d) const {
     const int* g = cfg.grid;
@@ -216,7 +230,7 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // Scratch layout of one DD rank (halo_internal.h): header | maps | force
 // buffers (paper protocol) | coordinate LL buffers | force LL buffers.
 struct ScratchLayout {
-  size_t map_stride, fbuf_stride, ll_stride, fsp_slots, total;
+  size_t map_stride, fbuf_stride, ll_stride, fsp_slots, mig_off, mig_stage, total;
 };
 static ScratchLayout scratch_layout(int P, int capacity, int layout) {
   ScratchLayout L;
@@ -226,6 +240,10 @@ static ScratchLayout scratch_layout(int P, int capacity, int layout) {
   L.fsp_slots = align_up(((size_t)capacity + kMinItemRows - 1) / kMinItemRows, 8);  // shift-force slots per pulse
   L.total = kHdrBytes + (size_t)P * L.map_stride * sizeof(int32_t) + (size_t)P * L.fbuf_stride * sizeof(float) +
             2 * (size_t)P * L.ll_stride * sizeof(uint64_t) + (size_t)P * L.fsp_slots * 6 * sizeof(uint64_t);
+  // halo_migrate staging-out and staging-in: x | v | gid rows, capacity each
+  L.mig_off = align_up(L.total, 256);
+  L.mig_stage = align_up((size_t)capacity * (2 * layout + 1) * sizeof(float), 256);
+  L.total = L.mig_off + 2 * L.mig_stage;
   return L;
 }
 
@@ -266,6 +284,11 @@ static halo_status validate(const halo_config* c, std::string& why) {
   if (nr % c->nprocs != 0) { why = "nranks must be a multiple of nprocs"; return HALO_ERR_ARG; }
   if (nr / c->nprocs > kMaxLocal) { why = "too many ranks per process (HALO_MAX_LOCAL)"; return HALO_ERR_UNSUPPORTED; }
   if (P > kMaxP) { why = "too many pulses"; return HALO_ERR_UNSUPPORTED; }
+  if ((c->flags & (HALO_F_TMA_STORE | HALO_F_TMA_GET)) &&
+      (!(c->flags & HALO_F_PAPER_FLAGS) || (c->flags & HALO_F_CE_PATH))) {
+    why = "HALO_F_TMA_STORE / HALO_F_TMA_GET are variants of the paper protocol (HALO_F_PAPER_FLAGS, no HALO_F_CE_PATH)";
+    return HALO_ERR_UNSUPPORTED;
+  }
   return HALO_OK;
 }
 
@@ -318,6 +341,8 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     ctx->fbuf_stride = SL.fbuf_stride;
     ctx->ll_stride = SL.ll_stride;
     ctx->fsp_slots = SL.fsp_slots;
+    ctx->mig_off = SL.mig_off;
+    ctx->mig_stage = SL.mig_stage;
     ctx->scratch_bytes = SL.total;
   }
   ctx->ce = (cfg->flags & HALO_F_CE_PATH) != 0;
@@ -326,12 +351,13 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   ctx->f.assign(ctx->n_local, nullptr);
   ctx->scratch.assign(ctx->n_local, nullptr);
   ctx->peer_x.assign(ctx->nranks, nullptr);
+  ctx->peer_f.assign(ctx->nranks, nullptr);
   ctx->peer_scratch.assign(ctx->nranks, nullptr);
   if (const char* e = getenv("HALO_ITEM_ROWS")) {
     ctx->item_rows = std::min(kMaxItemRows, std::max(kMinItemRows, atoi(e)));
     ctx->item_rows_fixed = true;
   }
-  if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = (uint32_t)std::max(0, atoi(e));
+  if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = atoi(e) < 0 ? kPollTight : (uint32_t)atoi(e);
   if (const char* e = getenv("HALO_RECV_MULT")) ctx->recv_mult = std::min(16, std::max(1, atoi(e)));
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
@@ -346,6 +372,9 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) { memset(ctx->err_host, 0, 64); e = cudaHostGetDevicePointer(&ctx->err_dev, ctx->err_host, 0); }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_small, 64 * 1024);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_mig, sizeof(MigRank) * ctx->n_local);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_migctrl, sizeof(MigCtrl));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_planes, sizeof(double) * 3 * (kMaxRanks + 1));
   if (e == cudaSuccess)
     e = ctx->ll ? max_coresident_ll(cfg->layout, false, &ctx->max_x, &ctx->max_f)
                 : max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
@@ -426,6 +455,7 @@ halo_status halo_register_buffers(halo_ctx* ctx, int local, void* x, void* f, vo
   ctx->scratch[local] = (char*)scratch;
   const int r = ctx->first_rank + local;
   ctx->peer_x[r] = (float*)x;
+  ctx->peer_f[r] = (float*)f;
   ctx->peer_scratch[r] = (char*)scratch;
   ctx->maps_ready = false;
   bool all = true;
@@ -468,6 +498,10 @@ halo_status halo_ipc_export(halo_ctx* ctx, void* blob, size_t* len) {
       return fail(ctx, HALO_ERR_PEER, "cuMemGetAddressRange(scratch) failed");
     CK(cudaIpcGetMemHandle(&be.hs, (void*)(uintptr_t)base));
     be.offs = (uintptr_t)ctx->scratch[l] - base;
+    if (range(&base, &sz, (unsigned long long)(uintptr_t)ctx->f[l]) != 0)
+      return fail(ctx, HALO_ERR_PEER, "cuMemGetAddressRange(f) failed");
+    CK(cudaIpcGetMemHandle(&be.hf, (void*)(uintptr_t)base));
+    be.offf = (uintptr_t)ctx->f[l] - base;
     memcpy(&ents[l], &be, sizeof be);
   }
   *len = need;
@@ -492,9 +526,9 @@ halo_status halo_ipc_import(halo_ctx* ctx, const void* blobs, size_t len_each) {
     for (int l = 0; l < h.n_local; ++l) {
       BlobEntry be;
       memcpy(&be, &ents[l], sizeof be);
-      char* bases[2] = {nullptr, nullptr};
-      const cudaIpcMemHandle_t* hs[2] = {&be.hx, &be.hs};
-      for (int k = 0; k < 2; ++k) {
+      char* bases[3] = {nullptr, nullptr, nullptr};
+      const cudaIpcMemHandle_t* hs[3] = {&be.hx, &be.hs, &be.hf};
+      for (int k = 0; k < 3; ++k) {
         std::string key((const char*)hs[k], sizeof(cudaIpcMemHandle_t));
         auto it = opened.find(key);
         if (it != opened.end()) { bases[k] = it->second; continue; }
@@ -511,6 +545,7 @@ halo_status halo_ipc_import(halo_ctx* ctx, const void* blobs, size_t len_each) {
       const int r = h.first_rank + l;
       ctx->peer_x[r] = reinterpret_cast<float*>(bases[0] + be.offx);
       ctx->peer_scratch[r] = bases[1] + be.offs;
+      ctx->peer_f[r] = reinterpret_cast<float*>(bases[2] + be.offf);
     }
   }
   for (int r = 0; r < ctx->nranks; ++r)
@@ -571,6 +606,8 @@ static void fill_pulse_dev(halo_ctx* ctx, int l, int p) {
   pd.chain = chain;
   pd.xll_dst = ctx->xll_of(lower) + (size_t)p * ctx->ll_stride;
   pd.fll_dst = ctx->fll_of(upper) + (size_t)p * ctx->ll_stride;
+  pd.f_src = ctx->peer_f[lower] + (size_t)ctx->remote_off[i] * W;
+  pd.consumed_dst = &ctx->hdr_of(lower)->consumed[p];
 }
 
 static void add_items(std::vector<Item>& v, int l, int p, uint8_t kind, int b, int e, int rows) {
@@ -871,6 +908,20 @@ static halo_status upload_plan(halo_ctx* ctx) {
   ctx->n_items_x = (int)ctx->h_items_x.size();
   ctx->n_items_f = (int)ctx->h_items_f.size();
   return HALO_OK;
+}
+
+// Sequence number of the next LL launch on `st`: by value (host mirror) unless the
+// ctx has ever been captured into a graph (then 0: the kernel reads the device
+// counter, which every LL launch advances).
+static uint64_t next_seq(halo_ctx* ctx, cudaStream_t st, uint64_t* host) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    (void)cudaGetLastError();
+    ctx->captured = true;
+  }
+  if (cs != cudaStreamCaptureStatusNone) ctx->captured = true;
+  ++*host;
+  return ctx->captured ? 0 : *host;
 }
 
 static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p_lo, int p_hi) {
@@ -1211,9 +1262,11 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     }
     if ((s = upload_plan(ctx)) != HALO_OK) return s;
     ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
-    if (ctx->ll)
+    if (ctx->ll) {
+      X.seq = next_seq(ctx, st, &ctx->seq_host_x);
       CK(launch_exchange_x_ll(X, W, grid_for(ctx->n_items_x, L, ctx->cap_x()), ctx->wide(), nullptr, st));
-    else
+    }
+    if (!ctx->ll)
       CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
     CK(cudaStreamSynchronize(st));
     if ((s = check_err_word(ctx)) != HALO_OK) return s;
@@ -1305,6 +1358,106 @@ halo_status halo_set_maps_explicit(halo_ctx* ctx, const int* n_home, const int* 
   return set_maps_impl(ctx, n_home, send_sizes, maps, (cudaStream_t)stream);
 }
 
+// NS-step redistribution (kernels_ns.cu).
+halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gid, float* const* v, int* n_home_out,
+                         void* stream) {
+  if (!ctx || !n_home_in || !gid || !n_home_out) return HALO_ERR_ARG;
+  if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "register buffers and import peers first");
+  const int L = ctx->n_local, W = ctx->W;
+  const bool has_v = v != nullptr;
+  for (int l = 0; l < L; ++l) {
+    if (!gid[l] || (has_v && !v[l])) return fail(ctx, HALO_ERR_ARG, "NULL gid / v array");
+    if (n_home_in[l] < 0 || n_home_in[l] > ctx->cfg.capacity) return fail(ctx, HALO_ERR_ARG, "n_home out of range");
+  }
+  CK(cudaSetDevice(ctx->cfg.device));
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  ctx->maps_ready = false;
+  ctx->x_done = false;
+  ctx->epoch++;
+  // stencil of every local rank: the distinct ranks of cells c + delta (R30)
+  std::vector<MigRank> mr(L);
+  for (int l = 0; l < L; ++l) {
+    MigRank& R = mr[l];
+    memset(&R, 0, sizeof R);
+    const int r = ctx->first_rank + l;
+    R.x = ctx->x[l];
+    R.gid = gid[l];
+    R.v = has_v ? v[l] : nullptr;
+    R.stage_out = ctx->scratch[l] + ctx->mig_off;
+    R.stage_in = ctx->scratch[l] + ctx->mig_off + ctx->mig_stage;
+    R.hdr = ctx->hdr_of(r);
+    R.rank = r;
+    R.n_home = n_home_in[l];
+    const int* g = ctx->cfg.grid;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          const int cx = ((ctx->cell(r, 0) + dx) % g[0] + g[0]) % g[0];
+          const int cy = ((ctx->cell(r, 1) + dy) % g[1] + g[1]) % g[1];
+          const int cz = ((ctx->cell(r, 2) + dz) % g[2] + g[2]) % g[2];
+          const int nb = ctx->rank_of(cx, cy, cz);
+          bool seen = false;
+          for (int k = 0; k < R.n_nb; ++k) seen |= R.nb_rank[k] == nb;
+          if (seen) continue;
+          R.nb_rank[R.n_nb] = nb;
+          R.nb_hdr[R.n_nb] = ctx->hdr_of(nb);
+          R.nb_stage[R.n_nb] = ctx->peer_scratch[nb] + ctx->mig_off;
+          R.n_nb++;
+        }
+  }
+  double planes[3 * (kMaxRanks + 1)] = {0};
+  for (int d = 0; d < 3; ++d)
+    for (int k = 0; k <= ctx->cfg.grid[d]; ++k) planes[d * (kMaxRanks + 1) + k] = ctx->plane(d, k);
+  CK(cudaMemcpyAsync(ctx->d_mig, mr.data(), sizeof(MigRank) * L, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->d_planes, planes, sizeof planes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->d_migctrl, 0, sizeof(MigCtrl), st));
+  MigParams M{};
+  M.r = ctx->d_mig;
+  M.ctrl = ctx->ctrl;
+  M.planes = ctx->d_planes;
+  for (int d = 0; d < 3; ++d) {
+    M.grid[d] = ctx->cfg.grid[d];
+    M.box[d] = ctx->cfg.box[d];
+  }
+  M.n_local = L;
+  M.layout = W;
+  M.has_v = has_v ? 1 : 0;
+  M.capacity = ctx->cfg.capacity;
+  M.epoch = ctx->epoch;
+  M.err_host = ctx->err_dev;
+  M.timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);
+  CK(launch_migrate(M, ctx->d_migctrl, ctx->cfg.capacity, 0, st));
+  // error agreement over all ranks (as set_maps), before any row moves
+  StatusParams SP{};
+  SP.ctrl = ctx->ctrl;
+  SP.epoch = ctx->epoch;
+  SP.nranks = ctx->nranks;
+  SP.n_local = L;
+  SP.first_rank = ctx->first_rank;
+  for (int l = 0; l < L; ++l) SP.own[l] = ctx->hdr_of(ctx->first_rank + l);
+  for (int r = 0; r < ctx->nranks; ++r) SP.all[r] = ctx->hdr_of(r);
+  SP.err_host = ctx->err_dev;
+  SP.timeout_ns = M.timeout_ns;
+  CK(launch_status(SP, st));
+  CK(launch_migrate(M, ctx->d_migctrl, ctx->cfg.capacity, 1, st));
+  int32_t agreed[kMaxLocal];
+  MigCtrl hc;
+  CK(cudaMemcpyAsync(agreed, ctx->ctrl->agreed_err, sizeof agreed, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&hc, ctx->d_migctrl, sizeof hc, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((s = check_err_word(ctx)) != HALO_OK) return s;
+  int any = 0;
+  for (int l = 0; l < L; ++l) any |= agreed[l];
+  if (any & kErrGeometry)
+    return fail(ctx, HALO_ERR_GEOMETRY, "an atom moved more than one cell (or a box length) since the last NS step");
+  if (any & kErrCapacity) return fail(ctx, HALO_ERR_CAPACITY, "a rank would hold more home rows than capacity");
+  if (any & kErrMap) return fail(ctx, HALO_ERR_ARG, "gid rows are not strictly ascending on some rank");
+  for (int l = 0; l < L; ++l) n_home_out[l] = hc.in_off[l][mr[l].n_nb];
+  return HALO_OK;
+}
+
 halo_status halo_get_layout(const halo_ctx* ctx, int local, int* n_home, int* n_total, int* npulse, int* recv_off,
                             int* recv_size, int* send_size, int* remote_off, unsigned* dep_mask) {
   if (!ctx || local < 0 || local >= ctx->n_local) return HALO_ERR_ARG;
@@ -1350,9 +1503,11 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, 0, ctx->P);
   const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
   ctx->last_grid[0] = grid;
-  if (ctx->ll)
+  if (ctx->ll) {
+    X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x);
     CK(launch_exchange_x_ll(X, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
-  else
+  }
+  if (!ctx->ll)
     CK(launch_exchange_x(X, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
 }
@@ -1375,9 +1530,11 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
     grid = std::max(grid, 1);
   }
   ctx->last_grid[1] = grid;
-  if (ctx->ll)
+  if (ctx->ll) {
+    F.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f);
     CK(launch_exchange_f_ll(F, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
-  else
+  }
+  if (!ctx->ll)
     CK(launch_exchange_f(F, ctx->W, grid, (cudaStream_t)stream));
   return HALO_OK;
 }
@@ -1625,6 +1782,9 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->ctrl) (void)cudaFree(ctx->ctrl);
   if (ctx->d_fshift_tmp) (void)cudaFree(ctx->d_fshift_tmp);
   if (ctx->d_small) (void)cudaFree(ctx->d_small);
+  if (ctx->d_mig) (void)cudaFree(ctx->d_mig);
+  if (ctx->d_migctrl) (void)cudaFree(ctx->d_migctrl);
+  if (ctx->d_planes) (void)cudaFree(ctx->d_planes);
   if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
   if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
   if (ctx->d_ce) (void)cudaFree(ctx->d_ce);

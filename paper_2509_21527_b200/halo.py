@@ -146,6 +146,16 @@ class Halo:
                                        out.ctypes.data_as(ctypes.POINTER(c_int)), c_int(n)))
         return out[:n]
 
+    def migrate(self, n_home, gid_ptrs, v_ptrs=None, stream=0):
+        """NS-step home-atom redistribution (halo_migrate); returns the new n_home per local rank."""
+        nl = len(n_home)
+        arr = (c_int * nl)(*[int(v) for v in n_home])
+        g = (c_void_p * nl)(*[c_void_p(p) for p in gid_ptrs])
+        vv = (c_void_p * nl)(*[c_void_p(p) for p in v_ptrs]) if v_ptrs is not None else None
+        out = (c_int * nl)()
+        self._ck(self.lib.halo_migrate(self.h, arr, g, vv, out, c_void_p(stream)))
+        return [int(out[l]) for l in range(nl)]
+
     def exchange_x(self, stream=0):
         self._ck(self.lib.halo_exchange_x(self.h, c_void_p(stream)))
 

@@ -86,6 +86,14 @@ class HaloSession:
     def set_maps_explicit(self, maps, stream=None):
         self.halo.set_maps_explicit(self.n_home, maps, stream=self._s(stream))
 
+    def migrate(self, gid, v=None, stream=None):
+        """NS-step redistribution of the home rows (halo_migrate): gid[l] / v[l] are
+        device tensors (int32 [capacity] / float32 [capacity, layout]) of local rank l,
+        rewritten in place with x; returns and records the new n_home per local rank."""
+        self.n_home = self.halo.migrate(self.n_home, [g.data_ptr() for g in gid],
+                                        [t.data_ptr() for t in v] if v is not None else None, stream=self._s(stream))
+        return list(self.n_home)
+
     def layout_of(self, l):
         return self.halo.get_layout(l)
 

@@ -1,0 +1,9 @@
+python -m paper_2509_21527_b200.build > gpurun_out/r_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q > gpurun_out/r_pytest1.log 2>&1; echo rc=$? >> gpurun_out/r_pytest1.log
+timeout 900 python -m pytest tests/test_gpu_multiproc.py -x -q > gpurun_out/r_pytest2.log 2>&1; echo rc=$? >> gpurun_out/r_pytest2.log
+L=tma=ab/libhalo_tma.so,cpa=ab/libhalo_rm.so@HALO_RECV_MULT=1
+python scripts/ab.py --libs $L --config C3 --gpus 1 --reps 3 > gpurun_out/r_ab_C3_n1.txt 2>&1
+python scripts/ab.py --libs $L --config C1 --gpus 2 --reps 3 > gpurun_out/r_ab_C1_n2.txt 2>&1
+python scripts/ab.py --libs $L --config C3 --gpus 2 --reps 2 > gpurun_out/r_ab_C3_n2.txt 2>&1
+python scripts/ab.py --libs $L --config C4-1D --gpus 2 --reps 2 > gpurun_out/r_ab_C41D_n2.txt 2>&1
+python scripts/ab.py --libs $L --config C4-bw8 --gpus 2 --reps 1 > gpurun_out/r_ab_C4bw8_n2.txt 2>&1

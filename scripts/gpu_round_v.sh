@@ -1,0 +1,10 @@
+python -m paper_2509_21527_b200.build > gpurun_out/v_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "tma" > gpurun_out/v_pytest0.log 2>&1; echo rc=$? >> gpurun_out/v_pytest0.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q > gpurun_out/v_pytest1.log 2>&1; echo rc=$? >> gpurun_out/v_pytest1.log
+timeout 900 python -m pytest tests/test_gpu_multiproc.py -x -q > gpurun_out/v_pytest2.log 2>&1; echo rc=$? >> gpurun_out/v_pytest2.log
+cp paper_2509_21527_b200/libhalo.so /tmp/lv.so
+L=paper=/tmp/lv.so+--proto+paper,tma=/tmp/lv.so+--proto+paper_tma,ll=/tmp/lv.so
+python scripts/ab.py --libs $L --config C1 --gpus 2 --reps 2 > gpurun_out/v_ab_C1_n2.txt 2>&1
+python scripts/ab.py --libs $L --config C4-1D --gpus 2 --reps 2 > gpurun_out/v_ab_C41D_n2.txt 2>&1
+python scripts/ab.py --libs $L --config C4-bw8 --gpus 2 --reps 1 > gpurun_out/v_ab_C4bw8_n2.txt 2>&1
+python scripts/ab.py --libs $L --config C3 --gpus 1 --reps 2 > gpurun_out/v_ab_C3_n1.txt 2>&1

@@ -127,3 +127,23 @@ def charges(n_atoms: int) -> np.ndarray:
     """SPC charges (O -0.82, H +0.41), used as the float4 ``w`` component."""
     q = np.tile(np.array([-0.82, 0.41, 0.41], dtype=np.float32), n_atoms // 3 + 1)
     return q[:n_atoms].copy()
+
+
+def displacements(X: np.ndarray, L, seed: int, sigma: float = 0.05, n_far: int = 16, far: float = 0.6) -> np.ndarray:
+    """Moved positions between two NS steps (input of halo_migrate tests/bench): every
+    atom moves by normal(0, sigma) nm per component (nstlist steps of thermal motion;
+    SPC water diffuses ~0.05 nm per 200 x 2 fs), and `n_far` random atoms move by
+    +-`far` nm in every component (diagonal cell crossings).  Positions are NOT
+    wrapped (atoms near a face leave the box): the wrap is the method's (R29).
+    float32 [N, 3]."""
+    rng = _rng(seed)
+    Xm = np.asarray(X, np.float64) + rng.normal(0.0, sigma, size=(X.shape[0], 3))
+    if n_far:
+        idx = rng.choice(X.shape[0], size=min(n_far, X.shape[0]), replace=False)
+        Xm[idx] += far * rng.choice([-1.0, 1.0], size=(idx.size, 3))
+    return Xm.astype(np.float32)
+
+
+def velocities(n_rows: int, seed: int, width: int = 3) -> np.ndarray:
+    """Per-atom payload carried by halo_migrate (velocities, nm/ps), float32 [n, width]."""
+    return _rng(seed).normal(0.0, 0.5, size=(n_rows, width)).astype(np.float32)

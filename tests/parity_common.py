@@ -133,3 +133,71 @@ def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit
             tol = 1e-10 * case.fabs_total
             assert np.all(np.abs(fs[l] - case.fshift[r]) <= tol), (r, fs[l], case.fshift[r])
     return True
+
+
+def moved_case(case: Case, seed: int):
+    """The second NS step of `case`: atoms displaced (synth.displacements), the
+    oracle's wrapped positions (R29) and a Case over them.  Returns (Xm, V, case2)."""
+    from oracle import wrap_coord
+    from synth import displacements, velocities
+    Xm = displacements(case.X, case.L, 100 + seed)
+    V = velocities(case.X.shape[0], 200 + seed, width=case.layout)
+    Xw = Xm.copy()
+    for i in range(Xm.shape[0]):
+        for d in range(3):
+            Xw[i, d] = wrap_coord(Xm[i, d], case.L[d])[0]
+    c2 = Case.__new__(Case)
+    c2.__dict__.update(case.__dict__)
+    c2.__dict__.pop("_absum", None)
+    c2.X = Xw
+    c2.states = decompose(Xw, case.L, case.rc, case.grid, case.pulses, W=case.W)
+    c2.capacity = max(max(s.x.shape[0] for s in c2.states), 1) + 64
+    c2.F = [forces_int(s.x.shape[0], 77 + s.rank, width=case.layout) for s in c2.states]
+    c2.Fo, c2.fshift = force_halo(c2.states, [f.copy() for f in c2.F])
+    c2.fabs_total = float(sum(np.abs(f[:, :3].astype(np.float64)).sum() for f in c2.F))
+    return Xm, V, c2
+
+
+def run_gpu_migrate(case: Case, c2: Case, Xm, V, sess, with_v=True, barrier=None, steps=2):
+    """NS step 1 + one exchange step on `case`; the home rows move to Xm; halo_migrate
+    vs oracle.migrate (bit-exact x, gid, payload, counts); then NS step 2 on the
+    migrated rows (maps, x halo, force halo vs the oracle of the moved system)."""
+    from oracle import migrate
+    run_gpu_case(case, sess, barrier=barrier)
+    layout, cap = case.layout, sess.capacity
+    homes = [None] * case.nranks
+    gid_t, v_t = [], []
+    for r, st in enumerate(case.states):
+        g = st.gid[: st.n_home]
+        rows = np.zeros((g.size, layout), np.float32)
+        rows[:, :3] = Xm[g]
+        if layout == 4:
+            rows[:, 3] = case.W[g]
+        homes[r] = (g, rows, V[g] if with_v else None)
+    for l in range(sess.n_local):
+        g, rows, _ = homes[sess.first_rank + l]
+        sess.x[l][: g.size] = torch.from_numpy(rows).to(sess.device)
+        gt = torch.zeros(cap, dtype=torch.int32, device=sess.device)
+        gt[: g.size] = torch.from_numpy(g.astype(np.int32)).to(sess.device)
+        gid_t.append(gt)
+        vt = torch.zeros(cap, layout, dtype=torch.float32, device=sess.device)
+        vt[: g.size] = torch.from_numpy(V[g]).to(sess.device)
+        v_t.append(vt)
+    torch.cuda.synchronize()
+    if barrier is not None:
+        barrier()
+    n_new = sess.migrate(gid_t, v_t if with_v else None)
+    torch.cuda.synchronize()
+    exp = migrate(homes, case.L, case.grid)
+    for l in range(sess.n_local):
+        r = sess.first_rank + l
+        g, x, v = exp[r]
+        assert n_new[l] == g.size, (r, n_new[l], g.size)
+        np.testing.assert_array_equal(gid_t[l][: g.size].cpu().numpy(), g.astype(np.int32))
+        np.testing.assert_array_equal(bits(sess.x[l][: g.size].cpu().numpy()), bits(x), err_msg=f"x rank {r}")
+        if with_v:
+            np.testing.assert_array_equal(bits(v_t[l][: g.size].cpu().numpy()), bits(v), err_msg=f"v rank {r}")
+        st2 = c2.states[r]
+        np.testing.assert_array_equal(g, st2.gid[: st2.n_home])  # = a fresh decomposition
+    run_gpu_case(c2, sess, steps=steps, barrier=barrier)
+    return True

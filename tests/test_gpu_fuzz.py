@@ -32,7 +32,7 @@ class FuzzCase:
         return s.x[: s.n_home]
 
 
-@pytest.mark.parametrize("proto", [0, 1 << 4, 1 << 5], ids=["ll", "paper", "ce"])
+@pytest.mark.parametrize("proto", [0, 1 << 4, (1 << 4) | (1 << 7) | (1 << 8), 1 << 5], ids=["ll", "paper", "paper_tma", "ce"])
 @pytest.mark.parametrize("seed", range(24))
 def test_fuzz_parity(seed, proto):
     from paper_2509_21527_b200.session import HaloSession

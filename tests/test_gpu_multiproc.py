@@ -51,6 +51,7 @@ def _worker(rank, world, port, cases, out):
 
 PAPER = 1 << 4
 CE = 1 << 5
+TMA = (1 << 7) | (1 << 8)  # HALO_F_TMA_STORE | HALO_F_TMA_GET
 CASES = [  # (config, seed, forces, flags, layout, steps); flags 0 = LL protocol
     ("C1", 1, "int", 0, 3, 2),
     ("W3", 1, "int", 0, 3, 1),
@@ -64,6 +65,8 @@ CASES = [  # (config, seed, forces, flags, layout, steps); flags 0 = LL protocol
     ("C3", 2, "normal", PAPER | 4, 3, 2),   # + HALO_F_GPU_FENCE (paper's exact fence scheme)
     ("C5", 1, "normal", PAPER, 3, 2),
     ("C3", 3, "int", PAPER | 1, 3, 2),      # + HALO_F_ATOMIC_UNPACK, integer forces: exact
+    ("C3", 1, "normal", PAPER | TMA, 3, 2),  # + TMA put of x / TMA get of f over NVLink (Alg. 3, Alg. 6)
+    ("T2P", 2, "int", PAPER | TMA, 4, 2),
     ("C1", 1, "int", CE, 3, 2),             # copy-engine path
     ("C3", 1, "normal", CE, 3, 3),
     ("C5", 2, "int", CE, 3, 2),
@@ -159,3 +162,48 @@ def _nranks(name):
     from tests.parity_common import load_system
     g = load_system(name, 1)[2]
     return g[0] * g[1] * g[2]
+
+
+def _worker_migrate(rank, world, port, cases, out):
+    """halo_migrate across processes (f2): rows leave through the peers' staging
+    areas over NVLink; then the new maps and both halos vs the oracle."""
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2509_21527_b200.session import HaloSession
+        from tests.parity_common import Case, moved_case, run_gpu_migrate
+        for (name, seed, flags, layout) in cases:
+            case = Case(name, seed=seed, force_kind="int", layout=layout)
+            if case.nranks % world:
+                continue
+            Xm, V, c2 = moved_case(case, seed)
+            cap = max(case.capacity, c2.capacity) + 64
+            sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout, capacity=cap,
+                               device=rank, flags=flags, nprocs=world, proc=rank, timeout_s=10.0)
+            run_gpu_migrate(case, c2, Xm, V, sess, barrier=dist.barrier)
+            dist.barrier()
+            sess.destroy()
+            dist.barrier()
+        out[rank] = "ok"
+        dist.destroy_process_group()
+    except Exception:
+        out[rank] = traceback.format_exc()
+
+
+MIGRATE_CASES = [("C1", 1, 0, 3), ("C3", 2, 0, 4), ("T2P", 1, 0, 3), ("C2", 3, PAPER, 3)]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multiprocess_migrate(world):
+    if _ndev() < world:
+        pytest.skip(f"needs {world} GPUs")
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker_migrate, args=(world, port, MIGRATE_CASES, out), nprocs=world, join=True)
+        out = dict(out)
+    for r in range(world):
+        assert out.get(r) == "ok", out.get(r)

@@ -14,7 +14,10 @@ pytestmark = pytest.mark.gpu
 
 PAPER = 1 << 4  # HALO_F_PAPER_FLAGS: the paper's per-pulse flag protocol; 0 = LL protocol (default)
 CE = 1 << 5  # HALO_F_CE_PATH: copy-engine path
-PROTOS = [pytest.param(0, id="ll"), pytest.param(PAPER, id="paper"), pytest.param(CE, id="ce")]
+TMA_STORE, TMA_GET = 1 << 7, 1 << 8  # the paper's TMA put of x (Alg. 3) / receiver-driven TMA get of f (Alg. 6)
+TMA = PAPER | TMA_STORE | TMA_GET
+PROTOS = [pytest.param(0, id="ll"), pytest.param(PAPER, id="paper"), pytest.param(TMA, id="paper_tma"),
+          pytest.param(CE, id="ce")]
 
 
 def session_for(case, flags=0, layout=None, capacity=None):
@@ -233,6 +236,32 @@ def test_errors():
         sess.exchange_f(accumulate=False)
     assert e.value.status == 8
     sess.destroy()
+
+
+@pytest.mark.parametrize("flags", [PAPER | TMA_STORE, PAPER | TMA_GET, PAPER | TMA_GET | 1],
+                         ids=["tma_put", "tma_get", "tma_get_atomic"])
+@pytest.mark.parametrize("name", ["W3", "T3D", "T2P", "C5", "C3"])
+def test_parity_tma_variants(name, flags):
+    """The paper's NVLink transports one at a time: TMA put of x only,
+    TMA get of f only (deterministic and atomic unpack; integer forces make the
+    atomic sums exact), float3 rows whose 12-B pitch leaves chunk ends unaligned."""
+    case = Case(name, seed=1, force_kind="int")
+    sess = session_for(case, flags=flags)
+    run_gpu_case(case, sess, steps=3)
+    sess.destroy()
+    case4 = Case(name, seed=2, layout=4, force_kind="int")
+    sess = session_for(case4, flags=flags, layout=4)
+    run_gpu_case(case4, sess, steps=2)
+    sess.destroy()
+
+
+def test_tma_flags_need_paper_protocol():
+    from paper_2509_21527_b200 import HaloError
+    case = Case("C1", seed=1)
+    for flags in (TMA_STORE, TMA_GET, CE | PAPER | TMA_GET):
+        with pytest.raises(HaloError) as e:
+            session_for(case, flags=flags)
+        assert e.value.status == 8
 
 
 @pytest.mark.parametrize("proto", PROTOS)
