@@ -175,6 +175,7 @@ def run_fused(args, rank, world, local):
     homes = assign_home(X, c.L, c.grid)
     cap = int(max(len(h) for h in homes) * 2.2) + 4096
     flags = (HALO_F_TIMERS if args.timers else 0) | PROTO_FLAGS[args.proto] | ((1 << 6) if args.l2_persist else 0)
+    flags |= (1 << 9) if args.zones == "rounded" else 0  # HALO_F_ROUNDED_ZONES (R31)
     sess = HaloSession(c.grid, c.L, c.rc, c.pulses, layout=args.layout, capacity=cap, device=local, flags=flags,
                        nprocs=world, proc=rank, timeout_s=20.0)
     first, nl = sess.first_rank, sess.n_local
@@ -331,9 +332,8 @@ def run_fused(args, rank, world, local):
         barrier()
         if rank == 0:
             peer = sess.first_rank + sess.n_local
-            area = (2 * P * cap * W * 8) // 16 * 16  # LL receive areas of the peer's scratch
+            # the probe writes into the peer's scratch from its LL areas on (>= 8 MiB at any capacity)
             for name, nb in (("8MiB", 8 << 20), ("1MiB", 1 << 20), ("64KiB", 64 << 10)):
-                nb = min(nb, area)
                 bw[name] = {"bytes": nb,
                             "sm_gbs": round(sess.halo.floor_bandwidth(peer, nb, mode=0, iters=50), 1),
                             "ce_gbs": round(sess.halo.floor_bandwidth(peer, nb, mode=1, iters=50), 1)}
@@ -376,7 +376,7 @@ def run_fused(args, rank, world, local):
         "warmup": args.warmup, "ms_per_step": round(res["step"] / 1e3, 6), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(workload_desc(c, world, W), parallelism=f"spatial DD {c.grid[0]}x{c.grid[1]}x{c.grid[2]}",
-                       protocol=args.proto, plan_in_l2=("persisting (HALO_F_L2_PERSIST)" if args.l2_persist
+                       protocol=args.proto, zones=args.zones, plan_in_l2=("persisting (HALO_F_L2_PERSIST)" if args.l2_persist
                                                         else "flushed with everything else"),
                        mode=("eager, one exchange_x + one exchange_f launch per GPU per step" if args.proto != "ce"
                              else "eager, copy-engine path: per pulse pack + cudaMemcpyAsync + flag kernels")),
@@ -599,6 +599,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-floors", action="store_true", help="skip the latency/bandwidth/launch floor probes")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--zones", default="slab", choices=("slab", "rounded"),
+                    help="import zones: slab (box-shaped, default) or GROMACS-style rounded (HALO_F_ROUNDED_ZONES)")
     ap.add_argument("--no-ns", action="store_true", help="skip the NS-step (halo_migrate + halo_set_maps) timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -100,7 +100,12 @@ typedef enum {
                                            scatter-adds it (same order, same bits as the push).  The reader then
                                            acks each slice (one flag per pulse), and an exchange_f launch
                                            completes only after its slices were read, so f may be overwritten
-                                           once the stream passes exchange_f (DESIGN R26).  f is peer-mapped. */
+                                           once the stream passes exchange_f (DESIGN R28).  f is peer-mapped. */
+#define HALO_F_ROUNDED_ZONES  (1u << 9) /* halo_set_maps: GROMACS-style rounded zones (SURVEY f2 variant, R31):
+                                           a row beyond this rank's upper face in another dim is sent only if
+                                           its float64 distance to the receiver's cell, dd^2 + sum (x_d' -
+                                           b_d'[c_d'+1])^2 over the dims it lies beyond, is < rc^2; default: the
+                                           slab criterion (box-shaped zones, R2).  Fewer halo rows in 2D/3D. */
 
 typedef struct {
   int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */

@@ -132,11 +132,17 @@ class RankState:
     pulses: list
 
 
-def decompose(X, L, rc, grid, pulses, W=None):
+def decompose(X, L, rc, grid, pulses, W=None, rounded=False):
     """Home assignment + coordinate halo (maps built on the way), serial.
 
     X: [N, 3] float32 global positions in [0, L).  W: optional [N] float32 w
     component (float4 layout; copied, never shifted, R25).
+    rounded: GROMACS-style rounded zones (R31, SURVEY §8(f) f2 variant): a
+    candidate that passes the slab test and lies beyond this rank's upper face
+    in some other dim d' is sent only if its squared distance to the RECEIVER's
+    cell, dd^2 + sum_{d' != d} max(0, x_d' - b_d'[c_d'+1])^2 (float64, dims
+    ascending), is < rc^2 (the eighth-shell zone with rounded edges/corners,
+    Hess2008 via P:143).
     Returns the list of RankState, one per rank.
     """
     check_geometry(L, rc, grid, pulses)
@@ -181,7 +187,19 @@ def decompose(X, L, rc, grid, pulses, W=None):
                 prev = st.pulses[p - 1]
                 cand = np.arange(prev.atom_offset, prev.atom_offset + prev.recv_size, dtype=np.int64)
             # selection: float64(x_d) - b_d[c_d] < float64(rc), strict (R2, R3)
-            sel = (st.x[cand, d].astype(np.float64) - b[d][c[d]]) < rc64
+            dd = st.x[cand, d].astype(np.float64) - b[d][c[d]]
+            sel = dd < rc64
+            if rounded:  # R31: distance to the receiver's cell box
+                r2 = dd * dd
+                beyond = np.zeros(cand.size, dtype=bool)
+                for d2 in range(3):
+                    if d2 == d:
+                        continue
+                    t = st.x[cand, d2].astype(np.float64) - b[d2][c[d2] + 1]
+                    pos = t > 0.0
+                    r2 = np.where(pos, r2 + t * t, r2)
+                    beyond |= pos
+                sel &= ~beyond | (r2 < rc64 * rc64)
             mp = cand[sel].astype(np.int32)  # ascending local row order (R11)
             lower = list(c)
             lower[d] = (c[d] - 1) % grid[d]

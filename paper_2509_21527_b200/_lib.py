@@ -23,6 +23,7 @@ HALO_F_CE_PATH = 1 << 5
 HALO_F_L2_PERSIST = 1 << 6
 HALO_F_TMA_STORE = 1 << 7
 HALO_F_TMA_GET = 1 << 8
+HALO_F_ROUNDED_ZONES = 1 << 9
 HALO_MAX_PULSES = 6
 
 # every symbol include/halo.h declares (checked by tests/test_abi.py)

@@ -288,6 +288,8 @@ struct SelParams {
   const double* b_lo;       // [n_local] lower plane b_d[c_d] of the pulse's dim
   const double* home_lo;    // [n_local][3] (home check; nullptr = skip)
   const double* home_hi;    // [n_local][3]
+  const double* b_up;       // [n_local][3] upper planes b_d[c_d+1]: rounded zones (R31); nullptr = slab
+  double rc2;               // float64(rc)^2 (R31)
   int decomposed_mask;      // bit d set iff grid[d] > 1
   int map_stride;
   int layout;

@@ -402,8 +402,25 @@ __global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelPara
     const int i = t0 + threadIdx.x;
     bool sel = false;
     if (i < c1) {
-      const double v = (double)rd.x[(size_t)i * S.layout + S.dim];
-      sel = __dsub_rn(v, blo) < S.rc;
+      const float* row = rd.x + (size_t)i * S.layout;
+      const double dd = __dsub_rn((double)row[S.dim], blo);
+      sel = dd < S.rc;
+      if (sel && S.b_up != nullptr) {
+        // rounded zones (R31): a row beyond this rank's upper face in another dim
+        // is sent only if its distance to the receiver's cell is < rc (fixed op
+        // order, no FMA contraction: the oracle's float64 ops)
+        double r2 = __dmul_rn(dd, dd);
+        bool beyond = false;
+        for (int d2 = 0; d2 < 3; ++d2) {
+          if (d2 == S.dim) continue;
+          const double t = __dsub_rn((double)row[d2], S.b_up[3 * lr + d2]);
+          if (t > 0.0) {
+            r2 = __dadd_rn(r2, __dmul_rn(t, t));
+            beyond = true;
+          }
+        }
+        sel = !beyond || r2 < S.rc2;
+      }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, sel);
     if (lane == 0) s_cnt[warp] = __popc(bal);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -242,7 +243,9 @@ static ScratchLayout scratch_layout(int P, int capacity, int layout) {
             2 * (size_t)P * L.ll_stride * sizeof(uint64_t) + (size_t)P * L.fsp_slots * 6 * sizeof(uint64_t);
   // halo_migrate staging-out and staging-in: x | v | gid rows, capacity each
   L.mig_off = align_up(L.total, 256);
-  L.mig_stage = align_up((size_t)capacity * (2 * layout + 1) * sizeof(float), 256);
+  // (at least 4 MiB each: with the LL areas before them they also give halo_floor_bandwidth
+  // a peer-mapped area of >= 8 MiB at any capacity)
+  L.mig_stage = std::max(align_up((size_t)capacity * (2 * layout + 1) * sizeof(float), 256), (size_t)4 << 20);
   L.total = L.mig_off + 2 * L.mig_stage;
   return L;
 }
@@ -1113,12 +1116,31 @@ static halo_status ce_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, 
 }
 
 // Shared driver of halo_set_maps / halo_set_maps_explicit.
+// HALO_PROFILE=1: host wall time of the set_maps phases on stderr (NS-step cost study).
+struct PhaseTimer {
+  bool on = getenv("HALO_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::string acc;
+  void lap(const char* name) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    char buf[96];
+    snprintf(buf, sizeof buf, " %s=%.0f", name, std::chrono::duration<double, std::micro>(now - t).count());
+    acc += buf;
+    t = now;
+  }
+  void print(int rank) const {
+    if (on) fprintf(stderr, "[halo_profile rank %d set_maps us]%s\n", rank, acc.c_str());
+  }
+};
+
 static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* send_sizes, const int* const* maps,
                                  cudaStream_t st) {
   if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "register buffers and import peers first");
   CK(cudaSetDevice(ctx->cfg.device));
   halo_status s = check_err_word(ctx);
   if (s != HALO_OK) return s;
+  PhaseTimer prof;
   const int L = ctx->n_local, P = ctx->P, W = ctx->W;
   ctx->maps_ready = false;
   ctx->x_done = false;
@@ -1225,11 +1247,14 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
       const bool check = (p == 0) && !(ctx->cfg.flags & HALO_F_NO_HOME_CHECK);
       S.home_lo = check ? reinterpret_cast<const double*>(sm + 4096) : nullptr;
       S.home_hi = check ? reinterpret_cast<const double*>(sm + 8192) : nullptr;
+      S.b_up = (ctx->cfg.flags & HALO_F_ROUNDED_ZONES) ? reinterpret_cast<const double*>(sm + 8192) : nullptr;
+      S.rc2 = S.rc * S.rc;
       S.decomposed_mask = (ctx->cfg.grid[0] > 1) | ((ctx->cfg.grid[1] > 1) << 1) | ((ctx->cfg.grid[2] > 1) << 2);
       S.map_stride = (int)ctx->map_stride;
       S.layout = W;
       CK(launch_select(S, L, st));
     }
+    prof.lap("select");
     // handshake with the neighbours (device flags)
     HsParams H{};
     H.ctrl = ctx->ctrl;
@@ -1250,6 +1275,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
     if ((s = check_err_word(ctx)) != HALO_OK) return s;
     if ((s = pull_maps(ctx, p, st)) != HALO_OK) return s;
+    prof.lap("handshake+pull");
     // exchange the coordinates of this pulse now: pulse p+1 forwards them
     for (int l = 0; l < L; ++l)
       for (int q = 0; q <= p; ++q) fill_pulse_dev(ctx, l, q);
@@ -1271,6 +1297,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     CK(cudaStreamSynchronize(st));
     if ((s = check_err_word(ctx)) != HALO_OK) return s;
   }
+  prof.lap("x_pulses");
   // error agreement over all ranks
   StatusParams SP{};
   SP.ctrl = ctx->ctrl;
@@ -1303,15 +1330,18 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     while (R < kMaxItemRows && rows / R > 2 * ctas) R *= 2;
     ctx->item_rows = R;
   }
+  prof.lap("status");
   // final plan: all pulses
   for (int l = 0; l < L; ++l)
     for (int p = 0; p < P; ++p) fill_pulse_dev(ctx, l, p);
   if (ctx->ll) {
     if ((s = build_csr(ctx, st)) != HALO_OK) return s;
+    prof.lap("csr");
     build_x_items_ll(ctx, 0, P);
     build_f_items_ll(ctx);
     build_xrec(ctx);
     if ((s = build_grec(ctx)) != HALO_OK) return s;
+    prof.lap("records");
   } else {
     ctx->h_xrec.clear();
     ctx->h_grec.clear();
@@ -1322,6 +1352,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   }
   fill_rank_dev(ctx);
   if ((s = upload_plan(ctx)) != HALO_OK) return s;
+  prof.lap("upload");
   if (ctx->ce && (s = build_ce(ctx)) != HALO_OK) return s;
   ctx->l2win = cudaAccessPolicyWindow{};
   if ((ctx->cfg.flags & HALO_F_L2_PERSIST) && ctx->ll) {
@@ -1340,6 +1371,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     ctx->l2win.hitProp = cudaAccessPropertyPersisting;
     ctx->l2win.missProp = cudaAccessPropertyStreaming;
   }
+  prof.lap("plan");
+  prof.print(ctx->first_rank);
   ctx->maps_ready = true;
   ctx->x_done = true;  // set_maps exchanged every pulse's coordinates
   return HALO_OK;
@@ -1734,10 +1767,13 @@ halo_status halo_floor_bandwidth(halo_ctx* ctx, int peer_rank, size_t bytes, int
   if (!ctx || peer_rank < 0 || peer_rank >= ctx->nranks || iters <= 0 || !gbs || (mode != 0 && mode != 1))
     return HALO_ERR_ARG;
   if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
-  // the coordinate + force LL receive areas of the peer's scratch (2 * P slots)
-  const size_t area = 2 * (size_t)ctx->P * ctx->ll_stride * sizeof(uint64_t);
+  // the peer's scratch from its coordinate LL receive area to the end (LL areas,
+  // shift-force slots, migration staging: >= 8 MiB, scratch_layout)
+  const size_t xll_off = kHdrBytes + (size_t)ctx->P * ctx->map_stride * sizeof(int32_t) +
+                         (size_t)ctx->P * ctx->fbuf_stride * sizeof(float);
+  const size_t area = ctx->scratch_bytes - xll_off;
   bytes = bytes / 16 * 16;
-  if (bytes == 0 || bytes > area) return fail(ctx, HALO_ERR_ARG, "bytes must be in [16, LL receive area]");
+  if (bytes == 0 || bytes > area) return fail(ctx, HALO_ERR_ARG, "bytes must be in [16, probe area]");
   CK(cudaSetDevice(ctx->cfg.device));
   const int me = ctx->first_rank;
   char* src = reinterpret_cast<char*>(ctx->xll_of(me));

@@ -43,10 +43,10 @@ def bits(a):
 class Case:
     """Oracle side of one parity case."""
 
-    def __init__(self, name, seed=1, layout=3, force_kind="int"):
-        self.name, self.seed, self.layout = name, seed, layout
+    def __init__(self, name, seed=1, layout=3, force_kind="int", rounded=False):
+        self.name, self.seed, self.layout, self.rounded = name, seed, layout, rounded
         self.L, self.rc, self.grid, self.pulses, self.X, self.W = load_system(name, seed, layout)
-        self.states = decompose(self.X, self.L, self.rc, self.grid, self.pulses, W=self.W)
+        self.states = decompose(self.X, self.L, self.rc, self.grid, self.pulses, W=self.W, rounded=rounded)
         self.nranks = len(self.states)
         self.capacity = max(max(s.x.shape[0] for s in self.states), 1) + 64
         mk = forces_int if force_kind == "int" else forces_normal
@@ -150,7 +150,7 @@ def moved_case(case: Case, seed: int):
     c2.__dict__.update(case.__dict__)
     c2.__dict__.pop("_absum", None)
     c2.X = Xw
-    c2.states = decompose(Xw, case.L, case.rc, case.grid, case.pulses, W=case.W)
+    c2.states = decompose(Xw, case.L, case.rc, case.grid, case.pulses, W=case.W, rounded=case.rounded)
     c2.capacity = max(max(s.x.shape[0] for s in c2.states), 1) + 64
     c2.F = [forces_int(s.x.shape[0], 77 + s.rank, width=case.layout) for s in c2.states]
     c2.Fo, c2.fshift = force_halo(c2.states, [f.copy() for f in c2.F])

@@ -54,6 +54,35 @@ def direct_gather(X, L, rc, grid, r, eps):
     return inner, outer
 
 
+def direct_gather_rounded(X, L, rc, grid, r, eps):
+    """As direct_gather for the rounded zones (R31): an image belongs to rank r's
+    import zone iff it lies at or above the cell's lower corner in every decomposed
+    dim and its Euclidean distance to the cell box is < rc (inner: < rc - eps,
+    outer: < rc + eps, lower faces widened by eps)."""
+    X64 = np.asarray(X, dtype=np.float64)
+    Lf = np.array([float(np.float32(v)) for v in L])
+    rc = float(np.float32(rc))
+    lo, hi = cell_bounds(L, grid, rank_cell(r, grid))
+    dec = [d for d in range(3) if grid[d] > 1]
+    inner, outer = set(), set()
+    for s in itertools.product(*[(0, 1) if d in dec else (0,) for d in range(3)]):
+        Y = X64 + np.array(s, dtype=np.float64) * Lf
+        above_in = np.ones(X.shape[0], bool)
+        above_out = np.ones(X.shape[0], bool)
+        dist2 = np.zeros(X.shape[0])
+        for d in dec:
+            above_in &= Y[:, d] >= lo[d]
+            above_out &= Y[:, d] >= lo[d] - eps
+            ex = np.maximum(Y[:, d] - hi[d], 0.0)
+            dist2 += ex * ex
+        dist = np.sqrt(dist2)
+        for g in np.nonzero(above_in & (dist < rc - eps))[0]:
+            inner.add((int(g), s))
+        for g in np.nonzero(above_out & (dist < rc + eps))[0]:
+            outer.add((int(g), s))
+    return inner, outer
+
+
 def close_pairs(X, L, rc, eps):
     """All pairs (i, j, n) with minimum-image distance < rc - eps, n = integer shift of j."""
     X64 = np.asarray(X, dtype=np.float64)

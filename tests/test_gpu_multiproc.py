@@ -34,7 +34,7 @@ def _worker(rank, world, port, cases, out):
         from paper_2509_21527_b200.session import HaloSession
         from tests.parity_common import Case, run_gpu_case
         for (name, seed, kind, flags, layout, steps) in cases:
-            case = Case(name, seed=seed, force_kind=kind, layout=layout)
+            case = Case(name, seed=seed, force_kind=kind, layout=layout, rounded=bool(flags & ROUNDED))
             if case.nranks % world:
                 continue
             sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout, capacity=case.capacity,
@@ -52,6 +52,7 @@ def _worker(rank, world, port, cases, out):
 PAPER = 1 << 4
 CE = 1 << 5
 TMA = (1 << 7) | (1 << 8)  # HALO_F_TMA_STORE | HALO_F_TMA_GET
+ROUNDED = 1 << 9  # HALO_F_ROUNDED_ZONES
 CASES = [  # (config, seed, forces, flags, layout, steps); flags 0 = LL protocol
     ("C1", 1, "int", 0, 3, 2),
     ("W3", 1, "int", 0, 3, 1),
@@ -67,6 +68,8 @@ CASES = [  # (config, seed, forces, flags, layout, steps); flags 0 = LL protocol
     ("C3", 3, "int", PAPER | 1, 3, 2),      # + HALO_F_ATOMIC_UNPACK, integer forces: exact
     ("C3", 1, "normal", PAPER | TMA, 3, 2),  # + TMA put of x / TMA get of f over NVLink (Alg. 3, Alg. 6)
     ("T2P", 2, "int", PAPER | TMA, 4, 2),
+    ("C3", 2, "int", ROUNDED, 3, 2),          # rounded zones (R31), LL protocol
+    ("C2", 1, "normal", PAPER | ROUNDED, 4, 2),
     ("C1", 1, "int", CE, 3, 2),             # copy-engine path
     ("C3", 1, "normal", CE, 3, 3),
     ("C5", 2, "int", CE, 3, 2),

@@ -255,6 +255,21 @@ def test_parity_tma_variants(name, flags):
     sess.destroy()
 
 
+ROUNDED = 1 << 9  # HALO_F_ROUNDED_ZONES (R31)
+
+
+@pytest.mark.parametrize("proto", PROTOS)
+@pytest.mark.parametrize("name,layout", [("W2", 3), ("T3D", 3), ("T2P", 4), ("T2D", 3), ("C2", 3), ("C5", 3),
+                                         ("C3", 4)])
+def test_parity_rounded_zones(name, layout, proto):
+    """GROMACS-style rounded zones (SURVEY f2 variant): maps, halo x and forces
+    bit-exact vs the oracle's rounded decomposition (pinned by Z1-Z3)."""
+    case = Case(name, seed=2, layout=layout, force_kind="int", rounded=True)
+    sess = session_for(case, flags=proto | ROUNDED, layout=layout)
+    run_gpu_case(case, sess, steps=2)
+    sess.destroy()
+
+
 def test_tma_flags_need_paper_protocol():
     from paper_2509_21527_b200 import HaloError
     case = Case("C1", seed=1)
