@@ -29,7 +29,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 # HALO_F_PAPER_FLAGS (+ HALO_F_TMA_STORE | HALO_F_TMA_GET: the paper's TMA put / get), HALO_F_CE_PATH
-PROTO_FLAGS = {"ll": 0, "paper": 1 << 4, "paper_tma": (1 << 4) | (1 << 7) | (1 << 8), "ce": 1 << 5}
+PROTO_FLAGS = {"ll": 0, "paper": 1 << 4, "paper_tma": (1 << 4) | (1 << 7) | (1 << 8), "ce": 1 << 5,
+               "auto": 1 << 10}  # HALO_F_AUTO_TRANSPORT: LL or copy engine by pulse size, per NS epoch
 METRIC = "x+f halo exchange us/step (max over ranks); achieved NVLink GB/s vs 900"
 UNIT = "us/step"
 SEED = 2509
@@ -177,10 +178,11 @@ def run_fused(args, rank, world, local):
     flags = (HALO_F_TIMERS if args.timers else 0) | PROTO_FLAGS[args.proto] | ((1 << 6) if args.l2_persist else 0)
     flags |= (1 << 9) if args.zones == "rounded" else 0  # HALO_F_ROUNDED_ZONES (R31)
     sess = HaloSession(c.grid, c.L, c.rc, c.pulses, layout=args.layout, capacity=cap, device=local, flags=flags,
-                       nprocs=world, proc=rank, timeout_s=20.0)
+                       nprocs=world, proc=rank, timeout_s=20.0, pme_rank=0 if args.pme else None)
     first, nl = sess.first_rank, sess.n_local
     sess.load_home([X[homes[first + l]] for l in range(nl)])
     sess.set_maps()
+    transport = sess.halo.transport()  # --proto auto: the one set_maps chose
     lay = [sess.layout_of(l) for l in range(nl)]
     P = sess.npulse
     W = args.layout
@@ -376,9 +378,9 @@ def run_fused(args, rank, world, local):
         "warmup": args.warmup, "ms_per_step": round(res["step"] / 1e3, 6), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(workload_desc(c, world, W), parallelism=f"spatial DD {c.grid[0]}x{c.grid[1]}x{c.grid[2]}",
-                       protocol=args.proto, zones=args.zones, plan_in_l2=("persisting (HALO_F_L2_PERSIST)" if args.l2_persist
+                       protocol=args.proto, transport=transport, zones=args.zones, plan_in_l2=("persisting (HALO_F_L2_PERSIST)" if args.l2_persist
                                                         else "flushed with everything else"),
-                       mode=("eager, one exchange_x + one exchange_f launch per GPU per step" if args.proto != "ce"
+                       mode=("eager, one exchange_x + one exchange_f launch per GPU per step" if transport != "ce"
                              else "eager, copy-engine path: per pulse pack + cudaMemcpyAsync + flag kernels")),
         "x_us": round(res["x"], 3), "f_us": round(res["f"], 3), "step_median_us": round(res["step_median"], 3),
         "step_percentiles_us": {"p90": round(res["step_p90"], 3), "p99": round(res["step_p99"], 3),
@@ -391,7 +393,7 @@ def run_fused(args, rank, world, local):
         "clocks": sampler.summary(),
         "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
                 "d2h_bytes_per_step": int(d2h) * world, "path": "halo_step_host (C ABI, pinned host buffers)"},
-        "gpu_launches": (2 if args.proto != "ce" else 4 * P) * K * world,
+        "gpu_launches": (2 if transport != "ce" else 4 * P) * K * world,
         "roofline": roof,
         "nvlink": {"bytes_per_step_per_gpu_per_direction": int(nvl_bytes),
                    "achieved_gbs": round(nvl_bytes / (res["step"] * 1e-6) / 1e9, 3) if nvl_bytes else 0.0,
@@ -432,6 +434,8 @@ def run_fused(args, rank, world, local):
         roof["latency"] = {"floor_us": round(fl2, 3), "frac": round(fl2 / res["step"], 4),
                            "definition": "2*P*t0 + (x+f NVLink bytes per direction)/BW_peer (measured SM peer-store GB/s, 8 MiB) "
                                          "+ 2 launches (eager)"}
+    if args.pme:
+        out["pme"] = pme_timing(sess, K, args.warmup, flush)
     if not args.no_ns:
         out["ns_step"] = ns_step_timing(sess, c, X, homes, dev)
     if world == 1 and rank == 0 and not args.no_cpu:
@@ -441,6 +445,31 @@ def run_fused(args, rank, world, local):
                                          f"steps (fixed-map x halo + force halo), numpy single thread"}
     sess.destroy()
     return out
+
+
+def pme_timing(sess, K, warmup, flush):
+    """PP <-> PME redistribution, PME task on DD rank 0's GPU: per
+    step halo_pme_send_x + halo_pme_recv_f (no PME compute in between), L2 flushed
+    before each step, CUDA events on the stream, mean per rank, max over ranks."""
+    import torch
+    n_total, _ = sess.pme_setup()
+    st = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for i in range(warmup + K):
+        flush.zero_()
+        if i >= warmup:
+            ev[i - warmup][0].record(st)
+        sess.pme_send_x()
+        sess.pme_recv_f()
+        if i >= warmup:
+            ev[i - warmup][1].record(st)
+    torch.cuda.synchronize()
+    us = statistics.mean(a.elapsed_time(b) * 1e3 for a, b in ev)
+    W = sess.layout
+    return {"us_per_step": round(max_over_ranks(us), 3), "rows": int(n_total),
+            "nvlink_bytes_per_step": int(n_total * W * 4 * 2), "pme_rank": 0,
+            "note": "halo_pme_send_x + halo_pme_recv_f per step (every DD rank's home x to the PME GPU, "
+                    "force slices back), L2 flushed before each step; not in value"}
 
 
 def ns_step_timing(sess, c, X, homes, dev, reps=3):
@@ -601,6 +630,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--zones", default="slab", choices=("slab", "rounded"),
                     help="import zones: slab (box-shaped, default) or GROMACS-style rounded (HALO_F_ROUNDED_ZONES)")
+    ap.add_argument("--pme", action="store_true", help="also time the PP<->PME redistribution (halo_pme_*)")
     ap.add_argument("--no-ns", action="store_true", help="skip the NS-step (halo_migrate + halo_set_maps) timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -106,6 +106,12 @@ typedef enum {
                                            its float64 distance to the receiver's cell, dd^2 + sum (x_d' -
                                            b_d'[c_d'+1])^2 over the dims it lies beyond, is < rc^2; default: the
                                            slab criterion (box-shaped zones, R2).  Fewer halo rows in 2D/3D. */
+#define HALO_F_AUTO_TRANSPORT (1u << 10) /* pick the transport per NS epoch by pulse size — the LL
+                                           protocol (latency regime) unless some rank's pulse sends at least
+                                           HALO_AUTO_CE_BYTES (env, default 4 MiB: the measured LL / copy-engine
+                                           crossover on B200), then the copy-engine path.  Decided
+                                           collectively in halo_set_maps (all ranks agree); results identical.
+                                           Not combinable with PAPER_FLAGS / CE_PATH / TMA_*.  */
 
 typedef struct {
   int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */
@@ -207,6 +213,48 @@ HALO_API halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* 
  * recv_off[p] = atomOffset, recv_size[p], send_size[p], remote_off[p] = where
  * this rank's pulse-p rows land on its receiver, dep_mask[p] = bit q set iff
  * map_p reads rows received in pulse q (the wait set of Alg. 4, R9). */
+/* ---- PP <-> PME coordinate / force redistribution ----
+ * The PME task runs on the GPU of DD rank `pme_rank`.  Its buffers pme_x / pme_f
+ * (rows of `layout` floats) hold the home rows of every DD rank concatenated in
+ * rank order — rank r at rows [row_off[r], row_off[r+1]) — and live in that
+ * rank's scratch (peer-mapped like the rest).  Per MD step:
+ *   halo_pme_send_x  (after the integration)  every rank's x[0:n_home) -> pme_x
+ *   ... the caller's PME kernel on the PME GPU reads pme_x, writes pme_f ...
+ *   halo_pme_recv_f  (after the PME kernel)    pme_f slices -> every rank's f[0:n_home)
+ * Same one-sided machinery as the halo: peer stores / loads over NVLink, one
+ * system-scope release flag per rank and direction, acks, 64-bit sequence numbers
+ * in device memory (graph-capturable), bounded waits. */
+
+/* Before halo_register_buffers, on every process with the same pme_rank: grows
+ * the scratch of the process hosting pme_rank by 2 * nranks * capacity rows
+ * (query halo_scratch_bytes after this call). */
+HALO_API halo_status halo_pme_reserve(halo_ctx* ctx, int pme_rank);
+
+/* COLLECTIVE, after every halo_set_maps (the home counts changed): all-gathers
+ * n_home over device flags and fixes row_off.  *n_total (optional) = sum of n_home.
+ * Host-synchronises on `stream`. */
+HALO_API halo_status halo_pme_setup(halo_ctx* ctx, void* stream, int* n_total);
+
+/* Device pointers of pme_x / pme_f on the process hosting pme_rank (NULL
+ * elsewhere); row_off (optional, host, nranks+1 ints) after halo_pme_setup. */
+HALO_API halo_status halo_pme_buffers(const halo_ctx* ctx, float** pme_x, float** pme_f, int* row_off);
+
+/* COLLECTIVE, asynchronous: every local rank stores x[0:n_home) into pme_x over
+ * NVLink and releases its flag on the PME rank; the PME process's launch
+ * completes when pme_x is complete (rows are bit-exact copies). */
+HALO_API halo_status halo_pme_send_x(halo_ctx* ctx, void* stream);
+
+/* COLLECTIVE, asynchronous: the PME process releases "pme_f ready" (its stream
+ * has run the PME force kernel); every local rank acquire-waits, then
+ * f[i] = f[i] + pme_f[row_off[r] + i] for its home rows (fp32 RNE per component;
+ * accumulate = 0 overwrites) and acks; the PME process's launch completes when
+ * every slice was read (pme_f may then be overwritten). */
+HALO_API halo_status halo_pme_recv_f(halo_ctx* ctx, int accumulate, void* stream);
+
+/* The transport the last halo_set_maps chose (HALO_F_AUTO_TRANSPORT, or fixed by the flags):
+ * 0 = LL protocol, 1 = paper protocol, 2 = copy engine. */
+HALO_API halo_status halo_transport(const halo_ctx* ctx, int* transport);
+
 HALO_API halo_status halo_get_layout(const halo_ctx* ctx, int local, int* n_home, int* n_total, int* npulse,
                             int* recv_off, int* recv_size, int* send_size, int* remote_off,
                             unsigned* dep_mask);

@@ -297,6 +297,28 @@ def migrate(homes, L, grid):
     return out
 
 
+def pme_gather(homes_x):
+    """PP -> PME coordinate redistribution ("the
+    communication of coordinates and forces to and from the PME tasks"): the PME
+    task receives the home rows of every DD rank, concatenated in rank order.
+    homes_x[r]: [n_r, W] float32.  Returns (pme_x [sum n_r, W], row_off [nranks+1])."""
+    off = [0]
+    for h in homes_x:
+        off.append(off[-1] + h.shape[0])
+    return np.concatenate(homes_x, axis=0).astype(np.float32), off
+
+
+def pme_return(f_home, pme_f, row_off, accumulate=True):
+    """PME -> PP force redistribution: rank r's home forces += its slice of pme_f
+    (rows [row_off[r], row_off[r+1])), one float32 RNE add per component
+    (accumulate=False: overwrite).  f_home[r]: [n_r, W] float32; returns new arrays."""
+    out = []
+    for r, f in enumerate(f_home):
+        sl = np.asarray(pme_f[row_off[r]: row_off[r + 1]], dtype=np.float32)
+        out.append((np.asarray(f, np.float32) + sl).astype(np.float32) if accumulate else sl.copy())
+    return out
+
+
 def coord_halo_step(states, x_home):
     """Per-step coordinate halo with the maps of the last neighbour-search step
     fixed (Alg. 3 P:252-262 with Alg. 4's forwarding, run serially pulse by

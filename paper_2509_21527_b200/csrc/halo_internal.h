@@ -4,7 +4,7 @@
 // Data layout in HBM:
 //   x, f      caller-owned, capacity rows x layout floats per DD rank
 //   scratch   caller-owned per DD rank, peer-mapped (CUDA IPC):
-//               [0, 4096)                ScratchHdr: flags written by peers
+//               [0, 8192)                ScratchHdr: flags written by peers
 //               [4096, ...)              P index maps (int32, capacity each)
 //               [..., ...)               P force receive buffers, flag protocol (capacity rows each)
 //               [..., ...)               P coordinate LL receive buffers (capacity*layout u64 units)
@@ -26,7 +26,7 @@ constexpr int kMaxP = HALO_MAX_PULSES;
 constexpr int kMaxLocal = HALO_MAX_LOCAL;
 constexpr int kMaxRanks = HALO_MAX_RANKS;
 constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
-constexpr int kHdrBytes = 4096;
+constexpr int kHdrBytes = 8192;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
 constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-force slot area)
 constexpr int kMaxItemRows = 512;      // largest work item (x items carry their map slice in shared memory)
@@ -50,6 +50,12 @@ struct __align__(128) ScratchHdr {
   uint64_t mig_cnt[kMaxRanks];  // rows source s sends here (release: its staging rows are written)
   uint64_t mig_off[kMaxRanks];  // where they start in source s's staging-out area
   uint64_t mig_ack[kMaxRanks];  // destination t has copied what this rank sent it
+  // PP <-> PME (kernels_pme.cu); pme_x_flag / pme_ack live on the PME rank:
+  uint64_t pme_nh[kMaxRanks];      // (epoch << 32) | n_home of rank t (halo_pme_setup all-gather)
+  uint64_t pme_x_flag[kMaxRanks];  // seq: rank t's home rows are in pme_x
+  uint64_t pme_ack[kMaxRanks];     // seq: rank t has read its slice of pme_f
+  uint64_t pme_f_flag;             // seq: pme_f holds this step's PME forces (written by the PME rank)
+  uint64_t pad5[15];
 };
 static_assert(sizeof(ScratchHdr) <= kHdrBytes, "ScratchHdr too large");
 
@@ -80,9 +86,15 @@ struct Ctrl {
   uint64_t trace[2][kTraceCTAs][8];
   // HALO_DEBUG & kCountNotify (pin G4): system-scope flag stores per (x/f, local rank, pulse), cumulative
   uint32_t notify[2][kMaxLocal][kMaxP];
+  // PP <-> PME (kernels_pme.cu)
+  uint64_t seq_pme_x, seq_pme_f;
+  uint32_t done_pme[2];
+  uint32_t cnt_pme[2][kMaxLocal];
+  int32_t pme_nh[kMaxLocal][kMaxRanks];   // halo_pme_setup: n_home of every rank, seen by local rank l
 };
 
-enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4 };
+enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4,
+                 kVoteCE = 256 };  // not an error: HALO_F_AUTO_TRANSPORT vote, ORed by the status exchange
 
 // ---------------------------------------------------------------- halo_migrate
 // (csrc/kernels_ns.cu).  The stencil of a rank = the distinct
@@ -316,6 +328,29 @@ struct StatusParams {
   int first_rank;
   ScratchHdr* own[kMaxLocal];
   ScratchHdr* all[kMaxRanks];       // every rank's scratch header (local or peer-mapped)
+  int* err_host;
+  uint64_t timeout_ns;
+};
+
+// PP <-> PME redistribution (halo_pme_*, kernels_pme.cu)
+struct PmeRank {
+  const float* x;           // own x (home rows sent)
+  float* f;                 // own f (home rows receive the PME forces)
+  ScratchHdr* hdr;          // own header
+  int n_home;
+  int off;                  // first row of this rank in pme_x / pme_f
+  int rank;
+  int pad;
+};
+struct PmeParams {
+  PmeRank r[kMaxLocal];
+  ScratchHdr* all_hdr[kMaxRanks];
+  ScratchHdr* pme_hdr;      // the PME rank's header (peer)
+  float* pme_x;             // the PME rank's coordinate / force buffers (peer)
+  float* pme_f;
+  Ctrl* ctrl;
+  int n_local, nranks, layout, hosts_pme, accumulate;
+  uint32_t epoch;
   int* err_host;
   uint64_t timeout_ns;
 };

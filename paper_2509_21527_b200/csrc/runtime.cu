@@ -21,6 +21,7 @@ cudaError_t launch_exchange_x(const ExParams& p, int layout, int grid, cudaStrea
 cudaError_t launch_exchange_f(const ExParams& p, int layout, int grid, cudaStream_t st);
 cudaError_t max_coresident(int layout, int* x_blocks, int* f_blocks);
 cudaError_t launch_migrate(const MigParams& M, MigCtrl* C, int max_rows, int phase, cudaStream_t st);
+cudaError_t launch_pme(const PmeParams& M, int which, int ctas_per_rank, cudaStream_t st);
 cudaError_t launch_select(const SelParams& s, int n_local, cudaStream_t st);
 cudaError_t launch_handshake(const HsParams& h, cudaStream_t st);
 cudaError_t launch_depmask(const RankDev* ranks, Ctrl* ctrl, int p, int map_stride, int n_local, cudaStream_t st);
@@ -95,6 +96,11 @@ struct halo_ctx {
   size_t map_stride = 0, fbuf_stride = 0, ll_stride = 0, fsp_slots = 0, scratch_bytes = 0;
   size_t mig_off = 0;                // halo_migrate staging: [out | in] at this scratch offset
   size_t mig_stage = 0;              // bytes of one staging area (x | v | gid rows, capacity each)
+  int pme_rank = -1;                 // halo_pme_reserve: DD rank whose scratch holds pme_x | pme_f
+  size_t pme_off = 0;                // their offset in that scratch (same layout on every rank)
+  bool pme_ready = false;            // halo_pme_setup done for the current maps
+  std::vector<int> pme_row_off;      // first pme row of every DD rank
+  int pme_total = 0;
   bool ll = true;                   // LL protocol (default) vs the paper's flag protocol
   bool ce = false;                  // copy-engine path (HALO_F_CE_PATH; set_maps uses the paper kernels)
   std::string last_error;
@@ -133,6 +139,8 @@ struct halo_ctx {
   std::vector<XRec> h_xrec;
   std::vector<int32_t> h_xmap;          // per x item: its map slice (item_rows entries)
   std::vector<char> h_xblk, h_fblk;     // item blocks [record | map slice] / [record | task records]
+  char* h_pin = nullptr;                // pinned image of the plan (one DMA per upload)
+  size_t h_pin_bytes = 0;
   char* d_xblk = nullptr;
   char* d_fblk = nullptr;
   std::vector<std::vector<std::vector<int32_t>>> h_maps;  // host copy of every local rank's maps [l][p]
@@ -181,6 +189,8 @@ struct halo_ctx {
   // counter, R17); every LL launch advances the device counter in any case
   uint64_t seq_host_x = 0, seq_host_f = 0;
   bool captured = false;
+  bool auto_tr = false;             // HALO_F_AUTO_TRANSPORT: LL or copy engine chosen at every set_maps
+  size_t auto_ce_bytes = (size_t)4 << 20;  // ... copy engine when some pulse sends >= this (HALO_AUTO_CE_BYTES)
   int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
 
   int cell(int r, int d) const {
@@ -287,6 +297,11 @@ static halo_status validate(const halo_config* c, std::string& why) {
   if (nr % c->nprocs != 0) { why = "nranks must be a multiple of nprocs"; return HALO_ERR_ARG; }
   if (nr / c->nprocs > kMaxLocal) { why = "too many ranks per process (HALO_MAX_LOCAL)"; return HALO_ERR_UNSUPPORTED; }
   if (P > kMaxP) { why = "too many pulses"; return HALO_ERR_UNSUPPORTED; }
+  if ((c->flags & HALO_F_AUTO_TRANSPORT) &&
+      (c->flags & (HALO_F_PAPER_FLAGS | HALO_F_CE_PATH | HALO_F_TMA_STORE | HALO_F_TMA_GET))) {
+    why = "HALO_F_AUTO_TRANSPORT chooses between the LL protocol and the copy engine itself";
+    return HALO_ERR_UNSUPPORTED;
+  }
   if ((c->flags & (HALO_F_TMA_STORE | HALO_F_TMA_GET)) &&
       (!(c->flags & HALO_F_PAPER_FLAGS) || (c->flags & HALO_F_CE_PATH))) {
     why = "HALO_F_TMA_STORE / HALO_F_TMA_GET are variants of the paper protocol (HALO_F_PAPER_FLAGS, no HALO_F_CE_PATH)";
@@ -350,6 +365,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   }
   ctx->ce = (cfg->flags & HALO_F_CE_PATH) != 0;
   ctx->ll = !(cfg->flags & HALO_F_PAPER_FLAGS) && !ctx->ce;
+  ctx->auto_tr = (cfg->flags & HALO_F_AUTO_TRANSPORT) != 0;
   ctx->x.assign(ctx->n_local, nullptr);
   ctx->f.assign(ctx->n_local, nullptr);
   ctx->scratch.assign(ctx->n_local, nullptr);
@@ -884,11 +900,17 @@ static halo_status upload_plan(halo_ctx* ctx) {
   const size_t ngr = align_up(std::max<size_t>(1, ctx->h_fblk.size()), a);
   const size_t nxm = 0;
   const size_t need = nr + np + nx + nf + nxr + ngr + nxm;
-  if (need > ctx->plan_bytes) {
+  if (need > ctx->plan_bytes) {  // 25% headroom: NS steps rarely grow the plan again
     if (ctx->plan) CK(cudaFree(ctx->plan));
     ctx->plan = nullptr;
-    CK(cudaMalloc(&ctx->plan, need));
-    ctx->plan_bytes = need;
+    CK(cudaMalloc(&ctx->plan, need + need / 4));
+    ctx->plan_bytes = need + need / 4;
+  }
+  if (need > ctx->h_pin_bytes) {
+    if (ctx->h_pin) CK(cudaFreeHost(ctx->h_pin));
+    ctx->h_pin = nullptr;
+    CK(cudaMallocHost(&ctx->h_pin, need + need / 4));
+    ctx->h_pin_bytes = need + need / 4;
   }
   ctx->d_ranks = reinterpret_cast<RankDev*>(ctx->plan);
   ctx->d_pulses = reinterpret_cast<PulseDev*>(ctx->plan + nr);
@@ -896,18 +918,21 @@ static halo_status upload_plan(halo_ctx* ctx) {
   ctx->d_items_f = reinterpret_cast<Item*>(ctx->plan + nr + np + nx);
   ctx->d_xblk = ctx->plan + nr + np + nx + nf;
   ctx->d_fblk = ctx->plan + nr + np + nx + nf + nxr;
-  if (!ctx->h_xblk.empty())
-    CK(cudaMemcpy(ctx->d_xblk, ctx->h_xblk.data(), ctx->h_xblk.size(), cudaMemcpyHostToDevice));
-  if (!ctx->h_fblk.empty())
-    CK(cudaMemcpy(ctx->d_fblk, ctx->h_fblk.data(), ctx->h_fblk.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->d_ranks, ctx->h_ranks.data(), sizeof(RankDev) * ctx->n_local, cudaMemcpyHostToDevice));
+  // the whole plan image in pinned memory, then one synchronous DMA (pageable
+  // copies of the MB-sized item blocks cost ms at the NS step)
+  char* img = ctx->h_pin;
+  auto put = [&](char* dev, const void* src, size_t n) {
+    if (n) memcpy(img + (dev - ctx->plan), src, n);
+  };
+  put(reinterpret_cast<char*>(ctx->d_ranks), ctx->h_ranks.data(), sizeof(RankDev) * ctx->n_local);
   if (ctx->P)
-    CK(cudaMemcpy(ctx->d_pulses, ctx->h_pulses.data(), sizeof(PulseDev) * ctx->n_local * ctx->P,
-                  cudaMemcpyHostToDevice));
-  if (!ctx->h_items_x.empty())
-    CK(cudaMemcpy(ctx->d_items_x, ctx->h_items_x.data(), sizeof(Item) * ctx->h_items_x.size(), cudaMemcpyHostToDevice));
-  if (!ctx->h_items_f.empty())
-    CK(cudaMemcpy(ctx->d_items_f, ctx->h_items_f.data(), sizeof(Item) * ctx->h_items_f.size(), cudaMemcpyHostToDevice));
+    put(reinterpret_cast<char*>(ctx->d_pulses), ctx->h_pulses.data(), sizeof(PulseDev) * ctx->n_local * ctx->P);
+  put(reinterpret_cast<char*>(ctx->d_items_x), ctx->h_items_x.data(), sizeof(Item) * ctx->h_items_x.size());
+  put(reinterpret_cast<char*>(ctx->d_items_f), ctx->h_items_f.data(), sizeof(Item) * ctx->h_items_f.size());
+  put(ctx->d_xblk, ctx->h_xblk.data(), ctx->h_xblk.size());
+  put(ctx->d_fblk, ctx->h_fblk.data(), ctx->h_fblk.size());
+  const size_t used = (size_t)(ctx->d_fblk - ctx->plan) + ctx->h_fblk.size();
+  CK(cudaMemcpy(ctx->plan, img, used, cudaMemcpyHostToDevice));
   ctx->n_items_x = (int)ctx->h_items_x.size();
   ctx->n_items_f = (int)ctx->h_items_f.size();
   return HALO_OK;
@@ -1141,7 +1166,12 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   halo_status s = check_err_word(ctx);
   if (s != HALO_OK) return s;
   PhaseTimer prof;
+  ctx->pme_ready = false;  // the home counts change: halo_pme_setup again
   const int L = ctx->n_local, P = ctx->P, W = ctx->W;
+  if (ctx->auto_tr) {  // the per-pulse exchanges below run the LL kernels; the vote decides the epoch's transport
+    ctx->ll = true;
+    ctx->ce = false;
+  }
   ctx->maps_ready = false;
   ctx->x_done = false;
   ctx->epoch++;
@@ -1298,6 +1328,21 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     if ((s = check_err_word(ctx)) != HALO_OK) return s;
   }
   prof.lap("x_pulses");
+  if (ctx->auto_tr) {
+    // HALO_F_AUTO_TRANSPORT: vote for the copy engine if one of this process's
+    // pulses is large (bandwidth regime); the status exchange ORs the votes, so
+    // every rank takes the same transport
+    size_t big = 0, thr = ctx->auto_ce_bytes;
+    if (const char* e = getenv("HALO_AUTO_CE_BYTES")) thr = (size_t)std::max(0LL, atoll(e));  // read per NS step
+    for (int i = 0; i < L * P; ++i) big = std::max(big, (size_t)ctx->send_size[i] * W * sizeof(float));
+    if (big >= thr) {
+      int32_t e[kMaxLocal];
+      CK(cudaMemcpyAsync(e, ctx->ctrl->err, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int l = 0; l < L; ++l) e[l] |= kVoteCE;
+      CK(cudaMemcpyAsync(ctx->ctrl->err, e, sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
+    }
+  }
   // error agreement over all ranks
   StatusParams SP{};
   SP.ctrl = ctx->ctrl;
@@ -1319,6 +1364,10 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   if (any & kErrCapacity) return fail(ctx, HALO_ERR_CAPACITY, "n_home + received rows exceed capacity on some rank");
   if (any & kErrGeometry) return fail(ctx, HALO_ERR_GEOMETRY, "a home atom lies outside its rank's cell");
   if (any & kErrMap) return fail(ctx, HALO_ERR_ARG, "invalid explicit map on some rank");
+  if (ctx->auto_tr && (any & kVoteCE)) {
+    ctx->ll = false;
+    ctx->ce = true;
+  }
   // work-item size: 64 rows (latency regime; swept 32-512 at C3) unless the
   // pulses are so large that a CTA would run more than ~2 items in sequence —
   // then larger items (fewer dependent record/map round trips per row)
@@ -1371,6 +1420,14 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     ctx->l2win.hitProp = cudaAccessPropertyPersisting;
     ctx->l2win.missProp = cudaAccessPropertyStreaming;
   }
+  // the LL launches take their sequence numbers by value from a host mirror: resync it
+  // with the device counters (the paper / copy-engine launches advance those too)
+  uint64_t seqs[2];
+  CK(cudaMemcpyAsync(&seqs[0], &ctx->ctrl->seq_x, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&seqs[1], &ctx->ctrl->seq_f, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->seq_host_x = seqs[0];
+  ctx->seq_host_f = seqs[1];
   prof.lap("plan");
   prof.print(ctx->first_rank);
   ctx->maps_ready = true;
@@ -1408,6 +1465,7 @@ halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gi
   cudaStream_t st = (cudaStream_t)stream;
   ctx->maps_ready = false;
   ctx->x_done = false;
+  ctx->pme_ready = false;
   ctx->epoch++;
   // stencil of every local rank: the distinct ranks of cells c + delta (R30)
   std::vector<MigRank> mr(L);
@@ -1488,6 +1546,120 @@ halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gi
   if (any & kErrCapacity) return fail(ctx, HALO_ERR_CAPACITY, "a rank would hold more home rows than capacity");
   if (any & kErrMap) return fail(ctx, HALO_ERR_ARG, "gid rows are not strictly ascending on some rank");
   for (int l = 0; l < L; ++l) n_home_out[l] = hc.in_off[l][mr[l].n_nb];
+  return HALO_OK;
+}
+
+// ------------------------------------------------------------ PP <-> PME (f4)
+halo_status halo_pme_reserve(halo_ctx* ctx, int pme_rank) {
+  if (!ctx || pme_rank < 0 || pme_rank >= ctx->nranks) return HALO_ERR_ARG;
+  if (ctx->pme_rank >= 0) return fail(ctx, HALO_ERR_STATE, "PME already reserved");
+  for (int l = 0; l < ctx->n_local; ++l)
+    if (ctx->scratch[l]) return fail(ctx, HALO_ERR_STATE, "halo_pme_reserve must precede halo_register_buffers");
+  ctx->pme_rank = pme_rank;
+  ctx->pme_off = align_up(ctx->scratch_bytes, 256);
+  const size_t area = align_up((size_t)ctx->nranks * ctx->cfg.capacity * ctx->W * sizeof(float), 256);
+  // only the process hosting pme_rank grows its scratch (the others map it)
+  if (pme_rank >= ctx->first_rank && pme_rank < ctx->first_rank + ctx->n_local) ctx->scratch_bytes = ctx->pme_off + 2 * area;
+  return HALO_OK;
+}
+
+static PmeParams pme_params(halo_ctx* ctx) {
+  PmeParams M{};
+  const size_t area = align_up((size_t)ctx->nranks * ctx->cfg.capacity * ctx->W * sizeof(float), 256);
+  char* base = ctx->peer_scratch[ctx->pme_rank] + ctx->pme_off;
+  M.pme_x = reinterpret_cast<float*>(base);
+  M.pme_f = reinterpret_cast<float*>(base + area);
+  M.pme_hdr = ctx->hdr_of(ctx->pme_rank);
+  for (int r = 0; r < ctx->nranks; ++r) M.all_hdr[r] = ctx->hdr_of(r);
+  for (int l = 0; l < ctx->n_local; ++l) {
+    const int r = ctx->first_rank + l;
+    M.r[l].x = ctx->x[l];
+    M.r[l].f = ctx->f[l];
+    M.r[l].hdr = ctx->hdr_of(r);
+    M.r[l].n_home = ctx->n_home.empty() ? 0 : ctx->n_home[l];
+    M.r[l].off = ctx->pme_row_off.empty() ? 0 : ctx->pme_row_off[r];
+    M.r[l].rank = r;
+  }
+  M.ctrl = ctx->ctrl;
+  M.n_local = ctx->n_local;
+  M.nranks = ctx->nranks;
+  M.layout = ctx->W;
+  M.hosts_pme = ctx->pme_rank >= ctx->first_rank && ctx->pme_rank < ctx->first_rank + ctx->n_local;
+  M.accumulate = 1;
+  M.epoch = ctx->epoch;
+  M.err_host = ctx->err_dev;
+  M.timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);
+  return M;
+}
+
+static int pme_ctas(halo_ctx* ctx) {
+  int mx = 0;
+  for (int l = 0; l < ctx->n_local; ++l) mx = std::max(mx, ctx->n_home[l]);
+  // ~512 rows per CTA (bandwidth regime needs the whole GPU); any grid size is safe:
+  // the PME CTA is row 0 of the grid, resident before every CTA that waits on it
+  return std::min(2048, std::max(1, (mx + 511) / 512));
+}
+
+halo_status halo_pme_setup(halo_ctx* ctx, void* stream, int* n_total) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (ctx->pme_rank < 0) return fail(ctx, HALO_ERR_STATE, "halo_pme_reserve first");
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "halo_pme_setup after halo_set_maps");
+  CK(cudaSetDevice(ctx->cfg.device));
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  ctx->epoch++;
+  ctx->pme_ready = false;
+  PmeParams M = pme_params(ctx);
+  CK(launch_pme(M, 0, 1, st));
+  std::vector<int32_t> nh(ctx->nranks);
+  CK(cudaMemcpyAsync(nh.data(), ctx->ctrl->pme_nh[0], sizeof(int32_t) * ctx->nranks, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((s = check_err_word(ctx)) != HALO_OK) return s;
+  ctx->pme_row_off.assign(ctx->nranks + 1, 0);
+  for (int r = 0; r < ctx->nranks; ++r) ctx->pme_row_off[r + 1] = ctx->pme_row_off[r] + nh[r];
+  ctx->pme_total = ctx->pme_row_off[ctx->nranks];
+  if (n_total) *n_total = ctx->pme_total;
+  ctx->pme_ready = true;
+  return HALO_OK;
+}
+
+halo_status halo_pme_buffers(const halo_ctx* ctx, float** pme_x, float** pme_f, int* row_off) {
+  if (!ctx || !pme_x || !pme_f) return HALO_ERR_ARG;
+  if (ctx->pme_rank < 0 || !ctx->peers_ready) return HALO_ERR_STATE;
+  const bool hosts = ctx->pme_rank >= ctx->first_rank && ctx->pme_rank < ctx->first_rank + ctx->n_local;
+  const size_t area = align_up((size_t)ctx->nranks * ctx->cfg.capacity * ctx->W * sizeof(float), 256);
+  char* base = hosts ? ctx->peer_scratch[ctx->pme_rank] + ctx->pme_off : nullptr;
+  *pme_x = hosts ? reinterpret_cast<float*>(base) : nullptr;
+  *pme_f = hosts ? reinterpret_cast<float*>(base + area) : nullptr;
+  if (row_off && ctx->pme_ready)
+    for (int r = 0; r <= ctx->nranks; ++r) row_off[r] = ctx->pme_row_off[r];
+  return HALO_OK;
+}
+
+halo_status halo_pme_send_x(halo_ctx* ctx, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->pme_ready || !ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "halo_pme_setup after every halo_set_maps");
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  CK(launch_pme(pme_params(ctx), 1, pme_ctas(ctx), (cudaStream_t)stream));
+  return HALO_OK;
+}
+
+halo_status halo_pme_recv_f(halo_ctx* ctx, int accumulate, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->pme_ready || !ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "halo_pme_setup after every halo_set_maps");
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  PmeParams M = pme_params(ctx);
+  M.accumulate = accumulate ? 1 : 0;
+  CK(launch_pme(M, 2, pme_ctas(ctx), (cudaStream_t)stream));
+  return HALO_OK;
+}
+
+halo_status halo_transport(const halo_ctx* ctx, int* transport) {
+  if (!ctx || !transport) return HALO_ERR_ARG;
+  *transport = ctx->ce ? 2 : (ctx->ll ? 0 : 1);
   return HALO_OK;
 }
 
@@ -1771,7 +1943,8 @@ halo_status halo_floor_bandwidth(halo_ctx* ctx, int peer_rank, size_t bytes, int
   // shift-force slots, migration staging: >= 8 MiB, scratch_layout)
   const size_t xll_off = kHdrBytes + (size_t)ctx->P * ctx->map_stride * sizeof(int32_t) +
                          (size_t)ctx->P * ctx->fbuf_stride * sizeof(float);
-  const size_t area = ctx->scratch_bytes - xll_off;
+  // (the base layout every rank shares; a PME rank's scratch is longer, halo_pme_reserve)
+  const size_t area = scratch_layout(ctx->P, ctx->cfg.capacity, ctx->W).total - xll_off;
   bytes = bytes / 16 * 16;
   if (bytes == 0 || bytes > area) return fail(ctx, HALO_ERR_ARG, "bytes must be in [16, probe area]");
   CK(cudaSetDevice(ctx->cfg.device));
@@ -1818,6 +1991,7 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->ctrl) (void)cudaFree(ctx->ctrl);
   if (ctx->d_fshift_tmp) (void)cudaFree(ctx->d_fshift_tmp);
   if (ctx->d_small) (void)cudaFree(ctx->d_small);
+  if (ctx->h_pin) (void)cudaFreeHost(ctx->h_pin);
   if (ctx->d_mig) (void)cudaFree(ctx->d_mig);
   if (ctx->d_migctrl) (void)cudaFree(ctx->d_migctrl);
   if (ctx->d_planes) (void)cudaFree(ctx->d_planes);

@@ -156,6 +156,33 @@ class Halo:
         self._ck(self.lib.halo_migrate(self.h, arr, g, vv, out, c_void_p(stream)))
         return [int(out[l]) for l in range(nl)]
 
+    # ---- PP <-> PME (halo_pme_*)
+    def pme_reserve(self, pme_rank):
+        self._ck(self.lib.halo_pme_reserve(self.h, int(pme_rank)))
+
+    def pme_setup(self, stream=0):
+        n = c_int()
+        self._ck(self.lib.halo_pme_setup(self.h, c_void_p(stream), ctypes.byref(n)))
+        return n.value
+
+    def pme_buffers(self, nranks):
+        x, f = c_void_p(), c_void_p()
+        off = (c_int * (nranks + 1))()
+        self._ck(self.lib.halo_pme_buffers(self.h, ctypes.byref(x), ctypes.byref(f), off))
+        return x.value or 0, f.value or 0, [int(v) for v in off]
+
+    def pme_send_x(self, stream=0):
+        self._ck(self.lib.halo_pme_send_x(self.h, c_void_p(stream)))
+
+    def pme_recv_f(self, accumulate=True, stream=0):
+        self._ck(self.lib.halo_pme_recv_f(self.h, int(bool(accumulate)), c_void_p(stream)))
+
+    def transport(self):
+        """Transport of the current NS epoch: 'll', 'paper' or 'ce' (HALO_F_AUTO_TRANSPORT chooses per epoch)."""
+        t = c_int()
+        self._ck(self.lib.halo_transport(self.h, ctypes.byref(t)))
+        return ("ll", "paper", "ce")[t.value]
+
     def exchange_x(self, stream=0):
         self._ck(self.lib.halo_exchange_x(self.h, c_void_p(stream)))
 

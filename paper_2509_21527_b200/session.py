@@ -36,7 +36,7 @@ class HaloSession:
     registers them, and imports the peers' IPC blobs over ``torch.distributed``."""
 
     def __init__(self, grid, box, cutoff, pulses, layout=3, capacity=1 << 16, device=0, flags=0,
-                 nprocs=1, proc=0, timeout_s=10.0, group=None):
+                 nprocs=1, proc=0, timeout_s=10.0, group=None, pme_rank=None):
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         self.halo = Halo(grid, box, cutoff, pulses, layout=layout, capacity=capacity, device=device, flags=flags,
@@ -45,6 +45,9 @@ class HaloSession:
         self.layout, self.capacity, self.nprocs, self.proc = layout, capacity, nprocs, proc
         self.first_rank, self.n_local = self.halo.local_ranks()
         self.npulse = len(self.halo.pulse_order())
+        self.pme_rank = pme_rank
+        if pme_rank is not None:  # PP <-> PME buffers in pme_rank's scratch (before registration)
+            self.halo.pme_reserve(pme_rank)
         sb = self.halo.scratch_bytes()
         # one allocation per array kind for all local ranks (views per rank, 512-B aligned rows blocks):
         # one copy resets every local rank's forces, one IPC handle covers every local rank
@@ -93,6 +96,38 @@ class HaloSession:
         self.n_home = self.halo.migrate(self.n_home, [g.data_ptr() for g in gid],
                                         [t.data_ptr() for t in v] if v is not None else None, stream=self._s(stream))
         return list(self.n_home)
+
+    # ---- PP <-> PME
+    def pme_setup(self, stream=None):
+        """After every set_maps: all-gather the home counts; returns (n_total, row_off)."""
+        n = self.halo.pme_setup(stream=self._s(stream))
+        nranks = self.grid[0] * self.grid[1] * self.grid[2]
+        _, _, off = self.halo.pme_buffers(nranks)
+        return n, off
+
+    def pme_buffers(self):
+        """(pme_x, pme_f) as float32 [nranks*capacity, layout] views of the scratch on the
+        process hosting pme_rank (None elsewhere)."""
+        nranks = self.grid[0] * self.grid[1] * self.grid[2]
+        px, pf, _ = self.halo.pme_buffers(nranks)
+        if not px:
+            return None, None
+        rows = nranks * self.capacity
+        out = []
+        for ptr in (px, pf):
+            for l in range(self.n_local):
+                base = self.scratch[l].data_ptr()
+                if base <= ptr < base + self.scratch[l].numel():
+                    o = ptr - base
+                    out.append(self.scratch[l][o: o + rows * self.layout * 4].view(torch.float32).view(rows, self.layout))
+                    break
+        return out[0], out[1]
+
+    def pme_send_x(self, stream=None):
+        self.halo.pme_send_x(stream=self._s(stream))
+
+    def pme_recv_f(self, accumulate=True, stream=None):
+        self.halo.pme_recv_f(accumulate, stream=self._s(stream))
 
     def layout_of(self, l):
         return self.halo.get_layout(l)

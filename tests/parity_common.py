@@ -201,3 +201,45 @@ def run_gpu_migrate(case: Case, c2: Case, Xm, V, sess, with_v=True, barrier=None
         np.testing.assert_array_equal(g, st2.gid[: st2.n_home])  # = a fresh decomposition
     run_gpu_case(c2, sess, steps=steps, barrier=barrier)
     return True
+
+
+def run_gpu_pme(case: Case, sess, steps=3, barrier=None):
+    """PP <-> PME redistribution vs oracle.pme_gather / pme_return,
+    bit-exact; `sess` was created with pme_rank.  Several steps (sequence numbers,
+    acks); the PME forces change every step."""
+    from oracle import pme_gather, pme_return
+    run_gpu_case(case, sess, check_forces=False, barrier=barrier)
+    n_total, off = sess.pme_setup()
+    exp_x, exp_off = pme_gather([s.x[: s.n_home] for s in case.states])
+    assert n_total == exp_x.shape[0] and list(off) == list(exp_off), (n_total, off[:4], exp_off[:4])
+    px, pf = sess.pme_buffers()
+    hosts = px is not None
+    for step in range(steps):
+        F = [forces_int(s.n_home, 300 + 10 * step + s.rank, width=case.layout) for s in case.states]
+        PF = forces_int(n_total, 900 + step, width=case.layout)
+        for l in range(sess.n_local):
+            r = sess.first_rank + l
+            sess.f[l][: case.states[r].n_home] = torch.from_numpy(F[r]).to(sess.device)
+        if hosts:
+            px[:n_total] = float("nan")  # every row must be overwritten
+        torch.cuda.synchronize()
+        if barrier is not None:
+            barrier()
+        sess.pme_send_x()
+        torch.cuda.synchronize()
+        if hosts:
+            np.testing.assert_array_equal(bits(px[:n_total].cpu().numpy()), bits(exp_x), err_msg=f"pme_x step {step}")
+            pf[:n_total] = torch.from_numpy(PF).to(sess.device)  # the PME task's forces
+            torch.cuda.synchronize()
+        acc = step != 1
+        sess.pme_recv_f(accumulate=acc)
+        torch.cuda.synchronize()
+        exp_f = pme_return(F, PF, exp_off, accumulate=acc)
+        for l in range(sess.n_local):
+            r = sess.first_rank + l
+            n = case.states[r].n_home
+            np.testing.assert_array_equal(bits(sess.f[l][:n].cpu().numpy()), bits(exp_f[r]),
+                                          err_msg=f"pme f rank {r} step {step}")
+        if barrier is not None:
+            barrier()
+    return True

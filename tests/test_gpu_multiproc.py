@@ -210,3 +210,46 @@ def test_multiprocess_migrate(world):
         out = dict(out)
     for r in range(world):
         assert out.get(r) == "ok", out.get(r)
+
+
+def _worker_pme(rank, world, port, cases, out):
+    """PP <-> PME across processes (f4): every rank's home rows to the PME rank's
+    buffer over NVLink and its force slice back."""
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2509_21527_b200.session import HaloSession
+        from tests.parity_common import Case, run_gpu_pme
+        for (name, seed, layout, pme_rank) in cases:
+            case = Case(name, seed=seed, force_kind="int", layout=layout)
+            if case.nranks % world:
+                continue
+            sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout, capacity=case.capacity,
+                               device=rank, nprocs=world, proc=rank, timeout_s=10.0, pme_rank=pme_rank)
+            run_gpu_pme(case, sess, barrier=dist.barrier)
+            dist.barrier()
+            sess.destroy()
+            dist.barrier()
+        out[rank] = "ok"
+        dist.destroy_process_group()
+    except Exception:
+        out[rank] = traceback.format_exc()
+
+
+PME_CASES = [("C1", 1, 3, 1), ("C3", 2, 4, 0), ("C2", 1, 3, 3)]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multiprocess_pme(world):
+    if _ndev() < world:
+        pytest.skip(f"needs {world} GPUs")
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker_pme, args=(world, port, PME_CASES, out), nprocs=world, join=True)
+        out = dict(out)
+    for r in range(world):
+        assert out.get(r) == "ok", out.get(r)

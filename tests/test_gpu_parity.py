@@ -426,3 +426,28 @@ def test_parity_under_concurrent_compute(proto):
             np.testing.assert_array_equal(bits(sess.f[l][:n].cpu().numpy()), bits(case.Fo[l]))
             assert np.all(np.abs(fs[l] - case.fshift[l]) <= 1e-10 * case.fabs_total)
     sess.destroy()
+
+
+def test_auto_transport_switches_per_epoch(monkeypatch):
+    """HALO_F_AUTO_TRANSPORT: set_maps votes LL or copy engine by pulse
+    size (threshold HALO_AUTO_CE_BYTES, read at every set_maps); switching between
+    NS epochs in both directions keeps the results bit-exact (sequence numbers
+    stay consistent across transports)."""
+    AUTO = 1 << 10
+    case = Case("T3D", seed=3, force_kind="int")
+    sess = session_for(case, flags=AUTO)
+    for thr, expect in (("1000000000", "ll"), ("1", "ce"), ("1000000000", "ll"), ("1", "ce")):
+        monkeypatch.setenv("HALO_AUTO_CE_BYTES", thr)
+        run_gpu_case(case, sess, steps=2)
+        assert sess.halo.transport() == expect
+    sess.destroy()
+    monkeypatch.delenv("HALO_AUTO_CE_BYTES")
+    big = Case("C3", seed=1, force_kind="int")  # pulses of ~2.5k rows: far below 4 MiB -> LL
+    sess = session_for(big, flags=AUTO)
+    run_gpu_case(big, sess)
+    assert sess.halo.transport() == "ll"
+    sess.destroy()
+    from paper_2509_21527_b200 import HaloError
+    with pytest.raises(HaloError) as e:
+        session_for(case, flags=AUTO | CE)
+    assert e.value.status == 8

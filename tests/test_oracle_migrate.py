@@ -129,3 +129,29 @@ def test_migrate_rejects_two_cell_moves():
     Xm[g7, 2] += np.float32(1.0)
     new = migrate(_homes(states, Xm), c.L, c.grid)
     assert g7 in new[0][0]
+
+
+def test_pme_gather_return_pins():
+    """P1: the PME buffer holds every atom exactly once, row = its global position
+    (the rank-order concatenation of the home rows, pinned against X through the
+    home assignment); P2: with integer forces the returned increments sum to the
+    PME forces exactly and each rank's rows get exactly its slice."""
+    from oracle import pme_gather, pme_return
+    from synth import forces_int
+    c = get_config("T3D")
+    X = water_box(c.n_atoms, c.L, 21)
+    st = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    pme_x, off = pme_gather([s.x[: s.n_home] for s in st])
+    gids = np.concatenate([s.gid[: s.n_home] for s in st])
+    assert pme_x.shape[0] == X.shape[0] and np.array_equal(np.sort(gids), np.arange(X.shape[0]))
+    np.testing.assert_array_equal(pme_x.view(np.int32), X[gids].view(np.int32))
+    assert off[-1] == X.shape[0] and all(off[r + 1] - off[r] == st[r].n_home for r in range(len(st)))
+    F = [forces_int(s.n_home, 50 + s.rank) for s in st]
+    pf = forces_int(X.shape[0], 99)
+    out = pme_return(F, pf, off)
+    tot = sum((o.astype(np.float64) - f.astype(np.float64)).sum(axis=0) for o, f in zip(out, F))
+    np.testing.assert_array_equal(tot, pf.astype(np.float64).sum(axis=0))
+    for r, o in enumerate(out):
+        np.testing.assert_array_equal(o - F[r], pf[off[r]: off[r + 1]])
+    ov = pme_return(F, pf, off, accumulate=False)
+    np.testing.assert_array_equal(np.concatenate(ov).view(np.int32), pf.view(np.int32))
