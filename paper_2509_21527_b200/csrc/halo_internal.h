@@ -103,6 +103,7 @@ enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4,
 // ranks it can receive atoms from.  Staging area rows are SoA: x (layout
 // floats), v (layout floats), gid (int32), capacity rows each.
 constexpr int kStencil = 27;
+constexpr int kMigBlocks = 64;     // classify CTAs per rank (contiguous row ranges, stable order)
 struct MigRank {
   float* x;                   // own x (rows re-written in place by the merge)
   int32_t* gid;               // own gid array (caller's)
@@ -140,6 +141,9 @@ struct MigCtrl {
   int32_t in_src_off[kMaxLocal][kStencil];  // ... starting there in its staging-out
   int32_t in_off[kMaxLocal][kStencil + 1];  // prefix of in_cnt: list k is rows [in_off[k], in_off[k+1]) of staging-in
   int32_t err[kMaxLocal];
+  // classify split over kMigBlocks CTAs per rank (contiguous row ranges): per-CTA
+  // group counts, then their exclusive prefix within each group
+  int32_t blk[kMaxLocal][kMigBlocks][kStencil];
 };
 
 // HALO_DEBUG bits: protocol mutations for the dependency-safety tests (G3);

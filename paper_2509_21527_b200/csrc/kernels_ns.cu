@@ -5,10 +5,11 @@
 // re-populated with the atoms inside their region before the send
 // maps are rebuilt (halo_set_maps).  Per local rank, stream-ordered:
 //
-//   k_mig_classify  wrap every home row into the box (R29), find its cell
-//                   (fp64 planes, R3/R4) and its stencil slot (R30), and write the
-//                   rows grouped by destination — a stable compaction, so every
-//                   group stays in ascending gid — into the own staging-out area
+//   k_mig_count     wrap every home row into the box (R29), find its cell
+//   k_mig_scan      (fp64 planes, R3/R4) and its stencil slot (R30); count per
+//   k_mig_scatter   CTA, prefix, then write the rows grouped by destination — a
+//                   stable compaction over contiguous CTA ranges, so every group
+//                   stays in ascending gid — into the own staging-out area
 //   k_mig_publish   per stencil rank: (offset, count) of its group into ITS
 //                   header, count by system-scope release (the rows before it)
 //   k_mig_wait      acquire every stencil rank's count for this rank; prefix ->
@@ -80,19 +81,27 @@ __device__ __forceinline__ int mig_slot(const MigParams& M, const MigRank& R, in
   return -1;
 }
 
+// CTA g of rank l handles rows [g*per, (g+1)*per): contiguous ranges keep the
+// per-group order stable across CTAs.
+__device__ __forceinline__ void mig_range(int n, int g, int& b, int& e) {
+  const int per = (n + kMigBlocks - 1) / kMigBlocks;
+  b = min(n, g * per);
+  e = min(n, b + per);
+}
+
+// pass 1 (grid kMigBlocks x n_local): group sizes per CTA; gid strictly ascending
 template <int W>
-__global__ void __launch_bounds__(1024) k_mig_classify(const __grid_constant__ MigParams M, MigCtrl* C) {
-  const int l = blockIdx.x;
+__global__ void __launch_bounds__(256) k_mig_count(const __grid_constant__ MigParams M, MigCtrl* C) {
+  const int l = blockIdx.y, g = blockIdx.x;
   const MigRank& R = M.r[l];
-  const int n = R.n_home, cap = M.capacity;
-  __shared__ int s_cnt[kStencil], s_base[kStencil], s_run[kStencil];
-  __shared__ int s_wcnt[32][kStencil];
+  __shared__ int s_cnt[kStencil];
   __shared__ int s_err;
-  if (threadIdx.x < kStencil) s_cnt[threadIdx.x] = s_run[threadIdx.x] = 0;
+  if (threadIdx.x < kStencil) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_err = 0;
   __syncthreads();
-  // pass 1: group sizes; gid strictly ascending (the caller's order, R11)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  int b, e;
+  mig_range(R.n_home, g, b, e);
+  for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
     float v[4];
     const int k = mig_slot<W>(M, R, i, v);
     if (k < 0) atomicOr(&s_err, kErrGeometry);
@@ -100,28 +109,55 @@ __global__ void __launch_bounds__(1024) k_mig_classify(const __grid_constant__ M
     if (i > 0 && R.gid[i] <= R.gid[i - 1]) atomicOr(&s_err, kErrMap);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int k = 0; k < R.n_nb; ++k) {
-      s_base[k] = acc;
-      C->out_off[l][k] = acc;
-      C->out_cnt[l][k] = s_cnt[k];
-      acc += s_cnt[k];
+  if (threadIdx.x < kStencil) C->blk[l][g][threadIdx.x] = s_cnt[threadIdx.x];
+  if (threadIdx.x == 0 && s_err) atomicOr(&C->err[l], s_err);
+}
+
+// group bases and per-CTA offsets inside each group (one warp per rank, lane = group)
+__global__ void k_mig_scan(const __grid_constant__ MigParams M, MigCtrl* C) {
+  const int l = blockIdx.x, k = threadIdx.x;
+  const MigRank& R = M.r[l];
+  __shared__ int s_tot[kStencil];
+  int acc = 0;
+  if (k < R.n_nb)
+    for (int g = 0; g < kMigBlocks; ++g) {
+      const int c = C->blk[l][g][k];
+      C->blk[l][g][k] = acc;
+      acc += c;
     }
-    C->err[l] = s_err;
+  if (k < kStencil) s_tot[k] = acc;
+  __syncwarp();
+  if (k < R.n_nb) {
+    int base = 0;
+    for (int j = 0; j < k; ++j) base += s_tot[j];
+    C->out_off[l][k] = base;
+    C->out_cnt[l][k] = acc;
   }
+}
+
+// pass 2 (grid kMigBlocks x n_local): stable scatter of the CTA's rows into the
+// staging-out groups, 256 rows at a time (per group: warp ballot rank + warp
+// prefix + running base)
+template <int W>
+__global__ void __launch_bounds__(256) k_mig_scatter(const __grid_constant__ MigParams M, const MigCtrl* C) {
+  const int l = blockIdx.y, g = blockIdx.x;
+  const MigRank& R = M.r[l];
+  const int cap = M.capacity;
+  __shared__ int s_run[kStencil];
+  __shared__ int s_wcnt[8][kStencil];
+  if (threadIdx.x < R.n_nb) s_run[threadIdx.x] = C->out_off[l][threadIdx.x] + C->blk[l][g][threadIdx.x];
   __syncthreads();
-  // pass 2: stable scatter, 1024 rows at a time (per slot: warp ballot rank +
-  // warp prefix + running base)
+  int b, e;
+  mig_range(R.n_home, g, b, e);
   float* sx = stage_x(R.stage_out);
   float* sv = stage_v(R.stage_out, cap, W);
   int32_t* sg = stage_gid(R.stage_out, cap, W);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  for (int base = 0; base < n; base += blockDim.x) {
+  for (int base = b; base < e; base += blockDim.x) {
     const int i = base + threadIdx.x;
     float v[4] = {0.f, 0.f, 0.f, 0.f};
-    const int k = (i < n) ? mig_slot<W>(M, R, i, v) : -1;
+    const int k = (i < e) ? mig_slot<W>(M, R, i, v) : -1;
     int in_warp = 0;
     for (int kk = 0; kk < R.n_nb; ++kk) {
       const uint32_t m = __ballot_sync(0xffffffffu, k == kk);
@@ -140,7 +176,7 @@ __global__ void __launch_bounds__(1024) k_mig_classify(const __grid_constant__ M
     }
     __syncthreads();
     if (k >= 0) {
-      const size_t pos = (size_t)s_base[k] + s_wcnt[warp][k] + in_warp;
+      const size_t pos = (size_t)s_wcnt[warp][k] + in_warp;
 #pragma unroll
       for (int c = 0; c < W; ++c) sx[pos * W + c] = v[c];
       sg[pos] = R.gid[i];
@@ -292,8 +328,12 @@ cudaError_t launch_migrate(const MigParams& M, MigCtrl* C, int max_rows, int pha
   void* a2[] = {(void*)&M, (void*)&C};
   cudaError_t e;
   if (phase == 0) {
-    e = cudaLaunchKernel(W == 4 ? (const void*)k_mig_classify<4> : (const void*)k_mig_classify<3>, dim3(L),
-                         dim3(1024), a2, 0, st);
+    const dim3 gb(kMigBlocks, L);
+    e = cudaLaunchKernel(W == 4 ? (const void*)k_mig_count<4> : (const void*)k_mig_count<3>, gb, dim3(256), a2, 0, st);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaLaunchKernel((const void*)k_mig_scan, dim3(L), dim3(32), a2, 0, st)) != cudaSuccess) return e;
+    e = cudaLaunchKernel(W == 4 ? (const void*)k_mig_scatter<4> : (const void*)k_mig_scatter<3>, gb, dim3(256), a2, 0,
+                         st);
     if (e != cudaSuccess) return e;
     if ((e = cudaLaunchKernel((const void*)k_mig_publish, dim3(L), dim3(32), a2, 0, st)) != cudaSuccess) return e;
     return cudaLaunchKernel((const void*)k_mig_wait, dim3(L), dim3(32), a2, 0, st);

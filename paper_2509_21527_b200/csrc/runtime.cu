@@ -7,11 +7,13 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "halo_internal.h"
@@ -704,65 +706,68 @@ static void build_x_items_ll(halo_ctx* ctx, int p_lo, int p_hi) {
 // NS step from the final maps: task rows in level order (slice rows of pulse
 // P-1, ..., of pulse 0, then home rows that receive forces) and, per task row,
 // its contributions (q, i) with map_q[i] == row, pulses descending (R15).
+// Per local rank (independent: one host thread each when several ranks share
+// the process — the NS-step cost of an 8-rank GPU is dominated by this build).
+static bool build_csr_rank(halo_ctx* ctx, int l, std::vector<int32_t>& r) {
+  const int P = ctx->P;
+  const int nt = ctx->n_total[l], nh = ctx->n_home[l];
+  std::vector<int> cnt(nt, 0);
+  std::vector<uint8_t> mask(nt, 0);
+  const std::vector<std::vector<int32_t>>& maps = ctx->h_maps[l];
+  for (int q = 0; q < P; ++q)
+    for (int32_t t : maps[q]) {
+      cnt[t]++;
+      mask[t] |= (uint8_t)(1u << q);
+    }
+  std::vector<int32_t> task_of(nt, -1), tr;
+  tr.reserve(nt);
+  auto& lb = ctx->level_begin[l];
+  for (int k = 0; k < P; ++k) {  // level k = pulse P-1-k
+    const int p = P - 1 - k;
+    lb[k] = (int)tr.size();
+    const int a = ctx->atom_offset[l * P + p], n = ctx->recv_size[l * P + p];
+    for (int t = a; t < a + n; ++t) {
+      task_of[t] = (int)tr.size();
+      tr.push_back(t);
+    }
+  }
+  lb[P] = (int)tr.size();
+  for (int t = 0; t < nh; ++t)
+    if (cnt[t]) {
+      task_of[t] = (int)tr.size();
+      tr.push_back(t);
+    }
+  lb[P + 1] = (int)tr.size();
+  // 32-B task records: row, n, contrib[0..5] (q << 24 | i), pulses descending
+  r.assign(tr.size() * 8 + 8, 0);
+  for (size_t k = 0; k < tr.size(); ++k) {
+    r[8 * k] = tr[k];
+    r[8 * k + 1] = cnt[tr[k]];
+  }
+  for (int q = 0; q < P; ++q)
+    for (size_t i = 0; i < maps[q].size(); ++i) {
+      const int t = maps[q][i];
+      if (task_of[t] < 0) return false;
+      const int pos = __builtin_popcount((unsigned)mask[t] >> (q + 1));
+      r[8 * (size_t)task_of[t] + 2 + pos] = (int32_t)(((uint32_t)q << 24) | (uint32_t)i);
+    }
+  return true;
+}
+
 static halo_status build_csr(halo_ctx* ctx, cudaStream_t st) {
   const int L = ctx->n_local, P = ctx->P;
-  std::vector<std::vector<int32_t>> trow(L), toff(L);
-  std::vector<std::vector<uint32_t>> contrib(L);
   ctx->level_begin.assign(L, std::vector<int>(P + 2, 0));
-  for (int l = 0; l < L; ++l) {
-    const int nt = ctx->n_total[l], nh = ctx->n_home[l];
-    std::vector<int> cnt(nt, 0);
-    std::vector<uint8_t> mask(nt, 0);
-    const std::vector<std::vector<int32_t>>& maps = ctx->h_maps[l];
-    for (int q = 0; q < P; ++q)
-      for (int32_t t : maps[q]) {
-        cnt[t]++;
-        mask[t] |= (uint8_t)(1u << q);
-      }
-    std::vector<int32_t> task_of(nt, -1);
-    auto& tr = trow[l];
-    auto& lb = ctx->level_begin[l];
-    for (int k = 0; k < P; ++k) {  // level k = pulse P-1-k
-      const int p = P - 1 - k;
-      lb[k] = (int)tr.size();
-      const int a = ctx->atom_offset[l * P + p], n = ctx->recv_size[l * P + p];
-      for (int t = a; t < a + n; ++t) {
-        task_of[t] = (int)tr.size();
-        tr.push_back(t);
-      }
-    }
-    lb[P] = (int)tr.size();
-    for (int t = 0; t < nh; ++t)
-      if (cnt[t]) {
-        task_of[t] = (int)tr.size();
-        tr.push_back(t);
-      }
-    lb[P + 1] = (int)tr.size();
-    auto& to = toff[l];
-    to.assign(tr.size() + 1, 0);
-    for (size_t k = 0; k < tr.size(); ++k) to[k + 1] = to[k] + cnt[tr[k]];
-    auto& cb = contrib[l];
-    cb.assign(to.back(), 0u);
-    for (int q = 0; q < P; ++q)
-      for (size_t i = 0; i < maps[q].size(); ++i) {
-        const int t = maps[q][i];
-        if (task_of[t] < 0) return fail(ctx, HALO_ERR_ARG, "map entry targets a row with no gather task");
-        const int pos = __builtin_popcount((unsigned)mask[t] >> (q + 1));
-        cb[to[task_of[t]] + pos] = ((uint32_t)q << 24) | (uint32_t)i;
-      }
-  }
-  // pack 32-B task records: row, n, contrib[0..5] (pulses descending)
   std::vector<std::vector<int32_t>> rec(L);
-  for (int l = 0; l < L; ++l) {
-    auto& r = rec[l];
-    r.assign(trow[l].size() * 8 + 8, 0);
-    for (size_t k = 0; k < trow[l].size(); ++k) {
-      const int n = toff[l][k + 1] - toff[l][k];
-      r[8 * k] = trow[l][k];
-      r[8 * k + 1] = n;
-      for (int j = 0; j < n; ++j) r[8 * k + 2 + j] = (int32_t)contrib[l][toff[l][k] + j];
-    }
+  std::vector<char> ok(L, 1);
+  if (L == 1) {
+    ok[0] = build_csr_rank(ctx, 0, rec[0]);
+  } else {
+    std::vector<std::thread> th;
+    for (int l = 0; l < L; ++l) th.emplace_back([&, l] { ok[l] = build_csr_rank(ctx, l, rec[l]); });
+    for (auto& t : th) t.join();
   }
+  for (int l = 0; l < L; ++l)
+    if (!ok[l]) return fail(ctx, HALO_ERR_ARG, "map entry targets a row with no gather task");
   // kept on the host: each f item block carries its rows' records (build_grec)
   ctx->h_tasks = std::move(rec);
   (void)st;
@@ -986,28 +991,29 @@ static int grid_for(int n_items, int n_local, int max_blocks) {
 // Pull the set_maps results of every local rank back to the host.
 static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st) {
   const int L = ctx->n_local, P = ctx->P;
-  std::vector<int32_t> buf(kMaxLocal * kMaxP);
-  auto pull = [&](void* dev, std::vector<int>& dst) -> halo_status {
-    cudaError_t e = cudaMemcpyAsync(buf.data(), dev, sizeof(int32_t) * kMaxLocal * kMaxP, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "pull_ctrl");
-    for (int l = 0; l < L; ++l)
-      for (int p = 0; p < P; ++p) dst[l * P + p] = buf[l * kMaxP + p];
-    return HALO_OK;
-  };
-  halo_status s;
-  if ((s = pull(ctx->ctrl->send_size, ctx->send_size)) != HALO_OK) return s;
-  if ((s = pull(ctx->ctrl->recv_size, ctx->recv_size)) != HALO_OK) return s;
-  if ((s = pull(ctx->ctrl->atom_offset, ctx->atom_offset)) != HALO_OK) return s;
-  if ((s = pull(ctx->ctrl->remote_off, ctx->remote_off)) != HALO_OK) return s;
-  if ((s = pull(ctx->ctrl->n_indep, ctx->n_indep)) != HALO_OK) return s;
-  std::vector<int> depi(L * P);
-  if ((s = pull(ctx->ctrl->dep, depi)) != HALO_OK) return s;
-  for (int i = 0; i < L * P; ++i) ctx->dep[i] = (unsigned)depi[i];
-  int32_t nt[kMaxLocal];
-  CK(cudaMemcpyAsync(nt, ctx->ctrl->n_total, sizeof nt, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (int l = 0; l < L; ++l) ctx->n_total[l] = nt[l];
+  // the set_maps result arrays are contiguous in Ctrl: one copy, one synchronisation
+  const char* lo = reinterpret_cast<const char*>(ctx->ctrl->send_size);
+  const char* hi = reinterpret_cast<const char*>(ctx->ctrl->n_total) + sizeof(ctx->ctrl->n_total);
+  static_assert(offsetof(Ctrl, n_indep) > offsetof(Ctrl, send_size) && offsetof(Ctrl, n_total) > offsetof(Ctrl, dep),
+                "set_maps result block layout");
+  std::vector<char> hbuf(sizeof(Ctrl));  // (Ctrl holds the trace arrays: too large for the stack)
+  const Ctrl& h = *reinterpret_cast<const Ctrl*>(hbuf.data());
+  char* hb = hbuf.data() + (lo - reinterpret_cast<const char*>(ctx->ctrl));
+  cudaError_t e = cudaMemcpyAsync(hb, lo, (size_t)(hi - lo), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "pull_ctrl");
+  for (int l = 0; l < L; ++l) {
+    for (int p = 0; p < P; ++p) {
+      const int i = l * P + p;
+      ctx->send_size[i] = h.send_size[l][p];
+      ctx->recv_size[i] = h.recv_size[l][p];
+      ctx->atom_offset[i] = h.atom_offset[l][p];
+      ctx->remote_off[i] = h.remote_off[l][p];
+      ctx->n_indep[i] = h.n_indep[l][p];
+      ctx->dep[i] = h.dep[l][p];
+    }
+    ctx->n_total[l] = h.n_total[l];
+  }
   return HALO_OK;
 }
 
@@ -1534,9 +1540,9 @@ halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gi
   CK(launch_status(SP, st));
   CK(launch_migrate(M, ctx->d_migctrl, ctx->cfg.capacity, 1, st));
   int32_t agreed[kMaxLocal];
-  MigCtrl hc;
+  int32_t in_off[kMaxLocal][kStencil + 1];  // (MigCtrl is large: copy only the row counts)
   CK(cudaMemcpyAsync(agreed, ctx->ctrl->agreed_err, sizeof agreed, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&hc, ctx->d_migctrl, sizeof hc, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(in_off, ctx->d_migctrl->in_off, sizeof in_off, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if ((s = check_err_word(ctx)) != HALO_OK) return s;
   int any = 0;
@@ -1545,7 +1551,7 @@ halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gi
     return fail(ctx, HALO_ERR_GEOMETRY, "an atom moved more than one cell (or a box length) since the last NS step");
   if (any & kErrCapacity) return fail(ctx, HALO_ERR_CAPACITY, "a rank would hold more home rows than capacity");
   if (any & kErrMap) return fail(ctx, HALO_ERR_ARG, "gid rows are not strictly ascending on some rank");
-  for (int l = 0; l < L; ++l) n_home_out[l] = hc.in_off[l][mr[l].n_nb];
+  for (int l = 0; l < L; ++l) n_home_out[l] = in_off[l][mr[l].n_nb];
   return HALO_OK;
 }
 

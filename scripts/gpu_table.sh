@@ -38,3 +38,4 @@ run C5 4 ll --no-cpu
 run C3 4 ce --proto ce --no-cpu --no-ns
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/t_reference_C3.json 2> gpurun_out/t_reference_C3.err
 timeout 1200 python -m pytest tests/test_gpu_multiproc.py -x -q > gpurun_out/t_pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/t_pytest_mp.log
+timeout 1200 python -m pytest tests -m gpu -x -q --ignore=tests/test_gpu_multiproc.py > gpurun_out/t_pytest_all.log 2>&1; echo rc=$? >> gpurun_out/t_pytest_all.log

@@ -19,7 +19,8 @@ for f in sorted(glob.glob(os.path.join(src, "t_*_n*_*.json"))):
     pme = (d.get("pme") or {}).get("us_per_step")
     ns = d.get("ns_step") or {}
     rows.append((c["workload"].split(":")[0], d["n_gpus"], c.get("dd_ranks_per_gpu"),
-                 c.get("transport", c.get("protocol")) + ("" if c.get("zones", "slab") == "slab" else ", rounded"),
+                 (c.get("protocol") if c.get("transport") in (None, c.get("protocol")) or c.get("protocol") != "auto"
+                  else f"auto → {c.get('transport')}") + ("" if c.get("zones", "slab") == "slab" else ", rounded"),
                  d["value"], d.get("step_median_us"), d.get("graph_us_per_step"), d.get("x_us"), d.get("f_us"),
                  (d.get("e2e") or {}).get("value"), nccl, fl.get("t0_one_way_us"), fl.get("floor_step_with_launch_us"),
                  fl.get("value_over_floor_with_launch"), (d.get("nvlink") or {}).get("achieved_gbs"),
