@@ -804,6 +804,23 @@ static void build_f_items_ll(halo_ctx* ctx) {
 }
 
 // 128-B work records of the LL kernels, one per item (halo_internal.h XRec/GRec).
+// Host loops of the NS-step plan build over many independent items: split over a
+// few threads (the item blocks are MBs at C3/C4; the NS step is host-bound).
+template <class F>
+static void parallel_for(size_t n, F&& body) {
+  const size_t T = n < 512 ? 1 : std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
+  if (T == 1) {
+    for (size_t k = 0; k < n; ++k) body(k);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (size_t t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (size_t k = n * t / T; k < n * (t + 1) / T; ++k) body(k);
+    });
+  for (auto& x : th) x.join();
+}
+
 static void build_xrec(halo_ctx* ctx) {
   const int W = ctx->W, P = ctx->P, R = ctx->item_rows;
   ctx->h_xrec.assign(ctx->h_items_x.size(), XRec{});
@@ -838,10 +855,10 @@ static void build_xrec(halo_ctx* ctx) {
   }
   const size_t XB = 128 + 4 * (size_t)R;
   ctx->h_xblk.assign(ctx->h_items_x.size() * XB, 0);
-  for (size_t k = 0; k < ctx->h_items_x.size(); ++k) {
+  parallel_for(ctx->h_items_x.size(), [&](size_t k) {
     memcpy(&ctx->h_xblk[k * XB], &ctx->h_xrec[k], sizeof(XRec));
     memcpy(&ctx->h_xblk[k * XB + 128], &ctx->h_xmap[k * (size_t)R], 4 * (size_t)R);
-  }
+  });
 }
 
 static halo_status build_grec(halo_ctx* ctx) {
@@ -886,12 +903,12 @@ static halo_status build_grec(halo_ctx* ctx) {
   }
   const size_t FB = 128 + 32 * (size_t)R;
   ctx->h_fblk.assign(ctx->h_items_f.size() * FB, 0);
-  for (size_t k = 0; k < ctx->h_items_f.size(); ++k) {
+  parallel_for(ctx->h_items_f.size(), [&](size_t k) {
     const Item& w = ctx->h_items_f[k];
     memcpy(&ctx->h_fblk[k * FB], &ctx->h_grec[k], sizeof(GRec));
     if (w.kind == kItemGather)
       memcpy(&ctx->h_fblk[k * FB + 128], &ctx->h_tasks[w.lrank][8 * (size_t)w.begin], 32 * (size_t)(w.end - w.begin));
-  }
+  });
   return HALO_OK;
 }
 

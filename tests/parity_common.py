@@ -140,7 +140,9 @@ def moved_case(case: Case, seed: int):
     oracle's wrapped positions (R29) and a Case over them.  Returns (Xm, V, case2)."""
     from oracle import wrap_coord
     from synth import displacements, velocities
-    Xm = displacements(case.X, case.L, 100 + seed)
+    # moves stay well inside one cell (R30): thermal sigma and a few diagonal jumps
+    cell = min(float(case.L[d]) / case.grid[d] for d in range(3))
+    Xm = displacements(case.X, case.L, 100 + seed, sigma=min(0.05, cell / 12), far=min(0.6, cell / 3))
     V = velocities(case.X.shape[0], 200 + seed, width=case.layout)
     Xw = Xm.copy()
     for i in range(Xm.shape[0]):

@@ -15,11 +15,13 @@ pytestmark = pytest.mark.gpu
 
 
 class FuzzCase:
-    def __init__(self, seed):
+    def __init__(self, seed, rounded=False):
         self.name = f"fuzz{seed}"
+        self.seed, self.rounded = seed, rounded
         self.L, self.rc, self.grid, self.pulses, self.X, self.layout = random_case(seed)
         W = charges(self.X.shape[0]) if self.layout == 4 else None
-        self.states = decompose(self.X, self.L, self.rc, self.grid, self.pulses, W=W)
+        self.W = W
+        self.states = decompose(self.X, self.L, self.rc, self.grid, self.pulses, W=W, rounded=rounded)
         self.nranks = len(self.states)
         self.capacity = max(max(s.x.shape[0] for s in self.states), 1) + 64
         mk = forces_int if seed % 2 == 0 else forces_normal
@@ -40,4 +42,32 @@ def test_fuzz_parity(seed, proto):
     sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=case.layout, capacity=case.capacity,
                        device=0, flags=proto, timeout_s=5.0)
     run_gpu_case(case, sess, steps=2)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_rounded_zones(seed):
+    """Rounded zones (R31) on the random geometries, LL protocol, bit-exact."""
+    from paper_2509_21527_b200.session import HaloSession
+    case = FuzzCase(seed, rounded=True)
+    sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=case.layout, capacity=case.capacity,
+                       device=0, flags=1 << 9, timeout_s=5.0)
+    run_gpu_case(case, sess, steps=2)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("seed", range(0, 24, 2))
+def test_fuzz_migrate(seed):
+    """halo_migrate on the random geometries (clustered atoms, empty ranks, 1-4
+    cells per dim): moves of up to a third of the smallest cell (R30 holds), then
+    the new maps and both halos, bit-exact vs the oracle."""
+    from paper_2509_21527_b200.session import HaloSession
+    from tests.parity_common import moved_case, run_gpu_migrate
+    case = FuzzCase(seed)
+    case.layout = case.layout
+    Xm, V, c2 = moved_case(case, seed)
+    cap = max(case.capacity, c2.capacity) + 64
+    sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=case.layout, capacity=cap, device=0,
+                       timeout_s=5.0)
+    run_gpu_migrate(case, c2, Xm, V, sess)
     sess.destroy()
