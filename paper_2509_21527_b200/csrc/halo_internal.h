@@ -216,7 +216,8 @@ struct __align__(128) XRec {
   const int32_t* map;       // send: map_p + begin
   const float* x;           // send: own x base
   uint64_t* ll;             // send: receiver's LL slot p + begin*W; recv: own LL slot p + begin*W
-  float* xdst;              // recv: own x + (recv_off_p + begin)*W
+  float* xdst;              // recv: own x + (recv_off_p + begin)*W; send: the receiver's x rows when the
+                            // receiver is a DD rank of this process (direct write, no receive item), else null
   const uint64_t* xll_own;  // dep send: own coordinate LL base (slot q at + q*ll_stride)
   int32_t recv_off[kMaxP];  // dep send: own receive ranges
   int32_t recv_size[kMaxP];

@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
           uint64_t* dst = (P.debug & kLocalSink) ? const_cast<uint64_t*>(r.xll_own) + (size_t)r.pulse * P.ll_stride + u
                                                  : r.ll + u;
           st_relaxed_sys(dst, ll_pack(o, tag));
+          if (r.xdst) r.xdst[u] = o;  // same-process receiver: its halo row directly (kernel end publishes it)
         }
       }
     } else {
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
           uint64_t* dst = (P.debug & kLocalSink) ? const_cast<uint64_t*>(r.xll_own) + (size_t)r.pulse * P.ll_stride + u
                                                  : r.ll + u;
           st_relaxed_sys(dst, ll_pack(v, tag));
+          if (r.xdst) r.xdst[u] = v;
         }
       }
     }

@@ -193,6 +193,7 @@ struct halo_ctx {
   bool captured = false;
   bool auto_tr = false;             // HALO_F_AUTO_TRANSPORT: LL or copy engine chosen at every set_maps
   size_t auto_ce_bytes = (size_t)4 << 20;  // ... copy engine when some pulse sends >= this (HALO_AUTO_CE_BYTES)
+  bool direct_x = true;             // LL: same-process receivers get their x rows from the sender (HALO_DIRECT_X=0: off)
   int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
 
   int cell(int r, int d) const {
@@ -202,6 +203,7 @@ struct halo_ctx {
     return r / (g[1] * g[2]);
   }
   int rank_of(int cx, int cy, int cz) const { return (cx * cfg.grid[1] + cy) * cfg.grid[2] + cz; }
+  bool is_local(int r) const { return r >= first_rank && r < first_rank + n_local; }
   int neighbour(int r, int d, int delta) const {
     int c[3] = {cell(r, 0), cell(r, 1), cell(r, 2)};
     c[d] = ((c[d] + delta) % cfg.grid[d] + cfg.grid[d]) % cfg.grid[d];
@@ -379,6 +381,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     ctx->item_rows_fixed = true;
   }
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = atoi(e) < 0 ? kPollTight : (uint32_t)atoi(e);
+  if (const char* e = getenv("HALO_DIRECT_X")) ctx->direct_x = atoi(e) != 0;
   if (const char* e = getenv("HALO_RECV_MULT")) ctx->recv_mult = std::min(16, std::max(1, atoi(e)));
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
@@ -697,9 +700,13 @@ static void build_x_items_ll(halo_ctx* ctx, int p_lo, int p_hi) {
       const int i = l * ctx->P + p;
       add_items(v, l, p, kItemXDep, ctx->n_indep[i], ctx->send_size[i], R);
     }
+  // receive items only for rows that arrive from another process: a sender in this
+  // process writes the receiver's x rows itself (direct_x; the launch's end makes
+  // them visible to the stream, as the receive items' copies would be)
   for (int p = p_lo; p < p_hi; ++p)
     for (int l = 0; l < ctx->n_local; ++l)
-      add_items(v, l, p, kItemXRecv, 0, ctx->recv_size[l * ctx->P + p], std::min(kMaxItemRows, ctx->recv_mult * R));
+      if (!(ctx->direct_x && ctx->is_local(ctx->neighbour(ctx->first_rank + l, ctx->pdim[p], +1))))
+        add_items(v, l, p, kItemXRecv, 0, ctx->recv_size[l * ctx->P + p], std::min(kMaxItemRows, ctx->recv_mult * R));
 }
 
 // Force gather plan of every local rank (LL protocol), built on the host at the
@@ -849,6 +856,7 @@ static void build_xrec(halo_ctx* ctx) {
     } else {
       r.map = pd.map + w.begin;
       r.ll = pd.xll_dst + (size_t)w.begin * W;
+      if (ctx->direct_x && ctx->is_local(ctx->neighbour(rk, ctx->pdim[p], -1))) r.xdst = pd.x_dst + (size_t)w.begin * W;
       const auto& m = ctx->h_maps[l][p];
       std::copy(m.begin() + w.begin, m.begin() + w.end, ctx->h_xmap.begin() + k * (size_t)R);
     }
