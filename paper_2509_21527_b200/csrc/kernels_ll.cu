@@ -270,10 +270,12 @@ __device__ __noinline__ double cta_reduce(double (*s_red)[kThreads], int j_out) 
 // CTA writes the rank's fshift.
 __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_red)[kThreads],
                                             uint32_t fsp_slots) {
-  // only this CTA writes the rank's fshift: read it now, off the tail
-  const double fs_old = (threadIdx.x < 9) ? P.fshift[9 * g.lrank + threadIdx.x] : 0.0;
+  // one combine per (rank, dim g.level): only this CTA writes fshift[dim][0..2]:
+  // read it now, off the tail
+  const int dim = g.level;
+  const double fs_old = (threadIdx.x < 3) ? P.fshift[9 * g.lrank + 3 * dim + threadIdx.x] : 0.0;
 #pragma unroll
-  for (int j = 0; j < 9; ++j) s_red[j][threadIdx.x] = 0.0;
+  for (int j = 0; j < 3; ++j) s_red[j][threadIdx.x] = 0.0;
   // one flat index space over (pulse, slot, component) triples; every load of a
   // thread is issued before any wait is resolved
   uint32_t off[kMaxP + 1];
@@ -295,7 +297,7 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
         while (e >= off[q + 1]) ++q;
         const uint32_t pp = e - off[q];  // slot * 3 + component
         ptr[k] = g.part + (size_t)q * fsp_slots * 6 + 2 * (size_t)pp;
-        dc[k] = 3 * g.pulse_dim[q] + (int)(pp % 3);
+        dc[k] = (int)(pp % 3);  // component (the item's pulses all shift along `dim`)
         hv[k] = ld_relaxed_sys(ptr[k]);
         lv[k] = ld_relaxed_sys(ptr[k] + 1);
       }
@@ -308,8 +310,8 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
       s_red[dc[k]][threadIdx.x] += __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
     }
   }
-  const double tot = cta_reduce<9>(s_red, threadIdx.x);
-  if (threadIdx.x < 9) P.fshift[9 * g.lrank + threadIdx.x] = fs_old + tot;
+  const double tot = cta_reduce<3>(s_red, threadIdx.x);
+  if (threadIdx.x < 3) P.fshift[9 * g.lrank + 3 * dim + threadIdx.x] = fs_old + tot;
 }
 
 // kF = units per thread per batch (1: latency regime, 2: large items), as kU above.
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(con
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq;
   __shared__ __align__(8) uint64_t s_bar[2];  // one mbarrier per item-block buffer
-  __shared__ double s_fs[9][kThreads];
+  __shared__ double s_fs[3][kThreads];
   const uint32_t FB = 128u + 32u * (uint32_t)P.item_rows;
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;

@@ -793,18 +793,23 @@ static void build_f_items_ll(halo_ctx* ctx) {
       const uint8_t level = k < P ? (uint8_t)(P - 1 - k) : kHomeLevel;
       add_items(v, l, level, kItemGather, lb[k], lb[k + 1], R);
     }
-  // shift-force combines last: each waits for the partials its pushers wrote
+  // shift-force combines last, one per (rank, dim it wrapped in): each waits for
+  // the partials its pushers wrote and owns the 3 components fshift[dim][*]
+  // (deterministic, no atomics; the dims of a rank combine in parallel CTAs)
   for (int l = 0; l < ctx->n_local; ++l) {
     const int rk = ctx->first_rank + l;
-    bool wraps = false;
-    for (int q = 0; q < P; ++q) wraps |= ctx->cell(rk, ctx->pdim[q]) == 0 && ctx->send_size[l * P + q] > 0;
-    if (!wraps) continue;
-    Item it;
-    it.lrank = (uint16_t)l;
-    it.pulse = kHomeLevel;
-    it.kind = kItemFshift;
-    it.begin = it.end = 0;
-    v.push_back(it);
+    for (int d = 0; d < 3; ++d) {
+      bool wraps = false;
+      for (int q = 0; q < P; ++q)
+        wraps |= ctx->pdim[q] == d && ctx->cell(rk, d) == 0 && ctx->send_size[l * P + q] > 0;
+      if (!wraps) continue;
+      Item it;
+      it.lrank = (uint16_t)l;
+      it.pulse = (uint8_t)d;  // the combine's dim
+      it.kind = kItemFshift;
+      it.begin = it.end = 0;
+      v.push_back(it);
+    }
   }
   ctx->n_tail_f = 0;
   for (const Item& it : v) ctx->n_tail_f += it.kind == kItemFshift;
@@ -903,10 +908,11 @@ static halo_status build_grec(halo_ctx* ctx) {
           g.part = ctx->fsp_of(upper) + ((size_t)p * ctx->fsp_slots + slot) * 6;
         }
       }
-    } else {  // kItemFshift: combine of the slots the pushers wrote into this rank
+    } else {  // kItemFshift: combine of the slots the pushers wrote into this rank, pulses of dim g.level
       g.part = ctx->fsp_of(rk);
       for (int q = 0; q < P; ++q)
-        g.nslot[q] = (g.wrap_mask >> q & 1u) ? (uint32_t)((ctx->send_size[l * P + q] + R - 1) / R) : 0u;
+        g.nslot[q] = ((g.wrap_mask >> q & 1u) && ctx->pdim[q] == (int)w.pulse)
+                         ? (uint32_t)((ctx->send_size[l * P + q] + R - 1) / R) : 0u;
     }
   }
   const size_t FB = 128 + 32 * (size_t)R;

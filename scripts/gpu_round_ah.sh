@@ -1,0 +1,8 @@
+python -m paper_2509_21527_b200.build > gpurun_out/ah_build.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q > gpurun_out/ah_pytest1.log 2>&1; echo rc=$? >> gpurun_out/ah_pytest1.log
+timeout 900 python -m pytest tests/test_gpu_multiproc.py -x -q -k "parity" > gpurun_out/ah_pytest2.log 2>&1; echo rc=$? >> gpurun_out/ah_pytest2.log
+L=dyn=ab/libhalo_dyn.so,stat=ab/libhalo_dyn.so@HALO_DYNAMIC_F=0,cs=ab/libhalo_cs.so,dx=ab/libhalo_dx.so
+python scripts/ab.py --libs $L --config C3 --gpus 1 --reps 3 > gpurun_out/ah_ab_C3_n1.txt 2>&1
+python scripts/ab.py --libs $L --config C5 --gpus 1 --reps 3 > gpurun_out/ah_ab_C5_n1.txt 2>&1
+python scripts/ab.py --libs $L --config C3 --gpus 2 --reps 2 > gpurun_out/ah_ab_C3_n2.txt 2>&1
+python scripts/ab.py --libs $L --config C4-1D --gpus 2 --reps 2 > gpurun_out/ah_ab_C41D_n2.txt 2>&1
