@@ -1247,6 +1247,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   // ranks/pulse tables are needed by the select/depmask kernels already
   ctx->h_items_x.clear();
   ctx->h_items_f.clear();
+  ctx->h_fblk.clear();  // the last epoch's force blocks: not re-uploaded with every pulse's x plan
+  ctx->h_xblk.clear();
   if ((s = upload_plan(ctx)) != HALO_OK) return s;
 
   const uint64_t timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);

@@ -39,3 +39,10 @@ run C3 4 ce --proto ce --no-cpu --no-ns
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/t_reference_C3.json 2> gpurun_out/t_reference_C3.err
 timeout 1200 python -m pytest tests/test_gpu_multiproc.py -x -q > gpurun_out/t_pytest_mp.log 2>&1; echo rc=$? >> gpurun_out/t_pytest_mp.log
 timeout 1200 python -m pytest tests -m gpu -x -q --ignore=tests/test_gpu_multiproc.py > gpurun_out/t_pytest_all.log 2>&1; echo rc=$? >> gpurun_out/t_pytest_all.log
+# final-build ncu evidence (1 GPU, C3 = 8 DD ranks)
+CMD="python bench.py --steps 20 --warmup 5 --no-cpu --no-graph --no-floors --no-ns --no-nccl"
+$CMD > gpurun_out/t_ncu_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/t_ncu_launches.csv $CMD > gpurun_out/t_ncu_l.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_exchange -s 20 -c 4 -o gpurun_out/t_ncu_full $CMD > gpurun_out/t_ncu_f.log 2>&1
+echo rc=$? > gpurun_out/t_ncu_rc.txt
+ncu -i gpurun_out/t_ncu_full.ncu-rep --page raw --csv > gpurun_out/t_ncu_raw.csv 2>/dev/null
