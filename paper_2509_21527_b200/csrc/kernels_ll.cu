@@ -246,14 +246,20 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // waits for another's polling loop (a full-mask SHFL right after the divergent
 // polling loop had cost ~10 us per level at C3); 2 barriers instead of the 9 of
 // a pairwise shared-memory tree.
+// threads per CTA of the f kernel (HALO_F_THREADS_128 build switch for the A/B)
+#ifndef HALO_F_THREADS
+#define HALO_F_THREADS 256
+#endif
+constexpr int kThreadsF = HALO_F_THREADS;
+
 template <int N>
-__device__ __noinline__ double cta_reduce(double (*s_red)[kThreads], int j_out) {
+__device__ __noinline__ double cta_reduce(double (*s_red)[kThreadsF], int j_out) {
   __shared__ double s_out[9];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
   for (int j = warp; j < N; j += nw) {
     double v = 0.0;
-    for (int t = lane; t < kThreads; t += 32) v += s_red[j][t];
+    for (int t = lane; t < kThreadsF; t += 32) v += s_red[j][t];
     v = warp_sum_d(v);
     if (lane == 0) s_out[j] = v;
   }
@@ -268,7 +274,7 @@ __device__ __noinline__ double cta_reduce(double (*s_red)[kThreads], int j_out) 
 // LL units: no flag, no fence).  One thread per (pulse, slot, component) triple
 // in a fixed assignment, then a fixed tree: deterministic, no atomics; only this
 // CTA writes the rank's fshift.
-__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_red)[kThreads],
+__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_red)[kThreadsF],
                                             uint32_t fsp_slots) {
   // one combine per (rank, dim g.level): only this CTA writes fshift[dim][0..2]:
   // read it now, off the tail
@@ -316,13 +322,14 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
 
 // kF = units per thread per batch (1: latency regime, 2: large items), as kU above.
 template <int W, int kF>
-__global__ void __launch_bounds__(kThreads, kF == 1 ? 5 : 4) k_exchange_f_ll(const __grid_constant__ ExParams P) {
+__global__ void __launch_bounds__(kThreadsF, kF == 1 ? 5 * 256 / kThreadsF : 4 * 256 / kThreadsF) k_exchange_f_ll(
+    const __grid_constant__ ExParams P) {
   // two item blocks [GRec | task records of item_rows rows (32 B each)], double-
   // buffered like the x kernel's
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq;
   __shared__ __align__(8) uint64_t s_bar[2];  // one mbarrier per item-block buffer
-  __shared__ double s_fs[3][kThreads];
+  __shared__ double s_fs[3][kThreadsF];
   const uint32_t FB = 128u + 32u * (uint32_t)P.item_rows;
   Ctrl* ctrl = P.ctrl;
   const bool trace = (P.flags & HALO_F_TIMERS) && threadIdx.x == 0 && blockIdx.x < kTraceCTAs;
@@ -508,7 +515,7 @@ cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool w
 cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
                                  cudaStream_t st) {
   void* args[] = {(void*)&p};
-  return launch_coop_kernel_ex(layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide), grid, kThreads, args, st, true,
+  return launch_coop_kernel_ex(layout == 4 ? f_fn<4>(wide) : f_fn<3>(wide), grid, kThreadsF, args, st, true,
                                f_smem_bytes(p.item_rows), win);
 }
 
@@ -530,7 +537,7 @@ cudaError_t max_coresident_ll(int layout, bool wide, int* x_blocks, int* f_block
   if (e != cudaSuccess) return e;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bx, fx, kThreads, x_smem_bytes(rows));
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, ff, kThreads, f_smem_bytes(rows));
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, ff, kThreadsF, f_smem_bytes(rows));
   if (e != cudaSuccess) return e;
   *x_blocks = bx * sms;
   *f_blocks = bf * sms;
