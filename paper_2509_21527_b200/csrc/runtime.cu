@@ -1850,7 +1850,9 @@ halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
         lo = std::min(lo, t[8 * i]);
         hi = std::max(hi, t[8 * i + 3]);
       }
-      v[which] = hi > lo ? hi - lo : 0;
+      // (with programmatic dependent launch the stamps of consecutive launches can
+      // interleave; keep the last arriver's span when the trace is inconsistent)
+      if (hi > lo) v[which] = hi - lo;
     }
   }
   if (x_ns) *x_ns = v[0];
