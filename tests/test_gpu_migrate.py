@@ -65,3 +65,33 @@ def test_migrate_errors():
         sess.exchange_x()
     assert e.value.status == 4
     sess.destroy()
+
+
+def test_migrate_capacity_overflow_is_agreed():
+    """A rank that would receive more home rows than `capacity` fails the call on
+    every rank (HALO_ERR_CAPACITY) and no row moves anywhere (x, gid unchanged)."""
+    from paper_2509_21527_b200 import HaloError
+    from paper_2509_21527_b200.session import HaloSession
+    case = Case("C1", seed=1)
+    cap = max(s.x.shape[0] for s in case.states) + 16
+    sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=3, capacity=cap, device=0, timeout_s=5.0)
+    run_gpu_case(case, sess, check_forces=False)
+    gid_t = []
+    for l in range(sess.n_local):
+        st = case.states[l]
+        gt = torch.zeros(cap, dtype=torch.int32, device=sess.device)
+        gt[: st.n_home] = torch.from_numpy(st.gid[: st.n_home].astype(np.int32)).to(sess.device)
+        gid_t.append(gt)
+    # move every atom of rank 1 (upper z cell) down into rank 0's cell: one cell, but too many rows
+    n1 = case.states[1].n_home
+    lo = float(np.float32(case.L[2])) / 2
+    sess.x[1][:n1, 2] = sess.x[1][:n1, 2] - lo
+    before = [sess.x[l][: case.states[l].n_home].clone() for l in range(2)]
+    with pytest.raises(HaloError) as e:
+        sess.migrate(gid_t)
+    assert e.value.status == 3
+    for l in range(2):
+        n = case.states[l].n_home
+        assert torch.equal(sess.x[l][:n], before[l])
+        assert torch.equal(gid_t[l][:n].cpu(), torch.from_numpy(case.states[l].gid[:n].astype(np.int32)))
+    sess.destroy()

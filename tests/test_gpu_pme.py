@@ -67,3 +67,24 @@ def test_pme_cuda_graph_replay():
             n = case.states[l].n_home
             np.testing.assert_array_equal(bits(sess.f[l][:n].cpu().numpy()), bits(exp_f[l]))
     sess.destroy()
+
+
+def test_pme_call_order_errors():
+    from paper_2509_21527_b200 import HaloError
+    from paper_2509_21527_b200.session import HaloSession
+    case = Case("C1", seed=1)
+    sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=3, capacity=case.capacity, device=0,
+                       timeout_s=5.0)
+    with pytest.raises(HaloError) as e:  # no halo_pme_reserve
+        sess.pme_setup()
+    assert e.value.status == 4
+    sess.destroy()
+    sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=3, capacity=case.capacity, device=0,
+                       timeout_s=5.0, pme_rank=1)
+    with pytest.raises(HaloError) as e:  # reserve after registration
+        sess.halo.pme_reserve(0)
+    assert e.value.status == 4
+    with pytest.raises(HaloError) as e:  # send before setup
+        sess.pme_send_x()
+    assert e.value.status == 4
+    sess.destroy()
