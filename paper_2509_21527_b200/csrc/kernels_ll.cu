@@ -13,10 +13,18 @@
 //     and a halo slice row is pushed back as soon as it is final (Alg. 5
 //     DEP_MGMT at row granularity).  Bit-exact with the oracle, no atomics.
 //
-// Each CTA loads one 128-B work record (XRec / GRec) per item: after an L2
-// flush the plan costs one memory round trip, not a chain of dependent loads.
-// Items are processed in a static order in which every wait targets an
-// earlier item, and the grid is launched cooperatively.
+//   * a receiver on the same GPU (a DD rank of this process) gets its halo
+//     rows stored directly by the sender; only rows from other GPUs go through
+//     receive items (LL units -> x);
+//   * shift forces: per-item fp64 partials of the pushers, one deterministic
+//     combine per (rank, wrapped dim) in its own CTA.
+//
+// Each CTA loads one work-item block (128-B XRec / GRec + map slice / task
+// records) per item with one bulk (TMA) copy on an mbarrier, the next one
+// while it processes the current: after an L2 flush the plan costs one memory
+// round trip, not a chain of dependent loads.  Items are processed in a static
+// order in which every wait targets an earlier item, every CTA
+// of the grid is co-resident, and launches use programmatic dependent launch.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -126,9 +134,9 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x_ll(const __grid_constan
     const uint32_t n = r.n_units;
     const uint32_t B = blockDim.x;
     if (r.kind == kItemXRecv) {
-      // this rank's halo rows of one pulse: LL units -> x rows.  Receive items are
-      // larger than send items (HALO_RECV_MULT x rows, runtime.cu) and always take
-      // 4 units per thread per batch: the polls of a batch are in flight together.
+      // this rank's halo rows of one pulse from another GPU: LL units -> x rows
+      // (HALO_RECV_MULT x the send item rows, default 1); 4 units per thread per
+      // batch: the polls of a batch are in flight together.
       constexpr int kR = 4;
       for (uint32_t base = threadIdx.x; base < n; base += kR * B) {
         uint64_t w[kR];
