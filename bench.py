@@ -644,9 +644,15 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    # one process per GPU (LOCAL_RANK = device).  HALO_BENCH_PG=gloo + more processes than GPUs
+    # (device = LOCAL_RANK mod GPUs) only checks the N-process path on a smaller box: not a bench value
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        if os.environ.get("HALO_BENCH_PG", "nccl") == "gloo":
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
     out = run_fused(args, rank, world, local)
     if rank == 0:
         print(json.dumps(out), flush=True)
