@@ -64,3 +64,23 @@ def test_null_ctx_calls_are_errors():
     assert lib.halo_exchange_f(None, None, 1, None) == 1
     assert lib.halo_sync(None) == 1
     assert lib.halo_destroy(None) == 0
+
+
+def test_flag_constants_match_header():
+    """Every HALO_F_* flag of include/halo.h has the same value in the Python binding and
+    in bench.py's protocol table (no drift between the ABI and its users)."""
+    with open(os.path.join(ROOT, "include", "halo.h")) as f:
+        src = f.read()
+    flags = {m.group(1): 1 << int(m.group(2)) for m in re.finditer(r"#define (HALO_F_\w+)\s+\(1u << (\d+)\)", src)}
+    assert len(flags) >= 11
+    for name, val in flags.items():
+        assert getattr(_lib, name) == val, name
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert bench.PROTO_FLAGS["paper"] == flags["HALO_F_PAPER_FLAGS"]
+    assert bench.PROTO_FLAGS["ce"] == flags["HALO_F_CE_PATH"]
+    assert bench.PROTO_FLAGS["auto"] == flags["HALO_F_AUTO_TRANSPORT"]
+    assert bench.PROTO_FLAGS["paper_tma"] == (flags["HALO_F_PAPER_FLAGS"] | flags["HALO_F_TMA_STORE"]
+                                              | flags["HALO_F_TMA_GET"])
