@@ -265,21 +265,27 @@ HALO_API halo_status halo_get_map(const halo_ctx* ctx, int local, int pulse, int
 /* COLLECTIVE, asynchronous, HOT PATH (Alg. 3 FusedPackCommX, Alg. 4, Alg. 5):
  * one kernel launch on `stream` that, for every local rank and pulse, gathers
  * x rows through the map, adds the periodic shift (float32 add of the full
- * 3-vector on the wrapping rank, R25), writes them straight into the receiver's
- * x at its atomOffset over NVLink peer stores, forwards dependent rows after an
- * acquire-wait on the flags of exactly the pulses they came from (R9), and
- * notifies each receiver with one system-scope release store per pulse.
+ * 3-vector on the wrapping rank, R25) and writes them to the receiver over
+ * NVLink peer stores; dependent rows are forwarded once the rows they come from
+ * have arrived (R8/R9).  Default (LL protocol): every 8-B store carries the
+ * step's sequence tag, a receiver on another GPU copies its tagged units into x,
+ * a receiver on this GPU gets its rows stored directly, and forwarding waits per
+ * row; HALO_F_PAPER_FLAGS: the paper's per-pulse scheme — rows straight into the
+ * receiver's x at its atomOffset, one system-scope release flag per pulse
+ * (P:427), acquire-waits on exactly the pulses a dependent chunk reads.
  * When `stream` has executed it, rows [n_home, n_total) hold this step's halo.
  * CUDA-graph capturable (the sequence number lives in device memory).
  * Precondition (R17): steps alternate exchange_x / exchange_f on all ranks. */
 HALO_API halo_status halo_exchange_x(halo_ctx* ctx, void* stream);
 
 /* COLLECTIVE, asynchronous, HOT PATH (Alg. 6 FusedCommUnpackF, Alg. 5 DEP_MGMT):
- * one kernel launch: each halo slice is pushed back to the rank that sent it
- * once every later pulse that forwarded rows of it has been unpacked locally
- * (P:412), and received slices are scatter-added into f through the map
- * (pulses descending, one float32 add per entry: bit-exact vs the oracle, R15;
- * HALO_F_ATOMIC_UNPACK: unordered).  fshift (device, [n_local][3][3] float64,
+ * one kernel launch: each halo slice row is pushed back to the rank that sent it
+ * once every later pulse that forwarded it has delivered its force (P:412,
+ * P:421), and the received forces are added into f through the maps (pulses
+ * descending, one float32 add per entry: bit-exact vs the oracle, R15).  Default
+ * (LL protocol): a deterministic gather per target row with row-level DEP_MGMT;
+ * HALO_F_PAPER_FLAGS: per-pulse push + flag + scatter-add (HALO_F_ATOMIC_UNPACK:
+ * the paper's unordered atomics; HALO_F_TMA_GET: the receiver-driven TMA get).  fshift (device, [n_local][3][3] float64,
  * may be NULL) is ADDED the received force sums of the pulses this rank
  * shifted (R13).  accumulate = 0 overwrites and is only supported with a single
  * pulse in total (R14), else HALO_ERR_UNSUPPORTED.  Halo rows of f keep their
