@@ -348,8 +348,12 @@ def coord_halo_step(states, x_home):
     return xs
 
 
-def force_halo(states, F, fshift_in=None, accumulate=True):
+def force_halo(states, F, fshift_in=None, accumulate=True, with_abs=False, terms_out=None):
     """Serial force halo (R15 order): returns (F_after list, fshift list [3][3] float64).
+    ``with_abs=True`` also returns, per rank, [3][3] float64 sums of |term| over the
+    same shift-force terms (the basis of the fp64 parity tolerance, R13).
+    ``terms_out`` (a list): receives, per rank, [dim][component] lists of the
+    float64 terms that fshift sums (tests of the tolerance's resolution).
 
     F: list of [n_rows_r, width] float32 arrays, the forces on every local row
     of every rank before the exchange (as a non-bonded kernel leaves them).
@@ -383,15 +387,22 @@ def force_halo(states, F, fshift_in=None, accumulate=True):
             if info.shift:
                 for c in range(3):
                     terms[q][info.dim][c].append(buf[:, c].astype(np.float64))
-    fshift = []
+    fshift, fabs = [], []
     for q in range(nr):
         fs = np.zeros((3, 3), dtype=np.float64) if fshift_in is None else np.array(fshift_in[q], dtype=np.float64)
+        fa = np.abs(fs)
         for d in range(3):
             for c in range(3):
                 if terms[q][d][c]:
                     vals = np.concatenate(terms[q][d][c]).tolist()
                     fs[d, c] = math.fsum([float(fs[d, c])] + vals)
+                    fa[d, c] = math.fsum([float(fa[d, c])] + [abs(v) for v in vals])
         fshift.append(fs)
+        fabs.append(fa)
+    if terms_out is not None:
+        terms_out.extend([[[np.concatenate(t) if t else np.zeros(0) for t in td] for td in tq] for tq in terms])
+    if with_abs:
+        return Fo, fshift, fabs
     return Fo, fshift
 
 

@@ -149,7 +149,18 @@ struct MigCtrl {
 // HALO_DEBUG bits: protocol mutations for the dependency-safety tests (G3);
 // never set in production.
 enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u, kCountNotify = 64u, kFenceAfterPeerStores = 128u,
-                   kLocalSink = 256u };  // timing experiment: peer stores go to own memory, receivers do not wait
+                   kLocalSink = 256u,  // timing experiment: peer stores go to own memory, receivers do not wait
+                   // G3 (ii): paper protocol, the a4/a5 pulse flags without release semantics (no
+                   // per-CTA fence, relaxed counter, relaxed flag store)
+                   kMutateRelaxedFlags = 512u,
+                   // G3 (iv): paper protocol, the paper-literal firstDependentPulse (x0 -> y0
+                   // only): a dependent item waits only for pulse p-1, not its whole dependency set (R9)
+                   kMutatePaperQ9 = 1024u,
+                   // slow producer (not a mutation; widens races for the G3 tests): the x send
+                   // items of pulse 0 sleep ~20 us before their data stores
+                   kDelayPulse0 = 2048u,
+                   // fshift partials accumulated in fp32 (shows the 1e-12 * sum|terms| bound catches it)
+                   kMutateFshiftF32 = 4096u};
 
 struct RankDev {
   float* x;                 // own x (capacity rows)

@@ -131,12 +131,17 @@ __device__ __forceinline__ void x_rows_tma(const PulseDev& pd, const float* __re
 // increments the pulse's completion counter; the last CTA stores the flag
 // (Alg. 5: "only threadIdx.x = 0 proceeds to notify").
 __device__ __forceinline__ void pulse_complete_sys(unsigned flags, uint32_t* cnt, int n_items, uint64_t* flag_dst,
-                                                   uint64_t seq, uint32_t* notify_count) {
-  if (flags & HALO_F_GPU_FENCE) fence_gpu(); else fence_sys();
-  uint32_t old = atom_add_acqrel_gpu(cnt, 1u);
+                                                   uint64_t seq, uint32_t* notify_count, bool relaxed = false) {
+  uint32_t old;
+  if (relaxed) {  // G3 (ii) mutation: no release anywhere on the notification path
+    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+  } else {
+    if (flags & HALO_F_GPU_FENCE) fence_gpu(); else fence_sys();
+    old = atom_add_acqrel_gpu(cnt, 1u);
+  }
   if (old == (uint32_t)n_items - 1) {
     *cnt = 0;  // no other CTA of this launch touches it again
-    st_release_sys(flag_dst, seq);
+    if (relaxed) st_relaxed_sys(flag_dst, seq); else st_release_sys(flag_dst, seq);
     if (notify_count) atomicAdd(notify_count, 1u);  // debug (pin G4): one notification per pulse per step
   }
 }
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
       // from (R9; pulses below p_lo completed in earlier launches), then a barrier.
       if (threadIdx.x == 0) {
         uint32_t m = pd.dep_x & ~lo_mask;
+        if (P.debug & kMutatePaperQ9) m &= (1u << w.pulse) >> 1;  // G3 (iv): only firstDependentPulse = p-1
         while (m) {
           const int q = __ffs(m) - 1;
           m &= m - 1;
@@ -170,6 +176,10 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
       }
       __syncthreads();
     }
+    if ((P.debug & kDelayPulse0) && w.pulse == 0) {  // slow producer (G3 race widening)
+      const uint64_t t0 = gtimer();
+      while (gtimer() - t0 < 20000) __nanosleep(1000);
+    }
     if constexpr (kTma)
       x_rows_tma<W>(pd, rd.x, w.begin, w.end, dep, s_stage);
     else
@@ -177,7 +187,8 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
     __syncthreads();
     if (threadIdx.x == 0)
       pulse_complete_sys(P.flags, &ctrl->cnt_x[w.lrank][w.pulse], pd.n_items_x, pd.flag_x_dst, seq,
-                         (P.debug & kCountNotify) ? &ctrl->notify[0][w.lrank][w.pulse] : nullptr);
+                         (P.debug & kCountNotify) ? &ctrl->notify[0][w.lrank][w.pulse] : nullptr,
+                         (P.debug & kMutateRelaxedFlags) != 0);
   }
   // The launch completes only when this process's halos are complete, so that
   // stream-ordered consumers (non-local NB) see them.
@@ -220,7 +231,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 // into shared memory (HALO_F_TMA_GET).
 template <int W, bool kSmem>
 __device__ __forceinline__ void unpack_rows(const PulseDev& pd, const float* buf, float* __restrict__ f, uint32_t b,
-                                            uint32_t e, bool atomic, bool accumulate, double* fshift_rank) {
+                                            uint32_t e, bool atomic, bool accumulate, double* fshift_rank,
+                                            bool f32 = false) {
   const int32_t* __restrict__ map = pd.map;
   const bool do_shift = (fshift_rank != nullptr) && pd.has_shift;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -257,6 +269,7 @@ __device__ __forceinline__ void unpack_rows(const PulseDev& pd, const float* buf
   }
   if (do_shift) {
     a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2);
+    if (f32) { a0 = (double)(float)a0; a1 = (double)(float)a1; a2 = (double)(float)a2; }  // mutation: fp32 partials
     if ((threadIdx.x & 31) == 0) {
       double* fs = fshift_rank + 3 * pd.dim;
       atomicAdd(fs + 0, a0); atomicAdd(fs + 1, a1); atomicAdd(fs + 2, a2);
@@ -310,7 +323,8 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
       __syncthreads();
       if (threadIdx.x == 0)
         pulse_complete_sys(P.flags, &ctrl->cnt_push[w.lrank][w.pulse], pd.n_items_push, pd.flag_f_dst, seq,
-                           (P.debug & kCountNotify) ? &ctrl->notify[1][w.lrank][w.pulse] : nullptr);
+                           (P.debug & kCountNotify) ? &ctrl->notify[1][w.lrank][w.pulse] : nullptr,
+                           (P.debug & kMutateRelaxedFlags) != 0);
     } else {  // kItemUnpack
       if (threadIdx.x == 0) {
         wait_geq<true>(&rd.hdr->flag_f[w.pulse], seq, P.timeout_ns, P.err_host, tcode(4, w.lrank, w.pulse), P.poll_ns);
@@ -341,9 +355,11 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
       if constexpr (kGet) {
         mbar_wait(&s_bar, phase);
         phase ^= 1u;
-        unpack_rows<W, true>(pd, buf, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs);
+        unpack_rows<W, true>(pd, buf, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs,
+                             (P.debug & kMutateFshiftF32) != 0);
       } else {
-        unpack_rows<W, false>(pd, buf, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs);
+        unpack_rows<W, false>(pd, buf, rd.f, w.begin, w.end, atomic, P.accumulate != 0, fs,
+                              (P.debug & kMutateFshiftF32) != 0);
       }
       __syncthreads();
       if (threadIdx.x == 0) {

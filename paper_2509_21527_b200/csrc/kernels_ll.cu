@@ -321,11 +321,15 @@ __device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, ui
       if (ptr[k] == nullptr) continue;
       if ((uint32_t)(hv[k] >> 32) != tag) hv[k] = ll_spin(ptr[k], tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0);
       if ((uint32_t)(lv[k] >> 32) != tag) lv[k] = ll_spin(ptr[k] + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0);
-      s_red[dc[k]][threadIdx.x] += __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
+      const double v = __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
+      s_red[dc[k]][threadIdx.x] = (P.debug & kMutateFshiftF32) ? (double)((float)s_red[dc[k]][threadIdx.x] + (float)v)
+                                                                : s_red[dc[k]][threadIdx.x] + v;
     }
   }
   const double tot = cta_reduce<3>(s_red, threadIdx.x);
-  if (threadIdx.x < 3) P.fshift[9 * g.lrank + 3 * dim + threadIdx.x] = fs_old + tot;
+  if (threadIdx.x < 3)
+    P.fshift[9 * g.lrank + 3 * dim + threadIdx.x] =
+        (P.debug & kMutateFshiftF32) ? (double)((float)fs_old + (float)tot) : fs_old + tot;
 }
 
 // kF = units per thread per batch (1: latency regime, 2: large items), as kU above.
@@ -469,7 +473,8 @@ __global__ void __launch_bounds__(kThreadsF, kF == 1 ? 5 * 256 / kThreadsF : 4 *
     if (part) {  // fixed-tree CTA sum of the pushed forces per component -> the x-sender's slot
 #pragma unroll
       for (int j = 0; j < 3; ++j) s_fs[j][threadIdx.x] = (threadIdx.x < S && c == j) ? acc : 0.0;
-      const double tot = cta_reduce<3>(s_fs, threadIdx.x);
+      double tot = cta_reduce<3>(s_fs, threadIdx.x);
+      if (P.debug & kMutateFshiftF32) tot = (double)(float)tot;  // mutation: fp32 partials
       if (threadIdx.x < 3) {
         st_relaxed_sys(g.part + 2 * threadIdx.x, ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));
         st_relaxed_sys(g.part + 2 * threadIdx.x + 1, ll_pack(__uint_as_float((uint32_t)__double2loint(tot)), tag));

@@ -26,8 +26,7 @@ class FuzzCase:
         self.capacity = max(max(s.x.shape[0] for s in self.states), 1) + 64
         mk = forces_int if seed % 2 == 0 else forces_normal
         self.F = [mk(s.x.shape[0], 31 * seed + s.rank, width=self.layout) for s in self.states]
-        self.Fo, self.fshift = force_halo(self.states, [f.copy() for f in self.F])
-        self.fabs_total = float(sum(np.abs(f[:, :3].astype(np.float64)).sum() for f in self.F))
+        self.Fo, self.fshift, self.fshift_abs = force_halo(self.states, [f.copy() for f in self.F], with_abs=True)
 
     def home_rows(self, r):
         s = self.states[r]

@@ -106,7 +106,7 @@ def _worker_g2(rank, world, port, cases, out):
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
         from paper_2509_21527_b200.nccl_baseline import NcclSchedule
         from paper_2509_21527_b200.session import HaloSession
-        from tests.parity_common import Case, bits, run_gpu_case
+        from tests.parity_common import Case, assert_fshift, bits, run_gpu_case
         for (name, seed, kind) in cases:
             case = Case(name, seed=seed, force_kind=kind)
             if case.nranks != world:
@@ -133,7 +133,7 @@ def _worker_g2(rank, world, port, cases, out):
                 torch.cuda.synchronize()
                 np.testing.assert_array_equal(bits(sess.f[0][:n].cpu().numpy()), bits(case.Fo[rank]),
                                               err_msg=f"NCCL schedule f rank {rank}")
-                assert np.all(np.abs(fshift[0].cpu().numpy() - case.fshift[rank]) <= 1e-10 * case.fabs_total)
+                assert_fshift(fshift[0].cpu().numpy(), case.fshift[rank], case.fshift_abs[rank], where="nccl")
                 dist.barrier()
                 # the fused / CE path still runs after the baseline touched the buffers
                 run_gpu_case(case, sess, steps=1, barrier=dist.barrier)

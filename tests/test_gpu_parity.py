@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.parity_common import Case, run_gpu_case, bits
+from tests.parity_common import Case, assert_fshift, bits, run_gpu_case
 
 pytestmark = pytest.mark.gpu
 
@@ -424,7 +424,7 @@ def test_parity_under_concurrent_compute(proto):
         for l in range(sess.n_local):
             n = case.F[l].shape[0]
             np.testing.assert_array_equal(bits(sess.f[l][:n].cpu().numpy()), bits(case.Fo[l]))
-            assert np.all(np.abs(fs[l] - case.fshift[l]) <= 1e-10 * case.fabs_total)
+            assert_fshift(fs[l], case.fshift[l], case.fshift_abs[l], where=f"rank {l}")
     sess.destroy()
 
 

@@ -385,3 +385,72 @@ def test_fuzz_geometries_pinned(seed):
     for d in range(3):
         exp = sum(f[s.s[:, d] == 1].astype(np.float64).sum(axis=0) for s, f in zip(st, F))
         np.testing.assert_array_equal(fs_tot[d], exp)
+
+
+# ---------------------------------------------------------------- fshift tolerance
+@pytest.mark.parametrize("name", ["T3D", "T2P", "W3"])
+def test_fshift_abs_closed_form_nonnegative_forces(name):
+    """sum|terms| (the fp64 tolerance basis) with every force >= 0 equals fshift itself
+    (no cancellation), and in general |fshift| <= sum|terms| (triangle inequality)."""
+    if name == "W3":
+        g = load("W3.json")
+        L, rc, grid, pulses = tuple(g["L"]), g["rc"], tuple(g["grid"]), tuple(g["pulses"])
+        st = decompose(np.array(g["X"], np.float32), L, rc, grid, pulses)
+    else:
+        c, X = system(name, 3)
+        st = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    F = [np.abs(forces_int(s.x.shape[0], 5 + s.rank)).astype(np.float32) for s in st]
+    _, fs, fa = force_halo(st, F, with_abs=True)
+    for a, b in zip(fs, fa):
+        np.testing.assert_array_equal(a, b)
+    Fn = [forces_normal(s.x.shape[0], 9 + s.rank) for s in st]
+    _, fs, fa = force_halo(st, Fn, with_abs=True)
+    for a, b in zip(fs, fa):
+        assert np.all(np.abs(a) <= b)
+
+
+@pytest.mark.parametrize("name", ["T3D", "T2P", "C1"])
+def test_fshift_tolerance_rejects_fp32(name):
+    """The parity bound for fshift (1e-12 * sum|terms| per rank, dim, component) must
+    tell an fp64 reduction from an fp32 one: re-summing the oracle's own terms in fp64
+    in another order (blocked + pairwise, as a GPU reduction does) passes; the same
+    terms accumulated in fp32 (sequential and pairwise) fail for every case."""
+    from tests.parity_common import fshift_violation
+    c, X = system(name, 2)
+    st = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    F = [forces_normal(s.x.shape[0], 40 + s.rank) for s in st]
+    terms = []
+    _, fs, fa = force_halo(st, F, with_abs=True, terms_out=terms)
+
+    def pairwise(v, dt):
+        v = v.astype(dt)
+        while v.size > 1:
+            if v.size % 2:
+                v = np.append(v, dt(0))
+            v = (v[0::2] + v[1::2]).astype(dt)
+        return dt(v[0]) if v.size else dt(0)
+
+    worst64, worst32s, worst32p = 0.0, [], []
+    for q in range(len(st)):
+        g64 = np.zeros((3, 3))
+        g32s = np.zeros((3, 3))
+        g32p = np.zeros((3, 3))
+        for d in range(3):
+            for comp in range(3):
+                t = terms[q][d][comp]
+                if t.size == 0:
+                    continue
+                blocks = [pairwise(t[i:i + 64], np.float64) for i in range(0, t.size, 64)]
+                g64[d, comp] = sum(blocks)
+                acc = np.float32(0)
+                for v in t.astype(np.float32):
+                    acc = np.float32(acc + v)
+                g32s[d, comp] = acc
+                g32p[d, comp] = pairwise(t, np.float32)
+        if np.any(fa[q] > 0):
+            worst64 = max(worst64, fshift_violation(g64, fs[q], fa[q]))
+            worst32s.append(fshift_violation(g32s, fs[q], fa[q]))
+            worst32p.append(fshift_violation(g32p, fs[q], fa[q]))
+    assert worst64 <= 1.0
+    assert worst32s and min(worst32s) > 10.0, worst32s
+    assert min(worst32p) > 10.0, worst32p
