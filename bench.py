@@ -73,7 +73,8 @@ def workload_desc(c, n_gpus, layout):
     return {"workload": f"{c.name}: {c.desc}", "n_atoms": int(c.n_atoms), "grid": list(c.grid),
             "pulses": list(c.pulses), "rc_nm": c.rc, "box_nm": list(c.L), "dd_ranks": c.nranks,
             "dd_ranks_per_gpu": c.nranks // n_gpus, "layout": f"float{layout}", "seed": SEED,
-            "l2": "flushed: 256 MiB write before every timed step",
+            "l2": "flushed: 256 MiB write before every timed step (then f is reset, so the forces are "
+                  "L2-resident as the non-bonded kernel leaves them; x, plan, maps, LL buffers are flushed)",
             "forces": "normal(0,300) float32, reset before every step"}
 
 
@@ -204,8 +205,8 @@ def run_fused(args, rank, world, local):
         sess.exchange_f(fshift=fshift)
 
     for _ in range(args.warmup):
-        reset_f()
         flush.fill_(1.0)
+        reset_f()
         step()
     torch.cuda.synchronize()
     barrier()
@@ -219,23 +220,45 @@ def run_fused(args, rank, world, local):
     torch.cuda.synchronize()
     barrier()
     for k in range(K):
-        reset_f()
         flush.fill_(float(k))
+        reset_f()
         ev[k][0].record(stream)
         sess.exchange_x()
         sess.exchange_f(fshift=fshift)
         ev[k][1].record(stream)
     torch.cuda.synchronize()
     barrier()
-    sampler.stop()
     tot = [ev[k][0].elapsed_time(ev[k][1]) * 1e3 for k in range(K)]
+    # the same steps as ONE fused launch each (halo_exchange_xf, LL protocol)
+    fused = None
+    if transport == "ll" and not args.no_fused:
+        for _ in range(args.warmup):
+            flush.fill_(1.0)
+            reset_f()
+            sess.exchange_xf(fshift=fshift)
+        torch.cuda.synchronize()
+        barrier()
+        evf = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+        for k in range(K):
+            flush.fill_(float(k))
+            reset_f()
+            evf[k][0].record(stream)
+            sess.exchange_xf(fshift=fshift)
+            evf[k][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        tf_ = [evf[k][0].elapsed_time(evf[k][1]) * 1e3 for k in range(K)]
+        fused = {"us_per_step": max_over_ranks(float(np.mean(tf_))),
+                 "median_us": max_over_ranks(float(np.median(tf_))),
+                 "p90_us": max_over_ranks(float(np.percentile(tf_, 90)))}
+    sampler.stop()
     # per-kernel split (roofline): isolated steps (device idle, ranks released together by a
     # host barrier), events around each kernel, same flush discipline
     Kx = min(K, 200)
     ev3 = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(Kx)]
     for k in range(Kx):
-        reset_f()
         flush.fill_(float(k))
+        reset_f()
         torch.cuda.synchronize()
         barrier()
         # ~40 us of GPU sleep: the host enqueues x and f behind it, so the events time
@@ -274,8 +297,8 @@ def run_fused(args, rank, world, local):
         barrier()
         gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
         for k in range(min(K, 2000) + args.warmup):
-            reset_f()
             flush.fill_(1.0)
+            reset_f()
             kk = k - args.warmup
             if kk >= 0:
                 gev[kk][0].record(stream)
@@ -390,6 +413,9 @@ def run_fused(args, rank, world, local):
                           "before each, so both launches are queued; events around each launch, i.e. no "
                           "programmatic dependent launch across the middle event), so x_us + f_us > value",
         "graph_us_per_step": None if graph_us is None else round(graph_us, 3),
+        "fused_xf": None if fused is None else {k: round(v, 3) for k, v in fused.items()} | {
+            "path": "halo_exchange_xf: x and f of the step in ONE launch; rank l's gather items start when "
+                    "l's halo rows are complete (the non-bonded kernel's slot, Alg. 2)"},
         "clocks": sampler.summary(),
         "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
                 "d2h_bytes_per_step": int(d2h) * world, "path": "halo_step_host (C ABI, pinned host buffers)"},
@@ -624,6 +650,7 @@ def main():
     ap.add_argument("--timers", action="store_true")
     ap.add_argument("--l2-persist", action="store_true", help="HALO_F_L2_PERSIST: static plan in persisting L2")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-fused", action="store_true", help="skip the fused x+f launch (halo_exchange_xf) timing")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-floors", action="store_true", help="skip the latency/bandwidth/launch floor probes")

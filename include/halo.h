@@ -112,6 +112,10 @@ typedef enum {
                                            crossover on B200), then the copy-engine path.  Decided
                                            collectively in halo_set_maps (all ranks agree); results identical.
                                            Not combinable with PAPER_FLAGS / CE_PATH / TMA_*.  */
+#define HALO_F_NCCL_BASELINE  (1u << 11) /* halo_exchange_x / halo_exchange_f run the NCCL send/recv schedule
+                                           (halo_nccl_exchange_x / _f; needs halo_nccl_init): the BASELINE the
+                                           fused kernels are measured against, not a
+                                           product transport.  set_maps still builds the maps on the GPU. */
 
 typedef struct {
   int grid[3];        /* cells per dim (np_x, np_y, np_z), each >= 1 */
@@ -175,8 +179,10 @@ HALO_API halo_status halo_ipc_import(halo_ctx* ctx, const void* blobs, size_t le
  * the coordinates pulse by pulse (forwarding needs the earlier pulses' rows).
  * Selection (R2, R3): float64(x_d) - b_d[c_d] < float64(rc), strict, over the
  * candidate rows (k = 0: all rows present before the dim's first pulse; k > 0:
- * rows received in pulse (d, k-1)), ascending row order (R11).  Host-synchronises.
- * Errors are agreed by all ranks (every rank returns the same status). */
+ * rows received in pulse (d, k-1)), ascending row order (R11).  Host-synchronises
+ * (device-wide first: exchanges still running on any stream of this device finish
+ * before the plan they read is rewritten).  Errors are agreed by all ranks (every
+ * rank returns the same status). */
 HALO_API halo_status halo_set_maps(halo_ctx* ctx, const int* n_home, void* stream);
 
 /* COLLECTIVE test entry: like halo_set_maps but with caller-given maps.
@@ -209,10 +215,6 @@ HALO_API halo_status halo_set_maps_explicit(halo_ctx* ctx, const int* n_home, co
 HALO_API halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gid, float* const* v,
                                   int* n_home_out, void* stream);
 
-/* Layout of local rank `local` after set_maps (host arrays sized npulse; any may be NULL):
- * recv_off[p] = atomOffset (P:216), recv_size[p], send_size[p], remote_off[p] = where
- * this rank's pulse-p rows land on its receiver, dep_mask[p] = bit q set iff
- * map_p reads rows received in pulse q (the wait set of Alg. 4, R9). */
 /* ---- PP <-> PME coordinate / force redistribution ----
  * The PME task runs on the GPU of DD rank `pme_rank`.  Its buffers pme_x / pme_f
  * (rows of `layout` floats) hold the home rows of every DD rank concatenated in
@@ -255,6 +257,10 @@ HALO_API halo_status halo_pme_recv_f(halo_ctx* ctx, int accumulate, void* stream
  * 0 = LL protocol, 1 = paper protocol, 2 = copy engine. */
 HALO_API halo_status halo_transport(const halo_ctx* ctx, int* transport);
 
+/* Layout of local rank `local` after set_maps (host arrays sized npulse; any may be NULL):
+ * recv_off[p] = atomOffset (P:216), recv_size[p], send_size[p], remote_off[p] = where
+ * this rank's pulse-p rows land on its receiver, dep_mask[p] = bit q set iff
+ * map_p reads rows received in pulse q (the wait set of Alg. 4, R9). */
 HALO_API halo_status halo_get_layout(const halo_ctx* ctx, int local, int* n_home, int* n_total, int* npulse,
                             int* recv_off, int* recv_size, int* send_size, int* remote_off,
                             unsigned* dep_mask);
@@ -274,7 +280,9 @@ HALO_API halo_status halo_get_map(const halo_ctx* ctx, int local, int pulse, int
  * receiver's x at its atomOffset, one system-scope release flag per pulse
  * (P:427), acquire-waits on exactly the pulses a dependent chunk reads.
  * When `stream` has executed it, rows [n_home, n_total) hold this step's halo.
- * CUDA-graph capturable (the sequence number lives in device memory).
+ * CUDA-graph capturable (the sequence number lives in device memory).  A captured
+ * launch holds the plan of the NS epoch it was captured in: re-capture after every
+ * halo_set_maps / halo_migrate (a graph replayed across them reads a stale or freed plan).
  * Precondition (R17): steps alternate exchange_x / exchange_f on all ranks. */
 HALO_API halo_status halo_exchange_x(halo_ctx* ctx, void* stream);
 
@@ -291,6 +299,43 @@ HALO_API halo_status halo_exchange_x(halo_ctx* ctx, void* stream);
  * pulse in total (R14), else HALO_ERR_UNSUPPORTED.  Halo rows of f keep their
  * values.  CUDA-graph capturable. */
 HALO_API halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void* stream);
+
+/* COLLECTIVE, asynchronous: exchange_x and exchange_f of one step in ONE launch
+ * (LL protocol only, "a single kernel for x+f when no compute
+ * sits between them" — the paper's one-launch-per-exchange design, taken
+ * one step further for a step with no non-bonded work between the halves).
+ * Results are identical to halo_exchange_x followed by halo_exchange_f with the
+ * same arguments (bit-exact).  Ordering inside the launch: the gather items of a
+ * local rank start only once every x item that completes that rank's halo rows
+ * has finished in this launch — the place of the non-bonded kernel of Alg. 2,
+ * so f may be written by nothing between the halves: the forces in
+ * f when the launch starts are the ones exchanged.  HALO_ERR_UNSUPPORTED for
+ * the paper / copy-engine transports.  CUDA-graph capturable. */
+HALO_API halo_status halo_exchange_xf(halo_ctx* ctx, double* fshift, int accumulate, void* stream);
+
+/* ---- NCCL send/recv baseline (pin G2) ----
+ * The paper's serialized schedule (Fig. 1) on the maps of
+ * the last halo_set_maps: per pulse ascending a pack kernel (gather + shift) and
+ * one ncclGroupStart / ncclSend (to the lower neighbour) / ncclRecv (the upper
+ * neighbour's rows straight into this rank's halo range) / ncclGroupEnd; forces
+ * per pulse descending: one group sending the halo slice back to the x-sender and
+ * receiving this rank's slice, then the ordered scatter-add kernel (+ fp64 shift
+ * forces).  All on `stream`: eager or captured in a CUDA graph.  Results are
+ * bit-identical to the fused path.  One DD rank per process (nprocs == nranks,
+ * NCCL rank = DD rank); NCCL is the libnccl.so.2 the process already loaded
+ * (torch's), else dlopen("libnccl.so.2") / $HALO_NCCL_LIB. */
+
+/* ncclGetUniqueId: id == NULL -> *len = 128; else writes the id (caller broadcasts it). */
+HALO_API halo_status halo_nccl_unique_id(void* id, size_t* len);
+/* COLLECTIVE over all processes: ncclCommInitRank(nprocs, id, proc). */
+HALO_API halo_status halo_nccl_init(halo_ctx* ctx, const void* id, size_t len);
+/* ncclGetVersion of the resolved library (0 if none). */
+HALO_API halo_status halo_nccl_version(int* version);
+/* COLLECTIVE, asynchronous: the baseline x halo (P pack kernels + P NCCL groups). */
+HALO_API halo_status halo_nccl_exchange_x(halo_ctx* ctx, void* stream);
+/* COLLECTIVE, asynchronous: the baseline force halo (P NCCL groups + P unpack kernels);
+ * fshift / accumulate as halo_exchange_f. */
+HALO_API halo_status halo_nccl_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void* stream);
 
 /* COLLECTIVE end-to-end step through host buffers (the e2e measurement path):
  * per local rank copies x_home[l] (n_home*layout floats, pinned host) and

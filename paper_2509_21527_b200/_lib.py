@@ -25,6 +25,7 @@ HALO_F_TMA_STORE = 1 << 7
 HALO_F_TMA_GET = 1 << 8
 HALO_F_ROUNDED_ZONES = 1 << 9
 HALO_F_AUTO_TRANSPORT = 1 << 10
+HALO_F_NCCL_BASELINE = 1 << 11
 HALO_MAX_PULSES = 6
 
 # every symbol include/halo.h declares (checked by tests/test_abi.py)
@@ -32,7 +33,8 @@ EXPORTS = [
     "halo_init", "halo_query_config", "halo_local_ranks", "halo_pulse_order", "halo_scratch_bytes", "halo_register_buffers",
     "halo_ipc_export", "halo_ipc_import", "halo_set_maps", "halo_set_maps_explicit", "halo_get_layout",
     "halo_get_map", "halo_migrate", "halo_transport", "halo_pme_reserve", "halo_pme_setup",
-    "halo_pme_buffers", "halo_pme_send_x", "halo_pme_recv_f", "halo_exchange_x", "halo_exchange_f", "halo_step_host", "halo_pack_x_pulse",
+    "halo_pme_buffers", "halo_pme_send_x", "halo_pme_recv_f", "halo_exchange_x", "halo_exchange_f", "halo_exchange_xf", "halo_nccl_unique_id", "halo_nccl_init", "halo_nccl_version", "halo_nccl_exchange_x",
+    "halo_nccl_exchange_f", "halo_step_host", "halo_pack_x_pulse",
     "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_launch_remote", "halo_floor_bandwidth", "halo_sync", "halo_strerror",
     "halo_last_error", "halo_destroy",
 ]
@@ -80,6 +82,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_pme_recv_f": ([P, c_int, P], c_int),
         "halo_exchange_x": ([P, P], c_int),
         "halo_exchange_f": ([P, P, c_int, P], c_int),
+        "halo_exchange_xf": ([P, P, c_int, P], c_int),
+        "halo_nccl_unique_id": ([P, POINTER(c_size_t)], c_int),
+        "halo_nccl_init": ([P, P, c_size_t], c_int),
+        "halo_nccl_version": ([IP], c_int),
+        "halo_nccl_exchange_x": ([P, P], c_int),
+        "halo_nccl_exchange_f": ([P, P, c_int, P], c_int),
         "halo_step_host": ([P, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), P, P], c_int),
         "halo_pack_x_pulse": ([P, c_int, c_int, P, P], c_int),
         "halo_unpack_f_pulse": ([P, c_int, c_int, P, P, c_int, P], c_int),

@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhalo.so")
-SOURCES = ["runtime.cu", "kernels.cu", "kernels_ll.cu", "kernels_ce.cu", "kernels_ns.cu", "kernels_pme.cu"]
+SOURCES = ["runtime.cu", "kernels.cu", "kernels_ll.cu", "kernels_ce.cu", "kernels_ns.cu", "kernels_pme.cu",
+           "nccl_baseline.cu"]
 HEADERS = ["halo_internal.h", "ptx.cuh", os.path.join("..", "..", "include", "halo.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -45,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-           "-Xcompiler", "-fPIC", *objs, "-lpthread", "-o", tmp]
+           "-Xcompiler", "-fPIC", *objs, "-lpthread", "-ldl", "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -28,8 +28,10 @@ constexpr int kMaxRanks = HALO_MAX_RANKS;
 constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
 constexpr int kHdrBytes = 8192;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
+constexpr int kTraceW = 16;            // ... words per CTA: 4 stamps + (tag, end) of its first 6 items
 constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-force slot area)
 constexpr int kMaxItemRows = 512;      // largest work item (x items carry their map slice in shared memory)
+constexpr int kRing = 4;               // LL kernels: item blocks in flight per CTA (narrow variants)
 constexpr uint32_t kPollTight = 0xffffffffu;  // ExParams.poll_ns: tight polling only, no backoff (HALO_POLL_NS=-1)
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
@@ -81,9 +83,9 @@ struct Ctrl {
   int32_t err[kMaxLocal];                 // set_maps error bits (kErr*)
   int32_t agreed_err[kMaxLocal];          // OR over all ranks after the status exchange
   // HALO_F_TIMERS: per-CTA %globaltimer stamps of the last x (0) / f (1) launch:
-  // [start, plan record loaded, items done, exit, item0 tag, item0 end, item1 tag, item1 end]
+  // [start, plan record loaded, items done, exit, item0 tag, item0 end, ..., item5 tag, item5 end]
   // tag = kind << 16 | lrank << 8 | pulse (level)
-  uint64_t trace[2][kTraceCTAs][8];
+  uint64_t trace[2][kTraceCTAs][kTraceW];
   // HALO_DEBUG & kCountNotify (pin G4): system-scope flag stores per (x/f, local rank, pulse), cumulative
   uint32_t notify[2][kMaxLocal][kMaxP];
   // PP <-> PME (kernels_pme.cu)
@@ -91,10 +93,15 @@ struct Ctrl {
   uint32_t done_pme[2];
   uint32_t cnt_pme[2][kMaxLocal];
   int32_t pme_nh[kMaxLocal][kMaxRanks];   // halo_pme_setup: n_home of every rank, seen by local rank l
+  // LL x items finished into each local rank's halo in this NS epoch (zeroed by
+  // set_maps): the fused x+f launch starts rank l's gather items at xin_n x launches
+  uint64_t xin[kMaxLocal];
 };
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4,
-                 kVoteCE = 256 };  // not an error: HALO_F_AUTO_TRANSPORT vote, ORed by the status exchange
+                 kVoteCE = 256,     // not errors: votes ORed by the status exchange (HALO_F_AUTO_TRANSPORT,
+                 kVoteRows = 4096,  // work-item size one-hot: kVoteRows << log2(R / kMinItemRows))
+                 kVoteRowsMask = 31 * 4096};
 
 // ---------------------------------------------------------------- halo_migrate
 // (csrc/kernels_ns.cu).  The stencil of a rank = the distinct
@@ -156,8 +163,9 @@ enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u, kCountNotify = 64u
                    // G3 (iv): paper protocol, the paper-literal firstDependentPulse (x0 -> y0
                    // only): a dependent item waits only for pulse p-1, not its whole dependency set (R9)
                    kMutatePaperQ9 = 1024u,
-                   // slow producer (not a mutation; widens races for the G3 tests): the x send
-                   // items of pulse 0 sleep ~20 us before their data stores
+                   // slow producer (not a mutation; widens races for the G3 tests): the pulse-0
+                   // x send items of ONE rank (the one sending to DD rank 0) sleep ~20 us before their
+                   // data stores, so rank 0's z0 rows arrive after everything else
                    kDelayPulse0 = 2048u,
                    // fshift partials accumulated in fp32 (shows the 1e-12 * sum|terms| bound catches it)
                    kMutateFshiftF32 = 4096u};
@@ -232,6 +240,8 @@ struct __align__(128) XRec {
   const uint64_t* xll_own;  // dep send: own coordinate LL base (slot q at + q*ll_stride)
   int32_t recv_off[kMaxP];  // dep send: own receive ranges
   int32_t recv_size[kMaxP];
+  uint64_t* xin;            // &ctrl->xin[l] of the local rank whose halo rows this item completes, or null
+  uint64_t pad;
 };
 static_assert(sizeof(XRec) == 128, "XRec must be one 128-B line");
 
@@ -251,7 +261,9 @@ struct __align__(128) GRec {
                             // shift-force slot of this item (3 doubles = 6 LL units, peer pointer);
                             // combine: own shift-force slot area
   uint32_t nslot[kMaxP];    // combine: slots of each pulse (0 unless this rank shifted in it)
-  uint8_t pad2[128 - 88];   // keep one 128-B line
+  const uint64_t* xin;      // fused launch: &ctrl->xin[lrank] (gather items wait for xin_n per x launch)
+  uint32_t xin_n;           // x items that complete this rank's halo rows
+  uint8_t pad2[128 - 100];  // keep one 128-B line
 };
 static_assert(sizeof(GRec) == 128, "GRec must be one 128-B line");
 
@@ -279,6 +291,11 @@ struct ExParams {
   const char* xblk;         // LL x item blocks: [XRec | map slice, item_rows int32], 128 + 4*item_rows B each
   const char* fblk;         // LL f item blocks: [GRec | task records, item_rows x 32 B], 128 + 32*item_rows B each
   int item_rows;
+  int n_items_x;            // fused launch: items [0, n_items_x) are x items, then the f items
+  int ring;                 // LL: item-block ring slots per CTA
+  uint64_t seq_f;           // fused launch: the f sequence number by value (0 = read ctrl->seq_f + 1)
+  uint64_t seq_x0;          // fused launch: ctrl->seq_x at the end of set_maps (xin counts from there)
+  int delay_rank;           // HALO_DEBUG kDelayPulse0: the DD rank whose pulse-0 sends are slowed
 };
 
 // Copy-engine path (HALO_F_CE_PATH, kernels_ce.cu): one entry per (pulse, local rank).

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) k_exchange_x(const __grid_constant__
       }
       __syncthreads();
     }
-    if ((P.debug & kDelayPulse0) && w.pulse == 0) {  // slow producer (G3 race widening)
+    if ((P.debug & kDelayPulse0) && w.pulse == 0 && rd.rank == P.delay_rank) {  // slow producer (G3)
       const uint64_t t0 = gtimer();
       while (gtimer() - t0 < 20000) __nanosleep(1000);
     }

@@ -34,17 +34,24 @@ cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* 
                             double* fs_dim, cudaStream_t st);
 cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
-cudaError_t launch_exchange_x_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
-                                 cudaStream_t st);
-cudaError_t launch_exchange_f_ll(const ExParams& p, int layout, int grid, bool wide, const cudaAccessPolicyWindow* win,
-                                 cudaStream_t st);
-cudaError_t max_coresident_ll(int layout, bool wide, int* x_blocks, int* f_blocks);
+cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
+                               const cudaAccessPolicyWindow* win, cudaStream_t st);
+cudaError_t max_coresident_ll(int layout, bool wide, int* blocks);
+int ll_ring(bool wide);
 cudaError_t launch_empty(int grid, cudaStream_t st, uint64_t* remote, uint32_t nwords);
 cudaError_t launch_ce_pack(int layout, const CeEnt* ents, int n_local, int max_rows, cudaStream_t st);
 cudaError_t launch_ce_unpack(int layout, const CeEnt* ents, int n_local, int max_rows, double* fshift, int accumulate,
                              cudaStream_t st);
 cudaError_t launch_ce_sync(const CeSyncParams& s, cudaStream_t st);
 cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
+// NCCL send/recv baseline (nccl_baseline.cu)
+bool nccl_available(std::string* why);
+int nccl_version();
+bool nccl_unique_id(void* out, std::string* why);
+void* nccl_comm_init(const void* id, int nranks, int rank, std::string* why);
+void nccl_comm_destroy(void* comm);
+std::string nccl_sendrecv(void* comm, const float* sbuf, size_t sn, int speer, float* rbuf, size_t rn, int rpeer,
+                          cudaStream_t st);
 }  // namespace halo
 
 using namespace halo;
@@ -175,12 +182,14 @@ struct halo_ctx {
   uint32_t epoch = 0;
   uint64_t ping_base = 0;
   cudaAccessPolicyWindow l2win{};    // HALO_F_L2_PERSIST: the static plan (item blocks) persists in L2
-  int max_x = 0, max_f = 0;         // co-resident CTAs of the exchange kernels (LL: narrow variants)
-  int max_x_w = 0, max_f_w = 0;     // LL: batched variants for large work items
+  int max_x = 0, max_f = 0, max_xf = 0;        // co-resident CTAs of the exchange kernels (LL: narrow variants)
+  int max_x_w = 0, max_f_w = 0, max_xf_w = 0;  // LL: batched variants for large work items
   int grid_cap = 0;                 // HALO_CTAS_PER_SM x SMs (0 = occupancy limit only)
   bool wide() const { return ll && item_rows >= 256; }
   int cap_x() const { const int c = wide() ? max_x_w : max_x; return grid_cap ? std::min(c, grid_cap) : c; }
   int cap_f() const { const int c = wide() ? max_f_w : max_f; return grid_cap ? std::min(c, grid_cap) : c; }
+  int cap_xf() const { const int c = wide() ? max_xf_w : max_xf; return grid_cap ? std::min(c, grid_cap) : c; }
+  uint64_t seq_x0 = 0;              // ctrl->seq_x when set_maps ended (the fused launch's xin base)
   int last_grid[2] = {0, 0};
   int item_rows = 64;
   bool item_rows_fixed = false;     // HALO_ITEM_ROWS given: no adaptive choice
@@ -195,6 +204,10 @@ struct halo_ctx {
   size_t auto_ce_bytes = (size_t)4 << 20;  // ... copy engine when some pulse sends >= this (HALO_AUTO_CE_BYTES)
   bool direct_x = true;             // LL: same-process receivers get their x rows from the sender (HALO_DIRECT_X=0: off)
   int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
+  // NCCL send/recv baseline (halo_nccl_*, HALO_F_NCCL_BASELINE): communicator + packed send rows
+  void* nccl_comm = nullptr;
+  float* d_nccl_send = nullptr;
+  size_t nccl_send_bytes = 0;
 
   int cell(int r, int d) const {
     const int* g = cfg.grid;
@@ -399,10 +412,16 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_mig, sizeof(MigRank) * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_migctrl, sizeof(MigCtrl));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_planes, sizeof(double) * 3 * (kMaxRanks + 1));
-  if (e == cudaSuccess)
-    e = ctx->ll ? max_coresident_ll(cfg->layout, false, &ctx->max_x, &ctx->max_f)
-                : max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
-  if (e == cudaSuccess && ctx->ll) e = max_coresident_ll(cfg->layout, true, &ctx->max_x_w, &ctx->max_f_w);
+  if (e == cudaSuccess) {
+    // LL occupancy always (HALO_F_AUTO_TRANSPORT can switch a ctx to LL); the paper
+    // protocol's kernels for the paper / copy-engine paths
+    int b[3] = {0, 0, 0}, bw[3] = {0, 0, 0};
+    e = max_coresident_ll(cfg->layout, false, b);
+    if (e == cudaSuccess) e = max_coresident_ll(cfg->layout, true, bw);
+    ctx->max_x = b[0]; ctx->max_f = b[1]; ctx->max_xf = b[2];
+    ctx->max_x_w = bw[0]; ctx->max_f_w = bw[1]; ctx->max_xf_w = bw[2];
+    if (e == cudaSuccess && !ctx->ll) e = max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
+  }
   if (e == cudaSuccess) {
     // HALO_CTAS_PER_SM: cap the exchange grids (fewer, longer-lived CTAs; leaves SM
     // slots to a concurrently running compute kernel, Alg. 2)
@@ -858,10 +877,15 @@ static void build_xrec(halo_ctx* ctx) {
     if (w.kind == kItemXRecv) {
       r.ll = ctx->xll_of(rk) + (size_t)p * ctx->ll_stride + (size_t)w.begin * W;
       r.xdst = ctx->x[l] + (size_t)(ctx->atom_offset[l * P + p] + w.begin) * W;
+      r.xin = &ctx->ctrl->xin[l];
     } else {
       r.map = pd.map + w.begin;
       r.ll = pd.xll_dst + (size_t)w.begin * W;
-      if (ctx->direct_x && ctx->is_local(ctx->neighbour(rk, ctx->pdim[p], -1))) r.xdst = pd.x_dst + (size_t)w.begin * W;
+      const int lower = ctx->neighbour(rk, ctx->pdim[p], -1);
+      if (ctx->direct_x && ctx->is_local(lower)) {
+        r.xdst = pd.x_dst + (size_t)w.begin * W;
+        r.xin = &ctx->ctrl->xin[lower - ctx->first_rank];
+      }
       const auto& m = ctx->h_maps[l][p];
       std::copy(m.begin() + w.begin, m.begin() + w.end, ctx->h_xmap.begin() + k * (size_t)R);
     }
@@ -877,6 +901,10 @@ static void build_xrec(halo_ctx* ctx) {
 static halo_status build_grec(halo_ctx* ctx) {
   const int W = ctx->W, P = ctx->P;
   const int R = ctx->item_rows;
+  // x items that complete each local rank's halo rows (the fused launch's xin targets)
+  std::vector<int> xin_n(ctx->n_local, 0);
+  for (const XRec& r : ctx->h_xrec)
+    if (r.xin != nullptr) xin_n[r.xin - &ctx->ctrl->xin[0]]++;
   ctx->h_grec.assign(ctx->h_items_f.size(), GRec{});
   for (size_t k = 0; k < ctx->h_items_f.size(); ++k) {
     const Item& w = ctx->h_items_f[k];
@@ -894,6 +922,8 @@ static halo_status build_grec(halo_ctx* ctx) {
     }
     g.f = ctx->f[l];
     g.fll_own = ctx->fll_of(rk);
+    g.xin = &ctx->ctrl->xin[l];
+    g.xin_n = (uint32_t)xin_n[l];
     if (w.kind == kItemGather) {
       g.tasks = nullptr;
       if (w.pulse != kHomeLevel) {
@@ -1011,6 +1041,9 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.xblk = ctx->d_xblk;
   P.fblk = ctx->d_fblk;
   P.item_rows = ctx->item_rows;
+  P.ring = ll_ring(ctx->wide());
+  P.delay_rank = ctx->P ? ctx->neighbour(0, ctx->pdim[0], +1) : -1;
+  P.seq_x0 = ctx->seq_x0;
   return P;
 }
 
@@ -1200,6 +1233,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
                                  cudaStream_t st) {
   if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "register buffers and import peers first");
   CK(cudaSetDevice(ctx->cfg.device));
+  // exchanges queued on any stream of this device read the plan rewritten below
+  CK(cudaDeviceSynchronize());
   halo_status s = check_err_word(ctx);
   if (s != HALO_OK) return s;
   PhaseTimer prof;
@@ -1359,7 +1394,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
     if (ctx->ll) {
       X.seq = next_seq(ctx, st, &ctx->seq_host_x);
-      CK(launch_exchange_x_ll(X, W, grid_for(ctx->n_items_x, L, ctx->cap_x()), ctx->wide(), nullptr, st));
+      X.n_items_x = ctx->n_items_x;
+      CK(launch_exchange_ll(X, 0, W, grid_for(ctx->n_items_x, L, ctx->cap_x()), ctx->wide(), nullptr, st));
     }
     if (!ctx->ll)
       CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
@@ -1367,20 +1403,36 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     if ((s = check_err_word(ctx)) != HALO_OK) return s;
   }
   prof.lap("x_pulses");
-  if (ctx->auto_tr) {
-    // HALO_F_AUTO_TRANSPORT: vote for the copy engine if one of this process's
-    // pulses is large (bandwidth regime); the status exchange ORs the votes, so
-    // every rank takes the same transport
-    size_t big = 0, thr = ctx->auto_ce_bytes;
-    if (const char* e = getenv("HALO_AUTO_CE_BYTES")) thr = (size_t)std::max(0LL, atoll(e));  // read per NS step
-    for (int i = 0; i < L * P; ++i) big = std::max(big, (size_t)ctx->send_size[i] * W * sizeof(float));
-    if (big >= thr) {
-      int32_t e[kMaxLocal];
-      CK(cudaMemcpyAsync(e, ctx->ctrl->err, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      for (int l = 0; l < L; ++l) e[l] |= kVoteCE;
-      CK(cudaMemcpyAsync(ctx->ctrl->err, e, sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
+  {
+    // votes that ride on the status exchange (OR over all ranks), so that every
+    // rank of every process takes the same decision:
+    //  * HALO_F_AUTO_TRANSPORT: the copy engine if some pulse is large (bandwidth regime);
+    //  * the work-item size R: the shift-force slot of a pusher's item is indexed by R
+    //    on both sides of a pulse (pusher and combine), so all ranks must use one R:
+    //    one-hot vote kVoteRows << log2(R/32), the largest voted R wins.
+    //    R = 64 rows (latency regime; swept 32-512 at C3) unless this process's pulses
+    //    are so large that a CTA would run more than ~2 items in sequence.
+    int32_t vote = 0;
+    if (ctx->auto_tr) {
+      size_t big = 0, thr = ctx->auto_ce_bytes;
+      if (const char* e = getenv("HALO_AUTO_CE_BYTES")) thr = (size_t)std::max(0LL, atoll(e));  // read per NS step
+      for (int i = 0; i < L * P; ++i) big = std::max(big, (size_t)ctx->send_size[i] * W * sizeof(float));
+      if (big >= thr) vote |= kVoteCE;
     }
+    int R = ctx->item_rows;
+    if (!ctx->item_rows_fixed) {
+      long rows = 0;
+      for (int i = 0; i < L * P; ++i) rows += std::max(ctx->send_size[i], ctx->recv_size[i]);
+      const long ctas = std::max(1, std::min(ctx->max_x, ctx->max_f));
+      R = 64;
+      while (R < kMaxItemRows && rows / R > 2 * ctas) R *= 2;
+    }
+    vote |= kVoteRows << (31 - __builtin_clz((unsigned)(R / kMinItemRows)));
+    int32_t e[kMaxLocal];
+    CK(cudaMemcpyAsync(e, ctx->ctrl->err, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int l = 0; l < L; ++l) e[l] |= vote;
+    CK(cudaMemcpyAsync(ctx->ctrl->err, e, sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
   }
   // error agreement over all ranks
   StatusParams SP{};
@@ -1407,16 +1459,10 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     ctx->ll = false;
     ctx->ce = true;
   }
-  // work-item size: 64 rows (latency regime; swept 32-512 at C3) unless the
-  // pulses are so large that a CTA would run more than ~2 items in sequence —
-  // then larger items (fewer dependent record/map round trips per row)
-  if (!ctx->item_rows_fixed) {
-    long rows = 0;
-    for (int i = 0; i < L * P; ++i) rows += std::max(ctx->send_size[i], ctx->recv_size[i]);
-    const long ctas = std::max(1, std::min(ctx->max_x, ctx->max_f));
-    int R = 64;
-    while (R < kMaxItemRows && rows / R > 2 * ctas) R *= 2;
-    ctx->item_rows = R;
+  {  // the largest work-item size any rank voted for
+    const uint32_t rv = ((uint32_t)any & kVoteRowsMask) / (uint32_t)kVoteRows;
+    if (rv == 0) return fail(ctx, HALO_ERR_STATE, "work-item size vote missing");
+    ctx->item_rows = kMinItemRows << (31 - __builtin_clz(rv));
   }
   prof.lap("status");
   // final plan: all pulses
@@ -1464,9 +1510,13 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   uint64_t seqs[2];
   CK(cudaMemcpyAsync(&seqs[0], &ctx->ctrl->seq_x, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&seqs[1], &ctx->ctrl->seq_f, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  // the fused launch's per-rank halo counters count from here (the per-pulse x
+  // launches above counted too)
+  CK(cudaMemsetAsync(ctx->ctrl->xin, 0, sizeof(ctx->ctrl->xin), st));
   CK(cudaStreamSynchronize(st));
   ctx->seq_host_x = seqs[0];
   ctx->seq_host_f = seqs[1];
+  ctx->seq_x0 = seqs[0];
   prof.lap("plan");
   prof.print(ctx->first_rank);
   ctx->maps_ready = true;
@@ -1736,6 +1786,91 @@ halo_status halo_get_map(const halo_ctx* ctx, int local, int pulse, int* host_ou
   return HALO_OK;
 }
 
+// ------------------------------------------------ NCCL send/recv baseline (G2)
+halo_status halo_nccl_unique_id(void* id, size_t* len) {
+  if (!len) return HALO_ERR_ARG;
+  if (!id) { *len = 128; return HALO_OK; }
+  if (*len < 128) return HALO_ERR_ARG;
+  std::string why;
+  if (!nccl_unique_id(id, &why)) {
+    fprintf(stderr, "halo_nccl_unique_id: %s\n", why.c_str());
+    return HALO_ERR_UNSUPPORTED;
+  }
+  *len = 128;
+  return HALO_OK;
+}
+
+halo_status halo_nccl_init(halo_ctx* ctx, const void* id, size_t len) {
+  if (!ctx || !id || len < 128) return HALO_ERR_ARG;
+  if (ctx->n_local != 1) return fail(ctx, HALO_ERR_UNSUPPORTED, "the NCCL baseline runs one DD rank per process");
+  if (ctx->nccl_comm) return fail(ctx, HALO_ERR_STATE, "NCCL communicator already initialised");
+  CK(cudaSetDevice(ctx->cfg.device));
+  std::string why;
+  ctx->nccl_comm = nccl_comm_init(id, ctx->cfg.nprocs, ctx->cfg.proc, &why);
+  if (!ctx->nccl_comm) return fail(ctx, HALO_ERR_PEER, why);
+  return HALO_OK;
+}
+
+halo_status halo_nccl_version(int* version) {
+  if (!version) return HALO_ERR_ARG;
+  *version = nccl_version();
+  return HALO_OK;
+}
+
+// x: per pulse ascending, pack kernel -> one NCCL group (send to the lower
+// neighbour, receive the upper one's rows into the halo range).
+halo_status halo_nccl_exchange_x(halo_ctx* ctx, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->nccl_comm) return fail(ctx, HALO_ERR_STATE, "halo_nccl_init first");
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "exchange before set_maps");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int W = ctx->W, P = ctx->P, r = ctx->first_rank;
+  size_t rows = 0;
+  for (int p = 0; p < P; ++p) rows += ctx->send_size[p];
+  if (rows * W * sizeof(float) > ctx->nccl_send_bytes) {  // NS-step sizes; first call of the epoch only
+    CK(cudaDeviceSynchronize());
+    if (ctx->d_nccl_send) CK(cudaFree(ctx->d_nccl_send));
+    ctx->nccl_send_bytes = std::max<size_t>(rows * W * sizeof(float) * 5 / 4, 256);
+    CK(cudaMalloc(&ctx->d_nccl_send, ctx->nccl_send_bytes));
+  }
+  ctx->x_done = true;
+  float* sbuf = ctx->d_nccl_send;
+  for (int p = 0; p < P; ++p) {
+    const PulseDev& pd = ctx->h_pulses[p];
+    const int ns = ctx->send_size[p], nr = ctx->recv_size[p];
+    if (ns) CK(launch_pack_x(W, pd.map, ns, ctx->x[0], sbuf, pd.has_shift, pd.shift, st));
+    const std::string e = nccl_sendrecv(ctx->nccl_comm, sbuf, (size_t)ns * W, ctx->neighbour(r, ctx->pdim[p], -1),
+                                        ctx->x[0] + (size_t)ctx->atom_offset[p] * W, (size_t)nr * W,
+                                        ctx->neighbour(r, ctx->pdim[p], +1), st);
+    if (!e.empty()) return fail(ctx, HALO_ERR_PEER, e);
+    sbuf += (size_t)ns * W;
+  }
+  return HALO_OK;
+}
+
+// f: per pulse descending, one NCCL group (the halo slice back to the x-sender,
+// this rank's returned slice from its x-receiver) -> ordered scatter-add kernel.
+halo_status halo_nccl_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->nccl_comm) return fail(ctx, HALO_ERR_STATE, "halo_nccl_init first");
+  if (!ctx->maps_ready || !ctx->x_done) return fail(ctx, HALO_ERR_STATE, "exchange_f before set_maps/exchange_x");
+  if (!accumulate && ctx->P != 1) return fail(ctx, HALO_ERR_UNSUPPORTED, "accumulate=0 needs exactly one pulse (R14)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int W = ctx->W, P = ctx->P, r = ctx->first_rank;
+  for (int p = P - 1; p >= 0; --p) {
+    const PulseDev& pd = ctx->h_pulses[p];
+    const int ns = ctx->send_size[p], nr = ctx->recv_size[p];
+    float* rbuf = ctx->fbuf_of(r) + (size_t)p * ctx->fbuf_stride;
+    const std::string e = nccl_sendrecv(ctx->nccl_comm, ctx->f[0] + (size_t)ctx->atom_offset[p] * W, (size_t)nr * W,
+                                        ctx->neighbour(r, ctx->pdim[p], +1), rbuf, (size_t)ns * W,
+                                        ctx->neighbour(r, ctx->pdim[p], -1), st);
+    if (!e.empty()) return fail(ctx, HALO_ERR_PEER, e);
+    double* fs = (fshift && pd.has_shift) ? fshift + 3 * pd.dim : nullptr;
+    if (ns) CK(launch_unpack_f(W, pd.map, ns, rbuf, ctx->f[0], accumulate ? 1 : 0, fs, st));
+  }
+  return HALO_OK;
+}
+
 halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   if (!ctx) return HALO_ERR_ARG;
   if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "exchange_x before set_maps");
@@ -1743,13 +1878,15 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   if (s != HALO_OK) return s;
   ctx->x_done = true;
   if (ctx->P == 0) return HALO_OK;
+  if (ctx->cfg.flags & HALO_F_NCCL_BASELINE) return halo_nccl_exchange_x(ctx, stream);
   if (ctx->ce) return ce_exchange_x(ctx, (cudaStream_t)stream);
   ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, 0, ctx->P);
   const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
   ctx->last_grid[0] = grid;
   if (ctx->ll) {
     X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x);
-    CK(launch_exchange_x_ll(X, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
+    X.n_items_x = ctx->n_items_x;
+    CK(launch_exchange_ll(X, 0, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
   }
   if (!ctx->ll)
     CK(launch_exchange_x(X, ctx->W, grid, (cudaStream_t)stream));
@@ -1763,6 +1900,7 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   halo_status s = check_err_word(ctx);
   if (s != HALO_OK) return s;
   if (ctx->P == 0) return HALO_OK;
+  if (ctx->cfg.flags & HALO_F_NCCL_BASELINE) return halo_nccl_exchange_f(ctx, fshift, accumulate, stream);
   if (ctx->ce) return ce_exchange_f(ctx, fshift, accumulate ? 1 : 0, (cudaStream_t)stream);
   ExParams F = make_params(ctx, ctx->d_items_f, ctx->n_items_f, 0, ctx->P);
   F.fshift = fshift;
@@ -1775,11 +1913,35 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   }
   ctx->last_grid[1] = grid;
   if (ctx->ll) {
-    F.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f);
-    CK(launch_exchange_f_ll(F, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
+    F.seq_f = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f);
+    CK(launch_exchange_ll(F, 1, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
   }
   if (!ctx->ll)
     CK(launch_exchange_f(F, ctx->W, grid, (cudaStream_t)stream));
+  return HALO_OK;
+}
+
+halo_status halo_exchange_xf(halo_ctx* ctx, double* fshift, int accumulate, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "exchange_xf before set_maps");
+  if (!accumulate && ctx->P != 1) return fail(ctx, HALO_ERR_UNSUPPORTED, "accumulate=0 needs exactly one pulse (R14)");
+  if (!ctx->ll) return fail(ctx, HALO_ERR_UNSUPPORTED, "the fused x+f launch exists for the LL protocol only");
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  ctx->x_done = true;
+  if (ctx->P == 0) return HALO_OK;
+  // one item list: every x item, then the gather items, then the combines (tail)
+  ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x + ctx->n_items_f, 0, ctx->P);
+  X.n_items_x = ctx->n_items_x;
+  X.n_tail = ctx->n_tail_f;
+  X.fshift = fshift;
+  X.accumulate = accumulate ? 1 : 0;
+  int grid = std::min(X.n_items - X.n_tail, ctx->cap_xf() - X.n_tail) + X.n_tail;
+  grid = std::max(grid, 1);
+  ctx->last_grid[0] = grid;
+  X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x);
+  X.seq_f = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f);
+  CK(launch_exchange_ll(X, 2, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
   return HALO_OK;
 }
 
@@ -1843,12 +2005,12 @@ halo_status halo_get_timers(halo_ctx* ctx, uint64_t* x_ns, uint64_t* f_ns) {
     for (int which = 0; which < 2; ++which) {
       const int m = std::min(ctx->last_grid[which], kTraceCTAs);
       if (m <= 0) continue;
-      std::vector<uint64_t> t(8 * (size_t)m);
-      CK(cudaMemcpy(t.data(), &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 8 * m, cudaMemcpyDeviceToHost));
+      std::vector<uint64_t> t(kTraceW * (size_t)m);
+      CK(cudaMemcpy(t.data(), &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * kTraceW * m, cudaMemcpyDeviceToHost));
       uint64_t lo = ~0ull, hi = 0;
       for (int i = 0; i < m; ++i) {
-        lo = std::min(lo, t[8 * i]);
-        hi = std::max(hi, t[8 * i + 3]);
+        lo = std::min(lo, t[kTraceW * i]);
+        hi = std::max(hi, t[kTraceW * i + 3]);
       }
       // (with programmatic dependent launch the stamps of consecutive launches can
       // interleave; keep the last arriver's span when the trace is inconsistent)
@@ -1873,12 +2035,12 @@ halo_status halo_get_notify_counts(halo_ctx* ctx, int which, uint32_t* out, int 
 
 halo_status halo_get_trace(halo_ctx* ctx, int which, uint64_t* out, int cap, int* n) {
   if (!ctx || which < 0 || which > 1 || !out || !n) return HALO_ERR_ARG;
-  const int m = std::min(std::min(ctx->last_grid[which], kTraceCTAs), cap / 8);
+  const int m = std::min(std::min(ctx->last_grid[which], kTraceCTAs), cap / kTraceW);
   *n = m;
   if (m <= 0) return HALO_OK;
   CK(cudaSetDevice(ctx->cfg.device));
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(out, &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * 8 * m, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, &ctx->ctrl->trace[which][0][0], sizeof(uint64_t) * kTraceW * m, cudaMemcpyDeviceToHost));
   return HALO_OK;
 }
 
@@ -2040,6 +2202,8 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
   if (ctx->d_ce) (void)cudaFree(ctx->d_ce);
   if (ctx->d_stage) (void)cudaFree(ctx->d_stage);
+  if (ctx->d_nccl_send) (void)cudaFree(ctx->d_nccl_send);
+  if (ctx->nccl_comm) nccl_comm_destroy(ctx->nccl_comm);
   if (ctx->err_host) (void)cudaFreeHost(ctx->err_host);
   (void)cudaGetLastError();
   delete ctx;

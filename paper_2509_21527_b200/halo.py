@@ -190,6 +190,28 @@ class Halo:
         self._ck(self.lib.halo_exchange_f(self.h, c_void_p(fshift_ptr or None), int(bool(accumulate)),
                                           c_void_p(stream)))
 
+    def exchange_xf(self, fshift_ptr=0, accumulate=True, stream=0):
+        self._ck(self.lib.halo_exchange_xf(self.h, c_void_p(fshift_ptr or None), int(bool(accumulate)),
+                                           c_void_p(stream)))
+
+    # NCCL send/recv baseline (halo_nccl_*; the paper's serialized schedule, not the product)
+    def nccl_unique_id(self) -> bytes:
+        n = c_size_t(128)
+        buf = ctypes.create_string_buffer(128)
+        self._ck(self.lib.halo_nccl_unique_id(buf, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def nccl_init(self, uid: bytes):
+        buf = ctypes.create_string_buffer(uid, len(uid))
+        self._ck(self.lib.halo_nccl_init(self.h, buf, len(uid)))
+
+    def nccl_exchange_x(self, stream=0):
+        self._ck(self.lib.halo_nccl_exchange_x(self.h, c_void_p(stream)))
+
+    def nccl_exchange_f(self, fshift_ptr=0, accumulate=True, stream=0):
+        self._ck(self.lib.halo_nccl_exchange_f(self.h, c_void_p(fshift_ptr or None), int(bool(accumulate)),
+                                               c_void_p(stream)))
+
     def step_host(self, x_home_ptrs, f_all_ptrs, x_halo_out_ptrs=None, f_home_out_ptrs=None, fshift_ptr=0,
                   stream=0):
         n = len(x_home_ptrs)
@@ -224,11 +246,11 @@ class Halo:
     def get_trace(self, which):
         """Per-CTA [start, record loaded, items done, exit, item0 tag, item0 end, item1 tag, item1 end]
         (ns; tag = kind << 16 | lrank << 8 | pulse) of the last x (0) / f (1) launch."""
-        cap = 8 * 2048
+        cap = 16 * 2048
         buf = (c_uint64 * cap)()
         n = c_int()
         self._ck(self.lib.halo_get_trace(self.h, int(which), buf, cap, ctypes.byref(n)))
-        return np.array(buf[: 8 * n.value], dtype=np.uint64).reshape(-1, 8)
+        return np.array(buf[: 16 * n.value], dtype=np.uint64).reshape(-1, 16)
 
     def floor_pingpong(self, peer_rank, iters=10000, relaxed=False) -> float:
         v = c_double()

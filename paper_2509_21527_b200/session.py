@@ -138,6 +138,18 @@ class HaloSession:
     def exchange_f(self, fshift=None, accumulate=True, stream=None):
         self.halo.exchange_f(fshift.data_ptr() if fshift is not None else 0, accumulate, stream=self._s(stream))
 
+    def nccl_init(self, group=None):
+        """NCCL communicator of the send/recv baseline (halo_nccl_init): process 0's
+        unique id is broadcast over torch.distributed; one DD rank per process."""
+        import torch.distributed as dist
+        uid = [self.halo.nccl_unique_id() if self.proc == 0 else None]
+        if self.nprocs > 1:
+            dist.broadcast_object_list(uid, src=0, group=group)
+        self.halo.nccl_init(uid[0])
+
+    def exchange_xf(self, fshift=None, accumulate=True, stream=None):
+        self.halo.exchange_xf(fshift.data_ptr() if fshift is not None else 0, accumulate, stream=self._s(stream))
+
     @staticmethod
     def _s(stream):
         if stream is None:

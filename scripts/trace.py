@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--no-fshift", action="store_true")
     ap.add_argument("--no-mid-event", action="store_true", help="no event between x and f (keeps PDL)")
     ap.add_argument("--queue", type=int, default=0, help="queue this many un-synchronised steps before the traced one")
+    ap.add_argument("--fused", action="store_true", help="trace the fused x+f launch (halo_exchange_xf)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -61,54 +62,65 @@ def main():
     F0_all = torch.zeros_like(sess.f_all)
     for l in range(nl):
         F0_all[l, : F0[l].shape[0]] = F0[l]
+    def one_step():
+        if args.fused:
+            sess.exchange_xf(fshift=None if args.no_fshift else fshift)
+        else:
+            sess.exchange_x()
+            sess.exchange_f(fshift=None if args.no_fshift else fshift)
+
     for k in range(args.steps):
         if world > 1:
             torch.cuda.synchronize()
             dist.barrier()  # start every traced step together (host skew is not kernel time)
         for _ in range(args.queue):  # steady state: the host runs ahead of the GPU
-            sess.f_all.copy_(F0_all)
             if args.flush:
                 flush.fill_(1.0)
-            sess.exchange_x()
-            sess.exchange_f(fshift=None if args.no_fshift else fshift)
-        sess.f_all.copy_(F0_all)
+            sess.f_all.copy_(F0_all)
+            one_step()
         if args.flush:
             flush.fill_(1.0)
+        sess.f_all.copy_(F0_all)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(st)
-        sess.exchange_x()
-        if not args.no_mid_event:
-            e1.record(st)
-        sess.exchange_f(fshift=None if args.no_fshift else fshift)
+        if args.fused:
+            sess.exchange_xf(fshift=None if args.no_fshift else fshift)
+        else:
+            sess.exchange_x()
+            if not args.no_mid_event:
+                e1.record(st)
+            sess.exchange_f(fshift=None if args.no_fshift else fshift)
         e2.record(st)
         torch.cuda.synchronize()
         tx = sess.halo.get_trace(0).astype(np.int64)
-        tf = sess.halo.get_trace(1).astype(np.int64)
+        tf = tx if args.fused else sess.halo.get_trace(1).astype(np.int64)
         t0 = tx[:, 0].min()
+        mid = not (args.no_mid_event or args.fused)
         res = {
-            "step": k, "rank": rank, "x_event_us": (round(e0.elapsed_time(e1) * 1e3, 2) if not args.no_mid_event else None),
-            "f_event_us": (round(e1.elapsed_time(e2) * 1e3, 2) if not args.no_mid_event else None),
+            "step": k, "rank": rank, "fused": args.fused,
+            "x_event_us": round(e0.elapsed_time(e1) * 1e3, 2) if mid else None,
+            "f_event_us": round(e1.elapsed_time(e2) * 1e3, 2) if mid else None,
             "step_event_us": round(e0.elapsed_time(e2) * 1e3, 2), "x_ctas": int(tx.shape[0]), "f_ctas": int(tf.shape[0]),
             "x_start": q((tx[:, 0] - t0) / 1e3), "x_rec": q((tx[:, 1] - t0) / 1e3),
             "x_done": q((tx[:, 2] - t0) / 1e3), "x_exit": q((tx[:, 3] - t0) / 1e3),
-            "gap_x_exit_to_f_start": round(float((tf[:, 0].min() - tx[:, 3].max()) / 1e3), 2),
-            "f_start": q((tf[:, 0] - t0) / 1e3), "f_rec": q((tf[:, 1] - t0) / 1e3),
-            "f_done": q((tf[:, 2] - t0) / 1e3), "f_exit": q((tf[:, 3] - t0) / 1e3),
         }
-        # per (kind, level) item end quantiles, relative to the kernel's first CTA start
-        x_end = tx[:, 3].max()
-        for nm, tr in (("x", tx), ("f", tf)):
-            # x items: relative to the x kernel's first CTA; f items: relative to the
-            # x kernel's last exit (with PDL the f CTAs start before it)
-            tk0 = tr[:, 0].min() if nm == "x" else x_end
+        if not args.fused:
+            res.update({"gap_x_exit_to_f_start": round(float((tf[:, 0].min() - tx[:, 3].max()) / 1e3), 2),
+                        "f_start": q((tf[:, 0] - t0) / 1e3), "f_rec": q((tf[:, 1] - t0) / 1e3),
+                        "f_done": q((tf[:, 2] - t0) / 1e3), "f_exit": q((tf[:, 3] - t0) / 1e3)})
+        # per (kind, level) item end quantiles [min, median, p90, max, count], µs relative
+        # to the first CTA start of the (x or fused) launch
+        kinds = {0: "xindep", 1: "xdep", 4: "xrecv", 5: "gather", 6: "fshift"}
+        for nm, tr in ((("xf", tx),) if args.fused else (("x", tx), ("f", tf))):
             groups = {}
             for row in tr:
-                for sl in range(2):
+                for sl in range((tr.shape[1] - 4) // 2):
                     tag, end = int(row[4 + 2 * sl]), int(row[5 + 2 * sl])
                     if end == 0 or end < tr[:, 0].min():
                         continue
-                    key = f"k{tag >> 16}_p{tag & 0xff}"
-                    groups.setdefault(key, []).append((end - tk0) / 1e3)
+                    lev = tag & 0xff
+                    key = f"{kinds.get(tag >> 16, tag >> 16)}_p{'home' if lev == 255 else lev}"
+                    groups.setdefault(key, []).append((end - t0) / 1e3)
             res[nm + "_items"] = {k: q(np.array(v)) + [len(v)] for k, v in sorted(groups.items())}
         out.append(res)
     if world > 1:

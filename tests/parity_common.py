@@ -91,9 +91,11 @@ class Case:
         return s.x[: s.n_home]
 
 
-def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit=False, steps=1, barrier=None):
+def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit=False, steps=1, barrier=None,
+                 fused=False):
     """Drive the CUDA path for the local ranks of `sess` and compare with the oracle.
-    Returns a dict of per-check booleans (asserts on the way)."""
+    fused: each step is one halo_exchange_xf launch (f loaded before it) instead of
+    exchange_x, check, exchange_f.  Returns True (asserts on the way)."""
     first, nl = sess.first_rank, sess.n_local
     sess.load_home([case.home_rows(first + l) for l in range(nl)])
     if use_explicit:
@@ -119,12 +121,20 @@ def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit
         for l in range(nl):
             st = case.states[first + l]
             sess.x[l][st.n_home: st.x.shape[0]] = float("nan")
+        if fused:
+            for l in range(nl):
+                r = first + l
+                sess.f[l][: case.F[r].shape[0]] = torch.from_numpy(case.F[r]).to(sess.device)
+            fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=sess.device)
         if barrier is not None:
             # the poison is written outside the protocol: every process must have
             # poisoned before any peer stores this step's halo (R17)
             torch.cuda.synchronize()
             barrier()
-        sess.exchange_x()
+        if fused:
+            sess.exchange_xf(fshift=fshift)
+        else:
+            sess.exchange_x()
         torch.cuda.synchronize()
         for l in range(nl):
             st = case.states[first + l]
@@ -132,13 +142,14 @@ def run_gpu_case(case: Case, sess, check_forces=True, atomic=False, use_explicit
             np.testing.assert_array_equal(bits(got), bits(st.x), err_msg=f"halo x rank {first + l} step {step}")
         if not check_forces:
             continue
-        for l in range(nl):
-            r = first + l
-            n = case.F[r].shape[0]
-            sess.f[l][:n] = torch.from_numpy(case.F[r]).to(sess.device)
-        fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=sess.device)
-        sess.exchange_f(fshift=fshift)
-        torch.cuda.synchronize()
+        if not fused:
+            for l in range(nl):
+                r = first + l
+                n = case.F[r].shape[0]
+                sess.f[l][:n] = torch.from_numpy(case.F[r]).to(sess.device)
+            fshift = torch.zeros(nl, 3, 3, dtype=torch.float64, device=sess.device)
+            sess.exchange_f(fshift=fshift)
+            torch.cuda.synchronize()
         fs = fshift.cpu().numpy()
         for l in range(nl):
             r = first + l

@@ -135,6 +135,28 @@ def _worker_g2(rank, world, port, cases, out):
                                               err_msg=f"NCCL schedule f rank {rank}")
                 assert_fshift(fshift[0].cpu().numpy(), case.fshift[rank], case.fshift_abs[rank], where="nccl")
                 dist.barrier()
+                # the same schedule captured into a CUDA graph (NCCL in the same graph)
+                gs = torch.cuda.Stream()
+                g = torch.cuda.CUDAGraph()
+                torch.cuda.synchronize()
+                dist.barrier()
+                with torch.cuda.graph(g, stream=gs):
+                    sched.step(fshift, stream=gs)
+                for _ in range(2):
+                    sess.x[0][nh:n] = float("nan")
+                    sess.f[0][:n] = torch.from_numpy(case.F[rank]).to(sess.device)
+                    fshift.zero_()
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    g.replay()
+                    torch.cuda.synchronize()
+                    np.testing.assert_array_equal(bits(sess.x[0][:n].cpu().numpy()), bits(st.x),
+                                                  err_msg=f"NCCL graph halo x rank {rank}")
+                    np.testing.assert_array_equal(bits(sess.f[0][:n].cpu().numpy()), bits(case.Fo[rank]),
+                                                  err_msg=f"NCCL graph f rank {rank}")
+                    assert_fshift(fshift[0].cpu().numpy(), case.fshift[rank], case.fshift_abs[rank], where="nccl g")
+                dist.barrier()
+                del g
                 # the fused / CE path still runs after the baseline touched the buffers
                 run_gpu_case(case, sess, steps=1, barrier=dist.barrier)
                 dist.barrier()

@@ -451,3 +451,67 @@ def test_auto_transport_switches_per_epoch(monkeypatch):
     with pytest.raises(HaloError) as e:
         session_for(case, flags=AUTO | CE)
     assert e.value.status == 8
+
+
+# ------------------------------------------------ fused x+f launch (halo_exchange_xf)
+@pytest.mark.parametrize("kind", ["int", "normal"])
+@pytest.mark.parametrize("name", ["W1", "W2", "W3", "C1", "T3D", "T2P", "T2D", "T4x2", "C2", "C5", "C3"])
+def test_parity_fused_xf(name, kind):
+    """One launch per step: x halo and forces bit-exact, fshift
+    within the fp64 bound, several steps (sequence numbers, per-rank halo counters)."""
+    case = Case(name, seed=1 if kind == "int" else 2, force_kind=kind)
+    sess = session_for(case)
+    run_gpu_case(case, sess, steps=3, fused=True)
+    run_gpu_case(case, sess, steps=1)  # the two-launch path in the same NS epoch
+    run_gpu_case(case, sess, steps=2, fused=True)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("name", ["T2P", "C3"])
+def test_parity_fused_xf_float4_and_large_items(name, monkeypatch):
+    monkeypatch.setenv("HALO_ITEM_ROWS", "256")  # batched (wide) variants
+    case = Case(name, seed=3, layout=4, force_kind="normal")
+    sess = session_for(case, layout=4)
+    run_gpu_case(case, sess, steps=2, fused=True)
+    sess.destroy()
+
+
+def test_parity_fused_xf_receive_path(monkeypatch):
+    """Fused launch with every halo row through receive items (the cross-GPU path)."""
+    monkeypatch.setenv("HALO_DIRECT_X", "0")
+    case = Case("C3", seed=1, force_kind="normal")
+    sess = session_for(case)
+    run_gpu_case(case, sess, steps=3, fused=True)
+    sess.destroy()
+
+
+def test_fused_xf_cuda_graph_replay():
+    """exchange_xf captured once and replayed: device-resident sequence numbers and
+    halo counters keep every replay bit-exact; mixed with eager two-launch steps."""
+    case = Case("C3", seed=2, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess, fused=True)
+    s = torch.cuda.Stream()
+    fshift = torch.zeros(sess.n_local, 3, 3, dtype=torch.float64, device=sess.device)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        sess.exchange_xf(fshift=fshift, stream=s)
+    for rep in range(4):
+        for l in range(sess.n_local):
+            st = case.states[l]
+            sess.x[l][st.n_home: st.x.shape[0]] = float("nan")
+            sess.f[l][: case.F[l].shape[0]] = torch.from_numpy(case.F[l]).to(sess.device)
+        fshift.zero_()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        for l in range(sess.n_local):
+            st = case.states[l]
+            np.testing.assert_array_equal(bits(sess.x[l][: st.x.shape[0]].cpu().numpy()), bits(st.x))
+            np.testing.assert_array_equal(bits(sess.f[l][: case.F[l].shape[0]].cpu().numpy()), bits(case.Fo[l]))
+            np.testing.assert_array_equal(fshift[l].cpu().numpy(), case.fshift[l])
+        if rep == 1:
+            sess.exchange_x()
+            sess.exchange_f()
+    sess.destroy()
