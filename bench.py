@@ -22,6 +22,11 @@ import sys
 import threading
 import time
 
+if "--cpu-child" in sys.argv or "reference" in sys.argv:
+    # the oracle legs run single-threaded (OMP/MKL/OPENBLAS_NUM_THREADS=1, one pinned core)
+    for _v in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ[_v] = "1"
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -138,9 +143,33 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ cpu legs
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def pin_one_core():
+    """Pin this process to one allowed core (taskset -c <first allowed>); returns it."""
+    try:
+        cpu = min(os.sched_getaffinity(0))
+        os.sched_setaffinity(0, {cpu})
+        return cpu
+    except (AttributeError, OSError):
+        return None
+
+
 def oracle_step_timing(c, X, budget_s=15.0, max_steps=None, warmup=1):
     """The oracle (as it stands) per step: fixed-map x halo + force halo, all DD
-    ranks serially, on this host; maps built once outside the timed region."""
+    ranks serially, on this host; maps built once outside the timed region.
+    Returns (mean us/step, steps, best-of-5 us/step)."""
     from oracle import coord_halo_step, decompose, force_halo  # cpu_baseline leg only
     from synth import forces_normal
     states = decompose(X, c.L, c.rc, c.grid, c.pulses)
@@ -149,15 +178,98 @@ def oracle_step_timing(c, X, budget_s=15.0, max_steps=None, warmup=1):
     for _ in range(warmup):
         coord_halo_step(states, xh)
         force_halo(states, F)
-    n, t0 = 0, time.perf_counter()
+    n, ts, t0 = 0, [], time.perf_counter()
     while True:
+        a = time.perf_counter()
         coord_halo_step(states, xh)
         force_halo(states, F)
+        ts.append(time.perf_counter() - a)
         n += 1
         el = time.perf_counter() - t0
         if el >= budget_s or (max_steps is not None and n >= max_steps):
             break
-    return el / n * 1e6, n
+    best5 = min(float(np.mean(ts[i:i + max(1, n // 5)])) for i in range(0, n, max(1, n // 5)))
+    return el / n * 1e6, n, best5 * 1e6
+
+
+def oracle_c1_pipeline():
+    """BASELINE.json configs[0] ("CPU oracle in seconds"): the whole C1 oracle pipeline —
+    generate the 3,000-atom box, decomposition + maps, x halo + force halo, and the
+    brute-force pins X2 (import zones), X3 (pair coverage), F1-F3 (integer forces: totals,
+    conservation, shift forces) — wall seconds on this core."""
+    from oracle import decompose, force_halo  # cpu_baseline leg only
+    from synth import forces_int, get_config, water_box
+    from tests import pins  # test-only brute-force checks
+    t0 = time.perf_counter()
+    c = get_config("C1")
+    X = water_box(c.n_atoms, c.L, 1)
+    st = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    F = [forces_int(s.x.shape[0], 100 + s.rank) for s in st]
+    Fo, fs = force_halo(st, [f.copy() for f in F])
+    t_core = time.perf_counter() - t0
+    ok = True
+    for s in st:  # X2
+        inner, outer = pins.direct_gather(X, c.L, c.rc, c.grid, s.rank, eps=1e-5)
+        hs = {(int(g), tuple(int(v) for v in sv)) for g, sv in zip(s.gid, s.s)}
+        ok &= inner <= hs <= outer
+    index = []
+    for s in st:  # X3
+        m = {}
+        for g, sv in zip(s.gid, s.s):
+            m.setdefault(int(g), set()).add(tuple(int(v) for v in sv))
+        index.append(m)
+    dec = [d for d in range(3) if c.grid[d] > 1]
+    pairs = pins.close_pairs(X, c.L, c.rc, eps=1e-5)
+    for i, j, n in pairs:
+        ok &= any(any(all(b[d] - a[d] == n[d] for d in dec) for a in m.get(i, ()) for b in m.get(j, ()))
+                  for m in index)
+    tot = pins.scatter_totals([s.gid for s in st], F, X.shape[0])  # F1
+    got = np.zeros((X.shape[0], 3))
+    for s, f in zip(st, Fo):
+        got[s.gid[:s.n_home]] = f[:s.n_home]
+    ok &= bool(np.array_equal(got, tot))
+    before = sum(f.astype(np.float64).sum(axis=0) for f in F)  # F2
+    after = sum(f[:s.n_home].astype(np.float64).sum(axis=0) for s, f in zip(st, Fo))
+    ok &= bool(np.array_equal(before, after))
+    fs_tot = sum(fs)  # F3
+    for d in range(3):
+        exp = sum(f[s.s[:, d] == 1].astype(np.float64).sum(axis=0) for s, f in zip(st, F))
+        ok &= bool(np.array_equal(fs_tot[d], exp))
+    return {"seconds": round(time.perf_counter() - t0, 2), "core_seconds": round(t_core, 3),
+            "pairs_checked": len(pairs), "pins_ok": bool(ok),
+            "what": "C1: generate 3,000 atoms + decomposition/maps + x halo + force halo (core_seconds), "
+                    "then brute-force pins X2, X3 (every pair within rc co-resident), F1-F3"}
+
+
+def cpu_child(args):
+    """--cpu-child: the cpu_baseline leg in its own pinned, single-threaded process."""
+    cpu = pin_one_core()
+    c, X = build_workload(args.config)
+    us, n, best = oracle_step_timing(c, X, budget_s=args.cpu_budget)
+    out = {"us": us, "n": n, "best5_us": best, "cpu": cpu}
+    if not args.no_c1_pipeline:
+        out["c1_pipeline"] = oracle_c1_pipeline()
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_leg(args, P, c):
+    import subprocess
+    env = dict(os.environ, OMP_NUM_THREADS="1", MKL_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1")
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-child", "--config", args.config,
+           "--cpu-budget", str(args.cpu_budget)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "error": r.stderr[-400:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    out = {"value": round(d["us"], 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+           "best_of_5_us": round(d["best5_us"], 1),
+           "sample": f"{c.name} full workload ({c.nranks} DD ranks, {P} pulses), {d['n']} oracle steps "
+                     f"(fixed-map x halo + force halo, all ranks serially), numpy, one thread pinned to "
+                     f"core {d['cpu']} (OMP/MKL/OPENBLAS_NUM_THREADS=1)",
+           **host_info()}
+    if "c1_pipeline" in d:
+        out["c1_pipeline"] = d["c1_pipeline"]
+    return out
 
 
 # ------------------------------------------------------------------ main arm
@@ -174,12 +286,13 @@ def run_fused(args, rank, world, local):
         raise SystemExit(f"config {c.name} has {c.nranks} DD ranks, not divisible by {world} GPUs")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    homes = assign_home(X, c.L, c.grid)
+    homes = assign_home(X, c.L, c.grid, c.rc, c.pulses, device=local)
     cap = int(max(len(h) for h in homes) * 2.2) + 4096
     flags = (HALO_F_TIMERS if args.timers else 0) | PROTO_FLAGS[args.proto] | ((1 << 6) if args.l2_persist else 0)
     flags |= (1 << 9) if args.zones == "rounded" else 0  # HALO_F_ROUNDED_ZONES (R31)
     sess = HaloSession(c.grid, c.L, c.rc, c.pulses, layout=args.layout, capacity=cap, device=local, flags=flags,
-                       nprocs=world, proc=rank, timeout_s=20.0, pme_rank=0 if args.pme else None)
+                       nprocs=world, proc=rank, timeout_s=20.0, pme_rank=0 if args.pme else None,
+                       probe_bytes=(64 << 20) if (world > 1 and not args.no_floors) else None)
     first, nl = sess.first_rank, sess.n_local
     sess.load_home([X[homes[first + l]] for l in range(nl)])
     sess.set_maps()
@@ -355,13 +468,32 @@ def run_fused(args, rank, world, local):
             t0 = sess.halo.floor_pingpong(peer, iters=10000, relaxed=False)
             t0r = sess.halo.floor_pingpong(peer, iters=10000, relaxed=True)
         barrier()
+        # t(B): payload + signal one-way latency, process 0 <-> process 1 (collective between them)
+        curve = []
+        for nb in (4 << 10, 16 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 64 << 20):
+            v = None
+            if rank in (0, 1):
+                peer = sess.first_rank + sess.n_local if rank == 0 else 0
+                v = sess.halo.floor_payload(peer, nb, iters=200 if nb <= (1 << 20) else 40)
+            barrier()
+            if rank == 0:
+                curve.append({"bytes": nb, "one_way_us": round(v, 3), "gbs": round(nb / (v * 1e-6) / 1e9, 1)})
         if rank == 0:
+            # bandwidth (64 MiB per peer, back-to-back): one pair, then every other process's first rank at once
+            per = sess.n_local
+            others = [q * per for q in range(1, world)]
+            for name, peers in (("1_peer", others[:1]), (f"{len(others)}_peers", others) if len(others) > 1 else (None, None)):
+                if name is None:
+                    continue
+                bw[name] = {"bytes_per_peer": 64 << 20, "peers": peers,
+                            "sm_gbs_total": round(sess.halo.floor_bandwidth_multi(peers, 64 << 20, mode=0, iters=20), 1),
+                            "ce_gbs_total": round(sess.halo.floor_bandwidth_multi(peers, 64 << 20, mode=1, iters=20), 1)}
             peer = sess.first_rank + sess.n_local
-            # the probe writes into the peer's scratch from its LL areas on (>= 8 MiB at any capacity)
             for name, nb in (("8MiB", 8 << 20), ("1MiB", 1 << 20), ("64KiB", 64 << 10)):
                 bw[name] = {"bytes": nb,
                             "sm_gbs": round(sess.halo.floor_bandwidth(peer, nb, mode=0, iters=50), 1),
                             "ce_gbs": round(sess.halo.floor_bandwidth(peer, nb, mode=1, iters=50), 1)}
+            bw["t_of_B"] = curve
         barrier()
         t0 = max_over_ranks(t0 or 0.0)
         t0r = max_over_ranks(t0r or 0.0)
@@ -445,11 +577,17 @@ def run_fused(args, rank, world, local):
     floor["launch_us_graph"] = round(launch_graph, 3)
     if floor.get("t0_one_way_us"):
         t0 = floor["t0_one_way_us"]
-        bw_peer = ((floor.get("bandwidth") or {}).get("8MiB") or {}).get("sm_gbs") or 770.0
+        bwd = floor.get("bandwidth") or {}
+        bw_peer = (bwd.get("1_peer") or {}).get("sm_gbs_total") or (bwd.get("8MiB") or {}).get("sm_gbs")
+        bw_src = "measured SM peer stores, 64 MiB, one pair" if (bwd.get("1_peer") or {}).get("sm_gbs_total") else \
+            ("measured SM peer stores, 8 MiB" if bw_peer else None)
+        if not bw_peer:  # N=1: no NVLink bytes; the guide's measured peer copy (B200_PROFILING.md), labelled
+            bw_peer, bw_src = 770.0, "not measured here (N=1, no NVLink traffic): B200_PROFILING.md peer copy 770 GB/s"
         # nvl_bytes already holds x out + f back (one direction): x and f are serial, so their
         # bandwidth terms add once each
         fl = 2 * P * t0 + nvl_bytes / (bw_peer * 1e9) * 1e6
-        out["nvlink"]["measured_peer_store_gbs"] = bw_peer
+        out["nvlink"]["bw_peer_gbs"] = bw_peer
+        out["nvlink"]["bw_peer_source"] = bw_src
         out["nvlink"]["frac_of_measured"] = round(out["nvlink"]["achieved_gbs"] / bw_peer, 4)
         floor["floor_step_us"] = round(fl, 3)
         floor["value_over_floor"] = round(res["step"] / fl, 3)
@@ -458,17 +596,14 @@ def run_fused(args, rank, world, local):
         floor["value_over_floor_with_launch"] = round(res["step"] / fl2, 3)
         # the bound that actually limits this path: the measured latency floor
         roof["latency"] = {"floor_us": round(fl2, 3), "frac": round(fl2 / res["step"], 4),
-                           "definition": "2*P*t0 + (x+f NVLink bytes per direction)/BW_peer (measured SM peer-store GB/s, 8 MiB) "
+                           "definition": "2*P*t0 + (x+f NVLink bytes per direction)/BW_peer (nvlink.bw_peer_source) "
                                          "+ 2 launches (eager)"}
     if args.pme:
         out["pme"] = pme_timing(sess, K, args.warmup, flush)
     if not args.no_ns:
         out["ns_step"] = ns_step_timing(sess, c, X, homes, dev)
     if world == 1 and rank == 0 and not args.no_cpu:
-        us, n = oracle_step_timing(c, X, budget_s=args.cpu_budget)
-        out["cpu_baseline"] = {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
-                               "sample": f"{c.name} full workload ({c.nranks} DD ranks, {P} pulses), {n} oracle "
-                                         f"steps (fixed-map x halo + force halo), numpy single thread"}
+        out["cpu_baseline"] = cpu_baseline_leg(args, P, c)
     sess.destroy()
     return out
 
@@ -553,8 +688,10 @@ def _neighbour(grid, r, d, delta):
 
 def run_nccl_baseline(sess, lay, F0, flush, K, warmup, W):
     """Serialized per-pulse schedule (Fig. 1) with NCCL send/recv on the same maps
-    (paper_2509_21527_b200.nccl_baseline): pack kernel -> grouped send/recv -> (forces, reverse)
-    send/recv -> unpack kernel."""
+    (halo_nccl_*, csrc/nccl_baseline.cu, torch's libnccl): pack kernel -> ncclGroupStart/Send/
+    Recv/GroupEnd per pulse ascending; forces: send/recv of the halo slice per pulse descending
+    -> ordered scatter-add kernel.  Timed eager and as one captured CUDA graph per step (the
+    same flush / f reset between steps as the fused arm), mean per rank, max over ranks."""
     import torch
     from paper_2509_21527_b200.nccl_baseline import NcclSchedule
     dev = sess.device
@@ -562,23 +699,47 @@ def run_nccl_baseline(sess, lay, F0, flush, K, warmup, W):
     fshift = torch.zeros(1, 3, 3, dtype=torch.float64, device=dev)
     f = sess.f[0]
     stream = torch.cuda.current_stream()
-    for _ in range(warmup):
-        f[: F0.shape[0]].copy_(F0)
-        sched.step(fshift)
-    torch.cuda.synchronize()
-    barrier()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
-    for k in range(K):
-        f[: F0.shape[0]].copy_(F0)
-        flush.fill_(1.0)
-        ev[k][0].record(stream)
-        sched.step(fshift)
-        ev[k][1].record(stream)
-    torch.cuda.synchronize()
-    us = max_over_ranks(float(np.mean([ev[k][0].elapsed_time(ev[k][1]) * 1e3 for k in range(K)])))
-    barrier()
-    return {"us_per_step": round(us, 3), "schedule": "per-pulse pack -> NCCL send/recv -> unpack (torch "
-            "batch_isend_irecv), same maps", "launches_per_step": 2 * sess.npulse}
+
+    def timed(run):
+        for _ in range(warmup):
+            f[: F0.shape[0]].copy_(F0)
+            flush.fill_(1.0)
+            run()
+        torch.cuda.synchronize()
+        barrier()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+        for k in range(K):
+            f[: F0.shape[0]].copy_(F0)
+            flush.fill_(1.0)
+            ev[k][0].record(stream)
+            run()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        us = max_over_ranks(float(np.mean([ev[k][0].elapsed_time(ev[k][1]) * 1e3 for k in range(K)])))
+        barrier()
+        return us
+
+    eager = timed(lambda: sched.step(fshift))
+    graph_us = None
+    try:
+        gs = torch.cuda.Stream(device=dev)
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        barrier()
+        with torch.cuda.graph(g, stream=gs):
+            sched.step(fshift, stream=gs)
+        torch.cuda.synchronize()
+        barrier()
+        graph_us = timed(g.replay)
+        del g
+    except Exception as e:  # pragma: no cover - recorded, not hidden
+        graph_us = f"capture failed: {e}"
+    return {"us_per_step": round(eager, 3), "graph_us_per_step": graph_us if isinstance(graph_us, str) or graph_us is None
+            else round(graph_us, 3),
+            "schedule": "per-pulse pack kernel -> ncclGroupStart/ncclSend/ncclRecv/ncclGroupEnd (C++, halo_nccl_*, "
+                        "torch's libnccl) -> reverse send/recv + ordered scatter-add, same maps; eager and one "
+                        "CUDA graph per step",
+            "launches_per_step": 2 * sess.npulse}
 
 
 def load_peaks():
@@ -605,6 +766,7 @@ def run_reference(args, rank, world):
     """--impl reference: the oracle as it stands, timed on the host cores (rank 0 only)."""
     if rank != 0:
         return None
+    cpu = pin_one_core()
     c, X = build_workload(args.config)
     # warm-up steps W, then K timed steps, each step one full oracle x+f over all DD ranks
     from oracle import coord_halo_step, decompose, force_halo
@@ -631,7 +793,8 @@ def run_reference(args, rank, world):
             "steps": len(ts), "warmup": args.warmup, "ms_per_step": round(us / 1e3, 4), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_desc(c, world, 3),
-            "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": samp},
+            "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": samp + f", one thread pinned to core {cpu}", **host_info()},
             "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -655,12 +818,17 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-floors", action="store_true", help="skip the latency/bandwidth/launch floor probes")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-c1-pipeline", action="store_true", help="cpu leg: skip the C1 whole-pipeline timing")
     ap.add_argument("--zones", default="slab", choices=("slab", "rounded"),
                     help="import zones: slab (box-shaped, default) or GROMACS-style rounded (HALO_F_ROUNDED_ZONES)")
     ap.add_argument("--pme", action="store_true", help="also time the PP<->PME redistribution (halo_pme_*)")
     ap.add_argument("--no-ns", action="store_true", help="skip the NS-step (halo_migrate + halo_set_maps) timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.cpu_child:
+        cpu_child(args)
+        return
     rank, world, local = dist_env()
     if args.gpus is not None and args.gpus != world and world != 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")

@@ -192,6 +192,22 @@ HALO_API halo_status halo_set_maps(halo_ctx* ctx, const int* n_home, void* strea
 HALO_API halo_status halo_set_maps_explicit(halo_ctx* ctx, const int* n_home, const int* send_sizes,
                                    const int* const* maps, void* stream);
 
+/* Initial domain assignment (the DD "divides the simulation box into
+ * spatial regions (domains)"; readings R3/R4): for the n_atoms rows of a GLOBAL
+ * coordinate array x (DEVICE float32, row i at x + i*stride, stride >= 3 floats,
+ * every x_d in [0, L_d)), the home rank of row i is (cx*np_y + cy)*np_z + cz with
+ * c_d = the number of interior planes float64(L_d)*k/grid[d], k = 1..grid[d]-1,
+ * that are <= float64(x_d) (a coordinate on a plane goes to the upper cell).
+ *   ids     (DEVICE int32[n_atoms], out) the atom ids grouped by home rank,
+ *           rank 0 first, ascending within each rank (a stable counting sort)
+ *   counts  (host int[nranks], out) atoms per rank: rank r's ids start at
+ *           counts[0] + ... + counts[r-1].
+ * Needs no peers (any process, before or after registration).  HALO_ERR_GEOMETRY
+ * if some coordinate lies outside [0, L_d) or is NaN (counts and ids are still
+ * written).  Host-synchronises on `stream`. */
+HALO_API halo_status halo_assign_home(halo_ctx* ctx, const float* x, int n_atoms, int stride, int32_t* ids,
+                                      int* counts, void* stream);
+
 /* COLLECTIVE, NS step: home-atom redistribution before
  * halo_set_maps.  Between NS steps atoms move (the decomposition is
  * rebuilt every nstlist steps); the domains own the atoms inside their region
@@ -412,6 +428,36 @@ HALO_API halo_status halo_floor_launch_remote(halo_ctx* ctx, int peer_rank, int 
  * live sequence number.  Synchronises. */
 HALO_API halo_status halo_floor_bandwidth(halo_ctx* ctx, int peer_rank, size_t bytes, int mode, int iters,
                                           double* gbs);
+
+/* Floor-probe area (SURVEY 8(d) floors i/ii at payloads up to 64 MB): before
+ * halo_register_buffers and halo_pme_reserve, on every process with the same
+ * max_bytes, grows every rank's scratch by 4 KiB + 2 * max_bytes (a counter, a
+ * send area, a receive area; query halo_scratch_bytes after this call).
+ * HALO_ERR_STATE when called late or twice. */
+HALO_API halo_status halo_probe_reserve(halo_ctx* ctx, size_t max_bytes);
+
+/* Latency-vs-payload floor t(B) (SURVEY 8(d) floor i: "payload stores before
+ * the flag"): a ping-pong between this process's local rank 0 and `peer_rank`
+ * in which each leg stores `bytes` (multiple of 16, <= the reserved probe bytes)
+ * from the sender's probe send area into the receiver's probe receive area from
+ * min(ctas, ceil(bytes / 16 KiB)) CTAs, each CTA then signalling its slice with
+ * fence.acq_rel.sys + a system-scope add on the receiver's probe counter (the
+ * paper's per-CTA completion + signal, Alg. 5); the receiver's CTAs
+ * wait for all slices, then answer.  *one_way_us = median round trip / 2 of
+ * `iters` round trips (0 on the responder).  COLLECTIVE between the two
+ * processes (both call it with the same arguments; the lower rank initiates;
+ * both ranks on this GPU: one launch plays both sides).  Synchronises. */
+HALO_API halo_status halo_floor_payload(halo_ctx* ctx, int peer_rank, size_t bytes, int iters, int ctas,
+                                        double* one_way_us);
+
+/* Bandwidth floor to several concurrent peers (SURVEY 8(d) floor ii "one pair,
+ * and 3 concurrent peers"): `iters` back-to-back transfers of `bytes` from local
+ * rank 0's probe send area into the probe receive area of each of the n ranks
+ * in peers[] at once.  mode 0 = SM 16-B stores (8 CTAs per SM split over the
+ * peers), mode 1 = one cudaMemcpyAsync stream per peer.  *gbs = total bytes out
+ * / elapsed (GB/s).  One-sided; the peers must be idle.  Synchronises. */
+HALO_API halo_status halo_floor_bandwidth_multi(halo_ctx* ctx, const int* peers, int n, size_t bytes, int mode,
+                                                int iters, double* gbs);
 
 /* Host-block until all work this ctx enqueued is done; surfaces device error
  * words (HALO_ERR_TIMEOUT) and CUDA errors. */

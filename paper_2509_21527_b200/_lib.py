@@ -32,10 +32,10 @@ HALO_MAX_PULSES = 6
 EXPORTS = [
     "halo_init", "halo_query_config", "halo_local_ranks", "halo_pulse_order", "halo_scratch_bytes", "halo_register_buffers",
     "halo_ipc_export", "halo_ipc_import", "halo_set_maps", "halo_set_maps_explicit", "halo_get_layout",
-    "halo_get_map", "halo_migrate", "halo_transport", "halo_pme_reserve", "halo_pme_setup",
+    "halo_get_map", "halo_assign_home", "halo_migrate", "halo_transport", "halo_pme_reserve", "halo_pme_setup",
     "halo_pme_buffers", "halo_pme_send_x", "halo_pme_recv_f", "halo_exchange_x", "halo_exchange_f", "halo_exchange_xf", "halo_nccl_unique_id", "halo_nccl_init", "halo_nccl_version", "halo_nccl_exchange_x",
     "halo_nccl_exchange_f", "halo_step_host", "halo_pack_x_pulse",
-    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_launch_remote", "halo_floor_bandwidth", "halo_sync", "halo_strerror",
+    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_launch_remote", "halo_floor_bandwidth", "halo_probe_reserve", "halo_floor_payload", "halo_floor_bandwidth_multi", "halo_sync", "halo_strerror",
     "halo_last_error", "halo_destroy",
 ]
 
@@ -73,6 +73,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_set_maps_explicit": ([P, IP, IP, POINTER(IP), P], c_int),
         "halo_get_layout": ([P, c_int, IP, IP, IP, IP, IP, IP, IP, POINTER(c_uint)], c_int),
         "halo_get_map": ([P, c_int, c_int, IP, c_int], c_int),
+        "halo_assign_home": ([P, P, c_int, c_int, P, IP, P], c_int),
         "halo_migrate": ([P, IP, POINTER(c_void_p), POINTER(c_void_p), IP, P], c_int),
         "halo_transport": ([P, IP], c_int),
         "halo_pme_reserve": ([P, c_int], c_int),
@@ -98,6 +99,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_floor_launch": ([P, c_int, c_int, POINTER(c_double)], c_int),
         "halo_floor_launch_remote": ([P, c_int, c_int, c_int, c_int, POINTER(c_double)], c_int),
         "halo_floor_bandwidth": ([P, c_int, c_size_t, c_int, c_int, POINTER(c_double)], c_int),
+        "halo_probe_reserve": ([P, c_size_t], c_int),
+        "halo_floor_payload": ([P, c_int, c_size_t, c_int, c_int, POINTER(c_double)], c_int),
+        "halo_floor_bandwidth_multi": ([P, IP, c_int, c_size_t, c_int, c_int, POINTER(c_double)], c_int),
         "halo_sync": ([P], c_int),
         "halo_strerror": ([c_int], c_char_p),
         "halo_last_error": ([P], c_char_p),

@@ -13,7 +13,8 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhalo.so")
 SOURCES = ["runtime.cu", "kernels.cu", "kernels_ll.cu", "kernels_ce.cu", "kernels_ns.cu", "kernels_pme.cu",
-           "nccl_baseline.cu"]
+           "nccl_baseline.cu",
+           "kernels_floor.cu"]
 HEADERS = ["halo_internal.h", "ptx.cuh", os.path.join("..", "..", "include", "halo.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

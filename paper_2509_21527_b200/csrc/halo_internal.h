@@ -140,6 +140,11 @@ struct MigParams {
   int* err_host;
   uint64_t timeout_ns;
 };
+// halo_assign_home (kernels_ns.cu)
+struct AssignParams {
+  const double* planes;  // as MigParams::planes
+  int grid[3];
+};
 // per local rank results of the migration kernels
 struct MigCtrl {
   int32_t out_cnt[kMaxLocal][kStencil];   // rows this rank sends to stencil rank k (self included)

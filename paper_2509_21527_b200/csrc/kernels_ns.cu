@@ -349,4 +349,86 @@ cudaError_t launch_migrate(const MigParams& M, MigCtrl* C, int max_rows, int pha
   return cudaLaunchKernel((const void*)k_mig_ack, dim3(L), dim3(32), a2, 0, st);
 }
 
+// ------------------------------------------------------------ home assignment
+// halo_assign_home: the home DD rank of every atom of a global coordinate array
+// ("divides the simulation box into spatial regions (domains)"; R3/R4:
+// c_d = the number of interior planes b_d[k] <= float64(x_d), ties go up; rank =
+// (cx*np_y + cy)*np_z + cz), then a stable counting sort of the atom ids by
+// rank.  Pass 1: rank per atom + per-rank counts (CTA histogram, one atomic per
+// rank and CTA); x outside [0, L_d) sets err.  Pass 2: one CTA per rank scans
+// the ranks in order and appends its atom ids (warp ballot + CTA prefix), so
+// every rank's ids come out ascending.
+__global__ void __launch_bounds__(256) k_home_rank(const float* __restrict__ x, int n, int stride, AssignParams A,
+                                                   int32_t* __restrict__ rank, int* __restrict__ counts, int* err) {
+  __shared__ int s_cnt[kMaxRanks];
+  const int nr = A.grid[0] * A.grid[1] * A.grid[2];
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) s_cnt[r] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    int cell[3];
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double xd = (double)x[(size_t)i * stride + d];
+      const double* b = A.planes + d * kPlaneStride;
+      ok &= xd >= 0.0 && xd < b[A.grid[d]];  // also false for NaN
+      int k = 0;
+      for (int kk = 1; kk < A.grid[d]; ++kk)
+        if (b[kk] <= xd) k = kk;
+      cell[d] = k;
+    }
+    if (!ok) atomicOr(err, 1);
+    const int r = (cell[0] * A.grid[1] + cell[1]) * A.grid[2] + cell[2];
+    rank[i] = r;
+    atomicAdd(&s_cnt[r], 1);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < nr; r += blockDim.x)
+    if (s_cnt[r]) atomicAdd(&counts[r], s_cnt[r]);
+}
+
+__global__ void __launch_bounds__(1024) k_home_compact(const int32_t* __restrict__ rank, int n,
+                                                       const int* __restrict__ counts, int32_t* __restrict__ ids) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int r = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int q = 0; q < r; ++q) b += counts[q];
+    s_base = b;
+  }
+  __syncthreads();
+  int base = s_base;
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    const bool mine = i < n && rank[i] == r;
+    const unsigned m = __ballot_sync(0xffffffffu, mine);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      const int c = s_warp[w];
+      before += w < warp ? c : 0;
+      tot += c;
+    }
+    if (mine) ids[base + before + __popc(m & ((1u << lane) - 1u))] = i;
+    base += tot;
+    __syncthreads();  // s_warp is rewritten by the next chunk
+  }
+}
+
+cudaError_t launch_assign_home(const float* x, int n, int stride, const AssignParams& A, int32_t* rank, int* counts,
+                               int32_t* ids, int* err, cudaStream_t st) {
+  const int nr = A.grid[0] * A.grid[1] * A.grid[2];
+  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int) * nr, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(err, 0, sizeof(int), st);
+  if (e != cudaSuccess || n == 0) return e;
+  k_home_rank<<<(n + 255) / 256, 256, 0, st>>>(x, n, stride, A, rank, counts, err);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_home_compact<<<nr, 1024, 0, st>>>(rank, n, counts, ids);
+  return cudaGetLastError();
+}
+
 }  // namespace halo

@@ -44,6 +44,15 @@ cudaError_t launch_ce_unpack(int layout, const CeEnt* ents, int n_local, int max
                              cudaStream_t st);
 cudaError_t launch_ce_sync(const CeSyncParams& s, cudaStream_t st);
 cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
+cudaError_t launch_assign_home(const float* x, int n, int stride, const AssignParams& A, int32_t* rank, int* counts,
+                               int32_t* ids, int* err, cudaStream_t st);
+// floors (kernels_floor.cu)
+cudaError_t launch_payload_pingpong(const void* src_own, void* dst_peer, const void* src_peer_side, void* dst_own,
+                                    uint64_t* cnt_own, uint64_t* cnt_peer, size_t bytes, int G, int iters,
+                                    uint64_t cnt_base, uint64_t cnt_base_peer, int mode, uint64_t* rtt_ns,
+                                    uint64_t timeout_ns, int* err_host, cudaStream_t st);
+cudaError_t launch_bw_multi(const void* src, void* const* dst, int n, size_t bytes, int ctas_per_peer,
+                            cudaStream_t st);
 // NCCL send/recv baseline (nccl_baseline.cu)
 bool nccl_available(std::string* why);
 int nccl_version();
@@ -105,6 +114,8 @@ struct halo_ctx {
   size_t map_stride = 0, fbuf_stride = 0, ll_stride = 0, fsp_slots = 0, scratch_bytes = 0;
   size_t mig_off = 0;                // halo_migrate staging: [out | in] at this scratch offset
   size_t mig_stage = 0;              // bytes of one staging area (x | v | gid rows, capacity each)
+  size_t probe_off = 0, probe_max = 0;  // halo_probe_reserve: [counter 256 B | send | recv] (probe_max each)
+  uint64_t probe_cnt[kMaxLocal] = {0};  // value of each local rank's probe counter (all increments it has seen)
   int pme_rank = -1;                 // halo_pme_reserve: DD rank whose scratch holds pme_x | pme_f
   size_t pme_off = 0;                // their offset in that scratch (same layout on every rank)
   bool pme_ready = false;            // halo_pme_setup done for the current maps
@@ -140,6 +151,8 @@ struct halo_ctx {
   MigCtrl* d_migctrl = nullptr;
   double* d_planes = nullptr;
   uint64_t* d_rtt = nullptr;
+  char* d_assign = nullptr;         // halo_assign_home: rank per atom | counts | error word
+  size_t assign_bytes = 0;
   int* err_host = nullptr;          // host-mapped error word
   int* err_dev = nullptr;
   char* d_csr = nullptr;            // force-gather tasks + CSR of all local ranks (LL protocol)
@@ -1638,6 +1651,51 @@ halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gi
   return HALO_OK;
 }
 
+// ------------------------------------------------------------ floor probe area
+halo_status halo_probe_reserve(halo_ctx* ctx, size_t max_bytes) {
+  if (!ctx || max_bytes < 16) return HALO_ERR_ARG;
+  if (ctx->probe_max) return fail(ctx, HALO_ERR_STATE, "probe area already reserved");
+  if (ctx->pme_rank >= 0) return fail(ctx, HALO_ERR_STATE, "halo_probe_reserve must precede halo_pme_reserve");
+  for (int l = 0; l < ctx->n_local; ++l)
+    if (ctx->scratch[l]) return fail(ctx, HALO_ERR_STATE, "halo_probe_reserve must precede halo_register_buffers");
+  ctx->probe_max = align_up(max_bytes, 4096);
+  ctx->probe_off = align_up(ctx->scratch_bytes, 4096);
+  ctx->scratch_bytes = ctx->probe_off + 4096 + 2 * ctx->probe_max;
+  return HALO_OK;
+}
+
+// ------------------------------------------------------------ home assignment
+halo_status halo_assign_home(halo_ctx* ctx, const float* x, int n_atoms, int stride, int32_t* ids, int* counts,
+                             void* stream) {
+  if (!ctx || n_atoms < 0 || (n_atoms > 0 && (!x || !ids)) || stride < 3 || !counts) return HALO_ERR_ARG;
+  if ((uintptr_t)x & 3) return fail(ctx, HALO_ERR_ARG, "x must be 4-B aligned");
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t need = align_up(sizeof(int32_t) * std::max(n_atoms, 1), 256) + sizeof(int) * (kMaxRanks + 64);
+  if (need > ctx->assign_bytes) {
+    if (ctx->d_assign) CK(cudaFree(ctx->d_assign));
+    CK(cudaMalloc(&ctx->d_assign, need));
+    ctx->assign_bytes = need;
+  }
+  int32_t* rank = reinterpret_cast<int32_t*>(ctx->d_assign);
+  int* cnt = reinterpret_cast<int*>(ctx->d_assign + align_up(sizeof(int32_t) * std::max(n_atoms, 1), 256));
+  int* err = cnt + kMaxRanks;
+  double planes[3 * (kMaxRanks + 1)] = {0};
+  for (int d = 0; d < 3; ++d)
+    for (int k = 0; k <= ctx->cfg.grid[d]; ++k) planes[d * (kMaxRanks + 1) + k] = ctx->plane(d, k);
+  CK(cudaMemcpyAsync(ctx->d_planes, planes, sizeof planes, cudaMemcpyHostToDevice, st));
+  AssignParams A{};
+  A.planes = ctx->d_planes;
+  for (int d = 0; d < 3; ++d) A.grid[d] = ctx->cfg.grid[d];
+  CK(launch_assign_home(x, n_atoms, stride, A, rank, cnt, ids, err, st));
+  int h[kMaxRanks + 1] = {0};
+  CK(cudaMemcpyAsync(h, cnt, sizeof(int) * (kMaxRanks + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int r = 0; r < ctx->nranks; ++r) counts[r] = h[r];
+  if (h[kMaxRanks]) return fail(ctx, HALO_ERR_GEOMETRY, "a coordinate lies outside [0, L_d) (or is NaN)");
+  return HALO_OK;
+}
+
 // ------------------------------------------------------------ PP <-> PME (f4)
 halo_status halo_pme_reserve(halo_ctx* ctx, int pme_rank) {
   if (!ctx || pme_rank < 0 || pme_rank >= ctx->nranks) return HALO_ERR_ARG;
@@ -2178,6 +2236,107 @@ halo_status halo_floor_bandwidth(halo_ctx* ctx, int peer_rank, size_t bytes, int
   return HALO_OK;
 }
 
+// t(B): one-way latency of a B-byte payload + its signal, half the median round trip.
+halo_status halo_floor_payload(halo_ctx* ctx, int peer_rank, size_t bytes, int iters, int ctas, double* one_way_us) {
+  if (!ctx || peer_rank < 0 || peer_rank >= ctx->nranks || iters <= 0 || ctas <= 0) return HALO_ERR_ARG;
+  if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
+  if (!ctx->probe_max) return fail(ctx, HALO_ERR_STATE, "halo_probe_reserve first");
+  bytes = bytes / 16 * 16;
+  if (bytes == 0 || bytes > ctx->probe_max) return fail(ctx, HALO_ERR_ARG, "bytes must be in [16, reserved probe bytes]");
+  const int me = ctx->first_rank;
+  if (peer_rank == me) return fail(ctx, HALO_ERR_ARG, "peer must differ from local rank 0");
+  const bool local = peer_rank >= ctx->first_rank && peer_rank < ctx->first_rank + ctx->n_local;
+  const bool initiator = local || me < peer_rank;
+  const int G = (int)std::min<size_t>((size_t)ctas, std::max<size_t>(1, (bytes + 16383) / 16384));
+  if (local && 2 * G > std::max(2, ctx->max_x)) return fail(ctx, HALO_ERR_ARG, "too many CTAs for a same-GPU probe");
+  CK(cudaSetDevice(ctx->cfg.device));
+  if (ctx->d_rtt == nullptr || iters > 1 << 16) {
+    if (ctx->d_rtt) CK(cudaFree(ctx->d_rtt));
+    CK(cudaMalloc(&ctx->d_rtt, sizeof(uint64_t) * std::max(iters, 1 << 16)));
+  }
+  auto area = [&](int r) { return ctx->peer_scratch[r] + ctx->probe_off; };
+  uint64_t* cnt_own = reinterpret_cast<uint64_t*>(area(me));
+  uint64_t* cnt_peer = reinterpret_cast<uint64_t*>(area(peer_rank));
+  const int lp = peer_rank - ctx->first_rank;
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CK(launch_payload_pingpong(area(me) + 4096, area(peer_rank) + 4096 + ctx->probe_max,
+                             local ? area(peer_rank) + 4096 : nullptr, area(me) + 4096 + ctx->probe_max, cnt_own,
+                             cnt_peer, bytes, G, iters, ctx->probe_cnt[0], local ? ctx->probe_cnt[lp] : 0,
+                             local ? 2 : (initiator ? 1 : 0), ctx->d_rtt, (uint64_t)(ctx->cfg.timeout_s * 1e9),
+                             ctx->err_dev, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaStreamDestroy(st));
+  ctx->probe_cnt[0] += (uint64_t)G * iters;
+  if (local) ctx->probe_cnt[lp] += (uint64_t)G * iters;
+  halo_status s = check_err_word(ctx);
+  if (s != HALO_OK) return s;
+  if (one_way_us) {
+    *one_way_us = 0.0;
+    if (initiator) {
+      std::vector<uint64_t> v(iters);
+      CK(cudaMemcpy(v.data(), ctx->d_rtt, sizeof(uint64_t) * iters, cudaMemcpyDeviceToHost));
+      std::sort(v.begin(), v.end());
+      *one_way_us = (double)v[iters / 2] / 2.0 / 1000.0;
+    }
+  }
+  return HALO_OK;
+}
+
+// SM peer-store (mode 0) or copy-engine (mode 1) bandwidth from local rank 0 to
+// n concurrent peers (bytes each, back-to-back launches); *gbs = total GB/s out.
+halo_status halo_floor_bandwidth_multi(halo_ctx* ctx, const int* peers, int n, size_t bytes, int mode, int iters,
+                                       double* gbs) {
+  if (!ctx || !peers || n <= 0 || n > kMaxRanks || iters <= 0 || !gbs || (mode != 0 && mode != 1)) return HALO_ERR_ARG;
+  if (!ctx->peers_ready) return fail(ctx, HALO_ERR_STATE, "import peers first");
+  if (!ctx->probe_max) return fail(ctx, HALO_ERR_STATE, "halo_probe_reserve first");
+  bytes = bytes / 16 * 16;
+  if (bytes == 0 || bytes > ctx->probe_max) return fail(ctx, HALO_ERR_ARG, "bytes must be in [16, reserved probe bytes]");
+  void* dst[kMaxRanks];
+  for (int i = 0; i < n; ++i) {
+    if (peers[i] < 0 || peers[i] >= ctx->nranks || peers[i] == ctx->first_rank) return HALO_ERR_ARG;
+    dst[i] = ctx->peer_scratch[peers[i]] + ctx->probe_off + 4096 + ctx->probe_max;
+  }
+  const char* src = ctx->scratch[0] + ctx->probe_off + 4096;
+  CK(cudaSetDevice(ctx->cfg.device));
+  int sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device));
+  std::vector<cudaStream_t> ss(mode == 1 ? n : 1);
+  for (auto& s : ss) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  std::vector<cudaEvent_t> ej(ss.size());
+  for (auto& e : ej) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  auto one = [&]() -> cudaError_t {
+    if (mode == 0) return launch_bw_multi(src, dst, n, bytes, std::max(1, 8 * sms / n), ss[0]);
+    for (int i = 0; i < n; ++i) {
+      cudaError_t e = cudaMemcpyAsync(dst[i], src, bytes, cudaMemcpyDefault, ss[i]);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  for (int i = 0; i < 3; ++i) CK(one());
+  // start: every stream past the warm-up; end: every stream's copies done
+  CK(cudaEventRecord(e0, ss[0]));
+  for (size_t i = 1; i < ss.size(); ++i) CK(cudaStreamWaitEvent(ss[i], e0, 0));
+  for (int i = 0; i < iters; ++i) CK(one());
+  for (size_t i = 1; i < ss.size(); ++i) {
+    CK(cudaEventRecord(ej[i], ss[i]));
+    CK(cudaStreamWaitEvent(ss[0], ej[i], 0));
+  }
+  CK(cudaEventRecord(e1, ss[0]));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  *gbs = (double)bytes * n * iters / (1e-3 * (double)ms) / 1e9;
+  CK(cudaEventDestroy(e0));
+  CK(cudaEventDestroy(e1));
+  for (auto& e : ej) CK(cudaEventDestroy(e));
+  for (auto& s : ss) CK(cudaStreamDestroy(s));
+  return HALO_OK;
+}
+
 halo_status halo_sync(halo_ctx* ctx) {
   if (!ctx) return HALO_ERR_ARG;
   CK(cudaSetDevice(ctx->cfg.device));
@@ -2199,6 +2358,7 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_migctrl) (void)cudaFree(ctx->d_migctrl);
   if (ctx->d_planes) (void)cudaFree(ctx->d_planes);
   if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
+  if (ctx->d_assign) (void)cudaFree(ctx->d_assign);
   if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
   if (ctx->d_ce) (void)cudaFree(ctx->d_ce);
   if (ctx->d_stage) (void)cudaFree(ctx->d_stage);

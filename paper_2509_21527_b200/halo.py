@@ -62,6 +62,7 @@ class Halo:
         cfg = make_config(grid, box, cutoff, pulses, layout, capacity, device, flags, nprocs, proc, timeout_s)
         self.cfg = cfg
         self.layout = int(layout)
+        self.nranks = int(grid[0]) * int(grid[1]) * int(grid[2])
         h = c_void_p()
         st = self.lib.halo_init(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:
@@ -145,6 +146,16 @@ class Halo:
         self._ck(self.lib.halo_get_map(self.h, int(local), int(pulse),
                                        out.ctypes.data_as(ctypes.POINTER(c_int)), c_int(n)))
         return out[:n]
+
+    def assign_home(self, x_ptr, n_atoms, stride, ids_ptr, stream=0):
+        """Home rank of every row of a global DEVICE coordinate array (halo_assign_home);
+        fills ids_ptr (device int32[n_atoms], grouped by rank, ascending) and returns the
+        per-rank counts."""
+        nr = self.nranks
+        cnt = (c_int * nr)()
+        self._ck(self.lib.halo_assign_home(self.h, c_void_p(x_ptr), int(n_atoms), int(stride), c_void_p(ids_ptr), cnt,
+                                           c_void_p(stream)))
+        return [int(cnt[r]) for r in range(nr)]
 
     def migrate(self, n_home, gid_ptrs, v_ptrs=None, stream=0):
         """NS-step home-atom redistribution (halo_migrate); returns the new n_home per local rank."""
@@ -273,6 +284,25 @@ class Halo:
         v = c_double()
         self._ck(self.lib.halo_floor_bandwidth(self.h, int(peer_rank), c_size_t(int(nbytes)), int(mode), int(iters),
                                                ctypes.byref(v)))
+        return v.value
+
+    def probe_reserve(self, max_bytes):
+        """Reserve the floor-probe area (before register_buffers; same size on every rank)."""
+        self._ck(self.lib.halo_probe_reserve(self.h, c_size_t(int(max_bytes))))
+
+    def floor_payload(self, peer_rank, nbytes, iters=200, ctas=592) -> float:
+        """One-way latency (us) of an nbytes payload + its signal to peer_rank (collective with the peer)."""
+        v = c_double()
+        self._ck(self.lib.halo_floor_payload(self.h, int(peer_rank), c_size_t(int(nbytes)), int(iters), int(ctas),
+                                             ctypes.byref(v)))
+        return v.value
+
+    def floor_bandwidth_multi(self, peers, nbytes, mode=0, iters=20) -> float:
+        """Total GB/s from local rank 0 to len(peers) concurrent peers (SM stores / copy engine)."""
+        arr = (c_int * len(peers))(*[int(p) for p in peers])
+        v = c_double()
+        self._ck(self.lib.halo_floor_bandwidth_multi(self.h, arr, len(peers), c_size_t(int(nbytes)), int(mode),
+                                                     int(iters), ctypes.byref(v)))
         return v.value
 
     def sync(self):

@@ -10,25 +10,23 @@ import torch
 from .halo import Halo
 
 
-def assign_home(X: np.ndarray, L, grid):
-    """Home DD rank of every atom (input preparation at a neighbour-search step,
-    not a hot-path step): c_d = number of interior planes float64(L_d)*k/grid[d]
-    (k = 1..grid[d]-1) that are <= float64(x_d); rank = (cx*np_y + cy)*np_z + cz.
-    Returns a list, per rank, of atom ids in ascending order."""
-    X = np.asarray(X, dtype=np.float32)
-    c = np.zeros((X.shape[0], 3), dtype=np.int64)
-    for d in range(3):
-        Ld = float(np.float32(L[d]))
-        inner = np.array([Ld * k / grid[d] for k in range(1, grid[d])], dtype=np.float64)
-        c[:, d] = np.searchsorted(inner, X[:, d].astype(np.float64), side="right")
-    r = (c[:, 0] * grid[1] + c[:, 1]) * grid[2] + c[:, 2]
-    order = np.argsort(r, kind="stable")
-    counts = np.bincount(r, minlength=grid[0] * grid[1] * grid[2])
-    out, s = [], 0
-    for n in counts:
-        out.append(order[s:s + n])
-        s += n
-    return out
+def assign_home(X: np.ndarray, L, grid, cutoff, pulses, device=0):
+    """Home DD rank of every atom at a neighbour-search step (input preparation,
+    not a hot-path step), computed on the GPU by ``halo_assign_home`` (R3/R4
+    planes, stable counting sort).  Returns a list, per rank, of atom ids in
+    ascending order."""
+    X = np.ascontiguousarray(np.asarray(X, dtype=np.float32))
+    dev = torch.device("cuda", device)
+    h = Halo(grid, L, cutoff, pulses, capacity=1, device=device)
+    try:
+        xd = torch.from_numpy(X).to(dev)
+        ids = torch.empty(max(X.shape[0], 1), dtype=torch.int32, device=dev)
+        counts = h.assign_home(xd.data_ptr(), X.shape[0], X.shape[1], ids.data_ptr(),
+                               torch.cuda.current_stream(dev).cuda_stream)
+        ids = ids[: X.shape[0]].cpu().numpy().astype(np.int64)
+    finally:
+        h.destroy()
+    return np.split(ids, np.cumsum(counts)[:-1])
 
 
 class HaloSession:
@@ -36,7 +34,7 @@ class HaloSession:
     registers them, and imports the peers' IPC blobs over ``torch.distributed``."""
 
     def __init__(self, grid, box, cutoff, pulses, layout=3, capacity=1 << 16, device=0, flags=0,
-                 nprocs=1, proc=0, timeout_s=10.0, group=None, pme_rank=None):
+                 nprocs=1, proc=0, timeout_s=10.0, group=None, pme_rank=None, probe_bytes=None):
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         self.halo = Halo(grid, box, cutoff, pulses, layout=layout, capacity=capacity, device=device, flags=flags,
@@ -46,6 +44,8 @@ class HaloSession:
         self.first_rank, self.n_local = self.halo.local_ranks()
         self.npulse = len(self.halo.pulse_order())
         self.pme_rank = pme_rank
+        if probe_bytes:  # floor-probe area (halo_probe_reserve), before PME and registration
+            self.halo.probe_reserve(probe_bytes)
         if pme_rank is not None:  # PP <-> PME buffers in pme_rank's scratch (before registration)
             self.halo.pme_reserve(pme_rank)
         sb = self.halo.scratch_bytes()

@@ -113,7 +113,7 @@ def main():
     from synth import forces_normal
 
     c, X = bench.build_workload(args.config)
-    homes = assign_home(X, c.L, c.grid)
+    homes = assign_home(X, c.L, c.grid, c.rc, c.pulses)
     cap = int(max(len(h) for h in homes) * 2.2) + 4096
     nl_ranks = c.nranks // world
     first = rank * nl_ranks

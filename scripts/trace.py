@@ -46,7 +46,7 @@ def main():
     from paper_2509_21527_b200.session import HaloSession, assign_home
     from synth import forces_normal
     c, X = bench.build_workload(args.config)
-    homes = assign_home(X, c.L, c.grid)
+    homes = assign_home(X, c.L, c.grid, c.rc, c.pulses)
     cap = int(max(len(h) for h in homes) * 2.2) + 4096
     dev = torch.device("cuda", local)
     sess = HaloSession(c.grid, c.L, c.rc, c.pulses, capacity=cap, device=local, flags=HALO_F_TIMERS | args.flags,
