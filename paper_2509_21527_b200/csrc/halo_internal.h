@@ -31,7 +31,10 @@ constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIM
 constexpr int kTraceW = 16;            // ... words per CTA: 4 stamps + (tag, end) of its first 6 items
 constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-force slot area)
 constexpr int kMaxItemRows = 512;      // largest work item (x items carry their map slice in shared memory)
-constexpr int kRing = 4;               // LL kernels: item blocks in flight per CTA (narrow variants)
+constexpr int kMaxTreeRows = 170;      // largest small-tree item (2 passes of 85 roots x 3 components)
+constexpr int kTreeRowsOcc = 85;       // tree item size the occupancy (co-resident grid) is computed for
+constexpr int kRing = 4;
+constexpr int kXCounters = 32;               // LL kernels: item blocks in flight per CTA (narrow variants)
 constexpr uint32_t kPollTight = 0xffffffffu;  // ExParams.poll_ns: tight polling only, no backoff (HALO_POLL_NS=-1)
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
@@ -93,9 +96,11 @@ struct Ctrl {
   uint32_t done_pme[2];
   uint32_t cnt_pme[2][kMaxLocal];
   int32_t pme_nh[kMaxLocal][kMaxRanks];   // halo_pme_setup: n_home of every rank, seen by local rank l
-  // LL x items finished into each local rank's halo in this NS epoch (zeroed by
-  // set_maps): the fused x+f launch starts rank l's gather items at xin_n x launches
-  uint64_t xin[kMaxLocal];
+  // LL x items finished in this NS epoch (zeroed by set_maps), counted by CTA
+  // (counter blockIdx mod 32, each on its own 32-B sector: no same-address
+  // serialisation); the fused x+f launch starts its tree items once every x item
+  // of the launch is done
+  uint64_t xcnt[kXCounters][4];
 };
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4,
@@ -173,7 +178,9 @@ enum : uint32_t { kMutateXNoWait = 16u, kMutateFNoWait = 32u, kCountNotify = 64u
                    // data stores, so rank 0's z0 rows arrive after everything else
                    kDelayPulse0 = 2048u,
                    // fshift partials accumulated in fp32 (shows the 1e-12 * sum|terms| bound catches it)
-                   kMutateFshiftF32 = 4096u};
+                   kMutateFshiftF32 = 4096u,
+                   // timing experiment: per-CTA stamps inside the first tree item (trace slots 10-13)
+                   kTraceDetail = 8192u};
 
 struct RankDev {
   float* x;                 // own x (capacity rows)
@@ -215,7 +222,7 @@ struct PulseDev {
 };
 
 enum : uint8_t { kItemXIndep = 0, kItemXDep = 1, kItemPush = 2, kItemUnpack = 3, kItemXRecv = 4, kItemGather = 5,
-                 kItemFshift = 6 };
+                 kItemFshift = 6, kItemXSend = 7, kItemTree = 8, kItemTreeG = 9 };
 constexpr uint8_t kHomeLevel = 0xff;   // Item.pulse of gather items over home rows
 
 struct Item {
@@ -226,49 +233,115 @@ struct Item {
   uint32_t end;
 };
 
-// LL protocol work records: each item's block starts with one 128-B record that
-// carries every pointer it needs, followed by the item's map slice (x) or task
-// records (f), so a cold-L2 launch pays one round trip for its plan instead of a
-// chain of dependent loads; the next item's block is prefetched (cp.async).
+// LL protocol work records.  Ranks of this process that share a GPU form one
+// HOP GROUP: a pulse between two ranks of a group is not a
+// transport hop, so the plan resolves it on the host at the NS step — every halo
+// row an item writes names its ORIGIN (a home row, or the LL unit in which it
+// crossed from another group) plus the periodic shifts of the pulses it went
+// through, and the force halo of a group is a set of TREES (a row, the images it
+// was sent as, their images, ...) each folded by one thread in the oracle's
+// order.  Only pulses between groups move LL units and wait for their tags.
+// Each item's block starts with one 128-B record followed by its entries (x),
+// or its roots and nodes (f); blocks are fixed-size and bulk-loaded into a ring
+// of shared-memory slots.
+struct LocalBase {          // per local rank, copied to shared memory at kernel start
+  float* x;                 // own x
+  float* f;                 // own f
+  uint64_t* xll;            // own coordinate LL area (slot q at + q*ll_stride)
+  uint64_t* fll;            // own force LL area
+  int32_t recv_off[kMaxP];  // own receive ranges (rows)
+  int32_t pad[2];
+};
+static_assert(sizeof(LocalBase) == 64, "LocalBase");
+
+// x entry (8 B): the origin of one halo row an item writes.
+//   row   origin row in x of local rank l (kind X), or the unit row i of l's
+//         coordinate LL slot q (kind LL: the row crossed from another group there)
+//   kq    bit 7: LL origin, bits 0-2: q
+//   mask  pulses whose +L shift the row picked up after its origin, ascending
+//         (R25: one fp32 add of the shift vector per such pulse)
+struct XEnt {
+  uint32_t row;
+  uint8_t l, kq, mask, pad;
+};
+static_assert(sizeof(XEnt) == 8, "XEnt");
+
 struct __align__(128) XRec {
-  uint8_t kind;             // kItemXIndep / kItemXDep / kItemXRecv
+  uint8_t kind;             // kItemXSend / kItemXRecv
   uint8_t pulse;
   uint16_t lrank;
   uint32_t n_units;         // rows * layout
-  float shift[3];           // +L_d on the dim axis, 0 elsewhere (R25)
-  uint32_t has_shift;
-  const int32_t* map;       // send: map_p + begin
-  const float* x;           // send: own x base
-  uint64_t* ll;             // send: receiver's LL slot p + begin*W; recv: own LL slot p + begin*W
-  float* xdst;              // recv: own x + (recv_off_p + begin)*W; send: the receiver's x rows when the
-                            // receiver is a DD rank of this process (direct write, no receive item), else null
-  const uint64_t* xll_own;  // dep send: own coordinate LL base (slot q at + q*ll_stride)
-  int32_t recv_off[kMaxP];  // dep send: own receive ranges
-  int32_t recv_size[kMaxP];
-  uint64_t* xin;            // &ctrl->xin[l] of the local rank whose halo rows this item completes, or null
-  uint64_t pad;
+  uint32_t begin;           // send: first send index (destination row remote_off + begin + e)
+  uint32_t cls;             // dependency class (plan order; trace only)
+  float* dst_x;             // send to a rank of this group: its x at row remote_off (direct store)
+  uint64_t* dst_ll;         // send to another group: the receiver's coordinate LL slot p
+  float shiftL[kMaxP];      // L_{d_q}: the shift of pulse q (applied iff the entry's mask has q)
+  uint8_t pdim[kMaxP];      // d_q
+  uint8_t pad0[2];
+  uint64_t* ll;             // recv: own LL slot p + begin*W
+  float* xdst;              // recv: own x + (recv_off_p + begin)*W
+  uint64_t pad2;
+  uint8_t pad1[128 - 88];
 };
 static_assert(sizeof(XRec) == 128, "XRec must be one 128-B line");
 
+// f trees.  value(node) = f[node] + sum over children, pulses descending (R15);
+// a node is a row of f of local rank l (kind F) or the LL unit in which a child
+// in another group pushed its value (kind LL: unit row i of l's force LL slot q).
+// F nodes with children store their value.  A root with its parent in another
+// group pushes its value to `push` (the parent's force LL slot) — Alg. 5 DEP_MGMT
+// across groups.  Every edge (parent, child) lies in the tree of its parent, so
+// the shift force of the edge (R13: the parent's rank wrapped in the edge's pulse)
+// is added there, into one of the item's buckets (targets 3 * local rank + dim).
+//
+// Small trees (<= kFastNodes nodes: every tree when P <= 3) — kItemTree blocks:
+// [GRec | TRoot x rows | node rows (8 x u32: row | l << 24, depth-first, children
+// in descending pulse order) x rows]; the tree's shape lives in the root record
+// as 4-bit fields, so a thread folds its tree in registers.
+struct TRoot {
+  uint64_t* push;           // or null
+  uint32_t par;             // nibble k: index of node k's parent (0xf: none / the root)
+  uint32_t bucket;          // nibble k: the item's shift-force bucket of the edge into node k (kFsNone: none)
+  uint32_t q;               // nibble k: pulse of node k when it is an LL node
+  uint8_t nn;               // nodes
+  uint8_t llmask;           // bit k: node k is an LL node
+  uint8_t stmask;           // bit k: node k (F, with children) stores its folded value
+  uint8_t pad0;
+  uint32_t pad1[2];
+};
+static_assert(sizeof(TRoot) == 32, "TRoot");
+// Larger trees — kItemTreeG blocks: [GRec | TRootG x rows/8 | TNode x (rest)].
+struct TRootG {
+  uint64_t* push;
+  uint32_t node_begin;
+  uint16_t n_nodes;
+  uint16_t pad;
+};
+static_assert(sizeof(TRootG) == 16, "TRootG");
+struct TNode {
+  uint32_t il;              // idx | l << 24 (F: row; LL: unit row i; rows < 2^24)
+  uint8_t kq;               // bit 7: LL node, bits 0-2: its pulse q, bits 3-6: the item's shift-force
+                            // bucket of the edge from the parent (kFsNone: none, kFsDirect: use fs)
+  uint8_t parent;           // index of the parent node in the tree (0xff: the root)
+  uint8_t flags;            // bit 0: store the folded value; bits 1-7: depth
+  uint8_t fs;               // shift-force target of that edge (3 * parent's local rank + dim), or 0xff
+};
+static_assert(sizeof(TNode) == 8, "TNode");
+constexpr int kMaxDepth = kMaxP + 1;
+constexpr int kFastNodes = 8;
+constexpr int kMaxBuckets = 8;     // distinct shift-force targets per f item (reduced in shared memory)
+constexpr uint8_t kFsNone = 15, kFsDirect = 14;
+constexpr uint32_t kMaxRows = 1u << 24;
+
 struct __align__(128) GRec {
-  uint8_t kind;             // kItemGather or kItemFshift
-  uint8_t level;            // slice of this pulse, or kHomeLevel
+  uint8_t kind;             // kItemTree / kItemTreeG
+  uint8_t level;            // dependency class
   uint16_t lrank;
-  uint32_t n_units;         // gather: tasks * layout
-  uint32_t wrap_mask;       // combine: pulses this rank shifted in (R13)
-  uint8_t pulse_dim[8];
-  uint32_t pad;
-  const int4* tasks;        // unused (the task records follow the GRec in its item block)
-  float* f;                 // gather: own f base
-  const uint64_t* fll_own;  // own force LL base (slot q at + q*ll_stride)
-  uint64_t* push;           // gather of slice rows: x-sender's LL slot p minus recv_off_p*W (index row*W + c)
-  uint64_t* part;           // gather of a slice whose x-sender shifted in that pulse: the x-sender's
-                            // shift-force slot of this item (3 doubles = 6 LL units, peer pointer);
-                            // combine: own shift-force slot area
-  uint32_t nslot[kMaxP];    // combine: slots of each pulse (0 unless this rank shifted in it)
-  const uint64_t* xin;      // fused launch: &ctrl->xin[lrank] (gather items wait for xin_n per x launch)
-  uint32_t xin_n;           // x items that complete this rank's halo rows
-  uint8_t pad2[128 - 100];  // keep one 128-B line
+  uint32_t n_units;         // roots * layout
+  uint32_t n_roots, n_nodes;
+  uint8_t n_buckets;        // shift-force buckets of this item's edges
+  uint8_t bucket_fs[kMaxBuckets];  // their targets (3 * local rank + dim)
+  uint8_t pad[128 - 16 - 1 - kMaxBuckets];
 };
 static_assert(sizeof(GRec) == 128, "GRec must be one 128-B line");
 
@@ -295,12 +368,14 @@ struct ExParams {
                             // ctrl->seq_x/f + 1 in the kernel: graph-captured launches, R17)
   const char* xblk;         // LL x item blocks: [XRec | map slice, item_rows int32], 128 + 4*item_rows B each
   const char* fblk;         // LL f item blocks: [GRec | task records, item_rows x 32 B], 128 + 32*item_rows B each
-  int item_rows;
+  int item_rows;            // LL: x entries per item (x block = 128 + 8 * item_rows B)
+  int tree_rows;            // LL: roots per small-tree item (f block = 128 + 64 * tree_rows B)
   int n_items_x;            // fused launch: items [0, n_items_x) are x items, then the f items
   int ring;                 // LL: item-block ring slots per CTA
   uint64_t seq_f;           // fused launch: the f sequence number by value (0 = read ctrl->seq_f + 1)
-  uint64_t seq_x0;          // fused launch: ctrl->seq_x at the end of set_maps (xin counts from there)
+  uint64_t seq_x0;          // fused launch: ctrl->seq_x at the end of set_maps (xcnt counts from there)
   int delay_rank;           // HALO_DEBUG kDelayPulse0: the DD rank whose pulse-0 sends are slowed
+  const LocalBase* lbase;   // LL: [n_local] (copied to shared memory by every CTA)
 };
 
 // Copy-engine path (HALO_F_CE_PATH, kernels_ce.cu): one entry per (pulse, local rank).

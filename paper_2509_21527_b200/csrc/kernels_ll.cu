@@ -3,37 +3,41 @@
 // The paper signals each pulse with one system-scope release flag issued by
 // the last CTA after a completion counter (Alg. 5).  On B200 each
 // such hop costs a MEMBAR.SYS per CTA + an atomic + a release store + the
-// remote poll.  Here every 8-byte store carries its own 32-bit sequence tag
-// next to one fp32 value (single-copy atomic), so:
+// remote poll.  Here every 8-byte store that crosses between GPUs carries its
+// own 32-bit sequence tag next to one fp32 value (single-copy atomic), so:
 //   * no fences, counters or flags on the data path;
-//   * forwarding is row-level: a dependent row is re-sent as soon as its
-//     units arrive (Alg. 4's dependency wait shrinks to the rows actually read);
-//   * the force halo is a deterministic GATHER: every target row adds its
-//     contributions in descending pulse order (R15) from the LL force buffers,
-//     and a halo slice row is pushed back as soon as it is final (Alg. 5
-//     DEP_MGMT at row granularity).  Bit-exact with the oracle, no atomics.
+//   * forwarding is row-level: a forwarded row leaves as soon as its own unit
+//     arrived (Alg. 4's dependency wait shrinks to the rows actually read);
+//   * the force halo is a deterministic fold in the oracle's order (R15), no
+//     atomics, and a row is pushed back as soon as it is final (Alg. 5
+//     DEP_MGMT at row granularity).
 //
-//   * a receiver on the same GPU (a DD rank of this process) gets its halo
-//     rows stored directly by the sender; only rows from other GPUs go through
-//     receive items (LL units -> x);
-//   * shift forces: per-item fp64 partials of the pushers, one deterministic
-//     combine per (rank, wrapped dim) in its own CTA.
+// Hop groups: the DD ranks a process drives share one GPU's
+// memory, so a pulse between two of them is not a transport hop.  The plan
+// (runtime.cu, at the NS step) resolves such pulses: every halo row an x item
+// writes names its origin — a home row, or the LL unit in which the row crossed
+// from another group — and the +L shifts it picked up on the way (applied in
+// pulse order: the oracle's fp32 adds, bit for bit); the force halo of a group
+// is a set of trees, each folded by one thread per component with children in
+// descending pulse order.  Only pulses between groups wait.  With one DD rank
+// per GPU (the paper's setup) every pulse is a hop and this is the paper's
+// staged schedule; HALO_COLLAPSE=0 makes every rank its own group on any GPU
+// count (the staged schedule on one GPU: the cross-GPU code paths under test).
 //
 // One kernel body serves three launches (kMode): the x halo, the f halo, and
 // both in ONE launch (halo_exchange_xf; "a single kernel for
-// x+f when no compute sits between them") in which the f items of a DD rank
-// start once that rank's halo rows are complete (per-rank item counter, the
+// x+f when no compute sits between them") in which the tree items start once
+// every halo row of the process is complete (a launch-wide item counter, the
 // place of the non-bonded kernel between the two exchanges, Alg. 2).
 //
-// Each CTA runs a static list of work items; every item is one contiguous
-// block in HBM (128-B XRec / GRec + map slice / task records).  A ring of
-// kRing shared-memory slots is filled by bulk (TMA) copies completing on
-// mbarriers: the first blocks are requested before griddepcontrol.wait (static
-// plan data, overlapped with the previous kernel's drain), and the block of
-// item j+ring is requested as soon as item j is done, so a CTA that runs
-// several items pays the cold-HBM round trip for its plan once.  Items are
-// processed in a static order in which every wait targets an earlier item
-// (DESIGN.md §6); the grid never exceeds the co-resident CTA count.
+// Each CTA runs a static list of work items; every item is one fixed-size block
+// in HBM.  A ring of kRing shared-memory slots is filled by bulk (TMA) copies
+// completing on mbarriers: the first blocks are requested before
+// griddepcontrol.wait (static plan data, overlapped with the previous kernel's
+// drain), and the block of item j+ring is requested as soon as item j is done.
+// Items are ordered by dependency class (a wait only targets an item of a lower
+// class on another GPU); the grid never exceeds the co-resident
+// CTA count.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -96,11 +100,12 @@ __device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64
 // a batch is issued before any store — the stores are asm volatile with a
 // memory clobber, so one unit at a time would serialise a memory latency each).
 template <int W, int kU>
-__device__ __forceinline__ void x_item(const XRec& r, const int32_t* s_map, const ExParams& P, uint32_t tag) {
+__device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const LocalBase* lb, const ExParams& P,
+                                       uint32_t tag) {
   const uint32_t n = r.n_units;
   const uint32_t B = blockDim.x;
   if (r.kind == kItemXRecv) {
-    // this rank's halo rows of one pulse from another GPU: LL units -> x rows;
+    // this rank's halo rows of one pulse from another group: LL units -> x rows;
     // 4 units per thread per batch: the polls of a batch are in flight together
     constexpr int kR = 4;
     for (uint32_t base = threadIdx.x; base < n; base += kR * B) {
@@ -112,302 +117,289 @@ __device__ __forceinline__ void x_item(const XRec& r, const int32_t* s_map, cons
       for (int k = 0; k < kR; ++k) {
         const uint32_t u = base + k * B;
         if (u >= n) continue;
-        if ((uint32_t)(w[k] >> 32) != tag && !(P.debug & kLocalSink))
+        if ((uint32_t)(w[k] >> 32) != tag)
           w[k] = ll_spin(r.ll + u, tag, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse), P.poll_ns);
         r.xdst[u] = __uint_as_float((uint32_t)w[k]);
       }
     }
-  } else if (r.kind == kItemXIndep) {
-    // SEND of home rows: gather through the map, shift (R25), tag, store into the receiver's LL slot
-    for (uint32_t base = threadIdx.x; base < n; base += kU * B) {
-      float v[kU];
+    return;
+  }
+  // SEND (Alg. 3 + Alg. 4): per halo row, its origin (home row, or the LL unit in
+  // which it entered this group: a row-level dependency wait) + its shifts (R25)
+  for (uint32_t base = threadIdx.x; base < n; base += kU * B) {
+    uint64_t w[kU];
+    const uint64_t* src[kU];
+    uint32_t mask[kU];
 #pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        const uint32_t u = base + k * B;
-        if (u < n) {
-          const uint32_t i = u / W;
-          v[k] = __ldg(r.x + (size_t)s_map[i] * W + (u - i * W));  // home row: never written during the kernel
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        const uint32_t u = base + k * B;
-        if (u >= n) continue;
-        const int c = (int)(u % W);
-        const float o = (r.has_shift && c < 3) ? __fadd_rn(v[k], r.shift[c]) : v[k];
-        uint64_t* dst = (P.debug & kLocalSink) ? const_cast<uint64_t*>(r.xll_own) + (size_t)r.pulse * P.ll_stride + u
-                                               : r.ll + u;
-        st_relaxed_sys(dst, ll_pack(o, tag));
-        if (r.xdst) r.xdst[u] = o;  // same-process receiver: its halo row directly (kernel end publishes it)
-      }
-    }
-  } else {
-    // SEND of forwarded rows: the pulse each arrived in (Alg. 4 dependent part, R8/R9);
-    // the row-level wait is the LL tag of the source unit
-    for (uint32_t base = threadIdx.x; base < n; base += kU * B) {
-      uint64_t w[kU];
-      const uint64_t* src[kU];
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        const uint32_t u = base + k * B;
-        src[k] = nullptr;
-        if (u < n) {
-          const uint32_t i = u / W;
-          const int c = (int)(u - i * W);
-          const int idx = s_map[i];
-          int q = 0;
-          while (q < P.P - 1 && (unsigned)(idx - r.recv_off[q]) >= (unsigned)r.recv_size[q]) ++q;
+    for (int k = 0; k < kU; ++k) {
+      const uint32_t u = base + k * B;
+      src[k] = nullptr;
+      if (u < n) {
+        const uint32_t e = u / W;
+        const int c = (int)(u - e * W);
+        const XEnt E = ent[e];
+        const LocalBase& L = lb[E.l];
+        mask[k] = E.mask;
+        if (!(E.kq & 0x80u)) {
+          // a home row: never written during the kernel
+          w[k] = ((uint64_t)tag << 32) | __float_as_uint(__ldg(L.x + (size_t)E.row * W + c));
+        } else {
+          const int q = E.kq & 7;
           if (q < P.p_lo || (P.debug & kMutateXNoWait)) {
-            // arrived in an earlier launch (set_maps); kMutateXNoWait: the protocol
-            // mutation the sentinel tests must catch (forward without waiting)
-            w[k] = ((uint64_t)tag << 32) | __float_as_uint(__ldcg(r.x + (size_t)idx * W + c));
+            // arrived in an earlier launch (set_maps' per-pulse exchanges): final in x.
+            // kMutateXNoWait: the protocol mutation the sentinel tests must catch —
+            // forward the row from x without waiting for its arrival
+            w[k] = ((uint64_t)tag << 32) | __float_as_uint(__ldcg(L.x + (size_t)(L.recv_off[q] + E.row) * W + c));
           } else {
-            src[k] = r.xll_own + (size_t)q * P.ll_stride + (size_t)(idx - r.recv_off[q]) * W + c;
+            src[k] = L.xll + (size_t)q * P.ll_stride + (size_t)E.row * W + c;
             w[k] = ld_relaxed_sys(src[k]);
           }
         }
       }
+    }
 #pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        const uint32_t u = base + k * B;
-        if (u >= n) continue;
-        if (src[k] != nullptr && (uint32_t)(w[k] >> 32) != tag && !(P.debug & kLocalSink))
-          w[k] = ll_spin(src[k], tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, r.pulse), P.poll_ns);
-        const int c = (int)(u % W);
-        float v = __uint_as_float((uint32_t)w[k]);
-        if (r.has_shift && c < 3) v = __fadd_rn(v, r.shift[c]);
-        uint64_t* dst = (P.debug & kLocalSink) ? const_cast<uint64_t*>(r.xll_own) + (size_t)r.pulse * P.ll_stride + u
-                                               : r.ll + u;
-        st_relaxed_sys(dst, ll_pack(v, tag));
-        if (r.xdst) r.xdst[u] = v;
+    for (int k = 0; k < kU; ++k) {
+      const uint32_t u = base + k * B;
+      if (u >= n) continue;
+      const uint32_t e = u / W;
+      const int c = (int)(u - e * W);
+      if (src[k] != nullptr && (uint32_t)(w[k] >> 32) != tag)
+        w[k] = ll_spin(src[k], tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, r.pulse), P.poll_ns);
+      float v = __uint_as_float((uint32_t)w[k]);
+      if (c < 3) {
+#pragma unroll
+        for (int q = 0; q < kMaxP; ++q)
+          if (mask[k] >> q & 1u) v = __fadd_rn(v, c == r.pdim[q] ? r.shiftL[q] : 0.0f);
       }
+      const size_t o = (size_t)(r.begin + e) * W + c;
+      if (r.dst_x != nullptr) r.dst_x[o] = v;  // a rank of this group: its halo row directly
+      else st_relaxed_sys(r.dst_ll + o, ll_pack(v, tag));
     }
   }
   // experiment (HALO_DEBUG=128): drain this thread's peer stores inside the item
-  if ((P.debug & kFenceAfterPeerStores) && r.kind != kItemXRecv) fence_sys();
+  if (P.debug & kFenceAfterPeerStores) fence_sys();
 }
 
 // ---------------------------------------------------------------- f items
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// threads per CTA of the LL kernels (HALO_F_THREADS build switch for the A/B)
-#ifndef HALO_F_THREADS
-#define HALO_F_THREADS 256
-#endif
-constexpr int kThreadsF = HALO_F_THREADS;
-static_assert(kThreadsF == kThreads || HALO_F_THREADS != 256, "LL CTA size");
-
-// Deterministic CTA reduction of N outputs held per thread in s_red[j][tid]:
-// output j is summed by warp (j mod warps), each lane over a fixed strided slice
-// of the threads, then a fixed xor-shuffle tree; threads j < N return output j.
-// Every thread has passed the __syncthreads before any shuffle, so no lane
-// waits for another's polling loop (a full-mask SHFL right after the divergent
-// polling loop had cost ~10 us per level at C3); 2 barriers instead of the 9 of
-// a pairwise shared-memory tree.
-template <int N>
-__device__ __noinline__ double cta_reduce(double (*s_red)[kThreadsF], int j_out) {
-  __shared__ double s_out[9];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
-  for (int j = warp; j < N; j += nw) {
-    double v = 0.0;
-    for (int t = lane; t < kThreadsF; t += 32) v += s_red[j][t];
-    v = warp_sum_d(v);
-    if (lane == 0) s_out[j] = v;
-  }
-  __syncthreads();
-  const double tot = (j_out < N) ? s_out[j_out] : 0.0;
-  __syncthreads();
-  return tot;
-}
-
-// Combine item of one rank (R13): the pushers of its wrapping pulses summed,
-// per work item, the forces they pushed back to it (3 doubles per slot as tagged
-// LL units: no flag, no fence).  One thread per (pulse, slot, component) triple
-// in a fixed assignment, then a fixed tree: deterministic, no atomics; only this
-// CTA writes the rank's fshift[dim].
-__device__ __noinline__ void fshift_combine(const GRec& g, const ExParams& P, uint32_t tag, double (*s_red)[kThreadsF],
-                                            uint32_t fsp_slots) {
-  const int dim = g.level;
-  const bool f32 = (P.debug & kMutateFshiftF32) != 0;  // mutation: fp32 accumulation
-  const double fs_old = (threadIdx.x < 3) ? P.fshift[9 * g.lrank + 3 * dim + threadIdx.x] : 0.0;
-#pragma unroll
-  for (int j = 0; j < 3; ++j) s_red[j][threadIdx.x] = 0.0;
-  // one flat index space over (pulse, slot, component) triples; every load of a
-  // thread is issued before any wait is resolved
-  uint32_t off[kMaxP + 1];
-  off[0] = 0;
-#pragma unroll
-  for (int q = 0; q < kMaxP; ++q) off[q + 1] = off[q] + (q < P.P ? g.nslot[q] * 3 : 0u);
-  const uint32_t n = off[kMaxP];
-  constexpr int kB = 4;
-  for (uint32_t base = threadIdx.x; base < n; base += kB * blockDim.x) {
-    const uint64_t* ptr[kB];
-    uint64_t hv[kB], lv[kB];
-    int dc[kB];
-#pragma unroll
-    for (int k = 0; k < kB; ++k) {
-      const uint32_t e = base + k * blockDim.x;
-      ptr[k] = nullptr;
-      if (e < n) {
-        int q = 0;
-        while (e >= off[q + 1]) ++q;
-        const uint32_t pp = e - off[q];  // slot * 3 + component
-        ptr[k] = g.part + (size_t)q * fsp_slots * 6 + 2 * (size_t)pp;
-        dc[k] = (int)(pp % 3);  // component (the item's pulses all shift along `dim`)
-        hv[k] = ld_relaxed_sys(ptr[k]);
-        lv[k] = ld_relaxed_sys(ptr[k] + 1);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kB; ++k) {
-      if (ptr[k] == nullptr) continue;
-      if ((uint32_t)(hv[k] >> 32) != tag) hv[k] = ll_spin(ptr[k], tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 0), 0);
-      if ((uint32_t)(lv[k] >> 32) != tag) lv[k] = ll_spin(ptr[k] + 1, tag, P.timeout_ns, P.err_host, tcode(13, g.lrank, 1), 0);
-      const double v = __hiloint2double((int)(uint32_t)hv[k], (int)(uint32_t)lv[k]);
-      double& a = s_red[dc[k]][threadIdx.x];
-      a = f32 ? (double)((float)a + (float)v) : a + v;
-    }
-  }
-  const double tot = cta_reduce<3>(s_red, threadIdx.x);
-  if (threadIdx.x < 3)
-    P.fshift[9 * g.lrank + 3 * dim + threadIdx.x] = f32 ? (double)((float)fs_old + (float)tot) : fs_old + tot;
-}
-
-// One gather item: every task row adds its contributions from the force LL
-// buffers in descending pulse order (R15: bit-exact with the oracle), is
-// written back, and — slice rows — pushed to the x-sender's force LL buffer at
-// once (Alg. 5 DEP_MGMT at row granularity).  The pushers of a slice whose
-// x-sender shifted also sum what they push (fixed tree) into its slot (R13).
-// kF = units per thread per batch (1: latency regime, 2: large items).
-template <int W, int kF>
-__device__ __forceinline__ void f_item(const GRec& g, const int4* tasks, const ExParams& P, uint32_t tag,
-                                       double (*s_fs)[kThreadsF]) {
-  const uint32_t n = g.n_units;
-  const bool push = g.level != kHomeLevel;
-  const bool part = (P.fshift != nullptr) && (g.part != nullptr) && !(P.debug & kLocalSink);
-  // stride = a multiple of W: every thread keeps one component c
-  const uint32_t S = (blockDim.x / W) * W;
-  const int c = (int)(threadIdx.x % W);
-  double acc = 0.0;
-  if (threadIdx.x < S) {
-    // task records, f and the contributions of a batch are loaded before any
-    // wait or store
-    for (uint32_t base = threadIdx.x; base < n; base += kF * S) {
-      int4 a[kF], b[kF];
-#pragma unroll
-      for (int k = 0; k < kF; ++k) {
-        const uint32_t u = base + k * S;
-        if (u >= n) continue;
-        a[k] = tasks[2 * (u / W)];
-        b[k] = tasks[2 * (u / W) + 1];
-      }
-      // contributions j < kPre are loaded with the batch, any further ones (more
-      // than kPre pulses touching one row) when resolved
-      constexpr int kPre = 3;
-      float v[kF];
-      uint64_t w[kF][kPre];
-#pragma unroll
-      for (int k = 0; k < kF; ++k) {
-        const uint32_t u = base + k * S;
-        if (u >= n) continue;
-        const uint32_t cc[kMaxP] = {(uint32_t)a[k].z, (uint32_t)a[k].w, (uint32_t)b[k].x,
-                                    (uint32_t)b[k].y, (uint32_t)b[k].z, (uint32_t)b[k].w};
-        v[k] = g.f[(size_t)a[k].x * W + c];
-#pragma unroll
-        for (int j = 0; j < kPre; ++j)
-          if (j < a[k].y)
-            w[k][j] = ld_relaxed_sys(g.fll_own + (size_t)(cc[j] >> 24) * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c);
-      }
-#pragma unroll
-      for (int k = 0; k < kF; ++k) {
-        const uint32_t u = base + k * S;
-        if (u >= n) continue;
-        const int t = a[k].x, m = a[k].y;
-        const uint32_t cc[kMaxP] = {(uint32_t)a[k].z, (uint32_t)a[k].w, (uint32_t)b[k].x,
-                                    (uint32_t)b[k].y, (uint32_t)b[k].z, (uint32_t)b[k].w};
-        float vv = v[k];
-#pragma unroll
-        for (int j = 0; j < kMaxP; ++j) {
-          if (j < m) {  // pulses descending (R15): one fp32 RNE add per (entry, pulse)
-            const int q = (int)(cc[j] >> 24);
-            const uint64_t* src = g.fll_own + (size_t)q * P.ll_stride + (size_t)(cc[j] & 0xffffffu) * W + c;
-            uint64_t wj = j < kPre ? w[k][j < kPre ? j : 0] : ld_relaxed_sys(src);
-            if ((uint32_t)(wj >> 32) != tag && !(P.debug & (kMutateFNoWait | kLocalSink)))
-              wj = ll_spin(src, tag, P.timeout_ns, P.err_host, tcode(12, g.lrank, q), P.poll_ns);
-            const float val = __uint_as_float((uint32_t)wj);
-            vv = P.accumulate ? __fadd_rn(vv, val) : val;
-          }
-        }
-        g.f[(size_t)t * W + c] = vv;
-        if (push)
-          st_relaxed_sys((P.debug & kLocalSink) ? const_cast<uint64_t*>(g.fll_own) + (size_t)t * W + c
-                                                : g.push + (size_t)t * W + c,
-                         ll_pack(vv, tag));
-        if (part) acc += (double)vv;
-      }
-    }
-  }
-  if ((P.debug & kFenceAfterPeerStores) && push) fence_sys();  // experiment (HALO_DEBUG=128)
-  if (part) {  // fixed-tree CTA sum of the pushed forces per component -> the x-sender's slot
-#pragma unroll
-    for (int j = 0; j < 3; ++j) s_fs[j][threadIdx.x] = (threadIdx.x < S && c == j) ? acc : 0.0;
-    double tot = cta_reduce<3>(s_fs, threadIdx.x);
-    if (P.debug & kMutateFshiftF32) tot = (double)(float)tot;  // mutation: fp32 partials
-    if (threadIdx.x < 3) {
-      st_relaxed_sys(g.part + 2 * threadIdx.x, ll_pack(__uint_as_float((uint32_t)__double2hiint(tot)), tag));
-      st_relaxed_sys(g.part + 2 * threadIdx.x + 1, ll_pack(__uint_as_float((uint32_t)__double2loint(tot)), tag));
-    }
-  }
-}
-
-// Fused launch: a gather item of rank l waits until every x item that completes
-// l's halo rows (same-GPU senders' direct rows, receive items) has finished in
-// this launch — the position of the non-bonded kernel between exchange_x and
-// exchange_f (Alg. 2).  Counters are monotonic within an NS epoch (zeroed by
-// set_maps; every LL x launch of the epoch adds its items), so the target of
-// this launch is xin_n * (x launches of the epoch up to this one).  Bounded.
-__device__ __noinline__ void xin_wait(const uint64_t* cnt, uint64_t target, const ExParams& P, int lrank) {
+// Fused launch: warp 0 waits until every x item of this launch is done.  Lane k
+// watches counter k (bumped after each x item i = k mod 32, by every x launch);
+// its target is the number of such items per launch times the x launches of
+// this NS epoch (`launches`).  Bounded like every wait.
+__device__ __noinline__ void xcount_wait(Ctrl* ctrl, int nx, uint64_t launches, const ExParams& P) {
+  const int k = threadIdx.x;
+  const uint64_t tgt = (k < nx ? (uint64_t)((nx - 1 - k) / kXCounters + 1) : 0u) * launches;
+  const uint64_t* cnt = &ctrl->xcnt[k][0];
   const uint64_t t0 = gtimer();
   for (uint32_t it = 1;; ++it) {
-    if (ld_relaxed_gpu(cnt) >= target) return;
+    if (__all_sync(0xffffffffu, ld_relaxed_gpu(cnt) >= tgt)) break;
     if ((it & 15u) == 0) {
       const uint64_t el = gtimer() - t0;
       if (el > 20000) __nanosleep(256);
       if ((it & 1023u) == 0) {
         if (el > P.timeout_ns) {
-          report_timeout(P.err_host, tcode(15, lrank, 0));
+          if (k == 0) report_timeout(P.err_host, tcode(15, 0, 0));
           return;
         }
         if (*(volatile int*)P.err_host != 0) return;
       }
     }
   }
+  (void)ld_acquire_gpu(cnt);  // the counted items' stores happen-before the tree items
 }
 
-__device__ __forceinline__ void red_add_gpu(uint64_t* p, uint64_t v) {
-  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Shift forces (R13; north_star): the value of every edge whose parent's rank
+// wrapped in the edge's pulse goes to fshift[rank][dim].  Each thread adds its
+// edges' values into its own column of the item's buckets (fp64, shared memory,
+// no atomics); after the item a fixed-order reduction per (bucket, component)
+// and ONE fp64 atomic add per (bucket, component) into fshift.  Edges of a tree
+// with more distinct targets than kMaxBuckets add directly (kFsDirect).
+__device__ __forceinline__ void fs_bucket_add(double (*s_v)[kThreads], int b, float v, const ExParams& P) {
+  double& a = s_v[b][threadIdx.x];
+  a = (P.debug & kMutateFshiftF32) ? (double)((float)a + v) : a + (double)v;  // mutation: fp32 accumulation
+}
+__device__ __forceinline__ void fs_add(double (*s_v)[kThreads], const TNode& nd, int c, float v,
+                                       const ExParams& P) {
+  const int b = (nd.kq >> 3) & 15;
+  if (b == kFsNone || c >= 3) return;
+  if (b == kFsDirect) atomicAdd(P.fshift + 3 * nd.fs + c, (double)v);
+  else fs_bucket_add(s_v, b, v, P);
+}
+
+__device__ __forceinline__ float ll_value(uint64_t w, const uint64_t* src, const ExParams& P, uint32_t tag,
+                                          int lrank, int q) {
+  if ((uint32_t)(w >> 32) != tag && !(P.debug & kMutateFNoWait))
+    w = ll_spin(src, tag, P.timeout_ns, P.err_host, tcode(12, lrank, q), P.poll_ns);
+  return __uint_as_float((uint32_t)w);
+}
+
+// Large trees (> kFastNodes nodes, P > 3): depth-first fold with an explicit
+// stack of open levels, one node at a time.
+template <int W>
+__device__ __noinline__ float tree_fold_generic(const TNode* nd, int nn, const LocalBase* lb, const ExParams& P,
+                                                int c, uint32_t tag, int lrank, double (*s_v)[kThreads], bool fs_on) {
+  float acc[kMaxDepth];
+  int stk[kMaxDepth];
+  int top = 0;
+  auto load = [&](const TNode& m) -> float {
+    const LocalBase& L = lb[m.il >> 24];
+    const uint32_t idx = m.il & (kMaxRows - 1);
+    if (!(m.kq & 0x80u)) return __ldcg(L.f + (size_t)idx * W + c);
+    const uint64_t* a = L.fll + (size_t)(m.kq & 7) * P.ll_stride + (size_t)idx * W + c;
+    return ll_value(ld_relaxed_sys(a), a, P, tag, lrank, m.kq & 7);
+  };
+  auto close_to = [&](int d) {
+    for (int t = top; t >= d && t >= 1; --t) {
+      const TNode& m = nd[stk[t]];
+      if (m.flags & 1u) lb[m.il >> 24].f[(size_t)(m.il & (kMaxRows - 1)) * W + c] = acc[t];
+      if (fs_on) fs_add(s_v, m, c, acc[t], P);
+      acc[t - 1] = P.accumulate ? __fadd_rn(acc[t - 1], acc[t]) : acc[t];
+    }
+    top = min(top, d - 1);
+  };
+  acc[0] = load(nd[0]);
+  stk[0] = 0;
+  for (int k = 1; k < nn; ++k) {
+    const int d = nd[k].flags >> 1;
+    close_to(d);
+    acc[d] = load(nd[k]);
+    stk[d] = k;
+    top = d;
+  }
+  close_to(1);
+  if (nd[0].flags & 1u) lb[nd[0].il >> 24].f[(size_t)(nd[0].il & (kMaxRows - 1)) * W + c] = acc[0];
+  return acc[0];
+}
+
+// After an item: the fixed-order reduction of its shift-force buckets; output
+// (b, comp) by warp (b*3 + comp) mod warps, lanes over the threads of that
+// component in a fixed order, then a fixed xor-shuffle tree, one fp64 atomic.
+template <int W>
+__device__ __forceinline__ void fs_flush(const GRec& g, double (*s_v)[kThreads], uint32_t S, const ExParams& P) {
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+  for (int o = warp; o < 3 * g.n_buckets; o += nw) {
+    const int b = o / 3, cc = o % 3;
+    double a = 0.0;
+    for (uint32_t t = cc + W * lane; t < S; t += 32 * W) a += s_v[b][t];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+    if (P.debug & kMutateFshiftF32) a = (double)(float)a;  // mutation: fp32 partials
+    if (lane == 0 && a != 0.0) atomicAdd(P.fshift + 3 * g.bucket_fs[b] + cc, a);
+  }
+}
+
+// One small-tree item: each (root, component) is folded by one thread.  All node
+// values are loaded first (every load in flight: F rows straight into v[], LL
+// units into w[]), then the fold runs in reverse preorder on the root record's
+// 4-bit shape fields: a node's children follow it in preorder, so they are final
+// when it is reached, and their in-order sum is its fold (f[node] + children,
+// pulses descending, one fp32 RNE add per child: the oracle's order, R15).
+template <int W>
+__device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, const uint4* nodes, const LocalBase* lb,
+                                          const ExParams& P, uint32_t tag, double (*s_v)[kThreads], uint64_t* tdet) {
+  const uint32_t n = g.n_units;
+  const uint32_t S = (blockDim.x / W) * W;  // stride: a multiple of W, every thread keeps one component
+  const int c = (int)(threadIdx.x % W);
+  const bool fs_on = P.fshift != nullptr && g.n_buckets > 0;
+  if (fs_on)
+    for (int b = 0; b < g.n_buckets; ++b) s_v[b][threadIdx.x] = 0.0;
+  for (uint32_t u = threadIdx.x; u < n && threadIdx.x < S; u += S) {
+    const uint32_t j = u / W;
+    const TRoot R = roots[j];
+    const uint4 n0 = nodes[2 * j], n1 = nodes[2 * j + 1];
+    const uint32_t il[kFastNodes] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+    const int nn = R.nn;
+    float v[kFastNodes];
+    uint64_t w[kFastNodes];
+    auto ll_addr = [&](int k) -> const uint64_t* {
+      return lb[il[k] >> 24].fll + (size_t)(R.q >> (4 * k) & 15u) * P.ll_stride +
+             (size_t)(il[k] & (kMaxRows - 1)) * W + c;
+    };
+#pragma unroll
+    for (int k = 0; k < kFastNodes; ++k) {
+      if (k < nn) {
+        if (R.llmask >> k & 1u) w[k] = ld_relaxed_sys(ll_addr(k));
+        else v[k] = __ldcg(lb[il[k] >> 24].f + (size_t)(il[k] & (kMaxRows - 1)) * W + c);
+      }
+    }
+    if (tdet && u == 0) tdet[0] = gtimer() + (__float_as_uint(v[0]) == 0x7fc00001u ? 1 : 0);  // loads landed
+    if (R.llmask) {
+#pragma unroll
+      for (int k = 1; k < kFastNodes; ++k)
+        if (k < nn && (R.llmask >> k & 1u)) {
+          if ((uint32_t)(w[k] >> 32) != tag && !(P.debug & kMutateFNoWait))
+            w[k] = ll_spin(ll_addr(k), tag, P.timeout_ns, P.err_host, tcode(12, g.lrank, R.q >> (4 * k) & 15u),
+                           P.poll_ns);
+          v[k] = __uint_as_float((uint32_t)w[k]);
+        }
+    }
+#pragma unroll
+    for (int k = kFastNodes - 1; k >= 0; --k) {
+      if (k < nn) {
+#pragma unroll
+        for (int m = k + 1; m < kFastNodes; ++m)
+          if ((R.par >> (4 * m) & 15u) == (uint32_t)k) v[k] = P.accumulate ? __fadd_rn(v[k], v[m]) : v[m];
+        if (R.stmask >> k & 1u) lb[il[k] >> 24].f[(size_t)(il[k] & (kMaxRows - 1)) * W + c] = v[k];
+        if (k > 0 && fs_on && c < 3) {
+          const int b = R.bucket >> (4 * k) & 15u;
+          if (b != kFsNone) fs_bucket_add(s_v, b, v[k], P);
+        }
+      }
+    }
+    if (R.push != nullptr) st_relaxed_sys(R.push + c, ll_pack(v[0], tag));
+    if (tdet && u == 0) tdet[1] = gtimer();  // folded and stored
+  }
+  if (tdet) tdet[2] = gtimer();  // (thread 0) before the shift-force flush
+  if (fs_on) fs_flush<W>(g, s_v, S, P);
+  if (tdet) tdet[3] = gtimer();
+}
+
+// One large-tree item (kItemTreeG): the generic fold, one (root, component) per thread.
+template <int W>
+__device__ __forceinline__ void tree_item_generic(const GRec& g, const TRootG* roots, const TNode* nodes,
+                                                  const LocalBase* lb, const ExParams& P, uint32_t tag,
+                                                  double (*s_v)[kThreads]) {
+  const uint32_t n = g.n_units;
+  const uint32_t S = (blockDim.x / W) * W;
+  const int c = (int)(threadIdx.x % W);
+  const bool fs_on = P.fshift != nullptr;
+  if (fs_on)
+    for (int b = 0; b < g.n_buckets; ++b) s_v[b][threadIdx.x] = 0.0;
+  for (uint32_t u = threadIdx.x; u < n && threadIdx.x < S; u += S) {
+    const TRootG R = roots[u / W];
+    const float root = tree_fold_generic<W>(nodes + R.node_begin, R.n_nodes, lb, P, c, tag, g.lrank, s_v, fs_on);
+    if (R.push != nullptr) st_relaxed_sys(R.push + c, ll_pack(root, tag));
+  }
+  if (fs_on && g.n_buckets > 0) fs_flush<W>(g, s_v, S, P);
+}
+
+// Item completion count: a release (after the CTA barrier that follows the item's
+// stores, so the CTA's stores are ordered before it); the waiters acquire.
+__device__ __forceinline__ void red_add_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // ---------------------------------------------------------------- kernel
 enum : int { kModeX = 0, kModeF = 1, kModeXF = 2 };
 
+// Item block sizes: x = record + item_rows entries; f = record + tree_rows small
+// tree roots (32 B) and their nodes (32 B) — a large-tree block has the same size.
+__host__ __device__ __forceinline__ uint32_t xblk_bytes(uint32_t R) { return 128u + 8u * R; }
+__host__ __device__ __forceinline__ uint32_t fblk_bytes(uint32_t R) { return 128u + 64u * R; }
+
 // Items of this CTA: [0, n_main) round-robin over CTAs [0, G - n_tail) (fused:
-// the x items first, then the f items), the n_tail shift-force combines (last in
-// the item order) one dedicated CTA each, so they start polling at once.
-template <int W, int kU, int kF, int kMode>
-__global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) : (kF == 1 ? 5 : 4)) k_exchange_ll(
+// the x items first, then the tree items); n_tail trailing items would get one
+// dedicated CTA each (none in the current plan).
+template <int W, int kU, int kMode>
+__global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) : 4) k_exchange_ll(
     const __grid_constant__ ExParams P) {
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq[2];
   __shared__ __align__(8) uint64_t s_bar[kRing];
-  __shared__ double s_fs[kMode == kModeX ? 1 : 3][kMode == kModeX ? 1 : kThreadsF];
-  const uint32_t R = (uint32_t)P.item_rows;
-  const uint32_t XB = 128u + 4u * R, FB = 128u + 32u * R;
+  __shared__ __align__(16) LocalBase s_lb[kMaxLocal];
+  __shared__ double s_v[kMode == kModeX ? 1 : kMaxBuckets][kThreads];  // shift-force buckets of an f item
+  const uint32_t R = (uint32_t)P.item_rows, RT = (uint32_t)P.tree_rows;
+  const uint32_t XB = xblk_bytes(R), FB = fblk_bytes(RT);
   const uint32_t SB = kMode == kModeX ? XB : FB;  // ring slot size
   const int nx = kMode == kModeF ? 0 : P.n_items_x;
   const int ring = P.ring;
@@ -426,14 +418,17 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
     return i < nx ? P.xblk + (size_t)i * XB : P.fblk + (size_t)(i - nx) * FB;
   };
   auto bytes_of = [&](int i) -> uint32_t { return i < nx ? XB : FB; };
-  // the first `ring` blocks are static plan data: bulk copies issued while the
-  // previous kernel of the stream drains (PDL); x, f, LL are touched after the wait
+  // static plan data, read while the previous kernel of the stream drains (PDL):
+  // the first `ring` item blocks (bulk copies) and the local-rank base table;
+  // x, f and the LL areas are touched after the wait
   if (threadIdx.x == 0) {
     for (int k = 0; k < ring; ++k) mbar_init(&s_bar[k], 1);
     fence_mbar_init();
     for (int k = 0, i = first; k < ring && i < end; ++k, i += stride)
       bulk_load(s_blk + (size_t)k * SB, blk_of(i), bytes_of(i), &s_bar[k]);
   }
+  for (int t = threadIdx.x; t < P.n_local * 4; t += blockDim.x)
+    reinterpret_cast<int4*>(s_lb)[t] = __ldg(reinterpret_cast<const int4*>(P.lbase) + t);
   pdl_wait();  // everything below may depend on earlier work of the stream
   // by value when the host knows them (no cold dependent load on the critical path)
   if (threadIdx.x == 0) {
@@ -441,10 +436,12 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
     if (kMode != kModeX) s_seq[1] = P.seq_f ? P.seq_f : ld_relaxed_gpu(&ctrl->seq_f) + 1;
   }
   timer_start(P.flags, kMode == kModeF ? &ctrl->t_start_f : &ctrl->t_start_x);
-  __syncthreads();  // barrier init and sequence numbers visible to every thread
+  __syncthreads();  // barrier init, base table and sequence numbers visible to every thread
   // arrive early: the atomic's latency hides behind the items (launch_arrive)
   const uint32_t arrived = launch_arrive(kMode == kModeF ? &ctrl->done_f : &ctrl->done_x);
   const uint32_t tag_x = (uint32_t)s_seq[0], tag_f = (uint32_t)s_seq[1];
+  bool xin_seen = false;
+  bool tdet_free = true;  // HALO_DEBUG kTraceDetail: stamps of the first tree item in trace slots 10-13
   int j = 0;
   for (int it = first; it < end; it += stride, ++j) {
     const int slot = j % ring;
@@ -453,23 +450,32 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
     if (trace && j == 0) ctrl->trace[tslot][blockIdx.x][1] = gtimer();
     if (kMode != kModeF && it < nx) {
       const XRec& r = *reinterpret_cast<const XRec*>(blk);
-      x_item<W, kU>(r, reinterpret_cast<const int32_t*>(blk + 128), P, tag_x);
+      x_item<W, kU>(r, reinterpret_cast<const XEnt*>(blk + 128), s_lb, P, tag_x);
       __syncthreads();  // the item's rows are stored (fused: before its count) and the slot is free
-      if (threadIdx.x == 0 && r.xin != nullptr) red_add_gpu(r.xin, 1u);
+      if (threadIdx.x == 0) {  // every x launch counts (the fused launch's targets count all of them)
+        uint64_t* cnt = &ctrl->xcnt[it % kXCounters][0];
+        if (kMode == kModeXF) red_add_release_gpu(cnt, 1u);
+        else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
+      }
     } else if constexpr (kMode != kModeX) {
       const GRec& g = *reinterpret_cast<const GRec*>(blk);
-      if (kMode == kModeXF && g.xin != nullptr) {  // this rank's halo is complete (the NB kernel's slot)
-        if (threadIdx.x == 0) xin_wait(g.xin, (uint64_t)g.xin_n * (s_seq[0] - P.seq_x0), P, g.lrank);
+      if (kMode == kModeXF && !xin_seen) {  // every halo row of this process is complete (the NB kernel's slot)
+        if (threadIdx.x < 32) xcount_wait(ctrl, nx, s_seq[0] - P.seq_x0, P);
         __syncthreads();
+        xin_seen = true;
       }
-      if (g.kind == kItemFshift) {
-        if (P.fshift != nullptr) fshift_combine(g, P, tag_f, s_fs, P.fsp_slots);
-      } else {
-        f_item<W, kF>(g, reinterpret_cast<const int4*>(blk + 128), P, tag_f, s_fs);
-      }
+      if (g.kind == kItemTree)
+        tree_item<W>(g, reinterpret_cast<const TRoot*>(blk + 128), reinterpret_cast<const uint4*>(blk + 128 + 32 * RT),
+                     s_lb, P, tag_f, s_v,
+                     (trace && (P.debug & kTraceDetail) && tdet_free) ? &ctrl->trace[tslot][blockIdx.x][10] : nullptr);
+      else
+        tree_item_generic<W>(g, reinterpret_cast<const TRootG*>(blk + 128),
+                             reinterpret_cast<const TNode*>(blk + 128 + 16 * (RT / 8 > 0 ? RT / 8 : 1)), s_lb, P,
+                             tag_f, s_v);
       __syncthreads();  // everyone is done with this slot
+      if (g.kind == kItemTree) tdet_free = false;
     }
-    if (trace && j < (kTraceW - 4) / 2) {
+    if (trace && j < ((P.debug & kTraceDetail) ? 3 : (kTraceW - 4) / 2)) {
       const uint8_t* b8 = reinterpret_cast<const uint8_t*>(blk);  // kind, pulse/level, lrank: same offsets in XRec/GRec
       ctrl->trace[tslot][blockIdx.x][4 + 2 * j] =
           ((uint64_t)b8[0] << 16) | ((uint64_t)(*reinterpret_cast<const uint16_t*>(b8 + 2)) << 8) | b8[1];
@@ -506,18 +512,20 @@ cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** ar
 
 template <int W>
 static const void* ll_fn(int mode, bool wide) {
-  if (mode == kModeX) return wide ? (const void*)k_exchange_ll<W, 4, 2, kModeX> : (const void*)k_exchange_ll<W, 1, 1, kModeX>;
-  if (mode == kModeF) return wide ? (const void*)k_exchange_ll<W, 4, 2, kModeF> : (const void*)k_exchange_ll<W, 1, 1, kModeF>;
-  return wide ? (const void*)k_exchange_ll<W, 4, 2, kModeXF> : (const void*)k_exchange_ll<W, 1, 1, kModeXF>;
+  if (mode == kModeX) return wide ? (const void*)k_exchange_ll<W, 4, kModeX> : (const void*)k_exchange_ll<W, 1, kModeX>;
+  if (mode == kModeF) return wide ? (const void*)k_exchange_ll<W, 4, kModeF> : (const void*)k_exchange_ll<W, 1, kModeF>;
+  return wide ? (const void*)k_exchange_ll<W, 4, kModeXF> : (const void*)k_exchange_ll<W, 1, kModeXF>;
 }
 static const void* ll_fn(int layout, int mode, bool wide) { return layout == 4 ? ll_fn<4>(mode, wide) : ll_fn<3>(mode, wide); }
 
 // Ring slots (item blocks in flight per CTA) and dynamic shared memory.
 int ll_ring(bool wide) { return wide ? 2 : kRing; }
-size_t ll_smem_bytes(int mode, int rows, bool wide) {
-  const size_t sb = mode == kModeX ? 128 + 4 * (size_t)rows : 128 + 32 * (size_t)rows;
+size_t ll_smem_bytes(int mode, int rows, int tree_rows, bool wide) {
+  const size_t sb = mode == kModeX ? xblk_bytes((uint32_t)rows) : fblk_bytes((uint32_t)tree_rows);
   return (size_t)ll_ring(wide) * sb;
 }
+uint32_t ll_xblk_bytes(int rows) { return xblk_bytes((uint32_t)rows); }
+uint32_t ll_fblk_bytes(int tree_rows) { return fblk_bytes((uint32_t)tree_rows); }
 
 // mode: 0 = x, 1 = f, 2 = fused x+f.  wide = the plan's work items are large
 // (bandwidth regime): batched variants.
@@ -525,7 +533,7 @@ cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid
                                const cudaAccessPolicyWindow* win, cudaStream_t st) {
   void* args[] = {(void*)&p};
   return launch_coop_kernel_ex(ll_fn(layout, mode, wide), grid, kThreads, args, st, true,
-                               ll_smem_bytes(mode, p.item_rows, wide), win);
+                               ll_smem_bytes(mode, p.item_rows, p.tree_rows, wide), win);
 }
 
 // Co-resident CTAs per GPU of each mode for the narrow (items <= 128 rows) or
@@ -540,10 +548,11 @@ cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [3]: x, f, x
   const int rows = wide ? kMaxItemRows : 128;
   for (int mode = 0; mode < 3; ++mode) {
     const void* fn = ll_fn(layout, mode, wide);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ll_smem_bytes(mode, kMaxItemRows, wide));
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ll_smem_bytes(mode, kMaxItemRows, kMaxTreeRows, wide));
     if (e != cudaSuccess) return e;
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, ll_smem_bytes(mode, rows, wide));
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, ll_smem_bytes(mode, rows, kTreeRowsOcc, wide));
     if (e != cudaSuccess) return e;
     blocks[mode] = b * sms;
   }

@@ -14,6 +14,7 @@
 #include <map>
 #include <string>
 #include <thread>
+#include <atomic>
 #include <vector>
 
 #include "halo_internal.h"
@@ -44,6 +45,8 @@ cudaError_t launch_ce_unpack(int layout, const CeEnt* ents, int n_local, int max
                              cudaStream_t st);
 cudaError_t launch_ce_sync(const CeSyncParams& s, cudaStream_t st);
 cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
+uint32_t ll_xblk_bytes(int rows);
+uint32_t ll_fblk_bytes(int rows);
 cudaError_t launch_assign_home(const float* x, int n, int stride, const AssignParams& A, int32_t* rank, int* counts,
                                int32_t* ids, int* err, cudaStream_t st);
 // floors (kernels_floor.cu)
@@ -155,18 +158,14 @@ struct halo_ctx {
   size_t assign_bytes = 0;
   int* err_host = nullptr;          // host-mapped error word
   int* err_dev = nullptr;
-  char* d_csr = nullptr;            // force-gather tasks + CSR of all local ranks (LL protocol)
-  size_t csr_bytes = 0;
-  std::vector<std::vector<int32_t>> h_tasks;  // per local rank: 32-B task records (row, n, contrib[6]), 8 ints each
-  std::vector<XRec> h_xrec;
-  std::vector<int32_t> h_xmap;          // per x item: its map slice (item_rows entries)
+  std::vector<LocalBase> h_lbase;       // LL: per local rank base pointers (copied to shared memory by the kernels)
+  LocalBase* d_lbase = nullptr;
   std::vector<char> h_xblk, h_fblk;     // item blocks [record | map slice] / [record | task records]
   char* h_pin = nullptr;                // pinned image of the plan (one DMA per upload)
   size_t h_pin_bytes = 0;
   char* d_xblk = nullptr;
   char* d_fblk = nullptr;
   std::vector<std::vector<std::vector<int32_t>>> h_maps;  // host copy of every local rank's maps [l][p]
-  std::vector<GRec> h_grec;
 
   // copy-engine path (HALO_F_CE_PATH): per pulse, per local rank
   struct CeCopy {
@@ -181,7 +180,6 @@ struct halo_ctx {
   float* d_stage = nullptr;                    // contiguous send rows of every (pulse, local rank) that packs
   size_t ce_bytes = 0, stage_bytes = 0;
 
-  std::vector<std::vector<int>> level_begin;  // [local][P+2]: task index where level P-1..0, home start
 
   // host plan
   std::vector<RankDev> h_ranks;
@@ -205,6 +203,7 @@ struct halo_ctx {
   uint64_t seq_x0 = 0;              // ctrl->seq_x when set_maps ended (the fused launch's xin base)
   int last_grid[2] = {0, 0};
   int item_rows = 64;
+  int tree_rows = 64;               // LL: roots per small-tree f item (chosen per NS epoch, build_ll_f)
   bool item_rows_fixed = false;     // HALO_ITEM_ROWS given: no adaptive choice
   uint32_t poll_ns = 0;
   uint32_t debug = 0;
@@ -215,7 +214,8 @@ struct halo_ctx {
   bool captured = false;
   bool auto_tr = false;             // HALO_F_AUTO_TRANSPORT: LL or copy engine chosen at every set_maps
   size_t auto_ce_bytes = (size_t)4 << 20;  // ... copy engine when some pulse sends >= this (HALO_AUTO_CE_BYTES)
-  bool direct_x = true;             // LL: same-process receivers get their x rows from the sender (HALO_DIRECT_X=0: off)
+  bool collapse = true;             // LL: the ranks of this process form one hop group (HALO_COLLAPSE=0 /
+                                    // HALO_DIRECT_X=0: every rank its own group, the staged schedule)
   int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
   // NCCL send/recv baseline (halo_nccl_*, HALO_F_NCCL_BASELINE): communicator + packed send rows
   void* nccl_comm = nullptr;
@@ -407,7 +407,8 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     ctx->item_rows_fixed = true;
   }
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = atoi(e) < 0 ? kPollTight : (uint32_t)atoi(e);
-  if (const char* e = getenv("HALO_DIRECT_X")) ctx->direct_x = atoi(e) != 0;
+  if (const char* e = getenv("HALO_DIRECT_X")) ctx->collapse = atoi(e) != 0;
+  if (const char* e = getenv("HALO_COLLAPSE")) ctx->collapse = atoi(e) != 0;
   if (const char* e = getenv("HALO_RECV_MULT")) ctx->recv_mult = std::min(16, std::max(1, atoi(e)));
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
@@ -719,135 +720,6 @@ static void build_f_items(halo_ctx* ctx) {
   }
 }
 
-// LL protocol x items: sends of independent entries (all pulses), sends of
-// dependent entries by pulse, then the receives (LL units -> x rows).
-static void build_x_items_ll(halo_ctx* ctx, int p_lo, int p_hi) {
-  auto& v = ctx->h_items_x;
-  v.clear();
-  const int R = ctx->item_rows;
-  for (int p = p_lo; p < p_hi; ++p)
-    for (int l = 0; l < ctx->n_local; ++l) add_items(v, l, p, kItemXIndep, 0, ctx->n_indep[l * ctx->P + p], R);
-  for (int p = p_lo; p < p_hi; ++p)
-    for (int l = 0; l < ctx->n_local; ++l) {
-      const int i = l * ctx->P + p;
-      add_items(v, l, p, kItemXDep, ctx->n_indep[i], ctx->send_size[i], R);
-    }
-  // receive items only for rows that arrive from another process: a sender in this
-  // process writes the receiver's x rows itself (direct_x; the launch's end makes
-  // them visible to the stream, as the receive items' copies would be)
-  for (int p = p_lo; p < p_hi; ++p)
-    for (int l = 0; l < ctx->n_local; ++l)
-      if (!(ctx->direct_x && ctx->is_local(ctx->neighbour(ctx->first_rank + l, ctx->pdim[p], +1))))
-        add_items(v, l, p, kItemXRecv, 0, ctx->recv_size[l * ctx->P + p], std::min(kMaxItemRows, ctx->recv_mult * R));
-}
-
-// Force gather plan of every local rank (LL protocol), built on the host at the
-// NS step from the final maps: task rows in level order (slice rows of pulse
-// P-1, ..., of pulse 0, then home rows that receive forces) and, per task row,
-// its contributions (q, i) with map_q[i] == row, pulses descending (R15).
-// Per local rank (independent: one host thread each when several ranks share
-// the process — the NS-step cost of an 8-rank GPU is dominated by this build).
-static bool build_csr_rank(halo_ctx* ctx, int l, std::vector<int32_t>& r) {
-  const int P = ctx->P;
-  const int nt = ctx->n_total[l], nh = ctx->n_home[l];
-  std::vector<int> cnt(nt, 0);
-  std::vector<uint8_t> mask(nt, 0);
-  const std::vector<std::vector<int32_t>>& maps = ctx->h_maps[l];
-  for (int q = 0; q < P; ++q)
-    for (int32_t t : maps[q]) {
-      cnt[t]++;
-      mask[t] |= (uint8_t)(1u << q);
-    }
-  std::vector<int32_t> task_of(nt, -1), tr;
-  tr.reserve(nt);
-  auto& lb = ctx->level_begin[l];
-  for (int k = 0; k < P; ++k) {  // level k = pulse P-1-k
-    const int p = P - 1 - k;
-    lb[k] = (int)tr.size();
-    const int a = ctx->atom_offset[l * P + p], n = ctx->recv_size[l * P + p];
-    for (int t = a; t < a + n; ++t) {
-      task_of[t] = (int)tr.size();
-      tr.push_back(t);
-    }
-  }
-  lb[P] = (int)tr.size();
-  for (int t = 0; t < nh; ++t)
-    if (cnt[t]) {
-      task_of[t] = (int)tr.size();
-      tr.push_back(t);
-    }
-  lb[P + 1] = (int)tr.size();
-  // 32-B task records: row, n, contrib[0..5] (q << 24 | i), pulses descending
-  r.assign(tr.size() * 8 + 8, 0);
-  for (size_t k = 0; k < tr.size(); ++k) {
-    r[8 * k] = tr[k];
-    r[8 * k + 1] = cnt[tr[k]];
-  }
-  for (int q = 0; q < P; ++q)
-    for (size_t i = 0; i < maps[q].size(); ++i) {
-      const int t = maps[q][i];
-      if (task_of[t] < 0) return false;
-      const int pos = __builtin_popcount((unsigned)mask[t] >> (q + 1));
-      r[8 * (size_t)task_of[t] + 2 + pos] = (int32_t)(((uint32_t)q << 24) | (uint32_t)i);
-    }
-  return true;
-}
-
-static halo_status build_csr(halo_ctx* ctx, cudaStream_t st) {
-  const int L = ctx->n_local, P = ctx->P;
-  ctx->level_begin.assign(L, std::vector<int>(P + 2, 0));
-  std::vector<std::vector<int32_t>> rec(L);
-  std::vector<char> ok(L, 1);
-  if (L == 1) {
-    ok[0] = build_csr_rank(ctx, 0, rec[0]);
-  } else {
-    std::vector<std::thread> th;
-    for (int l = 0; l < L; ++l) th.emplace_back([&, l] { ok[l] = build_csr_rank(ctx, l, rec[l]); });
-    for (auto& t : th) t.join();
-  }
-  for (int l = 0; l < L; ++l)
-    if (!ok[l]) return fail(ctx, HALO_ERR_ARG, "map entry targets a row with no gather task");
-  // kept on the host: each f item block carries its rows' records (build_grec)
-  ctx->h_tasks = std::move(rec);
-  (void)st;
-  return HALO_OK;
-}
-
-// LL protocol f items: gather tasks level by level (slice of pulse P-1 first),
-// home rows last: every wait targets a strictly earlier level.
-static void build_f_items_ll(halo_ctx* ctx) {
-  auto& v = ctx->h_items_f;
-  v.clear();
-  const int R = ctx->item_rows, P = ctx->P;
-  for (int k = 0; k <= P; ++k)
-    for (int l = 0; l < ctx->n_local; ++l) {
-      const auto& lb = ctx->level_begin[l];
-      const uint8_t level = k < P ? (uint8_t)(P - 1 - k) : kHomeLevel;
-      add_items(v, l, level, kItemGather, lb[k], lb[k + 1], R);
-    }
-  // shift-force combines last, one per (rank, dim it wrapped in): each waits for
-  // the partials its pushers wrote and owns the 3 components fshift[dim][*]
-  // (deterministic, no atomics; the dims of a rank combine in parallel CTAs)
-  for (int l = 0; l < ctx->n_local; ++l) {
-    const int rk = ctx->first_rank + l;
-    for (int d = 0; d < 3; ++d) {
-      bool wraps = false;
-      for (int q = 0; q < P; ++q)
-        wraps |= ctx->pdim[q] == d && ctx->cell(rk, d) == 0 && ctx->send_size[l * P + q] > 0;
-      if (!wraps) continue;
-      Item it;
-      it.lrank = (uint16_t)l;
-      it.pulse = (uint8_t)d;  // the combine's dim
-      it.kind = kItemFshift;
-      it.begin = it.end = 0;
-      v.push_back(it);
-    }
-  }
-  ctx->n_tail_f = 0;
-  for (const Item& it : v) ctx->n_tail_f += it.kind == kItemFshift;
-}
-
-// 128-B work records of the LL kernels, one per item (halo_internal.h XRec/GRec).
 // Host loops of the NS-step plan build over many independent items: split over a
 // few threads (the item blocks are MBs at C3/C4; the NS step is host-bound).
 template <class F>
@@ -865,107 +737,359 @@ static void parallel_for(size_t n, F&& body) {
   for (auto& x : th) x.join();
 }
 
-static void build_xrec(halo_ctx* ctx) {
-  const int W = ctx->W, P = ctx->P, R = ctx->item_rows;
-  ctx->h_xrec.assign(ctx->h_items_x.size(), XRec{});
-  ctx->h_xmap.assign(ctx->h_items_x.size() * (size_t)R, 0);
-  for (size_t k = 0; k < ctx->h_items_x.size(); ++k) {
-    const Item& w = ctx->h_items_x[k];
-    XRec& r = ctx->h_xrec[k];
-    memset(&r, 0, sizeof r);
-    const int l = w.lrank, p = w.pulse, rk = ctx->first_rank + l;
-    const PulseDev& pd = ctx->h_pulses[l * P + p];
-    r.kind = w.kind;
-    r.pulse = (uint8_t)p;
-    r.lrank = (uint16_t)l;
-    r.n_units = (w.end - w.begin) * W;
-    for (int c = 0; c < 3; ++c) r.shift[c] = pd.shift[c];
-    r.has_shift = pd.has_shift;
-    r.x = ctx->x[l];
-    r.xll_own = ctx->xll_of(rk);
-    for (int q = 0; q < kMaxP; ++q) {
-      r.recv_off[q] = q < P ? ctx->atom_offset[l * P + q] : 0;
-      r.recv_size[q] = q < P ? ctx->recv_size[l * P + q] : 0;
-    }
-    if (w.kind == kItemXRecv) {
-      r.ll = ctx->xll_of(rk) + (size_t)p * ctx->ll_stride + (size_t)w.begin * W;
-      r.xdst = ctx->x[l] + (size_t)(ctx->atom_offset[l * P + p] + w.begin) * W;
-      r.xin = &ctx->ctrl->xin[l];
-    } else {
-      r.map = pd.map + w.begin;
-      r.ll = pd.xll_dst + (size_t)w.begin * W;
-      const int lower = ctx->neighbour(rk, ctx->pdim[p], -1);
-      if (ctx->direct_x && ctx->is_local(lower)) {
-        r.xdst = pd.x_dst + (size_t)w.begin * W;
-        r.xin = &ctx->ctrl->xin[lower - ctx->first_rank];
-      }
-      const auto& m = ctx->h_maps[l][p];
-      std::copy(m.begin() + w.begin, m.begin() + w.end, ctx->h_xmap.begin() + k * (size_t)R);
-    }
+// ------------------------------------------------------------- LL plan (hop groups)
+// The DD ranks of this process share one GPU: they form one hop group (DESIGN.md
+// §6.1; HALO_COLLAPSE=0: every rank its own group).  A pulse between two ranks of
+// the group moves no data through the LL areas: the plan below resolves it.
+static bool same_group(const halo_ctx* ctx, int r1, int r2) {
+  return ctx->collapse && ctx->is_local(r1) && ctx->is_local(r2);
+}
+
+static void fill_lbase(halo_ctx* ctx) {
+  const int L = ctx->n_local, P = ctx->P;
+  ctx->h_lbase.assign(std::max(1, L), LocalBase{});
+  for (int l = 0; l < L; ++l) {
+    LocalBase& b = ctx->h_lbase[l];
+    const int r = ctx->first_rank + l;
+    b.x = ctx->x[l];
+    b.f = ctx->f[l];
+    b.xll = ctx->xll_of(r);
+    b.fll = ctx->fll_of(r);
+    for (int q = 0; q < kMaxP; ++q) b.recv_off[q] = q < P ? ctx->atom_offset[l * P + q] : 0;
   }
-  const size_t XB = 128 + 4 * (size_t)R;
-  ctx->h_xblk.assign(ctx->h_items_x.size() * XB, 0);
-  parallel_for(ctx->h_items_x.size(), [&](size_t k) {
-    memcpy(&ctx->h_xblk[k * XB], &ctx->h_xrec[k], sizeof(XRec));
-    memcpy(&ctx->h_xblk[k * XB + 128], &ctx->h_xmap[k * (size_t)R], 4 * (size_t)R);
+}
+
+// Origin of every row of every local rank, pulses < p_hi (the rows a send of
+// pulse < p_hi can read): a home row, or the LL unit in which the row entered
+// the group, plus the pulses whose shift it picked up since (R25).  cls = 0 for
+// a home origin, q+1 for an LL unit of pulse q (x dependency class).
+struct XOrig {
+  uint32_t row;
+  uint8_t l, kq, mask, cls;
+};
+static void resolve_origins(const halo_ctx* ctx, int p_hi, std::vector<std::vector<XOrig>>& org) {
+  const int L = ctx->n_local, P = ctx->P;
+  org.assign(L, {});
+  for (int l = 0; l < L; ++l) {
+    org[l].resize(ctx->n_total[l]);
+    for (int t = 0; t < ctx->n_home[l]; ++t) org[l][t] = XOrig{(uint32_t)t, (uint8_t)l, 0, 0, 0};
+  }
+  for (int q = 0; q < p_hi; ++q)
+    for (int l = 0; l < L; ++l) {
+      const int r = ctx->first_rank + l, i0 = ctx->atom_offset[l * P + q], n = ctx->recv_size[l * P + q];
+      const int s = ctx->neighbour(r, ctx->pdim[q], +1);  // the x-sender of this rank's pulse-q rows
+      if (same_group(ctx, r, s)) {
+        const int sl = s - ctx->first_rank;
+        const auto& m = ctx->h_maps[sl][q];
+        const bool wraps = ctx->cell(s, ctx->pdim[q]) == 0;
+        for (int i = 0; i < n; ++i) {
+          XOrig o = org[sl][m[i]];
+          if (wraps) o.mask |= (uint8_t)(1u << q);
+          org[l][i0 + i] = o;
+        }
+      } else {
+        for (int i = 0; i < n; ++i) org[l][i0 + i] = XOrig{(uint32_t)i, (uint8_t)l, (uint8_t)(0x80u | q), 0, (uint8_t)(q + 1)};
+      }
+    }
+}
+
+// x items of pulses [p_lo, p_hi): the sends of every local rank (entries = the
+// origins of the rows it sends, split into runs of one dependency class), sorted
+// by class (a wait targets a lower class only: deadlock-free static order), then
+// the receive items of the rows that come from another group.
+static void build_ll_x(halo_ctx* ctx, int p_lo, int p_hi) {
+  const int L = ctx->n_local, P = ctx->P, W = ctx->W, R = ctx->item_rows;
+  std::vector<std::vector<XOrig>> org;
+  resolve_origins(ctx, p_hi, org);
+  struct XI {
+    XRec rec;
+    std::vector<XEnt> ent;
+  };
+  std::vector<XI> items;
+  for (int p = p_lo; p < p_hi; ++p)
+    for (int l = 0; l < L; ++l) {
+      const int r = ctx->first_rank + l, d = ctx->pdim[p];
+      const auto& m = ctx->h_maps[l][p];
+      const int n = (int)m.size();
+      const int rcv = ctx->neighbour(r, d, -1);  // coordinates go to the lower neighbour (R1)
+      const bool wraps = ctx->cell(r, d) == 0;   // the wrapping sender adds +L_d (R25)
+      const bool local = same_group(ctx, r, rcv);
+      for (int b = 0; b < n;) {
+        const uint8_t cls = org[l][m[b]].cls;
+        int e = b;
+        while (e < n && e - b < R && org[l][m[e]].cls == cls) ++e;
+        XI it;
+        memset(&it.rec, 0, sizeof it.rec);
+        XRec& x = it.rec;
+        x.kind = kItemXSend;
+        x.pulse = (uint8_t)p;
+        x.lrank = (uint16_t)l;
+        x.n_units = (uint32_t)(e - b) * W;
+        x.begin = (uint32_t)b;
+        x.cls = cls;
+        if (local) {
+          x.dst_x = ctx->x[rcv - ctx->first_rank] + (size_t)ctx->remote_off[l * P + p] * W;
+        } else {
+          x.dst_ll = ctx->xll_of(rcv) + (size_t)p * ctx->ll_stride;
+        }
+        for (int q = 0; q < P; ++q) {
+          x.shiftL[q] = ctx->cfg.box[ctx->pdim[q]];
+          x.pdim[q] = (uint8_t)ctx->pdim[q];
+        }
+        it.ent.resize(e - b);
+        for (int k = b; k < e; ++k) {
+          const XOrig& o = org[l][m[k]];
+          it.ent[k - b] = XEnt{o.row, o.l, o.kq, (uint8_t)(o.mask | (wraps ? 1u << p : 0u)), 0};
+        }
+        items.push_back(std::move(it));
+        b = e;
+      }
+    }
+  std::stable_sort(items.begin(), items.end(), [](const XI& a, const XI& b) { return a.rec.cls < b.rec.cls; });
+  // receives: this rank's rows of a pulse whose sender is in another group
+  for (int p = p_lo; p < p_hi; ++p)
+    for (int l = 0; l < L; ++l) {
+      const int r = ctx->first_rank + l;
+      if (same_group(ctx, r, ctx->neighbour(r, ctx->pdim[p], +1))) continue;
+      const int n = ctx->recv_size[l * P + p];
+      const int RR = std::min(kMaxItemRows, ctx->recv_mult * R);
+      for (int b = 0; b < n; b += RR) {
+        const int e = std::min(n, b + RR);
+        XI it;
+        memset(&it.rec, 0, sizeof it.rec);
+        XRec& x = it.rec;
+        x.kind = kItemXRecv;
+        x.pulse = (uint8_t)p;
+        x.lrank = (uint16_t)l;
+        x.n_units = (uint32_t)(e - b) * W;
+        x.begin = (uint32_t)b;
+        x.cls = 0xff;
+        x.ll = ctx->xll_of(r) + (size_t)p * ctx->ll_stride + (size_t)b * W;
+        x.xdst = ctx->x[l] + (size_t)(ctx->atom_offset[l * P + p] + b) * W;
+        items.push_back(std::move(it));
+      }
+    }
+  const size_t XB = ll_xblk_bytes(R);
+  ctx->h_items_x.assign(items.size(), Item{});
+  ctx->h_xblk.assign(items.size() * XB, 0);
+  for (size_t k = 0; k < items.size(); ++k) {
+    Item& w = ctx->h_items_x[k];
+    w.lrank = items[k].rec.lrank;
+    w.pulse = items[k].rec.pulse;
+    w.kind = items[k].rec.kind;
+  }
+  parallel_for(items.size(), [&](size_t k) {
+    memcpy(&ctx->h_xblk[k * XB], &items[k].rec, sizeof(XRec));
+    if (!items[k].ent.empty()) memcpy(&ctx->h_xblk[k * XB + 128], items[k].ent.data(), sizeof(XEnt) * items[k].ent.size());
   });
 }
 
-static halo_status build_grec(halo_ctx* ctx) {
-  const int W = ctx->W, P = ctx->P;
-  const int R = ctx->item_rows;
-  // x items that complete each local rank's halo rows (the fused launch's xin targets)
-  std::vector<int> xin_n(ctx->n_local, 0);
-  for (const XRec& r : ctx->h_xrec)
-    if (r.xin != nullptr) xin_n[r.xin - &ctx->ctrl->xin[0]]++;
-  ctx->h_grec.assign(ctx->h_items_f.size(), GRec{});
-  for (size_t k = 0; k < ctx->h_items_f.size(); ++k) {
-    const Item& w = ctx->h_items_f[k];
-    GRec& g = ctx->h_grec[k];
-    memset(&g, 0, sizeof g);
-    const int l = w.lrank, rk = ctx->first_rank + l;
-    g.kind = w.kind;
-    g.level = w.pulse;
-    g.lrank = (uint16_t)l;
-    g.n_units = (w.end - w.begin) * W;
-    g.wrap_mask = 0;
-    for (int q = 0; q < P; ++q) {
-      g.pulse_dim[q] = (uint8_t)ctx->pdim[q];
-      if (ctx->cell(rk, ctx->pdim[q]) == 0) g.wrap_mask |= 1u << q;
-    }
-    g.f = ctx->f[l];
-    g.fll_own = ctx->fll_of(rk);
-    g.xin = &ctx->ctrl->xin[l];
-    g.xin_n = (uint32_t)xin_n[l];
-    if (w.kind == kItemGather) {
-      g.tasks = nullptr;
-      if (w.pulse != kHomeLevel) {
-        const int p = w.pulse;
-        const PulseDev& pd = ctx->h_pulses[l * P + p];
-        g.push = pd.fll_dst - (ptrdiff_t)ctx->atom_offset[l * P + p] * W;
-        // the x-sender of pulse p (upper neighbour) shifted these rows iff its cell is 0:
-        // this item also sums what it pushes into that rank's shift-force slot
-        const int upper = ctx->neighbour(rk, ctx->pdim[p], +1);
-        if (ctx->cell(upper, ctx->pdim[p]) == 0) {
-          const int slot = (int)(w.begin - ctx->level_begin[l][P - 1 - p]) / R;
-          g.part = ctx->fsp_of(upper) + ((size_t)p * ctx->fsp_slots + slot) * 6;
-        }
-      }
-    } else {  // kItemFshift: combine of the slots the pushers wrote into this rank, pulses of dim g.level
-      g.part = ctx->fsp_of(rk);
-      for (int q = 0; q < P; ++q)
-        g.nslot[q] = ((g.wrap_mask >> q & 1u) && ctx->pdim[q] == (int)w.pulse)
-                         ? (uint32_t)((ctx->send_size[l * P + q] + R - 1) / R) : 0u;
+// Node list of the tree under row t of local rank l, depth first, children in
+// descending pulse order (the oracle's accumulation order, R15).  `fs` of the
+// edge into a node: 3 * (parent's local rank) + dim when the parent's rank
+// wrapped in the edge's pulse (R13), else 0xff.
+static void emit_tree(const halo_ctx* ctx, const std::vector<std::vector<int32_t>>& child, int l, int t, int depth,
+                      int parent, uint8_t fs, std::vector<TNode>& v, int& lowest_ll) {
+  const int P = ctx->P, r = ctx->first_rank + l;
+  const size_t me = v.size();
+  v.push_back(TNode{(uint32_t)t | ((uint32_t)l << 24), 0, (uint8_t)(parent < 0 ? 0xff : parent),
+                    (uint8_t)(depth << 1), fs});
+  for (int q = P - 1; q >= 0; --q) {
+    const int i = child[l][(size_t)t * P + q];
+    if (i < 0) continue;
+    v[me].flags |= 1;  // has children: its folded value is stored
+    const int d = ctx->pdim[q];
+    const uint8_t efs = ctx->cell(r, d) == 0 ? (uint8_t)(3 * l + d) : (uint8_t)0xff;
+    const int rcv = ctx->neighbour(r, d, -1);
+    if (same_group(ctx, r, rcv)) {
+      emit_tree(ctx, child, rcv - ctx->first_rank, ctx->remote_off[l * P + q] + i, depth + 1, (int)me, efs, v,
+                lowest_ll);
+    } else {
+      v.push_back(TNode{(uint32_t)i | ((uint32_t)l << 24), (uint8_t)(0x80u | q), (uint8_t)me,
+                        (uint8_t)((depth + 1) << 1), efs});
+      lowest_ll = std::min(lowest_ll, q);
     }
   }
-  const size_t FB = 128 + 32 * (size_t)R;
-  ctx->h_fblk.assign(ctx->h_items_f.size() * FB, 0);
-  parallel_for(ctx->h_items_f.size(), [&](size_t k) {
-    const Item& w = ctx->h_items_f[k];
-    memcpy(&ctx->h_fblk[k * FB], &ctx->h_grec[k], sizeof(GRec));
-    if (w.kind == kItemGather)
-      memcpy(&ctx->h_fblk[k * FB + 128], &ctx->h_tasks[w.lrank][8 * (size_t)w.begin], 32 * (size_t)(w.end - w.begin));
+}
+
+// f items: the trees of this group.  A row's children are its images (one per
+// pulse whose map sends it); children in this group are nodes of the same tree,
+// children in another group are LL nodes (the value they push back).  Roots: home
+// rows with children, and halo rows whose x-sender is in another group (they push
+// their value back there).  Dependency class of a tree = P - (lowest pulse of its
+// LL nodes), 0 without: a pushed value comes from a tree whose LL nodes all have
+// higher pulses, i.e. a lower class.  Then one combine per (rank, wrapped dim).
+static halo_status build_ll_f(halo_ctx* ctx) {
+  const int L = ctx->n_local, P = ctx->P, W = ctx->W;
+  // child[l][t*P + q] = i: row t of rank l is entry i of map_q (one per pulse at most)
+  std::vector<std::vector<int32_t>> child(L);
+  parallel_for((size_t)L, [&](size_t l) {
+    child[l].assign((size_t)ctx->n_total[l] * P, -1);
+    for (int q = 0; q < P; ++q) {
+      const auto& m = ctx->h_maps[l][q];
+      for (size_t i = 0; i < m.size(); ++i) child[l][(size_t)m[i] * P + q] = (int32_t)i;
+    }
   });
+  struct Tree {
+    int l, t;
+    uint8_t cls;
+    bool small;
+    uint64_t* push;
+  };
+  std::vector<Tree> roots;
+  for (int l = 0; l < L; ++l) {
+    const int r = ctx->first_rank + l;
+    for (int t = 0; t < ctx->n_home[l]; ++t) {
+      bool any = false;
+      for (int q = 0; q < P && !any; ++q) any = child[l][(size_t)t * P + q] >= 0;
+      if (any) roots.push_back(Tree{l, t, 0, true, nullptr});
+    }
+    for (int q = 0; q < P; ++q) {
+      const int s = ctx->neighbour(r, ctx->pdim[q], +1);
+      if (same_group(ctx, r, s)) continue;
+      const int i0 = ctx->atom_offset[l * P + q];
+      uint64_t* base = ctx->fll_of(s) + (size_t)q * ctx->ll_stride;
+      for (int i = 0; i < ctx->recv_size[l * P + q]; ++i)
+        roots.push_back(Tree{l, i0 + i, 0, true, base + (size_t)i * W});
+    }
+  }
+  // depth-first node lists (children pulses descending, R15) and their shift-force targets
+  std::vector<std::vector<TNode>> tn(roots.size());
+  std::vector<std::vector<uint8_t>> tfs(roots.size());
+  parallel_for(roots.size(), [&](size_t k) {
+    int lowest_ll = P;
+    emit_tree(ctx, child, roots[k].l, roots[k].t, 0, -1, 0xff, tn[k], lowest_ll);
+    roots[k].cls = (uint8_t)(P - lowest_ll);
+    roots[k].small = tn[k].size() <= (size_t)kFastNodes;
+    for (const TNode& v : tn[k])
+      if (v.fs != 0xff && std::find(tfs[k].begin(), tfs[k].end(), v.fs) == tfs[k].end()) tfs[k].push_back(v.fs);
+  });
+  // items: roots ordered by class, rank, small/large, in row order
+  std::vector<size_t> order(roots.size());
+  for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+    const Tree &x = roots[a], &y = roots[b];
+    if (x.cls != y.cls) return x.cls < y.cls;
+    if (x.l != y.l) return x.l < y.l;
+    return x.small > y.small;
+  });
+  struct FI {
+    size_t b, e;  // range of `order`
+    bool small;
+    int nodes;
+    std::vector<uint8_t> fs;  // bucket targets
+  };
+  auto form = [&](int RT, std::vector<FI>& fis) {
+    fis.clear();
+    const int RG = std::max(1, RT / 8);                      // large trees per item
+    const int NG = (int)((ll_fblk_bytes(RT) - 128 - 16 * RG) / 8);  // their node capacity
+    for (size_t k = 0; k < order.size();) {
+      const Tree& t0 = roots[order[k]];
+      FI f{k, k, t0.small, 0, {}};
+      while (f.e < order.size()) {
+        const size_t o = order[f.e];
+        const Tree& t = roots[o];
+        if (t.cls != t0.cls || t.l != t0.l || t.small != t0.small) break;
+        if ((int)(f.e - f.b) >= (f.small ? RT : RG)) break;
+        if (!f.small && f.nodes + (int)tn[o].size() > NG && f.e > f.b) break;
+        if ((int)tfs[o].size() <= kMaxBuckets) {  // (a larger tree adds its edges directly)
+          std::vector<uint8_t> u = f.fs;
+          for (uint8_t x : tfs[o])
+            if (std::find(u.begin(), u.end(), x) == u.end()) u.push_back(x);
+          if ((int)u.size() > kMaxBuckets && f.e > f.b) break;
+          f.fs = std::move(u);
+        }
+        f.nodes += (int)tn[o].size();
+        ++f.e;
+      }
+      fis.push_back(std::move(f));
+      k = fis.back().e;
+    }
+  };
+  // roots per item: the smallest size whose items all fit the co-resident grid
+  // (one item per CTA, one pass of 3 components per root), else kTreeRowsOcc
+  std::vector<FI> fis;
+  int RT = 32;
+  for (;; RT = std::min(kTreeRowsOcc, RT + 16)) {
+    form(RT, fis);
+    if ((int)fis.size() <= ctx->cap_f() || RT == kTreeRowsOcc) break;
+  }
+  if (const char* e = getenv("HALO_TREE_ROWS")) {
+    RT = std::min(kTreeRowsOcc, std::max(8, atoi(e)));
+    form(RT, fis);
+  }
+  const int RG = std::max(1, RT / 8);
+  for (const FI& f : fis)
+    if (!f.small && (int)(128 + 16 * RG + 8 * f.nodes) > (int)ll_fblk_bytes(RT))
+      return fail(ctx, HALO_ERR_UNSUPPORTED, "a force tree exceeds the node capacity of a work item");
+  ctx->tree_rows = RT;
+  const size_t FB = ll_fblk_bytes(RT);
+  const size_t nt = fis.size();
+  ctx->h_items_f.assign(nt, Item{});
+  ctx->h_fblk.assign(nt * FB, 0);
+  parallel_for(nt, [&](size_t k) {
+    const FI& f = fis[k];
+    char* blk = &ctx->h_fblk[k * FB];
+    GRec g;
+    memset(&g, 0, sizeof g);
+    g.kind = f.small ? kItemTree : kItemTreeG;
+    g.level = roots[order[f.b]].cls;
+    g.lrank = (uint16_t)roots[order[f.b]].l;
+    g.n_roots = (uint32_t)(f.e - f.b);
+    g.n_units = g.n_roots * W;
+    g.n_nodes = (uint32_t)f.nodes;
+    g.n_buckets = (uint8_t)f.fs.size();
+    for (size_t b = 0; b < f.fs.size(); ++b) g.bucket_fs[b] = f.fs[b];
+    memcpy(blk, &g, sizeof g);
+    auto bucket_of = [&](const TNode& x, bool direct) -> uint8_t {
+      if (x.fs == 0xff) return kFsNone;
+      return direct ? kFsDirect : (uint8_t)(std::find(f.fs.begin(), f.fs.end(), x.fs) - f.fs.begin());
+    };
+    if (f.small) {
+      TRoot* rr = reinterpret_cast<TRoot*>(blk + 128);
+      uint32_t* il = reinterpret_cast<uint32_t*>(blk + 128 + 32 * (size_t)RT);
+      for (size_t j = f.b; j < f.e; ++j) {
+        const std::vector<TNode>& v = tn[order[j]];
+        TRoot R;
+        memset(&R, 0, sizeof R);
+        R.push = roots[order[j]].push;
+        R.par = 0xffffffffu;
+        R.bucket = 0xffffffffu;
+        R.nn = (uint8_t)v.size();
+        for (size_t m = 0; m < v.size(); ++m) {
+          const TNode& x = v[m];
+          const uint32_t sh = 4 * (uint32_t)m;
+          R.par = (R.par & ~(15u << sh)) | ((uint32_t)(x.parent == 0xff ? 15 : x.parent) << sh);
+          R.bucket = (R.bucket & ~(15u << sh)) | ((uint32_t)bucket_of(x, false) << sh);
+          R.q |= (uint32_t)(x.kq & 7) << sh;
+          if (x.kq & 0x80u) R.llmask |= (uint8_t)(1u << m);
+          if (x.flags & 1u) R.stmask |= (uint8_t)(1u << m);
+          il[8 * (j - f.b) + m] = x.il;
+        }
+        rr[j - f.b] = R;
+      }
+    } else {
+      TRootG* rr = reinterpret_cast<TRootG*>(blk + 128);
+      TNode* nn = reinterpret_cast<TNode*>(blk + 128 + 16 * (size_t)RG);
+      uint32_t at = 0;
+      for (size_t j = f.b; j < f.e; ++j) {
+        const std::vector<TNode>& v = tn[order[j]];
+        rr[j - f.b] = TRootG{roots[order[j]].push, at, (uint16_t)v.size(), 0};
+        const bool direct = tfs[order[j]].size() > (size_t)kMaxBuckets;
+        for (size_t m = 0; m < v.size(); ++m) {
+          TNode x = v[m];
+          x.kq = (uint8_t)((x.kq & 0x87u) | (bucket_of(x, direct) << 3));
+          nn[at + m] = x;
+        }
+        at += (uint32_t)v.size();
+      }
+    }
+    Item& w = ctx->h_items_f[k];
+    w.lrank = g.lrank;
+    w.pulse = g.level;
+    w.kind = g.kind;
+  });
+  ctx->n_tail_f = 0;
   return HALO_OK;
 }
 
@@ -977,8 +1101,8 @@ static halo_status upload_plan(halo_ctx* ctx) {
   const size_t nf = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_f.size()), a);
   const size_t nxr = align_up(std::max<size_t>(1, ctx->h_xblk.size()), a);
   const size_t ngr = align_up(std::max<size_t>(1, ctx->h_fblk.size()), a);
-  const size_t nxm = 0;
-  const size_t need = nr + np + nx + nf + nxr + ngr + nxm;
+  const size_t nlb = align_up(sizeof(LocalBase) * std::max<size_t>(1, ctx->h_lbase.size()), a);
+  const size_t need = nr + np + nx + nf + nxr + ngr + nlb;
   if (need > ctx->plan_bytes) {  // 25% headroom: NS steps rarely grow the plan again
     if (ctx->plan) CK(cudaFree(ctx->plan));
     ctx->plan = nullptr;
@@ -997,6 +1121,7 @@ static halo_status upload_plan(halo_ctx* ctx) {
   ctx->d_items_f = reinterpret_cast<Item*>(ctx->plan + nr + np + nx);
   ctx->d_xblk = ctx->plan + nr + np + nx + nf;
   ctx->d_fblk = ctx->plan + nr + np + nx + nf + nxr;
+  ctx->d_lbase = reinterpret_cast<LocalBase*>(ctx->plan + nr + np + nx + nf + nxr + ngr);
   // the whole plan image in pinned memory, then one synchronous DMA (pageable
   // copies of the MB-sized item blocks cost ms at the NS step)
   char* img = ctx->h_pin;
@@ -1010,7 +1135,8 @@ static halo_status upload_plan(halo_ctx* ctx) {
   put(reinterpret_cast<char*>(ctx->d_items_f), ctx->h_items_f.data(), sizeof(Item) * ctx->h_items_f.size());
   put(ctx->d_xblk, ctx->h_xblk.data(), ctx->h_xblk.size());
   put(ctx->d_fblk, ctx->h_fblk.data(), ctx->h_fblk.size());
-  const size_t used = (size_t)(ctx->d_fblk - ctx->plan) + ctx->h_fblk.size();
+  put(reinterpret_cast<char*>(ctx->d_lbase), ctx->h_lbase.data(), sizeof(LocalBase) * ctx->h_lbase.size());
+  const size_t used = (size_t)(reinterpret_cast<char*>(ctx->d_lbase) - ctx->plan) + sizeof(LocalBase) * ctx->h_lbase.size();
   CK(cudaMemcpy(ctx->plan, img, used, cudaMemcpyHostToDevice));
   ctx->n_items_x = (int)ctx->h_items_x.size();
   ctx->n_items_f = (int)ctx->h_items_f.size();
@@ -1054,9 +1180,11 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.xblk = ctx->d_xblk;
   P.fblk = ctx->d_fblk;
   P.item_rows = ctx->item_rows;
+  P.tree_rows = ctx->tree_rows;
   P.ring = ll_ring(ctx->wide());
   P.delay_rank = ctx->P ? ctx->neighbour(0, ctx->pdim[0], +1) : -1;
   P.seq_x0 = ctx->seq_x0;
+  P.lbase = ctx->d_lbase;
   return P;
 }
 
@@ -1398,8 +1526,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
       for (int q = 0; q <= p; ++q) fill_pulse_dev(ctx, l, q);
     fill_rank_dev(ctx);
     if (ctx->ll) {
-      build_x_items_ll(ctx, p, p + 1);
-      build_xrec(ctx);
+      fill_lbase(ctx);
+      build_ll_x(ctx, p, p + 1);
     } else {
       build_x_items(ctx, p, p + 1);
     }
@@ -1482,16 +1610,12 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   for (int l = 0; l < L; ++l)
     for (int p = 0; p < P; ++p) fill_pulse_dev(ctx, l, p);
   if (ctx->ll) {
-    if ((s = build_csr(ctx, st)) != HALO_OK) return s;
-    prof.lap("csr");
-    build_x_items_ll(ctx, 0, P);
-    build_f_items_ll(ctx);
-    build_xrec(ctx);
-    if ((s = build_grec(ctx)) != HALO_OK) return s;
-    prof.lap("records");
+    fill_lbase(ctx);
+    build_ll_x(ctx, 0, P);
+    prof.lap("x plan");
+    if ((s = build_ll_f(ctx)) != HALO_OK) return s;
+    prof.lap("f plan");
   } else {
-    ctx->h_xrec.clear();
-    ctx->h_grec.clear();
     ctx->h_xblk.clear();
     ctx->h_fblk.clear();
     build_x_items(ctx, 0, P);
@@ -1525,7 +1649,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   CK(cudaMemcpyAsync(&seqs[1], &ctx->ctrl->seq_f, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   // the fused launch's per-rank halo counters count from here (the per-pulse x
   // launches above counted too)
-  CK(cudaMemsetAsync(ctx->ctrl->xin, 0, sizeof(ctx->ctrl->xin), st));
+  CK(cudaMemsetAsync(ctx->ctrl->xcnt, 0, sizeof(ctx->ctrl->xcnt), st));
   CK(cudaStreamSynchronize(st));
   ctx->seq_host_x = seqs[0];
   ctx->seq_host_f = seqs[1];
@@ -2359,7 +2483,6 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_planes) (void)cudaFree(ctx->d_planes);
   if (ctx->d_rtt) (void)cudaFree(ctx->d_rtt);
   if (ctx->d_assign) (void)cudaFree(ctx->d_assign);
-  if (ctx->d_csr) (void)cudaFree(ctx->d_csr);
   if (ctx->d_ce) (void)cudaFree(ctx->d_ce);
   if (ctx->d_stage) (void)cudaFree(ctx->d_stage);
   if (ctx->d_nccl_send) (void)cudaFree(ctx->d_nccl_send);

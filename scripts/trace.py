@@ -108,9 +108,19 @@ def main():
             res.update({"gap_x_exit_to_f_start": round(float((tf[:, 0].min() - tx[:, 3].max()) / 1e3), 2),
                         "f_start": q((tf[:, 0] - t0) / 1e3), "f_rec": q((tf[:, 1] - t0) / 1e3),
                         "f_done": q((tf[:, 2] - t0) / 1e3), "f_exit": q((tf[:, 3] - t0) / 1e3)})
+        if os.environ.get("HALO_DEBUG") == "8192":  # kTraceDetail: stamps inside the first tree item
+            tr = tf
+            m = (tr[:, 10] > 0) & (tr[:, 13] >= tr[:, 10])
+            if m.any():
+                d = tr[m]
+                res["detail_rec_to_loads"] = q((d[:, 10] - d[:, 1]) / 1e3)
+                res["detail_loads_to_fold"] = q((d[:, 11] - d[:, 10]) / 1e3)
+                res["detail_fold_to_preflush"] = q((d[:, 12] - d[:, 11]) / 1e3)
+                res["detail_flush"] = q((d[:, 13] - d[:, 12]) / 1e3)
+                res["detail_flush_to_itemend"] = q((d[:, 5] - d[:, 13]) / 1e3)
         # per (kind, level) item end quantiles [min, median, p90, max, count], µs relative
         # to the first CTA start of the (x or fused) launch
-        kinds = {0: "xindep", 1: "xdep", 4: "xrecv", 5: "gather", 6: "fshift"}
+        kinds = {4: "xrecv", 6: "fshift", 7: "xsend", 8: "tree"}
         for nm, tr in ((("xf", tx),) if args.fused else (("x", tx), ("f", tf))):
             groups = {}
             for row in tr:

@@ -16,14 +16,30 @@ PAPER = 1 << 4  # HALO_F_PAPER_FLAGS: the paper's per-pulse flag protocol; 0 = L
 CE = 1 << 5  # HALO_F_CE_PATH: copy-engine path
 TMA_STORE, TMA_GET = 1 << 7, 1 << 8  # the paper's TMA put of x (Alg. 3) / receiver-driven TMA get of f (Alg. 6)
 TMA = PAPER | TMA_STORE | TMA_GET
-PROTOS = [pytest.param(0, id="ll"), pytest.param(PAPER, id="paper"), pytest.param(TMA, id="paper_tma"),
-          pytest.param(CE, id="ce")]
+# LL with HALO_COLLAPSE=0: every DD rank its own hop group (the staged per-pulse schedule
+# with LL transport, receive items and force pushes on every pulse: the code paths a
+# pulse between two GPUs takes); "ll" = the default, one hop group per process
+STAGED = 1 << 30  # test-side marker, stripped before halo_init
+PROTOS = [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged"), pytest.param(PAPER, id="paper"),
+          pytest.param(TMA, id="paper_tma"), pytest.param(CE, id="ce")]
 
 
 def session_for(case, flags=0, layout=None, capacity=None):
+    import os
     from paper_2509_21527_b200.session import HaloSession
-    return HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout or case.layout,
-                       capacity=capacity or case.capacity, device=0, flags=flags, timeout_s=5.0)
+    staged = bool(flags & STAGED)
+    old = os.environ.get("HALO_COLLAPSE")
+    if staged:
+        os.environ["HALO_COLLAPSE"] = "0"  # read at halo_init
+    try:
+        return HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout or case.layout,
+                           capacity=capacity or case.capacity, device=0, flags=flags & ~STAGED, timeout_s=5.0)
+    finally:
+        if staged:
+            if old is None:
+                os.environ.pop("HALO_COLLAPSE")
+            else:
+                os.environ["HALO_COLLAPSE"] = old
 
 
 @pytest.mark.parametrize("proto", PROTOS)
@@ -336,8 +352,10 @@ def test_mutation_is_caught(mut, monkeypatch):
     """Dependency safety (G3): with a protocol mutation (16: forward x rows without
     waiting for their arrival; 32: add force contributions without checking their
     sequence tag) the poisoned/bit-exact parity check must fail on a 3D grid with
-    forwarding.  Proves the parity tests can see a protocol race."""
+    forwarding.  Proves the parity tests can see a protocol race.  HALO_COLLAPSE=0:
+    every rank its own hop group, so every pulse waits (one group has no waits)."""
     monkeypatch.setenv("HALO_DEBUG", str(mut))
+    monkeypatch.setenv("HALO_COLLAPSE", "0")
     case = Case("C3", seed=1, force_kind="int")
     sess = session_for(case, capacity=case.capacity)
     failed = False

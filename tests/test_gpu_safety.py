@@ -89,7 +89,9 @@ def test_g3_relaxed_flags(name, monkeypatch):
 @pytest.mark.parametrize("mut", [KX_NOWAIT, KF_NOWAIT])
 def test_g3_ll_mutations_50(mut, monkeypatch):
     """(i) on the LL protocol: forward x rows without waiting for their tag /
-    add force contributions without checking theirs; caught in >= 1 of 50 runs."""
+    add force contributions without checking theirs; caught in >= 1 of 50 runs.
+    HALO_COLLAPSE=0: every rank its own hop group, every pulse waits."""
+    monkeypatch.setenv("HALO_COLLAPSE", "0")
     case = Case("C3", seed=1, force_kind="int")
     caught = count_catches(case, 0, mut, monkeypatch)
     log_g3({"mutation": f"i LL debug {mut}", "case": "C3", "runs": N_RUNS, "caught": caught})
