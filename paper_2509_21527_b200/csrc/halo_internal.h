@@ -307,7 +307,8 @@ struct TRoot {
   uint8_t llmask;           // bit k: node k is an LL node
   uint8_t stmask;           // bit k: node k (F, with children) stores its folded value
   uint8_t pad0;
-  uint32_t pad1[2];
+  uint32_t post;            // nibble e: the e-th non-root node in postorder (nn - 1 of them)
+  uint32_t pad1;
 };
 static_assert(sizeof(TRoot) == 32, "TRoot");
 // Larger trees — kItemTreeG blocks: [GRec | TRootG x rows/8 | TNode x (rest)].

@@ -288,75 +288,96 @@ __device__ __forceinline__ void fs_flush(const GRec& g, double (*s_v)[kThreads],
   }
 }
 
+// The LL nodes of a small tree: every unit requested, then each one checked for
+// this launch's tag (spinning until the remote push lands) into shared memory.
+template <int W>
+__device__ __noinline__ void tree_ll_nodes(const TRoot R, const uint32_t* il, const LocalBase* lb,
+                                           const ExParams& P, uint32_t tag, int lrank, float (*s_val)[kThreads]) {
+  const int c = (int)(threadIdx.x % W);
+  const uint64_t* a[kFastNodes];
+  uint64_t w[kFastNodes];
+#pragma unroll
+  for (int k = 0; k < kFastNodes; ++k)
+    if (k < R.nn && (R.llmask >> k & 1u)) {
+      a[k] = lb[il[k] >> 24].fll + (size_t)(R.q >> (4 * k) & 15u) * P.ll_stride + (size_t)(il[k] & (kMaxRows - 1)) * W + c;
+      w[k] = ld_relaxed_sys(a[k]);
+    }
+  for (int k = 0; k < kFastNodes; ++k)
+    if (k < R.nn && (R.llmask >> k & 1u)) {
+      uint64_t x = 0;
+#pragma unroll
+      for (int m = 0; m < kFastNodes; ++m)
+        if (m == k) x = w[m];
+      if ((uint32_t)(x >> 32) != tag && !(P.debug & kMutateFNoWait)) {
+        const uint64_t* ak = lb[il[k] >> 24].fll + (size_t)(R.q >> (4 * k) & 15u) * P.ll_stride +
+                             (size_t)(il[k] & (kMaxRows - 1)) * W + c;
+        x = ll_spin(ak, tag, P.timeout_ns, P.err_host, tcode(12, lrank, R.q >> (4 * k) & 15u), P.poll_ns);
+      }
+      s_val[k][threadIdx.x] = __uint_as_float((uint32_t)x);
+    }
+}
+
 // One small-tree item: each (root, component) is folded by one thread.  All node
-// values are loaded first (every load in flight: F rows straight into v[], LL
-// units into w[]), then the fold runs in reverse preorder on the root record's
-// 4-bit shape fields: a node's children follow it in preorder, so they are final
-// when it is reached, and their in-order sum is its fold (f[node] + children,
-// pulses descending, one fp32 RNE add per child: the oracle's order, R15).
+// values are loaded first (every load in flight) into the thread's column of
+// shared memory, then one add per edge in POSTORDER (the root record's 4-bit
+// fields): a node's children finish before it, in preorder = descending pulse
+// order, so its parent receives f[parent] + children in the oracle's order (R15:
+// one fp32 RNE add per child, the bits match).  A node's value is final when it
+// is reached: stored (F nodes with children), added to its shift-force bucket,
+// then added into its parent.  A root whose parent is in another group pushes
+// its value there.  ~10 instructions per edge, none for absent nodes.
 template <int W>
 __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, const uint4* nodes, const LocalBase* lb,
-                                          const ExParams& P, uint32_t tag, double (*s_v)[kThreads], uint64_t* tdet) {
+                                          const ExParams& P, uint32_t tag, double (*s_v)[kThreads],
+                                          float (*s_val)[kThreads], uint64_t* tdet) {
   const uint32_t n = g.n_units;
   const uint32_t S = (blockDim.x / W) * W;  // stride: a multiple of W, every thread keeps one component
   const int c = (int)(threadIdx.x % W);
+  const int tid = threadIdx.x;
   const bool fs_on = P.fshift != nullptr && g.n_buckets > 0;
   if (fs_on)
-    for (int b = 0; b < g.n_buckets; ++b) s_v[b][threadIdx.x] = 0.0;
-  for (uint32_t u = threadIdx.x; u < n && threadIdx.x < S; u += S) {
+    for (int b = 0; b < g.n_buckets; ++b) s_v[b][tid] = 0.0;
+  for (uint32_t u = tid; u < n && (uint32_t)tid < S; u += S) {
     const uint32_t j = u / W;
     const TRoot R = roots[j];
-    const uint4 n0 = nodes[2 * j], n1 = nodes[2 * j + 1];
-    const uint32_t il[kFastNodes] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+    const uint32_t* il = reinterpret_cast<const uint32_t*>(nodes + 2 * j);
     const int nn = R.nn;
-    float v[kFastNodes];
-    uint64_t w[kFastNodes];
-    auto ll_addr = [&](int k) -> const uint64_t* {
-      return lb[il[k] >> 24].fll + (size_t)(R.q >> (4 * k) & 15u) * P.ll_stride +
-             (size_t)(il[k] & (kMaxRows - 1)) * W + c;
-    };
+    if (tdet && u == 0) tdet[0] = gtimer() + (il[0] == 0xffffffffu ? 1 : 0);  // records read
+    // F node values straight into this thread's shared-memory column (LDGSTS: every
+    // load in flight, no registers held); LL nodes out of line (they wait for a
+    // remote push anyway)
 #pragma unroll
-    for (int k = 0; k < kFastNodes; ++k) {
-      if (k < nn) {
-        if (R.llmask >> k & 1u) w[k] = ld_relaxed_sys(ll_addr(k));
-        else v[k] = __ldcg(lb[il[k] >> 24].f + (size_t)(il[k] & (kMaxRows - 1)) * W + c);
+    for (int k = 0; k < kFastNodes; ++k)
+      if (k < nn && !(R.llmask >> k & 1u))
+        cp_async4(&s_val[k][tid], lb[il[k] >> 24].f + (size_t)(il[k] & (kMaxRows - 1)) * W + c);
+    cp_async_commit();
+    if (R.llmask) tree_ll_nodes<W>(R, il, lb, P, tag, g.lrank, s_val);
+    cp_async_wait_all();
+    if (tdet && u == 0) tdet[1] = gtimer() + (__float_as_uint(s_val[0][tid]) == 0x7fc00001u ? 1 : 0);  // loads landed
+    const uint32_t* ilr = il;
+    for (int e = 0; e < nn - 1; ++e) {
+      const int m = R.post >> (4 * e) & 15u;
+      const int pm = R.par >> (4 * m) & 15u;
+      const float vm = s_val[m][tid];
+      if (R.stmask >> m & 1u) lb[ilr[m] >> 24].f[(size_t)(ilr[m] & (kMaxRows - 1)) * W + c] = vm;
+      if (fs_on && c < 3) {
+        const int b = R.bucket >> (4 * m) & 15u;
+        if (b != kFsNone) fs_bucket_add(s_v, b, vm, P);
       }
+      s_val[pm][tid] = P.accumulate ? __fadd_rn(s_val[pm][tid], vm) : vm;
     }
-    if (tdet && u == 0) tdet[0] = gtimer() + (__float_as_uint(v[0]) == 0x7fc00001u ? 1 : 0);  // loads landed
-    if (R.llmask) {
-#pragma unroll
-      for (int k = 1; k < kFastNodes; ++k)
-        if (k < nn && (R.llmask >> k & 1u)) {
-          if ((uint32_t)(w[k] >> 32) != tag && !(P.debug & kMutateFNoWait))
-            w[k] = ll_spin(ll_addr(k), tag, P.timeout_ns, P.err_host, tcode(12, g.lrank, R.q >> (4 * k) & 15u),
-                           P.poll_ns);
-          v[k] = __uint_as_float((uint32_t)w[k]);
-        }
-    }
-#pragma unroll
-    for (int k = kFastNodes - 1; k >= 0; --k) {
-      if (k < nn) {
-#pragma unroll
-        for (int m = k + 1; m < kFastNodes; ++m)
-          if ((R.par >> (4 * m) & 15u) == (uint32_t)k) v[k] = P.accumulate ? __fadd_rn(v[k], v[m]) : v[m];
-        if (R.stmask >> k & 1u) lb[il[k] >> 24].f[(size_t)(il[k] & (kMaxRows - 1)) * W + c] = v[k];
-        if (k > 0 && fs_on && c < 3) {
-          const int b = R.bucket >> (4 * k) & 15u;
-          if (b != kFsNone) fs_bucket_add(s_v, b, v[k], P);
-        }
-      }
-    }
-    if (R.push != nullptr) st_relaxed_sys(R.push + c, ll_pack(v[0], tag));
-    if (tdet && u == 0) tdet[1] = gtimer();  // folded and stored
+    const float root = s_val[0][tid];
+    if (R.stmask & 1u) lb[il[0] >> 24].f[(size_t)(il[0] & (kMaxRows - 1)) * W + c] = root;
+    if (R.push != nullptr) st_relaxed_sys(R.push + c, ll_pack(root, tag));
+    if (tdet && u == 0) tdet[2] = gtimer();  // folded and stored
   }
-  if (tdet) tdet[2] = gtimer();  // (thread 0) before the shift-force flush
   if (fs_on) fs_flush<W>(g, s_v, S, P);
   if (tdet) tdet[3] = gtimer();
 }
 
 // One large-tree item (kItemTreeG): the generic fold, one (root, component) per thread.
 template <int W>
-__device__ __forceinline__ void tree_item_generic(const GRec& g, const TRootG* roots, const TNode* nodes,
+__device__ __noinline__ void tree_item_generic(const GRec& g, const TRootG* roots, const TNode* nodes,
                                                   const LocalBase* lb, const ExParams& P, uint32_t tag,
                                                   double (*s_v)[kThreads]) {
   const uint32_t n = g.n_units;
@@ -398,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
   __shared__ __align__(8) uint64_t s_bar[kRing];
   __shared__ __align__(16) LocalBase s_lb[kMaxLocal];
   __shared__ double s_v[kMode == kModeX ? 1 : kMaxBuckets][kThreads];  // shift-force buckets of an f item
+  __shared__ float s_val[kMode == kModeX ? 1 : kFastNodes][kThreads];   // tree node values, one column per thread
   const uint32_t R = (uint32_t)P.item_rows, RT = (uint32_t)P.tree_rows;
   const uint32_t XB = xblk_bytes(R), FB = fblk_bytes(RT);
   const uint32_t SB = kMode == kModeX ? XB : FB;  // ring slot size
@@ -466,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
       }
       if (g.kind == kItemTree)
         tree_item<W>(g, reinterpret_cast<const TRoot*>(blk + 128), reinterpret_cast<const uint4*>(blk + 128 + 32 * RT),
-                     s_lb, P, tag_f, s_v,
+                     s_lb, P, tag_f, s_v, s_val,
                      (trace && (P.debug & kTraceDetail) && tdet_free) ? &ctrl->trace[tslot][blockIdx.x][10] : nullptr);
       else
         tree_item_generic<W>(g, reinterpret_cast<const TRootG*>(blk + 128),

@@ -196,8 +196,14 @@ struct halo_ctx {
   int max_x = 0, max_f = 0, max_xf = 0;        // co-resident CTAs of the exchange kernels (LL: narrow variants)
   int max_x_w = 0, max_f_w = 0, max_xf_w = 0;  // LL: batched variants for large work items
   int grid_cap = 0;                 // HALO_CTAS_PER_SM x SMs (0 = occupancy limit only)
+  int x_cap = 0;                    // HALO_X_CTAS_PER_SM x SMs: the x kernel only (leaves SM room for
+                                    // the f kernel's CTAs to become resident early under PDL)
   bool wide() const { return ll && item_rows >= 256; }
-  int cap_x() const { const int c = wide() ? max_x_w : max_x; return grid_cap ? std::min(c, grid_cap) : c; }
+  int cap_x() const {
+    int c = wide() ? max_x_w : max_x;
+    if (grid_cap) c = std::min(c, grid_cap);
+    return x_cap ? std::min(c, x_cap) : c;
+  }
   int cap_f() const { const int c = wide() ? max_f_w : max_f; return grid_cap ? std::min(c, grid_cap) : c; }
   int cap_xf() const { const int c = wide() ? max_xf_w : max_xf; return grid_cap ? std::min(c, grid_cap) : c; }
   uint64_t seq_x0 = 0;              // ctrl->seq_x when set_maps ended (the fused launch's xin base)
@@ -443,6 +449,9 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
     if (const char* v = getenv("HALO_CTAS_PER_SM"))
       if (atoi(v) > 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess)
         ctx->grid_cap = atoi(v) * sms;
+    if (const char* v = getenv("HALO_X_CTAS_PER_SM"))
+      if (atoi(v) > 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess)
+        ctx->x_cap = atoi(v) * sms;
   }
   if (e != cudaSuccess) {
     // keep ctx to carry the message? The ABI returns NULL on error; print once.
@@ -1056,6 +1065,25 @@ static halo_status build_ll_f(halo_ctx* ctx) {
         R.par = 0xffffffffu;
         R.bucket = 0xffffffffu;
         R.nn = (uint8_t)v.size();
+        // postorder of the non-root nodes: a node after all its descendants, siblings
+        // in preorder (= descending pulse) order
+        {
+          std::vector<int> post;
+          std::vector<std::vector<int>> kids(v.size());
+          for (size_t m = 1; m < v.size(); ++m) kids[v[m].parent].push_back((int)m);
+          std::vector<std::pair<int, size_t>> st{{0, 0}};
+          while (!st.empty()) {
+            auto& [node, next] = st.back();
+            if (next < kids[node].size()) {
+              const int ch = kids[node][next++];
+              st.push_back({ch, 0});
+            } else {
+              if (node != 0) post.push_back(node);
+              st.pop_back();
+            }
+          }
+          for (size_t e = 0; e < post.size(); ++e) R.post |= (uint32_t)post[e] << (4 * e);
+        }
         for (size_t m = 0; m < v.size(); ++m) {
           const TNode& x = v[m];
           const uint32_t sh = 4 * (uint32_t)m;

@@ -113,10 +113,10 @@ def main():
             m = (tr[:, 10] > 0) & (tr[:, 13] >= tr[:, 10])
             if m.any():
                 d = tr[m]
-                res["detail_rec_to_loads"] = q((d[:, 10] - d[:, 1]) / 1e3)
-                res["detail_loads_to_fold"] = q((d[:, 11] - d[:, 10]) / 1e3)
-                res["detail_fold_to_preflush"] = q((d[:, 12] - d[:, 11]) / 1e3)
-                res["detail_flush"] = q((d[:, 13] - d[:, 12]) / 1e3)
+                res["detail_rec_to_records"] = q((d[:, 10] - d[:, 1]) / 1e3)
+                res["detail_records_to_loads"] = q((d[:, 11] - d[:, 10]) / 1e3)
+                res["detail_loads_to_fold"] = q((d[:, 12] - d[:, 11]) / 1e3)
+                res["detail_fold_to_flushed"] = q((d[:, 13] - d[:, 12]) / 1e3)
                 res["detail_flush_to_itemend"] = q((d[:, 5] - d[:, 13]) / 1e3)
         # per (kind, level) item end quantiles [min, median, p90, max, count], µs relative
         # to the first CTA start of the (x or fused) launch
