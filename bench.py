@@ -60,6 +60,17 @@ def max_over_ranks(v: float) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(v: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(v)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def barrier():
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
@@ -140,6 +151,55 @@ class ClockSampler:
         med = statistics.median(self.samples) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
+
+
+class NvlCounters:
+    """This GPU's NVLink data counters (NVML field values NVLINK_THROUGHPUT_DATA_TX/RX: user
+    payload bytes, KiB units, summed over every link with scopeId = UINT_MAX; per link if the
+    aggregate is not supported).  Read on both sides of the timed region: the hardware's own
+    count of the bytes the exchanges moved over NVLink, beside the algorithmic figure."""
+
+    def __init__(self, device):
+        self.ok, self.err = False, None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(device)
+            self.links = [0xFFFFFFFF]
+            if self._read_raw(self.links) is None:
+                self.links = list(range(18))
+                if self._read_raw(self.links) is None:
+                    raise RuntimeError("NVLink throughput field values not supported")
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML / no NVLink here
+            self.err = str(e)[:200]
+
+    def _read_raw(self, links):
+        nv = self.nv
+        ids = []
+        for l in links:
+            ids += [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l), (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l)]
+        vals = nv.nvmlDeviceGetFieldValues(self.h, ids)
+        tx = rx = 0
+        seen = False
+        for i, v in enumerate(vals):
+            if v.nvmlReturn != 0:
+                continue
+            seen = True
+            x = int(v.value.ullVal)
+            if i % 2 == 0:
+                tx += x
+            else:
+                rx += x
+        return (tx * 1024, rx * 1024) if seen else None
+
+    def read(self):
+        if not self.ok:
+            return None
+        try:
+            return self._read_raw(self.links)
+        except Exception:  # pragma: no cover
+            return None
 
 
 # ------------------------------------------------------------------ cpu legs
@@ -326,12 +386,15 @@ def run_fused(args, rank, world, local):
 
     sampler = ClockSampler([local])
     sampler.start()
+    nvc = NvlCounters(local) if world > 1 else None
     K = args.steps
     # main timed loop: events only at the step boundaries, so exchange_f is
     # launched right behind exchange_x (programmatic dependent launch)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
     torch.cuda.synchronize()
     barrier()
+    nv0 = nvc.read() if nvc else None
+    t_wall0 = time.perf_counter()
     for k in range(K):
         flush.fill_(float(k))
         reset_f()
@@ -340,8 +403,23 @@ def run_fused(args, rank, world, local):
         sess.exchange_f(fshift=fshift)
         ev[k][1].record(stream)
     torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    nv1 = nvc.read() if nvc else None
     barrier()
     tot = [ev[k][0].elapsed_time(ev[k][1]) * 1e3 for k in range(K)]
+    nvl_counted = None
+    if nvc is not None:  # every rank takes part in the reductions (collectives)
+        have = nv0 is not None and nv1 is not None
+        per = [(nv1[i] - nv0[i]) / K for i in range(2)] if have else [-1.0, -1.0]
+        tx_max, rx_max = max_over_ranks(per[0]), max_over_ranks(per[1])
+        tx_min = -max_over_ranks(-per[0])
+        if tx_min >= 0:
+            nvl_counted = {"tx_bytes_per_step": round(tx_max, 1), "rx_bytes_per_step": round(rx_max, 1),
+                           "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX (user payload, KiB counters) read around the "
+                                     "K timed steps, max over ranks; the flush and reset in that loop are local",
+                           "wall_s": round(t_wall, 4)}
+        else:
+            nvl_counted = {"unavailable": (nvc.err or "NVML NVLink field read failed") + " (on some rank)"}
     # the same steps as ONE fused launch each (halo_exchange_xf, LL protocol)
     fused = None
     if transport == "ll" and not args.no_fused:
@@ -424,33 +502,11 @@ def run_fused(args, rank, world, local):
         barrier()
         del g
 
-    # e2e through the C-ABI host-buffer call (pinned host memory; H2D + D2H inside)
-    xh = [torch.from_numpy(np.ascontiguousarray(
-        np.pad(X[homes[first + l]], ((0, 0), (0, W - 3))).astype(np.float32))).pin_memory() for l in range(nl)]
-    fa = [F0[l].cpu().pin_memory() for l in range(nl)]
-    xo = [torch.empty(max(lay[l]["n_total"] - lay[l]["n_home"], 1), W).pin_memory() for l in range(nl)]
-    fo = [torch.empty(max(lay[l]["n_home"], 1), W).pin_memory() for l in range(nl)]
-    fsh = torch.zeros(nl, 3, 3, dtype=torch.float64).pin_memory()
-    h2d = sum(4 * W * (lay[l]["n_home"] + lay[l]["n_total"]) for l in range(nl))
-    d2h = sum(4 * W * lay[l]["n_total"] for l in range(nl)) + 72 * nl
-
-    def host_step():
-        sess.halo.step_host([t.data_ptr() for t in xh], [t.data_ptr() for t in fa], [t.data_ptr() for t in xo],
-                            [t.data_ptr() for t in fo], fsh.data_ptr(), stream=stream.cuda_stream)
-
-    for _ in range(args.warmup):
-        host_step()
-    barrier()
-    Ke = K
-    eev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(Ke)]
-    for k in range(Ke):
-        flush.fill_(1.0)
-        eev[k][0].record(stream)
-        host_step()
-        eev[k][1].record(stream)
-    torch.cuda.synchronize()
-    e2e_us = max_over_ranks(float(np.mean([eev[k][0].elapsed_time(eev[k][1]) * 1e3 for k in range(Ke)])))
-    barrier()
+    # e2e through the C-ABI host-buffer call (halo_step_host_packed: one pinned host block
+    # in, one out; the H2D of the inputs and the D2H of the results inside the timed span)
+    e2e_us = h2d = d2h = None
+    if not args.no_e2e:
+        e2e_us, h2d, d2h = e2e_timing(sess, X, homes, F0, first, nl, W, flush, stream, K, args.warmup)
 
     # NCCL send/recv baseline on the same maps (one DD rank per GPU only)
     nccl = None
@@ -549,13 +605,15 @@ def run_fused(args, rank, world, local):
             "path": "halo_exchange_xf: x and f of the step in ONE launch; rank l's gather items start when "
                     "l's halo rows are complete (the non-bonded kernel's slot, Alg. 2)"},
         "clocks": sampler.summary(),
-        "e2e": {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
-                "d2h_bytes_per_step": int(d2h) * world, "path": "halo_step_host (C ABI, pinned host buffers)"},
+        "e2e": None if e2e_us is None else {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "path": "halo_step_host_packed (C ABI): one pinned host block in (x home rows + forces), one out "
+                        "(halo x rows + home forces + fshift) per process; 2 uploads + 2 downloads on 3 streams"},
         "gpu_launches": (2 if transport != "ce" else 4 * P) * K * world,
         "roofline": roof,
         "nvlink": {"bytes_per_step_per_gpu_per_direction": int(nvl_bytes),
                    "achieved_gbs": round(nvl_bytes / (res["step"] * 1e-6) / 1e9, 3) if nvl_bytes else 0.0,
-                   "peak_gbs": 900.0},
+                   "peak_gbs": 900.0, "counters": nvl_counted},
         "latency_floor": floor or None,
         "nccl_baseline": nccl,
         "device_spans": dev_spans,
@@ -606,6 +664,39 @@ def run_fused(args, rank, world, local):
         out["cpu_baseline"] = cpu_baseline_leg(args, P, c)
     sess.destroy()
     return out
+
+
+def e2e_timing(sess, X, homes, F0, first, nl, W, flush, stream, K, warmup):
+    """e2e through the C-ABI host-buffer call halo_step_host_packed: one pinned host block
+    in (x home rows + this step's forces), one out (halo x rows + home forces + fshift) per
+    process; the H2D of the inputs and the D2H of the results inside the timed span.
+    Returns (us/step max over ranks, H2D bytes, D2H bytes summed over processes)."""
+    import torch
+    in_b, out_b = sess.halo.packed_sizes()
+    blk = np.concatenate(
+        [np.pad(X[homes[first + l]], ((0, 0), (0, W - 3))).astype(np.float32).reshape(-1) for l in range(nl)] +
+        [F0[l].cpu().numpy().reshape(-1) for l in range(nl)]).astype(np.float32)
+    assert blk.nbytes == in_b, (blk.nbytes, in_b)
+    hin = torch.from_numpy(blk).pin_memory()
+    hout = torch.empty(out_b, dtype=torch.uint8).pin_memory()
+
+    def host_step():
+        sess.halo.step_host_packed(hin.data_ptr(), hout.data_ptr(), stream=stream.cuda_stream)
+
+    for _ in range(warmup):
+        host_step()
+    barrier()
+    eev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    for k in range(K):
+        flush.fill_(1.0)
+        eev[k][0].record(stream)
+        host_step()
+        eev[k][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_us = max_over_ranks(float(np.mean([eev[k][0].elapsed_time(eev[k][1]) * 1e3 for k in range(K)])))
+    h2d, d2h = sum_over_ranks(in_b), sum_over_ranks(out_b)  # every process's blocks
+    barrier()
+    return e2e_us, h2d, d2h
 
 
 def pme_timing(sess, K, warmup, flush):
@@ -823,6 +914,7 @@ def main():
     ap.add_argument("--zones", default="slab", choices=("slab", "rounded"),
                     help="import zones: slab (box-shaped, default) or GROMACS-style rounded (HALO_F_ROUNDED_ZONES)")
     ap.add_argument("--pme", action="store_true", help="also time the PP<->PME redistribution (halo_pme_*)")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e timing")
     ap.add_argument("--no-ns", action="store_true", help="skip the NS-step (halo_migrate + halo_set_maps) timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

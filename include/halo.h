@@ -363,6 +363,25 @@ HALO_API halo_status halo_step_host(halo_ctx* ctx, const float* const* x_home, c
                            float* const* x_halo_out, float* const* f_home_out, double* fshift_host,
                            void* stream);
 
+/* Host block sizes of halo_step_host_packed for the current maps (bytes).
+ * HALO_ERR_STATE before set_maps. */
+HALO_API halo_status halo_packed_sizes(const halo_ctx* ctx, size_t* in_bytes, size_t* out_bytes);
+
+/* COLLECTIVE end-to-end step through ONE host block in and ONE out (the e2e
+ * measurement path; same computation as halo_step_host, bit-identical).
+ *   in  (in_bytes, pinned host, caller-owned, read): the x home rows of local
+ *       ranks 0..L-1 concatenated (n_home*layout floats each), then the f rows
+ *       [0, n_total) of local ranks 0..L-1 (the step's non-bonded forces);
+ *   out (out_bytes, pinned host, caller-owned, written; NULL = no outputs): the
+ *       halo x rows [n_home, n_total) of every local rank, then the home f rows
+ *       of every local rank, then at the next 8-B aligned offset the shift
+ *       forces, n_local*9 doubles ([local][dim][component], zeroed each step).
+ * Two uploads (x home, then the forces on a library-owned side stream while x
+ * is exchanged), two downloads (halo x on a side stream while f is exchanged,
+ * then the forces); packing to and from the per-rank rows is done by a copy
+ * kernel.  Enqueued on `stream`; synchronises it.  Not graph-capturable. */
+HALO_API halo_status halo_step_host_packed(halo_ctx* ctx, const void* in, void* out, void* stream);
+
 /* Baseline building blocks (the NCCL send/recv schedule of P:178-181 / Fig. 1
  * drives these from the host; not on the fused path):
  * pack pulse p of local rank into sendbuf (send_size*layout floats, shift applied);

@@ -34,7 +34,7 @@ EXPORTS = [
     "halo_ipc_export", "halo_ipc_import", "halo_set_maps", "halo_set_maps_explicit", "halo_get_layout",
     "halo_get_map", "halo_assign_home", "halo_migrate", "halo_transport", "halo_pme_reserve", "halo_pme_setup",
     "halo_pme_buffers", "halo_pme_send_x", "halo_pme_recv_f", "halo_exchange_x", "halo_exchange_f", "halo_exchange_xf", "halo_nccl_unique_id", "halo_nccl_init", "halo_nccl_version", "halo_nccl_exchange_x",
-    "halo_nccl_exchange_f", "halo_step_host", "halo_pack_x_pulse",
+    "halo_nccl_exchange_f", "halo_step_host", "halo_packed_sizes", "halo_step_host_packed", "halo_pack_x_pulse",
     "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_launch_remote", "halo_floor_bandwidth", "halo_probe_reserve", "halo_floor_payload", "halo_floor_bandwidth_multi", "halo_sync", "halo_strerror",
     "halo_last_error", "halo_destroy",
 ]
@@ -90,6 +90,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_nccl_exchange_x": ([P, P], c_int),
         "halo_nccl_exchange_f": ([P, P, c_int, P], c_int),
         "halo_step_host": ([P, POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), P, P], c_int),
+        "halo_packed_sizes": ([P, POINTER(c_size_t), POINTER(c_size_t)], c_int),
+        "halo_step_host_packed": ([P, P, P, P], c_int),
         "halo_pack_x_pulse": ([P, c_int, c_int, P, P], c_int),
         "halo_unpack_f_pulse": ([P, c_int, c_int, P, P, c_int, P], c_int),
         "halo_get_timers": ([P, POINTER(c_uint64), POINTER(c_uint64)], c_int),

@@ -26,6 +26,7 @@ constexpr int kMaxP = HALO_MAX_PULSES;
 constexpr int kMaxLocal = HALO_MAX_LOCAL;
 constexpr int kMaxRanks = HALO_MAX_RANKS;
 constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
+constexpr int kThreadsXNarrow = 128;   // ... of the LL x kernel with latency-regime items (<= 128 rows)
 constexpr int kHdrBytes = 8192;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
 constexpr int kTraceW = 16;            // ... words per CTA: 4 stamps + (tag, end) of its first 6 items
@@ -35,6 +36,15 @@ constexpr int kMaxTreeRows = 170;      // largest small-tree item (2 passes of 8
 constexpr int kTreeRowsOcc = 85;       // tree item size the occupancy (co-resident grid) is computed for
 constexpr int kRing = 4;
 constexpr int kXCounters = 32;               // LL kernels: item blocks in flight per CTA (narrow variants)
+// LL sequence numbers: the tag of a launch is the low 32 bits of its sequence number;
+// values whose tag would be 0 are skipped (a never-written unit is zero), and every
+// set_maps zeroes the LL areas, so a unit carries this launch's tag only if this
+// launch wrote it (within an NS epoch of < 2^32 launches).
+__host__ __device__ __forceinline__ uint64_t ll_seq_next(uint64_t s) {
+  ++s;
+  return (uint32_t)s == 0 ? s + 1 : s;
+}
+constexpr int kErrKindStalePlan = 31;        // error-word kind: a replayed graph met a plan of another NS epoch
 constexpr uint32_t kPollTight = 0xffffffffu;  // ExParams.poll_ns: tight polling only, no backoff (HALO_POLL_NS=-1)
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
@@ -61,6 +71,8 @@ struct __align__(128) ScratchHdr {
   uint64_t pme_ack[kMaxRanks];     // seq: rank t has read its slice of pme_f
   uint64_t pme_f_flag;             // seq: pme_f holds this step's PME forces (written by the PME rank)
   uint64_t pad5[15];
+  uint64_t ns_x[8];        // set_maps: (epoch << 32) | 1: the x-sender's NS-step rows of pulse p landed
+  uint64_t pad6[8];
 };
 static_assert(sizeof(ScratchHdr) <= kHdrBytes, "ScratchHdr too large");
 
@@ -250,7 +262,8 @@ struct LocalBase {          // per local rank, copied to shared memory at kernel
   uint64_t* xll;            // own coordinate LL area (slot q at + q*ll_stride)
   uint64_t* fll;            // own force LL area
   int32_t recv_off[kMaxP];  // own receive ranges (rows)
-  int32_t pad[2];
+  int32_t n_home;           // home rows (the x launch's L2 prefetch)
+  int32_t pad;
 };
 static_assert(sizeof(LocalBase) == 64, "LocalBase");
 
@@ -280,7 +293,8 @@ struct __align__(128) XRec {
   uint8_t pad0[2];
   uint64_t* ll;             // recv: own LL slot p + begin*W
   float* xdst;              // recv: own x + (recv_off_p + begin)*W
-  uint64_t pad2;
+  uint32_t epoch;           // NS epoch of the plan (a graph captured before a later set_maps is refused)
+  uint32_t pad2;
   uint8_t pad1[128 - 88];
 };
 static_assert(sizeof(XRec) == 128, "XRec must be one 128-B line");
@@ -342,7 +356,9 @@ struct __align__(128) GRec {
   uint32_t n_roots, n_nodes;
   uint8_t n_buckets;        // shift-force buckets of this item's edges
   uint8_t bucket_fs[kMaxBuckets];  // their targets (3 * local rank + dim)
-  uint8_t pad[128 - 16 - 1 - kMaxBuckets];
+  uint8_t pad0[3];
+  uint32_t epoch;           // NS epoch of the plan (as XRec.epoch)
+  uint8_t pad[128 - 16 - 1 - kMaxBuckets - 3 - 4];
 };
 static_assert(sizeof(GRec) == 128, "GRec must be one 128-B line");
 
@@ -377,6 +393,64 @@ struct ExParams {
   uint64_t seq_x0;          // fused launch: ctrl->seq_x at the end of set_maps (xcnt counts from there)
   int delay_rank;           // HALO_DEBUG kDelayPulse0: the DD rank whose pulse-0 sends are slowed
   const LocalBase* lbase;   // LL: [n_local] (copied to shared memory by every CTA)
+  // x launch: L2 prefetch (before griddepcontrol.wait) of the f kernel's item blocks and
+  // of the home x rows the sends read, spread over the CTAs (0 bytes = off, HALO_PREFETCH=0)
+  const char* pf_f;
+  uint64_t pf_f_bytes;
+  int pf_x;                 // 1: prefetch every local rank's home x rows
+  uint32_t plan_epoch;      // LL: the NS epoch whose item blocks this launch expects (records carry theirs)
+};
+
+// GPU plan build of the LL protocol (set_maps, P <= 3: every force tree has <= 8
+// nodes): the x send items and the force trees are built by kernels_plan.cu from the
+// device-resident maps; the host only fills this descriptor (per (local rank, pulse)
+// relations, pointers, and after the counting pass the item offsets).
+struct PlanLQ {
+  float* dst_x;             // send of (l, q) to a rank of this group: its x + remote_off rows
+  uint64_t* dst_ll;         // ... to another group: the receiver's coordinate LL slot q
+  uint64_t* push;           // rows of (l, q) whose x-sender is in another group: its force LL slot q
+  int32_t rcv_l;            // the receiver's (lower neighbour) local index if in this group, else -1
+  int32_t snd_l;            // the sender's (upper neighbour) local index if in this group, else -1
+  int32_t remote_off;       // where the receiver put this rank's pulse-q rows
+  int32_t atom_offset;      // own receive range of pulse q
+  int32_t send_size, recv_size;
+  uint8_t wraps;            // this rank adds +L_{d_q} in pulse q (R1, R25)
+  uint8_t efs;              // 3 * l + d_q if wraps, else 0xff (shift-force target of its edges, R13)
+  uint8_t pad[6];
+};
+struct PlanDev {
+  int L, P, W, R, RT, cap, map_stride;
+  uint32_t epoch;
+  uint32_t XB, FB;          // item block sizes
+  PlanLQ lq[kMaxLocal][kMaxP];
+  int32_t n_home[kMaxLocal], n_total[kMaxLocal];
+  const int32_t* maps[kMaxLocal];
+  uint8_t bucket_fs[kMaxLocal][kMaxBuckets];  // shift-force targets of every tree rooted at rank l
+  uint8_t n_buckets[kMaxLocal];
+  float shiftL[kMaxP];
+  uint8_t pdim[kMaxP];
+  uint8_t pad0[2];
+  // device scratch ([L][cap] rows)
+  uint64_t* org;            // x origin of every row: row | l << 24 | kq << 32 | mask << 40 | cls << 48
+  int32_t* child;           // [L][cap][P]: entry of row t in map q, or -1
+  uint8_t* rcls;            // tree class of a root row, 0xff = not a root
+  int32_t* rrank;           // rank of a root row among the roots of its (class, local rank)
+  int32_t* xcnt;            // [P][L][P + 1] send items per class (counting pass)
+  int32_t* rcnt;            // [L][P + 1] roots per class
+  // second pass (after the counts): item offsets and the block areas
+  int32_t xoff[kMaxP + 1][kMaxP][kMaxLocal];  // first x item of (class, pulse, local rank)
+  int32_t foff[kMaxP + 1][kMaxLocal];         // first f item of (class, local rank)
+  int32_t fcnt[kMaxP + 1][kMaxLocal];         // roots of (class, local rank)
+  char* xblk;
+  char* fblk;
+};
+
+// halo_step_host_packed: one contiguous copy between a packed staging buffer and
+// one local rank's rows (4-B words).
+struct SegCopy {
+  const uint32_t* src;
+  uint32_t* dst;
+  size_t words;
 };
 
 // Copy-engine path (HALO_F_CE_PATH, kernels_ce.cu): one entry per (pulse, local rank).
@@ -411,14 +485,48 @@ struct SelParams {
   int dim;
   double rc;
   const int32_t* cand;      // [n_local][2] candidate row range
-  const double* b_lo;       // [n_local] lower plane b_d[c_d] of the pulse's dim
+  const double* b_lo;       // [n_local][3] lower planes b_d[c_d] (the pulse's dim is used)
   const double* home_lo;    // [n_local][3] (home check; nullptr = skip)
   const double* home_hi;    // [n_local][3]
   const double* b_up;       // [n_local][3] upper planes b_d[c_d+1]: rounded zones (R31); nullptr = slab
+  int kfirst;               // 1: the dim's first pulse (candidates [0, n_total)); 0: the rows received
+                            // in pulse p-1 (cand == nullptr: both from the device-side handshake results)
+  uint32_t epoch;
+  uint32_t wait_mask[kMaxLocal];   // pulses q < p whose x-sender is in another process: wait ns_x[q]
+  int* err_host;
+  uint64_t timeout_ns;
   double rc2;               // float64(rc)^2 (R31)
   int decomposed_mask;      // bit d set iff grid[d] > 1
   int map_stride;
   int layout;
+};
+
+// set_maps: the coordinate exchange of one pulse (k_ns_x), driven by the device-side
+// sizes and offsets of the handshake (no host round trip per pulse).
+struct NsXParams {
+  const RankDev* ranks;
+  Ctrl* ctrl;
+  int p;
+  int dim;
+  int map_stride;
+  int n_local;
+  uint32_t epoch;
+  float* dst_x[kMaxLocal];         // the receiver's x (peer pointer; rows at remote_off)
+  uint64_t* flag_dst[kMaxLocal];   // the receiver's ns_x[p] when it is in another process, else null
+  float shift[kMaxLocal];          // +L_d when the sender wraps (R1, R25), applied iff has_shift
+  int has_shift[kMaxLocal];
+  uint32_t wait_mask[kMaxLocal];   // pulses q < p whose x-sender is in another process (forwarded rows)
+  int* err_host;
+  uint64_t timeout_ns;
+};
+
+struct NsWaitParams {
+  int n_local;
+  uint32_t epoch;
+  ScratchHdr* own[kMaxLocal];
+  uint32_t mask[kMaxLocal];        // pulses whose x-sender is in another process
+  int* err_host;
+  uint64_t timeout_ns;
 };
 
 struct HsParams {

@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <algorithm>
 #include "halo_internal.h"
 #include "ptx.cuh"
 
@@ -397,7 +399,12 @@ __global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelPara
   __shared__ int s_cnt[32];
   __shared__ int s_total;
   __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    // rows that came from another process in earlier pulses: wait for their arrival
+    for (uint32_t m = S.wait_mask[lr]; m; m &= m - 1)
+      (void)wait_epoch(&rd.hdr->ns_x[__ffs(m) - 1], S.epoch, S.timeout_ns, S.err_host, tcode(9, lr, __ffs(m) - 1));
+  }
   __syncthreads();
   if (S.home_lo != nullptr) {
     for (int i = threadIdx.x; i < rd.n_home; i += blockDim.x) {
@@ -410,9 +417,19 @@ __global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelPara
       if (bad) s_bad = 1;
     }
   }
-  const int c0 = S.cand[2 * lr], c1 = S.cand[2 * lr + 1];
+  int c0, c1;
+  if (S.cand != nullptr) {
+    c0 = S.cand[2 * lr];
+    c1 = S.cand[2 * lr + 1];
+  } else if (S.kfirst) {  // every row present before the dim's first pulse
+    c0 = 0;
+    c1 = S.ctrl->n_total[lr];
+  } else {  // the rows received in the previous pulse of the dim
+    c0 = S.ctrl->atom_offset[lr][S.p - 1];
+    c1 = c0 + S.ctrl->recv_size[lr][S.p - 1];
+  }
   int32_t* out = rd.maps + (size_t)S.p * S.map_stride;
-  const double blo = S.b_lo[lr];
+  const double blo = S.b_lo[3 * lr + S.dim];
   int base = 0;
   for (int t0 = c0; t0 < c1; t0 += blockDim.x) {
     const int i = t0 + threadIdx.x;
@@ -531,6 +548,72 @@ __global__ void __launch_bounds__(256) k_depmask(const RankDev* ranks, Ctrl* ctr
   }
 }
 
+// set_maps, pulse p: x[map_p] (+shift) -> the receiver's x at remote_off (R12),
+// sizes and offsets from the handshake results in device memory.  blockIdx.y =
+// local rank, rows grid-strided.  Same-process receivers are covered by stream
+// order; k_ns_flag then releases the others' ns_x[p].
+template <int W>
+__global__ void __launch_bounds__(256) k_ns_x(const __grid_constant__ NsXParams X) {
+  const int lr = blockIdx.y;
+  const RankDev& rd = X.ranks[lr];
+  if (X.wait_mask[lr]) {  // forwarded rows that came from another process: arrived
+    if (threadIdx.x == 0)
+      for (uint32_t m = X.wait_mask[lr]; m; m &= m - 1)
+        (void)wait_epoch(&rd.hdr->ns_x[__ffs(m) - 1], X.epoch, X.timeout_ns, X.err_host, tcode(9, lr, __ffs(m) - 1));
+    __syncthreads();
+  }
+  const int n = X.ctrl->send_size[lr][X.p];
+  const int ro = X.ctrl->remote_off[lr][X.p];
+  const int32_t* map = rd.maps + (size_t)X.p * X.map_stride;
+  float* dst = X.dst_x[lr] + (size_t)ro * W;
+  const bool sh = X.has_shift[lr] != 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float* src = rd.x + (size_t)map[i] * W;
+    float v[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) v[c] = src[c];
+    if (sh) {  // the full 3-vector (R25); float4 w is never shifted
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[c] = __fadd_rn(v[c], c == X.dim ? X.shift[lr] : 0.0f);
+    }
+#pragma unroll
+    for (int c = 0; c < W; ++c) dst[(size_t)i * W + c] = v[c];
+  }
+}
+
+__global__ void k_ns_flag(const __grid_constant__ NsXParams X) {
+  const int lr = threadIdx.x;
+  if (lr >= X.n_local || X.flag_dst[lr] == nullptr) return;
+  fence_sys();  // k_ns_x's peer stores (stream order) before the flag
+  st_release_sys(X.flag_dst[lr], ((uint64_t)X.epoch << 32) | 1u);
+}
+
+// set_maps end: every local rank acquires the ns_x flags of its pulses from other processes.
+__global__ void k_ns_wait(const __grid_constant__ NsWaitParams W) {
+  const int lr = threadIdx.x;
+  if (lr >= W.n_local) return;
+  for (uint32_t m = W.mask[lr]; m; m &= m - 1)
+    (void)wait_epoch(&W.own[lr]->ns_x[__ffs(m) - 1], W.epoch, W.timeout_ns, W.err_host, tcode(9, lr, __ffs(m) - 1));
+}
+
+cudaError_t launch_ns_wait(const NsWaitParams& W, cudaStream_t st) {
+  void* args[] = {(void*)&W};
+  return cudaLaunchKernel((const void*)k_ns_wait, dim3(1), dim3(kMaxLocal), args, 0, st);
+}
+
+cudaError_t launch_ns_x(const NsXParams& X, int layout, int max_rows, cudaStream_t st) {
+  if (X.n_local <= 0) return cudaSuccess;
+  const int gx = std::max(1, std::min((max_rows + 255) / 256, std::max(1, 148 * 8 / X.n_local)));
+  void* args[] = {(void*)&X};
+  cudaError_t e = cudaLaunchKernel(layout == 4 ? (const void*)k_ns_x<4> : (const void*)k_ns_x<3>,
+                                   dim3(gx, X.n_local), dim3(256), args, 0, st);
+  if (e != cudaSuccess) return e;
+  bool remote = false;
+  for (int l = 0; l < X.n_local; ++l) remote |= X.flag_dst[l] != nullptr;
+  if (!remote) return cudaSuccess;
+  return cudaLaunchKernel((const void*)k_ns_flag, dim3(1), dim3(kMaxLocal), args, 0, st);
+}
+
 // One CTA per local rank, one thread per destination rank: error agreement.
 __global__ void k_status(const __grid_constant__ StatusParams S) {
   const int lr = blockIdx.x;
@@ -644,6 +727,30 @@ cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, c
   return cudaGetLastError();
 }
 
+// Packed host-buffer step (halo_step_host_packed): copies between the packed
+// staging buffers and the per-rank x / f rows, one segment per blockIdx.y,
+// 4-B words (rows are 12 B: 4-B aligned only), 4 loads in flight per thread.
+__global__ void __launch_bounds__(256) k_seg_copy(const SegCopy* __restrict__ segs) {
+  const SegCopy S = segs[blockIdx.y];
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < S.words; i += 4 * stride) {
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k * stride < S.words) v[k] = __ldcg(S.src + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k * stride < S.words) S.dst[i + k * stride] = v[k];
+  }
+}
+
+cudaError_t launch_seg_copy(const SegCopy* segs, int nseg, size_t max_words, cudaStream_t st) {
+  if (nseg <= 0 || max_words == 0) return cudaSuccess;
+  const unsigned gx = (unsigned)std::min<size_t>(64, (max_words + 1023) / 1024);
+  k_seg_copy<<<dim3(gx, (unsigned)nseg), 256, 0, st>>>(segs);
+  return cudaGetLastError();
+}
+
 // Empty kernel with the exchange kernels' PDL prologue (launch floor).
 // remote != nullptr: threads [0, nwords) of the grid also store one 8-B word
 // each there (a peer's scratch): the launch floor of a kernel that wrote to
@@ -661,11 +768,15 @@ __global__ void k_empty(uint64_t* remote, uint32_t nwords) {
 // kernel.  Without it, co-residency holds because the grid never exceeds the
 // occupancy-computed capacity and PDL dependents are only scheduled once every
 // CTA of the primary grid is resident.
+// Cooperative launch (hardware-checked co-residency): HALO_COOP=1, and by default
+// under MPS (an active-thread percentage can leave fewer SMs to this context than the
+// occupancy calculation assumes).
 static int coop_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HALO_COOP");
-    v = (e && e[0] == '1') ? 1 : 0;
+    if (e) v = e[0] == '1' ? 1 : 0;
+    else v = (getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE") || getenv("CUDA_MPS_PIPE_DIRECTORY")) ? 1 : 0;
   }
   return v;
 }

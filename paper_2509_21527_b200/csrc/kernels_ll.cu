@@ -36,8 +36,14 @@
 // griddepcontrol.wait (static plan data, overlapped with the previous kernel's
 // drain), and the block of item j+ring is requested as soon as item j is done.
 // Items are ordered by dependency class (a wait only targets an item of a lower
-// class on another GPU); the grid never exceeds the co-resident
-// CTA count.
+// class on another GPU).  Progress needs every CTA of the grid to
+// be resident at once: the grid never exceeds the occupancy-computed capacity of
+// the device, which holds when this context may use every SM (launches are not
+// cooperative by default: a cooperative launch disables programmatic dependent
+// launch).  Where that is not guaranteed — MPS with an active-thread percentage,
+// green contexts, a persistent kernel holding SMs — the launch is cooperative
+// (HALO_COOP=1; the default under MPS), and the driver refuses a grid that cannot
+// be co-resident instead of letting it spin until the timeout.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -86,6 +92,12 @@ __device__ __forceinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uin
   }
 }
 
+// An item of another NS epoch's plan (a stale graph replay): report once, do nothing.
+__device__ __noinline__ uint32_t stale_item(const ExParams& P) {
+  if (threadIdx.x == 0) report_timeout(P.err_host, tcode(kErrKindStalePlan, 0, 0));
+  return 0;
+}
+
 __device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64_t timeout_ns, int* err_host,
                                          int code, uint32_t sleep_ns) {
   uint64_t v = ld_relaxed_sys(u);
@@ -102,7 +114,9 @@ __device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64
 template <int W, int kU>
 __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const LocalBase* lb, const ExParams& P,
                                        uint32_t tag) {
-  const uint32_t n = r.n_units;
+  // a CUDA graph captured before the last NS step replays with this epoch: every item of
+  // a replaced (or zeroed) plan carries another one and is treated as empty
+  const uint32_t n = r.epoch == P.plan_epoch ? r.n_units : stale_item(P);
   const uint32_t B = blockDim.x;
   if (r.kind == kItemXRecv) {
     // this rank's halo rows of one pulse from another group: LL units -> x rows;
@@ -330,11 +344,11 @@ template <int W>
 __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, const uint4* nodes, const LocalBase* lb,
                                           const ExParams& P, uint32_t tag, double (*s_v)[kThreads],
                                           float (*s_val)[kThreads], uint64_t* tdet) {
-  const uint32_t n = g.n_units;
+  const uint32_t n = g.epoch == P.plan_epoch ? g.n_units : stale_item(P);  // (as x_item)
   const uint32_t S = (blockDim.x / W) * W;  // stride: a multiple of W, every thread keeps one component
   const int c = (int)(threadIdx.x % W);
   const int tid = threadIdx.x;
-  const bool fs_on = P.fshift != nullptr && g.n_buckets > 0;
+  const bool fs_on = P.fshift != nullptr && g.n_buckets > 0 && n > 0;
   if (fs_on)
     for (int b = 0; b < g.n_buckets; ++b) s_v[b][tid] = 0.0;
   for (uint32_t u = tid; u < n && (uint32_t)tid < S; u += S) {
@@ -380,10 +394,10 @@ template <int W>
 __device__ __noinline__ void tree_item_generic(const GRec& g, const TRootG* roots, const TNode* nodes,
                                                   const LocalBase* lb, const ExParams& P, uint32_t tag,
                                                   double (*s_v)[kThreads]) {
-  const uint32_t n = g.n_units;
+  const uint32_t n = g.epoch == P.plan_epoch ? g.n_units : stale_item(P);  // (as x_item)
   const uint32_t S = (blockDim.x / W) * W;
   const int c = (int)(threadIdx.x % W);
-  const bool fs_on = P.fshift != nullptr;
+  const bool fs_on = P.fshift != nullptr && n > 0;
   if (fs_on)
     for (int b = 0; b < g.n_buckets; ++b) s_v[b][threadIdx.x] = 0.0;
   for (uint32_t u = threadIdx.x; u < n && threadIdx.x < S; u += S) {
@@ -400,6 +414,35 @@ __device__ __forceinline__ void red_add_release_gpu(uint64_t* p, uint64_t v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// x launch prologue (one thread per CTA, before griddepcontrol.wait): L2 prefetch
+// in 4 KiB chunks spread over the CTAs of the f launch's item blocks (its CTAs
+// start as ours exit; their bulk loads then hit L2) and of the home x rows our
+// sends read (their TLB walks and HBM reads overlap our own item-block loads).  A
+// prefetch carries no data to the SM, so issuing it before griddepcontrol.wait
+// cannot expose stale x.  Out of line: keeps the kernel's registers.
+template <int W>
+__device__ __noinline__ void prefetch_l2(const ExParams& P) {
+  constexpr uint64_t kCh = 4096;
+  const uint64_t G = gridDim.x;
+  const uint64_t nf = P.pf_f_bytes / kCh + ((P.pf_f_bytes % kCh) >= 16 ? 1 : 0);
+  uint64_t c = blockIdx.x;
+  for (; c < nf; c += G) {
+    const uint64_t o = c * kCh;
+    prefetch_l2_bulk(P.pf_f + o, (uint32_t)(min(kCh, P.pf_f_bytes - o) & ~15ull));
+  }
+  if (!P.pf_x) return;
+  c -= nf;  // continue the same round-robin over the x rows of every local rank
+  for (int l = 0; l < P.n_local; ++l) {
+    const uint64_t b = (uint64_t)P.lbase[l].n_home * W * sizeof(float);
+    const uint64_t nx = b / kCh + ((b % kCh) >= 16 ? 1 : 0);
+    for (; c < nx; c += G) {
+      const uint64_t o = c * kCh;
+      prefetch_l2_bulk(reinterpret_cast<const char*>(P.lbase[l].x) + o, (uint32_t)(min(kCh, b - o) & ~15ull));
+    }
+    c -= nx;
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 enum : int { kModeX = 0, kModeF = 1, kModeXF = 2 };
 
@@ -411,8 +454,16 @@ __host__ __device__ __forceinline__ uint32_t fblk_bytes(uint32_t R) { return 128
 // Items of this CTA: [0, n_main) round-robin over CTAs [0, G - n_tail) (fused:
 // the x items first, then the tree items); n_tail trailing items would get one
 // dedicated CTA each (none in the current plan).
+// CTA size: the narrow x variant (kU = 2) runs 128-thread CTAs, so the x grid takes at
+// most half of an SM's thread slots and the f launch's CTAs become resident (PDL) while
+// x still runs: their item blocks are in shared memory when griddepcontrol.wait releases.
+template <int kU, int kMode>
+__host__ __device__ constexpr int ll_threads() {
+  return kMode != 0 ? kThreads : kU == 2 ? kThreadsXNarrow : kU == 3 ? 64 : kThreads;
+}
+
 template <int W, int kU, int kMode>
-__global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) : 4) k_exchange_ll(
+__global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 : 4) k_exchange_ll(
     const __grid_constant__ ExParams P) {
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq[2];
@@ -451,14 +502,17 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
   }
   for (int t = threadIdx.x; t < P.n_local * 4; t += blockDim.x)
     reinterpret_cast<int4*>(s_lb)[t] = __ldg(reinterpret_cast<const int4*>(P.lbase) + t);
+  if (kMode == kModeX && (P.pf_f_bytes | (uint64_t)P.pf_x) != 0 && threadIdx.x == 32) prefetch_l2<W>(P);
   pdl_wait();  // everything below may depend on earlier work of the stream
+  if (trace && (P.debug & kTraceDetail)) ctrl->trace[tslot][blockIdx.x][14] = gtimer();  // wait released
   // by value when the host knows them (no cold dependent load on the critical path)
   if (threadIdx.x == 0) {
-    if (kMode != kModeF) s_seq[0] = P.seq ? P.seq : ld_relaxed_gpu(&ctrl->seq_x) + 1;
-    if (kMode != kModeX) s_seq[1] = P.seq_f ? P.seq_f : ld_relaxed_gpu(&ctrl->seq_f) + 1;
+    if (kMode != kModeF) s_seq[0] = P.seq ? P.seq : ll_seq_next(ld_relaxed_gpu(&ctrl->seq_x));
+    if (kMode != kModeX) s_seq[1] = P.seq_f ? P.seq_f : ll_seq_next(ld_relaxed_gpu(&ctrl->seq_f));
   }
   timer_start(P.flags, kMode == kModeF ? &ctrl->t_start_f : &ctrl->t_start_x);
   __syncthreads();  // barrier init, base table and sequence numbers visible to every thread
+  if (trace && (P.debug & kTraceDetail)) ctrl->trace[tslot][blockIdx.x][15] = gtimer();  // prologue done
   // arrive early: the atomic's latency hides behind the items (launch_arrive)
   const uint32_t arrived = launch_arrive(kMode == kModeF ? &ctrl->done_f : &ctrl->done_x);
   const uint32_t tag_x = (uint32_t)s_seq[0], tag_f = (uint32_t)s_seq[1];
@@ -482,7 +536,9 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
     } else if constexpr (kMode != kModeX) {
       const GRec& g = *reinterpret_cast<const GRec*>(blk);
       if (kMode == kModeXF && !xin_seen) {  // every halo row of this process is complete (the NB kernel's slot)
-        if (threadIdx.x < 32) xcount_wait(ctrl, nx, s_seq[0] - P.seq_x0, P);
+        // x launches since set_maps (each 2^32 boundary skipped one value, ll_seq_next)
+        const uint64_t launches = (s_seq[0] - P.seq_x0) - ((s_seq[0] >> 32) - (P.seq_x0 >> 32));
+        if (threadIdx.x < 32) xcount_wait(ctrl, nx, launches, P);
         __syncthreads();
         xin_seen = true;
       }
@@ -532,13 +588,29 @@ __global__ void __launch_bounds__(kThreads, kMode == kModeX ? (kU == 1 ? 8 : 4) 
 cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl,
                                   size_t smem, const cudaAccessPolicyWindow* win);
 
+// Narrow x variant (HALO_X_VARIANT): 0 = 256-thread CTAs, one unit per thread (default);
+// 1 = 128 threads, 2 units; 2 = 64 threads, 3 units.  Same items, same results.  Measured
+// (C3, 1 GPU, A/B): 17.36 / 17.62 / 18.67 us/step — the smaller CTAs were meant to let
+// the f launch's CTAs become resident during x, but the register file (64 regs x 256
+// threads per f CTA) admits only one of them beside the x CTAs.
+static int g_x_variant = 0;
+void ll_set_x_variant(int v) { g_x_variant = v < 0 || v > 2 ? 0 : v; }
 template <int W>
 static const void* ll_fn(int mode, bool wide) {
-  if (mode == kModeX) return wide ? (const void*)k_exchange_ll<W, 4, kModeX> : (const void*)k_exchange_ll<W, 1, kModeX>;
+  if (mode == kModeX && !wide)
+    return g_x_variant == 0 ? (const void*)k_exchange_ll<W, 1, kModeX>
+                            : g_x_variant == 2 ? (const void*)k_exchange_ll<W, 3, kModeX>
+                                               : (const void*)k_exchange_ll<W, 2, kModeX>;
+  if (mode == kModeX) return (const void*)k_exchange_ll<W, 4, kModeX>;
   if (mode == kModeF) return wide ? (const void*)k_exchange_ll<W, 4, kModeF> : (const void*)k_exchange_ll<W, 1, kModeF>;
   return wide ? (const void*)k_exchange_ll<W, 4, kModeXF> : (const void*)k_exchange_ll<W, 1, kModeXF>;
 }
 static const void* ll_fn(int layout, int mode, bool wide) { return layout == 4 ? ll_fn<4>(mode, wide) : ll_fn<3>(mode, wide); }
+
+int ll_block(int mode, bool wide) {
+  if (mode != kModeX || wide) return kThreads;
+  return g_x_variant == 0 ? kThreads : g_x_variant == 2 ? 64 : kThreadsXNarrow;
+}
 
 // Ring slots (item blocks in flight per CTA) and dynamic shared memory.
 int ll_ring(bool wide) { return wide ? 2 : kRing; }
@@ -554,7 +626,7 @@ uint32_t ll_fblk_bytes(int tree_rows) { return fblk_bytes((uint32_t)tree_rows); 
 cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
                                const cudaAccessPolicyWindow* win, cudaStream_t st) {
   void* args[] = {(void*)&p};
-  return launch_coop_kernel_ex(ll_fn(layout, mode, wide), grid, kThreads, args, st, true,
+  return launch_coop_kernel_ex(ll_fn(layout, mode, wide), grid, ll_block(mode, wide), args, st, true,
                                ll_smem_bytes(mode, p.item_rows, p.tree_rows, wide), win);
 }
 
@@ -574,7 +646,8 @@ cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [3]: x, f, x
                              (int)ll_smem_bytes(mode, kMaxItemRows, kMaxTreeRows, wide));
     if (e != cudaSuccess) return e;
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, ll_smem_bytes(mode, rows, kTreeRowsOcc, wide));
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, ll_block(mode, wide),
+                                                      ll_smem_bytes(mode, rows, kTreeRowsOcc, wide));
     if (e != cudaSuccess) return e;
     blocks[mode] = b * sms;
   }

@@ -1,0 +1,384 @@
+// kernels_plan.cu — GPU build of the LL protocol's per-epoch plan (set_maps, SURVEY
+// §8(f) f2: "the map build ... and the gather plan on the device").
+//
+// The host version (runtime.cu build_ll_x / build_ll_f) walks every halo row of every
+// local rank; at C3 that took milliseconds of host time per NS step plus the download
+// of every map and the upload of the MB-sized item blocks.  Here the maps never leave
+// the device: the host fills a small descriptor (PlanDev: per (local rank, pulse)
+// relations and pointers), the kernels below count the work items, the host reads the
+// counts (a few hundred bytes) and fixes the item offsets, and the kernels write the
+// item blocks in place.  The blocks are the ones the host builds,
+// except that a force item's shift-force buckets are the targets of every tree rooted
+// at its rank (<= 2^P - 1 <= 7 for P <= 3, R13) instead of its own trees' targets.
+//
+//   x (Alg. 3/4, rows from their origin):
+//     k_plan_org_home / k_plan_org_pulse(q): the origin of every row (a home row of a
+//       rank of this group, or the LL unit in which it entered the group) and the
+//       pulses whose +L shift it picked up since (R25), pulses in order;
+//     k_plan_x<false/true>: per (pulse, local rank) the send entries cut into items at
+//       every change of dependency class and every R rows (count, then write).
+//   f (Alg. 5/6, trees):
+//     k_plan_child: the inverse maps (row t of rank l is entry i of map q);
+//     k_plan_roots: which rows root a tree and its class (a depth-first walk, children
+//       in descending pulse order: R15); k_plan_rank: each root's rank within its
+//       (class, local rank), in row order;
+//     k_plan_f: each root's 32-B record + node indices into its item, item records.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "halo_internal.h"
+
+namespace halo {
+
+namespace {
+
+constexpr int kPB = 256;  // threads per CTA of the scan kernels
+
+__device__ __forceinline__ uint64_t org_pack(uint32_t row, uint32_t l, uint32_t kq, uint32_t mask, uint32_t cls) {
+  return (uint64_t)row | ((uint64_t)l << 24) | ((uint64_t)kq << 32) | ((uint64_t)mask << 40) | ((uint64_t)cls << 48);
+}
+__device__ __forceinline__ uint32_t org_cls(uint64_t o) { return (uint32_t)(o >> 48) & 0xffu; }
+
+// Inclusive max-scan over the CTA (kPB threads); every thread gets its prefix.
+__device__ __forceinline__ int block_scan_max(int v, int* s_w) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = max(v, y);
+  }
+  if (lane == 31) s_w[w] = v;
+  __syncthreads();
+  int pre = -1;
+  for (int k = 0; k < w; ++k) pre = max(pre, s_w[k]);
+  __syncthreads();
+  return max(v, pre);
+}
+
+// Per class c < nc: the number of threads t <= me with pred && cls == c (inclusive),
+// returned for the caller's own class (pred or not; 0 <= cls < nc); totals of every
+// class into s_tot.
+__device__ __forceinline__ int block_count_class(bool pred, int cls, int nc, int (*s_w)[kPB / 32], int* s_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int mine = 0;
+  for (int c = 0; c < nc; ++c) {
+    const unsigned b = __ballot_sync(0xffffffffu, pred && cls == c);
+    if (lane == 0) s_w[c][w] = __popc(b);
+    if (cls == c) mine = __popc(b & (0xffffffffu >> (31 - lane)));
+  }
+  __syncthreads();
+  int pre = 0;  // (every thread: an entry inside an item counts the starts before it too)
+  for (int k = 0; k < w; ++k) pre += s_w[cls][k];
+  if (threadIdx.x < nc) {
+    int t = 0;
+    for (int k = 0; k < kPB / 32; ++k) t += s_w[threadIdx.x][k];
+    s_tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+  return pre + mine;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ x origins
+__global__ void k_plan_org_home(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.y;
+  const int n = D->n_home[l];
+  uint64_t* o = D->org + (size_t)l * D->cap;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    o[t] = org_pack((uint32_t)t, (uint32_t)l, 0, 0, 0);
+}
+
+// The rows this rank received in pulse q: from a rank of this group, the origin of the
+// sent row (+ this pulse's shift bit if the sender wrapped); from another group, the
+// LL unit i of slot q (class q + 1).  Pulses in order (stream-ordered launches).
+__global__ void k_plan_org_pulse(const PlanDev* __restrict__ D, int q) {
+  const int l = blockIdx.y;
+  const PlanLQ& a = D->lq[l][q];
+  uint64_t* o = D->org + (size_t)l * D->cap + a.atom_offset;
+  const int s = a.snd_l;
+  const int32_t* m = s >= 0 ? D->maps[s] + (size_t)q * D->map_stride : nullptr;
+  const uint64_t sh = (s >= 0 && D->lq[s][q].wraps) ? ((uint64_t)(1u << q) << 40) : 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.recv_size; i += gridDim.x * blockDim.x)
+    o[i] = s >= 0 ? (D->org[(size_t)s * D->cap + m[i]] | sh)
+                  : org_pack((uint32_t)i, (uint32_t)l, 0x80u | (uint32_t)q, 0, (uint32_t)q + 1);
+}
+
+// ------------------------------------------------------------------ x items
+// One CTA per (pulse p, local rank l): the map's entries in order; an item starts at
+// every change of class and every R entries within a run of one class (the host's
+// build_ll_x).  kWrite = false: items per class -> xcnt; true: every entry's XEnt and,
+// by the item's last entry, its XRec, at item xoff[class][p][l] + (index in class).
+template <bool kWrite>
+__global__ void __launch_bounds__(kPB) k_plan_x(const PlanDev* __restrict__ D) {
+  const int p = blockIdx.x, l = blockIdx.y;
+  const PlanLQ& a = D->lq[l][p];
+  const int n = a.send_size, R = D->R, nc = D->P + 1;
+  const int32_t* m = D->maps[l] + (size_t)p * D->map_stride;
+  const uint64_t* org = D->org + (size_t)l * D->cap;
+  __shared__ int s_w[kMaxP + 1][kPB / 32];
+  __shared__ int s_mx[kPB / 32];
+  __shared__ int s_tot[kMaxP + 1];
+  __shared__ int s_cnt[kMaxP + 1];
+  __shared__ int s_carry[3];  // run start, item start, class of the previous chunk's last entry
+  __shared__ uint8_t s_cls[kPB + 1];
+  if (threadIdx.x <= kMaxP) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) { s_carry[0] = -1; s_carry[1] = -1; s_carry[2] = -1; }
+  __syncthreads();
+  for (int base = 0; base < n; base += kPB) {
+    const int k = base + threadIdx.x;
+    const bool valid = k < n;
+    const uint64_t o = valid ? org[m[k]] : 0;
+    const int cls = valid ? (int)org_cls(o) : 0;
+    s_cls[threadIdx.x] = (uint8_t)cls;
+    if (threadIdx.x == 0) s_cls[kPB] = (k + kPB < n) ? (uint8_t)org_cls(org[m[k + kPB]]) : 0xffu;
+    __syncthreads();
+    const int prev = threadIdx.x == 0 ? s_carry[2] : (int)s_cls[threadIdx.x - 1];
+    const bool change = valid && (k == 0 || cls != prev);
+    const int runstart = max(block_scan_max(change ? k : -1, s_mx), s_carry[0]);
+    const bool start = valid && (change || (k - runstart) % R == 0);
+    const int istart = max(block_scan_max(start ? k : -1, s_mx), s_carry[1]);
+    const int idx = block_count_class(start, cls, nc, s_w, s_tot);  // inclusive count of my class's starts
+    if (kWrite && valid) {
+      const int item = D->xoff[cls][p][l] + s_cnt[cls] + idx - 1;
+      char* blk = D->xblk + (size_t)item * D->XB;
+      const int e = k - istart;
+      XEnt E;
+      E.row = (uint32_t)(o & 0xffffffu);
+      E.l = (uint8_t)((o >> 24) & 0xffu);
+      E.kq = (uint8_t)((o >> 32) & 0xffu);
+      E.mask = (uint8_t)(((o >> 40) & 0xffu) | (a.wraps ? 1u << p : 0u));
+      E.pad = 0;
+      reinterpret_cast<XEnt*>(blk + 128)[e] = E;
+      // the item's last entry writes its record
+      const int ncls = threadIdx.x == kPB - 1 ? (int)s_cls[kPB] : (int)s_cls[threadIdx.x + 1];
+      const bool last = k + 1 == n || ncls != cls || (k + 1 - runstart) % R == 0;
+      if (last) {
+        XRec r;
+        memset(&r, 0, sizeof r);
+        r.kind = kItemXSend;
+        r.pulse = (uint8_t)p;
+        r.lrank = (uint16_t)l;
+        r.n_units = (uint32_t)(e + 1) * D->W;
+        r.begin = (uint32_t)istart;
+        r.cls = (uint32_t)cls;
+        r.dst_x = a.rcv_l >= 0 ? a.dst_x : nullptr;
+        r.dst_ll = a.rcv_l >= 0 ? nullptr : a.dst_ll;
+        for (int q = 0; q < kMaxP; ++q) {
+          r.shiftL[q] = D->shiftL[q];
+          r.pdim[q] = D->pdim[q];
+        }
+        r.epoch = D->epoch;
+        *reinterpret_cast<XRec*>(blk) = r;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == kPB - 1 || k == n - 1) {  // carries to the next chunk (the chunk's last valid entry)
+      if (valid && (k == n - 1 || threadIdx.x == kPB - 1)) {
+        s_carry[0] = runstart;
+        s_carry[1] = istart;
+        s_carry[2] = cls;
+      }
+    }
+    if (threadIdx.x < nc) s_cnt[threadIdx.x] += s_tot[threadIdx.x];
+    __syncthreads();
+  }
+  if (!kWrite && threadIdx.x < nc) D->xcnt[((size_t)p * D->L + l) * nc + threadIdx.x] = s_cnt[threadIdx.x];
+}
+
+// ------------------------------------------------------------------ f trees
+__global__ void k_plan_child(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.y / D->P, q = blockIdx.y % D->P;
+  const int n = D->lq[l][q].send_size;
+  const int32_t* m = D->maps[l] + (size_t)q * D->map_stride;
+  int32_t* c = D->child + (size_t)l * D->cap * D->P;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    c[(size_t)m[i] * D->P + q] = i;
+}
+
+// Depth-first node list of the tree under row t of local rank l, children in
+// descending pulse order (the oracle's accumulation order, R15) — the host's emit_tree.
+// Returns the node count (<= 2^P <= kFastNodes); lowest = lowest pulse of its LL nodes.
+__device__ int plan_tree(const PlanDev* __restrict__ D, int l, int t, TNode* v, int& lowest) {
+  struct Fr {
+    int l, t, me, q, depth;
+  } st[kMaxP + 1];
+  const int P = D->P;
+  int n = 0, top = 0;
+  v[n++] = TNode{(uint32_t)t | ((uint32_t)l << 24), 0, 0xff, 0, 0xff};
+  st[top++] = Fr{l, t, 0, P - 1, 0};
+  lowest = P;
+  while (top > 0) {
+    Fr& f = st[top - 1];
+    if (f.q < 0) {
+      --top;
+      continue;
+    }
+    const int q = f.q--;
+    const int i = D->child[((size_t)f.l * D->cap + f.t) * P + q];
+    if (i < 0) continue;
+    v[f.me].flags |= 1;  // has children: its folded value is stored
+    const PlanLQ& a = D->lq[f.l][q];
+    const int fl = f.l, fme = f.me, fd = f.depth;
+    if (a.rcv_l >= 0) {
+      const int me = n;
+      v[n++] = TNode{(uint32_t)(a.remote_off + i) | ((uint32_t)a.rcv_l << 24), 0, (uint8_t)fme,
+                     (uint8_t)((fd + 1) << 1), a.efs};
+      st[top++] = Fr{a.rcv_l, a.remote_off + i, me, P - 1, fd + 1};
+    } else {
+      v[n++] = TNode{(uint32_t)i | ((uint32_t)fl << 24), (uint8_t)(0x80u | q), (uint8_t)fme,
+                     (uint8_t)((fd + 1) << 1), a.efs};
+      lowest = min(lowest, q);
+    }
+  }
+  return n;
+}
+
+// Is row t of local rank l a root?  Home rows with images; halo rows whose x-sender is
+// in another group (they push their value back there; push = that LL unit).
+__device__ __forceinline__ bool plan_is_root(const PlanDev* __restrict__ D, int l, int t, uint64_t** push) {
+  const int P = D->P;
+  *push = nullptr;
+  if (t < D->n_home[l]) {
+    const int32_t* c = D->child + ((size_t)l * D->cap + t) * P;
+    for (int q = 0; q < P; ++q)
+      if (c[q] >= 0) return true;
+    return false;
+  }
+  for (int q = 0; q < P; ++q) {
+    const PlanLQ& a = D->lq[l][q];
+    if (t >= a.atom_offset && t < a.atom_offset + a.recv_size) {
+      if (a.snd_l >= 0) return false;
+      *push = a.push + (size_t)(t - a.atom_offset) * D->W;
+      return true;
+    }
+  }
+  return false;
+}
+
+__global__ void k_plan_roots(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.y;
+  const int n = D->n_total[l];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    uint64_t* push;
+    uint8_t cls = 0xff;
+    if (plan_is_root(D, l, t, &push)) {
+      TNode v[kFastNodes];
+      int lowest;
+      (void)plan_tree(D, l, t, v, lowest);
+      cls = (uint8_t)(D->P - lowest);
+    }
+    D->rcls[(size_t)l * D->cap + t] = cls;
+  }
+}
+
+// One CTA per local rank: rank of every root among the roots of its class, row order.
+__global__ void __launch_bounds__(kPB) k_plan_rank(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.x, nc = D->P + 1;
+  const int n = D->n_total[l];
+  __shared__ int s_w[kMaxP + 1][kPB / 32];
+  __shared__ int s_tot[kMaxP + 1];
+  __shared__ int s_cnt[kMaxP + 1];
+  if (threadIdx.x <= kMaxP) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += kPB) {
+    const int t = base + threadIdx.x;
+    const int c = t < n ? (int)D->rcls[(size_t)l * D->cap + t] : 0xff;
+    const bool root = c != 0xff;
+    const int idx = block_count_class(root, root ? c : 0, nc, s_w, s_tot);
+    if (root) D->rrank[(size_t)l * D->cap + t] = s_cnt[c] + idx - 1;
+    __syncthreads();
+    if (threadIdx.x < nc) s_cnt[threadIdx.x] += s_tot[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x < nc) D->rcnt[l * nc + threadIdx.x] = s_cnt[threadIdx.x];
+}
+
+// Every root writes its 32-B record and node indices into slot rank % RT of item
+// foff[class][l] + rank / RT; slot 0 also writes the item's record.
+__global__ void k_plan_f(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.y;
+  const int n = D->n_total[l], RT = D->RT;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint8_t cls = D->rcls[(size_t)l * D->cap + t];
+    if (cls == 0xff) continue;
+    uint64_t* push;
+    (void)plan_is_root(D, l, t, &push);
+    TNode v[kFastNodes];
+    int lowest;
+    const int nn = plan_tree(D, l, t, v, lowest);
+    const int rank = D->rrank[(size_t)l * D->cap + t];
+    const int item = D->foff[cls][l] + rank / RT, slot = rank % RT;
+    char* blk = D->fblk + (size_t)item * D->FB;
+    TRoot R;
+    memset(&R, 0, sizeof R);
+    R.push = push;
+    R.par = 0xffffffffu;
+    R.bucket = 0xffffffffu;
+    R.nn = (uint8_t)nn;
+    {  // postorder of the non-root nodes: close every open node at least as deep as the next
+      int stk[kFastNodes], top = 0, e = 0;
+      for (int k = 0; k <= nn; ++k) {
+        const int dk = k < nn ? (v[k].flags >> 1) : 0;
+        while (top > 0 && (v[stk[top - 1]].flags >> 1) >= dk) {
+          const int c = stk[--top];
+          if (c != 0) R.post |= (uint32_t)c << (4 * e++);
+        }
+        if (k < nn) stk[top++] = k;
+      }
+    }
+    uint32_t* il = reinterpret_cast<uint32_t*>(blk + 128 + 32 * (size_t)RT) + 8 * slot;
+    for (int k = 0; k < nn; ++k) {
+      const TNode& x = v[k];
+      const uint32_t sh = 4 * (uint32_t)k;
+      uint32_t b = kFsNone;
+      if (x.fs != 0xff)
+        for (int j = 0; j < D->n_buckets[l]; ++j)
+          if (D->bucket_fs[l][j] == x.fs) b = (uint32_t)j;
+      R.par = (R.par & ~(15u << sh)) | ((uint32_t)(x.parent == 0xff ? 15 : x.parent) << sh);
+      R.bucket = (R.bucket & ~(15u << sh)) | (b << sh);
+      R.q |= (uint32_t)(x.kq & 7) << sh;
+      if (x.kq & 0x80u) R.llmask |= (uint8_t)(1u << k);
+      if (x.flags & 1u) R.stmask |= (uint8_t)(1u << k);
+      il[k] = x.il;
+    }
+    reinterpret_cast<TRoot*>(blk + 128)[slot] = R;
+    if (slot == 0) {
+      GRec g;
+      memset(&g, 0, sizeof g);
+      g.kind = kItemTree;
+      g.level = cls;
+      g.lrank = (uint16_t)l;
+      g.n_roots = (uint32_t)min(RT, D->fcnt[cls][l] - rank);
+      g.n_units = g.n_roots * D->W;
+      g.n_buckets = D->n_buckets[l];
+      for (int j = 0; j < kMaxBuckets; ++j) g.bucket_fs[j] = D->bucket_fs[l][j];
+      g.epoch = D->epoch;
+      *reinterpret_cast<GRec*>(blk) = g;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static unsigned plan_gx(int rows) { return (unsigned)std::max(1, std::min(64, (rows + 255) / 256)); }
+
+cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st) {
+  const unsigned gx = plan_gx(max_rows);
+  k_plan_org_home<<<dim3(gx, L), 256, 0, st>>>(D);
+  for (int q = 0; q < P; ++q) k_plan_org_pulse<<<dim3(gx, L), 256, 0, st>>>(D, q);
+  k_plan_x<false><<<dim3(P, L), kPB, 0, st>>>(D);
+  k_plan_child<<<dim3(gx, L * P), 256, 0, st>>>(D);
+  k_plan_roots<<<dim3(gx, L), 256, 0, st>>>(D);
+  k_plan_rank<<<L, kPB, 0, st>>>(D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st) {
+  k_plan_x<true><<<dim3(P, L), kPB, 0, st>>>(D);
+  k_plan_f<<<dim3(plan_gx(max_rows), L), 256, 0, st>>>(D);
+  return cudaGetLastError();
+}
+
+}  // namespace halo

@@ -124,6 +124,11 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 
 // Programmatic dependent launch (sm_90+): let the next kernel of the stream be
 // scheduled now, and block until the previous kernel's memory is complete.
+// Bulk L2 prefetch (no data returned; a hint, coherent with later loads): 16-B
+// aligned address, size a multiple of 16.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 

@@ -39,12 +39,18 @@ cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid
                                const cudaAccessPolicyWindow* win, cudaStream_t st);
 cudaError_t max_coresident_ll(int layout, bool wide, int* blocks);
 int ll_ring(bool wide);
+void ll_set_x_variant(int v);
 cudaError_t launch_empty(int grid, cudaStream_t st, uint64_t* remote, uint32_t nwords);
 cudaError_t launch_ce_pack(int layout, const CeEnt* ents, int n_local, int max_rows, cudaStream_t st);
 cudaError_t launch_ce_unpack(int layout, const CeEnt* ents, int n_local, int max_rows, double* fshift, int accumulate,
                              cudaStream_t st);
 cudaError_t launch_ce_sync(const CeSyncParams& s, cudaStream_t st);
 cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
+cudaError_t launch_seg_copy(const SegCopy* segs, int nseg, size_t max_words, cudaStream_t st);
+cudaError_t launch_ns_x(const NsXParams& X, int layout, int max_rows, cudaStream_t st);
+cudaError_t launch_ns_wait(const NsWaitParams& W, cudaStream_t st);
+cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st);
+cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st);
 uint32_t ll_xblk_bytes(int rows);
 uint32_t ll_fblk_bytes(int rows);
 cudaError_t launch_assign_home(const float* x, int n, int stride, const AssignParams& A, int32_t* rank, int* counts,
@@ -142,6 +148,18 @@ struct halo_ctx {
   Ctrl* ctrl = nullptr;
   char* plan = nullptr;
   size_t plan_bytes = 0;
+  std::vector<char*> retired;       // plans replaced while a captured graph may reference them
+  // GPU-built LL plan (kernels_plan.cu): block areas written by the kernels
+  size_t gpu_xblk_bytes = 0, gpu_fblk_bytes = 0;
+  int gpu_n_items_x = 0, gpu_n_items_f = 0;
+  bool gpu_plan = true;             // HALO_PLAN_HOST=1: the host builder (reference; also P > 3)
+  PlanDev* d_pl = nullptr;          // descriptor + scratch of the GPU plan build
+  PlanDev* h_pl = nullptr;          // (pinned host copy)
+  char* d_pl_scratch = nullptr;
+  size_t pl_scratch_bytes = 0;
+  int32_t* h_pl_cnt = nullptr;      // pinned: xcnt | rcnt read back after the counting pass
+  XRec* h_recv = nullptr;           // pinned: the receive items' records
+  size_t h_recv_cap = 0;
   RankDev* d_ranks = nullptr;
   PulseDev* d_pulses = nullptr;
   Item* d_items_x = nullptr;
@@ -149,6 +167,16 @@ struct halo_ctx {
   int n_items_x = 0, n_items_f = 0;
   int n_tail_f = 0;                 // LL: shift-force combine items at the end of the f list
   double* d_fshift_tmp = nullptr;  // halo_step_host
+  // halo_step_host_packed: packed staging in / out, segment tables (x unpack | f unpack | pack),
+  // rebuilt once per NS epoch; side streams for the f upload and the halo-x download
+  char* d_pk_in = nullptr;
+  char* d_pk_out = nullptr;
+  size_t pk_in_cap = 0, pk_out_cap = 0;
+  SegCopy* d_segs = nullptr;
+  uint32_t pk_epoch = 0;
+  size_t pk_max_words[3] = {0, 0, 0};
+  cudaStream_t pk_h2d = nullptr, pk_d2h = nullptr;
+  cudaEvent_t pk_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   char* d_small = nullptr;          // set_maps argument staging
   MigRank* d_mig = nullptr;         // halo_migrate: per local rank tables
   MigCtrl* d_migctrl = nullptr;
@@ -222,6 +250,8 @@ struct halo_ctx {
   size_t auto_ce_bytes = (size_t)4 << 20;  // ... copy engine when some pulse sends >= this (HALO_AUTO_CE_BYTES)
   bool collapse = true;             // LL: the ranks of this process form one hop group (HALO_COLLAPSE=0 /
                                     // HALO_DIRECT_X=0: every rank its own group, the staged schedule)
+  bool prefetch = false;            // LL x launch: L2 prefetch of the f item blocks and home x rows (HALO_PREFETCH=1;
+                                    // measured slower at C3: 17.3 -> 18.1 us/step, the prefetches delay the x blocks)
   int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
   // NCCL send/recv baseline (halo_nccl_*, HALO_F_NCCL_BASELINE): communicator + packed send rows
   void* nccl_comm = nullptr;
@@ -300,6 +330,9 @@ static halo_status check_err_word(halo_ctx* ctx) {
   if (ctx->err_host && *(volatile int*)ctx->err_host != 0) {
     char buf[128];
     int code = *(volatile int*)ctx->err_host;
+    if ((code >> 16) == kErrKindStalePlan)
+      return fail(ctx, HALO_ERR_STATE, "a CUDA graph captured before the last halo_set_maps / halo_migrate was "
+                                       "replayed (its plan is gone): re-capture after every NS step");
     snprintf(buf, sizeof buf, "device wait timed out (kind %d, local rank %d, pulse %d)", code >> 16,
              (code >> 8) & 0xff, code & 0xff);
     return fail(ctx, HALO_ERR_TIMEOUT, buf);
@@ -416,6 +449,10 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (const char* e = getenv("HALO_DIRECT_X")) ctx->collapse = atoi(e) != 0;
   if (const char* e = getenv("HALO_COLLAPSE")) ctx->collapse = atoi(e) != 0;
   if (const char* e = getenv("HALO_RECV_MULT")) ctx->recv_mult = std::min(16, std::max(1, atoi(e)));
+  if (const char* e = getenv("HALO_PREFETCH")) ctx->prefetch = atoi(e) != 0;
+  if (const char* e = getenv("HALO_PLAN_HOST")) ctx->gpu_plan = atoi(e) == 0;
+  if (const char* e = getenv("HALO_TIMEOUT_S")) ctx->cfg.timeout_s = std::max(0.001, atof(e));  // sanitizer runs
+  ll_set_x_variant(getenv("HALO_X_VARIANT") ? atoi(getenv("HALO_X_VARIANT")) : 0);
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
   cudaError_t e = cudaSetDevice(cfg->device);
@@ -424,6 +461,10 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) {
     uint64_t init[4] = {~0ull, 0, ~0ull, 0};
     e = cudaMemcpy(&ctx->ctrl->t_start_x, init, sizeof init, cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && getenv("HALO_SEQ_BASE")) {  // test hook: start the sequence numbers near a tag wrap
+    const uint64_t b[2] = {strtoull(getenv("HALO_SEQ_BASE"), nullptr, 0), strtoull(getenv("HALO_SEQ_BASE"), nullptr, 0)};
+    e = cudaMemcpy(&ctx->ctrl->seq_x, b, sizeof b, cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess) e = cudaHostAlloc(&ctx->err_host, 64, cudaHostAllocMapped);
   if (e == cudaSuccess) { memset(ctx->err_host, 0, 64); e = cudaHostGetDevicePointer(&ctx->err_dev, ctx->err_host, 0); }
@@ -765,6 +806,7 @@ static void fill_lbase(halo_ctx* ctx) {
     b.xll = ctx->xll_of(r);
     b.fll = ctx->fll_of(r);
     for (int q = 0; q < kMaxP; ++q) b.recv_off[q] = q < P ? ctx->atom_offset[l * P + q] : 0;
+    b.n_home = ctx->n_home[l];
   }
 }
 
@@ -836,6 +878,7 @@ static void build_ll_x(halo_ctx* ctx, int p_lo, int p_hi) {
         x.n_units = (uint32_t)(e - b) * W;
         x.begin = (uint32_t)b;
         x.cls = cls;
+        x.epoch = ctx->epoch;
         if (local) {
           x.dst_x = ctx->x[rcv - ctx->first_rank] + (size_t)ctx->remote_off[l * P + p] * W;
         } else {
@@ -873,6 +916,7 @@ static void build_ll_x(halo_ctx* ctx, int p_lo, int p_hi) {
         x.n_units = (uint32_t)(e - b) * W;
         x.begin = (uint32_t)b;
         x.cls = 0xff;
+        x.epoch = ctx->epoch;
         x.ll = ctx->xll_of(r) + (size_t)p * ctx->ll_stride + (size_t)b * W;
         x.xdst = ctx->x[l] + (size_t)(ctx->atom_offset[l * P + p] + b) * W;
         items.push_back(std::move(it));
@@ -896,9 +940,10 @@ static void build_ll_x(halo_ctx* ctx, int p_lo, int p_hi) {
 // Node list of the tree under row t of local rank l, depth first, children in
 // descending pulse order (the oracle's accumulation order, R15).  `fs` of the
 // edge into a node: 3 * (parent's local rank) + dim when the parent's rank
-// wrapped in the edge's pulse (R13), else 0xff.
+// wrapped in the edge's pulse (R13), else 0xff.  Appends to `v` (a per-thread
+// arena: no allocation per tree).
 static void emit_tree(const halo_ctx* ctx, const std::vector<std::vector<int32_t>>& child, int l, int t, int depth,
-                      int parent, uint8_t fs, std::vector<TNode>& v, int& lowest_ll) {
+                      int parent, uint8_t fs, std::vector<TNode>& v, size_t base, int& lowest_ll) {
   const int P = ctx->P, r = ctx->first_rank + l;
   const size_t me = v.size();
   v.push_back(TNode{(uint32_t)t | ((uint32_t)l << 24), 0, (uint8_t)(parent < 0 ? 0xff : parent),
@@ -911,15 +956,49 @@ static void emit_tree(const halo_ctx* ctx, const std::vector<std::vector<int32_t
     const uint8_t efs = ctx->cell(r, d) == 0 ? (uint8_t)(3 * l + d) : (uint8_t)0xff;
     const int rcv = ctx->neighbour(r, d, -1);
     if (same_group(ctx, r, rcv)) {
-      emit_tree(ctx, child, rcv - ctx->first_rank, ctx->remote_off[l * P + q] + i, depth + 1, (int)me, efs, v,
-                lowest_ll);
+      emit_tree(ctx, child, rcv - ctx->first_rank, ctx->remote_off[l * P + q] + i, depth + 1, (int)(me - base), efs,
+                v, base, lowest_ll);
     } else {
-      v.push_back(TNode{(uint32_t)i | ((uint32_t)l << 24), (uint8_t)(0x80u | q), (uint8_t)me,
+      v.push_back(TNode{(uint32_t)i | ((uint32_t)l << 24), (uint8_t)(0x80u | q), (uint8_t)(me - base),
                         (uint8_t)((depth + 1) << 1), efs});
       lowest_ll = std::min(lowest_ll, q);
     }
   }
 }
+
+struct PhaseTimer {
+  bool on = getenv("HALO_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::string acc;
+  void lap(const char* name) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    char buf[96];
+    snprintf(buf, sizeof buf, " %s=%.0f", name, std::chrono::duration<double, std::micro>(now - t).count());
+    acc += buf;
+    t = now;
+  }
+  void print(int rank) const {
+    if (on) fprintf(stderr, "[halo_profile rank %d set_maps us]%s\n", rank, acc.c_str());
+  }
+};
+
+// Distinct shift-force targets of one tree or one item (<= kMaxBuckets + 1 kept).
+struct FsSet {
+  uint8_t v[kMaxBuckets + 1];
+  int n = 0;
+  bool add(uint8_t x) {  // false once more than kMaxBuckets distinct targets were seen
+    for (int k = 0; k < n; ++k)
+      if (v[k] == x) return true;
+    if (n <= kMaxBuckets) v[n++] = x;
+    return n <= kMaxBuckets;
+  }
+  int find(uint8_t x) const {
+    for (int k = 0; k < n; ++k)
+      if (v[k] == x) return k;
+    return -1;
+  }
+};
 
 // f items: the trees of this group.  A row's children are its images (one per
 // pulse whose map sends it); children in this group are nodes of the same tree,
@@ -927,8 +1006,9 @@ static void emit_tree(const halo_ctx* ctx, const std::vector<std::vector<int32_t
 // rows with children, and halo rows whose x-sender is in another group (they push
 // their value back there).  Dependency class of a tree = P - (lowest pulse of its
 // LL nodes), 0 without: a pushed value comes from a tree whose LL nodes all have
-// higher pulses, i.e. a lower class.  Then one combine per (rank, wrapped dim).
-static halo_status build_ll_f(halo_ctx* ctx) {
+// higher pulses, i.e. a lower class.  NS-step host work: no allocation per tree
+// (per-thread node arenas, fixed-size shift-force sets and postorder stacks).
+static halo_status build_ll_f(halo_ctx* ctx, PhaseTimer* prof = nullptr) {
   const int L = ctx->n_local, P = ctx->P, W = ctx->W;
   // child[l][t*P + q] = i: row t of rank l is entry i of map_q (one per pulse at most)
   std::vector<std::vector<int32_t>> child(L);
@@ -939,19 +1019,30 @@ static halo_status build_ll_f(halo_ctx* ctx) {
       for (size_t i = 0; i < m.size(); ++i) child[l][(size_t)m[i] * P + q] = (int32_t)i;
     }
   });
+  if (prof) prof->lap("f:child");
   struct Tree {
     int l, t;
     uint8_t cls;
     bool small;
+    bool direct;  // more than kMaxBuckets shift-force targets: its edges add directly
+    uint16_t nn;
+    const TNode* nodes;
     uint64_t* push;
+    FsSet fs;
   };
   std::vector<Tree> roots;
+  {
+    size_t nr = 0;
+    for (int l = 0; l < L; ++l) nr += ctx->n_total[l];
+    roots.reserve(nr);
+  }
   for (int l = 0; l < L; ++l) {
     const int r = ctx->first_rank + l;
+    const int32_t* cl = child[l].data();
     for (int t = 0; t < ctx->n_home[l]; ++t) {
       bool any = false;
-      for (int q = 0; q < P && !any; ++q) any = child[l][(size_t)t * P + q] >= 0;
-      if (any) roots.push_back(Tree{l, t, 0, true, nullptr});
+      for (int q = 0; q < P && !any; ++q) any = cl[(size_t)t * P + q] >= 0;
+      if (any) roots.push_back(Tree{l, t, 0, true, false, 0, nullptr, nullptr, {}});
     }
     for (int q = 0; q < P; ++q) {
       const int s = ctx->neighbour(r, ctx->pdim[q], +1);
@@ -959,24 +1050,44 @@ static halo_status build_ll_f(halo_ctx* ctx) {
       const int i0 = ctx->atom_offset[l * P + q];
       uint64_t* base = ctx->fll_of(s) + (size_t)q * ctx->ll_stride;
       for (int i = 0; i < ctx->recv_size[l * P + q]; ++i)
-        roots.push_back(Tree{l, i0 + i, 0, true, base + (size_t)i * W});
+        roots.push_back(Tree{l, i0 + i, 0, true, false, 0, nullptr, base + (size_t)i * W, {}});
     }
   }
-  // depth-first node lists (children pulses descending, R15) and their shift-force targets
-  std::vector<std::vector<TNode>> tn(roots.size());
-  std::vector<std::vector<uint8_t>> tfs(roots.size());
-  parallel_for(roots.size(), [&](size_t k) {
-    int lowest_ll = P;
-    emit_tree(ctx, child, roots[k].l, roots[k].t, 0, -1, 0xff, tn[k], lowest_ll);
-    roots[k].cls = (uint8_t)(P - lowest_ll);
-    roots[k].small = tn[k].size() <= (size_t)kFastNodes;
-    for (const TNode& v : tn[k])
-      if (v.fs != 0xff && std::find(tfs[k].begin(), tfs[k].end(), v.fs) == tfs[k].end()) tfs[k].push_back(v.fs);
-  });
+  if (prof) prof->lap("f:roots");
+  // depth-first node lists (children pulses descending, R15) into per-thread arenas
+  const size_t NR = roots.size();
+  const size_t T = NR < 4096 ? 1 : std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::vector<TNode>> arena(T);
+  auto emit_range = [&](size_t th) {
+    const size_t k0 = NR * th / T, k1 = NR * (th + 1) / T;
+    auto& v = arena[th];
+    v.reserve((k1 - k0) * 3 + 16);
+    std::vector<size_t> begin(k1 - k0);
+    for (size_t k = k0; k < k1; ++k) {
+      int lowest_ll = P;
+      begin[k - k0] = v.size();
+      emit_tree(ctx, child, roots[k].l, roots[k].t, 0, -1, 0xff, v, v.size(), lowest_ll);
+      Tree& R = roots[k];
+      R.cls = (uint8_t)(P - lowest_ll);
+      R.nn = (uint16_t)(v.size() - begin[k - k0]);
+      R.small = R.nn <= kFastNodes;
+      for (size_t m = begin[k - k0]; m < v.size(); ++m)
+        if (v[m].fs != 0xff && !R.fs.add(v[m].fs)) R.direct = true;
+    }
+    for (size_t k = k0; k < k1; ++k) roots[k].nodes = v.data() + begin[k - k0];  // the arena no longer grows
+  };
+  if (T == 1) {
+    emit_range(0);
+  } else {
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < T; ++t) th.emplace_back(emit_range, t);
+    for (auto& x : th) x.join();
+  }
+  if (prof) prof->lap("f:emit");
   // items: roots ordered by class, rank, small/large, in row order
-  std::vector<size_t> order(roots.size());
-  for (size_t k = 0; k < order.size(); ++k) order[k] = k;
-  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+  std::vector<uint32_t> order(NR);
+  for (size_t k = 0; k < NR; ++k) order[k] = (uint32_t)k;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
     const Tree &x = roots[a], &y = roots[b];
     if (x.cls != y.cls) return x.cls < y.cls;
     if (x.l != y.l) return x.l < y.l;
@@ -986,32 +1097,31 @@ static halo_status build_ll_f(halo_ctx* ctx) {
     size_t b, e;  // range of `order`
     bool small;
     int nodes;
-    std::vector<uint8_t> fs;  // bucket targets
+    FsSet fs;     // bucket targets
   };
   auto form = [&](int RT, std::vector<FI>& fis) {
     fis.clear();
     const int RG = std::max(1, RT / 8);                      // large trees per item
     const int NG = (int)((ll_fblk_bytes(RT) - 128 - 16 * RG) / 8);  // their node capacity
-    for (size_t k = 0; k < order.size();) {
+    for (size_t k = 0; k < NR;) {
       const Tree& t0 = roots[order[k]];
       FI f{k, k, t0.small, 0, {}};
-      while (f.e < order.size()) {
-        const size_t o = order[f.e];
-        const Tree& t = roots[o];
+      while (f.e < NR) {
+        const Tree& t = roots[order[f.e]];
         if (t.cls != t0.cls || t.l != t0.l || t.small != t0.small) break;
         if ((int)(f.e - f.b) >= (f.small ? RT : RG)) break;
-        if (!f.small && f.nodes + (int)tn[o].size() > NG && f.e > f.b) break;
-        if ((int)tfs[o].size() <= kMaxBuckets) {  // (a larger tree adds its edges directly)
-          std::vector<uint8_t> u = f.fs;
-          for (uint8_t x : tfs[o])
-            if (std::find(u.begin(), u.end(), x) == u.end()) u.push_back(x);
-          if ((int)u.size() > kMaxBuckets && f.e > f.b) break;
-          f.fs = std::move(u);
+        if (!f.small && f.nodes + (int)t.nn > NG && f.e > f.b) break;
+        if (!t.direct) {  // (a tree with more targets than buckets adds its edges directly)
+          FsSet u = f.fs;
+          bool ok = true;
+          for (int j = 0; j < t.fs.n && ok; ++j) ok = u.add(t.fs.v[j]);
+          if (!ok && f.e > f.b) break;
+          f.fs = u;
         }
-        f.nodes += (int)tn[o].size();
+        f.nodes += (int)t.nn;
         ++f.e;
       }
-      fis.push_back(std::move(f));
+      fis.push_back(f);
       k = fis.back().e;
     }
   };
@@ -1027,6 +1137,7 @@ static halo_status build_ll_f(halo_ctx* ctx) {
     RT = std::min(kTreeRowsOcc, std::max(8, atoi(e)));
     form(RT, fis);
   }
+  if (prof) prof->lap("f:form");
   const int RG = std::max(1, RT / 8);
   for (const FI& f : fis)
     if (!f.small && (int)(128 + 16 * RG + 8 * f.nodes) > (int)ll_fblk_bytes(RT))
@@ -1047,44 +1158,42 @@ static halo_status build_ll_f(halo_ctx* ctx) {
     g.n_roots = (uint32_t)(f.e - f.b);
     g.n_units = g.n_roots * W;
     g.n_nodes = (uint32_t)f.nodes;
-    g.n_buckets = (uint8_t)f.fs.size();
-    for (size_t b = 0; b < f.fs.size(); ++b) g.bucket_fs[b] = f.fs[b];
+    g.n_buckets = (uint8_t)f.fs.n;
+    g.epoch = ctx->epoch;
+    for (int b = 0; b < f.fs.n; ++b) g.bucket_fs[b] = f.fs.v[b];
     memcpy(blk, &g, sizeof g);
     auto bucket_of = [&](const TNode& x, bool direct) -> uint8_t {
       if (x.fs == 0xff) return kFsNone;
-      return direct ? kFsDirect : (uint8_t)(std::find(f.fs.begin(), f.fs.end(), x.fs) - f.fs.begin());
+      return direct ? kFsDirect : (uint8_t)f.fs.find(x.fs);
     };
     if (f.small) {
       TRoot* rr = reinterpret_cast<TRoot*>(blk + 128);
       uint32_t* il = reinterpret_cast<uint32_t*>(blk + 128 + 32 * (size_t)RT);
       for (size_t j = f.b; j < f.e; ++j) {
-        const std::vector<TNode>& v = tn[order[j]];
+        const Tree& tr = roots[order[j]];
+        const TNode* v = tr.nodes;
+        const int nn = tr.nn;
         TRoot R;
         memset(&R, 0, sizeof R);
-        R.push = roots[order[j]].push;
+        R.push = tr.push;
         R.par = 0xffffffffu;
         R.bucket = 0xffffffffu;
-        R.nn = (uint8_t)v.size();
-        // postorder of the non-root nodes: a node after all its descendants, siblings
-        // in preorder (= descending pulse) order
+        R.nn = (uint8_t)nn;
+        // postorder of the non-root nodes (a node after all its descendants, siblings in
+        // preorder = descending pulse order): close every open node at least as deep as
+        // the next node in preorder
         {
-          std::vector<int> post;
-          std::vector<std::vector<int>> kids(v.size());
-          for (size_t m = 1; m < v.size(); ++m) kids[v[m].parent].push_back((int)m);
-          std::vector<std::pair<int, size_t>> st{{0, 0}};
-          while (!st.empty()) {
-            auto& [node, next] = st.back();
-            if (next < kids[node].size()) {
-              const int ch = kids[node][next++];
-              st.push_back({ch, 0});
-            } else {
-              if (node != 0) post.push_back(node);
-              st.pop_back();
+          int stk[kFastNodes], top = 0, e = 0;
+          for (int m = 0; m <= nn; ++m) {
+            const int dm = m < nn ? (v[m].flags >> 1) : 0;
+            while (top > 0 && (v[stk[top - 1]].flags >> 1) >= dm) {
+              const int c = stk[--top];
+              if (c != 0) R.post |= (uint32_t)c << (4 * e++);
             }
+            if (m < nn) stk[top++] = m;
           }
-          for (size_t e = 0; e < post.size(); ++e) R.post |= (uint32_t)post[e] << (4 * e);
         }
-        for (size_t m = 0; m < v.size(); ++m) {
+        for (int m = 0; m < nn; ++m) {
           const TNode& x = v[m];
           const uint32_t sh = 4 * (uint32_t)m;
           R.par = (R.par & ~(15u << sh)) | ((uint32_t)(x.parent == 0xff ? 15 : x.parent) << sh);
@@ -1101,15 +1210,14 @@ static halo_status build_ll_f(halo_ctx* ctx) {
       TNode* nn = reinterpret_cast<TNode*>(blk + 128 + 16 * (size_t)RG);
       uint32_t at = 0;
       for (size_t j = f.b; j < f.e; ++j) {
-        const std::vector<TNode>& v = tn[order[j]];
-        rr[j - f.b] = TRootG{roots[order[j]].push, at, (uint16_t)v.size(), 0};
-        const bool direct = tfs[order[j]].size() > (size_t)kMaxBuckets;
-        for (size_t m = 0; m < v.size(); ++m) {
-          TNode x = v[m];
-          x.kq = (uint8_t)((x.kq & 0x87u) | (bucket_of(x, direct) << 3));
+        const Tree& tr = roots[order[j]];
+        rr[j - f.b] = TRootG{tr.push, at, tr.nn, 0};
+        for (int m = 0; m < tr.nn; ++m) {
+          TNode x = tr.nodes[m];
+          x.kq = (uint8_t)((x.kq & 0x87u) | (bucket_of(x, tr.direct) << 3));
           nn[at + m] = x;
         }
-        at += (uint32_t)v.size();
+        at += tr.nn;
       }
     }
     Item& w = ctx->h_items_f[k];
@@ -1118,40 +1226,307 @@ static halo_status build_ll_f(halo_ctx* ctx) {
     w.kind = g.kind;
   });
   ctx->n_tail_f = 0;
+  if (prof) prof->lap("f:blocks");
   return HALO_OK;
 }
 
+// Shift-force targets of every force tree rooted at local rank l (R13): the edges of
+// the rank-level tree (a row of rank r received in pulse qlast can be sent in any later
+// pulse q; a wrapping sender's edges add into fshift[r][d_q]; same-group receivers
+// continue the tree).  At most 2^P - 1 edges, i.e. <= kMaxBuckets for P <= 3.
+static halo_status upload_plan(halo_ctx* ctx);
+static halo_status pull_maps(halo_ctx* ctx, int p, cudaStream_t st);
+
+static bool rank_tree_fs(const halo_ctx* ctx, int r, int qlast, FsSet& fs) {
+  for (int q = qlast + 1; q < ctx->P; ++q) {
+    const int d = ctx->pdim[q];
+    if (ctx->cell(r, d) == 0 && !fs.add((uint8_t)(3 * (r - ctx->first_rank) + d))) return false;
+    const int rcv = ctx->neighbour(r, d, -1);
+    if (same_group(ctx, r, rcv) && !rank_tree_fs(ctx, rcv, q, fs)) return false;
+  }
+  return true;
+}
+
+// HALO_PLAN_CHECK=1 (debug): the host builder's plan of the same maps vs the GPU-built
+// blocks, field by field (the shift-force bucket numbering differs by design); the
+// first mismatches go to stderr and fail set_maps.
+static halo_status plan_check(halo_ctx* ctx, cudaStream_t st) {
+  const int P = ctx->P;
+  const int nx = ctx->gpu_n_items_x, nf = ctx->gpu_n_items_f;
+  const uint32_t XB = ll_xblk_bytes(ctx->item_rows), FB = ll_fblk_bytes(ctx->tree_rows);
+  std::vector<char> gx((size_t)nx * XB), gf((size_t)nf * FB);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(gx.data(), ctx->d_xblk, gx.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(gf.data(), ctx->d_fblk, gf.size(), cudaMemcpyDeviceToHost));
+  for (int p = 0; p < P; ++p) {
+    halo_status s = pull_maps(ctx, p, st);
+    if (s != HALO_OK) return s;
+  }
+  const int RT = ctx->tree_rows;
+  build_ll_x(ctx, 0, P);
+  halo_status s = build_ll_f(ctx);
+  if (s != HALO_OK) return s;
+  int bad = 0;
+  auto report = [&](const char* what, int item, int k, long a, long b) {
+    if (bad++ < 12) fprintf(stderr, "[plan_check] %s item %d k %d: gpu %ld host %ld\n", what, item, k, a, b);
+  };
+  if ((int)ctx->h_items_x.size() != nx) report("n_items_x", -1, -1, nx, (long)ctx->h_items_x.size());
+  for (int i = 0; i < std::min(nx, (int)ctx->h_items_x.size()); ++i) {
+    const XRec& g = *reinterpret_cast<const XRec*>(&gx[(size_t)i * XB]);
+    const XRec& h = *reinterpret_cast<const XRec*>(&ctx->h_xblk[(size_t)i * XB]);
+    if (memcmp(&g, &h, sizeof(XRec)) != 0) {
+      report("XRec kind", i, 0, g.kind, h.kind);
+      report("XRec pulse/lrank", i, 0, g.pulse * 1000 + g.lrank, h.pulse * 1000 + h.lrank);
+      report("XRec n_units/begin", i, 0, (long)g.n_units * 100000 + g.begin, (long)h.n_units * 100000 + h.begin);
+      report("XRec cls/epoch", i, 0, (long)g.cls * 100000 + g.epoch, (long)h.cls * 100000 + h.epoch);
+      report("XRec dst", i, 0, (long)(uintptr_t)g.dst_x ^ (long)(uintptr_t)g.dst_ll, (long)(uintptr_t)h.dst_x ^ (long)(uintptr_t)h.dst_ll);
+      continue;
+    }
+    for (uint32_t e = 0; e < h.n_units / ctx->W && h.kind == kItemXSend; ++e) {
+      const XEnt& a = reinterpret_cast<const XEnt*>(&gx[(size_t)i * XB + 128])[e];
+      const XEnt& b = reinterpret_cast<const XEnt*>(&ctx->h_xblk[(size_t)i * XB + 128])[e];
+      if (memcmp(&a, &b, sizeof(XEnt)) != 0) report("XEnt row|l|kq|mask", i, (int)e,
+          ((long)a.row << 24) | (a.l << 16) | (a.kq << 8) | a.mask, ((long)b.row << 24) | (b.l << 16) | (b.kq << 8) | b.mask);
+    }
+  }
+  if ((int)ctx->h_items_f.size() != nf) report("n_items_f", -1, -1, nf, (long)ctx->h_items_f.size());
+  if (ctx->tree_rows != RT) report("tree_rows", -1, -1, RT, ctx->tree_rows);
+  for (int i = 0; i < std::min(nf, (int)ctx->h_items_f.size()) && ctx->tree_rows == RT; ++i) {
+    const GRec& g = *reinterpret_cast<const GRec*>(&gf[(size_t)i * FB]);
+    const GRec& h = *reinterpret_cast<const GRec*>(&ctx->h_fblk[(size_t)i * FB]);
+    if (g.kind != h.kind || g.level != h.level || g.lrank != h.lrank || g.n_roots != h.n_roots || g.n_units != h.n_units ||
+        g.epoch != h.epoch) {
+      report("GRec kind/level/lrank", i, 0, g.kind * 10000 + g.level * 1000 + g.lrank, h.kind * 10000 + h.level * 1000 + h.lrank);
+      report("GRec n_roots/n_units", i, 0, (long)g.n_roots * 100000 + g.n_units, (long)h.n_roots * 100000 + h.n_units);
+      continue;
+    }
+    for (uint32_t j = 0; j < h.n_roots; ++j) {
+      const TRoot& a = reinterpret_cast<const TRoot*>(&gf[(size_t)i * FB + 128])[j];
+      const TRoot& b = reinterpret_cast<const TRoot*>(&ctx->h_fblk[(size_t)i * FB + 128])[j];
+      if (a.push != b.push || a.par != b.par || a.q != b.q || a.nn != b.nn || a.llmask != b.llmask ||
+          a.stmask != b.stmask || a.post != b.post)
+        report("TRoot nn|par|post", i, (int)j, ((long)a.nn << 40) ^ ((long)a.par << 8) ^ a.post,
+               ((long)b.nn << 40) ^ ((long)b.par << 8) ^ b.post);
+      const uint32_t* ia = reinterpret_cast<const uint32_t*>(&gf[(size_t)i * FB + 128 + 32 * (size_t)RT]) + 8 * j;
+      const uint32_t* ib = reinterpret_cast<const uint32_t*>(&ctx->h_fblk[(size_t)i * FB + 128 + 32 * (size_t)RT]) + 8 * j;
+      for (int k = 0; k < b.nn; ++k)
+        if (ia[k] != ib[k]) report("TRoot il", i, (int)j * 8 + k, ia[k], ib[k]);
+    }
+  }
+  ctx->h_items_x.clear();
+  ctx->h_items_f.clear();
+  ctx->h_xblk.clear();
+  ctx->h_fblk.clear();
+  fprintf(stderr, "[plan_check] rank %d: %d mismatches (x items %d, f items %d)\n", ctx->first_rank, bad, nx, nf);
+  return bad ? fail(ctx, HALO_ERR_STATE, "GPU plan != host plan (HALO_PLAN_CHECK)") : HALO_OK;
+}
+
+static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer* prof) {
+  const int L = ctx->n_local, P = ctx->P, W = ctx->W, R = ctx->item_rows;
+  const size_t cap = (size_t)ctx->cfg.capacity;
+  if (!ctx->d_pl) {
+    CK(cudaMalloc(&ctx->d_pl, sizeof(PlanDev)));
+    CK(cudaMallocHost(&ctx->h_pl, sizeof(PlanDev)));
+    CK(cudaMallocHost(&ctx->h_pl_cnt, sizeof(int32_t) * (kMaxP + 1) * (kMaxP + 1) * kMaxLocal));
+  }
+  const size_t so = align_up(sizeof(uint64_t) * L * cap, 256), sc = align_up(sizeof(int32_t) * L * cap * P, 256),
+               sr = align_up(L * cap, 256), sk = align_up(sizeof(int32_t) * L * cap, 256),
+               sx = align_up(sizeof(int32_t) * (P * L + L) * (P + 1), 256);
+  const size_t sbytes = so + sc + sr + sk + sx;
+  if (sbytes > ctx->pl_scratch_bytes) {
+    if (ctx->d_pl_scratch) CK(cudaFree(ctx->d_pl_scratch));
+    ctx->d_pl_scratch = nullptr;
+    CK(cudaMalloc(&ctx->d_pl_scratch, sbytes));
+    ctx->pl_scratch_bytes = sbytes;
+  }
+  PlanDev& H = *ctx->h_pl;
+  memset(&H, 0, sizeof H);
+  H.L = L;
+  H.P = P;
+  H.W = W;
+  H.R = R;
+  H.cap = (int)cap;
+  H.map_stride = (int)ctx->map_stride;
+  H.epoch = ctx->epoch;
+  H.XB = ll_xblk_bytes(R);
+  for (int q = 0; q < P; ++q) {
+    H.shiftL[q] = ctx->cfg.box[ctx->pdim[q]];
+    H.pdim[q] = (uint8_t)ctx->pdim[q];
+  }
+  int max_rows = 1;
+  for (int l = 0; l < L; ++l) {
+    const int r = ctx->first_rank + l;
+    H.n_home[l] = ctx->n_home[l];
+    H.n_total[l] = ctx->n_total[l];
+    max_rows = std::max(max_rows, ctx->n_total[l]);
+    H.maps[l] = ctx->maps_of_local(l);
+    FsSet fs;
+    if (!rank_tree_fs(ctx, r, -1, fs)) return HALO_ERR_UNSUPPORTED;  // host builder
+    H.n_buckets[l] = (uint8_t)fs.n;
+    for (int b = 0; b < fs.n; ++b) H.bucket_fs[l][b] = fs.v[b];
+    for (int q = 0; q < P; ++q) {
+      const int i = l * P + q, d = ctx->pdim[q];
+      const int rcv = ctx->neighbour(r, d, -1), snd = ctx->neighbour(r, d, +1);  // coordinates go down (R1)
+      PlanLQ& a = H.lq[l][q];
+      a.rcv_l = same_group(ctx, r, rcv) ? rcv - ctx->first_rank : -1;
+      a.snd_l = same_group(ctx, r, snd) ? snd - ctx->first_rank : -1;
+      a.dst_x = a.rcv_l >= 0 ? ctx->x[a.rcv_l] + (size_t)ctx->remote_off[i] * W : nullptr;
+      a.dst_ll = a.rcv_l >= 0 ? nullptr : ctx->xll_of(rcv) + (size_t)q * ctx->ll_stride;
+      a.push = a.snd_l >= 0 ? nullptr : ctx->fll_of(snd) + (size_t)q * ctx->ll_stride;
+      a.remote_off = ctx->remote_off[i];
+      a.atom_offset = ctx->atom_offset[i];
+      a.send_size = ctx->send_size[i];
+      a.recv_size = ctx->recv_size[i];
+      a.wraps = ctx->cell(r, d) == 0;  // the wrapping sender adds +L_d (R25)
+      a.efs = a.wraps ? (uint8_t)(3 * l + d) : (uint8_t)0xff;
+    }
+  }
+  char* sp = ctx->d_pl_scratch;
+  H.org = reinterpret_cast<uint64_t*>(sp);
+  H.child = reinterpret_cast<int32_t*>(sp + so);
+  H.rcls = reinterpret_cast<uint8_t*>(sp + so + sc);
+  H.rrank = reinterpret_cast<int32_t*>(sp + so + sc + sr);
+  H.xcnt = reinterpret_cast<int32_t*>(sp + so + sc + sr + sk);
+  H.rcnt = H.xcnt + (size_t)P * L * (P + 1);
+  CK(cudaMemcpyAsync(ctx->d_pl, &H, sizeof(PlanDev), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(H.child, 0xff, sizeof(int32_t) * L * cap * P, st));
+  CK(launch_plan_count(ctx->d_pl, L, P, max_rows, st));
+  const size_t ncnt = (size_t)(P * L + L) * (P + 1);
+  CK(cudaMemcpyAsync(ctx->h_pl_cnt, H.xcnt, sizeof(int32_t) * ncnt, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (prof) prof->lap("plan:count");
+  const int32_t* xc = ctx->h_pl_cnt;
+  const int32_t* rc = ctx->h_pl_cnt + (size_t)P * L * (P + 1);
+  // x items: class-major (a wait only targets a lower class: deadlock-free static
+  // order), then pulse, then local rank; the receives last
+  int nx = 0;
+  for (int c = 0; c <= P; ++c)
+    for (int p = 0; p < P; ++p)
+      for (int l = 0; l < L; ++l) {
+        H.xoff[c][p][l] = nx;
+        nx += xc[((size_t)p * L + l) * (P + 1) + c];
+      }
+  std::vector<XRec> recv;
+  for (int p = 0; p < P; ++p)
+    for (int l = 0; l < L; ++l) {
+      const int r = ctx->first_rank + l;
+      if (same_group(ctx, r, ctx->neighbour(r, ctx->pdim[p], +1))) continue;
+      const int n = ctx->recv_size[l * P + p];
+      const int RR = std::min(kMaxItemRows, ctx->recv_mult * R);
+      for (int b = 0; b < n; b += RR) {
+        XRec x;
+        memset(&x, 0, sizeof x);
+        x.kind = kItemXRecv;
+        x.pulse = (uint8_t)p;
+        x.lrank = (uint16_t)l;
+        x.n_units = (uint32_t)(std::min(n, b + RR) - b) * W;
+        x.begin = (uint32_t)b;
+        x.cls = 0xff;
+        x.ll = ctx->xll_of(r) + (size_t)p * ctx->ll_stride + (size_t)b * W;
+        x.xdst = ctx->x[l] + (size_t)(ctx->atom_offset[l * P + p] + b) * W;
+        x.epoch = ctx->epoch;
+        recv.push_back(x);
+      }
+    }
+  const int n_send = nx;
+  nx += (int)recv.size();
+  // f items: roots per item (RT) the smallest size whose items all fit the co-resident
+  // grid (one item per CTA), else kTreeRowsOcc; class-major, then local rank
+  auto f_items = [&](int RT) {
+    int n = 0;
+    for (int c = 0; c <= P; ++c)
+      for (int l = 0; l < L; ++l) n += (rc[l * (P + 1) + c] + RT - 1) / RT;
+    return n;
+  };
+  int RT = 32;
+  while (f_items(RT) > ctx->cap_f() && RT < kTreeRowsOcc) RT = std::min(kTreeRowsOcc, RT + 16);
+  if (const char* e = getenv("HALO_TREE_ROWS")) RT = std::min(kTreeRowsOcc, std::max(8, atoi(e)));
+  int nf = 0;
+  for (int c = 0; c <= P; ++c)
+    for (int l = 0; l < L; ++l) {
+      H.foff[c][l] = nf;
+      H.fcnt[c][l] = rc[l * (P + 1) + c];
+      nf += (H.fcnt[c][l] + RT - 1) / RT;
+    }
+  ctx->tree_rows = RT;
+  H.RT = RT;
+  H.FB = ll_fblk_bytes(RT);
+  ctx->h_items_x.clear();
+  ctx->h_items_f.clear();
+  ctx->h_xblk.clear();
+  ctx->h_fblk.clear();
+  ctx->gpu_n_items_x = nx;
+  ctx->gpu_n_items_f = nf;
+  ctx->gpu_xblk_bytes = std::max<size_t>(1, (size_t)nx * H.XB);
+  ctx->gpu_fblk_bytes = std::max<size_t>(1, (size_t)nf * H.FB);
+  fill_rank_dev(ctx);
+  halo_status s = upload_plan(ctx);
+  if (s != HALO_OK) return s;
+  H.xblk = ctx->d_xblk;
+  H.fblk = ctx->d_fblk;
+  CK(cudaMemcpyAsync(ctx->d_pl, &H, sizeof(PlanDev), cudaMemcpyHostToDevice, st));
+  if (!recv.empty()) {  // the receive items' records (no entries): straight from pinned memory
+    if (ctx->h_recv_cap < recv.size()) {
+      if (ctx->h_recv) CK(cudaFreeHost(ctx->h_recv));
+      ctx->h_recv = nullptr;
+      CK(cudaMallocHost(&ctx->h_recv, sizeof(XRec) * recv.size()));
+      ctx->h_recv_cap = recv.size();
+    }
+    memcpy(ctx->h_recv, recv.data(), sizeof(XRec) * recv.size());
+    CK(cudaMemcpy2DAsync(ctx->d_xblk + (size_t)n_send * H.XB, H.XB, ctx->h_recv, sizeof(XRec), sizeof(XRec),
+                         recv.size(), cudaMemcpyHostToDevice, st));
+  }
+  CK(launch_plan_write(ctx->d_pl, L, P, max_rows, st));
+  ctx->n_tail_f = 0;
+  if (prof) prof->lap("plan:write");
+  if (getenv("HALO_PLAN_CHECK")) return plan_check(ctx, st);
+  return HALO_OK;
+}
+
+// Plan layout: RankDev | PulseDev | x items | f items | LocalBase | x item blocks | f
+// item blocks.  Host-built plans (h_xblk / h_fblk) go up in one DMA from a pinned
+// image; a GPU-built plan (gpu_xblk_bytes > 0, kernels_plan.cu) uploads only the head
+// and leaves the block areas to the kernels.
 static halo_status upload_plan(halo_ctx* ctx) {
   const size_t a = 256;
+  const bool gpu = ctx->gpu_xblk_bytes > 0;
   const size_t nr = align_up(sizeof(RankDev) * ctx->n_local, a);
   const size_t np = align_up(sizeof(PulseDev) * std::max(1, ctx->n_local * ctx->P), a);
   const size_t nx = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_x.size()), a);
   const size_t nf = align_up(sizeof(Item) * std::max<size_t>(1, ctx->h_items_f.size()), a);
-  const size_t nxr = align_up(std::max<size_t>(1, ctx->h_xblk.size()), a);
-  const size_t ngr = align_up(std::max<size_t>(1, ctx->h_fblk.size()), a);
   const size_t nlb = align_up(sizeof(LocalBase) * std::max<size_t>(1, ctx->h_lbase.size()), a);
-  const size_t need = nr + np + nx + nf + nxr + ngr + nlb;
+  const size_t nxr = align_up(std::max<size_t>(1, gpu ? ctx->gpu_xblk_bytes : ctx->h_xblk.size()), a);
+  const size_t ngr = align_up(std::max<size_t>(1, gpu ? ctx->gpu_fblk_bytes : ctx->h_fblk.size()), a);
+  const size_t need = nr + np + nx + nf + nlb + nxr + ngr;
   if (need > ctx->plan_bytes) {  // 25% headroom: NS steps rarely grow the plan again
-    if (ctx->plan) CK(cudaFree(ctx->plan));
+    if (ctx->plan && ctx->captured) {
+      // a captured graph may still reference the old plan: keep it mapped, with every
+      // record's epoch zeroed (a replay then refuses every item, HALO_ERR_STATE)
+      CK(cudaMemset(ctx->plan, 0, ctx->plan_bytes));
+      ctx->retired.push_back(ctx->plan);
+    } else if (ctx->plan) {
+      CK(cudaFree(ctx->plan));
+    }
     ctx->plan = nullptr;
     CK(cudaMalloc(&ctx->plan, need + need / 4));
     ctx->plan_bytes = need + need / 4;
   }
-  if (need > ctx->h_pin_bytes) {
+  const size_t img_need = gpu ? nr + np + nx + nf + nlb : need;
+  if (img_need > ctx->h_pin_bytes) {
     if (ctx->h_pin) CK(cudaFreeHost(ctx->h_pin));
     ctx->h_pin = nullptr;
-    CK(cudaMallocHost(&ctx->h_pin, need + need / 4));
-    ctx->h_pin_bytes = need + need / 4;
+    CK(cudaMallocHost(&ctx->h_pin, img_need + img_need / 4));
+    ctx->h_pin_bytes = img_need + img_need / 4;
   }
   ctx->d_ranks = reinterpret_cast<RankDev*>(ctx->plan);
   ctx->d_pulses = reinterpret_cast<PulseDev*>(ctx->plan + nr);
   ctx->d_items_x = reinterpret_cast<Item*>(ctx->plan + nr + np);
   ctx->d_items_f = reinterpret_cast<Item*>(ctx->plan + nr + np + nx);
-  ctx->d_xblk = ctx->plan + nr + np + nx + nf;
-  ctx->d_fblk = ctx->plan + nr + np + nx + nf + nxr;
-  ctx->d_lbase = reinterpret_cast<LocalBase*>(ctx->plan + nr + np + nx + nf + nxr + ngr);
-  // the whole plan image in pinned memory, then one synchronous DMA (pageable
-  // copies of the MB-sized item blocks cost ms at the NS step)
+  ctx->d_lbase = reinterpret_cast<LocalBase*>(ctx->plan + nr + np + nx + nf);
+  ctx->d_xblk = ctx->plan + nr + np + nx + nf + nlb;
+  ctx->d_fblk = ctx->plan + nr + np + nx + nf + nlb + nxr;
+  // the plan image in pinned memory, then one synchronous DMA (pageable copies of
+  // the MB-sized item blocks cost ms at the NS step)
   char* img = ctx->h_pin;
   auto put = [&](char* dev, const void* src, size_t n) {
     if (n) memcpy(img + (dev - ctx->plan), src, n);
@@ -1161,13 +1536,17 @@ static halo_status upload_plan(halo_ctx* ctx) {
     put(reinterpret_cast<char*>(ctx->d_pulses), ctx->h_pulses.data(), sizeof(PulseDev) * ctx->n_local * ctx->P);
   put(reinterpret_cast<char*>(ctx->d_items_x), ctx->h_items_x.data(), sizeof(Item) * ctx->h_items_x.size());
   put(reinterpret_cast<char*>(ctx->d_items_f), ctx->h_items_f.data(), sizeof(Item) * ctx->h_items_f.size());
-  put(ctx->d_xblk, ctx->h_xblk.data(), ctx->h_xblk.size());
-  put(ctx->d_fblk, ctx->h_fblk.data(), ctx->h_fblk.size());
   put(reinterpret_cast<char*>(ctx->d_lbase), ctx->h_lbase.data(), sizeof(LocalBase) * ctx->h_lbase.size());
-  const size_t used = (size_t)(reinterpret_cast<char*>(ctx->d_lbase) - ctx->plan) + sizeof(LocalBase) * ctx->h_lbase.size();
+  size_t used = (size_t)(reinterpret_cast<char*>(ctx->d_lbase) - ctx->plan) + sizeof(LocalBase) * ctx->h_lbase.size();
+  if (!gpu) {
+    put(ctx->d_xblk, ctx->h_xblk.data(), ctx->h_xblk.size());
+    put(ctx->d_fblk, ctx->h_fblk.data(), ctx->h_fblk.size());
+    if (!ctx->h_fblk.empty()) used = (size_t)(ctx->d_fblk - ctx->plan) + ctx->h_fblk.size();
+    else if (!ctx->h_xblk.empty()) used = (size_t)(ctx->d_xblk - ctx->plan) + ctx->h_xblk.size();
+  }
   CK(cudaMemcpy(ctx->plan, img, used, cudaMemcpyHostToDevice));
-  ctx->n_items_x = (int)ctx->h_items_x.size();
-  ctx->n_items_f = (int)ctx->h_items_f.size();
+  ctx->n_items_x = gpu ? ctx->gpu_n_items_x : (int)ctx->h_items_x.size();
+  ctx->n_items_f = gpu ? ctx->gpu_n_items_f : (int)ctx->h_items_f.size();
   return HALO_OK;
 }
 
@@ -1181,7 +1560,7 @@ static uint64_t next_seq(halo_ctx* ctx, cudaStream_t st, uint64_t* host) {
     ctx->captured = true;
   }
   if (cs != cudaStreamCaptureStatusNone) ctx->captured = true;
-  ++*host;
+  *host = ll_seq_next(*host);
   return ctx->captured ? 0 : *host;
 }
 
@@ -1213,6 +1592,7 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.delay_rank = ctx->P ? ctx->neighbour(0, ctx->pdim[0], +1) : -1;
   P.seq_x0 = ctx->seq_x0;
   P.lbase = ctx->d_lbase;
+  P.plan_epoch = ctx->epoch;
   return P;
 }
 
@@ -1381,22 +1761,6 @@ static halo_status ce_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, 
 
 // Shared driver of halo_set_maps / halo_set_maps_explicit.
 // HALO_PROFILE=1: host wall time of the set_maps phases on stderr (NS-step cost study).
-struct PhaseTimer {
-  bool on = getenv("HALO_PROFILE") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  std::string acc;
-  void lap(const char* name) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    char buf[96];
-    snprintf(buf, sizeof buf, " %s=%.0f", name, std::chrono::duration<double, std::micro>(now - t).count());
-    acc += buf;
-    t = now;
-  }
-  void print(int rank) const {
-    if (on) fprintf(stderr, "[halo_profile rank %d set_maps us]%s\n", rank, acc.c_str());
-  }
-};
 
 static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* send_sizes, const int* const* maps,
                                  cudaStream_t st) {
@@ -1447,20 +1811,39 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     for (int l = 0; l < L; ++l) ctx->n_total[l] = nt[l];
   }
   ctx->n_home.assign(ctx->n_total.begin(), ctx->n_total.end());
+  // LL areas zeroed every NS epoch (ll_seq_next): no peer writes them before the
+  // pulse-0 handshake below, which this stream reaches only after the memset
+  if (ctx->ll || ctx->auto_tr)
+    for (int l = 0; l < L; ++l)
+      CK(cudaMemsetAsync(ctx->xll_of(ctx->first_rank + l), 0, sizeof(uint64_t) * 2 * (size_t)P * ctx->ll_stride, st));
   fill_rank_dev(ctx);
   // ranks/pulse tables are needed by the select/depmask kernels already
   ctx->h_items_x.clear();
   ctx->h_items_f.clear();
   ctx->h_fblk.clear();  // the last epoch's force blocks: not re-uploaded with every pulse's x plan
   ctx->h_xblk.clear();
+  ctx->gpu_xblk_bytes = ctx->gpu_fblk_bytes = 0;
   if ((s = upload_plan(ctx)) != HALO_OK) return s;
 
   const uint64_t timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);
-  std::vector<int> dim_start(L, 0);
+  // static planes of the GPU map builder (R2, R3): b_d[c_d] of every dim, and b_d[c_d + 1]
+  char* sm = ctx->d_small;
+  if (!maps) {
+    std::vector<double> blo(3 * L), bhi(3 * L);
+    for (int l = 0; l < L; ++l)
+      for (int dd = 0; dd < 3; ++dd) {
+        blo[3 * l + dd] = ctx->plane(dd, ctx->cell(ctx->first_rank + l, dd));
+        bhi[3 * l + dd] = ctx->plane(dd, ctx->cell(ctx->first_rank + l, dd) + 1);
+      }
+    CK(cudaMemcpyAsync(sm + 4096, blo.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(sm + 8192, bhi.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
+  }
+  // Per pulse, all stream-ordered on the device (no host round trip): select (fp64
+  // predicate + compaction) -> handshake (sizes / offsets with the neighbours) ->
+  // dependency masks -> the pulse's coordinate exchange (pulse p+1 selects among
+  // and forwards these rows).  The explicit-map test entry validates on the host.
   for (int p = 0; p < P; ++p) {
     const int d = ctx->pdim[p], k = ctx->pk[p];
-    if (k == 0)
-      for (int l = 0; l < L; ++l) dim_start[l] = ctx->n_total[l];
     if (maps) {
       // explicit maps (test entry): validate on the host and upload
       int errs_now = 0;
@@ -1485,38 +1868,15 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
         }
       }
     } else {
-      // GPU map builder: candidate ranges and planes (R2, R3)
-      char* sm = ctx->d_small;
-      std::vector<int32_t> cand(2 * L);
-      std::vector<double> blo(L), hlo(3 * L), hhi(3 * L);
-      for (int l = 0; l < L; ++l) {
-        const int r = ctx->first_rank + l;
-        if (k == 0) {
-          cand[2 * l] = 0;
-          cand[2 * l + 1] = dim_start[l];
-        } else {
-          const int q = l * P + (p - 1);
-          cand[2 * l] = ctx->atom_offset[q];
-          cand[2 * l + 1] = ctx->atom_offset[q] + ctx->recv_size[q];
-        }
-        blo[l] = ctx->plane(d, ctx->cell(r, d));
-        for (int dd = 0; dd < 3; ++dd) {
-          hlo[3 * l + dd] = ctx->plane(dd, ctx->cell(r, dd));
-          hhi[3 * l + dd] = ctx->plane(dd, ctx->cell(r, dd) + 1);
-        }
-      }
-      CK(cudaMemcpyAsync(sm, cand.data(), sizeof(int32_t) * 2 * L, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(sm + 2048, blo.data(), sizeof(double) * L, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(sm + 4096, hlo.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(sm + 8192, hhi.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
       SelParams S{};
       S.ranks = ctx->d_ranks;
       S.ctrl = ctx->ctrl;
       S.p = p;
       S.dim = d;
       S.rc = (double)ctx->cfg.cutoff;
-      S.cand = reinterpret_cast<const int32_t*>(sm);
-      S.b_lo = reinterpret_cast<const double*>(sm + 2048);
+      S.cand = nullptr;  // from the device-side handshake results
+      S.kfirst = k == 0;
+      S.b_lo = reinterpret_cast<const double*>(sm + 4096);  // [n_local][3]: b_d[c_d]
       const bool check = (p == 0) && !(ctx->cfg.flags & HALO_F_NO_HOME_CHECK);
       S.home_lo = check ? reinterpret_cast<const double*>(sm + 4096) : nullptr;
       S.home_hi = check ? reinterpret_cast<const double*>(sm + 8192) : nullptr;
@@ -1525,9 +1885,16 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
       S.decomposed_mask = (ctx->cfg.grid[0] > 1) | ((ctx->cfg.grid[1] > 1) << 1) | ((ctx->cfg.grid[2] > 1) << 2);
       S.map_stride = (int)ctx->map_stride;
       S.layout = W;
+      S.epoch = ctx->epoch;
+      S.err_host = ctx->err_dev;
+      S.timeout_ns = timeout_ns;
+      for (int l = 0; l < L; ++l) {
+        const int r = ctx->first_rank + l;
+        for (int q = 0; q < p; ++q)
+          if (!ctx->is_local(ctx->neighbour(r, ctx->pdim[q], +1))) S.wait_mask[l] |= 1u << q;
+      }
       CK(launch_select(S, L, st));
     }
-    prof.lap("select");
     // handshake with the neighbours (device flags)
     HsParams H{};
     H.ctrl = ctx->ctrl;
@@ -1545,32 +1912,51 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     }
     CK(launch_handshake(H, st));
     CK(launch_depmask(ctx->d_ranks, ctx->ctrl, p, (int)ctx->map_stride, L, st));
-    if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
-    if ((s = check_err_word(ctx)) != HALO_OK) return s;
-    if ((s = pull_maps(ctx, p, st)) != HALO_OK) return s;
-    prof.lap("handshake+pull");
-    // exchange the coordinates of this pulse now: pulse p+1 forwards them
-    for (int l = 0; l < L; ++l)
-      for (int q = 0; q <= p; ++q) fill_pulse_dev(ctx, l, q);
-    fill_rank_dev(ctx);
-    if (ctx->ll) {
-      fill_lbase(ctx);
-      build_ll_x(ctx, p, p + 1);
-    } else {
-      build_x_items(ctx, p, p + 1);
+    if (maps) {  // the next pulse's host validation needs n_total
+      if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
+      if ((s = check_err_word(ctx)) != HALO_OK) return s;
     }
-    if ((s = upload_plan(ctx)) != HALO_OK) return s;
-    ExParams X = make_params(ctx, ctx->d_items_x, ctx->n_items_x, p, p + 1);
-    if (ctx->ll) {
-      X.seq = next_seq(ctx, st, &ctx->seq_host_x);
-      X.n_items_x = ctx->n_items_x;
-      CK(launch_exchange_ll(X, 0, W, grid_for(ctx->n_items_x, L, ctx->cap_x()), ctx->wide(), nullptr, st));
+    // this pulse's coordinates now: pulse p+1 selects among and forwards them
+    NsXParams NX{};
+    NX.ranks = ctx->d_ranks;
+    NX.ctrl = ctx->ctrl;
+    NX.p = p;
+    NX.dim = d;
+    NX.map_stride = (int)ctx->map_stride;
+    NX.n_local = L;
+    NX.epoch = ctx->epoch;
+    for (int l = 0; l < L; ++l) {
+      const int r = ctx->first_rank + l, lower = ctx->neighbour(r, d, -1);  // coordinates go down (R1)
+      NX.dst_x[l] = ctx->peer_x[lower];
+      NX.flag_dst[l] = ctx->is_local(lower) ? nullptr : &ctx->hdr_of(lower)->ns_x[p];
+      NX.has_shift[l] = ctx->cell(r, d) == 0;  // the wrapping sender adds +L_d (R25)
+      NX.shift[l] = ctx->cfg.box[d];
+      for (int q = 0; q < p; ++q)
+        if (!ctx->is_local(ctx->neighbour(r, ctx->pdim[q], +1))) NX.wait_mask[l] |= 1u << q;
     }
-    if (!ctx->ll)
-      CK(launch_exchange_x(X, W, grid_for(ctx->n_items_x, L, ctx->max_x), st));
-    CK(cudaStreamSynchronize(st));
-    if ((s = check_err_word(ctx)) != HALO_OK) return s;
+    NX.err_host = ctx->err_dev;
+    NX.timeout_ns = timeout_ns;
+    CK(launch_ns_x(NX, W, ctx->cfg.capacity, st));
+    prof.lap("pulse");
   }
+  {  // rows from other processes: in x before set_maps returns (the caller may read them)
+    NsWaitParams NW{};
+    NW.n_local = L;
+    NW.epoch = ctx->epoch;
+    NW.err_host = ctx->err_dev;
+    NW.timeout_ns = timeout_ns;
+    bool any = false;
+    for (int l = 0; l < L; ++l) {
+      const int r = ctx->first_rank + l;
+      NW.own[l] = ctx->hdr_of(r);
+      for (int q = 0; q < P; ++q)
+        if (!ctx->is_local(ctx->neighbour(r, ctx->pdim[q], +1))) NW.mask[l] |= 1u << q;
+      any |= NW.mask[l] != 0;
+    }
+    if (any) CK(launch_ns_wait(NW, st));
+  }
+  if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
+  if ((s = check_err_word(ctx)) != HALO_OK) return s;
   prof.lap("x_pulses");
   {
     // votes that ride on the status exchange (OR over all ranks), so that every
@@ -1637,21 +2023,36 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   // final plan: all pulses
   for (int l = 0; l < L; ++l)
     for (int p = 0; p < P; ++p) fill_pulse_dev(ctx, l, p);
+  bool gpu_built = false;
+  ctx->gpu_xblk_bytes = ctx->gpu_fblk_bytes = 0;
   if (ctx->ll) {
     fill_lbase(ctx);
-    build_ll_x(ctx, 0, P);
-    prof.lap("x plan");
-    if ((s = build_ll_f(ctx)) != HALO_OK) return s;
-    prof.lap("f plan");
-  } else {
-    ctx->h_xblk.clear();
-    ctx->h_fblk.clear();
-    build_x_items(ctx, 0, P);
-    build_f_items(ctx);
+    if (ctx->gpu_plan && P <= 3) {  // the plan built on the device from the device-resident maps
+      s = build_ll_plan_gpu(ctx, st, &prof);
+      if (s == HALO_OK) gpu_built = true;
+      else if (s != HALO_ERR_UNSUPPORTED) return s;
+      else ctx->gpu_xblk_bytes = ctx->gpu_fblk_bytes = 0;
+    }
   }
-  fill_rank_dev(ctx);
-  if ((s = upload_plan(ctx)) != HALO_OK) return s;
-  prof.lap("upload");
+  if (!gpu_built) {  // host builders: every map on the host
+    for (int p = 0; p < P; ++p)
+      if ((s = pull_maps(ctx, p, st)) != HALO_OK) return s;
+    prof.lap("pull maps");
+    if (ctx->ll) {
+      build_ll_x(ctx, 0, P);
+      prof.lap("x plan");
+      if ((s = build_ll_f(ctx, &prof)) != HALO_OK) return s;
+      prof.lap("f plan");
+    } else {
+      ctx->h_xblk.clear();
+      ctx->h_fblk.clear();
+      build_x_items(ctx, 0, P);
+      build_f_items(ctx);
+    }
+    fill_rank_dev(ctx);
+    if ((s = upload_plan(ctx)) != HALO_OK) return s;
+    prof.lap("upload");
+  }
   if (ctx->ce && (s = build_ce(ctx)) != HALO_OK) return s;
   ctx->l2win = cudaAccessPolicyWindow{};
   if ((ctx->cfg.flags & HALO_F_L2_PERSIST) && ctx->ll) {
@@ -1721,6 +2122,8 @@ halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gi
   ctx->x_done = false;
   ctx->pme_ready = false;
   ctx->epoch++;
+  // the home rows move: a graph captured with the current plan must not run it again
+  if (ctx->captured && ctx->plan) CK(cudaMemsetAsync(ctx->plan, 0, ctx->plan_bytes, st));
   // stencil of every local rank: the distinct ranks of cells c + delta (R30)
   std::vector<MigRank> mr(L);
   for (int l = 0; l < L; ++l) {
@@ -2096,6 +2499,11 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   if (ctx->ll) {
     X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x);
     X.n_items_x = ctx->n_items_x;
+    if (ctx->prefetch) {  // the f launch's item blocks and the home x rows (L2 prefetch)
+      X.pf_f = ctx->d_fblk;
+      X.pf_f_bytes = (uint64_t)ctx->n_items_f * ll_fblk_bytes(ctx->tree_rows);
+      X.pf_x = 1;
+    }
     CK(launch_exchange_ll(X, 0, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
   }
   if (!ctx->ll)
@@ -2183,6 +2591,138 @@ halo_status halo_step_host(halo_ctx* ctx, const float* const* x_home, const floa
         CK(cudaMemcpyAsync(f_home_out[l], ctx->f[l], sizeof(float) * W * ctx->n_home[l], cudaMemcpyDeviceToHost, st));
   if (fshift_host)
     CK(cudaMemcpyAsync(fshift_host, ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return check_err_word(ctx);
+}
+
+// Packed host layout (halo_step_host_packed): in = [x home rows of local ranks 0..L-1 |
+// f rows [0, n_total) of local ranks 0..L-1]; out = [x halo rows of every local rank |
+// f home rows of every local rank | fshift, n_local*9 doubles, at an 8-B aligned offset].
+static void packed_sizes(const halo_ctx* ctx, size_t* in_b, size_t* out_b, size_t* fs_off) {
+  size_t xh = 0, fa = 0, xo = 0, fo = 0;
+  for (int l = 0; l < ctx->n_local; ++l) {
+    xh += ctx->n_home[l];
+    fa += ctx->n_total[l];
+    xo += ctx->n_total[l] - ctx->n_home[l];
+    fo += ctx->n_home[l];
+  }
+  const size_t rb = sizeof(float) * ctx->W;
+  *in_b = (xh + fa) * rb;
+  *fs_off = align_up((xo + fo) * rb, 8);
+  *out_b = *fs_off + sizeof(double) * 9 * ctx->n_local;
+}
+
+static halo_status packed_prepare(halo_ctx* ctx) {
+  size_t in_b, out_b, fs_off;
+  packed_sizes(ctx, &in_b, &out_b, &fs_off);
+  const int L = ctx->n_local;
+  if (in_b > ctx->pk_in_cap) {
+    if (ctx->d_pk_in) CK(cudaFree(ctx->d_pk_in));
+    ctx->d_pk_in = nullptr;
+    CK(cudaMalloc(&ctx->d_pk_in, in_b + in_b / 4));
+    ctx->pk_in_cap = in_b + in_b / 4;
+  }
+  if (out_b > ctx->pk_out_cap) {
+    if (ctx->d_pk_out) CK(cudaFree(ctx->d_pk_out));
+    ctx->d_pk_out = nullptr;
+    CK(cudaMalloc(&ctx->d_pk_out, out_b + out_b / 4));
+    ctx->pk_out_cap = out_b + out_b / 4;
+  }
+  if (!ctx->d_segs) CK(cudaMalloc(&ctx->d_segs, sizeof(SegCopy) * (4 * kMaxLocal + 1)));
+  if (!ctx->pk_h2d) {
+    CK(cudaStreamCreateWithFlags(&ctx->pk_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->pk_d2h, cudaStreamNonBlocking));
+    for (auto& e : ctx->pk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // segment tables: [0, L) x home in; [L, 2L) f in; [2L, 4L+1) out (x halo, f home, fshift)
+  std::vector<SegCopy> sg(4 * L + 1);
+  const size_t W = ctx->W;
+  size_t o = 0;
+  for (auto& m : ctx->pk_max_words) m = 0;
+  auto words = [](size_t b) { return b / 4; };
+  for (int l = 0; l < L; ++l) {
+    sg[l] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->d_pk_in + o), reinterpret_cast<uint32_t*>(ctx->x[l]),
+                    W * ctx->n_home[l]};
+    o += 4 * W * ctx->n_home[l];
+    ctx->pk_max_words[0] = std::max(ctx->pk_max_words[0], sg[l].words);
+  }
+  for (int l = 0; l < L; ++l) {
+    sg[L + l] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->d_pk_in + o), reinterpret_cast<uint32_t*>(ctx->f[l]),
+                        W * ctx->n_total[l]};
+    o += 4 * W * ctx->n_total[l];
+    ctx->pk_max_words[1] = std::max(ctx->pk_max_words[1], sg[L + l].words);
+  }
+  o = 0;
+  for (int l = 0; l < L; ++l) {
+    const size_t nh = ctx->n_total[l] - ctx->n_home[l];
+    sg[2 * L + l] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->x[l] + W * ctx->n_home[l]),
+                            reinterpret_cast<uint32_t*>(ctx->d_pk_out + o), W * nh};
+    o += 4 * W * nh;
+  }
+  for (int l = 0; l < L; ++l) {
+    sg[3 * L + l] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->f[l]), reinterpret_cast<uint32_t*>(ctx->d_pk_out + o),
+                            W * ctx->n_home[l]};
+    o += 4 * W * ctx->n_home[l];
+  }
+  sg[4 * L] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->d_fshift_tmp),
+                      reinterpret_cast<uint32_t*>(ctx->d_pk_out + fs_off), words(sizeof(double) * 9 * L)};
+  for (int k = 2 * L; k <= 4 * L; ++k) ctx->pk_max_words[2] = std::max(ctx->pk_max_words[2], sg[k].words);
+  CK(cudaMemcpy(ctx->d_segs, sg.data(), sizeof(SegCopy) * sg.size(), cudaMemcpyHostToDevice));
+  ctx->pk_epoch = ctx->epoch;
+  return HALO_OK;
+}
+
+halo_status halo_packed_sizes(const halo_ctx* ctx, size_t* in_bytes, size_t* out_bytes) {
+  if (!ctx || !in_bytes || !out_bytes) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return HALO_ERR_STATE;
+  size_t fs_off;
+  packed_sizes(ctx, in_bytes, out_bytes, &fs_off);
+  return HALO_OK;
+}
+
+halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_host, void* stream) {
+  if (!ctx || !in_host) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "step before set_maps");
+  halo_status s;
+  if (ctx->pk_epoch != ctx->epoch || !ctx->d_segs)
+    if ((s = packed_prepare(ctx)) != HALO_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int L = ctx->n_local;
+  size_t in_b, out_b, fs_off;
+  packed_sizes(ctx, &in_b, &out_b, &fs_off);
+  size_t bx = 0, bxo = 0;
+  for (int l = 0; l < L; ++l) {
+    bx += sizeof(float) * ctx->W * ctx->n_home[l];
+    bxo += sizeof(float) * ctx->W * (ctx->n_total[l] - ctx->n_home[l]);
+  }
+  const char* in = static_cast<const char*>(in_host);
+  char* out = static_cast<char*>(out_host);
+  // x home rows first; the forces follow on a side stream (PCIe H2D) while x is exchanged
+  CK(cudaMemcpyAsync(ctx->d_pk_in, in, bx, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(ctx->pk_ev[0], st));
+  CK(cudaStreamWaitEvent(ctx->pk_h2d, ctx->pk_ev[0], 0));
+  CK(cudaMemcpyAsync(ctx->d_pk_in + bx, in + bx, in_b - bx, cudaMemcpyHostToDevice, ctx->pk_h2d));
+  CK(cudaEventRecord(ctx->pk_ev[1], ctx->pk_h2d));
+  CK(launch_seg_copy(ctx->d_segs, L, ctx->pk_max_words[0], st));
+  if ((s = halo_exchange_x(ctx, stream)) != HALO_OK) return s;
+  // halo x rows -> staging (before exchange_f: a neighbour's next exchange_x may only
+  // overwrite them after our exchange_f, R17), downloaded on a side stream (PCIe D2H)
+  CK(launch_seg_copy(ctx->d_segs + 2 * L, L, ctx->pk_max_words[2], st));
+  CK(cudaEventRecord(ctx->pk_ev[2], st));
+  if (out) {
+    CK(cudaStreamWaitEvent(ctx->pk_d2h, ctx->pk_ev[2], 0));
+    CK(cudaMemcpyAsync(out, ctx->d_pk_out, bxo, cudaMemcpyDeviceToHost, ctx->pk_d2h));
+    CK(cudaEventRecord(ctx->pk_ev[3], ctx->pk_d2h));
+  }
+  CK(cudaStreamWaitEvent(st, ctx->pk_ev[1], 0));
+  CK(launch_seg_copy(ctx->d_segs + L, L, ctx->pk_max_words[1], st));
+  CK(cudaMemsetAsync(ctx->d_fshift_tmp, 0, sizeof(double) * 9 * L, st));
+  if ((s = halo_exchange_f(ctx, ctx->d_fshift_tmp, 1, stream)) != HALO_OK) return s;
+  if (out) {
+    CK(launch_seg_copy(ctx->d_segs + 3 * L, L + 1, ctx->pk_max_words[2], st));
+    CK(cudaMemcpyAsync(out + bxo, ctx->d_pk_out + bxo, out_b - bxo, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamWaitEvent(st, ctx->pk_ev[3], 0));
+  }
   CK(cudaStreamSynchronize(st));
   return check_err_word(ctx);
 }
@@ -2502,8 +3042,21 @@ halo_status halo_destroy(halo_ctx* ctx) {
   (void)cudaDeviceSynchronize();
   for (void* p : ctx->opened) (void)cudaIpcCloseMemHandle(p);
   if (ctx->plan) (void)cudaFree(ctx->plan);
+  for (char* r : ctx->retired) (void)cudaFree(r);
   if (ctx->ctrl) (void)cudaFree(ctx->ctrl);
   if (ctx->d_fshift_tmp) (void)cudaFree(ctx->d_fshift_tmp);
+  if (ctx->d_pk_in) (void)cudaFree(ctx->d_pk_in);
+  if (ctx->d_pk_out) (void)cudaFree(ctx->d_pk_out);
+  if (ctx->d_segs) (void)cudaFree(ctx->d_segs);
+  if (ctx->d_pl) (void)cudaFree(ctx->d_pl);
+  if (ctx->h_pl) (void)cudaFreeHost(ctx->h_pl);
+  if (ctx->h_pl_cnt) (void)cudaFreeHost(ctx->h_pl_cnt);
+  if (ctx->d_pl_scratch) (void)cudaFree(ctx->d_pl_scratch);
+  if (ctx->h_recv) (void)cudaFreeHost(ctx->h_recv);
+  for (auto e : ctx->pk_ev)
+    if (e) (void)cudaEventDestroy(e);
+  if (ctx->pk_h2d) (void)cudaStreamDestroy(ctx->pk_h2d);
+  if (ctx->pk_d2h) (void)cudaStreamDestroy(ctx->pk_d2h);
   if (ctx->d_small) (void)cudaFree(ctx->d_small);
   if (ctx->h_pin) (void)cudaFreeHost(ctx->h_pin);
   if (ctx->d_mig) (void)cudaFree(ctx->d_mig);

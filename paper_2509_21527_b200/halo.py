@@ -235,6 +235,15 @@ class Halo:
         self._ck(self.lib.halo_step_host(self.h, arr(x_home_ptrs), arr(f_all_ptrs), arr(x_halo_out_ptrs),
                                          arr(f_home_out_ptrs), c_void_p(fshift_ptr or None), c_void_p(stream)))
 
+    def packed_sizes(self):
+        """(in_bytes, out_bytes) of halo_step_host_packed's host blocks for the current maps."""
+        a, b = c_size_t(0), c_size_t(0)
+        self._ck(self.lib.halo_packed_sizes(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def step_host_packed(self, in_ptr, out_ptr=0, stream=0):
+        self._ck(self.lib.halo_step_host_packed(self.h, c_void_p(in_ptr), c_void_p(out_ptr or None), c_void_p(stream)))
+
     def pack_x_pulse(self, local, pulse, sendbuf_ptr, stream=0):
         self._ck(self.lib.halo_pack_x_pulse(self.h, int(local), int(pulse), c_void_p(sendbuf_ptr), c_void_p(stream)))
 

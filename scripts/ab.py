@@ -28,7 +28,7 @@ def run(lib, args, port):
             k, v = kv.split("=", 1)
             env[k] = v
     bench = [os.path.join(ROOT, "bench.py"), "--steps", str(args.steps), "--warmup", "20", "--config", args.config,
-             "--no-graph", "--no-cpu", "--no-nccl", "--no-floors", "--no-ns", "--proto", args.proto, *args.bench_args.split(), *[a for a in extra.split("+") if a]]
+             "--no-graph", "--no-cpu", "--no-nccl", "--no-floors", "--no-ns", "--no-e2e", "--proto", args.proto, *args.bench_args.split(), *[a for a in extra.split("+") if a]]
     if args.gpus > 1:
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr", "127.0.0.1", "--master-port", str(port), *bench, "--gpus", str(args.gpus)]

@@ -109,6 +109,10 @@ def main():
                         "f_start": q((tf[:, 0] - t0) / 1e3), "f_rec": q((tf[:, 1] - t0) / 1e3),
                         "f_done": q((tf[:, 2] - t0) / 1e3), "f_exit": q((tf[:, 3] - t0) / 1e3)})
         if os.environ.get("HALO_DEBUG") == "8192":  # kTraceDetail: stamps inside the first tree item
+            for nm, tr in (("x", tx), ("f", tf)):  # griddepcontrol.wait released / prologue done (slots 14, 15)
+                if (tr[:, 14] > 0).all():
+                    res[nm + "_wait_released"] = q((tr[:, 14] - t0) / 1e3)
+                    res[nm + "_prologue_done"] = q((tr[:, 15] - t0) / 1e3)
             tr = tf
             m = (tr[:, 10] > 0) & (tr[:, 13] >= tr[:, 10])
             if m.any():

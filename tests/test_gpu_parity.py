@@ -153,6 +153,70 @@ def test_cuda_graph_replay(proto):
     sess.destroy()
 
 
+@pytest.mark.parametrize("renew", ["set_maps", "migrate"])
+def test_stale_graph_replay_refused(renew):
+    """A graph captured before an NS step (set_maps / migrate) and replayed after it:
+    every item of the new plan carries the new epoch, so the replay touches nothing
+    and the next call reports HALO_ERR_STATE (ADVICE: captured launches freeze the plan)."""
+    from paper_2509_21527_b200.halo import HaloError
+    case = Case("T3D", seed=2, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess)
+    s = torch.cuda.Stream()
+    fshift = torch.zeros(sess.n_local, 3, 3, dtype=torch.float64, device=sess.device)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        sess.exchange_x(stream=s)
+        sess.exchange_f(fshift=fshift, stream=s)
+    g.replay()  # the current epoch: fine
+    torch.cuda.synchronize()
+    sess.halo.sync()
+    if renew == "set_maps":
+        sess.set_maps()
+    else:
+        gid = [torch.zeros(sess.capacity, dtype=torch.int32, device=sess.device) for _ in range(sess.n_local)]
+        for l in range(sess.n_local):
+            gid[l][: sess.n_home[l]] = torch.from_numpy(case.states[l].gid[: sess.n_home[l]].astype(np.int32))
+        sess.migrate(gid)
+    torch.cuda.synchronize()
+    for l in range(sess.n_local):
+        sess.x[l][sess.n_home[l]:] = float("nan")
+    g.replay()
+    torch.cuda.synchronize()
+    for l in range(sess.n_local):
+        assert torch.isnan(sess.x[l][sess.n_home[l]: sess.n_home[l] + 8]).all(), "a stale replay wrote x"
+    with pytest.raises(HaloError, match="HALO_ERR_STATE"):
+        sess.halo.sync()
+    del g
+    sess.halo.destroy()
+
+
+@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged")])
+@pytest.mark.parametrize("name", ["T3D", "T2P", "T4x2", "C2", "C5", "C3"])
+def test_gpu_plan_equals_host_plan(name, proto, monkeypatch):
+    """The LL plan built on the device (kernels_plan.cu) == the host builder's plan of the
+    same maps, item by item and field by field (HALO_PLAN_CHECK: set_maps fails on any
+    difference; the shift-force bucket numbering differs by design), and parity holds."""
+    monkeypatch.setenv("HALO_PLAN_CHECK", "1")
+    case = Case(name, seed=1, force_kind="normal")
+    sess = session_for(case, flags=proto)
+    run_gpu_case(case, sess)
+    sess.destroy()
+
+
+@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged")])
+@pytest.mark.parametrize("fused", [False, True])
+def test_ll_tag_wrap(proto, fused, monkeypatch):
+    """LL units carry the low 32 bits of the launch's sequence number: starting 3 below
+    2^32, the steps cross the wrap (tag 0 is skipped) and stay bit-exact."""
+    monkeypatch.setenv("HALO_SEQ_BASE", str((1 << 32) - 3))
+    case = Case("T3D", seed=1, force_kind="int")
+    sess = session_for(case, flags=proto)
+    run_gpu_case(case, sess, steps=6, fused=fused)
+    sess.destroy()
+
+
 def test_step_host_e2e():
     case = Case("C2", seed=1, force_kind="int")
     sess = session_for(case)
@@ -170,6 +234,42 @@ def test_step_host_e2e():
         np.testing.assert_array_equal(bits(xo[l].numpy()), bits(st.x[st.n_home:]))
         np.testing.assert_array_equal(bits(fo[l].numpy()), bits(case.Fo[l][: st.n_home]))
         np.testing.assert_array_equal(fs[l].numpy(), case.fshift[l])
+    sess.destroy()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "T2P"])
+def test_step_host_packed_e2e(cfg):
+    """halo_step_host_packed (one host block in, one out) == the oracle, twice in a row."""
+    case = Case(cfg, seed=2, force_kind="int")
+    sess = session_for(case)
+    run_gpu_case(case, sess, check_forces=False)
+    nl = sess.n_local
+    in_b, out_b = sess.halo.packed_sizes()
+    xs = [np.ascontiguousarray(case.home_rows(l)) for l in range(nl)]
+    fs_ = [case.F[l] for l in range(nl)]
+    blk = np.concatenate([a.reshape(-1) for a in xs] + [a.reshape(-1) for a in fs_]).astype(np.float32)
+    assert blk.nbytes == in_b
+    hin = torch.from_numpy(blk).pin_memory()
+    hout = torch.empty(out_b, dtype=torch.uint8).pin_memory()
+    for _ in range(2):
+        hout.fill_(0xFF)
+        sess.halo.step_host_packed(hin.data_ptr(), hout.data_ptr(), stream=torch.cuda.current_stream().cuda_stream)
+        raw = hout.numpy()
+        o = 0
+        for l in range(nl):
+            st = case.states[l]
+            n = (st.x.shape[0] - st.n_home) * st.x.shape[1] * 4
+            np.testing.assert_array_equal(raw[o:o + n].view(np.int32), bits(st.x[st.n_home:]).reshape(-1))
+            o += n
+        for l in range(nl):
+            st = case.states[l]
+            n = st.n_home * case.Fo[l].shape[1] * 4
+            np.testing.assert_array_equal(raw[o:o + n].view(np.int32), bits(case.Fo[l][: st.n_home]).reshape(-1))
+            o += n
+        o = (o + 7) // 8 * 8
+        fsh = raw[o:o + nl * 72].view(np.float64).reshape(nl, 3, 3)
+        for l in range(nl):
+            np.testing.assert_array_equal(fsh[l], case.fshift[l])
     sess.destroy()
 
 
