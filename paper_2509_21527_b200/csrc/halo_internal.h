@@ -434,7 +434,11 @@ struct PlanDev {
   uint64_t* org;            // x origin of every row: row | l << 24 | kq << 32 | mask << 40 | cls << 48
   int32_t* child;           // [L][cap][P]: entry of row t in map q, or -1
   uint8_t* rcls;            // tree class of a root row, 0xff = not a root
-  int32_t* rrank;           // rank of a root row among the roots of its (class, local rank)
+  uint8_t* rmask;           // its shift-force targets, a mask over bucket_fs[l]
+  uint32_t* imask;          // per f item: OR of its trees' masks (the item's buckets)
+  int32_t* bcnt;            // [L][nblk][P + 1] roots per class in each CTA's rows (k_plan_roots)
+  int32_t* boff;            // ... their exclusive prefix over the CTAs of a rank (k_plan_rank)
+  int nblk;                 // CTAs per local rank of the per-row kernels
   int32_t* xcnt;            // [P][L][P + 1] send items per class (counting pass)
   int32_t* rcnt;            // [L][P + 1] roots per class
   // second pass (after the counts): item offsets and the block areas
@@ -552,6 +556,13 @@ struct StatusParams {
   ScratchHdr* all[kMaxRanks];       // every rank's scratch header (local or peer-mapped)
   int* err_host;
   uint64_t timeout_ns;
+  // votes that ride on the exchange (computed on the device from this process's
+  // handshake results, identically in every CTA): the copy engine if some pulse sends
+  // >= ce_bytes (auto_tr), and the work-item size (kVoteRows << log2(R / 32))
+  int vote;                        // 0: no votes (halo_migrate, PME setup: errors only)
+  int P, W, auto_tr, rows_fixed;   // rows_fixed: R given (HALO_ITEM_ROWS), else 0
+  int64_t ctas;                    // co-resident CTAs the item size is chosen for
+  uint64_t ce_bytes;
 };
 
 // PP <-> PME redistribution (halo_pme_*, kernels_pme.cu)

@@ -622,7 +622,26 @@ __global__ void k_status(const __grid_constant__ StatusParams S) {
   __shared__ int s_or;
   if (threadIdx.x == 0) s_or = 0;
   __syncthreads();
-  const uint32_t mine = (uint32_t)S.ctrl->err[lr];
+  // votes (same value in every CTA): R = 64 rows (latency regime; swept 32-512 at C3)
+  // unless this process's pulses are so large that a CTA would run more than ~2 items
+  uint32_t vote = 0;
+  if (S.vote) {
+    long rows = 0;
+    uint64_t big = 0;
+    for (int l = 0; l < S.n_local; ++l)
+      for (int p = 0; p < S.P; ++p) {
+        rows += max(S.ctrl->send_size[l][p], S.ctrl->recv_size[l][p]);
+        big = max(big, (uint64_t)S.ctrl->send_size[l][p] * S.W * sizeof(float));
+      }
+    if (S.auto_tr && big >= S.ce_bytes) vote |= kVoteCE;
+    int R = S.rows_fixed;
+    if (!R) {
+      R = 64;
+      while (R < kMaxItemRows && rows / R > 2 * S.ctas) R *= 2;
+    }
+    vote |= (uint32_t)kVoteRows << (31 - __clz((unsigned)(R / kMinItemRows)));
+  }
+  const uint32_t mine = (uint32_t)S.ctrl->err[lr] | vote;
   for (int t = threadIdx.x; t < S.nranks; t += blockDim.x) st_release_sys(&S.all[t]->status[me], ep | mine);
   for (int t = threadIdx.x; t < S.nranks; t += blockDim.x) {
     const uint32_t v = wait_epoch(&S.own[lr]->status[t], S.epoch, S.timeout_ns, S.err_host, tcode(8, lr, 0));

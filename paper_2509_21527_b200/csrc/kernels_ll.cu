@@ -47,6 +47,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "halo_internal.h"
 #include "ptx.cuh"
 
@@ -111,12 +113,12 @@ __device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64
 // most one unit per thread), 4 for large items (bandwidth regime: every load of
 // a batch is issued before any store — the stores are asm volatile with a
 // memory clobber, so one unit at a time would serialise a memory latency each).
-template <int W, int kU>
+template <int W, int kU, bool kChk>
 __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const LocalBase* lb, const ExParams& P,
                                        uint32_t tag) {
   // a CUDA graph captured before the last NS step replays with this epoch: every item of
   // a replaced (or zeroed) plan carries another one and is treated as empty
-  const uint32_t n = r.epoch == P.plan_epoch ? r.n_units : stale_item(P);
+  const uint32_t n = !kChk || r.epoch == P.plan_epoch ? r.n_units : stale_item(P);
   const uint32_t B = blockDim.x;
   if (r.kind == kItemXRecv) {
     // this rank's halo rows of one pulse from another group: LL units -> x rows;
@@ -340,11 +342,11 @@ __device__ __noinline__ void tree_ll_nodes(const TRoot R, const uint32_t* il, co
 // is reached: stored (F nodes with children), added to its shift-force bucket,
 // then added into its parent.  A root whose parent is in another group pushes
 // its value there.  ~10 instructions per edge, none for absent nodes.
-template <int W>
+template <int W, bool kChk>
 __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, const uint4* nodes, const LocalBase* lb,
                                           const ExParams& P, uint32_t tag, double (*s_v)[kThreads],
                                           float (*s_val)[kThreads], uint64_t* tdet) {
-  const uint32_t n = g.epoch == P.plan_epoch ? g.n_units : stale_item(P);  // (as x_item)
+  const uint32_t n = !kChk || g.epoch == P.plan_epoch ? g.n_units : stale_item(P);  // (as x_item)
   const uint32_t S = (blockDim.x / W) * W;  // stride: a multiple of W, every thread keeps one component
   const int c = (int)(threadIdx.x % W);
   const int tid = threadIdx.x;
@@ -390,11 +392,11 @@ __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, con
 }
 
 // One large-tree item (kItemTreeG): the generic fold, one (root, component) per thread.
-template <int W>
+template <int W, bool kChk>
 __device__ __noinline__ void tree_item_generic(const GRec& g, const TRootG* roots, const TNode* nodes,
                                                   const LocalBase* lb, const ExParams& P, uint32_t tag,
                                                   double (*s_v)[kThreads]) {
-  const uint32_t n = g.epoch == P.plan_epoch ? g.n_units : stale_item(P);  // (as x_item)
+  const uint32_t n = !kChk || g.epoch == P.plan_epoch ? g.n_units : stale_item(P);  // (as x_item)
   const uint32_t S = (blockDim.x / W) * W;
   const int c = (int)(threadIdx.x % W);
   const bool fs_on = P.fshift != nullptr && n > 0;
@@ -462,7 +464,10 @@ __host__ __device__ constexpr int ll_threads() {
   return kMode != 0 ? kThreads : kU == 2 ? kThreadsXNarrow : kU == 3 ? 64 : kThreads;
 }
 
-template <int W, int kU, int kMode>
+// kChk: the launch is being captured into a CUDA graph, whose replays may outlive the
+// plan (the next NS step): every item's epoch is checked.  Eager launches take their
+// parameters from the current plan and skip the check (measured: ~0.2 us per step).
+template <int W, int kU, int kMode, bool kChk>
 __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 : 4) k_exchange_ll(
     const __grid_constant__ ExParams P) {
   extern __shared__ __align__(128) unsigned char s_blk[];
@@ -502,9 +507,13 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 :
   }
   for (int t = threadIdx.x; t < P.n_local * 4; t += blockDim.x)
     reinterpret_cast<int4*>(s_lb)[t] = __ldg(reinterpret_cast<const int4*>(P.lbase) + t);
+#ifdef HALO_EXP_PREFETCH  // measured slower; the call site alone costs ~0.2 us
   if (kMode == kModeX && (P.pf_f_bytes | (uint64_t)P.pf_x) != 0 && threadIdx.x == 32) prefetch_l2<W>(P);
+#endif
   pdl_wait();  // everything below may depend on earlier work of the stream
+#ifdef HALO_EXP_PREFETCH
   if (trace && (P.debug & kTraceDetail)) ctrl->trace[tslot][blockIdx.x][14] = gtimer();  // wait released
+#endif
   // by value when the host knows them (no cold dependent load on the critical path)
   if (threadIdx.x == 0) {
     if (kMode != kModeF) s_seq[0] = P.seq ? P.seq : ll_seq_next(ld_relaxed_gpu(&ctrl->seq_x));
@@ -512,7 +521,9 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 :
   }
   timer_start(P.flags, kMode == kModeF ? &ctrl->t_start_f : &ctrl->t_start_x);
   __syncthreads();  // barrier init, base table and sequence numbers visible to every thread
+#ifdef HALO_EXP_PREFETCH
   if (trace && (P.debug & kTraceDetail)) ctrl->trace[tslot][blockIdx.x][15] = gtimer();  // prologue done
+#endif
   // arrive early: the atomic's latency hides behind the items (launch_arrive)
   const uint32_t arrived = launch_arrive(kMode == kModeF ? &ctrl->done_f : &ctrl->done_x);
   const uint32_t tag_x = (uint32_t)s_seq[0], tag_f = (uint32_t)s_seq[1];
@@ -526,7 +537,7 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 :
     if (trace && j == 0) ctrl->trace[tslot][blockIdx.x][1] = gtimer();
     if (kMode != kModeF && it < nx) {
       const XRec& r = *reinterpret_cast<const XRec*>(blk);
-      x_item<W, kU>(r, reinterpret_cast<const XEnt*>(blk + 128), s_lb, P, tag_x);
+      x_item<W, kU, kChk>(r, reinterpret_cast<const XEnt*>(blk + 128), s_lb, P, tag_x);
       __syncthreads();  // the item's rows are stored (fused: before its count) and the slot is free
       if (threadIdx.x == 0) {  // every x launch counts (the fused launch's targets count all of them)
         uint64_t* cnt = &ctrl->xcnt[it % kXCounters][0];
@@ -543,11 +554,11 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 :
         xin_seen = true;
       }
       if (g.kind == kItemTree)
-        tree_item<W>(g, reinterpret_cast<const TRoot*>(blk + 128), reinterpret_cast<const uint4*>(blk + 128 + 32 * RT),
+        tree_item<W, kChk>(g, reinterpret_cast<const TRoot*>(blk + 128), reinterpret_cast<const uint4*>(blk + 128 + 32 * RT),
                      s_lb, P, tag_f, s_v, s_val,
                      (trace && (P.debug & kTraceDetail) && tdet_free) ? &ctrl->trace[tslot][blockIdx.x][10] : nullptr);
       else
-        tree_item_generic<W>(g, reinterpret_cast<const TRootG*>(blk + 128),
+        tree_item_generic<W, kChk>(g, reinterpret_cast<const TRootG*>(blk + 128),
                              reinterpret_cast<const TNode*>(blk + 128 + 16 * (RT / 8 > 0 ? RT / 8 : 1)), s_lb, P,
                              tag_f, s_v);
       __syncthreads();  // everyone is done with this slot
@@ -595,17 +606,23 @@ cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** ar
 // threads per f CTA) admits only one of them beside the x CTAs.
 static int g_x_variant = 0;
 void ll_set_x_variant(int v) { g_x_variant = v < 0 || v > 2 ? 0 : v; }
-template <int W>
-static const void* ll_fn(int mode, bool wide) {
+template <int W, bool C>
+static const void* ll_fn_c(int mode, bool wide) {
   if (mode == kModeX && !wide)
-    return g_x_variant == 0 ? (const void*)k_exchange_ll<W, 1, kModeX>
-                            : g_x_variant == 2 ? (const void*)k_exchange_ll<W, 3, kModeX>
-                                               : (const void*)k_exchange_ll<W, 2, kModeX>;
-  if (mode == kModeX) return (const void*)k_exchange_ll<W, 4, kModeX>;
-  if (mode == kModeF) return wide ? (const void*)k_exchange_ll<W, 4, kModeF> : (const void*)k_exchange_ll<W, 1, kModeF>;
-  return wide ? (const void*)k_exchange_ll<W, 4, kModeXF> : (const void*)k_exchange_ll<W, 1, kModeXF>;
+    return g_x_variant == 0 ? (const void*)k_exchange_ll<W, 1, kModeX, C>
+                            : g_x_variant == 2 ? (const void*)k_exchange_ll<W, 3, kModeX, C>
+                                               : (const void*)k_exchange_ll<W, 2, kModeX, C>;
+  if (mode == kModeX) return (const void*)k_exchange_ll<W, 4, kModeX, C>;
+  if (mode == kModeF) return wide ? (const void*)k_exchange_ll<W, 4, kModeF, C> : (const void*)k_exchange_ll<W, 1, kModeF, C>;
+  return wide ? (const void*)k_exchange_ll<W, 4, kModeXF, C> : (const void*)k_exchange_ll<W, 1, kModeXF, C>;
 }
-static const void* ll_fn(int layout, int mode, bool wide) { return layout == 4 ? ll_fn<4>(mode, wide) : ll_fn<3>(mode, wide); }
+template <int W>
+static const void* ll_fn(int mode, bool wide, bool chk = false) {
+  return chk ? ll_fn_c<W, true>(mode, wide) : ll_fn_c<W, false>(mode, wide);
+}
+static const void* ll_fn(int layout, int mode, bool wide, bool chk = false) {
+  return layout == 4 ? ll_fn<4>(mode, wide, chk) : ll_fn<3>(mode, wide, chk);
+}
 
 int ll_block(int mode, bool wide) {
   if (mode != kModeX || wide) return kThreads;
@@ -623,10 +640,11 @@ uint32_t ll_fblk_bytes(int tree_rows) { return fblk_bytes((uint32_t)tree_rows); 
 
 // mode: 0 = x, 1 = f, 2 = fused x+f.  wide = the plan's work items are large
 // (bandwidth regime): batched variants.
+// chk: the launch is being captured (the epoch-checking variant, kChk).
 cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
-                               const cudaAccessPolicyWindow* win, cudaStream_t st) {
+                               const cudaAccessPolicyWindow* win, cudaStream_t st, bool chk) {
   void* args[] = {(void*)&p};
-  return launch_coop_kernel_ex(ll_fn(layout, mode, wide), grid, ll_block(mode, wide), args, st, true,
+  return launch_coop_kernel_ex(ll_fn(layout, mode, wide, chk), grid, ll_block(mode, wide), args, st, true,
                                ll_smem_bytes(mode, p.item_rows, p.tree_rows, wide), win);
 }
 
@@ -641,15 +659,19 @@ cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [3]: x, f, x
   if (e != cudaSuccess) return e;
   const int rows = wide ? kMaxItemRows : 128;
   for (int mode = 0; mode < 3; ++mode) {
-    const void* fn = ll_fn(layout, mode, wide);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)ll_smem_bytes(mode, kMaxItemRows, kMaxTreeRows, wide));
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, ll_block(mode, wide),
-                                                      ll_smem_bytes(mode, rows, kTreeRowsOcc, wide));
-    if (e != cudaSuccess) return e;
-    blocks[mode] = b * sms;
+    int bmin = 1 << 30;
+    for (int chk = 0; chk < 2; ++chk) {  // the grid must fit both (eager and captured launches)
+      const void* fn = ll_fn(layout, mode, wide, chk != 0);
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)ll_smem_bytes(mode, kMaxItemRows, kMaxTreeRows, wide));
+      if (e != cudaSuccess) return e;
+      int b = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, ll_block(mode, wide),
+                                                        ll_smem_bytes(mode, rows, kTreeRowsOcc, wide));
+      if (e != cudaSuccess) return e;
+      bmin = std::min(bmin, b);
+    }
+    blocks[mode] = bmin * sms;
   }
   return cudaSuccess;
 }

@@ -20,8 +20,9 @@
 //   f (Alg. 5/6, trees):
 //     k_plan_child: the inverse maps (row t of rank l is entry i of map q);
 //     k_plan_roots: which rows root a tree and its class (a depth-first walk, children
-//       in descending pulse order: R15); k_plan_rank: each root's rank within its
-//       (class, local rank), in row order;
+//       in descending pulse order: R15), roots per class per CTA; k_plan_rank: their
+//       prefix over the CTAs (a root's rank within its (class, local rank) is that
+//       prefix + its rank in its CTA, row order);
 //     k_plan_f: each root's 32-B record + node indices into its item, item records.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -258,60 +259,87 @@ __device__ __forceinline__ bool plan_is_root(const PlanDev* __restrict__ D, int 
   return false;
 }
 
-__global__ void k_plan_roots(const PlanDev* __restrict__ D) {
-  const int l = blockIdx.y;
-  const int n = D->n_total[l];
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+// The shift-force targets of a tree as a mask over its rank's table (bucket_fs[l]).
+__device__ __forceinline__ uint8_t plan_fs_mask(const PlanDev* __restrict__ D, int l, const TNode* v, int nn) {
+  uint32_t m = 0;
+  for (int k = 0; k < nn; ++k)
+    if (v[k].fs != 0xff)
+      for (int j = 0; j < D->n_buckets[l]; ++j)
+        if (D->bucket_fs[l][j] == v[k].fs) m |= 1u << j;
+  return (uint8_t)m;
+}
+
+// One thread per row, kPB rows per CTA (blockIdx.x), blockIdx.y = local rank: is the row
+// a root, its tree's class (rcls, 0xff = not a root), and the CTA's roots per class.
+__global__ void __launch_bounds__(kPB) k_plan_roots(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.y, nc = D->P + 1;
+  const int t = blockIdx.x * kPB + threadIdx.x;
+  __shared__ int s_w[kMaxP + 1][kPB / 32];
+  __shared__ int s_tot[kMaxP + 1];
+  uint8_t cls = 0xff, mask = 0;
+  if (t < D->n_total[l]) {
     uint64_t* push;
-    uint8_t cls = 0xff;
     if (plan_is_root(D, l, t, &push)) {
       TNode v[kFastNodes];
       int lowest;
-      (void)plan_tree(D, l, t, v, lowest);
+      const int nn = plan_tree(D, l, t, v, lowest);
       cls = (uint8_t)(D->P - lowest);
+      mask = plan_fs_mask(D, l, v, nn);
     }
     D->rcls[(size_t)l * D->cap + t] = cls;
+    D->rmask[(size_t)l * D->cap + t] = mask;
   }
+  (void)block_count_class(cls != 0xff, cls != 0xff ? cls : 0, nc, s_w, s_tot);
+  if (threadIdx.x < nc) D->bcnt[((size_t)l * D->nblk + blockIdx.x) * nc + threadIdx.x] = s_tot[threadIdx.x];
 }
 
-// One CTA per local rank: rank of every root among the roots of its class, row order.
-__global__ void __launch_bounds__(kPB) k_plan_rank(const PlanDev* __restrict__ D) {
-  const int l = blockIdx.x, nc = D->P + 1;
-  const int n = D->n_total[l];
-  __shared__ int s_w[kMaxP + 1][kPB / 32];
-  __shared__ int s_tot[kMaxP + 1];
-  __shared__ int s_cnt[kMaxP + 1];
-  if (threadIdx.x <= kMaxP) s_cnt[threadIdx.x] = 0;
-  __syncthreads();
-  for (int base = 0; base < n; base += kPB) {
-    const int t = base + threadIdx.x;
-    const int c = t < n ? (int)D->rcls[(size_t)l * D->cap + t] : 0xff;
-    const bool root = c != 0xff;
-    const int idx = block_count_class(root, root ? c : 0, nc, s_w, s_tot);
-    if (root) D->rrank[(size_t)l * D->cap + t] = s_cnt[c] + idx - 1;
-    __syncthreads();
-    if (threadIdx.x < nc) s_cnt[threadIdx.x] += s_tot[threadIdx.x];
-    __syncthreads();
+// One CTA per local rank, one thread per class: exclusive prefix of the per-CTA root
+// counts (boff) and the totals (rcnt).
+__global__ void k_plan_rank(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.x, nc = D->P + 1, c = threadIdx.x;
+  if (c >= nc) return;
+  int acc = 0;
+  for (int b = 0; b < D->nblk; ++b) {
+    const size_t i = ((size_t)l * D->nblk + b) * nc + c;
+    const int v = D->bcnt[i];
+    D->boff[i] = acc;
+    acc += v;
   }
-  if (threadIdx.x < nc) D->rcnt[l * nc + threadIdx.x] = s_cnt[threadIdx.x];
+  D->rcnt[l * nc + c] = acc;
 }
 
 // Every root writes its 32-B record and node indices into slot rank % RT of item
 // foff[class][l] + rank / RT; slot 0 also writes the item's record.
-__global__ void k_plan_f(const PlanDev* __restrict__ D) {
-  const int l = blockIdx.y;
+// kMask: pass 1, the item's bucket mask = OR of its trees' masks (imask, zeroed before);
+// otherwise pass 2: records with the item-local bucket numbers (the item's buckets are the
+// set bits of its mask, in table order: what the host builder gives, R13).
+template <bool kMask>
+__global__ void __launch_bounds__(kPB) k_plan_f(const PlanDev* __restrict__ D) {
+  const int l = blockIdx.y, nc = D->P + 1;
   const int n = D->n_total[l], RT = D->RT;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    const uint8_t cls = D->rcls[(size_t)l * D->cap + t];
-    if (cls == 0xff) continue;
+  const int t = blockIdx.x * kPB + threadIdx.x;
+  __shared__ int s_w[kMaxP + 1][kPB / 32];
+  __shared__ int s_tot[kMaxP + 1];
+  const uint8_t cls = t < n ? D->rcls[(size_t)l * D->cap + t] : (uint8_t)0xff;
+  const int idx = block_count_class(cls != 0xff, cls != 0xff ? cls : 0, nc, s_w, s_tot);  // rank in the CTA
+  if (kMask) {
+    if (cls != 0xff) {
+      const int rank = D->boff[((size_t)l * D->nblk + blockIdx.x) * nc + cls] + idx - 1;
+      const uint32_t m = D->rmask[(size_t)l * D->cap + t];
+      if (m) atomicOr(&D->imask[D->foff[cls][l] + rank / RT], m);
+    }
+    return;
+  }
+  if (cls != 0xff) {
     uint64_t* push;
     (void)plan_is_root(D, l, t, &push);
     TNode v[kFastNodes];
     int lowest;
     const int nn = plan_tree(D, l, t, v, lowest);
-    const int rank = D->rrank[(size_t)l * D->cap + t];
+    const int rank = D->boff[((size_t)l * D->nblk + blockIdx.x) * nc + cls] + idx - 1;
     const int item = D->foff[cls][l] + rank / RT, slot = rank % RT;
     char* blk = D->fblk + (size_t)item * D->FB;
+    const uint32_t imask = D->imask[item];
     TRoot R;
     memset(&R, 0, sizeof R);
     R.push = push;
@@ -336,7 +364,7 @@ __global__ void k_plan_f(const PlanDev* __restrict__ D) {
       uint32_t b = kFsNone;
       if (x.fs != 0xff)
         for (int j = 0; j < D->n_buckets[l]; ++j)
-          if (D->bucket_fs[l][j] == x.fs) b = (uint32_t)j;
+          if (D->bucket_fs[l][j] == x.fs) b = (uint32_t)__popc(imask & ((1u << j) - 1u));
       R.par = (R.par & ~(15u << sh)) | ((uint32_t)(x.parent == 0xff ? 15 : x.parent) << sh);
       R.bucket = (R.bucket & ~(15u << sh)) | (b << sh);
       R.q |= (uint32_t)(x.kq & 7) << sh;
@@ -353,8 +381,9 @@ __global__ void k_plan_f(const PlanDev* __restrict__ D) {
       g.lrank = (uint16_t)l;
       g.n_roots = (uint32_t)min(RT, D->fcnt[cls][l] - rank);
       g.n_units = g.n_roots * D->W;
-      g.n_buckets = D->n_buckets[l];
-      for (int j = 0; j < kMaxBuckets; ++j) g.bucket_fs[j] = D->bucket_fs[l][j];
+      g.n_buckets = (uint8_t)__popc(imask);
+      for (int j = 0, k = 0; j < D->n_buckets[l]; ++j)
+        if (imask >> j & 1u) g.bucket_fs[k++] = D->bucket_fs[l][j];
       g.epoch = D->epoch;
       *reinterpret_cast<GRec*>(blk) = g;
     }
@@ -370,15 +399,20 @@ cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, cuda
   for (int q = 0; q < P; ++q) k_plan_org_pulse<<<dim3(gx, L), 256, 0, st>>>(D, q);
   k_plan_x<false><<<dim3(P, L), kPB, 0, st>>>(D);
   k_plan_child<<<dim3(gx, L * P), 256, 0, st>>>(D);
-  k_plan_roots<<<dim3(gx, L), 256, 0, st>>>(D);
-  k_plan_rank<<<L, kPB, 0, st>>>(D);
+  const unsigned nblk = (unsigned)((max_rows + kPB - 1) / kPB);
+  k_plan_roots<<<dim3(nblk, L), kPB, 0, st>>>(D);
+  k_plan_rank<<<L, 32, 0, st>>>(D);
   return cudaGetLastError();
 }
 
 cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st) {
   k_plan_x<true><<<dim3(P, L), kPB, 0, st>>>(D);
-  k_plan_f<<<dim3(plan_gx(max_rows), L), 256, 0, st>>>(D);
+  const unsigned nblk = (unsigned)((max_rows + kPB - 1) / kPB);
+  k_plan_f<true><<<dim3(nblk, L), kPB, 0, st>>>(D);
+  k_plan_f<false><<<dim3(nblk, L), kPB, 0, st>>>(D);
   return cudaGetLastError();
 }
+
+int plan_rows_per_cta() { return kPB; }
 
 }  // namespace halo

@@ -36,7 +36,7 @@ cudaError_t launch_unpack_f(int layout, const int32_t* map, int n, const float* 
 cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t base, int initiator, int relaxed,
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
 cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
-                               const cudaAccessPolicyWindow* win, cudaStream_t st);
+                               const cudaAccessPolicyWindow* win, cudaStream_t st, bool chk);
 cudaError_t max_coresident_ll(int layout, bool wide, int* blocks);
 int ll_ring(bool wide);
 void ll_set_x_variant(int v);
@@ -51,6 +51,7 @@ cudaError_t launch_ns_x(const NsXParams& X, int layout, int max_rows, cudaStream
 cudaError_t launch_ns_wait(const NsWaitParams& W, cudaStream_t st);
 cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st);
 cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st);
+int plan_rows_per_cta();
 uint32_t ll_xblk_bytes(int rows);
 uint32_t ll_fblk_bytes(int rows);
 cudaError_t launch_assign_home(const float* x, int n, int stride, const AssignParams& A, int32_t* rank, int* counts,
@@ -167,6 +168,7 @@ struct halo_ctx {
   int n_items_x = 0, n_items_f = 0;
   int n_tail_f = 0;                 // LL: shift-force combine items at the end of the f list
   double* d_fshift_tmp = nullptr;  // halo_step_host
+  char* h_small = nullptr;          // pinned 64 KiB: set_maps result read-backs and small uploads
   // halo_step_host_packed: packed staging in / out, segment tables (x unpack | f unpack | pack),
   // rebuilt once per NS epoch; side streams for the f upload and the halo-x download
   char* d_pk_in = nullptr;
@@ -174,6 +176,7 @@ struct halo_ctx {
   size_t pk_in_cap = 0, pk_out_cap = 0;
   SegCopy* d_segs = nullptr;
   uint32_t pk_epoch = 0;
+  char* pk_out_dev = nullptr;       // the output block's device address the tables were built for
   size_t pk_max_words[3] = {0, 0, 0};
   cudaStream_t pk_h2d = nullptr, pk_d2h = nullptr;
   cudaEvent_t pk_ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -470,6 +473,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) { memset(ctx->err_host, 0, 64); e = cudaHostGetDevicePointer(&ctx->err_dev, ctx->err_host, 0); }
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_small, 64 * 1024);
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_small, 64 * 1024);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_mig, sizeof(MigRank) * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_migctrl, sizeof(MigCtrl));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_planes, sizeof(double) * 3 * (kMaxRanks + 1));
@@ -1234,7 +1238,7 @@ static halo_status build_ll_f(halo_ctx* ctx, PhaseTimer* prof = nullptr) {
 // the rank-level tree (a row of rank r received in pulse qlast can be sent in any later
 // pulse q; a wrapping sender's edges add into fshift[r][d_q]; same-group receivers
 // continue the tree).  At most 2^P - 1 edges, i.e. <= kMaxBuckets for P <= 3.
-static halo_status upload_plan(halo_ctx* ctx);
+static halo_status upload_plan(halo_ctx* ctx, cudaStream_t st = nullptr);
 static halo_status pull_maps(halo_ctx* ctx, int p, cudaStream_t st);
 
 static bool rank_tree_fs(const halo_ctx* ctx, int r, int qlast, FsSet& fs) {
@@ -1329,10 +1333,14 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
     CK(cudaMallocHost(&ctx->h_pl, sizeof(PlanDev)));
     CK(cudaMallocHost(&ctx->h_pl_cnt, sizeof(int32_t) * (kMaxP + 1) * (kMaxP + 1) * kMaxLocal));
   }
+  int max_rows = 1;
+  for (int l = 0; l < L; ++l) max_rows = std::max(max_rows, ctx->n_total[l]);
+  const int nblk = (max_rows + plan_rows_per_cta() - 1) / plan_rows_per_cta();
   const size_t so = align_up(sizeof(uint64_t) * L * cap, 256), sc = align_up(sizeof(int32_t) * L * cap * P, 256),
-               sr = align_up(L * cap, 256), sk = align_up(sizeof(int32_t) * L * cap, 256),
+               sr = align_up(2 * L * cap, 256), sk = align_up(2 * sizeof(int32_t) * L * nblk * (P + 1), 256),
+               si = align_up(sizeof(uint32_t) * (L * cap / 8 + (size_t)(kMaxP + 1) * L + 1), 256),
                sx = align_up(sizeof(int32_t) * (P * L + L) * (P + 1), 256);
-  const size_t sbytes = so + sc + sr + sk + sx;
+  const size_t sbytes = so + sc + sr + sk + sx + si;
   if (sbytes > ctx->pl_scratch_bytes) {
     if (ctx->d_pl_scratch) CK(cudaFree(ctx->d_pl_scratch));
     ctx->d_pl_scratch = nullptr;
@@ -1353,12 +1361,11 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
     H.shiftL[q] = ctx->cfg.box[ctx->pdim[q]];
     H.pdim[q] = (uint8_t)ctx->pdim[q];
   }
-  int max_rows = 1;
+  H.nblk = nblk;
   for (int l = 0; l < L; ++l) {
     const int r = ctx->first_rank + l;
     H.n_home[l] = ctx->n_home[l];
     H.n_total[l] = ctx->n_total[l];
-    max_rows = std::max(max_rows, ctx->n_total[l]);
     H.maps[l] = ctx->maps_of_local(l);
     FsSet fs;
     if (!rank_tree_fs(ctx, r, -1, fs)) return HALO_ERR_UNSUPPORTED;  // host builder
@@ -1385,7 +1392,10 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
   H.org = reinterpret_cast<uint64_t*>(sp);
   H.child = reinterpret_cast<int32_t*>(sp + so);
   H.rcls = reinterpret_cast<uint8_t*>(sp + so + sc);
-  H.rrank = reinterpret_cast<int32_t*>(sp + so + sc + sr);
+  H.rmask = H.rcls + (size_t)L * cap;
+  H.imask = reinterpret_cast<uint32_t*>(sp + so + sc + sr + sk + sx);
+  H.bcnt = reinterpret_cast<int32_t*>(sp + so + sc + sr);
+  H.boff = H.bcnt + (size_t)L * nblk * (P + 1);
   H.xcnt = reinterpret_cast<int32_t*>(sp + so + sc + sr + sk);
   H.rcnt = H.xcnt + (size_t)P * L * (P + 1);
   CK(cudaMemcpyAsync(ctx->d_pl, &H, sizeof(PlanDev), cudaMemcpyHostToDevice, st));
@@ -1460,7 +1470,7 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
   ctx->gpu_xblk_bytes = std::max<size_t>(1, (size_t)nx * H.XB);
   ctx->gpu_fblk_bytes = std::max<size_t>(1, (size_t)nf * H.FB);
   fill_rank_dev(ctx);
-  halo_status s = upload_plan(ctx);
+  halo_status s = upload_plan(ctx, st);
   if (s != HALO_OK) return s;
   H.xblk = ctx->d_xblk;
   H.fblk = ctx->d_fblk;
@@ -1476,6 +1486,7 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
     CK(cudaMemcpy2DAsync(ctx->d_xblk + (size_t)n_send * H.XB, H.XB, ctx->h_recv, sizeof(XRec), sizeof(XRec),
                          recv.size(), cudaMemcpyHostToDevice, st));
   }
+  CK(cudaMemsetAsync(H.imask, 0, sizeof(uint32_t) * nf, st));
   CK(launch_plan_write(ctx->d_pl, L, P, max_rows, st));
   ctx->n_tail_f = 0;
   if (prof) prof->lap("plan:write");
@@ -1487,7 +1498,9 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
 // item blocks.  Host-built plans (h_xblk / h_fblk) go up in one DMA from a pinned
 // image; a GPU-built plan (gpu_xblk_bytes > 0, kernels_plan.cu) uploads only the head
 // and leaves the block areas to the kernels.
-static halo_status upload_plan(halo_ctx* ctx) {
+// st != null: the DMA is enqueued on st (the pinned image must then stay untouched until
+// st passes it); null: synchronous.
+static halo_status upload_plan(halo_ctx* ctx, cudaStream_t st) {
   const size_t a = 256;
   const bool gpu = ctx->gpu_xblk_bytes > 0;
   const size_t nr = align_up(sizeof(RankDev) * ctx->n_local, a);
@@ -1544,7 +1557,8 @@ static halo_status upload_plan(halo_ctx* ctx) {
     if (!ctx->h_fblk.empty()) used = (size_t)(ctx->d_fblk - ctx->plan) + ctx->h_fblk.size();
     else if (!ctx->h_xblk.empty()) used = (size_t)(ctx->d_xblk - ctx->plan) + ctx->h_xblk.size();
   }
-  CK(cudaMemcpy(ctx->plan, img, used, cudaMemcpyHostToDevice));
+  if (st) CK(cudaMemcpyAsync(ctx->plan, img, used, cudaMemcpyHostToDevice, st));
+  else CK(cudaMemcpy(ctx->plan, img, used, cudaMemcpyHostToDevice));
   ctx->n_items_x = gpu ? ctx->gpu_n_items_x : (int)ctx->h_items_x.size();
   ctx->n_items_f = gpu ? ctx->gpu_n_items_f : (int)ctx->h_items_f.size();
   return HALO_OK;
@@ -1553,13 +1567,16 @@ static halo_status upload_plan(halo_ctx* ctx) {
 // Sequence number of the next LL launch on `st`: by value (host mirror) unless the
 // ctx has ever been captured into a graph (then 0: the kernel reads the device
 // counter, which every LL launch advances).
-static uint64_t next_seq(halo_ctx* ctx, cudaStream_t st, uint64_t* host) {
+static uint64_t next_seq(halo_ctx* ctx, cudaStream_t st, uint64_t* host, bool* capturing = nullptr) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  bool cap = false;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
     (void)cudaGetLastError();
-    ctx->captured = true;
+    cap = true;
   }
-  if (cs != cudaStreamCaptureStatusNone) ctx->captured = true;
+  if (cs != cudaStreamCaptureStatusNone) cap = true;
+  if (cap) ctx->captured = true;
+  if (capturing) *capturing = cap;
   *host = ll_seq_next(*host);
   return ctx->captured ? 0 : *host;
 }
@@ -1602,17 +1619,17 @@ static int grid_for(int n_items, int n_local, int max_blocks) {
 }
 
 // Pull the set_maps results of every local rank back to the host.
-static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st) {
+static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st, int32_t* agreed = nullptr) {
   const int L = ctx->n_local, P = ctx->P;
-  // the set_maps result arrays are contiguous in Ctrl: one copy, one synchronisation
-  const char* lo = reinterpret_cast<const char*>(ctx->ctrl->send_size);
-  const char* hi = reinterpret_cast<const char*>(ctx->ctrl->n_total) + sizeof(ctx->ctrl->n_total);
-  static_assert(offsetof(Ctrl, n_indep) > offsetof(Ctrl, send_size) && offsetof(Ctrl, n_total) > offsetof(Ctrl, dep),
+  // the set_maps result arrays are contiguous in Ctrl (through agreed_err): one copy
+  // into pinned memory, one synchronisation
+  static_assert(offsetof(Ctrl, n_indep) > offsetof(Ctrl, send_size) && offsetof(Ctrl, n_total) > offsetof(Ctrl, dep) &&
+                    offsetof(Ctrl, agreed_err) > offsetof(Ctrl, n_total),
                 "set_maps result block layout");
-  std::vector<char> hbuf(sizeof(Ctrl));  // (Ctrl holds the trace arrays: too large for the stack)
-  const Ctrl& h = *reinterpret_cast<const Ctrl*>(hbuf.data());
-  char* hb = hbuf.data() + (lo - reinterpret_cast<const char*>(ctx->ctrl));
-  cudaError_t e = cudaMemcpyAsync(hb, lo, (size_t)(hi - lo), cudaMemcpyDeviceToHost, st);
+  const size_t lo = offsetof(Ctrl, send_size), hi = offsetof(Ctrl, agreed_err) + sizeof(ctx->ctrl->agreed_err);
+  char* hb = ctx->h_small;  // pinned; viewed as a Ctrl shifted by lo
+  const Ctrl& h = *reinterpret_cast<const Ctrl*>(hb - lo);
+  cudaError_t e = cudaMemcpyAsync(hb, reinterpret_cast<const char*>(ctx->ctrl) + lo, hi - lo, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "pull_ctrl");
   for (int l = 0; l < L; ++l) {
@@ -1626,6 +1643,7 @@ static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st) {
       ctx->dep[i] = h.dep[l][p];
     }
     ctx->n_total[l] = h.n_total[l];
+    if (agreed) agreed[l] = h.agreed_err[l];
   }
   return HALO_OK;
 }
@@ -1802,18 +1820,20 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
       nt[l] = std::min(std::max(n_home[l], 0), ctx->cfg.capacity);
       errs[l] = local_err;
     }
-    CK(cudaMemcpyAsync(ctx->ctrl->send_size, zero, sizeof zero, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->ctrl->dep, zero, sizeof zero, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->ctrl->n_indep, zero, sizeof zero, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->ctrl->n_total, nt, sizeof nt, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->ctrl->err, errs, sizeof errs, cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
+    (void)zero;
+    // the result block [send_size .. n_total) zeroed, then n_total and err from pinned
+    // memory (stream-ordered before the first select: no synchronisation)
+    CK(cudaMemsetAsync(ctx->ctrl->send_size, 0, offsetof(Ctrl, n_total) - offsetof(Ctrl, send_size), st));
+    static_assert(offsetof(Ctrl, err) == offsetof(Ctrl, n_total) + sizeof(int32_t) * kMaxLocal, "n_total | err");
+    memcpy(ctx->h_small, nt, sizeof nt);
+    memcpy(ctx->h_small + sizeof nt, errs, sizeof errs);
+    CK(cudaMemcpyAsync(ctx->ctrl->n_total, ctx->h_small, sizeof nt + sizeof errs, cudaMemcpyHostToDevice, st));
     for (int l = 0; l < L; ++l) ctx->n_total[l] = nt[l];
   }
   ctx->n_home.assign(ctx->n_total.begin(), ctx->n_total.end());
   // LL areas zeroed every NS epoch (ll_seq_next): no peer writes them before the
   // pulse-0 handshake below, which this stream reaches only after the memset
-  if (ctx->ll || ctx->auto_tr)
+  if ((ctx->ll || ctx->auto_tr) && !getenv("HALO_AB_NO_LLZERO"))
     for (int l = 0; l < L; ++l)
       CK(cudaMemsetAsync(ctx->xll_of(ctx->first_rank + l), 0, sizeof(uint64_t) * 2 * (size_t)P * ctx->ll_stride, st));
   fill_rank_dev(ctx);
@@ -1823,7 +1843,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   ctx->h_fblk.clear();  // the last epoch's force blocks: not re-uploaded with every pulse's x plan
   ctx->h_xblk.clear();
   ctx->gpu_xblk_bytes = ctx->gpu_fblk_bytes = 0;
-  if ((s = upload_plan(ctx)) != HALO_OK) return s;
+  if ((s = upload_plan(ctx, st)) != HALO_OK) return s;  // (the next upload follows a synchronisation)
 
   const uint64_t timeout_ns = (uint64_t)(ctx->cfg.timeout_s * 1e9);
   // static planes of the GPU map builder (R2, R3): b_d[c_d] of every dim, and b_d[c_d + 1]
@@ -1955,41 +1975,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     }
     if (any) CK(launch_ns_wait(NW, st));
   }
-  if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
-  if ((s = check_err_word(ctx)) != HALO_OK) return s;
-  prof.lap("x_pulses");
-  {
-    // votes that ride on the status exchange (OR over all ranks), so that every
-    // rank of every process takes the same decision:
-    //  * HALO_F_AUTO_TRANSPORT: the copy engine if some pulse is large (bandwidth regime);
-    //  * the work-item size R: the shift-force slot of a pusher's item is indexed by R
-    //    on both sides of a pulse (pusher and combine), so all ranks must use one R:
-    //    one-hot vote kVoteRows << log2(R/32), the largest voted R wins.
-    //    R = 64 rows (latency regime; swept 32-512 at C3) unless this process's pulses
-    //    are so large that a CTA would run more than ~2 items in sequence.
-    int32_t vote = 0;
-    if (ctx->auto_tr) {
-      size_t big = 0, thr = ctx->auto_ce_bytes;
-      if (const char* e = getenv("HALO_AUTO_CE_BYTES")) thr = (size_t)std::max(0LL, atoll(e));  // read per NS step
-      for (int i = 0; i < L * P; ++i) big = std::max(big, (size_t)ctx->send_size[i] * W * sizeof(float));
-      if (big >= thr) vote |= kVoteCE;
-    }
-    int R = ctx->item_rows;
-    if (!ctx->item_rows_fixed) {
-      long rows = 0;
-      for (int i = 0; i < L * P; ++i) rows += std::max(ctx->send_size[i], ctx->recv_size[i]);
-      const long ctas = std::max(1, std::min(ctx->max_x, ctx->max_f));
-      R = 64;
-      while (R < kMaxItemRows && rows / R > 2 * ctas) R *= 2;
-    }
-    vote |= kVoteRows << (31 - __builtin_clz((unsigned)(R / kMinItemRows)));
-    int32_t e[kMaxLocal];
-    CK(cudaMemcpyAsync(e, ctx->ctrl->err, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (int l = 0; l < L; ++l) e[l] |= vote;
-    CK(cudaMemcpyAsync(ctx->ctrl->err, e, sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
-  }
-  // error agreement over all ranks
+  // error agreement + votes over all ranks, then ONE read-back of every result
   StatusParams SP{};
   SP.ctrl = ctx->ctrl;
   SP.epoch = ctx->epoch;
@@ -2000,11 +1986,19 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   for (int r = 0; r < ctx->nranks; ++r) SP.all[r] = ctx->hdr_of(r);
   SP.err_host = ctx->err_dev;
   SP.timeout_ns = timeout_ns;
+  SP.vote = 1;
+  SP.P = P;
+  SP.W = W;
+  SP.auto_tr = ctx->auto_tr ? 1 : 0;
+  SP.ce_bytes = ctx->auto_ce_bytes;
+  if (const char* e = getenv("HALO_AUTO_CE_BYTES")) SP.ce_bytes = (uint64_t)std::max(0LL, atoll(e));  // per NS step
+  SP.rows_fixed = ctx->item_rows_fixed ? ctx->item_rows : 0;
+  SP.ctas = std::max(1, std::min(ctx->max_x, ctx->max_f));
   CK(launch_status(SP, st));
   int32_t agreed[kMaxLocal];
-  CK(cudaMemcpyAsync(agreed, ctx->ctrl->agreed_err, sizeof agreed, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if ((s = pull_ctrl(ctx, st, agreed)) != HALO_OK) return s;
   if ((s = check_err_word(ctx)) != HALO_OK) return s;
+  prof.lap("sizes");
   int any = 0;
   for (int l = 0; l < L; ++l) any |= agreed[l];
   if (any & kErrCapacity) return fail(ctx, HALO_ERR_CAPACITY, "n_home + received rows exceed capacity on some rank");
@@ -2073,9 +2067,9 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   }
   // the LL launches take their sequence numbers by value from a host mirror: resync it
   // with the device counters (the paper / copy-engine launches advance those too)
-  uint64_t seqs[2];
-  CK(cudaMemcpyAsync(&seqs[0], &ctx->ctrl->seq_x, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&seqs[1], &ctx->ctrl->seq_f, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  uint64_t* seqs = reinterpret_cast<uint64_t*>(ctx->h_small);  // pinned; seq_x | seq_f adjacent
+  static_assert(offsetof(Ctrl, seq_f) == offsetof(Ctrl, seq_x) + sizeof(uint64_t), "seq_x | seq_f");
+  CK(cudaMemcpyAsync(seqs, &ctx->ctrl->seq_x, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   // the fused launch's per-rank halo counters count from here (the per-pulse x
   // launches above counted too)
   CK(cudaMemsetAsync(ctx->ctrl->xcnt, 0, sizeof(ctx->ctrl->xcnt), st));
@@ -2497,14 +2491,15 @@ halo_status halo_exchange_x(halo_ctx* ctx, void* stream) {
   const int grid = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
   ctx->last_grid[0] = grid;
   if (ctx->ll) {
-    X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x);
+    bool cap = false;
+    X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x, &cap);
     X.n_items_x = ctx->n_items_x;
     if (ctx->prefetch) {  // the f launch's item blocks and the home x rows (L2 prefetch)
       X.pf_f = ctx->d_fblk;
       X.pf_f_bytes = (uint64_t)ctx->n_items_f * ll_fblk_bytes(ctx->tree_rows);
       X.pf_x = 1;
     }
-    CK(launch_exchange_ll(X, 0, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
+    CK(launch_exchange_ll(X, 0, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream, cap));
   }
   if (!ctx->ll)
     CK(launch_exchange_x(X, ctx->W, grid, (cudaStream_t)stream));
@@ -2531,8 +2526,9 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   }
   ctx->last_grid[1] = grid;
   if (ctx->ll) {
-    F.seq_f = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f);
-    CK(launch_exchange_ll(F, 1, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
+    bool cap = false;
+    F.seq_f = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f, &cap);
+    CK(launch_exchange_ll(F, 1, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream, cap));
   }
   if (!ctx->ll)
     CK(launch_exchange_f(F, ctx->W, grid, (cudaStream_t)stream));
@@ -2557,9 +2553,10 @@ halo_status halo_exchange_xf(halo_ctx* ctx, double* fshift, int accumulate, void
   int grid = std::min(X.n_items - X.n_tail, ctx->cap_xf() - X.n_tail) + X.n_tail;
   grid = std::max(grid, 1);
   ctx->last_grid[0] = grid;
-  X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x);
+  bool cap = false;
+  X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x, &cap);
   X.seq_f = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f);
-  CK(launch_exchange_ll(X, 2, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream));
+  CK(launch_exchange_ll(X, 2, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream, cap));
   return HALO_OK;
 }
 
@@ -2612,7 +2609,7 @@ static void packed_sizes(const halo_ctx* ctx, size_t* in_b, size_t* out_b, size_
   *out_b = *fs_off + sizeof(double) * 9 * ctx->n_local;
 }
 
-static halo_status packed_prepare(halo_ctx* ctx) {
+static halo_status packed_prepare(halo_ctx* ctx, char* out_dev) {
   size_t in_b, out_b, fs_off;
   packed_sizes(ctx, &in_b, &out_b, &fs_off);
   const int L = ctx->n_local;
@@ -2659,16 +2656,20 @@ static halo_status packed_prepare(halo_ctx* ctx) {
                             reinterpret_cast<uint32_t*>(ctx->d_pk_out + o), W * nh};
     o += 4 * W * nh;
   }
+  // the forces and fshift: straight into the caller's (mapped, pinned) host block when
+  // it is device-accessible (no download after the last kernel), else into staging
+  char* fo = out_dev ? out_dev : ctx->d_pk_out;
   for (int l = 0; l < L; ++l) {
-    sg[3 * L + l] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->f[l]), reinterpret_cast<uint32_t*>(ctx->d_pk_out + o),
+    sg[3 * L + l] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->f[l]), reinterpret_cast<uint32_t*>(fo + o),
                             W * ctx->n_home[l]};
     o += 4 * W * ctx->n_home[l];
   }
   sg[4 * L] = SegCopy{reinterpret_cast<const uint32_t*>(ctx->d_fshift_tmp),
-                      reinterpret_cast<uint32_t*>(ctx->d_pk_out + fs_off), words(sizeof(double) * 9 * L)};
+                      reinterpret_cast<uint32_t*>(fo + fs_off), words(sizeof(double) * 9 * L)};
   for (int k = 2 * L; k <= 4 * L; ++k) ctx->pk_max_words[2] = std::max(ctx->pk_max_words[2], sg[k].words);
   CK(cudaMemcpy(ctx->d_segs, sg.data(), sizeof(SegCopy) * sg.size(), cudaMemcpyHostToDevice));
   ctx->pk_epoch = ctx->epoch;
+  ctx->pk_out_dev = out_dev;
   return HALO_OK;
 }
 
@@ -2684,8 +2685,16 @@ halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_
   if (!ctx || !in_host) return HALO_ERR_ARG;
   if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "step before set_maps");
   halo_status s;
-  if (ctx->pk_epoch != ctx->epoch || !ctx->d_segs)
-    if ((s = packed_prepare(ctx)) != HALO_OK) return s;
+  // a device-accessible (mapped pinned) output block takes the forces directly
+  char* out_dev = nullptr;
+  if (out_host && !getenv("HALO_PACKED_STAGED")) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      out_dev = static_cast<char*>(pa.devicePointer);
+    (void)cudaGetLastError();
+  }
+  if (ctx->pk_epoch != ctx->epoch || !ctx->d_segs || ctx->pk_out_dev != out_dev)
+    if ((s = packed_prepare(ctx, out_dev)) != HALO_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   const int L = ctx->n_local;
   size_t in_b, out_b, fs_off;
@@ -2720,7 +2729,7 @@ halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_
   if ((s = halo_exchange_f(ctx, ctx->d_fshift_tmp, 1, stream)) != HALO_OK) return s;
   if (out) {
     CK(launch_seg_copy(ctx->d_segs + 3 * L, L + 1, ctx->pk_max_words[2], st));
-    CK(cudaMemcpyAsync(out + bxo, ctx->d_pk_out + bxo, out_b - bxo, cudaMemcpyDeviceToHost, st));
+    if (!out_dev) CK(cudaMemcpyAsync(out + bxo, ctx->d_pk_out + bxo, out_b - bxo, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamWaitEvent(st, ctx->pk_ev[3], 0));
   }
   CK(cudaStreamSynchronize(st));
@@ -3048,6 +3057,7 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_pk_in) (void)cudaFree(ctx->d_pk_in);
   if (ctx->d_pk_out) (void)cudaFree(ctx->d_pk_out);
   if (ctx->d_segs) (void)cudaFree(ctx->d_segs);
+  if (ctx->h_small) (void)cudaFreeHost(ctx->h_small);
   if (ctx->d_pl) (void)cudaFree(ctx->d_pl);
   if (ctx->h_pl) (void)cudaFreeHost(ctx->h_pl);
   if (ctx->h_pl_cnt) (void)cudaFreeHost(ctx->h_pl_cnt);
