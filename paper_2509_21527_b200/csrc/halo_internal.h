@@ -439,7 +439,11 @@ struct PlanDev {
   int32_t* bcnt;            // [L][nblk][P + 1] roots per class in each CTA's rows (k_plan_roots)
   int32_t* boff;            // ... their exclusive prefix over the CTAs of a rank (k_plan_rank)
   int nblk;                 // CTAs per local rank of the per-row kernels
-  int32_t* xcnt;            // [P][L][P + 1] send items per class (counting pass)
+  int32_t* xcnt;            // [P][L][P + 1] send items per class (counting pass, zeroed before)
+  int32_t* xlast;           // [P*L][xnch]: last class change in each kPB-entry chunk of a map (or -1)
+  int32_t* xlstart;         // ... last item start in the chunk
+  int32_t* xccnt;           // [P*L][xnch][kMaxP + 1]: item starts per class in the chunk
+  int xnch;                 // chunks per map
   int32_t* rcnt;            // [L][P + 1] roots per class
   // second pass (after the counts): item offsets and the block areas
   int32_t xoff[kMaxP + 1][kMaxP][kMaxLocal];  // first x item of (class, pulse, local rank)
@@ -499,6 +503,8 @@ struct SelParams {
   uint32_t wait_mask[kMaxLocal];   // pulses q < p whose x-sender is in another process: wait ns_x[q]
   int* err_host;
   uint64_t timeout_ns;
+  int32_t* sel_cnt;         // [n_local][max_chunks] selected rows per 1024-row chunk (count pass)
+  int max_chunks;           // chunks per local rank (>= candidates / 1024)
   double rc2;               // float64(rc)^2 (R31)
   int decomposed_mask;      // bit d set iff grid[d] > 1
   int map_stride;

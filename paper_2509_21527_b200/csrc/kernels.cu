@@ -392,32 +392,31 @@ __global__ void __launch_bounds__(kThreads) k_exchange_f(const __grid_constant__
 // One CTA (1024 threads) per local rank: ordered compaction of the candidate
 // rows [cand0, cand1) with the fp64 slab predicate (R2, R3).  Also checks, on
 // the first pulse, that home atoms lie in the rank's cell.
-__global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelParams S) {
-  const int lr = blockIdx.x;
-  const RankDev& rd = S.ranks[lr];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ int s_cnt[32];
-  __shared__ int s_total;
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) {
-    s_bad = 0;
-    // rows that came from another process in earlier pulses: wait for their arrival
-    for (uint32_t m = S.wait_mask[lr]; m; m &= m - 1)
-      (void)wait_epoch(&rd.hdr->ns_x[__ffs(m) - 1], S.epoch, S.timeout_ns, S.err_host, tcode(9, lr, __ffs(m) - 1));
-  }
-  __syncthreads();
-  if (S.home_lo != nullptr) {
-    for (int i = threadIdx.x; i < rd.n_home; i += blockDim.x) {
-      bool bad = false;
-      for (int d = 0; d < 3; ++d) {
-        if (!(S.decomposed_mask & (1 << d))) continue;
-        const double v = (double)rd.x[(size_t)i * S.layout + d];
-        bad |= !(v >= S.home_lo[3 * lr + d] && v < S.home_hi[3 * lr + d]);
+// The slab predicate of candidate row i (R2, R3) and, with rounded zones, R31.
+__device__ __forceinline__ bool select_row(const SelParams& S, const RankDev& rd, int lr, int i, double blo) {
+  const float* row = rd.x + (size_t)i * S.layout;
+  const double dd = __dsub_rn((double)row[S.dim], blo);
+  bool sel = dd < S.rc;
+  if (sel && S.b_up != nullptr) {
+    // rounded zones (R31): a row beyond this rank's upper face in another dim
+    // is sent only if its distance to the receiver's cell is < rc (fixed op
+    // order, no FMA contraction: the oracle's float64 ops)
+    double r2 = __dmul_rn(dd, dd);
+    bool beyond = false;
+    for (int d2 = 0; d2 < 3; ++d2) {
+      if (d2 == S.dim) continue;
+      const double t = __dsub_rn((double)row[d2], S.b_up[3 * lr + d2]);
+      if (t > 0.0) {
+        r2 = __dadd_rn(r2, __dmul_rn(t, t));
+        beyond = true;
       }
-      if (bad) s_bad = 1;
     }
+    sel = !beyond || r2 < S.rc2;
   }
-  int c0, c1;
+  return sel;
+}
+
+__device__ __forceinline__ void select_range(const SelParams& S, int lr, int& c0, int& c1) {
   if (S.cand != nullptr) {
     c0 = S.cand[2 * lr];
     c1 = S.cand[2 * lr + 1];
@@ -428,56 +427,71 @@ __global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelPara
     c0 = S.ctrl->atom_offset[lr][S.p - 1];
     c1 = c0 + S.ctrl->recv_size[lr][S.p - 1];
   }
-  int32_t* out = rd.maps + (size_t)S.p * S.map_stride;
-  const double blo = S.b_lo[3 * lr + S.dim];
-  int base = 0;
-  for (int t0 = c0; t0 < c1; t0 += blockDim.x) {
-    const int i = t0 + threadIdx.x;
-    bool sel = false;
-    if (i < c1) {
-      const float* row = rd.x + (size_t)i * S.layout;
-      const double dd = __dsub_rn((double)row[S.dim], blo);
-      sel = dd < S.rc;
-      if (sel && S.b_up != nullptr) {
-        // rounded zones (R31): a row beyond this rank's upper face in another dim
-        // is sent only if its distance to the receiver's cell is < rc (fixed op
-        // order, no FMA contraction: the oracle's float64 ops)
-        double r2 = __dmul_rn(dd, dd);
-        bool beyond = false;
-        for (int d2 = 0; d2 < 3; ++d2) {
-          if (d2 == S.dim) continue;
-          const double t = __dsub_rn((double)row[d2], S.b_up[3 * lr + d2]);
-          if (t > 0.0) {
-            r2 = __dadd_rn(r2, __dmul_rn(t, t));
-            beyond = true;
-          }
-        }
-        sel = !beyond || r2 < S.rc2;
+}
+
+// Order-preserving compaction of the candidate rows [c0, c1) with the fp64 slab
+// predicate, over many CTAs per local rank (blockIdx.y): kWrite = false counts each
+// CTA's selected rows (sel_cnt) and checks, on the first pulse, that home atoms lie in
+// the rank's cell; kWrite = true sums the counts of the CTAs before it (its output
+// offset; the map stays in ascending row order, R11) and writes its rows; its last CTA
+// writes send_size.  CTA c covers rows c0 + [c*1024, (c+1)*1024).
+template <bool kWrite>
+__global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelParams S) {
+  const int lr = blockIdx.y;
+  const RankDev& rd = S.ranks[lr];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_cnt[32];
+  __shared__ int s_total, s_base;
+  if (!kWrite && threadIdx.x == 0) {
+    // rows that came from another process in earlier pulses: wait for their arrival
+    for (uint32_t m = S.wait_mask[lr]; m; m &= m - 1)
+      (void)wait_epoch(&rd.hdr->ns_x[__ffs(m) - 1], S.epoch, S.timeout_ns, S.err_host, tcode(9, lr, __ffs(m) - 1));
+  }
+  __syncthreads();
+  if (!kWrite && S.home_lo != nullptr) {
+    bool bad = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rd.n_home; i += gridDim.x * blockDim.x)
+      for (int d = 0; d < 3; ++d) {
+        if (!(S.decomposed_mask & (1 << d))) continue;
+        const double v = (double)rd.x[(size_t)i * S.layout + d];
+        bad |= !(v >= S.home_lo[3 * lr + d] && v < S.home_hi[3 * lr + d]);
       }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, sel);
-    if (lane == 0) s_cnt[warp] = __popc(bal);
-    __syncthreads();
-    if (warp == 0) {
-      const int c = (lane < (int)(blockDim.x >> 5)) ? s_cnt[lane] : 0;
-      int incl = c;
+    if (bad) atomicOr(&S.ctrl->err[lr], kErrGeometry);
+  }
+  int c0, c1;
+  select_range(S, lr, c0, c1);
+  const int nchunk = (c1 - c0 + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int i = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool sel = blockIdx.x < nchunk && i < c1 && select_row(S, rd, lr, i, S.b_lo[3 * lr + S.dim]);
+  const unsigned bal = __ballot_sync(0xffffffffu, sel);
+  if (lane == 0) s_cnt[warp] = __popc(bal);
+  if (kWrite && warp == 1) {  // this CTA's output offset: the rows of the CTAs before it
+    int b = 0;
+    for (int k = lane; k < (int)blockIdx.x && k < nchunk; k += 32) b += S.sel_cnt[lr * S.max_chunks + k];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      s_cnt[lane] = incl - c;
-      if (lane == 31) s_total = incl;
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (lane == 0) s_base = b;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int c = (lane < (int)(blockDim.x >> 5)) ? s_cnt[lane] : 0;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    __syncthreads();
-    if (sel) out[base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u))] = i;
-    base += s_total;
-    __syncthreads();
+    s_cnt[lane] = incl - c;
+    if (lane == 31) s_total = incl;
   }
-  if (threadIdx.x == 0) {
-    S.ctrl->send_size[lr][S.p] = base;
-    if (s_bad) S.ctrl->err[lr] |= kErrGeometry;
+  __syncthreads();
+  if (!kWrite) {
+    if (threadIdx.x == 0) S.sel_cnt[lr * S.max_chunks + blockIdx.x] = s_total;
+    return;
   }
+  int32_t* out = rd.maps + (size_t)S.p * S.map_stride;
+  if (sel) out[s_base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u))] = i;
+  if (threadIdx.x == 0 && (int)blockIdx.x == max(nchunk, 1) - 1) S.ctrl->send_size[lr][S.p] = s_base + s_total;
 }
 
 // One warp per local rank (lane 0): size -> receiver, wait own size, grant
@@ -897,7 +911,10 @@ cudaError_t max_coresident(int layout, int* x_blocks, int* f_blocks) {
 
 cudaError_t launch_select(const SelParams& s, int n_local, cudaStream_t st) {
   void* args[] = {(void*)&s};
-  return cudaLaunchKernel((const void*)k_select, dim3(n_local), dim3(1024), args, 0, st);
+  const dim3 grid((unsigned)std::max(1, s.max_chunks), (unsigned)n_local);
+  cudaError_t e = cudaLaunchKernel((const void*)k_select<false>, grid, dim3(1024), args, 0, st);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernel((const void*)k_select<true>, grid, dim3(1024), args, 0, st);
 }
 
 cudaError_t launch_handshake(const HsParams& h, cudaStream_t st) {

@@ -15,8 +15,9 @@
 //     k_plan_org_home / k_plan_org_pulse(q): the origin of every row (a home row of a
 //       rank of this group, or the LL unit in which it entered the group) and the
 //       pulses whose +L shift it picked up since (R25), pulses in order;
-//     k_plan_x<false/true>: per (pulse, local rank) the send entries cut into items at
-//       every change of dependency class and every R rows (count, then write).
+//     k_plan_x<0/1/2>: the send entries of every (pulse, local rank) cut into items at
+//       every change of dependency class and every R rows (chunked: last class changes,
+//       counts, then write).
 //   f (Alg. 5/6, trees):
 //     k_plan_child: the inverse maps (row t of rank l is entry i of map q);
 //     k_plan_roots: which rows root a tree and its class (a depth-first walk, children
@@ -108,85 +109,118 @@ __global__ void k_plan_org_pulse(const PlanDev* __restrict__ D, int q) {
 }
 
 // ------------------------------------------------------------------ x items
-// One CTA per (pulse p, local rank l): the map's entries in order; an item starts at
-// every change of class and every R entries within a run of one class (the host's
-// build_ll_x).  kWrite = false: items per class -> xcnt; true: every entry's XEnt and,
-// by the item's last entry, its XRec, at item xoff[class][p][l] + (index in class).
-template <bool kWrite>
+// The send entries of (pulse p, local rank l), map order, cut into items at every change
+// of dependency class and every R entries within a run of one class (the host's
+// build_ll_x).  kPB entries per CTA (blockIdx.x = chunk, blockIdx.y = p * L + l); three
+// passes so that no CTA walks a whole map:
+//   A: the last class change in each chunk (xlast[pl][c]);
+//   B: with the run start carried from the chunks before (max of their last changes),
+//      the item starts per class (xcnt totals, xccnt per chunk) and the last start;
+//   C: with every carry (run start, item start, items per class before the chunk), each
+//      entry's XEnt and, by each item's last entry, its XRec, at item
+//      xoff[class][p][l] + (index in class).
+__device__ __forceinline__ int plan_x_cls(const uint64_t* org, const int32_t* m, int k) {
+  return (int)org_cls(org[m[k]]);
+}
+
+template <int kPass>
 __global__ void __launch_bounds__(kPB) k_plan_x(const PlanDev* __restrict__ D) {
-  const int p = blockIdx.x, l = blockIdx.y;
+  const int pl = blockIdx.y, p = pl / D->L, l = pl % D->L, c = blockIdx.x;
   const PlanLQ& a = D->lq[l][p];
   const int n = a.send_size, R = D->R, nc = D->P + 1;
+  const int k = c * kPB + threadIdx.x;
+  if (c * kPB >= max(n, 1)) return;  // (uniform per CTA)
   const int32_t* m = D->maps[l] + (size_t)p * D->map_stride;
   const uint64_t* org = D->org + (size_t)l * D->cap;
+  const size_t cb = (size_t)pl * D->xnch;  // this (p, l)'s chunk records
   __shared__ int s_w[kMaxP + 1][kPB / 32];
   __shared__ int s_mx[kPB / 32];
   __shared__ int s_tot[kMaxP + 1];
-  __shared__ int s_cnt[kMaxP + 1];
-  __shared__ int s_carry[3];  // run start, item start, class of the previous chunk's last entry
+  __shared__ int s_carry[2 + kMaxP + 1];  // run start, item start, items per class before this chunk
   __shared__ uint8_t s_cls[kPB + 1];
-  if (threadIdx.x <= kMaxP) s_cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { s_carry[0] = -1; s_carry[1] = -1; s_carry[2] = -1; }
-  __syncthreads();
-  for (int base = 0; base < n; base += kPB) {
-    const int k = base + threadIdx.x;
-    const bool valid = k < n;
-    const uint64_t o = valid ? org[m[k]] : 0;
-    const int cls = valid ? (int)org_cls(o) : 0;
-    s_cls[threadIdx.x] = (uint8_t)cls;
-    if (threadIdx.x == 0) s_cls[kPB] = (k + kPB < n) ? (uint8_t)org_cls(org[m[k + kPB]]) : 0xffu;
-    __syncthreads();
-    const int prev = threadIdx.x == 0 ? s_carry[2] : (int)s_cls[threadIdx.x - 1];
-    const bool change = valid && (k == 0 || cls != prev);
-    const int runstart = max(block_scan_max(change ? k : -1, s_mx), s_carry[0]);
-    const bool start = valid && (change || (k - runstart) % R == 0);
-    const int istart = max(block_scan_max(start ? k : -1, s_mx), s_carry[1]);
-    const int idx = block_count_class(start, cls, nc, s_w, s_tot);  // inclusive count of my class's starts
-    if (kWrite && valid) {
-      const int item = D->xoff[cls][p][l] + s_cnt[cls] + idx - 1;
-      char* blk = D->xblk + (size_t)item * D->XB;
-      const int e = k - istart;
-      XEnt E;
-      E.row = (uint32_t)(o & 0xffffffu);
-      E.l = (uint8_t)((o >> 24) & 0xffu);
-      E.kq = (uint8_t)((o >> 32) & 0xffu);
-      E.mask = (uint8_t)(((o >> 40) & 0xffu) | (a.wraps ? 1u << p : 0u));
-      E.pad = 0;
-      reinterpret_cast<XEnt*>(blk + 128)[e] = E;
-      // the item's last entry writes its record
-      const int ncls = threadIdx.x == kPB - 1 ? (int)s_cls[kPB] : (int)s_cls[threadIdx.x + 1];
-      const bool last = k + 1 == n || ncls != cls || (k + 1 - runstart) % R == 0;
-      if (last) {
-        XRec r;
-        memset(&r, 0, sizeof r);
-        r.kind = kItemXSend;
-        r.pulse = (uint8_t)p;
-        r.lrank = (uint16_t)l;
-        r.n_units = (uint32_t)(e + 1) * D->W;
-        r.begin = (uint32_t)istart;
-        r.cls = (uint32_t)cls;
-        r.dst_x = a.rcv_l >= 0 ? a.dst_x : nullptr;
-        r.dst_ll = a.rcv_l >= 0 ? nullptr : a.dst_ll;
-        for (int q = 0; q < kMaxP; ++q) {
-          r.shiftL[q] = D->shiftL[q];
-          r.pdim[q] = D->pdim[q];
-        }
-        r.epoch = D->epoch;
-        *reinterpret_cast<XRec*>(blk) = r;
-      }
+  const bool valid = k < n;
+  const uint64_t o = valid ? org[m[k]] : 0;
+  const int cls = valid ? (int)org_cls(o) : 0;
+  s_cls[threadIdx.x] = (uint8_t)cls;
+  if (threadIdx.x == 0) s_cls[kPB] = (k + kPB < n) ? (uint8_t)plan_x_cls(org, m, k + kPB) : 0xffu;
+  if (kPass > 0 && threadIdx.x < 32) {  // carries from the chunks before this one
+    int rs = -1, is = -1;
+    for (int j = threadIdx.x; j < c; j += 32) {
+      rs = max(rs, D->xlast[cb + j]);
+      if (kPass == 2) is = max(is, D->xlstart[cb + j]);
     }
-    __syncthreads();
-    if (threadIdx.x == kPB - 1 || k == n - 1) {  // carries to the next chunk (the chunk's last valid entry)
-      if (valid && (k == n - 1 || threadIdx.x == kPB - 1)) {
-        s_carry[0] = runstart;
-        s_carry[1] = istart;
-        s_carry[2] = cls;
-      }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) {
+      rs = max(rs, __shfl_xor_sync(0xffffffffu, rs, o2));
+      is = max(is, __shfl_xor_sync(0xffffffffu, is, o2));
     }
-    if (threadIdx.x < nc) s_cnt[threadIdx.x] += s_tot[threadIdx.x];
-    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_carry[0] = rs;
+      s_carry[1] = is;
+    }
+    if (kPass == 2)
+      for (int cc = 0; cc < nc; ++cc) {
+        int t = 0;
+        for (int j = threadIdx.x; j < c; j += 32) t += D->xccnt[(cb + j) * (kMaxP + 1) + cc];
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o2);
+        if (threadIdx.x == 0) s_carry[2 + cc] = t;
+      }
   }
-  if (!kWrite && threadIdx.x < nc) D->xcnt[((size_t)p * D->L + l) * nc + threadIdx.x] = s_cnt[threadIdx.x];
+  __syncthreads();
+  const int prev = threadIdx.x == 0 ? (k > 0 && valid ? plan_x_cls(org, m, k - 1) : -1) : (int)s_cls[threadIdx.x - 1];
+  const bool change = valid && (k == 0 || cls != prev);
+  if (kPass == 0) {
+    const int lc = block_scan_max(change ? k : -1, s_mx);
+    if (threadIdx.x == kPB - 1) D->xlast[cb + c] = lc;
+    return;
+  }
+  const int runstart = max(block_scan_max(change ? k : -1, s_mx), s_carry[0]);
+  const bool start = valid && (change || (k - runstart) % R == 0);
+  if (kPass == 1) {
+    const int ls = block_scan_max(start ? k : -1, s_mx);
+    (void)block_count_class(start, cls, nc, s_w, s_tot);
+    if (threadIdx.x == kPB - 1) D->xlstart[cb + c] = ls;
+    if (threadIdx.x < nc) {
+      D->xccnt[(cb + c) * (kMaxP + 1) + threadIdx.x] = s_tot[threadIdx.x];
+      if (s_tot[threadIdx.x]) atomicAdd(&D->xcnt[((size_t)p * D->L + l) * nc + threadIdx.x], s_tot[threadIdx.x]);
+    }
+    return;
+  }
+  const int istart = max(block_scan_max(start ? k : -1, s_mx), s_carry[1]);
+  const int idx = block_count_class(start, cls, nc, s_w, s_tot);  // inclusive count of my class's starts
+  if (!valid) return;
+  const int item = D->xoff[cls][p][l] + s_carry[2 + cls] + idx - 1;
+  char* blk = D->xblk + (size_t)item * D->XB;
+  const int e = k - istart;
+  XEnt E;
+  E.row = (uint32_t)(o & 0xffffffu);
+  E.l = (uint8_t)((o >> 24) & 0xffu);
+  E.kq = (uint8_t)((o >> 32) & 0xffu);
+  E.mask = (uint8_t)(((o >> 40) & 0xffu) | (a.wraps ? 1u << p : 0u));
+  E.pad = 0;
+  reinterpret_cast<XEnt*>(blk + 128)[e] = E;
+  // the item's last entry writes its record
+  const int ncls = (int)s_cls[threadIdx.x + 1];
+  const bool last = k + 1 == n || ncls != cls || (k + 1 - runstart) % R == 0;
+  if (last) {
+    XRec r;
+    memset(&r, 0, sizeof r);
+    r.kind = kItemXSend;
+    r.pulse = (uint8_t)p;
+    r.lrank = (uint16_t)l;
+    r.n_units = (uint32_t)(e + 1) * D->W;
+    r.begin = (uint32_t)istart;
+    r.cls = (uint32_t)cls;
+    r.dst_x = a.rcv_l >= 0 ? a.dst_x : nullptr;
+    r.dst_ll = a.rcv_l >= 0 ? nullptr : a.dst_ll;
+    for (int q = 0; q < kMaxP; ++q) {
+      r.shiftL[q] = D->shiftL[q];
+      r.pdim[q] = D->pdim[q];
+    }
+    r.epoch = D->epoch;
+    *reinterpret_cast<XRec*>(blk) = r;
+  }
 }
 
 // ------------------------------------------------------------------ f trees
@@ -393,11 +427,13 @@ __global__ void __launch_bounds__(kPB) k_plan_f(const PlanDev* __restrict__ D) {
 // ------------------------------------------------------------------ launchers
 static unsigned plan_gx(int rows) { return (unsigned)std::max(1, std::min(64, (rows + 255) / 256)); }
 
-cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st) {
+cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st) {
   const unsigned gx = plan_gx(max_rows);
   k_plan_org_home<<<dim3(gx, L), 256, 0, st>>>(D);
   for (int q = 0; q < P; ++q) k_plan_org_pulse<<<dim3(gx, L), 256, 0, st>>>(D, q);
-  k_plan_x<false><<<dim3(P, L), kPB, 0, st>>>(D);
+  const unsigned xnch = (unsigned)((max_send + kPB - 1) / kPB);
+  k_plan_x<0><<<dim3(std::max(1u, xnch), P * L), kPB, 0, st>>>(D);
+  k_plan_x<1><<<dim3(std::max(1u, xnch), P * L), kPB, 0, st>>>(D);
   k_plan_child<<<dim3(gx, L * P), 256, 0, st>>>(D);
   const unsigned nblk = (unsigned)((max_rows + kPB - 1) / kPB);
   k_plan_roots<<<dim3(nblk, L), kPB, 0, st>>>(D);
@@ -405,8 +441,9 @@ cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st) {
-  k_plan_x<true><<<dim3(P, L), kPB, 0, st>>>(D);
+cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st) {
+  const unsigned xnch = (unsigned)((max_send + kPB - 1) / kPB);
+  k_plan_x<2><<<dim3(std::max(1u, xnch), P * L), kPB, 0, st>>>(D);
   const unsigned nblk = (unsigned)((max_rows + kPB - 1) / kPB);
   k_plan_f<true><<<dim3(nblk, L), kPB, 0, st>>>(D);
   k_plan_f<false><<<dim3(nblk, L), kPB, 0, st>>>(D);

@@ -49,8 +49,8 @@ cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, c
 cudaError_t launch_seg_copy(const SegCopy* segs, int nseg, size_t max_words, cudaStream_t st);
 cudaError_t launch_ns_x(const NsXParams& X, int layout, int max_rows, cudaStream_t st);
 cudaError_t launch_ns_wait(const NsWaitParams& W, cudaStream_t st);
-cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st);
-cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, cudaStream_t st);
+cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st);
+cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st);
 int plan_rows_per_cta();
 uint32_t ll_xblk_bytes(int rows);
 uint32_t ll_fblk_bytes(int rows);
@@ -169,6 +169,7 @@ struct halo_ctx {
   int n_tail_f = 0;                 // LL: shift-force combine items at the end of the f list
   double* d_fshift_tmp = nullptr;  // halo_step_host
   char* h_small = nullptr;          // pinned 64 KiB: set_maps result read-backs and small uploads
+  int32_t* d_selcnt = nullptr;      // set_maps select: rows per 1024-row chunk
   // halo_step_host_packed: packed staging in / out, segment tables (x unpack | f unpack | pack),
   // rebuilt once per NS epoch; side streams for the f upload and the halo-x download
   char* d_pk_in = nullptr;
@@ -474,6 +475,8 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_fshift_tmp, sizeof(double) * 9 * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_small, 64 * 1024);
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_small, 64 * 1024);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&ctx->d_selcnt, sizeof(int32_t) * ctx->n_local * ((cfg->capacity + 1023) / 1024 + 1));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_mig, sizeof(MigRank) * ctx->n_local);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_migctrl, sizeof(MigCtrl));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_planes, sizeof(double) * 3 * (kMaxRanks + 1));
@@ -1333,14 +1336,17 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
     CK(cudaMallocHost(&ctx->h_pl, sizeof(PlanDev)));
     CK(cudaMallocHost(&ctx->h_pl_cnt, sizeof(int32_t) * (kMaxP + 1) * (kMaxP + 1) * kMaxLocal));
   }
-  int max_rows = 1;
+  int max_rows = 1, max_send = 1;
   for (int l = 0; l < L; ++l) max_rows = std::max(max_rows, ctx->n_total[l]);
+  for (int i = 0; i < L * P; ++i) max_send = std::max(max_send, ctx->send_size[i]);
   const int nblk = (max_rows + plan_rows_per_cta() - 1) / plan_rows_per_cta();
+  const int xnch = (max_send + plan_rows_per_cta() - 1) / plan_rows_per_cta();
+  const size_t sxc = align_up(sizeof(int32_t) * (size_t)P * L * xnch * (2 + kMaxP + 1), 256);
   const size_t so = align_up(sizeof(uint64_t) * L * cap, 256), sc = align_up(sizeof(int32_t) * L * cap * P, 256),
                sr = align_up(2 * L * cap, 256), sk = align_up(2 * sizeof(int32_t) * L * nblk * (P + 1), 256),
                si = align_up(sizeof(uint32_t) * (L * cap / 8 + (size_t)(kMaxP + 1) * L + 1), 256),
                sx = align_up(sizeof(int32_t) * (P * L + L) * (P + 1), 256);
-  const size_t sbytes = so + sc + sr + sk + sx + si;
+  const size_t sbytes = so + sc + sr + sk + sx + si + sxc;
   if (sbytes > ctx->pl_scratch_bytes) {
     if (ctx->d_pl_scratch) CK(cudaFree(ctx->d_pl_scratch));
     ctx->d_pl_scratch = nullptr;
@@ -1394,13 +1400,18 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
   H.rcls = reinterpret_cast<uint8_t*>(sp + so + sc);
   H.rmask = H.rcls + (size_t)L * cap;
   H.imask = reinterpret_cast<uint32_t*>(sp + so + sc + sr + sk + sx);
+  H.xnch = xnch;
+  H.xlast = reinterpret_cast<int32_t*>(sp + so + sc + sr + sk + sx + si);
+  H.xlstart = H.xlast + (size_t)P * L * xnch;
+  H.xccnt = H.xlstart + (size_t)P * L * xnch;
   H.bcnt = reinterpret_cast<int32_t*>(sp + so + sc + sr);
   H.boff = H.bcnt + (size_t)L * nblk * (P + 1);
   H.xcnt = reinterpret_cast<int32_t*>(sp + so + sc + sr + sk);
   H.rcnt = H.xcnt + (size_t)P * L * (P + 1);
   CK(cudaMemcpyAsync(ctx->d_pl, &H, sizeof(PlanDev), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(H.child, 0xff, sizeof(int32_t) * L * cap * P, st));
-  CK(launch_plan_count(ctx->d_pl, L, P, max_rows, st));
+  CK(cudaMemsetAsync(H.xcnt, 0, sizeof(int32_t) * (size_t)P * L * (P + 1), st));
+  CK(launch_plan_count(ctx->d_pl, L, P, max_rows, max_send, st));
   const size_t ncnt = (size_t)(P * L + L) * (P + 1);
   CK(cudaMemcpyAsync(ctx->h_pl_cnt, H.xcnt, sizeof(int32_t) * ncnt, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1487,7 +1498,7 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
                          recv.size(), cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemsetAsync(H.imask, 0, sizeof(uint32_t) * nf, st));
-  CK(launch_plan_write(ctx->d_pl, L, P, max_rows, st));
+  CK(launch_plan_write(ctx->d_pl, L, P, max_rows, max_send, st));
   ctx->n_tail_f = 0;
   if (prof) prof->lap("plan:write");
   if (getenv("HALO_PLAN_CHECK")) return plan_check(ctx, st);
@@ -1908,6 +1919,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
       S.epoch = ctx->epoch;
       S.err_host = ctx->err_dev;
       S.timeout_ns = timeout_ns;
+      S.max_chunks = (ctx->cfg.capacity + 1023) / 1024;
+      S.sel_cnt = ctx->d_selcnt;
       for (int l = 0; l < L; ++l) {
         const int r = ctx->first_rank + l;
         for (int q = 0; q < p; ++q)
@@ -3058,6 +3071,7 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->d_pk_out) (void)cudaFree(ctx->d_pk_out);
   if (ctx->d_segs) (void)cudaFree(ctx->d_segs);
   if (ctx->h_small) (void)cudaFreeHost(ctx->h_small);
+  if (ctx->d_selcnt) (void)cudaFree(ctx->d_selcnt);
   if (ctx->d_pl) (void)cudaFree(ctx->d_pl);
   if (ctx->h_pl) (void)cudaFreeHost(ctx->h_pl);
   if (ctx->h_pl_cnt) (void)cudaFreeHost(ctx->h_pl_cnt);
