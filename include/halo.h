@@ -377,12 +377,11 @@ HALO_API halo_status halo_packed_sizes(const halo_ctx* ctx, size_t* in_bytes, si
  *       of every local rank, then at the next 8-B aligned offset the shift
  *       forces, n_local*9 doubles ([local][dim][component], zeroed each step).
  * Two uploads (x home, then the forces on a library-owned side stream while x
- * is exchanged), one download of the halo x (side stream, while f is
- * exchanged); the forces and fshift are written by the last copy kernel
- * straight into `out` when it is device-accessible pinned memory
- * (cudaHostAlloc / torch pin_memory), else staged and downloaded
- * (HALO_PACKED_STAGED=1 forces that).  Packing to and from the per-rank rows
- * is done by a copy kernel.  Enqueued on `stream`; synchronises it.  Not
+ * is exchanged), two downloads (halo x on a side stream while f is exchanged,
+ * then the forces and fshift); packing to and from the per-rank rows is done
+ * by a copy kernel.  HALO_PACKED_DIRECT=1: the last copy kernel writes the
+ * forces straight into `out` when it is device-accessible pinned memory
+ * (measured slower).  Enqueued on `stream`; synchronises it.  Not
  * graph-capturable. */
 HALO_API halo_status halo_step_host_packed(halo_ctx* ctx, const void* in, void* out, void* stream);
 

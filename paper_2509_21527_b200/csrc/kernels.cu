@@ -581,8 +581,24 @@ __global__ void __launch_bounds__(256) k_ns_x(const __grid_constant__ NsXParams 
   const int32_t* map = rd.maps + (size_t)X.p * X.map_stride;
   float* dst = X.dst_x[lr] + (size_t)ro * W;
   const bool sh = X.has_shift[lr] != 0;
+  // the dependency mask of the pulse (which earlier receive ranges the map reads, R9)
+  // and the entries < n_home (depOffset split, R8), on the way
+  unsigned dm = 0;
+  int indep = 0;
+  bool bad = false;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const float* src = rd.x + (size_t)map[i] * W;
+    const int idx = map[i];
+    if (idx < rd.n_home) {
+      ++indep;
+    } else {
+      bool found = false;
+      for (int q = 0; q < X.p; ++q) {
+        const int a0 = X.ctrl->atom_offset[lr][q], r0 = X.ctrl->recv_size[lr][q];
+        if (idx >= a0 && idx < a0 + r0) { dm |= 1u << q; found = true; break; }
+      }
+      bad |= !found;
+    }
+    const float* src = rd.x + (size_t)idx * W;
     float v[W];
 #pragma unroll
     for (int c = 0; c < W; ++c) v[c] = src[c];
@@ -593,6 +609,32 @@ __global__ void __launch_bounds__(256) k_ns_x(const __grid_constant__ NsXParams 
 #pragma unroll
     for (int c = 0; c < W; ++c) dst[(size_t)i * W + c] = v[c];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dm |= __shfl_xor_sync(0xffffffffu, dm, o);
+    indep += __shfl_xor_sync(0xffffffffu, indep, o);
+  }
+  const bool anybad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (dm) atomicOr(&X.ctrl->dep[lr][X.p], dm);
+    if (indep) atomicAdd(&X.ctrl->n_indep[lr][X.p], indep);
+    if (anybad) atomicOr(&X.ctrl->err[lr], kErrMap);
+  }
+}
+
+// set_maps start: zero the LL receive areas of every local rank (one launch).
+__global__ void k_zero_ll(uint64_t* const* base, size_t units, int n) {
+  const int l = blockIdx.y;
+  if (l >= n) return;
+  uint4* p = reinterpret_cast<uint4*>(base[l]);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < units / 2; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(0, 0, 0, 0);
+}
+
+cudaError_t launch_zero_ll(uint64_t* const* base_dev, size_t units, int n, cudaStream_t st) {
+  if (n <= 0 || units == 0) return cudaSuccess;
+  k_zero_ll<<<dim3(64, n), 256, 0, st>>>(base_dev, units, n);
+  return cudaGetLastError();
 }
 
 __global__ void k_ns_flag(const __grid_constant__ NsXParams X) {

@@ -48,6 +48,7 @@ cudaError_t launch_ce_sync(const CeSyncParams& s, cudaStream_t st);
 cudaError_t launch_bw_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
 cudaError_t launch_seg_copy(const SegCopy* segs, int nseg, size_t max_words, cudaStream_t st);
 cudaError_t launch_ns_x(const NsXParams& X, int layout, int max_rows, cudaStream_t st);
+cudaError_t launch_zero_ll(uint64_t* const* base_dev, size_t units, int n, cudaStream_t st);
 cudaError_t launch_ns_wait(const NsWaitParams& W, cudaStream_t st);
 cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st);
 cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st);
@@ -1630,6 +1631,12 @@ static int grid_for(int n_items, int n_local, int max_blocks) {
 }
 
 // Pull the set_maps results of every local rank back to the host.
+// ctx->h_small (pinned 64 KiB) regions: set_maps result read-back (and the seq read-back
+// after it) | reset upload | LL-area table | planes
+constexpr size_t kPinResults = 0, kPinReset = 16384, kPinLLTab = 20480, kPinPlanes = 24576;
+static_assert(offsetof(Ctrl, agreed_err) + sizeof(int32_t) * kMaxLocal - offsetof(Ctrl, send_size) <= kPinReset,
+              "pinned result region");
+
 static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st, int32_t* agreed = nullptr) {
   const int L = ctx->n_local, P = ctx->P;
   // the set_maps result arrays are contiguous in Ctrl (through agreed_err): one copy
@@ -1638,7 +1645,7 @@ static halo_status pull_ctrl(halo_ctx* ctx, cudaStream_t st, int32_t* agreed = n
                     offsetof(Ctrl, agreed_err) > offsetof(Ctrl, n_total),
                 "set_maps result block layout");
   const size_t lo = offsetof(Ctrl, send_size), hi = offsetof(Ctrl, agreed_err) + sizeof(ctx->ctrl->agreed_err);
-  char* hb = ctx->h_small;  // pinned; viewed as a Ctrl shifted by lo
+  char* hb = ctx->h_small + kPinResults;  // pinned; viewed as a Ctrl shifted by lo
   const Ctrl& h = *reinterpret_cast<const Ctrl*>(hb - lo);
   cudaError_t e = cudaMemcpyAsync(hb, reinterpret_cast<const char*>(ctx->ctrl) + lo, hi - lo, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -1836,17 +1843,21 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     // memory (stream-ordered before the first select: no synchronisation)
     CK(cudaMemsetAsync(ctx->ctrl->send_size, 0, offsetof(Ctrl, n_total) - offsetof(Ctrl, send_size), st));
     static_assert(offsetof(Ctrl, err) == offsetof(Ctrl, n_total) + sizeof(int32_t) * kMaxLocal, "n_total | err");
-    memcpy(ctx->h_small, nt, sizeof nt);
-    memcpy(ctx->h_small + sizeof nt, errs, sizeof errs);
-    CK(cudaMemcpyAsync(ctx->ctrl->n_total, ctx->h_small, sizeof nt + sizeof errs, cudaMemcpyHostToDevice, st));
+    char* pin = ctx->h_small + kPinReset;
+    memcpy(pin, nt, sizeof nt);
+    memcpy(pin + sizeof nt, errs, sizeof errs);
+    CK(cudaMemcpyAsync(ctx->ctrl->n_total, pin, sizeof nt + sizeof errs, cudaMemcpyHostToDevice, st));
     for (int l = 0; l < L; ++l) ctx->n_total[l] = nt[l];
   }
   ctx->n_home.assign(ctx->n_total.begin(), ctx->n_total.end());
   // LL areas zeroed every NS epoch (ll_seq_next): no peer writes them before the
   // pulse-0 handshake below, which this stream reaches only after the memset
-  if ((ctx->ll || ctx->auto_tr) && !getenv("HALO_AB_NO_LLZERO"))
-    for (int l = 0; l < L; ++l)
-      CK(cudaMemsetAsync(ctx->xll_of(ctx->first_rank + l), 0, sizeof(uint64_t) * 2 * (size_t)P * ctx->ll_stride, st));
+  if (ctx->ll || ctx->auto_tr) {
+    uint64_t** tab = reinterpret_cast<uint64_t**>(ctx->h_small + kPinLLTab);  // pinned
+    for (int l = 0; l < L; ++l) tab[l] = ctx->xll_of(ctx->first_rank + l);
+    CK(cudaMemcpyAsync(ctx->d_small + 16384, tab, sizeof(uint64_t*) * L, cudaMemcpyHostToDevice, st));
+    CK(launch_zero_ll(reinterpret_cast<uint64_t* const*>(ctx->d_small + 16384), 2 * (size_t)P * ctx->ll_stride, L, st));
+  }
   fill_rank_dev(ctx);
   // ranks/pulse tables are needed by the select/depmask kernels already
   ctx->h_items_x.clear();
@@ -1866,8 +1877,11 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
         blo[3 * l + dd] = ctx->plane(dd, ctx->cell(ctx->first_rank + l, dd));
         bhi[3 * l + dd] = ctx->plane(dd, ctx->cell(ctx->first_rank + l, dd) + 1);
       }
-    CK(cudaMemcpyAsync(sm + 4096, blo.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(sm + 8192, bhi.data(), sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
+    double* pin = reinterpret_cast<double*>(ctx->h_small + kPinPlanes);  // pinned: [blo | bhi], 4 KiB each
+    memcpy(pin, blo.data(), sizeof(double) * 3 * L);
+    memcpy(pin + 512, bhi.data(), sizeof(double) * 3 * L);
+    CK(cudaMemcpyAsync(sm + 4096, pin, sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(sm + 8192, pin + 512, sizeof(double) * 3 * L, cudaMemcpyHostToDevice, st));
   }
   // Per pulse, all stream-ordered on the device (no host round trip): select (fp64
   // predicate + compaction) -> handshake (sizes / offsets with the neighbours) ->
@@ -1943,8 +1957,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
       H.size_dst[l] = &ctx->hdr_of(ctx->neighbour(r, d, -1))->meta_size[p];
       H.off_dst[l] = &ctx->hdr_of(ctx->neighbour(r, d, +1))->meta_off[p];
     }
-    CK(launch_handshake(H, st));
-    CK(launch_depmask(ctx->d_ranks, ctx->ctrl, p, (int)ctx->map_stride, L, st));
+    CK(launch_handshake(H, st));  // (dependency masks: in k_ns_x below)
     if (maps) {  // the next pulse's host validation needs n_total
       if ((s = pull_ctrl(ctx, st)) != HALO_OK) return s;
       if ((s = check_err_word(ctx)) != HALO_OK) return s;
@@ -2700,7 +2713,7 @@ halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_
   halo_status s;
   // a device-accessible (mapped pinned) output block takes the forces directly
   char* out_dev = nullptr;
-  if (out_host && !getenv("HALO_PACKED_STAGED")) {
+  if (out_host && getenv("HALO_PACKED_DIRECT")) {  // measured slower than staging + one copy (C3: 184 vs 130 us)
     cudaPointerAttributes pa{};
     if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
       out_dev = static_cast<char*>(pa.devicePointer);

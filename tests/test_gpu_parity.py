@@ -237,13 +237,14 @@ def test_step_host_e2e():
     sess.destroy()
 
 
-@pytest.mark.parametrize("staged", [False, True])
+@pytest.mark.parametrize("direct", [False, True])
 @pytest.mark.parametrize("cfg", ["C2", "C3", "T2P"])
-def test_step_host_packed_e2e(cfg, staged, monkeypatch):
+def test_step_host_packed_e2e(cfg, direct, monkeypatch):
     """halo_step_host_packed (one host block in, one out) == the oracle, twice in a row;
-    forces written straight into the mapped output block, or (staged) downloaded."""
-    if staged:
-        monkeypatch.setenv("HALO_PACKED_STAGED", "1")
+    forces staged and downloaded (default), or (direct) written by the last kernel
+    straight into the mapped output block."""
+    if direct:
+        monkeypatch.setenv("HALO_PACKED_DIRECT", "1")
     case = Case(cfg, seed=2, force_kind="int")
     sess = session_for(case)
     run_gpu_case(case, sess, check_forces=False)
