@@ -633,6 +633,23 @@ def run_fused(args, rank, world, local):
         out["latency_floor"] = floor
     floor["launch_us_eager"] = round(launch_eager, 3)
     floor["launch_us_graph"] = round(launch_graph, 3)
+    if not args.no_floors:
+        # the step's fixed cost: the same loop as the timed step (flush, reset, events)
+        # around two EMPTY kernels with the x / f grids and launch attributes
+        evp = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(min(K, 300))]
+        for k in range(-args.warmup, len(evp)):
+            flush.fill_(1.0)
+            reset_f()
+            if k >= 0:
+                evp[k][0].record(stream)
+            sess.halo.floor_empty_pair(stream.cuda_stream)
+            if k >= 0:
+                evp[k][1].record(stream)
+        torch.cuda.synchronize()
+        floor["empty_step_us"] = round(max_over_ranks(float(np.mean([a.elapsed_time(b) * 1e3 for a, b in evp]))), 3)
+        floor["empty_step_note"] = ("two empty kernels with the x / f grids and PDL attributes, timed like the step "
+                                    "(L2 flush + f reset before each, events around): the launch / drain / hand-off "
+                                    "cost every two-launch step pays")
     if floor.get("t0_one_way_us"):
         t0 = floor["t0_one_way_us"]
         bwd = floor.get("bandwidth") or {}

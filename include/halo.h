@@ -65,6 +65,8 @@ typedef enum {
 } halo_status;
 
 /* Flags (halo_config.flags). */
+#define HALO_F_DETERMINISTIC  0u        /* the default (no bit): forces added in the oracle's fixed order
+                                           (pulses descending, one fp32 RNE add per image), bit-exact (R15) */
 #define HALO_F_ATOMIC_UNPACK  (1u << 0) /* unordered f unpack (paper's atomicAdd); default is the
                                            deterministic pulse-descending order (bit-exact vs oracle, R15) */
 #define HALO_F_NO_HOME_CHECK  (1u << 1) /* skip the "home atoms lie in their cell" check in halo_set_maps */
@@ -428,6 +430,12 @@ HALO_API halo_status halo_floor_pingpong(halo_ctx* ctx, int peer_rank, int iters
  * (regular launch + programmatic dependent launch), `iters` launches between
  * two events on an internal stream; graph = 1 captures them in a CUDA graph and
  * times its replay.  Synchronises. */
+/* Launch floor of one step: enqueues on `stream` two EMPTY kernels with the grids
+ * and launch attributes of the current exchange_x / exchange_f launches (PDL), so a
+ * caller can time the step's fixed cost (launch, grid drain, hand-off) with the
+ * same events, flush and reset as the real step.  HALO_ERR_STATE before set_maps. */
+HALO_API halo_status halo_floor_empty_pair(halo_ctx* ctx, void* stream);
+
 HALO_API halo_status halo_floor_launch(halo_ctx* ctx, int iters, int graph, double* us_per_launch);
 
 /* Launch floor of a kernel that wrote to (NVLink) peer memory: as

@@ -14,6 +14,7 @@ STATUS_NAMES = {0: "HALO_OK", 1: "HALO_ERR_ARG", 2: "HALO_ERR_GEOMETRY", 3: "HAL
                 4: "HALO_ERR_STATE", 5: "HALO_ERR_CUDA", 6: "HALO_ERR_PEER", 7: "HALO_ERR_TIMEOUT",
                 8: "HALO_ERR_UNSUPPORTED"}
 
+HALO_F_DETERMINISTIC = 0  # the default: the oracle's accumulation order, bit-exact (R15)
 HALO_F_ATOMIC_UNPACK = 1 << 0
 HALO_F_NO_HOME_CHECK = 1 << 1
 HALO_F_GPU_FENCE = 1 << 2
@@ -35,7 +36,7 @@ EXPORTS = [
     "halo_get_map", "halo_assign_home", "halo_migrate", "halo_transport", "halo_pme_reserve", "halo_pme_setup",
     "halo_pme_buffers", "halo_pme_send_x", "halo_pme_recv_f", "halo_exchange_x", "halo_exchange_f", "halo_exchange_xf", "halo_nccl_unique_id", "halo_nccl_init", "halo_nccl_version", "halo_nccl_exchange_x",
     "halo_nccl_exchange_f", "halo_step_host", "halo_packed_sizes", "halo_step_host_packed", "halo_pack_x_pulse",
-    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_launch_remote", "halo_floor_bandwidth", "halo_probe_reserve", "halo_floor_payload", "halo_floor_bandwidth_multi", "halo_sync", "halo_strerror",
+    "halo_unpack_f_pulse", "halo_get_timers", "halo_get_trace", "halo_get_notify_counts", "halo_floor_pingpong", "halo_floor_launch", "halo_floor_empty_pair", "halo_floor_launch_remote", "halo_floor_bandwidth", "halo_probe_reserve", "halo_floor_payload", "halo_floor_bandwidth_multi", "halo_sync", "halo_strerror",
     "halo_last_error", "halo_destroy",
 ]
 
@@ -99,6 +100,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "halo_get_notify_counts": ([P, c_int, POINTER(c_uint), c_int], c_int),
         "halo_floor_pingpong": ([P, c_int, c_int, c_int, POINTER(c_double)], c_int),
         "halo_floor_launch": ([P, c_int, c_int, POINTER(c_double)], c_int),
+        "halo_floor_empty_pair": ([P, P], c_int),
         "halo_floor_launch_remote": ([P, c_int, c_int, c_int, c_int, POINTER(c_double)], c_int),
         "halo_floor_bandwidth": ([P, c_int, c_size_t, c_int, c_int, POINTER(c_double)], c_int),
         "halo_probe_reserve": ([P, c_size_t], c_int),

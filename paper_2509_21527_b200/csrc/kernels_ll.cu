@@ -630,10 +630,19 @@ int ll_block(int mode, bool wide) {
 }
 
 // Ring slots (item blocks in flight per CTA) and dynamic shared memory.
-int ll_ring(bool wide) { return wide ? 2 : kRing; }
+// Item blocks in flight per CTA: kRing, two in the wide (bandwidth-regime) variants,
+// whose blocks are larger (x 4.2 KiB; f up to 11 KiB with kMaxTreeRows roots): the
+// dynamic shared memory stays what the co-resident grid was computed for
+// (HALO_RING_F: the f / fused launches' ring, A/B; measured at C4-bw8: 4 is not faster).
+static int g_ring_f = 0;
+void ll_set_ring_f(int r) { g_ring_f = r <= 0 ? 0 : r < 2 ? 2 : r > kRing ? kRing : r; }
+int ll_ring(int mode, bool wide) {
+  if (mode != kModeX && g_ring_f) return g_ring_f;
+  return wide ? 2 : kRing;
+}
 size_t ll_smem_bytes(int mode, int rows, int tree_rows, bool wide) {
   const size_t sb = mode == kModeX ? xblk_bytes((uint32_t)rows) : fblk_bytes((uint32_t)tree_rows);
-  return (size_t)ll_ring(wide) * sb;
+  return (size_t)ll_ring(mode, wide) * sb;
 }
 uint32_t ll_xblk_bytes(int rows) { return xblk_bytes((uint32_t)rows); }
 uint32_t ll_fblk_bytes(int tree_rows) { return fblk_bytes((uint32_t)tree_rows); }
@@ -667,7 +676,7 @@ cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [3]: x, f, x
       if (e != cudaSuccess) return e;
       int b = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, ll_block(mode, wide),
-                                                        ll_smem_bytes(mode, rows, kTreeRowsOcc, wide));
+                                                        ll_smem_bytes(mode, rows, wide ? kMaxTreeRows : kTreeRowsOcc, wide));
       if (e != cudaSuccess) return e;
       bmin = std::min(bmin, b);
     }

@@ -38,7 +38,8 @@ cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t b
 cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
                                const cudaAccessPolicyWindow* win, cudaStream_t st, bool chk);
 cudaError_t max_coresident_ll(int layout, bool wide, int* blocks);
-int ll_ring(bool wide);
+int ll_ring(int mode, bool wide);
+void ll_set_ring_f(int r);
 void ll_set_x_variant(int v);
 cudaError_t launch_empty(int grid, cudaStream_t st, uint64_t* remote, uint32_t nwords);
 cudaError_t launch_ce_pack(int layout, const CeEnt* ents, int n_local, int max_rows, cudaStream_t st);
@@ -243,6 +244,8 @@ struct halo_ctx {
   int last_grid[2] = {0, 0};
   int item_rows = 64;
   int tree_rows = 64;               // LL: roots per small-tree f item (chosen per NS epoch, build_ll_f)
+  int tree_rows_max = kMaxTreeRows; // ... at most (more roots than fit the co-resident grid at kTreeRowsOcc:
+                                    // the bandwidth regime; two passes per thread)
   bool item_rows_fixed = false;     // HALO_ITEM_ROWS given: no adaptive choice
   uint32_t poll_ns = 0;
   uint32_t debug = 0;
@@ -458,6 +461,8 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (const char* e = getenv("HALO_PLAN_HOST")) ctx->gpu_plan = atoi(e) == 0;
   if (const char* e = getenv("HALO_TIMEOUT_S")) ctx->cfg.timeout_s = std::max(0.001, atof(e));  // sanitizer runs
   ll_set_x_variant(getenv("HALO_X_VARIANT") ? atoi(getenv("HALO_X_VARIANT")) : 0);
+  ll_set_ring_f(getenv("HALO_RING_F") ? atoi(getenv("HALO_RING_F")) : 0);
+  if (const char* e = getenv("HALO_TREE_ROWS_MAX")) ctx->tree_rows_max = std::min(kMaxTreeRows, std::max(8, atoi(e)));
   if (const char* e = getenv("HALO_DEBUG")) ctx->debug = (uint32_t)std::max(0, atoi(e));
 
   cudaError_t e = cudaSetDevice(cfg->device);
@@ -1462,7 +1467,9 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
   };
   int RT = 32;
   while (f_items(RT) > ctx->cap_f() && RT < kTreeRowsOcc) RT = std::min(kTreeRowsOcc, RT + 16);
-  if (const char* e = getenv("HALO_TREE_ROWS")) RT = std::min(kTreeRowsOcc, std::max(8, atoi(e)));
+  // bandwidth regime: fewer, larger items (two passes of kTreeRowsOcc roots per thread)
+  while (f_items(RT) > ctx->cap_f() && RT < ctx->tree_rows_max) RT = std::min(ctx->tree_rows_max, RT + 17);
+  if (const char* e = getenv("HALO_TREE_ROWS")) RT = std::min(kMaxTreeRows, std::max(8, atoi(e)));
   int nf = 0;
   for (int c = 0; c <= P; ++c)
     for (int l = 0; l < L; ++l) {
@@ -1617,7 +1624,7 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.fblk = ctx->d_fblk;
   P.item_rows = ctx->item_rows;
   P.tree_rows = ctx->tree_rows;
-  P.ring = ll_ring(ctx->wide());
+  P.ring = ll_ring(0, ctx->wide());  // (the f and fused launches set theirs)
   P.delay_rank = ctx->P ? ctx->neighbour(0, ctx->pdim[0], +1) : -1;
   P.seq_x0 = ctx->seq_x0;
   P.lbase = ctx->d_lbase;
@@ -2553,6 +2560,7 @@ halo_status halo_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, void*
   ctx->last_grid[1] = grid;
   if (ctx->ll) {
     bool cap = false;
+    F.ring = ll_ring(1, ctx->wide());
     F.seq_f = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f, &cap);
     CK(launch_exchange_ll(F, 1, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream, cap));
   }
@@ -2580,6 +2588,7 @@ halo_status halo_exchange_xf(halo_ctx* ctx, double* fshift, int accumulate, void
   grid = std::max(grid, 1);
   ctx->last_grid[0] = grid;
   bool cap = false;
+  X.ring = ll_ring(2, ctx->wide());
   X.seq = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_x, &cap);
   X.seq_f = next_seq(ctx, (cudaStream_t)stream, &ctx->seq_host_f);
   CK(launch_exchange_ll(X, 2, ctx->W, grid, ctx->wide(), &ctx->l2win, (cudaStream_t)stream, cap));
@@ -2905,6 +2914,18 @@ static halo_status floor_launch_impl(halo_ctx* ctx, int iters, int graph, uint64
   CK(cudaEventDestroy(e0));
   CK(cudaEventDestroy(e1));
   CK(cudaStreamDestroy(st));
+  return HALO_OK;
+}
+
+halo_status halo_floor_empty_pair(halo_ctx* ctx, void* stream) {
+  if (!ctx) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "floor before set_maps");
+  // the step's two launches with no work: the grids of the current x and f launches,
+  // the same programmatic-dependent-launch attributes, empty bodies
+  const int gx = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
+  const int gf = grid_for(ctx->n_items_f, ctx->n_local, ctx->cap_f());
+  CK(launch_empty(gx, (cudaStream_t)stream, nullptr, 0));
+  CK(launch_empty(gf, (cudaStream_t)stream, nullptr, 0));
   return HALO_OK;
 }
 

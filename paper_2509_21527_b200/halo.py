@@ -235,6 +235,9 @@ class Halo:
         self._ck(self.lib.halo_step_host(self.h, arr(x_home_ptrs), arr(f_all_ptrs), arr(x_halo_out_ptrs),
                                          arr(f_home_out_ptrs), c_void_p(fshift_ptr or None), c_void_p(stream)))
 
+    def floor_empty_pair(self, stream=0):
+        self._ck(self.lib.halo_floor_empty_pair(self.h, c_void_p(stream)))
+
     def packed_sizes(self):
         """(in_bytes, out_bytes) of halo_step_host_packed's host blocks for the current maps."""
         a, b = c_size_t(0), c_size_t(0)
