@@ -108,6 +108,36 @@ def as_dict(c):
 
 
 @pytest.mark.parametrize("name", SMALL)
+def test_x0_home_cell_exact_rationals(name):
+    """X0 pinned without the oracle's plane formula: the home cell of every atom is
+    floor(x * grid / L) in exact rational arithmetic (fractions.Fraction of the float32
+    values).  Where an atom lies within 1e-12 * L of a plane (the only place where the
+    double-precision planes of R3 can round differently) the oracle must put it in a
+    neighbouring cell, the higher one if it is exactly on the double plane (R4)."""
+    from fractions import Fraction
+    c, X = system(name, 1)
+    st = decompose(X, c.L, c.rc, c.grid, c.pulses)
+    home = {}
+    for s in st:
+        for g in s.gid[: s.n_home]:
+            home[int(g)] = pins.rank_cell(s.rank, c.grid)
+    assert len(home) == X.shape[0]
+    for g in range(X.shape[0]):
+        for d in range(3):
+            if c.grid[d] == 1:
+                continue
+            L = Fraction(float(np.float32(c.L[d])))
+            x = Fraction(float(X[g, d]))
+            q = x * c.grid[d] / L
+            exact = int(q)  # x >= 0: floor
+            near = abs(q - round(q)) * L / c.grid[d] < Fraction(1, 10 ** 12) * L
+            if near:
+                assert home[g][d] in (exact - 1, exact, min(exact, c.grid[d] - 1)), (g, d)
+            else:
+                assert home[g][d] == min(exact, c.grid[d] - 1), (g, d, float(q))
+
+
+@pytest.mark.parametrize("name", SMALL)
 @pytest.mark.parametrize("seed", [1, 2])
 def test_x0_x1_x4_structure_and_closed_form(name, seed):
     c, X = system(name, seed)
