@@ -421,27 +421,7 @@ def run_fused(args, rank, world, local):
         else:
             nvl_counted = {"unavailable": (nvc.err or "NVML NVLink field read failed") + " (on some rank)"}
     # the same steps as ONE fused launch each (halo_exchange_xf, LL protocol)
-    fused = None
-    if transport == "ll" and not args.no_fused:
-        for _ in range(args.warmup):
-            flush.fill_(1.0)
-            reset_f()
-            sess.exchange_xf(fshift=fshift)
-        torch.cuda.synchronize()
-        barrier()
-        evf = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
-        for k in range(K):
-            flush.fill_(float(k))
-            reset_f()
-            evf[k][0].record(stream)
-            sess.exchange_xf(fshift=fshift)
-            evf[k][1].record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        tf_ = [evf[k][0].elapsed_time(evf[k][1]) * 1e3 for k in range(K)]
-        fused = {"us_per_step": max_over_ranks(float(np.mean(tf_))),
-                 "median_us": max_over_ranks(float(np.median(tf_))),
-                 "p90_us": max_over_ranks(float(np.percentile(tf_, 90)))}
+    fused = None  # timed last (fused_timing): a failure there cannot take the other numbers with it
     sampler.stop()
     # per-kernel split (roofline): isolated steps (device idle, ranks released together by a
     # host barrier), events around each kernel, same flush discipline
@@ -601,9 +581,7 @@ def run_fused(args, rank, world, local):
                           "before each, so both launches are queued; events around each launch, i.e. no "
                           "programmatic dependent launch across the middle event), so x_us + f_us > value",
         "graph_us_per_step": None if graph_us is None else round(graph_us, 3),
-        "fused_xf": None if fused is None else {k: round(v, 3) for k, v in fused.items()} | {
-            "path": "halo_exchange_xf: x and f of the step in ONE launch; rank l's gather items start when "
-                    "l's halo rows are complete (the non-bonded kernel's slot, Alg. 2)"},
+        "fused_xf": None,
         "clocks": sampler.summary(),
         "e2e": None if e2e_us is None else {"value": round(e2e_us, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
@@ -677,10 +655,46 @@ def run_fused(args, rank, world, local):
         out["pme"] = pme_timing(sess, K, args.warmup, flush)
     if not args.no_ns:
         out["ns_step"] = ns_step_timing(sess, c, X, homes, dev)
+    if transport == "ll" and not args.no_fused:
+        out["fused_xf"] = fused_timing(sess, fshift, flush, reset_f, stream, K, args.warmup)
     if world == 1 and rank == 0 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline_leg(args, P, c)
     sess.destroy()
     return out
+
+
+def fused_timing(sess, fshift, flush, reset_f, stream, K, warmup):
+    """The same steps as ONE fused launch each (halo_exchange_xf, LL protocol; SURVEY §7
+    step 9), timed like the two-launch step.  Run last; an error is reported in the line
+    (every rank agrees on success before the reductions)."""
+    import torch
+    tf_, err = None, None
+    try:
+        for _ in range(warmup):
+            flush.fill_(1.0)
+            reset_f()
+            sess.exchange_xf(fshift=fshift)
+        torch.cuda.synchronize()
+        barrier()
+        evf = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+        for k in range(K):
+            flush.fill_(float(k))
+            reset_f()
+            evf[k][0].record(stream)
+            sess.exchange_xf(fshift=fshift)
+            evf[k][1].record(stream)
+        torch.cuda.synchronize()
+        tf_ = [evf[k][0].elapsed_time(evf[k][1]) * 1e3 for k in range(K)]
+    except Exception as e:  # noqa: BLE001 - reported, not raised
+        err = str(e)[:200]
+    ok = -max_over_ranks(-(1.0 if err is None else 0.0))  # min over ranks
+    if ok < 1.0:
+        return {"error": err or "failed on another rank"}
+    return {"us_per_step": round(max_over_ranks(float(np.mean(tf_))), 3),
+            "median_us": round(max_over_ranks(float(np.median(tf_))), 3),
+            "p90_us": round(max_over_ranks(float(np.percentile(tf_, 90))), 3),
+            "path": "halo_exchange_xf: x and f of the step in ONE launch; rank l's gather items start when "
+                    "l's halo rows are complete (the non-bonded kernel's slot, Alg. 2)"}
 
 
 def e2e_timing(sess, X, homes, F0, first, nl, W, flush, stream, K, warmup):

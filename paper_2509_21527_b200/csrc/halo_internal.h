@@ -34,8 +34,7 @@ constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-fo
 constexpr int kMaxItemRows = 512;      // largest work item (x items carry their map slice in shared memory)
 constexpr int kMaxTreeRows = 170;      // largest small-tree item (2 passes of 85 roots x 3 components)
 constexpr int kTreeRowsOcc = 85;       // tree item size the occupancy (co-resident grid) is computed for
-constexpr int kRing = 4;
-constexpr int kXCounters = 32;               // LL kernels: item blocks in flight per CTA (narrow variants)
+constexpr int kRing = 4;                 // LL kernels: item blocks in flight per CTA (narrow variants)
 // LL sequence numbers: the tag of a launch is the low 32 bits of its sequence number;
 // values whose tag would be 0 are skipped (a never-written unit is zero), and every
 // set_maps zeroes the LL areas, so a unit carries this launch's tag only if this
@@ -108,11 +107,13 @@ struct Ctrl {
   uint32_t done_pme[2];
   uint32_t cnt_pme[2][kMaxLocal];
   int32_t pme_nh[kMaxLocal][kMaxRanks];   // halo_pme_setup: n_home of every rank, seen by local rank l
-  // LL x items finished in this NS epoch (zeroed by set_maps), counted by CTA
-  // (counter blockIdx mod 32, each on its own 32-B sector: no same-address
-  // serialisation); the fused x+f launch starts its tree items once every x item
-  // of the launch is done
-  uint64_t xcnt[kXCounters][4];
+  // fused x+f launch: x items finished in the current launch (acq_rel increments; the
+  // last one resets it and releases xf_done = the launch's x sequence number, which
+  // the tree items acquire: the non-bonded kernel's slot, Alg. 2).  Own 128-B lines.
+  uint32_t xf_cnt;
+  uint32_t pad_xf0[31];
+  uint64_t xf_done;
+  uint64_t pad_xf1[15];
 };
 
 enum : int32_t { kErrCapacity = 1, kErrGeometry = 2, kErrMap = 4,
@@ -390,7 +391,6 @@ struct ExParams {
   int n_items_x;            // fused launch: items [0, n_items_x) are x items, then the f items
   int ring;                 // LL: item-block ring slots per CTA
   uint64_t seq_f;           // fused launch: the f sequence number by value (0 = read ctrl->seq_f + 1)
-  uint64_t seq_x0;          // fused launch: ctrl->seq_x at the end of set_maps (xcnt counts from there)
   int delay_rank;           // HALO_DEBUG kDelayPulse0: the DD rank whose pulse-0 sends are slowed
   const LocalBase* lbase;   // LL: [n_local] (copied to shared memory by every CTA)
   // x launch: L2 prefetch (before griddepcontrol.wait) of the f kernel's item blocks and

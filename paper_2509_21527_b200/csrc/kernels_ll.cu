@@ -196,31 +196,83 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
   if (P.debug & kFenceAfterPeerStores) fence_sys();
 }
 
-// ---------------------------------------------------------------- f items
-// Fused launch: warp 0 waits until every x item of this launch is done.  Lane k
-// watches counter k (bumped after each x item i = k mod 32, by every x launch);
-// its target is the number of such items per launch times the x launches of
-// this NS epoch (`launches`).  Bounded like every wait.
-__device__ __noinline__ void xcount_wait(Ctrl* ctrl, int nx, uint64_t launches, const ExParams& P) {
-  const int k = threadIdx.x;
-  const uint64_t tgt = (k < nx ? (uint64_t)((nx - 1 - k) / kXCounters + 1) : 0u) * launches;
-  const uint64_t* cnt = &ctrl->xcnt[k][0];
-  const uint64_t t0 = gtimer();
-  for (uint32_t it = 1;; ++it) {
-    if (__all_sync(0xffffffffu, ld_relaxed_gpu(cnt) >= tgt)) break;
-    if ((it & 15u) == 0) {
-      const uint64_t el = gtimer() - t0;
-      if (el > 20000) __nanosleep(256);
-      if ((it & 1023u) == 0) {
-        if (el > P.timeout_ns) {
-          if (k == 0) report_timeout(P.err_host, tcode(15, 0, 0));
-          return;
+// Two send items at once (the fused launch: its x phase runs at the f kernel's 4 CTAs
+// per SM, so a CTA holds ~1.6 x items; processing two together keeps one load of each
+// in flight per thread instead of two dependent rounds).  Same arithmetic as x_item.
+template <int W, bool kChk>
+__device__ __forceinline__ void x_send_pair(const XRec& r0, const XEnt* e0, const XRec& r1, const XEnt* e1,
+                                            const LocalBase* lb, const ExParams& P, uint32_t tag) {
+  const XRec* rr[2] = {&r0, &r1};
+  const XEnt* ee[2] = {e0, e1};
+  uint32_t n[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) n[i] = !kChk || rr[i]->epoch == P.plan_epoch ? rr[i]->n_units : stale_item(P);
+  const uint32_t B = blockDim.x;
+  for (uint32_t u = threadIdx.x; u < max(n[0], n[1]); u += B) {
+    uint64_t w[2];
+    const uint64_t* src[2];
+    uint32_t mask[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      src[i] = nullptr;
+      if (u < n[i]) {
+        const uint32_t e = u / W;
+        const int c = (int)(u - e * W);
+        const XEnt E = ee[i][e];
+        const LocalBase& L = lb[E.l];
+        mask[i] = E.mask;
+        if (!(E.kq & 0x80u)) {
+          w[i] = ((uint64_t)tag << 32) | __float_as_uint(__ldg(L.x + (size_t)E.row * W + c));
+        } else {
+          const int q = E.kq & 7;
+          if (q < P.p_lo || (P.debug & kMutateXNoWait)) {
+            w[i] = ((uint64_t)tag << 32) | __float_as_uint(__ldcg(L.x + (size_t)(L.recv_off[q] + E.row) * W + c));
+          } else {
+            src[i] = L.xll + (size_t)q * P.ll_stride + (size_t)E.row * W + c;
+            w[i] = ld_relaxed_sys(src[i]);
+          }
         }
-        if (*(volatile int*)P.err_host != 0) return;
       }
     }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (u >= n[i]) continue;
+      const XRec& r = *rr[i];
+      const uint32_t e = u / W;
+      const int c = (int)(u - e * W);
+      if (src[i] != nullptr && (uint32_t)(w[i] >> 32) != tag)
+        w[i] = ll_spin(src[i], tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, r.pulse), P.poll_ns);
+      float v = __uint_as_float((uint32_t)w[i]);
+      if (c < 3) {
+#pragma unroll
+        for (int q = 0; q < kMaxP; ++q)
+          if (mask[i] >> q & 1u) v = __fadd_rn(v, c == r.pdim[q] ? r.shiftL[q] : 0.0f);
+      }
+      const size_t o = (size_t)(r.begin + e) * W + c;
+      if (r.dst_x != nullptr) r.dst_x[o] = v;
+      else st_relaxed_sys(r.dst_ll + o, ll_pack(v, tag));
+    }
   }
-  (void)ld_acquire_gpu(cnt);  // the counted items' stores happen-before the tree items
+}
+
+// ---------------------------------------------------------------- f items
+// Fused launch: thread 0 waits until the last x item of this launch released
+// xf_done = seq (polling one word, with a short sleep between polls so that ~600
+// waiting CTAs do not flood the line the x items' counter shares the L2 with).
+// Bounded like every wait.
+__device__ __noinline__ void xdone_wait(Ctrl* ctrl, uint64_t seq, const ExParams& P) {
+  const uint64_t t0 = gtimer();
+  for (uint32_t it = 1;; ++it) {
+    if (ld_acquire_gpu(&ctrl->xf_done) >= seq) return;  // the counted items' stores happen-before
+    __nanosleep(it < 8 ? 32 : 128);
+    if ((it & 255u) == 0) {
+      if (gtimer() - t0 > P.timeout_ns) {
+        report_timeout(P.err_host, tcode(15, 0, 0));
+        return;
+      }
+      if (*(volatile int*)P.err_host != 0) return;
+    }
+  }
 }
 
 // Shift forces (R13; north_star): the value of every edge whose parent's rank
@@ -410,41 +462,6 @@ __device__ __noinline__ void tree_item_generic(const GRec& g, const TRootG* root
   if (fs_on && g.n_buckets > 0) fs_flush<W>(g, s_v, S, P);
 }
 
-// Item completion count: a release (after the CTA barrier that follows the item's
-// stores, so the CTA's stores are ordered before it); the waiters acquire.
-__device__ __forceinline__ void red_add_release_gpu(uint64_t* p, uint64_t v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// x launch prologue (one thread per CTA, before griddepcontrol.wait): L2 prefetch
-// in 4 KiB chunks spread over the CTAs of the f launch's item blocks (its CTAs
-// start as ours exit; their bulk loads then hit L2) and of the home x rows our
-// sends read (their TLB walks and HBM reads overlap our own item-block loads).  A
-// prefetch carries no data to the SM, so issuing it before griddepcontrol.wait
-// cannot expose stale x.  Out of line: keeps the kernel's registers.
-template <int W>
-__device__ __noinline__ void prefetch_l2(const ExParams& P) {
-  constexpr uint64_t kCh = 4096;
-  const uint64_t G = gridDim.x;
-  const uint64_t nf = P.pf_f_bytes / kCh + ((P.pf_f_bytes % kCh) >= 16 ? 1 : 0);
-  uint64_t c = blockIdx.x;
-  for (; c < nf; c += G) {
-    const uint64_t o = c * kCh;
-    prefetch_l2_bulk(P.pf_f + o, (uint32_t)(min(kCh, P.pf_f_bytes - o) & ~15ull));
-  }
-  if (!P.pf_x) return;
-  c -= nf;  // continue the same round-robin over the x rows of every local rank
-  for (int l = 0; l < P.n_local; ++l) {
-    const uint64_t b = (uint64_t)P.lbase[l].n_home * W * sizeof(float);
-    const uint64_t nx = b / kCh + ((b % kCh) >= 16 ? 1 : 0);
-    for (; c < nx; c += G) {
-      const uint64_t o = c * kCh;
-      prefetch_l2_bulk(reinterpret_cast<const char*>(P.lbase[l].x) + o, (uint32_t)(min(kCh, b - o) & ~15ull));
-    }
-    c -= nx;
-  }
-}
-
 // ---------------------------------------------------------------- kernel
 enum : int { kModeX = 0, kModeF = 1, kModeXF = 2 };
 
@@ -456,19 +473,18 @@ __host__ __device__ __forceinline__ uint32_t fblk_bytes(uint32_t R) { return 128
 // Items of this CTA: [0, n_main) round-robin over CTAs [0, G - n_tail) (fused:
 // the x items first, then the tree items); n_tail trailing items would get one
 // dedicated CTA each (none in the current plan).
-// CTA size: the narrow x variant (kU = 2) runs 128-thread CTAs, so the x grid takes at
-// most half of an SM's thread slots and the f launch's CTAs become resident (PDL) while
-// x still runs: their item blocks are in shared memory when griddepcontrol.wait releases.
+// CTA size: 256 threads, except the experimental x variant kU = 3 (64-thread CTAs, meant
+// to leave SM room for the f launch's CTAs under PDL; measured slower, see ll_fn_c).
 template <int kU, int kMode>
 __host__ __device__ constexpr int ll_threads() {
-  return kMode != 0 ? kThreads : kU == 2 ? kThreadsXNarrow : kU == 3 ? 64 : kThreads;
+  return kMode == 0 && kU == 3 ? 64 : kThreads;
 }
 
 // kChk: the launch is being captured into a CUDA graph, whose replays may outlive the
 // plan (the next NS step): every item's epoch is checked.  Eager launches take their
 // parameters from the current plan and skip the check (measured: ~0.2 us per step).
 template <int W, int kU, int kMode, bool kChk>
-__global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 : 4) k_exchange_ll(
+__global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU == 1 || kU == 3 ? 8 : 4) : 4) k_exchange_ll(
     const __grid_constant__ ExParams P) {
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq[2];
@@ -535,21 +551,50 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 :
     unsigned char* blk = s_blk + (size_t)slot * SB;
     mbar_wait(&s_bar[slot], (uint32_t)(j / ring) & 1u);
     if (trace && j == 0) ctrl->trace[tslot][blockIdx.x][1] = gtimer();
+    if (kMode == kModeXF && it < nx && it + stride < nx && ring >= 2 && !(P.debug & kTraceDetail)) {
+      // two send items of this CTA at once (their blocks are both in the ring)
+      const int slot2 = (j + 1) % ring;
+      unsigned char* blk2 = s_blk + (size_t)slot2 * SB;
+      mbar_wait(&s_bar[slot2], (uint32_t)((j + 1) / ring) & 1u);
+      const XRec& r0 = *reinterpret_cast<const XRec*>(blk);
+      const XRec& r1 = *reinterpret_cast<const XRec*>(blk2);
+      if (r0.kind == kItemXRecv || r1.kind == kItemXRecv) {
+        x_item<W, kU, kChk>(r0, reinterpret_cast<const XEnt*>(blk + 128), s_lb, P, tag_x);
+        x_item<W, kU, kChk>(r1, reinterpret_cast<const XEnt*>(blk2 + 128), s_lb, P, tag_x);
+      } else {
+        x_send_pair<W, kChk>(r0, reinterpret_cast<const XEnt*>(blk + 128), r1,
+                             reinterpret_cast<const XEnt*>(blk2 + 128), s_lb, P, tag_x);
+      }
+      __syncthreads();  // both items' rows are stored before their count; both slots are free
+      if (threadIdx.x == 0) {
+        if (atom_add_acqrel_gpu(&ctrl->xf_cnt, 2u) == (uint32_t)nx - 2u) {
+          ctrl->xf_cnt = 0;  // (the next fused launch's x items start after this launch completes)
+          st_release_gpu(&ctrl->xf_done, s_seq[0]);
+        }
+        fence_proxy_async_smem();
+        for (int k2 = 0; k2 < 2; ++k2) {  // refill both slots (items it + ring*stride, it + (ring+1)*stride)
+          const int nxt = it + (ring + k2) * stride;
+          if (nxt < end) bulk_load(k2 ? blk2 : blk, blk_of(nxt), bytes_of(nxt), &s_bar[k2 ? slot2 : slot]);
+        }
+      }
+      it += stride;
+      ++j;
+      continue;
+    }
     if (kMode != kModeF && it < nx) {
-      const XRec& r = *reinterpret_cast<const XRec*>(blk);
-      x_item<W, kU, kChk>(r, reinterpret_cast<const XEnt*>(blk + 128), s_lb, P, tag_x);
+      x_item<W, kU, kChk>(*reinterpret_cast<const XRec*>(blk), reinterpret_cast<const XEnt*>(blk + 128), s_lb, P,
+                          tag_x);
       __syncthreads();  // the item's rows are stored (fused: before its count) and the slot is free
-      if (threadIdx.x == 0) {  // every x launch counts (the fused launch's targets count all of them)
-        uint64_t* cnt = &ctrl->xcnt[it % kXCounters][0];
-        if (kMode == kModeXF) red_add_release_gpu(cnt, 1u);
-        else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
+      if (kMode == kModeXF && threadIdx.x == 0) {  // the launch's last x item releases xf_done
+        if (atom_add_acqrel_gpu(&ctrl->xf_cnt, 1u) == (uint32_t)nx - 1u) {
+          ctrl->xf_cnt = 0;  // (the next fused launch's x items start after this launch completes)
+          st_release_gpu(&ctrl->xf_done, s_seq[0]);
+        }
       }
     } else if constexpr (kMode != kModeX) {
       const GRec& g = *reinterpret_cast<const GRec*>(blk);
       if (kMode == kModeXF && !xin_seen) {  // every halo row of this process is complete (the NB kernel's slot)
-        // x launches since set_maps (each 2^32 boundary skipped one value, ll_seq_next)
-        const uint64_t launches = (s_seq[0] - P.seq_x0) - ((s_seq[0] >> 32) - (P.seq_x0 >> 32));
-        if (threadIdx.x < 32) xcount_wait(ctrl, nx, launches, P);
+        if (threadIdx.x == 0 && nx > 0) xdone_wait(ctrl, s_seq[0], P);
         __syncthreads();
         xin_seen = true;
       }
@@ -599,34 +644,37 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? 8 :
 cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** args, cudaStream_t st, bool pdl,
                                   size_t smem, const cudaAccessPolicyWindow* win);
 
-// Narrow x variant (HALO_X_VARIANT): 0 = 256-thread CTAs, one unit per thread (default);
-// 1 = 128 threads, 2 units; 2 = 64 threads, 3 units.  Same items, same results.  Measured
-// (C3, 1 GPU, A/B): 17.36 / 17.62 / 18.67 us/step — the smaller CTAs were meant to let
-// the f launch's CTAs become resident during x, but the register file (64 regs x 256
-// threads per f CTA) admits only one of them beside the x CTAs.
+// Narrow x variant (HALO_X_VARIANT): 0 = automatic (one unit per thread for items of
+// <= 64 rows, two for larger ones: every load of an item in flight together); 1 = two
+// units per thread always; 2 = 64-thread CTAs with 3 units (experiment: the smaller x
+// CTAs were meant to let the f launch's CTAs become resident during x, but the register
+// file — 64 regs x 256 threads per f CTA — admits only one of them beside the x CTAs;
+// measured at C3 1 GPU, A/B: 128-thread CTAs 17.62, 64-thread 18.67 vs 17.36 us/step).
+// The fused launch's x items use two units per thread (items of up to 128 rows).
 static int g_x_variant = 0;
 void ll_set_x_variant(int v) { g_x_variant = v < 0 || v > 2 ? 0 : v; }
 template <int W, bool C>
-static const void* ll_fn_c(int mode, bool wide) {
-  if (mode == kModeX && !wide)
-    return g_x_variant == 0 ? (const void*)k_exchange_ll<W, 1, kModeX, C>
-                            : g_x_variant == 2 ? (const void*)k_exchange_ll<W, 3, kModeX, C>
-                                               : (const void*)k_exchange_ll<W, 2, kModeX, C>;
+static const void* ll_fn_c(int mode, bool wide, int rows) {
+  if (mode == kModeX && !wide) {
+    if (g_x_variant == 2) return (const void*)k_exchange_ll<W, 3, kModeX, C>;
+    return (g_x_variant == 1 || rows > 64) ? (const void*)k_exchange_ll<W, 2, kModeX, C>
+                                           : (const void*)k_exchange_ll<W, 1, kModeX, C>;
+  }
   if (mode == kModeX) return (const void*)k_exchange_ll<W, 4, kModeX, C>;
   if (mode == kModeF) return wide ? (const void*)k_exchange_ll<W, 4, kModeF, C> : (const void*)k_exchange_ll<W, 1, kModeF, C>;
-  return wide ? (const void*)k_exchange_ll<W, 4, kModeXF, C> : (const void*)k_exchange_ll<W, 1, kModeXF, C>;
+  return wide ? (const void*)k_exchange_ll<W, 4, kModeXF, C> : (const void*)k_exchange_ll<W, 2, kModeXF, C>;
 }
 template <int W>
-static const void* ll_fn(int mode, bool wide, bool chk = false) {
-  return chk ? ll_fn_c<W, true>(mode, wide) : ll_fn_c<W, false>(mode, wide);
+static const void* ll_fn(int mode, bool wide, bool chk, int rows) {
+  return chk ? ll_fn_c<W, true>(mode, wide, rows) : ll_fn_c<W, false>(mode, wide, rows);
 }
-static const void* ll_fn(int layout, int mode, bool wide, bool chk = false) {
-  return layout == 4 ? ll_fn<4>(mode, wide, chk) : ll_fn<3>(mode, wide, chk);
+static const void* ll_fn(int layout, int mode, bool wide, bool chk = false, int rows = 64) {
+  return layout == 4 ? ll_fn<4>(mode, wide, chk, rows) : ll_fn<3>(mode, wide, chk, rows);
 }
 
 int ll_block(int mode, bool wide) {
   if (mode != kModeX || wide) return kThreads;
-  return g_x_variant == 0 ? kThreads : g_x_variant == 2 ? 64 : kThreadsXNarrow;
+  return g_x_variant == 2 ? 64 : kThreads;
 }
 
 // Ring slots (item blocks in flight per CTA) and dynamic shared memory.
@@ -653,30 +701,31 @@ uint32_t ll_fblk_bytes(int tree_rows) { return fblk_bytes((uint32_t)tree_rows); 
 cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
                                const cudaAccessPolicyWindow* win, cudaStream_t st, bool chk) {
   void* args[] = {(void*)&p};
-  return launch_coop_kernel_ex(ll_fn(layout, mode, wide, chk), grid, ll_block(mode, wide), args, st, true,
+  return launch_coop_kernel_ex(ll_fn(layout, mode, wide, chk, p.item_rows), grid, ll_block(mode, wide), args, st, true,
                                ll_smem_bytes(mode, p.item_rows, p.tree_rows, wide), win);
 }
 
 // Co-resident CTAs per GPU of each mode for the narrow (items <= 128 rows) or
 // wide (<= 512) variants, at the largest item size each runs with (a smaller
 // launch only fits more).  Also opts the kernels into their dynamic shared memory.
-cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [3]: x, f, xf */) {
+cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [4]: x, f, xf, x with 128-row items */) {
   int dev = 0, sms = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   const int rows = wide ? kMaxItemRows : 128;
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     int bmin = 1 << 30;
+    const int m = mode == 3 ? 0 : mode, irows = mode == 3 ? 128 : 64;
     for (int chk = 0; chk < 2; ++chk) {  // the grid must fit both (eager and captured launches)
-      const void* fn = ll_fn(layout, mode, wide, chk != 0);
+      const void* fn = ll_fn(layout, m, wide, chk != 0, irows);
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)ll_smem_bytes(mode, kMaxItemRows, kMaxTreeRows, wide));
+                               (int)ll_smem_bytes(m, kMaxItemRows, kMaxTreeRows, wide));
       if (e != cudaSuccess) return e;
       int b = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, ll_block(mode, wide),
-                                                        ll_smem_bytes(mode, rows, wide ? kMaxTreeRows : kTreeRowsOcc, wide));
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, ll_block(m, wide),
+                                                        ll_smem_bytes(m, rows, wide ? kMaxTreeRows : kTreeRowsOcc, wide));
       if (e != cudaSuccess) return e;
       bmin = std::min(bmin, b);
     }

@@ -228,19 +228,19 @@ struct halo_ctx {
   uint64_t ping_base = 0;
   cudaAccessPolicyWindow l2win{};    // HALO_F_L2_PERSIST: the static plan (item blocks) persists in L2
   int max_x = 0, max_f = 0, max_xf = 0;        // co-resident CTAs of the exchange kernels (LL: narrow variants)
+  int max_x128 = 0;                              // ... of the x kernel with 128-row items (two units per thread)
   int max_x_w = 0, max_f_w = 0, max_xf_w = 0;  // LL: batched variants for large work items
   int grid_cap = 0;                 // HALO_CTAS_PER_SM x SMs (0 = occupancy limit only)
   int x_cap = 0;                    // HALO_X_CTAS_PER_SM x SMs: the x kernel only (leaves SM room for
                                     // the f kernel's CTAs to become resident early under PDL)
   bool wide() const { return ll && item_rows >= 256; }
   int cap_x() const {
-    int c = wide() ? max_x_w : max_x;
+    int c = wide() ? max_x_w : item_rows > 64 ? max_x128 : max_x;
     if (grid_cap) c = std::min(c, grid_cap);
     return x_cap ? std::min(c, x_cap) : c;
   }
   int cap_f() const { const int c = wide() ? max_f_w : max_f; return grid_cap ? std::min(c, grid_cap) : c; }
   int cap_xf() const { const int c = wide() ? max_xf_w : max_xf; return grid_cap ? std::min(c, grid_cap) : c; }
-  uint64_t seq_x0 = 0;              // ctrl->seq_x when set_maps ended (the fused launch's xin base)
   int last_grid[2] = {0, 0};
   int item_rows = 64;
   int tree_rows = 64;               // LL: roots per small-tree f item (chosen per NS epoch, build_ll_f)
@@ -489,10 +489,10 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) {
     // LL occupancy always (HALO_F_AUTO_TRANSPORT can switch a ctx to LL); the paper
     // protocol's kernels for the paper / copy-engine paths
-    int b[3] = {0, 0, 0}, bw[3] = {0, 0, 0};
+    int b[4] = {0, 0, 0, 0}, bw[4] = {0, 0, 0, 0};
     e = max_coresident_ll(cfg->layout, false, b);
     if (e == cudaSuccess) e = max_coresident_ll(cfg->layout, true, bw);
-    ctx->max_x = b[0]; ctx->max_f = b[1]; ctx->max_xf = b[2];
+    ctx->max_x = b[0]; ctx->max_f = b[1]; ctx->max_xf = b[2]; ctx->max_x128 = b[3];
     ctx->max_x_w = bw[0]; ctx->max_f_w = bw[1]; ctx->max_xf_w = bw[2];
     if (e == cudaSuccess && !ctx->ll) e = max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
   }
@@ -1467,9 +1467,12 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
   };
   int RT = 32;
   while (f_items(RT) > ctx->cap_f() && RT < kTreeRowsOcc) RT = std::min(kTreeRowsOcc, RT + 16);
-  // bandwidth regime: fewer, larger items (two passes of kTreeRowsOcc roots per thread)
-  while (f_items(RT) > ctx->cap_f() && RT < ctx->tree_rows_max) RT = std::min(ctx->tree_rows_max, RT + 17);
-  if (const char* e = getenv("HALO_TREE_ROWS")) RT = std::min(kMaxTreeRows, std::max(8, atoi(e)));
+  // bandwidth regime (wide variants: two item blocks in flight, so the shared memory the
+  // co-resident grid was computed for holds kMaxTreeRows): fewer, larger items, two
+  // passes of kTreeRowsOcc roots per thread
+  const int rt_max = ctx->wide() ? ctx->tree_rows_max : kTreeRowsOcc;
+  while (f_items(RT) > ctx->cap_f() && RT < rt_max) RT = std::min(rt_max, RT + 17);
+  if (const char* e = getenv("HALO_TREE_ROWS")) RT = std::min(rt_max, std::max(8, atoi(e)));
   int nf = 0;
   for (int c = 0; c <= P; ++c)
     for (int l = 0; l < L; ++l) {
@@ -1626,7 +1629,6 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.tree_rows = ctx->tree_rows;
   P.ring = ll_ring(0, ctx->wide());  // (the f and fused launches set theirs)
   P.delay_rank = ctx->P ? ctx->neighbour(0, ctx->pdim[0], +1) : -1;
-  P.seq_x0 = ctx->seq_x0;
   P.lbase = ctx->d_lbase;
   P.plan_epoch = ctx->epoch;
   return P;
@@ -2105,11 +2107,10 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   CK(cudaMemcpyAsync(seqs, &ctx->ctrl->seq_x, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   // the fused launch's per-rank halo counters count from here (the per-pulse x
   // launches above counted too)
-  CK(cudaMemsetAsync(ctx->ctrl->xcnt, 0, sizeof(ctx->ctrl->xcnt), st));
+  CK(cudaMemsetAsync(&ctx->ctrl->xf_cnt, 0, sizeof(uint32_t), st));
   CK(cudaStreamSynchronize(st));
   ctx->seq_host_x = seqs[0];
   ctx->seq_host_f = seqs[1];
-  ctx->seq_x0 = seqs[0];
   prof.lap("plan");
   prof.print(ctx->first_rank);
   ctx->maps_ready = true;
