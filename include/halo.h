@@ -381,10 +381,12 @@ HALO_API halo_status halo_packed_sizes(const halo_ctx* ctx, size_t* in_bytes, si
  * Two uploads (x home, then the forces on a library-owned side stream while x
  * is exchanged), two downloads (halo x on a side stream while f is exchanged,
  * then the forces and fshift); packing to and from the per-rank rows is done
- * by a copy kernel.  HALO_PACKED_DIRECT=1: the last copy kernel writes the
- * forces straight into `out` when it is device-accessible pinned memory
- * (measured slower).  Enqueued on `stream`; synchronises it.  Not
- * graph-capturable. */
+ * by a copy kernel.  The whole sequence is captured once per (NS epoch, in,
+ * out) into a library-owned CUDA graph and replayed on `stream`
+ * (HALO_PACKED_GRAPH=0: enqueued eagerly).  HALO_PACKED_DIRECT=1: the last copy
+ * kernel writes the forces straight into `out` when it is device-accessible
+ * pinned memory (measured slower).  Synchronises `stream`.  Not itself
+ * graph-capturable by the caller. */
 HALO_API halo_status halo_step_host_packed(halo_ctx* ctx, const void* in, void* out, void* stream);
 
 /* Baseline building blocks (the NCCL send/recv schedule of P:178-181 / Fig. 1

@@ -484,7 +484,11 @@ __host__ __device__ constexpr int ll_threads() {
 // plan (the next NS step): every item's epoch is checked.  Eager launches take their
 // parameters from the current plan and skip the check (measured: ~0.2 us per step).
 template <int W, int kU, int kMode, bool kChk>
-__global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU == 1 || kU == 3 ? 8 : 4) : 4) k_exchange_ll(
+#ifndef HALO_XF_MIN_BLOCKS
+#define HALO_XF_MIN_BLOCKS 4  // fused launch: CTAs per SM the registers are budgeted for (A/B switch)
+#endif
+__global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU == 1 || kU == 3 ? 8 : 4)
+                                                           : kMode == kModeXF ? HALO_XF_MIN_BLOCKS : 4) k_exchange_ll(
     const __grid_constant__ ExParams P) {
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq[2];

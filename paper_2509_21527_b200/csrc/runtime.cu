@@ -183,6 +183,11 @@ struct halo_ctx {
   size_t pk_max_words[3] = {0, 0, 0};
   cudaStream_t pk_h2d = nullptr, pk_d2h = nullptr;
   cudaEvent_t pk_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t pk_cap = nullptr;    // capture stream of the packed-step graph
+  cudaGraphExec_t pk_exec = nullptr;
+  uint32_t pk_g_epoch = 0;
+  const void* pk_g_in = nullptr;
+  const void* pk_g_out = nullptr;
   char* d_small = nullptr;          // set_maps argument staging
   MigRank* d_mig = nullptr;         // halo_migrate: per local rank tables
   MigCtrl* d_migctrl = nullptr;
@@ -2717,21 +2722,9 @@ halo_status halo_packed_sizes(const halo_ctx* ctx, size_t* in_bytes, size_t* out
   return HALO_OK;
 }
 
-halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_host, void* stream) {
-  if (!ctx || !in_host) return HALO_ERR_ARG;
-  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "step before set_maps");
+// The packed step's operations, enqueued on st (eager, or under capture: packed_graph).
+static halo_status packed_enqueue(halo_ctx* ctx, const void* in_host, void* out_host, char* out_dev, cudaStream_t st) {
   halo_status s;
-  // a device-accessible (mapped pinned) output block takes the forces directly
-  char* out_dev = nullptr;
-  if (out_host && getenv("HALO_PACKED_DIRECT")) {  // measured slower than staging + one copy (C3: 184 vs 130 us)
-    cudaPointerAttributes pa{};
-    if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
-      out_dev = static_cast<char*>(pa.devicePointer);
-    (void)cudaGetLastError();
-  }
-  if (ctx->pk_epoch != ctx->epoch || !ctx->d_segs || ctx->pk_out_dev != out_dev)
-    if ((s = packed_prepare(ctx, out_dev)) != HALO_OK) return s;
-  cudaStream_t st = (cudaStream_t)stream;
   const int L = ctx->n_local;
   size_t in_b, out_b, fs_off;
   packed_sizes(ctx, &in_b, &out_b, &fs_off);
@@ -2749,7 +2742,7 @@ halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_
   CK(cudaMemcpyAsync(ctx->d_pk_in + bx, in + bx, in_b - bx, cudaMemcpyHostToDevice, ctx->pk_h2d));
   CK(cudaEventRecord(ctx->pk_ev[1], ctx->pk_h2d));
   CK(launch_seg_copy(ctx->d_segs, L, ctx->pk_max_words[0], st));
-  if ((s = halo_exchange_x(ctx, stream)) != HALO_OK) return s;
+  if ((s = halo_exchange_x(ctx, st)) != HALO_OK) return s;
   // halo x rows -> staging (before exchange_f: a neighbour's next exchange_x may only
   // overwrite them after our exchange_f, R17), downloaded on a side stream (PCIe D2H)
   CK(launch_seg_copy(ctx->d_segs + 2 * L, L, ctx->pk_max_words[2], st));
@@ -2762,11 +2755,65 @@ halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_
   CK(cudaStreamWaitEvent(st, ctx->pk_ev[1], 0));
   CK(launch_seg_copy(ctx->d_segs + L, L, ctx->pk_max_words[1], st));
   CK(cudaMemsetAsync(ctx->d_fshift_tmp, 0, sizeof(double) * 9 * L, st));
-  if ((s = halo_exchange_f(ctx, ctx->d_fshift_tmp, 1, stream)) != HALO_OK) return s;
+  if ((s = halo_exchange_f(ctx, ctx->d_fshift_tmp, 1, st)) != HALO_OK) return s;
   if (out) {
     CK(launch_seg_copy(ctx->d_segs + 3 * L, L + 1, ctx->pk_max_words[2], st));
     if (!out_dev) CK(cudaMemcpyAsync(out + bxo, ctx->d_pk_out + bxo, out_b - bxo, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamWaitEvent(st, ctx->pk_ev[3], 0));
+  }
+  return HALO_OK;
+}
+
+halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_host, void* stream) {
+  if (!ctx || !in_host) return HALO_ERR_ARG;
+  if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "step before set_maps");
+  halo_status s;
+  // a device-accessible (mapped pinned) output block takes the forces directly
+  char* out_dev = nullptr;
+  if (out_host && getenv("HALO_PACKED_DIRECT")) {  // measured slower than staging + one copy (C3: 184 vs 130 us)
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, out_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      out_dev = static_cast<char*>(pa.devicePointer);
+    (void)cudaGetLastError();
+  }
+  if (ctx->pk_epoch != ctx->epoch || !ctx->d_segs || ctx->pk_out_dev != out_dev)
+    if ((s = packed_prepare(ctx, out_dev)) != HALO_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (getenv("HALO_PACKED_GRAPH") && atoi(getenv("HALO_PACKED_GRAPH")) == 0) {
+    if ((s = packed_enqueue(ctx, in_host, out_host, out_dev, st)) != HALO_OK) return s;
+  } else {
+    // the whole step (2 uploads, 4 copy kernels, 2 exchanges, 2 downloads on 3 streams) as
+    // ONE CUDA graph per (NS epoch, host blocks): one launch instead of ~14 API calls
+    if (!ctx->pk_exec || ctx->pk_g_epoch != ctx->epoch || ctx->pk_g_in != in_host || ctx->pk_g_out != out_host) {
+      if (ctx->pk_exec) CK(cudaGraphExecDestroy(ctx->pk_exec));
+      ctx->pk_exec = nullptr;
+      if (!ctx->pk_cap) CK(cudaStreamCreateWithFlags(&ctx->pk_cap, cudaStreamNonBlocking));
+      const bool was = ctx->captured;
+      const uint64_t sx = ctx->seq_host_x, sf = ctx->seq_host_f;
+      CK(cudaStreamBeginCapture(ctx->pk_cap, cudaStreamCaptureModeThreadLocal));
+      const halo_status se = packed_enqueue(ctx, in_host, out_host, out_dev, ctx->pk_cap);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ee = cudaStreamEndCapture(ctx->pk_cap, &g);
+      ctx->captured = was;  // the capture launched nothing: the eager launches keep their by-value numbers
+      ctx->seq_host_x = sx;
+      ctx->seq_host_f = sf;
+      if (se != HALO_OK) {
+        if (g) (void)cudaGraphDestroy(g);
+        return se;
+      }
+      if (ee != cudaSuccess) return cuda_fail(ctx, ee, "packed step capture");
+      CK(cudaGraphInstantiate(&ctx->pk_exec, g, 0));
+      CK(cudaGraphDestroy(g));
+      ctx->pk_g_epoch = ctx->epoch;
+      ctx->pk_g_in = in_host;
+      ctx->pk_g_out = out_host;
+    }
+    CK(cudaGraphLaunch(ctx->pk_exec, st));
+    // the replay advanced the device sequence counters by one x and one f launch
+    if (ctx->ll) {
+      ctx->seq_host_x = ll_seq_next(ctx->seq_host_x);
+      ctx->seq_host_f = ll_seq_next(ctx->seq_host_f);
+    }
   }
   CK(cudaStreamSynchronize(st));
   return check_err_word(ctx);
@@ -3114,6 +3161,8 @@ halo_status halo_destroy(halo_ctx* ctx) {
   if (ctx->h_recv) (void)cudaFreeHost(ctx->h_recv);
   for (auto e : ctx->pk_ev)
     if (e) (void)cudaEventDestroy(e);
+  if (ctx->pk_exec) (void)cudaGraphExecDestroy(ctx->pk_exec);
+  if (ctx->pk_cap) (void)cudaStreamDestroy(ctx->pk_cap);
   if (ctx->pk_h2d) (void)cudaStreamDestroy(ctx->pk_h2d);
   if (ctx->pk_d2h) (void)cudaStreamDestroy(ctx->pk_d2h);
   if (ctx->d_small) (void)cudaFree(ctx->d_small);

@@ -62,14 +62,14 @@ def main():
             port += 1
             try:
                 d = run(lib, args, port)
-                res[n].append((d["value"], d["x_us"], d["f_us"]))
+                res[n].append((d["value"], d["x_us"], d["f_us"], (d.get("fused_xf") or {}).get("us_per_step") or 0.0))
             except Exception as e:  # keep going: one failed run must not hide the others
                 print(json.dumps({"lib": n, "error": str(e)[-500:]}), flush=True)
     for n, v in res.items():
         if v:
             med = [statistics.median(c) for c in zip(*v)]
             print(json.dumps({"config": args.config, "gpus": args.gpus, "lib": n, "value": med[0], "x_us": med[1],
-                              "f_us": med[2], "runs": v}), flush=True)
+                              "f_us": med[2], "fused_us": med[3], "runs": v}), flush=True)
 
 
 if __name__ == "__main__":

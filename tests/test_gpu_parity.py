@@ -237,13 +237,15 @@ def test_step_host_e2e():
     sess.destroy()
 
 
-@pytest.mark.parametrize("direct", [False, True])
+@pytest.mark.parametrize("mode", ["graph", "eager", "direct"])
 @pytest.mark.parametrize("cfg", ["C2", "C3", "T2P"])
-def test_step_host_packed_e2e(cfg, direct, monkeypatch):
-    """halo_step_host_packed (one host block in, one out) == the oracle, twice in a row;
-    forces staged and downloaded (default), or (direct) written by the last kernel
-    straight into the mapped output block."""
-    if direct:
+def test_step_host_packed_e2e(cfg, mode, monkeypatch):
+    """halo_step_host_packed (one host block in, one out) == the oracle, twice in a row:
+    as one cached CUDA graph (default), eagerly, or with the forces written by the last
+    kernel straight into the mapped output block; then a two-launch eager step."""
+    if mode == "eager":
+        monkeypatch.setenv("HALO_PACKED_GRAPH", "0")
+    if mode == "direct":
         monkeypatch.setenv("HALO_PACKED_DIRECT", "1")
     case = Case(cfg, seed=2, force_kind="int")
     sess = session_for(case)
@@ -275,6 +277,7 @@ def test_step_host_packed_e2e(cfg, direct, monkeypatch):
         fsh = raw[o:o + nl * 72].view(np.float64).reshape(nl, 3, 3)
         for l in range(nl):
             np.testing.assert_array_equal(fsh[l], case.fshift[l])
+    run_gpu_case(case, sess)  # eager launches after the graph replays (host sequence mirror in step)
     sess.destroy()
 
 
