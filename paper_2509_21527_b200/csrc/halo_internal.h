@@ -399,6 +399,7 @@ struct ExParams {
   uint64_t pf_f_bytes;
   int pf_x;                 // 1: prefetch every local rank's home x rows
   uint32_t plan_epoch;      // LL: the NS epoch whose item blocks this launch expects (records carry theirs)
+  int all_local;            // LL: every pulse of every local rank stays in this hop group (no LL units)
 };
 
 // GPU plan build of the LL protocol (set_maps, P <= 3: every force tree has <= 8

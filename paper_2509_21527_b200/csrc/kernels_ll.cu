@@ -113,14 +113,16 @@ __device__ __forceinline__ float ll_wait(const uint64_t* u, uint32_t tag, uint64
 // most one unit per thread), 4 for large items (bandwidth regime: every load of
 // a batch is issued before any store — the stores are asm volatile with a
 // memory clobber, so one unit at a time would serialise a memory latency each).
-template <int W, int kU, bool kChk>
+// kLocal: every item of the plan stays in this hop group (one process hosts every DD
+// rank: no LL units anywhere) — the LL paths are compiled out (less code to fetch cold).
+template <int W, int kU, bool kChk, bool kLocal = false>
 __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const LocalBase* lb, const ExParams& P,
                                        uint32_t tag) {
   // a CUDA graph captured before the last NS step replays with this epoch: every item of
   // a replaced (or zeroed) plan carries another one and is treated as empty
   const uint32_t n = !kChk || r.epoch == P.plan_epoch ? r.n_units : stale_item(P);
   const uint32_t B = blockDim.x;
-  if (r.kind == kItemXRecv) {
+  if (!kLocal && r.kind == kItemXRecv) {
     // this rank's halo rows of one pulse from another group: LL units -> x rows;
     // 4 units per thread per batch: the polls of a batch are in flight together
     constexpr int kR = 4;
@@ -156,7 +158,7 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
         const XEnt E = ent[e];
         const LocalBase& L = lb[E.l];
         mask[k] = E.mask;
-        if (!(E.kq & 0x80u)) {
+        if (kLocal || !(E.kq & 0x80u)) {
           // a home row: never written during the kernel
           w[k] = ((uint64_t)tag << 32) | __float_as_uint(__ldg(L.x + (size_t)E.row * W + c));
         } else {
@@ -179,7 +181,7 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
       if (u >= n) continue;
       const uint32_t e = u / W;
       const int c = (int)(u - e * W);
-      if (src[k] != nullptr && (uint32_t)(w[k] >> 32) != tag)
+      if (!kLocal && src[k] != nullptr && (uint32_t)(w[k] >> 32) != tag)
         w[k] = ll_spin(src[k], tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, r.pulse), P.poll_ns);
       float v = __uint_as_float((uint32_t)w[k]);
       if (c < 3) {
@@ -188,7 +190,7 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
           if (mask[k] >> q & 1u) v = __fadd_rn(v, c == r.pdim[q] ? r.shiftL[q] : 0.0f);
       }
       const size_t o = (size_t)(r.begin + e) * W + c;
-      if (r.dst_x != nullptr) r.dst_x[o] = v;  // a rank of this group: its halo row directly
+      if (kLocal || r.dst_x != nullptr) r.dst_x[o] = v;  // a rank of this group: its halo row directly
       else st_relaxed_sys(r.dst_ll + o, ll_pack(v, tag));
     }
   }
@@ -394,7 +396,7 @@ __device__ __noinline__ void tree_ll_nodes(const TRoot R, const uint32_t* il, co
 // is reached: stored (F nodes with children), added to its shift-force bucket,
 // then added into its parent.  A root whose parent is in another group pushes
 // its value there.  ~10 instructions per edge, none for absent nodes.
-template <int W, bool kChk>
+template <int W, bool kChk, bool kLocal = false>
 __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, const uint4* nodes, const LocalBase* lb,
                                           const ExParams& P, uint32_t tag, double (*s_v)[kThreads],
                                           float (*s_val)[kThreads], uint64_t* tdet) {
@@ -419,7 +421,7 @@ __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, con
       if (k < nn && !(R.llmask >> k & 1u))
         cp_async4(&s_val[k][tid], lb[il[k] >> 24].f + (size_t)(il[k] & (kMaxRows - 1)) * W + c);
     cp_async_commit();
-    if (R.llmask) tree_ll_nodes<W>(R, il, lb, P, tag, g.lrank, s_val);
+    if (!kLocal && R.llmask) tree_ll_nodes<W>(R, il, lb, P, tag, g.lrank, s_val);
     cp_async_wait_all();
     if (tdet && u == 0) tdet[1] = gtimer() + (__float_as_uint(s_val[0][tid]) == 0x7fc00001u ? 1 : 0);  // loads landed
     const uint32_t* ilr = il;
@@ -436,7 +438,7 @@ __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, con
     }
     const float root = s_val[0][tid];
     if (R.stmask & 1u) lb[il[0] >> 24].f[(size_t)(il[0] & (kMaxRows - 1)) * W + c] = root;
-    if (R.push != nullptr) st_relaxed_sys(R.push + c, ll_pack(root, tag));
+    if (!kLocal && R.push != nullptr) st_relaxed_sys(R.push + c, ll_pack(root, tag));
     if (tdet && u == 0) tdet[2] = gtimer();  // folded and stored
   }
   if (fs_on) fs_flush<W>(g, s_v, S, P);
@@ -480,13 +482,13 @@ __host__ __device__ constexpr int ll_threads() {
   return kMode == 0 && kU == 3 ? 64 : kThreads;
 }
 
-// kChk: the launch is being captured into a CUDA graph, whose replays may outlive the
-// plan (the next NS step): every item's epoch is checked.  Eager launches take their
-// parameters from the current plan and skip the check (measured: ~0.2 us per step).
-template <int W, int kU, int kMode, bool kChk>
 #ifndef HALO_XF_MIN_BLOCKS
 #define HALO_XF_MIN_BLOCKS 4  // fused launch: CTAs per SM the registers are budgeted for (A/B switch)
 #endif
+// kChk: the launch is being captured into a CUDA graph, whose replays may outlive the
+// plan (the next NS step): every item's epoch is checked.  Eager launches take their
+// parameters from the current plan and skip the check (measured: ~0.2 us per step).
+template <int W, int kU, int kMode, bool kChk, bool kLocal = false>
 __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU == 1 || kU == 3 ? 8 : 4)
                                                            : kMode == kModeXF ? HALO_XF_MIN_BLOCKS : 4) k_exchange_ll(
     const __grid_constant__ ExParams P) {
@@ -586,8 +588,8 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU
       continue;
     }
     if (kMode != kModeF && it < nx) {
-      x_item<W, kU, kChk>(*reinterpret_cast<const XRec*>(blk), reinterpret_cast<const XEnt*>(blk + 128), s_lb, P,
-                          tag_x);
+      x_item<W, kU, kChk, kLocal>(*reinterpret_cast<const XRec*>(blk), reinterpret_cast<const XEnt*>(blk + 128), s_lb,
+                                  P, tag_x);
       __syncthreads();  // the item's rows are stored (fused: before its count) and the slot is free
       if (kMode == kModeXF && threadIdx.x == 0) {  // the launch's last x item releases xf_done
         if (atom_add_acqrel_gpu(&ctrl->xf_cnt, 1u) == (uint32_t)nx - 1u) {
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU
         xin_seen = true;
       }
       if (g.kind == kItemTree)
-        tree_item<W, kChk>(g, reinterpret_cast<const TRoot*>(blk + 128), reinterpret_cast<const uint4*>(blk + 128 + 32 * RT),
+        tree_item<W, kChk, kLocal>(g, reinterpret_cast<const TRoot*>(blk + 128), reinterpret_cast<const uint4*>(blk + 128 + 32 * RT),
                      s_lb, P, tag_f, s_v, s_val,
                      (trace && (P.debug & kTraceDetail) && tdet_free) ? &ctrl->trace[tslot][blockIdx.x][10] : nullptr);
       else
@@ -658,22 +660,24 @@ cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** ar
 static int g_x_variant = 0;
 void ll_set_x_variant(int v) { g_x_variant = v < 0 || v > 2 ? 0 : v; }
 template <int W, bool C>
-static const void* ll_fn_c(int mode, bool wide, int rows) {
+static const void* ll_fn_c(int mode, bool wide, int rows, bool local) {
   if (mode == kModeX && !wide) {
     if (g_x_variant == 2) return (const void*)k_exchange_ll<W, 3, kModeX, C>;
-    return (g_x_variant == 1 || rows > 64) ? (const void*)k_exchange_ll<W, 2, kModeX, C>
-                                           : (const void*)k_exchange_ll<W, 1, kModeX, C>;
+    if (g_x_variant == 1 || rows > 64) return (const void*)k_exchange_ll<W, 2, kModeX, C>;
+    return local ? (const void*)k_exchange_ll<W, 1, kModeX, C, true> : (const void*)k_exchange_ll<W, 1, kModeX, C>;
   }
   if (mode == kModeX) return (const void*)k_exchange_ll<W, 4, kModeX, C>;
-  if (mode == kModeF) return wide ? (const void*)k_exchange_ll<W, 4, kModeF, C> : (const void*)k_exchange_ll<W, 1, kModeF, C>;
+  if (mode == kModeF && !wide)
+    return local ? (const void*)k_exchange_ll<W, 1, kModeF, C, true> : (const void*)k_exchange_ll<W, 1, kModeF, C>;
+  if (mode == kModeF) return (const void*)k_exchange_ll<W, 4, kModeF, C>;
   return wide ? (const void*)k_exchange_ll<W, 4, kModeXF, C> : (const void*)k_exchange_ll<W, 2, kModeXF, C>;
 }
 template <int W>
-static const void* ll_fn(int mode, bool wide, bool chk, int rows) {
-  return chk ? ll_fn_c<W, true>(mode, wide, rows) : ll_fn_c<W, false>(mode, wide, rows);
+static const void* ll_fn(int mode, bool wide, bool chk, int rows, bool local) {
+  return chk ? ll_fn_c<W, true>(mode, wide, rows, local) : ll_fn_c<W, false>(mode, wide, rows, local);
 }
-static const void* ll_fn(int layout, int mode, bool wide, bool chk = false, int rows = 64) {
-  return layout == 4 ? ll_fn<4>(mode, wide, chk, rows) : ll_fn<3>(mode, wide, chk, rows);
+static const void* ll_fn(int layout, int mode, bool wide, bool chk = false, int rows = 64, bool local = false) {
+  return layout == 4 ? ll_fn<4>(mode, wide, chk, rows, local) : ll_fn<3>(mode, wide, chk, rows, local);
 }
 
 int ll_block(int mode, bool wide) {
@@ -705,7 +709,8 @@ uint32_t ll_fblk_bytes(int tree_rows) { return fblk_bytes((uint32_t)tree_rows); 
 cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
                                const cudaAccessPolicyWindow* win, cudaStream_t st, bool chk) {
   void* args[] = {(void*)&p};
-  return launch_coop_kernel_ex(ll_fn(layout, mode, wide, chk, p.item_rows), grid, ll_block(mode, wide), args, st, true,
+  return launch_coop_kernel_ex(ll_fn(layout, mode, wide, chk, p.item_rows, p.all_local != 0), grid, ll_block(mode, wide),
+                               args, st, true,
                                ll_smem_bytes(mode, p.item_rows, p.tree_rows, wide), win);
 }
 
@@ -722,8 +727,9 @@ cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [4]: x, f, x
   for (int mode = 0; mode < 4; ++mode) {
     int bmin = 1 << 30;
     const int m = mode == 3 ? 0 : mode, irows = mode == 3 ? 128 : 64;
-    for (int chk = 0; chk < 2; ++chk) {  // the grid must fit both (eager and captured launches)
-      const void* fn = ll_fn(layout, m, wide, chk != 0, irows);
+    for (int v = 0; v < 4; ++v) {  // the grid must fit every variant (eager / captured, hop-group-local)
+      const int chk = v & 1;
+      const void* fn = ll_fn(layout, m, wide, chk != 0, irows, (v & 2) != 0);
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)ll_smem_bytes(m, kMaxItemRows, kMaxTreeRows, wide));
       if (e != cudaSuccess) return e;

@@ -234,6 +234,7 @@ struct halo_ctx {
   cudaAccessPolicyWindow l2win{};    // HALO_F_L2_PERSIST: the static plan (item blocks) persists in L2
   int max_x = 0, max_f = 0, max_xf = 0;        // co-resident CTAs of the exchange kernels (LL: narrow variants)
   int max_x128 = 0;                              // ... of the x kernel with 128-row items (two units per thread)
+  bool all_local = false;           // LL plan: every pulse of every local rank stays in this hop group
   int max_x_w = 0, max_f_w = 0, max_xf_w = 0;  // LL: batched variants for large work items
   int grid_cap = 0;                 // HALO_CTAS_PER_SM x SMs (0 = occupancy limit only)
   int x_cap = 0;                    // HALO_X_CTAS_PER_SM x SMs: the x kernel only (leaves SM room for
@@ -1636,6 +1637,7 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.delay_rank = ctx->P ? ctx->neighbour(0, ctx->pdim[0], +1) : -1;
   P.lbase = ctx->d_lbase;
   P.plan_epoch = ctx->epoch;
+  P.all_local = ctx->all_local ? 1 : 0;
   return P;
 }
 
@@ -2059,6 +2061,13 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     for (int p = 0; p < P; ++p) fill_pulse_dev(ctx, l, p);
   bool gpu_built = false;
   ctx->gpu_xblk_bytes = ctx->gpu_fblk_bytes = 0;
+  ctx->all_local = ctx->ll && !getenv("HALO_NO_LOCAL_VARIANT");
+  for (int l = 0; l < L && ctx->all_local; ++l)
+    for (int q = 0; q < P; ++q) {
+      const int r = ctx->first_rank + l;
+      if (!same_group(ctx, r, ctx->neighbour(r, ctx->pdim[q], -1)) || !same_group(ctx, r, ctx->neighbour(r, ctx->pdim[q], +1)))
+        ctx->all_local = false;
+    }
   if (ctx->ll) {
     fill_lbase(ctx);
     if (ctx->gpu_plan && P <= 3) {  // the plan built on the device from the device-resident maps
