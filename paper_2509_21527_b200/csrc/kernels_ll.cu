@@ -201,7 +201,7 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
 // Two send items at once (the fused launch: its x phase runs at the f kernel's 4 CTAs
 // per SM, so a CTA holds ~1.6 x items; processing two together keeps one load of each
 // in flight per thread instead of two dependent rounds).  Same arithmetic as x_item.
-template <int W, bool kChk>
+template <int W, bool kChk, bool kLocal = false>
 __device__ __forceinline__ void x_send_pair(const XRec& r0, const XEnt* e0, const XRec& r1, const XEnt* e1,
                                             const LocalBase* lb, const ExParams& P, uint32_t tag) {
   const XRec* rr[2] = {&r0, &r1};
@@ -223,7 +223,7 @@ __device__ __forceinline__ void x_send_pair(const XRec& r0, const XEnt* e0, cons
         const XEnt E = ee[i][e];
         const LocalBase& L = lb[E.l];
         mask[i] = E.mask;
-        if (!(E.kq & 0x80u)) {
+        if (kLocal || !(E.kq & 0x80u)) {
           w[i] = ((uint64_t)tag << 32) | __float_as_uint(__ldg(L.x + (size_t)E.row * W + c));
         } else {
           const int q = E.kq & 7;
@@ -242,7 +242,7 @@ __device__ __forceinline__ void x_send_pair(const XRec& r0, const XEnt* e0, cons
       const XRec& r = *rr[i];
       const uint32_t e = u / W;
       const int c = (int)(u - e * W);
-      if (src[i] != nullptr && (uint32_t)(w[i] >> 32) != tag)
+      if (!kLocal && src[i] != nullptr && (uint32_t)(w[i] >> 32) != tag)
         w[i] = ll_spin(src[i], tag, P.timeout_ns, P.err_host, tcode(11, r.lrank, r.pulse), P.poll_ns);
       float v = __uint_as_float((uint32_t)w[i]);
       if (c < 3) {
@@ -251,7 +251,7 @@ __device__ __forceinline__ void x_send_pair(const XRec& r0, const XEnt* e0, cons
           if (mask[i] >> q & 1u) v = __fadd_rn(v, c == r.pdim[q] ? r.shiftL[q] : 0.0f);
       }
       const size_t o = (size_t)(r.begin + e) * W + c;
-      if (r.dst_x != nullptr) r.dst_x[o] = v;
+      if (kLocal || r.dst_x != nullptr) r.dst_x[o] = v;
       else st_relaxed_sys(r.dst_ll + o, ll_pack(v, tag));
     }
   }
@@ -564,12 +564,12 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU
       mbar_wait(&s_bar[slot2], (uint32_t)((j + 1) / ring) & 1u);
       const XRec& r0 = *reinterpret_cast<const XRec*>(blk);
       const XRec& r1 = *reinterpret_cast<const XRec*>(blk2);
-      if (r0.kind == kItemXRecv || r1.kind == kItemXRecv) {
+      if (!kLocal && (r0.kind == kItemXRecv || r1.kind == kItemXRecv)) {
         x_item<W, kU, kChk>(r0, reinterpret_cast<const XEnt*>(blk + 128), s_lb, P, tag_x);
         x_item<W, kU, kChk>(r1, reinterpret_cast<const XEnt*>(blk2 + 128), s_lb, P, tag_x);
       } else {
-        x_send_pair<W, kChk>(r0, reinterpret_cast<const XEnt*>(blk + 128), r1,
-                             reinterpret_cast<const XEnt*>(blk2 + 128), s_lb, P, tag_x);
+        x_send_pair<W, kChk, kLocal>(r0, reinterpret_cast<const XEnt*>(blk + 128), r1,
+                                     reinterpret_cast<const XEnt*>(blk2 + 128), s_lb, P, tag_x);
       }
       __syncthreads();  // both items' rows are stored before their count; both slots are free
       if (threadIdx.x == 0) {
@@ -670,7 +670,8 @@ static const void* ll_fn_c(int mode, bool wide, int rows, bool local) {
   if (mode == kModeF && !wide)
     return local ? (const void*)k_exchange_ll<W, 1, kModeF, C, true> : (const void*)k_exchange_ll<W, 1, kModeF, C>;
   if (mode == kModeF) return (const void*)k_exchange_ll<W, 4, kModeF, C>;
-  return wide ? (const void*)k_exchange_ll<W, 4, kModeXF, C> : (const void*)k_exchange_ll<W, 2, kModeXF, C>;
+  if (wide) return (const void*)k_exchange_ll<W, 4, kModeXF, C>;
+  return local ? (const void*)k_exchange_ll<W, 2, kModeXF, C, true> : (const void*)k_exchange_ll<W, 2, kModeXF, C>;
 }
 template <int W>
 static const void* ll_fn(int mode, bool wide, bool chk, int rows, bool local) {
