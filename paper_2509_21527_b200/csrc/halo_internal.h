@@ -26,7 +26,6 @@ constexpr int kMaxP = HALO_MAX_PULSES;
 constexpr int kMaxLocal = HALO_MAX_LOCAL;
 constexpr int kMaxRanks = HALO_MAX_RANKS;
 constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
-constexpr int kThreadsXNarrow = 128;   // ... of the LL x kernel with latency-regime items (<= 128 rows)
 constexpr int kHdrBytes = 8192;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS
 constexpr int kTraceW = 16;            // ... words per CTA: 4 stamps + (tag, end) of its first 6 items
