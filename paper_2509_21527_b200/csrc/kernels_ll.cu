@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU
     unsigned char* blk = s_blk + (size_t)slot * SB;
     mbar_wait(&s_bar[slot], (uint32_t)(j / ring) & 1u);
     if (trace && j == 0) ctrl->trace[tslot][blockIdx.x][1] = gtimer();
-    if (kMode == kModeXF && it < nx && it + stride < nx && ring >= 2 && !(P.debug & kTraceDetail)) {
+    if (kMode == kModeXF && kLocal && it < nx && it + stride < nx && ring >= 2 && !(P.debug & kTraceDetail)) {
       // two send items of this CTA at once (their blocks are both in the ring)
       const int slot2 = (j + 1) % ring;
       unsigned char* blk2 = s_blk + (size_t)slot2 * SB;
@@ -671,7 +671,9 @@ static const void* ll_fn_c(int mode, bool wide, int rows, bool local) {
     return local ? (const void*)k_exchange_ll<W, 1, kModeF, C, true> : (const void*)k_exchange_ll<W, 1, kModeF, C>;
   if (mode == kModeF) return (const void*)k_exchange_ll<W, 4, kModeF, C>;
   if (wide) return (const void*)k_exchange_ll<W, 4, kModeXF, C>;
-  return local ? (const void*)k_exchange_ll<W, 2, kModeXF, C, true> : (const void*)k_exchange_ll<W, 2, kModeXF, C>;
+  // (pairs of x items only in the local variant: with the LL paths they cost the tree code
+  // its registers — 236 B of spills)
+  return local ? (const void*)k_exchange_ll<W, 2, kModeXF, C, true> : (const void*)k_exchange_ll<W, 1, kModeXF, C>;
 }
 template <int W>
 static const void* ll_fn(int mode, bool wide, bool chk, int rows, bool local) {
