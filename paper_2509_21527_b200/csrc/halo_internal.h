@@ -31,6 +31,7 @@ constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIM
 constexpr int kTraceW = 16;            // ... words per CTA: 4 stamps + (tag, end) of its first 6 items
 constexpr int kMinItemRows = 32;       // smallest work item (sizes the shift-force slot area)
 constexpr int kMaxItemRows = 512;      // largest work item (x items carry their map slice in shared memory)
+constexpr int kBulkRowsDefault = 0;  // bulk x pulses from HALO_BULK_ROWS rows; 0: off (measured slower)
 constexpr int kMaxTreeRows = 170;      // largest small-tree item (2 passes of 85 roots x 3 components)
 constexpr int kTreeRowsOcc = 85;       // tree item size the occupancy (co-resident grid) is computed for
 constexpr int kRing = 4;                 // LL kernels: item blocks in flight per CTA (narrow variants)
@@ -71,6 +72,11 @@ struct __align__(128) ScratchHdr {
   uint64_t pad5[15];
   uint64_t ns_x[8];        // set_maps: (epoch << 32) | 1: the x-sender's NS-step rows of pulse p landed
   uint64_t pad6[8];
+  // bulk x pulses: rows of pulse p the x-sender has stored into this
+  // rank's x (one release add per launch, by the item that completed the pulse); the
+  // receive's wait item subtracts recv_size once it saw them all: 0 between launches
+  uint64_t bulk_x[8];
+  uint64_t pad7[8];
 };
 static_assert(sizeof(ScratchHdr) <= kHdrBytes, "ScratchHdr too large");
 
@@ -111,6 +117,7 @@ struct Ctrl {
   // the tree items acquire: the non-bonded kernel's slot, Alg. 2).  Own 128-B lines.
   uint32_t xf_cnt;
   uint32_t pad_xf0[31];
+  uint32_t bulk_rows[kMaxLocal][kMaxP];  // rows of bulk pulse (l, p) stored in the current launch (gpu scope)
   uint64_t xf_done;
   uint64_t pad_xf1[15];
 };
@@ -234,7 +241,7 @@ struct PulseDev {
 };
 
 enum : uint8_t { kItemXIndep = 0, kItemXDep = 1, kItemPush = 2, kItemUnpack = 3, kItemXRecv = 4, kItemGather = 5,
-                 kItemFshift = 6, kItemXSend = 7, kItemTree = 8, kItemTreeG = 9 };
+                 kItemFshift = 6, kItemXSend = 7, kItemTree = 8, kItemTreeG = 9, kItemXWait = 10 };
 constexpr uint8_t kHomeLevel = 0xff;   // Item.pulse of gather items over home rows
 
 struct Item {
@@ -280,13 +287,13 @@ struct XEnt {
 static_assert(sizeof(XEnt) == 8, "XEnt");
 
 struct __align__(128) XRec {
-  uint8_t kind;             // kItemXSend / kItemXRecv
+  uint8_t kind;             // kItemXSend / kItemXRecv / kItemXWait
   uint8_t pulse;
   uint16_t lrank;
   uint32_t n_units;         // rows * layout
   uint32_t begin;           // send: first send index (destination row remote_off + begin + e)
   uint32_t cls;             // dependency class (plan order; trace only)
-  float* dst_x;             // send to a rank of this group: its x at row remote_off (direct store)
+  float* dst_x;             // send to a rank of this group, or a bulk pulse: its x at row remote_off (direct store)
   uint64_t* dst_ll;         // send to another group: the receiver's coordinate LL slot p
   float shiftL[kMaxP];      // L_{d_q}: the shift of pulse q (applied iff the entry's mask has q)
   uint8_t pdim[kMaxP];      // d_q
@@ -295,7 +302,10 @@ struct __align__(128) XRec {
   float* xdst;              // recv: own x + (recv_off_p + begin)*W
   uint32_t epoch;           // NS epoch of the plan (a graph captured before a later set_maps is refused)
   uint32_t pad2;
-  uint8_t pad1[128 - 88];
+  uint64_t* bulk;           // bulk pulse: send: &receiver.hdr->bulk_x[p] (release-add the item's rows);
+                            // wait (n_units = recv_size rows): &own hdr->bulk_x[p]
+  uint32_t bulk_total;      // bulk send: rows of the whole pulse (the item completing them releases them all)
+  uint8_t pad1[128 - 100];
 };
 static_assert(sizeof(XRec) == 128, "XRec must be one 128-B line");
 
@@ -409,6 +419,7 @@ struct PlanLQ {
   float* dst_x;             // send of (l, q) to a rank of this group: its x + remote_off rows
   uint64_t* dst_ll;         // ... to another group: the receiver's coordinate LL slot q
   uint64_t* push;           // rows of (l, q) whose x-sender is in another group: its force LL slot q
+  uint64_t* bulk;           // bulk pulse: &receiver.hdr->bulk_x[q] (dst_x is then its x)
   int32_t rcv_l;            // the receiver's (lower neighbour) local index if in this group, else -1
   int32_t snd_l;            // the sender's (upper neighbour) local index if in this group, else -1
   int32_t remote_off;       // where the receiver put this rank's pulse-q rows

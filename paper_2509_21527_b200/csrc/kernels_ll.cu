@@ -122,6 +122,15 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
   // a replaced (or zeroed) plan carries another one and is treated as empty
   const uint32_t n = !kChk || r.epoch == P.plan_epoch ? r.n_units : stale_item(P);
   const uint32_t B = blockDim.x;
+  if (!kLocal && r.kind == kItemXWait) {
+    // a bulk pulse: the x-sender stored this rank's rows straight into
+    // x and counts them here (one release add per send item); wait for all n, then take
+    // them back off so the word is 0 for the next launch
+    if (threadIdx.x == 0 && n != 0 &&
+        wait_geq<true>(r.bulk, n, P.timeout_ns, P.err_host, tcode(10, r.lrank, r.pulse), P.poll_ns))
+      red_add_relaxed_sys(r.bulk, (uint64_t)0 - n);
+    return;
+  }
   if (!kLocal && r.kind == kItemXRecv) {
     // this rank's halo rows of one pulse from another group: LL units -> x rows;
     // 4 units per thread per batch: the polls of a batch are in flight together
@@ -591,6 +600,21 @@ __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU
       x_item<W, kU, kChk, kLocal>(*reinterpret_cast<const XRec*>(blk), reinterpret_cast<const XEnt*>(blk + 128), s_lb,
                                   P, tag_x);
       __syncthreads();  // the item's rows are stored (fused: before its count) and the slot is free
+      if constexpr (!kLocal) {
+        // a bulk pulse's send item: its rows (every thread's stores, ordered by the barrier)
+        // are counted; the receiver's wait item acquires the total
+        const XRec& r = *reinterpret_cast<const XRec*>(blk);
+        if (threadIdx.x == 0 && r.bulk != nullptr && r.kind == kItemXSend && (!kChk || r.epoch == P.plan_epoch)) {
+          // counted at gpu scope; the pulse's last item issues the one system-scope release
+          // (a release per item measured 1.5x slower: every CTA stalls on its NVLink stores)
+          const uint32_t rows = r.n_units / W;
+          uint32_t* c = &ctrl->bulk_rows[r.lrank][r.pulse];
+          if (atom_add_acqrel_gpu(c, rows) + rows == r.bulk_total) {
+            *c = 0;  // (the next launch's items start after this launch completes)
+            red_add_release_sys(r.bulk, r.bulk_total);
+          }
+        }
+      }
       if (kMode == kModeXF && threadIdx.x == 0) {  // the launch's last x item releases xf_done
         if (atom_add_acqrel_gpu(&ctrl->xf_cnt, 1u) == (uint32_t)nx - 1u) {
           ctrl->xf_cnt = 0;  // (the next fused launch's x items start after this launch completes)

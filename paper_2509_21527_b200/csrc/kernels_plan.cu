@@ -212,8 +212,10 @@ __global__ void __launch_bounds__(kPB) k_plan_x(const PlanDev* __restrict__ D) {
     r.n_units = (uint32_t)(e + 1) * D->W;
     r.begin = (uint32_t)istart;
     r.cls = (uint32_t)cls;
-    r.dst_x = a.rcv_l >= 0 ? a.dst_x : nullptr;
-    r.dst_ll = a.rcv_l >= 0 ? nullptr : a.dst_ll;
+    r.dst_x = a.dst_x;    // a rank of this group, or a bulk pulse (the host set exactly one of the two)
+    r.dst_ll = a.dst_ll;
+    r.bulk = a.bulk;
+    r.bulk_total = a.bulk ? (uint32_t)n : 0u;
     for (int q = 0; q < kMaxP; ++q) {
       r.shiftL[q] = D->shiftL[q];
       r.pdim[q] = D->pdim[q];

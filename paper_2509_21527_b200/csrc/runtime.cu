@@ -266,6 +266,7 @@ struct halo_ctx {
                                     // HALO_DIRECT_X=0: every rank its own group, the staged schedule)
   bool prefetch = false;            // LL x launch: L2 prefetch of the f item blocks and home x rows (HALO_PREFETCH=1;
                                     // measured slower at C3: 17.3 -> 18.1 us/step, the prefetches delay the x blocks)
+  int bulk_rows = kBulkRowsDefault;  // bulk x pulses from this many rows (HALO_BULK_ROWS; 0: never, the default), §6.9
   int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
   // NCCL send/recv baseline (halo_nccl_*, HALO_F_NCCL_BASELINE): communicator + packed send rows
   void* nccl_comm = nullptr;
@@ -462,6 +463,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = atoi(e) < 0 ? kPollTight : (uint32_t)atoi(e);
   if (const char* e = getenv("HALO_DIRECT_X")) ctx->collapse = atoi(e) != 0;
   if (const char* e = getenv("HALO_COLLAPSE")) ctx->collapse = atoi(e) != 0;
+  if (const char* e = getenv("HALO_BULK_ROWS")) ctx->bulk_rows = std::max(0, atoi(e));
   if (const char* e = getenv("HALO_RECV_MULT")) ctx->recv_mult = std::min(16, std::max(1, atoi(e)));
   if (const char* e = getenv("HALO_PREFETCH")) ctx->prefetch = atoi(e) != 0;
   if (const char* e = getenv("HALO_PLAN_HOST")) ctx->gpu_plan = atoi(e) == 0;
@@ -814,6 +816,15 @@ static bool same_group(const halo_ctx* ctx, int r1, int r2) {
   return ctx->collapse && ctx->is_local(r1) && ctx->is_local(r2);
 }
 
+// A bulk x pulse: the last pulse (no later pulse forwards its rows)
+// from another hop group, rows >= bulk_rows.  The x-sender stores the rows straight
+// into the receiver's x and counts them in its header; the receiver waits for the
+// count instead of polling LL units: each byte crosses NVLink once, untagged.  Both
+// ends decide on the same number (the sender's send_size is the receiver's recv_size).
+static bool bulk_pulse(const halo_ctx* ctx, int p, int rows) {
+  return ctx->bulk_rows > 0 && p == ctx->P - 1 && rows >= ctx->bulk_rows;
+}
+
 static void fill_lbase(halo_ctx* ctx) {
   const int L = ctx->n_local, P = ctx->P;
   ctx->h_lbase.assign(std::max(1, L), LocalBase{});
@@ -884,6 +895,7 @@ static void build_ll_x(halo_ctx* ctx, int p_lo, int p_hi) {
       const int rcv = ctx->neighbour(r, d, -1);  // coordinates go to the lower neighbour (R1)
       const bool wraps = ctx->cell(r, d) == 0;   // the wrapping sender adds +L_d (R25)
       const bool local = same_group(ctx, r, rcv);
+      const bool bulk = !local && bulk_pulse(ctx, p, n);
       for (int b = 0; b < n;) {
         const uint8_t cls = org[l][m[b]].cls;
         int e = b;
@@ -900,6 +912,10 @@ static void build_ll_x(halo_ctx* ctx, int p_lo, int p_hi) {
         x.epoch = ctx->epoch;
         if (local) {
           x.dst_x = ctx->x[rcv - ctx->first_rank] + (size_t)ctx->remote_off[l * P + p] * W;
+        } else if (bulk) {
+          x.dst_x = ctx->peer_x[rcv] + (size_t)ctx->remote_off[l * P + p] * W;
+          x.bulk = &ctx->hdr_of(rcv)->bulk_x[p];
+          x.bulk_total = (uint32_t)n;
         } else {
           x.dst_ll = ctx->xll_of(rcv) + (size_t)p * ctx->ll_stride;
         }
@@ -923,6 +939,19 @@ static void build_ll_x(halo_ctx* ctx, int p_lo, int p_hi) {
       const int r = ctx->first_rank + l;
       if (same_group(ctx, r, ctx->neighbour(r, ctx->pdim[p], +1))) continue;
       const int n = ctx->recv_size[l * P + p];
+      if (bulk_pulse(ctx, p, n)) {  // one wait item for the whole pulse
+        XI it;
+        memset(&it.rec, 0, sizeof it.rec);
+        it.rec.kind = kItemXWait;
+        it.rec.pulse = (uint8_t)p;
+        it.rec.lrank = (uint16_t)l;
+        it.rec.n_units = (uint32_t)n;  // rows
+        it.rec.cls = 0xff;
+        it.rec.epoch = ctx->epoch;
+        it.rec.bulk = &ctx->hdr_of(r)->bulk_x[p];
+        items.push_back(std::move(it));
+        continue;
+      }
       const int RR = std::min(kMaxItemRows, ctx->recv_mult * R);
       for (int b = 0; b < n; b += RR) {
         const int e = std::min(n, b + RR);
@@ -1395,8 +1424,12 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
       PlanLQ& a = H.lq[l][q];
       a.rcv_l = same_group(ctx, r, rcv) ? rcv - ctx->first_rank : -1;
       a.snd_l = same_group(ctx, r, snd) ? snd - ctx->first_rank : -1;
-      a.dst_x = a.rcv_l >= 0 ? ctx->x[a.rcv_l] + (size_t)ctx->remote_off[i] * W : nullptr;
-      a.dst_ll = a.rcv_l >= 0 ? nullptr : ctx->xll_of(rcv) + (size_t)q * ctx->ll_stride;
+      const bool bulk = a.rcv_l < 0 && bulk_pulse(ctx, q, ctx->send_size[i]);
+      a.dst_x = a.rcv_l >= 0 ? ctx->x[a.rcv_l] + (size_t)ctx->remote_off[i] * W
+                : bulk     ? ctx->peer_x[rcv] + (size_t)ctx->remote_off[i] * W
+                           : nullptr;
+      a.dst_ll = a.rcv_l >= 0 || bulk ? nullptr : ctx->xll_of(rcv) + (size_t)q * ctx->ll_stride;
+      a.bulk = bulk ? &ctx->hdr_of(rcv)->bulk_x[q] : nullptr;
       a.push = a.snd_l >= 0 ? nullptr : ctx->fll_of(snd) + (size_t)q * ctx->ll_stride;
       a.remote_off = ctx->remote_off[i];
       a.atom_offset = ctx->atom_offset[i];
@@ -1445,6 +1478,19 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
       const int r = ctx->first_rank + l;
       if (same_group(ctx, r, ctx->neighbour(r, ctx->pdim[p], +1))) continue;
       const int n = ctx->recv_size[l * P + p];
+      if (bulk_pulse(ctx, p, n)) {  // one wait item for the whole pulse (build_ll_x)
+        XRec x;
+        memset(&x, 0, sizeof x);
+        x.kind = kItemXWait;
+        x.pulse = (uint8_t)p;
+        x.lrank = (uint16_t)l;
+        x.n_units = (uint32_t)n;
+        x.cls = 0xff;
+        x.epoch = ctx->epoch;
+        x.bulk = &ctx->hdr_of(r)->bulk_x[p];
+        recv.push_back(x);
+        continue;
+      }
       const int RR = std::min(kMaxItemRows, ctx->recv_mult * R);
       for (int b = 0; b < n; b += RR) {
         XRec x;
@@ -1873,6 +1919,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     for (int l = 0; l < L; ++l) tab[l] = ctx->xll_of(ctx->first_rank + l);
     CK(cudaMemcpyAsync(ctx->d_small + 16384, tab, sizeof(uint64_t*) * L, cudaMemcpyHostToDevice, st));
     CK(launch_zero_ll(reinterpret_cast<uint64_t* const*>(ctx->d_small + 16384), 2 * (size_t)P * ctx->ll_stride, L, st));
+    for (int l = 0; l < L; ++l)  // bulk x counters (0 between launches; reset after an aborted one)
+      CK(cudaMemsetAsync(ctx->hdr_of(ctx->first_rank + l)->bulk_x, 0, sizeof(ScratchHdr::bulk_x), st));
   }
   fill_rank_dev(ctx);
   // ranks/pulse tables are needed by the select/depmask kernels already
@@ -2122,6 +2170,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   // the fused launch's per-rank halo counters count from here (the per-pulse x
   // launches above counted too)
   CK(cudaMemsetAsync(&ctx->ctrl->xf_cnt, 0, sizeof(uint32_t), st));
+  CK(cudaMemsetAsync(ctx->ctrl->bulk_rows, 0, sizeof(Ctrl::bulk_rows), st));
   CK(cudaStreamSynchronize(st));
   ctx->seq_host_x = seqs[0];
   ctx->seq_host_f = seqs[1];

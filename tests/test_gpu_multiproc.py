@@ -38,9 +38,14 @@ def _worker(rank, world, port, cases, out):
             case = Case(name, seed=seed, force_kind=kind, layout=layout, rounded=bool(flags & ROUNDED))
             if case.nranks % world:
                 continue
+            if flags & BULK:
+                os.environ["HALO_BULK_ROWS"] = "1"  # read at halo_init (every process sets it)
+            else:
+                os.environ.pop("HALO_BULK_ROWS", None)
             sess = HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout, capacity=case.capacity,
-                               device=dev, flags=flags, nprocs=world, proc=rank, timeout_s=30.0)
-            run_gpu_case(case, sess, steps=steps, atomic=bool(flags & 1) and kind != "int", barrier=dist.barrier)
+                               device=dev, flags=flags & ~(BULK | FUSED), nprocs=world, proc=rank, timeout_s=30.0)
+            run_gpu_case(case, sess, steps=steps, atomic=bool(flags & 1) and kind != "int", barrier=dist.barrier,
+                         fused=bool(flags & FUSED))
             dist.barrier()
             sess.destroy()
             dist.barrier()
@@ -54,6 +59,9 @@ PAPER = 1 << 4
 CE = 1 << 5
 TMA = (1 << 7) | (1 << 8)  # HALO_F_TMA_STORE | HALO_F_TMA_GET
 ROUNDED = 1 << 9  # HALO_F_ROUNDED_ZONES
+# test-side markers, stripped before halo_init: BULK = HALO_BULK_ROWS=1 (every last pulse
+# between processes is a bulk pulse); FUSED = one halo_exchange_xf per step
+BULK, FUSED = 1 << 28, 1 << 29
 CASES = [  # (config, seed, forces, flags, layout, steps); flags 0 = LL protocol
     ("C1", 1, "int", 0, 3, 2),
     ("W3", 1, "int", 0, 3, 1),
@@ -71,6 +79,10 @@ CASES = [  # (config, seed, forces, flags, layout, steps); flags 0 = LL protocol
     ("T2P", 2, "int", PAPER | TMA, 4, 2),
     ("C3", 2, "int", ROUNDED, 3, 2),          # rounded zones (R31), LL protocol
     ("C2", 1, "normal", PAPER | ROUNDED, 4, 2),
+    ("C3", 1, "normal", BULK, 3, 3),         # bulk x pulses over NVLink (last pulse stored straight into x)
+    ("T2P", 1, "int", BULK, 4, 2),
+    ("C1", 2, "normal", BULK | FUSED, 3, 3),
+    ("C5", 2, "normal", BULK | FUSED, 3, 2),
     ("C1", 1, "int", CE, 3, 2),             # copy-engine path
     ("C3", 1, "normal", CE, 3, 3),
     ("C5", 2, "int", CE, 3, 2),

@@ -20,26 +20,33 @@ TMA = PAPER | TMA_STORE | TMA_GET
 # with LL transport, receive items and force pushes on every pulse: the code paths a
 # pulse between two GPUs takes); "ll" = the default, one hop group per process
 STAGED = 1 << 30  # test-side marker, stripped before halo_init
-PROTOS = [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged"), pytest.param(PAPER, id="paper"),
-          pytest.param(TMA, id="paper_tma"), pytest.param(CE, id="ce")]
+# ll_staged + HALO_BULK_ROWS=1: every last pulse is a bulk pulse (the
+# x-sender stores into the receiver's x, one wait item counts the rows)
+BULK = 1 << 29
+PROTOS = [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged"), pytest.param(BULK, id="ll_bulk"),
+          pytest.param(PAPER, id="paper"), pytest.param(TMA, id="paper_tma"), pytest.param(CE, id="ce")]
 
 
 def session_for(case, flags=0, layout=None, capacity=None):
     import os
     from paper_2509_21527_b200.session import HaloSession
-    staged = bool(flags & STAGED)
-    old = os.environ.get("HALO_COLLAPSE")
-    if staged:
-        os.environ["HALO_COLLAPSE"] = "0"  # read at halo_init
+    env = {}
+    if flags & (STAGED | BULK):
+        env["HALO_COLLAPSE"] = "0"  # read at halo_init
+    if flags & BULK:
+        env["HALO_BULK_ROWS"] = "1"
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         return HaloSession(case.grid, case.L, case.rc, case.pulses, layout=layout or case.layout,
-                           capacity=capacity or case.capacity, device=0, flags=flags & ~STAGED, timeout_s=5.0)
+                           capacity=capacity or case.capacity, device=0, flags=flags & ~(STAGED | BULK),
+                           timeout_s=5.0)
     finally:
-        if staged:
-            if old is None:
-                os.environ.pop("HALO_COLLAPSE")
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k)
             else:
-                os.environ["HALO_COLLAPSE"] = old
+                os.environ[k] = v
 
 
 @pytest.mark.parametrize("proto", PROTOS)
@@ -153,14 +160,15 @@ def test_cuda_graph_replay(proto):
     sess.destroy()
 
 
+@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(BULK, id="ll_bulk")])
 @pytest.mark.parametrize("renew", ["set_maps", "migrate"])
-def test_stale_graph_replay_refused(renew):
+def test_stale_graph_replay_refused(renew, proto):
     """A graph captured before an NS step (set_maps / migrate) and replayed after it:
     every item of the new plan carries the new epoch, so the replay touches nothing
     and the next call reports HALO_ERR_STATE (ADVICE: captured launches freeze the plan)."""
     from paper_2509_21527_b200.halo import HaloError
     case = Case("T3D", seed=2, force_kind="int")
-    sess = session_for(case)
+    sess = session_for(case, flags=proto)
     run_gpu_case(case, sess)
     s = torch.cuda.Stream()
     fshift = torch.zeros(sess.n_local, 3, 3, dtype=torch.float64, device=sess.device)
@@ -192,7 +200,8 @@ def test_stale_graph_replay_refused(renew):
     sess.halo.destroy()
 
 
-@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged")])
+@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged"),
+                                   pytest.param(BULK, id="ll_bulk")])
 @pytest.mark.parametrize("name", ["T3D", "T2P", "T4x2", "C2", "C5", "C3"])
 def test_gpu_plan_equals_host_plan(name, proto, monkeypatch):
     """The LL plan built on the device (kernels_plan.cu) == the host builder's plan of the
@@ -205,7 +214,8 @@ def test_gpu_plan_equals_host_plan(name, proto, monkeypatch):
     sess.destroy()
 
 
-@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged")])
+@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged"),
+                                   pytest.param(BULK, id="ll_bulk")])
 @pytest.mark.parametrize("fused", [False, True])
 def test_ll_tag_wrap(proto, fused, monkeypatch):
     """LL units carry the low 32 bits of the launch's sequence number: starting 3 below
