@@ -561,6 +561,7 @@ struct HsParams {
   uint64_t* off_dst[kMaxLocal];    // &upper.hdr->meta_off[p]
   int* err_host;
   uint64_t timeout_ns;
+  uint32_t sys_mask;               // bit l: size_dst[l] in another process; bit 16+l: off_dst[l] (else gpu-scope release)
 };
 
 struct StatusParams {
@@ -580,6 +581,7 @@ struct StatusParams {
   int P, W, auto_tr, rows_fixed;   // rows_fixed: R given (HALO_ITEM_ROWS), else 0
   int64_t ctas;                    // co-resident CTAs the item size is chosen for
   uint64_t ce_bytes;
+  int all_local;                   // every rank in this process: gpu-scope releases suffice
 };
 
 // PP <-> PME redistribution (halo_pme_*, kernels_pme.cu)

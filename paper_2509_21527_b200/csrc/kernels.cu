@@ -503,7 +503,9 @@ __global__ void k_handshake(const __grid_constant__ HsParams H) {
   const int p = H.p;
   const uint64_t ep = (uint64_t)H.epoch << 32;
   const uint32_t sz = (uint32_t)c->send_size[lr][p];
-  st_release_sys(H.size_dst[lr], ep | sz);
+  // a neighbour in this process reads at gpu scope: no system-scope fence (NS-step latency)
+  if (H.sys_mask >> lr & 1u) st_release_sys(H.size_dst[lr], ep | sz);
+  else st_release_gpu(H.size_dst[lr], ep | sz);
   uint32_t recv = wait_epoch(&H.own[lr]->meta_size[p], H.epoch, H.timeout_ns, H.err_host, tcode(6, lr, p));
   if (recv == 0xffffffffu) recv = 0;
   const int off = c->n_total[lr];
@@ -513,7 +515,8 @@ __global__ void k_handshake(const __grid_constant__ HsParams H) {
     grant = 0xffffffffu;
     recv = 0;
   }
-  st_release_sys(H.off_dst[lr], ep | grant);
+  if (H.sys_mask >> (16 + lr) & 1u) st_release_sys(H.off_dst[lr], ep | grant);
+  else st_release_gpu(H.off_dst[lr], ep | grant);
   const uint32_t roff = wait_epoch(&H.own[lr]->meta_off[p], H.epoch, H.timeout_ns, H.err_host, tcode(7, lr, p));
   if (roff == 0xffffffffu) {  // receiver out of capacity (or timeout): send nothing
     c->send_size[lr][p] = 0;
@@ -698,7 +701,10 @@ __global__ void k_status(const __grid_constant__ StatusParams S) {
     vote |= (uint32_t)kVoteRows << (31 - __clz((unsigned)(R / kMinItemRows)));
   }
   const uint32_t mine = (uint32_t)S.ctrl->err[lr] | vote;
-  for (int t = threadIdx.x; t < S.nranks; t += blockDim.x) st_release_sys(&S.all[t]->status[me], ep | mine);
+  for (int t = threadIdx.x; t < S.nranks; t += blockDim.x) {
+    if (S.all_local) st_release_gpu(&S.all[t]->status[me], ep | mine);
+    else st_release_sys(&S.all[t]->status[me], ep | mine);
+  }
   for (int t = threadIdx.x; t < S.nranks; t += blockDim.x) {
     const uint32_t v = wait_epoch(&S.own[lr]->status[t], S.epoch, S.timeout_ns, S.err_host, tcode(8, lr, 0));
     if (v != 0xffffffffu && v != 0) atomicOr(&s_or, (int)v);

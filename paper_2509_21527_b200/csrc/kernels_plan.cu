@@ -32,6 +32,31 @@
 
 #include "halo_internal.h"
 
+namespace {
+// The plan kernels run back to back on one stream, each a programmatic dependent of
+// the previous one (plan_launch): its CTAs become resident while the previous grid
+// drains, and griddepcontrol.wait holds them until that grid completed and its
+// writes are visible (each kernel waits before touching memory, so the chain is
+// transitive).  Saves the launch gap between the ~12 small kernels of an NS step.
+__device__ __forceinline__ void plan_pdl() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... Args, typename... Actual>
+cudaError_t plan_launch(void (*k)(Args...), dim3 grid, unsigned block, cudaStream_t st, Actual... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<Args>(args)...);
+}
+}  // namespace
+
 namespace halo {
 
 namespace {
@@ -86,6 +111,7 @@ __device__ __forceinline__ int block_count_class(bool pred, int cls, int nc, int
 
 // ------------------------------------------------------------------ x origins
 __global__ void k_plan_org_home(const PlanDev* __restrict__ D) {
+  plan_pdl();
   const int l = blockIdx.y;
   const int n = D->n_home[l];
   uint64_t* o = D->org + (size_t)l * D->cap;
@@ -97,6 +123,7 @@ __global__ void k_plan_org_home(const PlanDev* __restrict__ D) {
 // sent row (+ this pulse's shift bit if the sender wrapped); from another group, the
 // LL unit i of slot q (class q + 1).  Pulses in order (stream-ordered launches).
 __global__ void k_plan_org_pulse(const PlanDev* __restrict__ D, int q) {
+  plan_pdl();
   const int l = blockIdx.y;
   const PlanLQ& a = D->lq[l][q];
   uint64_t* o = D->org + (size_t)l * D->cap + a.atom_offset;
@@ -125,6 +152,7 @@ __device__ __forceinline__ int plan_x_cls(const uint64_t* org, const int32_t* m,
 
 template <int kPass>
 __global__ void __launch_bounds__(kPB) k_plan_x(const PlanDev* __restrict__ D) {
+  plan_pdl();
   const int pl = blockIdx.y, p = pl / D->L, l = pl % D->L, c = blockIdx.x;
   const PlanLQ& a = D->lq[l][p];
   const int n = a.send_size, R = D->R, nc = D->P + 1;
@@ -227,6 +255,7 @@ __global__ void __launch_bounds__(kPB) k_plan_x(const PlanDev* __restrict__ D) {
 
 // ------------------------------------------------------------------ f trees
 __global__ void k_plan_child(const PlanDev* __restrict__ D) {
+  plan_pdl();
   const int l = blockIdx.y / D->P, q = blockIdx.y % D->P;
   const int n = D->lq[l][q].send_size;
   const int32_t* m = D->maps[l] + (size_t)q * D->map_stride;
@@ -308,6 +337,7 @@ __device__ __forceinline__ uint8_t plan_fs_mask(const PlanDev* __restrict__ D, i
 // One thread per row, kPB rows per CTA (blockIdx.x), blockIdx.y = local rank: is the row
 // a root, its tree's class (rcls, 0xff = not a root), and the CTA's roots per class.
 __global__ void __launch_bounds__(kPB) k_plan_roots(const PlanDev* __restrict__ D) {
+  plan_pdl();
   const int l = blockIdx.y, nc = D->P + 1;
   const int t = blockIdx.x * kPB + threadIdx.x;
   __shared__ int s_w[kMaxP + 1][kPB / 32];
@@ -329,19 +359,28 @@ __global__ void __launch_bounds__(kPB) k_plan_roots(const PlanDev* __restrict__ 
   if (threadIdx.x < nc) D->bcnt[((size_t)l * D->nblk + blockIdx.x) * nc + threadIdx.x] = s_tot[threadIdx.x];
 }
 
-// One CTA per local rank, one thread per class: exclusive prefix of the per-CTA root
-// counts (boff) and the totals (rcnt).
+// One CTA per local rank, one warp per class: exclusive prefix of the per-CTA root
+// counts (boff) and the totals (rcnt), 32 blocks per step (shuffle scan).
 __global__ void k_plan_rank(const PlanDev* __restrict__ D) {
-  const int l = blockIdx.x, nc = D->P + 1, c = threadIdx.x;
+  plan_pdl();
+  const int l = blockIdx.x, nc = D->P + 1, c = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (c >= nc) return;
+  const int nb = D->nblk;
   int acc = 0;
-  for (int b = 0; b < D->nblk; ++b) {
-    const size_t i = ((size_t)l * D->nblk + b) * nc + c;
-    const int v = D->bcnt[i];
-    D->boff[i] = acc;
-    acc += v;
+  for (int b0 = 0; b0 < nb; b0 += 32) {
+    const int b = b0 + lane;
+    const size_t i = ((size_t)l * nb + b) * nc + c;
+    const int v = b < nb ? D->bcnt[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (b < nb) D->boff[i] = acc + incl - v;
+    acc += __shfl_sync(0xffffffffu, incl, 31);
   }
-  D->rcnt[l * nc + c] = acc;
+  if (lane == 0) D->rcnt[l * nc + c] = acc;
 }
 
 // Every root writes its 32-B record and node indices into slot rank % RT of item
@@ -351,6 +390,7 @@ __global__ void k_plan_rank(const PlanDev* __restrict__ D) {
 // set bits of its mask, in table order: what the host builder gives, R13).
 template <bool kMask>
 __global__ void __launch_bounds__(kPB) k_plan_f(const PlanDev* __restrict__ D) {
+  plan_pdl();
   const int l = blockIdx.y, nc = D->P + 1;
   const int n = D->n_total[l], RT = D->RT;
   const int t = blockIdx.x * kPB + threadIdx.x;
@@ -431,25 +471,25 @@ static unsigned plan_gx(int rows) { return (unsigned)std::max(1, std::min(64, (r
 
 cudaError_t launch_plan_count(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st) {
   const unsigned gx = plan_gx(max_rows);
-  k_plan_org_home<<<dim3(gx, L), 256, 0, st>>>(D);
-  for (int q = 0; q < P; ++q) k_plan_org_pulse<<<dim3(gx, L), 256, 0, st>>>(D, q);
+  cudaError_t e = plan_launch(k_plan_org_home, dim3(gx, L), 256, st, D);
+  for (int q = 0; q < P && e == cudaSuccess; ++q) e = plan_launch(k_plan_org_pulse, dim3(gx, L), 256, st, D, q);
   const unsigned xnch = (unsigned)((max_send + kPB - 1) / kPB);
-  k_plan_x<0><<<dim3(std::max(1u, xnch), P * L), kPB, 0, st>>>(D);
-  k_plan_x<1><<<dim3(std::max(1u, xnch), P * L), kPB, 0, st>>>(D);
-  k_plan_child<<<dim3(gx, L * P), 256, 0, st>>>(D);
+  if (e == cudaSuccess) e = plan_launch(k_plan_x<0>, dim3(std::max(1u, xnch), P * L), kPB, st, D);
+  if (e == cudaSuccess) e = plan_launch(k_plan_x<1>, dim3(std::max(1u, xnch), P * L), kPB, st, D);
+  if (e == cudaSuccess) e = plan_launch(k_plan_child, dim3(gx, L * P), 256, st, D);
   const unsigned nblk = (unsigned)((max_rows + kPB - 1) / kPB);
-  k_plan_roots<<<dim3(nblk, L), kPB, 0, st>>>(D);
-  k_plan_rank<<<L, 32, 0, st>>>(D);
-  return cudaGetLastError();
+  if (e == cudaSuccess) e = plan_launch(k_plan_roots, dim3(nblk, L), kPB, st, D);
+  if (e == cudaSuccess) e = plan_launch(k_plan_rank, dim3(L), 32 * (P + 1), st, D);
+  return e;
 }
 
 cudaError_t launch_plan_write(const PlanDev* D, int L, int P, int max_rows, int max_send, cudaStream_t st) {
   const unsigned xnch = (unsigned)((max_send + kPB - 1) / kPB);
-  k_plan_x<2><<<dim3(std::max(1u, xnch), P * L), kPB, 0, st>>>(D);
+  cudaError_t e = plan_launch(k_plan_x<2>, dim3(std::max(1u, xnch), P * L), kPB, st, D);
   const unsigned nblk = (unsigned)((max_rows + kPB - 1) / kPB);
-  k_plan_f<true><<<dim3(nblk, L), kPB, 0, st>>>(D);
-  k_plan_f<false><<<dim3(nblk, L), kPB, 0, st>>>(D);
-  return cudaGetLastError();
+  if (e == cudaSuccess) e = plan_launch(k_plan_f<true>, dim3(nblk, L), kPB, st, D);
+  if (e == cudaSuccess) e = plan_launch(k_plan_f<false>, dim3(nblk, L), kPB, st, D);
+  return e;
 }
 
 int plan_rows_per_cta() { return kPB; }

@@ -266,6 +266,7 @@ struct halo_ctx {
                                     // HALO_DIRECT_X=0: every rank its own group, the staged schedule)
   bool prefetch = false;            // LL x launch: L2 prefetch of the f item blocks and home x rows (HALO_PREFETCH=1;
                                     // measured slower at C3: 17.3 -> 18.1 us/step, the prefetches delay the x blocks)
+  bool packed_blocking = false;      // halo_step_host_packed waits with cudaStreamSynchronize (HALO_PACKED_BLOCKING)
   int bulk_rows = kBulkRowsDefault;  // bulk x pulses from this many rows (HALO_BULK_ROWS; 0: never, the default), §6.9
   int recv_mult = 1;                // x receive items are recv_mult x item_rows rows (HALO_RECV_MULT; 2, 4 measured slower)
   // NCCL send/recv baseline (halo_nccl_*, HALO_F_NCCL_BASELINE): communicator + packed send rows
@@ -463,6 +464,7 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (const char* e = getenv("HALO_POLL_NS")) ctx->poll_ns = atoi(e) < 0 ? kPollTight : (uint32_t)atoi(e);
   if (const char* e = getenv("HALO_DIRECT_X")) ctx->collapse = atoi(e) != 0;
   if (const char* e = getenv("HALO_COLLAPSE")) ctx->collapse = atoi(e) != 0;
+  if (const char* e = getenv("HALO_PACKED_BLOCKING")) ctx->packed_blocking = atoi(e) != 0;
   if (const char* e = getenv("HALO_BULK_ROWS")) ctx->bulk_rows = std::max(0, atoi(e));
   if (const char* e = getenv("HALO_RECV_MULT")) ctx->recv_mult = std::min(16, std::max(1, atoi(e)));
   if (const char* e = getenv("HALO_PREFETCH")) ctx->prefetch = atoi(e) != 0;
@@ -1919,7 +1921,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     for (int l = 0; l < L; ++l) tab[l] = ctx->xll_of(ctx->first_rank + l);
     CK(cudaMemcpyAsync(ctx->d_small + 16384, tab, sizeof(uint64_t*) * L, cudaMemcpyHostToDevice, st));
     CK(launch_zero_ll(reinterpret_cast<uint64_t* const*>(ctx->d_small + 16384), 2 * (size_t)P * ctx->ll_stride, L, st));
-    for (int l = 0; l < L; ++l)  // bulk x counters (0 between launches; reset after an aborted one)
+    for (int l = 0; l < L && ctx->bulk_rows > 0; ++l)  // bulk x counters (0 between launches; reset after an aborted one)
       CK(cudaMemsetAsync(ctx->hdr_of(ctx->first_rank + l)->bulk_x, 0, sizeof(ScratchHdr::bulk_x), st));
   }
   fill_rank_dev(ctx);
@@ -2020,6 +2022,8 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
       H.own[l] = ctx->hdr_of(r);
       H.size_dst[l] = &ctx->hdr_of(ctx->neighbour(r, d, -1))->meta_size[p];
       H.off_dst[l] = &ctx->hdr_of(ctx->neighbour(r, d, +1))->meta_off[p];
+      if (!ctx->is_local(ctx->neighbour(r, d, -1))) H.sys_mask |= 1u << l;
+      if (!ctx->is_local(ctx->neighbour(r, d, +1))) H.sys_mask |= 1u << (16 + l);
     }
     CK(launch_handshake(H, st));  // (dependency masks: in k_ns_x below)
     if (maps) {  // the next pulse's host validation needs n_total
@@ -2074,6 +2078,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   SP.first_rank = ctx->first_rank;
   for (int l = 0; l < L; ++l) SP.own[l] = ctx->hdr_of(ctx->first_rank + l);
   for (int r = 0; r < ctx->nranks; ++r) SP.all[r] = ctx->hdr_of(r);
+  SP.all_local = ctx->nranks == ctx->n_local;
   SP.err_host = ctx->err_dev;
   SP.timeout_ns = timeout_ns;
   SP.vote = 1;
@@ -2170,7 +2175,7 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   // the fused launch's per-rank halo counters count from here (the per-pulse x
   // launches above counted too)
   CK(cudaMemsetAsync(&ctx->ctrl->xf_cnt, 0, sizeof(uint32_t), st));
-  CK(cudaMemsetAsync(ctx->ctrl->bulk_rows, 0, sizeof(Ctrl::bulk_rows), st));
+  if (ctx->bulk_rows > 0) CK(cudaMemsetAsync(ctx->ctrl->bulk_rows, 0, sizeof(Ctrl::bulk_rows), st));
   CK(cudaStreamSynchronize(st));
   ctx->seq_host_x = seqs[0];
   ctx->seq_host_f = seqs[1];
@@ -2277,6 +2282,7 @@ halo_status halo_migrate(halo_ctx* ctx, const int* n_home_in, int32_t* const* gi
   SP.first_rank = ctx->first_rank;
   for (int l = 0; l < L; ++l) SP.own[l] = ctx->hdr_of(ctx->first_rank + l);
   for (int r = 0; r < ctx->nranks; ++r) SP.all[r] = ctx->hdr_of(r);
+  SP.all_local = ctx->nranks == ctx->n_local;
   SP.err_host = ctx->err_dev;
   SP.timeout_ns = M.timeout_ns;
   CK(launch_status(SP, st));
@@ -2873,7 +2879,17 @@ halo_status halo_step_host_packed(halo_ctx* ctx, const void* in_host, void* out_
       ctx->seq_host_f = ll_seq_next(ctx->seq_host_f);
     }
   }
-  CK(cudaStreamSynchronize(st));
+  // the caller's results are in out_host when this returns: poll the stream instead of a
+  // blocking synchronise (whose yield / wake-up latency lands in every step of a
+  // latency-bound host loop); HALO_PACKED_BLOCKING=1 restores cudaStreamSynchronize
+  if (ctx->packed_blocking) {
+    CK(cudaStreamSynchronize(st));
+  } else {
+    cudaError_t q;
+    while ((q = cudaStreamQuery(st)) == cudaErrorNotReady) {
+    }
+    CK(q);
+  }
   return check_err_word(ctx);
 }
 
