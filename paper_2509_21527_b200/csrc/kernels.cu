@@ -905,7 +905,8 @@ cudaError_t launch_coop_kernel_ex(const void* fn, int grid, int block, void** ar
 
 cudaError_t launch_empty(int grid, cudaStream_t st, uint64_t* remote, uint32_t nwords) {
   void* args[] = {(void*)&remote, (void*)&nwords};
-  return launch_coop_kernel_ex((const void*)k_empty, grid, kThreads, args, st, true, 0, nullptr);
+  static const int block = getenv("HALO_EMPTY_BLOCK") ? atoi(getenv("HALO_EMPTY_BLOCK")) : kThreads;  // grid-size study
+  return launch_coop_kernel_ex((const void*)k_empty, grid, block, args, st, true, 0, nullptr);
 }
 
 cudaError_t launch_coop_kernel(const void* fn, int grid, int block, void** args, cudaStream_t st) {

@@ -3044,8 +3044,11 @@ halo_status halo_floor_empty_pair(halo_ctx* ctx, void* stream) {
   if (!ctx->maps_ready) return fail(ctx, HALO_ERR_STATE, "floor before set_maps");
   // the step's two launches with no work: the grids of the current x and f launches,
   // the same programmatic-dependent-launch attributes, empty bodies
-  const int gx = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
-  const int gf = grid_for(ctx->n_items_f, ctx->n_local, ctx->cap_f());
+  int gx = grid_for(ctx->n_items_x, ctx->n_local, ctx->cap_x());
+  int gf = grid_for(ctx->n_items_f, ctx->n_local, ctx->cap_f());
+  // grid-size study (HALO_EMPTY_GX / HALO_EMPTY_GF): what the CTA count alone costs
+  if (const char* e = getenv("HALO_EMPTY_GX")) gx = std::max(1, atoi(e));
+  if (const char* e = getenv("HALO_EMPTY_GF")) gf = std::max(1, atoi(e));
   CK(launch_empty(gx, (cudaStream_t)stream, nullptr, 0));
   CK(launch_empty(gf, (cudaStream_t)stream, nullptr, 0));
   return HALO_OK;
