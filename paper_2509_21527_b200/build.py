@@ -12,6 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhalo.so")
+# the checked build (-DHALO_BOUNDS_CHECK, scripts/bounds_check.py, tests/test_gpu_bounds.py)
+CHECKED = os.path.join(HERE, "libhalo_checked.so")
 SOURCES = ["runtime.cu", "kernels.cu", "kernels_ll.cu", "kernels_ce.cu", "kernels_ns.cu", "kernels_pme.cu", "kernels_plan.cu",
            "nccl_baseline.cu",
            "kernels_floor.cu"]
@@ -34,9 +36,10 @@ def _newest_input() -> float:
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
     """defines: extra -D switches (A/B timing variants in scripts/, written to `out`)."""
-    if not force and out == LIB and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_input():
-        return LIB
-    objs = [os.path.join(CSRC, src.replace(".cu", ".o" if out == LIB else ".ab.o")) for src in SOURCES]
+    if not force and out in (LIB, CHECKED) and os.path.exists(out) and os.path.getmtime(out) >= _newest_input():
+        return out
+    tag = ".o" if out == LIB else ".checked.o" if out == CHECKED else ".ab.o"
+    objs = [os.path.join(CSRC, src.replace(".cu", tag)) for src in SOURCES]
 
     def compile_one(k):
         cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
@@ -67,5 +70,12 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+def build_checked(force: bool = False) -> str:
+    """The bounds-checked variant of the library (same sources, -DHALO_BOUNDS_CHECK)."""
+    return build(force=force, out=CHECKED, defines=("HALO_BOUNDS_CHECK",))
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))

@@ -44,6 +44,7 @@ __host__ __device__ __forceinline__ uint64_t ll_seq_next(uint64_t s) {
   return (uint32_t)s == 0 ? s + 1 : s;
 }
 constexpr int kErrKindStalePlan = 31;        // error-word kind: a replayed graph met a plan of another NS epoch
+constexpr int kErrKindBounds = 30;           // error-word kind: a bounds check of the checked build (HALO_BOUNDS_CHECK) failed
 constexpr uint32_t kPollTight = 0xffffffffu;  // ExParams.poll_ns: tight polling only, no backoff (HALO_POLL_NS=-1)
 
 // Written by PEERS (system scope).  Each array on its own 128-B lines.
@@ -409,6 +410,7 @@ struct ExParams {
   int pf_x;                 // 1: prefetch every local rank's home x rows
   uint32_t plan_epoch;      // LL: the NS epoch whose item blocks this launch expects (records carry theirs)
   int all_local;            // LL: every pulse of every local rank stays in this hop group (no LL units)
+  int cap_rows;             // rows of every x / f buffer (the checked build's bounds)
 };
 
 // GPU plan build of the LL protocol (set_maps, P <= 3: every force tree has <= 8

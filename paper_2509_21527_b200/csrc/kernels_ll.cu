@@ -94,6 +94,20 @@ __device__ __forceinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uin
   }
 }
 
+// Checked build (-DHALO_BOUNDS_CHECK, scripts/bounds_check.py; compute-sanitizer is closed
+// on this GPU pool): every global index the kernel derives from a plan record is checked
+// against its buffer; a failed check reports kErrKindBounds (local rank, check number),
+// and the access goes to index 0 instead.  The production build compiles the checks out.
+#ifdef HALO_BOUNDS_CHECK
+__device__ __noinline__ bool bc_fail(const ExParams& P, int code, int lr) {
+  report_timeout(P.err_host, tcode(kErrKindBounds, lr & 0xff, code));
+  return false;
+}
+#define HALO_BC(cond, code, lr) ((cond) ? true : bc_fail(P, (code), (lr)))
+#else
+#define HALO_BC(cond, code, lr) true
+#endif
+
 // An item of another NS epoch's plan (a stale graph replay): report once, do nothing.
 __device__ __noinline__ uint32_t stale_item(const ExParams& P) {
   if (threadIdx.x == 0) report_timeout(P.err_host, tcode(kErrKindStalePlan, 0, 0));
@@ -135,6 +149,8 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
     // this rank's halo rows of one pulse from another group: LL units -> x rows;
     // 4 units per thread per batch: the polls of a batch are in flight together
     constexpr int kR = 4;
+    if (!HALO_BC((uint64_t)r.begin * W + n <= P.ll_stride && r.begin + n / W <= (uint32_t)P.cap_rows, 7, r.lrank))
+      return;
     for (uint32_t base = threadIdx.x; base < n; base += kR * B) {
       uint64_t w[kR];
 #pragma unroll
@@ -164,14 +180,19 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
       if (u < n) {
         const uint32_t e = u / W;
         const int c = (int)(u - e * W);
-        const XEnt E = ent[e];
+        XEnt E = ent[e];
+        if (!HALO_BC(E.l < (uint32_t)P.n_local, 1, r.lrank)) E.l = 0;
         const LocalBase& L = lb[E.l];
         mask[k] = E.mask;
         if (kLocal || !(E.kq & 0x80u)) {
           // a home row: never written during the kernel
+          if (!HALO_BC(E.row < (uint32_t)P.cap_rows, 2, r.lrank)) E.row = 0;
           w[k] = ((uint64_t)tag << 32) | __float_as_uint(__ldg(L.x + (size_t)E.row * W + c));
         } else {
           const int q = E.kq & 7;
+          if (!HALO_BC(q < P.P && (uint64_t)E.row * W + c < P.ll_stride &&
+                           (uint32_t)L.recv_off[q] + E.row < (uint32_t)P.cap_rows, 3, r.lrank))
+            E.row = 0;
           if (q < P.p_lo || (P.debug & kMutateXNoWait)) {
             // arrived in an earlier launch (set_maps' per-pulse exchanges): final in x.
             // kMutateXNoWait: the protocol mutation the sentinel tests must catch —
@@ -198,7 +219,9 @@ __device__ __forceinline__ void x_item(const XRec& r, const XEnt* ent, const Loc
         for (int q = 0; q < kMaxP; ++q)
           if (mask[k] >> q & 1u) v = __fadd_rn(v, c == r.pdim[q] ? r.shiftL[q] : 0.0f);
       }
-      const size_t o = (size_t)(r.begin + e) * W + c;
+      size_t o = (size_t)(r.begin + e) * W + c;
+      if (!HALO_BC(kLocal || r.dst_x != nullptr ? r.begin + e < (uint32_t)P.cap_rows : o < P.ll_stride, 4, r.lrank))
+        o = 0;
       if (kLocal || r.dst_x != nullptr) r.dst_x[o] = v;  // a rank of this group: its halo row directly
       else st_relaxed_sys(r.dst_ll + o, ll_pack(v, tag));
     }
@@ -229,7 +252,9 @@ __device__ __forceinline__ void x_send_pair(const XRec& r0, const XEnt* e0, cons
       if (u < n[i]) {
         const uint32_t e = u / W;
         const int c = (int)(u - e * W);
-        const XEnt E = ee[i][e];
+        XEnt E = ee[i][e];
+        if (!HALO_BC(E.l < (uint32_t)P.n_local, 1, rr[i]->lrank)) E.l = 0;
+        if (!HALO_BC(E.row < (uint32_t)P.cap_rows, 2, rr[i]->lrank)) E.row = 0;
         const LocalBase& L = lb[E.l];
         mask[i] = E.mask;
         if (kLocal || !(E.kq & 0x80u)) {
@@ -259,7 +284,9 @@ __device__ __forceinline__ void x_send_pair(const XRec& r0, const XEnt* e0, cons
         for (int q = 0; q < kMaxP; ++q)
           if (mask[i] >> q & 1u) v = __fadd_rn(v, c == r.pdim[q] ? r.shiftL[q] : 0.0f);
       }
-      const size_t o = (size_t)(r.begin + e) * W + c;
+      size_t o = (size_t)(r.begin + e) * W + c;
+      if (!HALO_BC(kLocal || r.dst_x != nullptr ? r.begin + e < (uint32_t)P.cap_rows : o < P.ll_stride, 4, r.lrank))
+        o = 0;
       if (kLocal || r.dst_x != nullptr) r.dst_x[o] = v;
       else st_relaxed_sys(r.dst_ll + o, ll_pack(v, tag));
     }
@@ -421,6 +448,19 @@ __device__ __forceinline__ void tree_item(const GRec& g, const TRoot* roots, con
     const TRoot R = roots[j];
     const uint32_t* il = reinterpret_cast<const uint32_t*>(nodes + 2 * j);
     const int nn = R.nn;
+#ifdef HALO_BOUNDS_CHECK
+    if (!HALO_BC(nn >= 1 && nn <= kFastNodes && j < (uint32_t)P.tree_rows, 9, g.lrank)) continue;
+    {
+      bool bad = false;
+      for (int k = 0; k < nn; ++k) {
+        const uint32_t l = il[k] >> 24, i = il[k] & (kMaxRows - 1);
+        bad |= l >= (uint32_t)P.n_local;
+        bad |= (R.llmask >> k & 1u) ? (uint64_t)i * W + c >= P.ll_stride || (int)(R.q >> (4 * k) & 15u) >= P.P
+                                   : i >= (uint32_t)P.cap_rows;
+      }
+      if (!HALO_BC(!bad, 10, g.lrank)) continue;
+    }
+#endif
     if (tdet && u == 0) tdet[0] = gtimer() + (il[0] == 0xffffffffu ? 1 : 0);  // records read
     // F node values straight into this thread's shared-memory column (LDGSTS: every
     // load in flight, no registers held); LL nodes out of line (they wait for a

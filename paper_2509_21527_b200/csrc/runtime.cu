@@ -346,6 +346,11 @@ static halo_status check_err_word(halo_ctx* ctx) {
   if (ctx->err_host && *(volatile int*)ctx->err_host != 0) {
     char buf[128];
     int code = *(volatile int*)ctx->err_host;
+    if ((code >> 16) == kErrKindBounds) {
+      snprintf(buf, sizeof buf, "bounds check failed in the checked build (local rank %d, check %d)",
+               (code >> 8) & 0xff, code & 0xff);
+      return fail(ctx, HALO_ERR_STATE, buf);
+    }
     if ((code >> 16) == kErrKindStalePlan)
       return fail(ctx, HALO_ERR_STATE, "a CUDA graph captured before the last halo_set_maps / halo_migrate was "
                                        "replayed (its plan is gone): re-capture after every NS step");
@@ -1686,6 +1691,11 @@ static ExParams make_params(halo_ctx* ctx, const Item* items, int n_items, int p
   P.lbase = ctx->d_lbase;
   P.plan_epoch = ctx->epoch;
   P.all_local = ctx->all_local ? 1 : 0;
+  P.cap_rows = ctx->cfg.capacity;
+#ifdef HALO_BOUNDS_CHECK
+  // self-test of the checked build: pretend the buffers hold this many rows (the checks must fire)
+  if (const char* e = getenv("HALO_BC_CAP")) P.cap_rows = std::max(1, atoi(e));
+#endif
   return P;
 }
 
