@@ -32,8 +32,10 @@ def _worker(rank, world, port, cases, out):
         dev = rank % torch.cuda.device_count()  # world 8 on 4 GPUs: two processes per GPU
         torch.cuda.set_device(dev)
         dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2509_21527_b200 import _lib
         from paper_2509_21527_b200.session import HaloSession
         from tests.parity_common import Case, run_gpu_case
+        assert _lib.LIB_PATH == os.environ.get("HALO_LIB_PATH", _lib.LIB_PATH)  # (the checked build when set)
         for (name, seed, kind, flags, layout, steps) in cases:
             case = Case(name, seed=seed, force_kind=kind, layout=layout, rounded=bool(flags & ROUNDED))
             if case.nranks % world:
@@ -46,6 +48,7 @@ def _worker(rank, world, port, cases, out):
                                device=dev, flags=flags & ~(BULK | FUSED), nprocs=world, proc=rank, timeout_s=30.0)
             run_gpu_case(case, sess, steps=steps, atomic=bool(flags & 1) and kind != "int", barrier=dist.barrier,
                          fused=bool(flags & FUSED))
+            sess.halo.sync()  # (the checked build: raises if a bounds check fired)
             dist.barrier()
             sess.destroy()
             dist.barrier()
@@ -102,6 +105,35 @@ def test_multiprocess_parity(world):
         out = mgr.dict()
         mp.spawn(_worker, args=(world, port, cases, out), nprocs=world, join=True)
         out = dict(out)
+    for r in range(world):
+        assert out.get(r) == "ok", out.get(r)
+
+
+BOUNDS_CASES = [("C3", 1, "normal", 0, 3, 2), ("T2P", 1, "int", 0, 4, 2), ("C1", 2, "normal", BULK, 3, 2),
+                ("C5", 1, "normal", BULK | FUSED, 3, 2)]
+
+
+@pytest.mark.parametrize("world", [2])
+def test_multiprocess_bounds_checked(world):
+    """The cross-process LL paths through the bounds-checked build (DESIGN.md §7,
+    tests/test_gpu_bounds.py): the spawned processes load libhalo_checked.so."""
+    if _ndev() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from paper_2509_21527_b200.build import build_checked
+    lib = build_checked()
+    old = os.environ.get("HALO_LIB_PATH")
+    os.environ["HALO_LIB_PATH"] = lib  # read at import by every spawned process
+    try:
+        port = _free_port()
+        with mp.Manager() as mgr:
+            out = mgr.dict()
+            mp.spawn(_worker, args=(world, port, BOUNDS_CASES, out), nprocs=world, join=True)
+            out = dict(out)
+    finally:
+        if old is None:
+            os.environ.pop("HALO_LIB_PATH")
+        else:
+            os.environ["HALO_LIB_PATH"] = old
     for r in range(world):
         assert out.get(r) == "ok", out.get(r)
 
