@@ -464,6 +464,8 @@ struct PlanDev {
   int32_t fcnt[kMaxP + 1][kMaxLocal];         // roots of (class, local rank)
   char* xblk;
   char* fblk;
+  int nx_send, nf;          // send items / f items (the checked build's bounds of the block writes)
+  int* err_host;            // host-mapped error word (the checked build reports failed checks there)
 };
 
 // halo_step_host_packed: one contiguous copy between a packed staging buffer and

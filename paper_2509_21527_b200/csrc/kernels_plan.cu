@@ -42,6 +42,20 @@ __device__ __forceinline__ void plan_pdl() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Checked build (-DHALO_BOUNDS_CHECK): item indices of the block writes and
+// map entries are checked; a failure reports kErrKindBounds (local rank 0xfe = plan) and
+// the write is skipped.
+#ifdef HALO_BOUNDS_CHECK
+__device__ __noinline__ bool plan_bc_fail(const halo::PlanDev* D, int code) {
+  volatile int* e = D->err_host;
+  if (*e == 0) *e = (halo::kErrKindBounds << 16) | (0xfe << 8) | code;
+  __threadfence_system();
+  return false;
+}
+#define PLAN_BC(cond, code) ((cond) ? true : plan_bc_fail(D, (code)))
+#else
+#define PLAN_BC(cond, code) true
+#endif
 template <typename... Args, typename... Actual>
 cudaError_t plan_launch(void (*k)(Args...), dim3 grid, unsigned block, cudaStream_t st, Actual... args) {
   cudaLaunchConfig_t cfg = {};
@@ -221,6 +235,7 @@ __global__ void __launch_bounds__(kPB) k_plan_x(const PlanDev* __restrict__ D) {
   const int item = D->xoff[cls][p][l] + s_carry[2 + cls] + idx - 1;
   char* blk = D->xblk + (size_t)item * D->XB;
   const int e = k - istart;
+  if (!PLAN_BC(item >= 0 && item < D->nx_send && e >= 0 && e < R, 20)) return;
   XEnt E;
   E.row = (uint32_t)(o & 0xffffffu);
   E.l = (uint8_t)((o >> 24) & 0xffu);
@@ -261,7 +276,7 @@ __global__ void k_plan_child(const PlanDev* __restrict__ D) {
   const int32_t* m = D->maps[l] + (size_t)q * D->map_stride;
   int32_t* c = D->child + (size_t)l * D->cap * D->P;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    c[(size_t)m[i] * D->P + q] = i;
+    if (PLAN_BC(m[i] >= 0 && m[i] < D->n_total[l], 21)) c[(size_t)m[i] * D->P + q] = i;
 }
 
 // Depth-first node list of the tree under row t of local rank l, children in
@@ -402,6 +417,7 @@ __global__ void __launch_bounds__(kPB) k_plan_f(const PlanDev* __restrict__ D) {
     if (cls != 0xff) {
       const int rank = D->boff[((size_t)l * D->nblk + blockIdx.x) * nc + cls] + idx - 1;
       const uint32_t m = D->rmask[(size_t)l * D->cap + t];
+      if (!PLAN_BC(D->foff[cls][l] + rank / RT < D->nf, 22)) return;
       if (m) atomicOr(&D->imask[D->foff[cls][l] + rank / RT], m);
     }
     return;
@@ -414,6 +430,7 @@ __global__ void __launch_bounds__(kPB) k_plan_f(const PlanDev* __restrict__ D) {
     const int nn = plan_tree(D, l, t, v, lowest);
     const int rank = D->boff[((size_t)l * D->nblk + blockIdx.x) * nc + cls] + idx - 1;
     const int item = D->foff[cls][l] + rank / RT, slot = rank % RT;
+    if (!PLAN_BC(item >= 0 && item < D->nf && nn >= 1 && nn <= kFastNodes, 23)) return;
     char* blk = D->fblk + (size_t)item * D->FB;
     const uint32_t imask = D->imask[item];
     TRoot R;

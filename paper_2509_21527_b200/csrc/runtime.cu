@@ -1403,6 +1403,7 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
   }
   PlanDev& H = *ctx->h_pl;
   memset(&H, 0, sizeof H);
+  H.err_host = ctx->err_dev;
   H.L = L;
   H.P = P;
   H.W = W;
@@ -1555,6 +1556,12 @@ static halo_status build_ll_plan_gpu(halo_ctx* ctx, cudaStream_t st, PhaseTimer*
   if (s != HALO_OK) return s;
   H.xblk = ctx->d_xblk;
   H.fblk = ctx->d_fblk;
+  H.nx_send = n_send;
+  H.nf = nf;
+  H.err_host = ctx->err_dev;
+#ifdef HALO_BOUNDS_CHECK
+  if (getenv("HALO_BC_ITEMS")) H.nx_send = H.nf = 1;  // self-test: the plan-write checks must fire
+#endif
   CK(cudaMemcpyAsync(ctx->d_pl, &H, sizeof(PlanDev), cudaMemcpyHostToDevice, st));
   if (!recv.empty()) {  // the receive items' records (no entries): straight from pinned memory
     if (ctx->h_recv_cap < recv.size()) {

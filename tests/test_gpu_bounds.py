@@ -32,8 +32,11 @@ def test_bounds_checked_parity():
     assert r.stdout.count(": ok") >= 14, r.stdout
 
 
-@pytest.mark.parametrize("spec", ["T3D:ll", "T3D:staged", "C3:ll:fused"])
-def test_bounds_check_fires(spec):
-    r = _run([spec], {"HALO_BC_CAP": "8"})
+@pytest.mark.parametrize("spec,env", [("T3D:ll", "HALO_BC_CAP"), ("T3D:staged", "HALO_BC_CAP"),
+                                      ("C3:ll:fused", "HALO_BC_CAP"), ("C3:ll", "HALO_BC_ITEMS")])
+def test_bounds_check_fires(spec, env):
+    # HALO_BC_CAP: the exchange kernels see 8-row buffers; HALO_BC_ITEMS: the plan kernels
+    # see one x item and one f item
+    r = _run([spec], {env: "8" if env == "HALO_BC_CAP" else "1"})
     assert r.returncode != 0, r.stdout
     assert "bounds check failed" in r.stderr, r.stderr[-4000:]
