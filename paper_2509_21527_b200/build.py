@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhalo.so")
-# the checked build (-DHALO_BOUNDS_CHECK, scripts/bounds_check.py, tests/test_gpu_bounds.py)
+# the checked build (-DHALO_BOUNDS_CHECK, tests/bounds_check_run.py, tests/test_gpu_bounds.py)
 CHECKED = os.path.join(HERE, "libhalo_checked.so")
 SOURCES = ["runtime.cu", "kernels.cu", "kernels_ll.cu", "kernels_ce.cu", "kernels_ns.cu", "kernels_pme.cu", "kernels_plan.cu",
            "nccl_baseline.cu",

@@ -94,7 +94,7 @@ __device__ __forceinline__ uint64_t ll_spin(const uint64_t* u, uint32_t tag, uin
   }
 }
 
-// Checked build (-DHALO_BOUNDS_CHECK, scripts/bounds_check.py; compute-sanitizer is closed
+// Checked build (-DHALO_BOUNDS_CHECK, tests/bounds_check_run.py; compute-sanitizer is closed
 // on this GPU pool): every global index the kernel derives from a plan record is checked
 // against its buffer; a failed check reports kErrKindBounds (local rank, check number),
 // and the access goes to index 0 instead.  The production build compiles the checks out.

@@ -1,9 +1,9 @@
-"""Parity cases through the CHECKED build of the library (-DHALO_BOUNDS_CHECK: every
-global index the LL kernels derive from a plan record is checked against its buffer;
+"""Test infrastructure (run by tests/test_gpu_bounds.py; it calls the oracle): parity
+cases through the CHECKED build of the library (-DHALO_BOUNDS_CHECK: every global index the LL kernels derive from a plan record is checked against its buffer;
 DESIGN.md §7).  compute-sanitizer is closed on this GPU pool (profiles/r02s4/
 compute_sanitizer_closed.txt); this is the bounds-check substitute it recommends.
 
-    HALO_LIB_PATH=paper_2509_21527_b200/libhalo_checked.so python scripts/bounds_check.py [CASE ...]
+    HALO_LIB_PATH=paper_2509_21527_b200/libhalo_checked.so python tests/bounds_check_run.py [CASE ...]
 
 A case is NAME[:mode[:fused]] with mode ll (one hop group), staged (every DD rank its
 own group: the LL receive paths) or bulk (staged + every last pulse a bulk pulse).

@@ -1,4 +1,4 @@
-"""Checked build (-DHALO_BOUNDS_CHECK): the parity cases of scripts/bounds_check.py run
+"""Checked build (-DHALO_BOUNDS_CHECK): the parity cases of tests/bounds_check_run.py run
 through libhalo_checked.so, where every global index the LL kernels derive from a plan
 record is checked against its buffer (compute-sanitizer is closed on this GPU pool:
 profiles/r02s4/compute_sanitizer_closed.txt).  Each run is a subprocess (one library
@@ -22,7 +22,7 @@ def _checked_lib():
 
 def _run(args, extra_env=None, timeout=600):
     env = dict(os.environ, HALO_LIB_PATH=_checked_lib(), **(extra_env or {}))
-    return subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "bounds_check.py"), *args], env=env,
+    return subprocess.run([sys.executable, os.path.join(ROOT, "tests", "bounds_check_run.py"), *args], env=env,
                           capture_output=True, text=True, timeout=timeout, cwd=ROOT)
 
 
