@@ -532,14 +532,21 @@ __host__ __device__ constexpr int ll_threads() {
 }
 
 #ifndef HALO_XF_MIN_BLOCKS
-#define HALO_XF_MIN_BLOCKS 4  // fused launch: CTAs per SM the registers are budgeted for (A/B switch)
+#define HALO_XF_MIN_BLOCKS 3  // fused launch with LL paths: CTAs per SM the registers are budgeted for (3: no spills)
+#endif
+#ifndef HALO_F_MIN_BLOCKS
+#define HALO_F_MIN_BLOCKS 3   // f launch with LL paths (N > 1): CTAs per SM the registers are budgeted for
+                              // (3: no spills; C3 2 GPUs 28.7 -> 27.0, C4-1D 30.9 -> 30.1 us vs 4; the
+                              // hop-group-local variants keep 4: fewer registers, and 3 costs them ~1.8 us fused)
 #endif
 // kChk: the launch is being captured into a CUDA graph, whose replays may outlive the
 // plan (the next NS step): every item's epoch is checked.  Eager launches take their
 // parameters from the current plan and skip the check (measured: ~0.2 us per step).
 template <int W, int kU, int kMode, bool kChk, bool kLocal = false>
 __global__ void __launch_bounds__(ll_threads<kU, kMode>(), kMode == kModeX ? (kU == 1 || kU == 3 ? 8 : 4)
-                                                           : kMode == kModeXF ? HALO_XF_MIN_BLOCKS : 4) k_exchange_ll(
+                                                           : kLocal           ? 4
+                                                           : kMode == kModeXF ? HALO_XF_MIN_BLOCKS
+                                                                              : HALO_F_MIN_BLOCKS) k_exchange_ll(
     const __grid_constant__ ExParams P) {
   extern __shared__ __align__(128) unsigned char s_blk[];
   __shared__ uint64_t s_seq[2];
@@ -784,7 +791,10 @@ cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid
 // Co-resident CTAs per GPU of each mode for the narrow (items <= 128 rows) or
 // wide (<= 512) variants, at the largest item size each runs with (a smaller
 // launch only fits more).  Also opts the kernels into their dynamic shared memory.
-cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [4]: x, f, xf, x with 128-row items */) {
+// local_sel: -1 every variant, 0 the variants with LL paths, 1 the hop-group-local ones
+// (their register budgets differ: HALO_F_MIN_BLOCKS / HALO_XF_MIN_BLOCKS)
+cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [4]: x, f, xf, x with 128-row items */,
+                              int local_sel) {
   int dev = 0, sms = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -794,7 +804,8 @@ cudaError_t max_coresident_ll(int layout, bool wide, int* blocks /* [4]: x, f, x
   for (int mode = 0; mode < 4; ++mode) {
     int bmin = 1 << 30;
     const int m = mode == 3 ? 0 : mode, irows = mode == 3 ? 128 : 64;
-    for (int v = 0; v < 4; ++v) {  // the grid must fit every variant (eager / captured, hop-group-local)
+    for (int v = 0; v < 4; ++v) {  // the grid must fit every variant (eager / captured[, hop-group-local])
+      if (local_sel >= 0 && ((v & 2) != 0) != (local_sel == 1)) continue;
       const int chk = v & 1;
       const void* fn = ll_fn(layout, m, wide, chk != 0, irows, (v & 2) != 0);
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -37,7 +37,7 @@ cudaError_t launch_pingpong(uint64_t* own, uint64_t* peer, int iters, uint64_t b
                             uint64_t* rtt_ns, uint64_t timeout_ns, int* err_host, cudaStream_t st);
 cudaError_t launch_exchange_ll(const ExParams& p, int mode, int layout, int grid, bool wide,
                                const cudaAccessPolicyWindow* win, cudaStream_t st, bool chk);
-cudaError_t max_coresident_ll(int layout, bool wide, int* blocks);
+cudaError_t max_coresident_ll(int layout, bool wide, int* blocks, int local_sel);
 int ll_ring(int mode, bool wide);
 void ll_set_ring_f(int r);
 void ll_set_x_variant(int v);
@@ -234,19 +234,28 @@ struct halo_ctx {
   cudaAccessPolicyWindow l2win{};    // HALO_F_L2_PERSIST: the static plan (item blocks) persists in L2
   int max_x = 0, max_f = 0, max_xf = 0;        // co-resident CTAs of the exchange kernels (LL: narrow variants)
   int max_x128 = 0;                              // ... of the x kernel with 128-row items (two units per thread)
+  // ... of the hop-group-local variants (used when all_local: their register budget differs)
+  int max_x_loc = 0, max_f_loc = 0, max_xf_loc = 0, max_x128_loc = 0;
   bool all_local = false;           // LL plan: every pulse of every local rank stays in this hop group
   int max_x_w = 0, max_f_w = 0, max_xf_w = 0;  // LL: batched variants for large work items
   int grid_cap = 0;                 // HALO_CTAS_PER_SM x SMs (0 = occupancy limit only)
   int x_cap = 0;                    // HALO_X_CTAS_PER_SM x SMs: the x kernel only (leaves SM room for
                                     // the f kernel's CTAs to become resident early under PDL)
   bool wide() const { return ll && item_rows >= 256; }
+  bool loc() const { return ll && all_local && max_f_loc > 0; }
   int cap_x() const {
-    int c = wide() ? max_x_w : item_rows > 64 ? max_x128 : max_x;
+    int c = wide() ? max_x_w : item_rows > 64 ? (loc() ? max_x128_loc : max_x128) : (loc() ? max_x_loc : max_x);
     if (grid_cap) c = std::min(c, grid_cap);
     return x_cap ? std::min(c, x_cap) : c;
   }
-  int cap_f() const { const int c = wide() ? max_f_w : max_f; return grid_cap ? std::min(c, grid_cap) : c; }
-  int cap_xf() const { const int c = wide() ? max_xf_w : max_xf; return grid_cap ? std::min(c, grid_cap) : c; }
+  int cap_f() const {
+    const int c = wide() ? max_f_w : loc() ? max_f_loc : max_f;
+    return grid_cap ? std::min(c, grid_cap) : c;
+  }
+  int cap_xf() const {
+    const int c = wide() ? max_xf_w : loc() ? max_xf_loc : max_xf;
+    return grid_cap ? std::min(c, grid_cap) : c;
+  }
   int last_grid[2] = {0, 0};
   int item_rows = 64;
   int tree_rows = 64;               // LL: roots per small-tree f item (chosen per NS epoch, build_ll_f)
@@ -504,10 +513,12 @@ halo_status halo_init(const halo_config* cfg, halo_ctx** out) {
   if (e == cudaSuccess) {
     // LL occupancy always (HALO_F_AUTO_TRANSPORT can switch a ctx to LL); the paper
     // protocol's kernels for the paper / copy-engine paths
-    int b[4] = {0, 0, 0, 0}, bw[4] = {0, 0, 0, 0};
-    e = max_coresident_ll(cfg->layout, false, b);
-    if (e == cudaSuccess) e = max_coresident_ll(cfg->layout, true, bw);
+    int b[4] = {0, 0, 0, 0}, bl[4] = {0, 0, 0, 0}, bw[4] = {0, 0, 0, 0};
+    e = max_coresident_ll(cfg->layout, false, b, 0);
+    if (e == cudaSuccess) e = max_coresident_ll(cfg->layout, false, bl, 1);
+    if (e == cudaSuccess) e = max_coresident_ll(cfg->layout, true, bw, -1);
     ctx->max_x = b[0]; ctx->max_f = b[1]; ctx->max_xf = b[2]; ctx->max_x128 = b[3];
+    ctx->max_x_loc = bl[0]; ctx->max_f_loc = bl[1]; ctx->max_xf_loc = bl[2]; ctx->max_x128_loc = bl[3];
     ctx->max_x_w = bw[0]; ctx->max_f_w = bw[1]; ctx->max_xf_w = bw[2];
     if (e == cudaSuccess && !ctx->ll) e = max_coresident(cfg->layout, &ctx->max_x, &ctx->max_f);
   }
@@ -2105,7 +2116,10 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   SP.ce_bytes = ctx->auto_ce_bytes;
   if (const char* e = getenv("HALO_AUTO_CE_BYTES")) SP.ce_bytes = (uint64_t)std::max(0LL, atoll(e));  // per NS step
   SP.rows_fixed = ctx->item_rows_fixed ? ctx->item_rows : 0;
-  SP.ctas = std::max(1, std::min(ctx->max_x, ctx->max_f));
+  // the CTA budget the item size is voted for: the same number in every process (the f grid
+  // of the larger-occupancy variant: the hop-group-local one's 4 CTAs per SM, not the 3 of the
+  // variant with LL paths, HALO_F_MIN_BLOCKS — C3 keeps R = 64 rows on 1 GPU)
+  SP.ctas = std::max(1, std::min(ctx->max_x, std::max(ctx->max_f, ctx->max_f_loc)));
   CK(launch_status(SP, st));
   int32_t agreed[kMaxLocal];
   if ((s = pull_ctrl(ctx, st, agreed)) != HALO_OK) return s;
@@ -2198,6 +2212,11 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
   ctx->seq_host_f = seqs[1];
   prof.lap("plan");
   prof.print(ctx->first_rank);
+  if (prof.on)
+    fprintf(stderr, "[halo_profile rank %d] items x %d f %d, grid caps x %d f %d xf %d (local variants: %d), R %d RT %d\n",
+            ctx->first_rank, ctx->gpu_n_items_x ? ctx->gpu_n_items_x : (int)ctx->h_items_x.size(),
+            ctx->gpu_n_items_f ? ctx->gpu_n_items_f : (int)ctx->h_items_f.size(), ctx->cap_x(), ctx->cap_f(),
+            ctx->cap_xf(), ctx->loc() ? 1 : 0, ctx->item_rows, ctx->tree_rows);
   ctx->maps_ready = true;
   ctx->x_done = true;  // set_maps exchanged every pulse's coordinates
   return HALO_OK;
