@@ -543,6 +543,7 @@ struct NsXParams {
   uint32_t wait_mask[kMaxLocal];   // pulses q < p whose x-sender is in another process (forwarded rows)
   int* err_host;
   uint64_t timeout_ns;
+  int cap;                         // rows of every x buffer (the checked build's bounds)
 };
 
 struct NsWaitParams {

@@ -490,7 +490,14 @@ __global__ void __launch_bounds__(1024) k_select(const __grid_constant__ SelPara
     return;
   }
   int32_t* out = rd.maps + (size_t)S.p * S.map_stride;
-  if (sel) out[s_base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u))] = i;
+  const int slot = s_base + s_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
+#ifdef HALO_BOUNDS_CHECK  // a map entry beyond the pulse's map slot
+  if (sel && (slot < 0 || slot >= S.map_stride)) {
+    report_timeout(S.err_host, tcode(kErrKindBounds, lr, 30));
+    return;
+  }
+#endif
+  if (sel) out[slot] = i;
   if (threadIdx.x == 0 && (int)blockIdx.x == max(nchunk, 1) - 1) S.ctrl->send_size[lr][S.p] = s_base + s_total;
 }
 
@@ -591,6 +598,12 @@ __global__ void __launch_bounds__(256) k_ns_x(const __grid_constant__ NsXParams 
   bool bad = false;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int idx = map[i];
+#ifdef HALO_BOUNDS_CHECK  // the source row, the destination row
+    if (idx < 0 || idx >= X.cap || ro < 0 || ro + i >= X.cap || i >= X.map_stride) {
+      report_timeout(X.err_host, tcode(kErrKindBounds, lr, 31));
+      continue;
+    }
+#endif
     if (idx < rd.n_home) {
       ++indep;
     } else {

@@ -2078,6 +2078,10 @@ static halo_status set_maps_impl(halo_ctx* ctx, const int* n_home, const int* se
     }
     NX.err_host = ctx->err_dev;
     NX.timeout_ns = timeout_ns;
+    NX.cap = ctx->cfg.capacity;
+#ifdef HALO_BOUNDS_CHECK
+    if (const char* e = getenv("HALO_BC_NS")) NX.cap = std::max(1, atoi(e));  // self-test: the NS checks must fire
+#endif
     CK(launch_ns_x(NX, W, ctx->cfg.capacity, st));
     prof.lap("pulse");
   }

@@ -33,10 +33,11 @@ def test_bounds_checked_parity():
 
 
 @pytest.mark.parametrize("spec,env", [("T3D:ll", "HALO_BC_CAP"), ("T3D:staged", "HALO_BC_CAP"),
-                                      ("C3:ll:fused", "HALO_BC_CAP"), ("C3:ll", "HALO_BC_ITEMS")])
+                                      ("C3:ll:fused", "HALO_BC_CAP"), ("C3:ll", "HALO_BC_ITEMS"),
+                                      ("T2P:staged", "HALO_BC_NS")])
 def test_bounds_check_fires(spec, env):
     # HALO_BC_CAP: the exchange kernels see 8-row buffers; HALO_BC_ITEMS: the plan kernels
-    # see one x item and one f item
-    r = _run([spec], {env: "8" if env == "HALO_BC_CAP" else "1"})
+    # see one x item and one f item; HALO_BC_NS: the NS-step coordinate exchange sees 8 rows
+    r = _run([spec], {env: "1" if env == "HALO_BC_ITEMS" else "8"})
     assert r.returncode != 0, r.stdout
     assert "bounds check failed" in r.stderr, r.stderr[-4000:]
