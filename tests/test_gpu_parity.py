@@ -160,6 +160,36 @@ def test_cuda_graph_replay(proto):
     sess.destroy()
 
 
+@pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(STAGED, id="ll_staged")])
+def test_long_run_stays_exact(proto):
+    """50,000 exchange steps on one NS epoch (100,000 launches: sequence numbers, LL tags,
+    completion counters cycling), then one step on fresh inputs without a set_maps in
+    between: still bit-exact (x, f) and exact fshift (integer forces)."""
+    case = Case("C3", seed=1, force_kind="int")
+    sess = session_for(case, flags=proto)
+    run_gpu_case(case, sess)
+    fshift = torch.zeros(sess.n_local, 3, 3, dtype=torch.float64, device=sess.device)
+    for _ in range(50000):
+        sess.exchange_x()
+        sess.exchange_f(fshift=fshift)
+    torch.cuda.synchronize()
+    sess.halo.sync()
+    for l in range(sess.n_local):
+        st = case.states[l]
+        sess.x[l][st.n_home: st.x.shape[0]] = float("nan")
+        sess.f[l][: case.F[l].shape[0]] = torch.from_numpy(case.F[l]).to(sess.device)
+    fshift.zero_()
+    sess.exchange_x()
+    sess.exchange_f(fshift=fshift)
+    torch.cuda.synchronize()
+    for l in range(sess.n_local):
+        st = case.states[l]
+        np.testing.assert_array_equal(bits(sess.x[l][: st.x.shape[0]].cpu().numpy()), bits(st.x))
+        np.testing.assert_array_equal(bits(sess.f[l][: case.F[l].shape[0]].cpu().numpy()), bits(case.Fo[l]))
+        np.testing.assert_array_equal(fshift[l].cpu().numpy(), case.fshift[l])
+    sess.destroy()
+
+
 @pytest.mark.parametrize("proto", [pytest.param(0, id="ll"), pytest.param(BULK, id="ll_bulk")])
 @pytest.mark.parametrize("renew", ["set_maps", "migrate"])
 def test_stale_graph_replay_refused(renew, proto):
