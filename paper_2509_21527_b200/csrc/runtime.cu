@@ -214,6 +214,15 @@ struct halo_ctx {
   };
   std::vector<CeEnt> h_ce_pack, h_ce_unpack;   // [P][n_local]
   std::vector<CeCopy> ce_copy_x, ce_copy_f;    // [P][n_local]
+  // HALO_CE_PROFILE=1: CUDA events between the copy-engine path's operations (study of
+  // where its time goes); the mean per operation is printed at halo_destroy
+  struct CeProf {
+    bool on = getenv("HALO_CE_PROFILE") != nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pend;  // (start, end) per op, in order
+    std::vector<std::string> names, agg_names;
+    std::vector<double> sum;
+    std::vector<int> cnt;
+  } ce_prof;
   std::vector<int> ce_pack_rows, ce_unpack_rows;  // [P]: largest entry needing the kernel (0 = no launch)
   CeEnt* d_ce = nullptr;                       // pack table then unpack table
   float* d_stage = nullptr;                    // contiguous send rows of every (pulse, local rank) that packs
@@ -1857,15 +1866,65 @@ static CeSyncParams ce_sync_params(halo_ctx* ctx, int kind, int p, bool publish)
   return S;
 }
 
+// HALO_CE_PROFILE: one timed event pair around an operation of the CE path.
+struct CeMark {
+  halo_ctx* ctx;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  const char* name;
+  CeMark(halo_ctx* c, cudaStream_t s, const char* n) : ctx(c), st(s), name(n) {
+    if (!ctx->ce_prof.on) return;
+    (void)cudaEventCreate(&a);
+    (void)cudaEventRecord(a, st);
+  }
+  ~CeMark() {
+    if (!ctx->ce_prof.on) return;
+    cudaEvent_t b = nullptr;
+    (void)cudaEventCreate(&b);
+    (void)cudaEventRecord(b, st);
+    ctx->ce_prof.pend.push_back({a, b});
+    ctx->ce_prof.names.push_back(name);
+  }
+};
+static void ce_prof_collect(halo_ctx* ctx) {
+  auto& P = ctx->ce_prof;
+  if (!P.on || P.pend.empty()) return;
+  (void)cudaDeviceSynchronize();
+  for (size_t i = 0; i < P.pend.size(); ++i) {
+    float ms = 0.f;
+    (void)cudaEventElapsedTime(&ms, P.pend[i].first, P.pend[i].second);
+    (void)cudaEventDestroy(P.pend[i].first);
+    (void)cudaEventDestroy(P.pend[i].second);
+    size_t k = 0;
+    while (k < P.agg_names.size() && P.agg_names[k] != P.names[i]) ++k;
+    if (k == P.agg_names.size()) {
+      P.agg_names.push_back(P.names[i]);
+      P.sum.push_back(0.0);
+      P.cnt.push_back(0);
+    }
+    P.sum[k] += ms * 1e3;
+    P.cnt[k] += 1;
+  }
+  P.pend.clear();
+  P.names.clear();
+}
+
 // x over the copy engine: per pulse ascending, gather -> CE copy -> flag + wait.
 static halo_status ce_exchange_x(halo_ctx* ctx, cudaStream_t st) {
   const int L = ctx->n_local, P = ctx->P;
   for (int p = 0; p < P; ++p) {
-    CK(launch_ce_pack(ctx->W, ctx->d_ce + (size_t)p * L, L, ctx->ce_pack_rows[p], st));
-    for (int l = 0; l < L; ++l) {
-      const halo_ctx::CeCopy& c = ctx->ce_copy_x[(size_t)p * L + l];
-      if (c.bytes) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, st));
+    {
+      CeMark m(ctx, st, "x pack");
+      CK(launch_ce_pack(ctx->W, ctx->d_ce + (size_t)p * L, L, ctx->ce_pack_rows[p], st));
     }
+    {
+      CeMark m(ctx, st, "x copy");
+      for (int l = 0; l < L; ++l) {
+        const halo_ctx::CeCopy& c = ctx->ce_copy_x[(size_t)p * L + l];
+        if (c.bytes) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, st));
+      }
+    }
+    CeMark m(ctx, st, "x sync");
     CK(launch_ce_sync(ce_sync_params(ctx, 0, p, p == P - 1), st));
   }
   return HALO_OK;
@@ -1876,14 +1935,22 @@ static halo_status ce_exchange_x(halo_ctx* ctx, cudaStream_t st) {
 static halo_status ce_exchange_f(halo_ctx* ctx, double* fshift, int accumulate, cudaStream_t st) {
   const int L = ctx->n_local, P = ctx->P;
   for (int p = P - 1; p >= 0; --p) {
-    for (int l = 0; l < L; ++l) {
-      const halo_ctx::CeCopy& c = ctx->ce_copy_f[(size_t)p * L + l];
-      if (c.bytes) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, st));
+    {
+      CeMark m(ctx, st, "f copy");
+      for (int l = 0; l < L; ++l) {
+        const halo_ctx::CeCopy& c = ctx->ce_copy_f[(size_t)p * L + l];
+        if (c.bytes) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDefault, st));
+      }
     }
-    CK(launch_ce_sync(ce_sync_params(ctx, 1, p, p == 0), st));
+    {
+      CeMark m(ctx, st, "f sync");
+      CK(launch_ce_sync(ce_sync_params(ctx, 1, p, p == 0), st));
+    }
+    CeMark m(ctx, st, "f unpack");
     CK(launch_ce_unpack(ctx->W, ctx->d_ce + (size_t)P * L + (size_t)p * L, L, ctx->ce_unpack_rows[p], fshift,
                         accumulate, st));
   }
+  if (ctx->ce_prof.on && ctx->ce_prof.pend.size() > 4096) ce_prof_collect(ctx);
   return HALO_OK;
 }
 
@@ -3258,6 +3325,13 @@ halo_status halo_sync(halo_ctx* ctx) {
 }
 
 halo_status halo_destroy(halo_ctx* ctx) {
+  if (ctx && ctx->ce_prof.on) {
+    ce_prof_collect(ctx);
+    for (size_t j = 0; j < ctx->ce_prof.sum.size(); ++j)
+      if (ctx->ce_prof.cnt[j])
+        fprintf(stderr, "[halo_ce_profile rank %d] %-9s %8.2f us (n=%d)\n", ctx->first_rank, ctx->ce_prof.agg_names[j].c_str(),
+                ctx->ce_prof.sum[j] / ctx->ce_prof.cnt[j], ctx->ce_prof.cnt[j]);
+  }
   if (!ctx) return HALO_OK;
   (void)cudaSetDevice(ctx->cfg.device);
   (void)cudaDeviceSynchronize();
