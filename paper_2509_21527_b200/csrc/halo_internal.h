@@ -25,6 +25,7 @@ namespace halo {
 constexpr int kMaxP = HALO_MAX_PULSES;
 constexpr int kMaxLocal = HALO_MAX_LOCAL;
 constexpr int kMaxRanks = HALO_MAX_RANKS;
+constexpr int kAssignSegs = 64;  // atom segments of halo_assign_home's compaction (one CTA per rank and segment)
 constexpr int kThreads = 256;          // threads per CTA of the exchange kernels
 constexpr int kHdrBytes = 8192;
 constexpr int kTraceCTAs = 2048;       // per-CTA timestamps kept for HALO_F_TIMERS

@@ -355,11 +355,13 @@ cudaError_t launch_migrate(const MigParams& M, MigCtrl* C, int max_rows, int pha
 // c_d = the number of interior planes b_d[k] <= float64(x_d), ties go up; rank =
 // (cx*np_y + cy)*np_z + cz), then a stable counting sort of the atom ids by
 // rank.  Pass 1: rank per atom + per-rank counts (CTA histogram, one atomic per
-// rank and CTA); x outside [0, L_d) sets err.  Pass 2: one CTA per rank scans
-// the ranks in order and appends its atom ids (warp ballot + CTA prefix), so
-// every rank's ids come out ascending.
+// rank and CTA, also binned per atom segment); x outside [0, L_d) sets err.
+// Pass 2: one CTA per (rank, segment) scans its segment in order and appends
+// the rank's atom ids (warp ballot + CTA prefix) at the rank's offset plus the
+// rank's count in the earlier segments, so every rank's ids come out ascending.
 __global__ void __launch_bounds__(256) k_home_rank(const float* __restrict__ x, int n, int stride, AssignParams A,
-                                                   int32_t* __restrict__ rank, int* __restrict__ counts, int* err) {
+                                                   int32_t* __restrict__ rank, int* __restrict__ counts,
+                                                   int* __restrict__ seg, int seg_len, int* err) {
   __shared__ int s_cnt[kMaxRanks];
   const int nr = A.grid[0] * A.grid[1] * A.grid[2];
   for (int r = threadIdx.x; r < nr; r += blockDim.x) s_cnt[r] = 0;
@@ -384,26 +386,34 @@ __global__ void __launch_bounds__(256) k_home_rank(const float* __restrict__ x, 
     atomicAdd(&s_cnt[r], 1);
   }
   __syncthreads();
+  // seg_len is a multiple of blockDim.x: the CTA lies in one segment
+  const int sg = (int)(((size_t)blockIdx.x * blockDim.x) / seg_len);
   for (int r = threadIdx.x; r < nr; r += blockDim.x)
-    if (s_cnt[r]) atomicAdd(&counts[r], s_cnt[r]);
+    if (s_cnt[r]) {
+      atomicAdd(&counts[r], s_cnt[r]);
+      atomicAdd(&seg[sg * nr + r], s_cnt[r]);
+    }
 }
 
 __global__ void __launch_bounds__(1024) k_home_compact(const int32_t* __restrict__ rank, int n,
-                                                       const int* __restrict__ counts, int32_t* __restrict__ ids) {
+                                                       const int* __restrict__ counts, const int* __restrict__ seg,
+                                                       int seg_len, int32_t* __restrict__ ids) {
   __shared__ int s_warp[32];
   __shared__ int s_base;
-  const int r = blockIdx.x;
+  const int r = blockIdx.x, sg = blockIdx.y, nr = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x == 0) {
     int b = 0;
     for (int q = 0; q < r; ++q) b += counts[q];
+    for (int t = 0; t < sg; ++t) b += seg[t * nr + r];
     s_base = b;
   }
   __syncthreads();
   int base = s_base;
-  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+  const int lo = sg * seg_len, hi = min(n, lo + seg_len);
+  for (int c0 = lo; c0 < hi; c0 += blockDim.x) {
     const int i = c0 + threadIdx.x;
-    const bool mine = i < n && rank[i] == r;
+    const bool mine = i < hi && rank[i] == r;
     const unsigned m = __ballot_sync(0xffffffffu, mine);
     if (lane == 0) s_warp[warp] = __popc(m);
     __syncthreads();
@@ -420,14 +430,19 @@ __global__ void __launch_bounds__(1024) k_home_compact(const int32_t* __restrict
 }
 
 cudaError_t launch_assign_home(const float* x, int n, int stride, const AssignParams& A, int32_t* rank, int* counts,
-                               int32_t* ids, int* err, cudaStream_t st) {
+                               int* seg, int32_t* ids, int* err, cudaStream_t st) {
   const int nr = A.grid[0] * A.grid[1] * A.grid[2];
   cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int) * nr, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(err, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(seg, 0, sizeof(int) * kAssignSegs * nr, st);
   if (e != cudaSuccess || n == 0) return e;
-  k_home_rank<<<(n + 255) / 256, 256, 0, st>>>(x, n, stride, A, rank, counts, err);
+  // segments of a whole number of pass-1 CTAs; at most kAssignSegs of them
+  const int per = (n + kAssignSegs - 1) / kAssignSegs;
+  const int seg_len = (per + 255) / 256 * 256;
+  const int nseg = (n + seg_len - 1) / seg_len;
+  k_home_rank<<<(n + 255) / 256, 256, 0, st>>>(x, n, stride, A, rank, counts, seg, seg_len, err);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k_home_compact<<<nr, 1024, 0, st>>>(rank, n, counts, ids);
+  k_home_compact<<<dim3(nr, nseg), 1024, 0, st>>>(rank, n, counts, seg, seg_len, ids);
   return cudaGetLastError();
 }
 

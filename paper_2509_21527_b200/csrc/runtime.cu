@@ -57,7 +57,7 @@ int plan_rows_per_cta();
 uint32_t ll_xblk_bytes(int rows);
 uint32_t ll_fblk_bytes(int rows);
 cudaError_t launch_assign_home(const float* x, int n, int stride, const AssignParams& A, int32_t* rank, int* counts,
-                               int32_t* ids, int* err, cudaStream_t st);
+                               int* seg, int32_t* ids, int* err, cudaStream_t st);
 // floors (kernels_floor.cu)
 cudaError_t launch_payload_pingpong(const void* src_own, void* dst_peer, const void* src_peer_side, void* dst_own,
                                     uint64_t* cnt_own, uint64_t* cnt_peer, size_t bytes, int G, int iters,
@@ -2430,7 +2430,7 @@ halo_status halo_assign_home(halo_ctx* ctx, const float* x, int n_atoms, int str
   if ((uintptr_t)x & 3) return fail(ctx, HALO_ERR_ARG, "x must be 4-B aligned");
   CK(cudaSetDevice(ctx->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t need = align_up(sizeof(int32_t) * std::max(n_atoms, 1), 256) + sizeof(int) * (kMaxRanks + 64);
+  const size_t need = align_up(sizeof(int32_t) * std::max(n_atoms, 1), 256) + sizeof(int) * (kMaxRanks + 64 + kAssignSegs * kMaxRanks);
   if (need > ctx->assign_bytes) {
     if (ctx->d_assign) CK(cudaFree(ctx->d_assign));
     CK(cudaMalloc(&ctx->d_assign, need));
@@ -2439,6 +2439,7 @@ halo_status halo_assign_home(halo_ctx* ctx, const float* x, int n_atoms, int str
   int32_t* rank = reinterpret_cast<int32_t*>(ctx->d_assign);
   int* cnt = reinterpret_cast<int*>(ctx->d_assign + align_up(sizeof(int32_t) * std::max(n_atoms, 1), 256));
   int* err = cnt + kMaxRanks;
+  int* seg = cnt + kMaxRanks + 64;  // [kAssignSegs][nranks] per-segment counts
   double planes[3 * (kMaxRanks + 1)] = {0};
   for (int d = 0; d < 3; ++d)
     for (int k = 0; k <= ctx->cfg.grid[d]; ++k) planes[d * (kMaxRanks + 1) + k] = ctx->plane(d, k);
@@ -2446,7 +2447,7 @@ halo_status halo_assign_home(halo_ctx* ctx, const float* x, int n_atoms, int str
   AssignParams A{};
   A.planes = ctx->d_planes;
   for (int d = 0; d < 3; ++d) A.grid[d] = ctx->cfg.grid[d];
-  CK(launch_assign_home(x, n_atoms, stride, A, rank, cnt, ids, err, st));
+  CK(launch_assign_home(x, n_atoms, stride, A, rank, cnt, seg, ids, err, st));
   int h[kMaxRanks + 1] = {0};
   CK(cudaMemcpyAsync(h, cnt, sizeof(int) * (kMaxRanks + 1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
