@@ -40,3 +40,30 @@ def test_assign_home_plane_ties_and_errors():
     with pytest.raises(HaloError):
         h.assign_home(x.data_ptr(), 1, 3, ids.data_ptr())
     h.destroy()
+
+
+@pytest.mark.parametrize("n,grid,clustered", [(1, (2, 2, 2), False), (255, (2, 2, 2), False),
+                                              (257, (1, 2, 3), False), (16385, (2, 2, 2), False),
+                                              (40001, (4, 2, 2), True)])
+def test_assign_home_ragged_sizes(n, grid, clustered):
+    """Sizes around the compaction's 256-atom CTAs and its 64 atom segments (one CTA per
+    rank and segment); a clustered case leaves some (rank, segment) pairs
+    empty.  Expected ranks from the oracle's R4 cell and R5 rank, atom by atom."""
+    from oracle import home_cell, planes, rank_of
+    from paper_2509_21527_b200.session import assign_home
+    L = (8.0, 6.0, 7.5)
+    rng = np.random.default_rng(n)
+    X = (rng.random((n, 3)) * np.array(L)).astype(np.float32)
+    if clustered:  # 3/4 of the atoms in one corner, in runs
+        k = 3 * n // 4
+        X[:k] = (rng.random((k, 3)) * np.array(L) * 0.2).astype(np.float32)
+    X = np.minimum(X, np.nextafter(np.array(L, np.float32), 0, dtype=np.float32))
+    homes = assign_home(X, L, grid, 1.0, tuple(1 if g > 1 else 0 for g in grid))
+    b = planes(L, grid)
+    nr = grid[0] * grid[1] * grid[2]
+    want = [[] for _ in range(nr)]
+    for i in range(n):
+        want[rank_of(home_cell(X[i], b, grid), grid)].append(i)
+    assert len(homes) == nr
+    for r in range(nr):
+        np.testing.assert_array_equal(homes[r], np.array(want[r], np.int64))
